@@ -1,0 +1,513 @@
+"""Pins of the CPU oracle to things other than itself ("Pins").
+
+Each test names the passage it checks.  Independent references used here:
+numpy's Philox bit generator, mpmath at 40 digits, numpy.linalg (LAPACK),
+scipy's incomplete beta, hand 2x2 algebra, the paper's closed forms and the
+worked examples in tests/golden/spec_paper_examples.json.
+"""
+import json
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+from tests._util import normalized_err
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_paper_examples.json")))
+C = 299792458.0
+
+
+def fc_for(lam):
+    return C / lam
+
+
+# --------------------------------------------------------------------------- a1: RNG and drops
+def test_philox_matches_numpy_bit_generator(orc):
+    """R19: Philox4x64-10 (Salmon et al.) == numpy.random.Philox, whose first block is
+    generated from counter+1 (numpy increments before generating)."""
+    rng = np.random.default_rng(1234)
+    for _ in range(20):
+        ctr = rng.integers(0, 2 ** 63, size=4, dtype=np.uint64)
+        ctr[0] = ctr[0] & np.uint64(0x7FFFFFFFFFFFFFF0)  # avoid carry out of word 0
+        key = rng.integers(0, 2 ** 63, size=2, dtype=np.uint64)
+        ref = np.random.Philox(counter=ctr, key=key).random_raw(4)
+        nxt = ctr.copy()
+        nxt[0] += np.uint64(1)
+        assert np.array_equal(orc.philox4x64_10(nxt, key), ref)
+
+
+def test_gen_drops_law_and_determinism(orc):
+    """R3: r ~ U[r_min, r_max] from the array centre, az ~ U[az_min, az_max] from broadside."""
+    u = orc.users(r=(3.0, 30.0), az=(-60.0, 60.0))
+    p1 = orc.gen_drops(u, 8, 4000, seed=7)
+    p2 = orc.gen_drops(u, 8, 4000, seed=7)
+    assert np.array_equal(p1, p2)
+    assert not np.array_equal(p1, orc.gen_drops(u, 8, 4000, seed=8))
+    r = np.hypot(p1[..., 0], p1[..., 1])
+    az = np.degrees(np.arctan2(p1[..., 1], p1[..., 0]))
+    assert r.min() >= 3.0 - 1e-12 and r.max() <= 30.0 + 1e-12
+    assert az.min() >= -60.0 - 1e-9 and az.max() <= 60.0 + 1e-9
+    assert np.all(p1[..., 0] > 0) and np.all(p1[..., 2] == 0.0)
+    n = r.size
+    assert abs(r.mean() - 16.5) < 4 * (27.0 / math.sqrt(12)) / math.sqrt(n)
+    assert abs(az.mean()) < 4 * (120.0 / math.sqrt(12)) / math.sqrt(n)
+    # first_drop offset addresses the same stream (checkpoint / sharding property)
+    assert np.array_equal(orc.gen_drops(u, 8, 100, seed=7, first_drop=1000), p1[1000:1100])
+
+
+# --------------------------------------------------------------------------- a2: geometry + channel
+@pytest.mark.parametrize("ex", GOLD["element_y"])
+def test_element_coordinates_spec_examples(orc, ex):
+    arr = orc.array("ula", n_y=ex["M"], fc_hz=fc_for(ex["lambda"]))
+    y, z = orc.element_pos(arr, ex["m"] - 1)
+    assert y == pytest.approx(ex["y"], abs=1e-15) and z == 0.0
+
+
+def test_element_coordinates_symmetric(orc):
+    """SPEC.md:86 midpoint symmetry y(m) + y(M+1-m) = 0."""
+    for M in (1, 2, 7, 256):
+        arr = orc.array("ula", n_y=M)
+        ys = [orc.element_pos(arr, m)[0] for m in range(M)]
+        assert max(abs(a + b) for a, b in zip(ys, ys[::-1])) < 1e-15
+
+
+@pytest.mark.parametrize("ex", GOLD["coef_magnitude"])
+def test_coef_magnitude_spec_examples(orc, ex):
+    arr = orc.array("ula", n_y=ex["M"], fc_hz=fc_for(ex["lambda"]))
+    h = orc.channel_coef(arr, [ex["user"][0], ex["user"][1], 0.0], 0)
+    assert abs(h) == pytest.approx(ex["abs_h"], rel=1e-14)
+
+
+def _mp_coef(lam, beta0, ux, uy, uz, ey, ez, xeff):
+    r = mp.sqrt(mp.mpf(ux) ** 2 + (mp.mpf(uy) - ey) ** 2 + (mp.mpf(uz) - ez) ** 2)
+    return mp.sqrt(beta0) * mp.exp(-2j * mp.pi * r / lam) / r * mp.sqrt(xeff / r)
+
+
+def _mp_gram(kind, n_y, n_z, fc, pos):
+    """40-digit brute force of Eq. (3) and G = H^H H (P12)."""
+    mp.mp.dps = 40
+    lam = mp.mpf(C) / mp.mpf(fc)
+    pitch = lam / 2
+    K = pos.shape[0]
+    els = []
+    if kind == "ula":
+        for m in range(n_y):
+            els.append(((m + 1 - mp.mpf(n_y + 1) / 2) * pitch, mp.mpf(0)))
+    else:
+        for q in range(n_z):
+            for p in range(n_y):
+                els.append(((p + 1 - mp.mpf(n_y + 1) / 2) * pitch, (q + 1 - mp.mpf(n_z + 1) / 2) * pitch))
+    H = []
+    for i in range(K):
+        ux, uy, uz = (mp.mpf(float(v)) for v in pos[i])
+        xeff = mp.sqrt(ux ** 2 + uz ** 2) if kind == "ula" else abs(ux)
+        H.append([_mp_coef(lam, 1, ux, uy, uz, ey, ez, xeff) for (ey, ez) in els])
+    G = np.zeros((K, K), dtype=complex)
+    for i in range(K):
+        for j in range(K):
+            s = mp.fsum(mp.conj(a) * b for a, b in zip(H[i], H[j]))
+            G[i, j] = complex(s)
+    return G, H
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,fc", [("ula", 64, 1, 100e9), ("ula", 33, 1, 28e9), ("upa", 6, 5, 100e9)])
+def test_gram_exact_vs_mpmath(orc, kind, n_y, n_z, fc):
+    """P12: oracle exact Gram (a3) equals a 40-digit brute force of Eq. (3) + H^H H
+    within the fp64 phase-reduction floor (q ~ 1e4 => ~1e-12 rad)."""
+    rng = np.random.default_rng(5)
+    el = (-30.0, 30.0) if kind == "upa" else (0.0, 0.0)
+    u = orc.users(r=(2.0, 20.0), az=(-70.0, 70.0), el=el)
+    pos = orc.gen_drops(u, 4, 1, seed=int(rng.integers(1 << 30)))
+    arr = orc.array(kind, n_y=n_y, n_z=n_z, fc_hz=fc)
+    G = orc.gram_exact(arr, pos)[0]
+    Gmp, Hmp = _mp_gram(kind, n_y, n_z, fc, pos[0])
+    assert normalized_err(G, Gmp) < 2e-11
+    # and the per-coefficient channel (a2)
+    H = orc.channel_matrix(arr, pos[0])
+    Href = np.array([[complex(v) for v in row] for row in Hmp]).T
+    assert np.max(np.abs(H - Href) / np.abs(Href)) < 2e-11
+
+
+def test_gram_invariants(orc):
+    """P4: Hermitian, real positive diagonal, PSD, |rho_ij| <= 1."""
+    u = orc.users(r=(2.0, 20.0), az=(-75.0, 75.0))
+    pos = orc.gen_drops(u, 6, 5, seed=3)
+    G = orc.gram_exact(orc.array("ula", n_y=512, fc_hz=100e9), pos)
+    assert np.array_equal(G, np.conj(np.swapaxes(G, 1, 2)))
+    d = np.real(np.diagonal(G, axis1=1, axis2=2))
+    assert np.all(d > 0) and np.all(np.imag(np.diagonal(G, axis1=1, axis2=2)) == 0)
+    for g in G:
+        ev = np.linalg.eigvalsh(g)
+        assert ev.min() >= -1e-9 * np.trace(g).real
+    rho = np.abs(G) / np.sqrt(d[:, :, None] * d[:, None, :])
+    assert rho.max() <= 1 + 1e-12
+
+
+def test_single_element_rank_one(orc):
+    """P14: N = 1 => G = h h^H (rank one) and ZF fails (flag bit 0) for K >= 2."""
+    pos = orc.gen_drops(orc.users(), 3, 1, seed=1)
+    G = orc.gram_exact(orc.array("ula", n_y=1), pos)
+    h = orc.channel_matrix(orc.array("ula", n_y=1), pos[0])[0]
+    assert np.allclose(G[0], np.outer(np.conj(h), h), rtol=1e-14, atol=0)
+    rates, fl = orc.sum_rate(G, [10.0], orc.RECV_ZF | orc.RECV_MMSE)
+    assert fl[0] & 1 and np.isnan(rates[0, 0, 0]) and np.isfinite(rates[0, 0, 1])
+
+
+# --------------------------------------------------------------------------- Eq. (4)/(5)/(12): power
+def test_diag_matches_eq4(orc):
+    """P1: exact G_ii (Eq. 3 summed) vs the closed-form Eq. (4) midpoint-rule integral:
+    <= 6e-6 relative for every N, <= 1e-7 once N >= 4096 and x >= 3 m."""
+    cases = [(1.0, 0.0), (5.0, 2.0), (3.0, -10.0), (30.0, 0.0), (1.5, 7.0), (0.2, 0.1)]
+    for fc in (28e9, 100e9, 140e9):
+        for N in (16, 256, 4096, 65536):
+            arr = orc.array("ula", n_y=N, fc_hz=fc)
+            lam = orc.wavelength(arr)
+            pos = np.array([[[x, y, 0.0] for (x, y) in cases]])
+            G = orc.gram_exact(arr, pos)[0]
+            for i, (x, y) in enumerate(cases):
+                ref = orc.power_eq4(N, lam, 1.0, x, y)
+                rel = abs(G[i, i].real - ref) / ref
+                assert rel < 6e-6
+                if N >= 4096 and x >= 3.0:
+                    assert rel < 1e-7
+
+
+@pytest.mark.parametrize("t", [0.5, 0.8, 0.9, 0.99])
+@pytest.mark.parametrize("x", [1.0, 5.0, 10.0])
+def test_eq4_over_eq5_is_t_at_eq12(orc, t, x):
+    """P2: Eqs. (10)-(12): at y = 0 and real M = 4 x t/(lambda sqrt(1-t^2)), Eq.(4)/Eq.(5) == t."""
+    lam = C / 100e9
+    M = 4 * x * t / (lam * math.sqrt(1 - t * t))
+    r = orc.power_eq4(M, lam, 1.0, x, 0.0) / orc.power_limit_eq5(lam, 1.0, x)
+    assert r == pytest.approx(t, abs=2e-15)
+
+
+def test_eq4_eq5_spec_examples(orc):
+    for ex in GOLD["power_limit_eq5"]:
+        assert orc.power_limit_eq5(ex["lambda"], ex["beta0"], ex["x"]) == pytest.approx(ex["value"], rel=1e-14)
+    for ex in GOLD["eq4_threshold"]:
+        r = orc.power_eq4(ex["M"], ex["lambda"], 1.0, ex["x"], ex["y"]) / orc.power_limit_eq5(ex["lambda"], 1.0, ex["x"])
+        assert r == pytest.approx(ex["t"], abs=ex["ratio_tol"]) and r >= ex["t"]
+    for ex in GOLD["eq12_threshold"]:
+        M = 4 * ex["x"] * ex["t"] / (ex["lambda"] * math.sqrt(1 - ex["t"] ** 2))
+        assert M == pytest.approx(ex["M_real"], abs=ex["tol"])
+    # Eq. (4) -> Eq. (5) as M -> infinity and monotone in M
+    lam = 0.003
+    vals = [orc.power_eq4(M, lam, 1.0, 1.0, 0.3) for M in (10, 100, 1000, 10 ** 4, 10 ** 6, 10 ** 9)]
+    assert all(b >= a for a, b in zip(vals, vals[1:]))
+    assert vals[-1] == pytest.approx(orc.power_limit_eq5(lam, 1.0, 1.0), rel=1e-8)
+
+
+# --------------------------------------------------------------------------- Eq. (6)/(8): correlation
+def test_corr_eq6_vs_exact_spm_regime(orc):
+    """P3 / R6: |rho_exact| and arg(rho_exact) (rho = h_i^H h_j/(|h_i||h_j|))
+    agree with Eq. (6) where the stationary point u* lies well inside the array
+    (|u*| <= N lambda/40) and ||x_i|-|x_j|| >= 10 lambda: <= 2.5 % / 0.02 rad at
+    N = 16384, 100 GHz (1.73 % / 0.0125 rad)."""
+    fc, N = 100e9, 16384
+    lam = C / fc
+    arr = orc.array("ula", n_y=N, fc_hz=fc)
+    rng = np.random.default_rng(11)
+    got = 0
+    while got < 12:
+        xi, xj = rng.uniform(1, 10, 2)
+        yi, yj = rng.uniform(-7.5, 7.5, 2)
+        if abs(xi - xj) < 10 * lam:
+            continue
+        ustar = yi - xi * (yj - yi) / (xj - xi)
+        if abs(ustar) > N * lam / 40:
+            continue
+        got += 1
+        pos = np.array([[[xi, yi, 0.0], [xj, yj, 0.0]]])
+        G = orc.gram_exact(arr, pos)[0]
+        rho = G[0, 1] / math.sqrt(G[0, 0].real * G[1, 1].real)
+        ref = orc.corr_eq6(N, lam, xi, yi, xj, yj)
+        assert abs(abs(rho) - abs(ref)) / abs(ref) < 0.025
+        assert abs(np.angle(rho / ref)) < 0.02
+
+
+def test_corr_exact_tends_to_eq8(orc):
+    """P3: as N grows the exact correlation tends to the constant of Eq. (8)."""
+    fc = 100e9
+    lam = C / fc
+    xi, yi, xj, yj = 1.0, 0.2, 2.0, 0.1
+    lim = orc.corr_limit_eq8(lam, xi, yi, xj, yj)
+    errs = []
+    for N in (2 ** 14, 2 ** 16, 2 ** 18):
+        G = orc.gram_exact(orc.array("ula", n_y=N, fc_hz=fc), np.array([[[xi, yi, 0.0], [xj, yj, 0.0]]]))[0]
+        rho = G[0, 1] / math.sqrt(G[0, 0].real * G[1, 1].real)
+        errs.append(abs(rho - lim) / abs(lim))
+    assert errs[-1] < 2e-3 and errs[-1] < errs[0]
+    # Eq. (6) itself tends to Eq. (8) as M -> infinity
+    assert abs(orc.corr_eq6(1e12, lam, xi, yi, xj, yj) - lim) < 1e-8 * abs(lim)
+
+
+def test_corr_spec_examples(orc):
+    for ex in GOLD["corr_limit_eq8"]:
+        r = orc.corr_limit_eq8(ex["lambda"], ex["ui"][0], ex["ui"][1], ex["uj"][0], ex["uj"][1])
+        assert abs(r) == pytest.approx(ex["abs_rho"], rel=1e-13)
+        # sgn(|x_i| - |x_j|) = sgn(-1) = -1: phase = -(2 pi d/lambda - pi/4) (SPEC.md:236 text garbled)
+        d = 1.0
+        ph = -(2 * math.pi * d / ex["lambda"] - math.pi / 4)
+        assert abs(np.angle(r / abs(r) / complex(math.cos(ph), math.sin(ph)))) < 1e-9
+    # equal radial distance => zero, sgn(0) = -1 (Eq. 7)
+    assert abs(orc.corr_eq6(1000, 0.003, 2.0, 0.0, 2.0, 1.0)) == 0.0
+    # swap i<->j conjugates (R6)
+    a = orc.corr_eq6(5000, 0.003, 1.3, 0.2, 2.1, -0.4)
+    b = orc.corr_eq6(5000, 0.003, 2.1, -0.4, 1.3, 0.2)
+    assert abs(a - np.conj(b)) < 1e-9 * abs(a)
+
+
+# --------------------------------------------------------------------------- a4: closed-form Gram
+def test_closed_form_gram_structure(orc):
+    """Eqs. (22)-(23): diag = Eq. (4); off-diag magnitude equals the
+    simplified form 2 beta0 |dx| / (sqrt(lambda) d^{3/2} sqrt(x_i x_j)) (the Eq. 4 brackets
+    cancel, R8) -- an algebraic identity independent of how the oracle writes Eq. (6)."""
+    arr = orc.array("ula", n_y=4096, fc_hz=100e9)
+    lam = orc.wavelength(arr)
+    pos = orc.gen_drops(orc.users(r=(2.0, 20.0), az=(-75.0, 75.0)), 6, 3, seed=2)
+    G, fl = orc.gram_closed_form(arr, pos)
+    for d in range(3):
+        assert np.array_equal(G[d], np.conj(G[d].T))
+        for i in range(6):
+            xi, yi = pos[d, i, 0], pos[d, i, 1]
+            assert G[d, i, i].real == pytest.approx(orc.power_eq4(4096, lam, 1.0, xi, yi), rel=1e-15)
+            for j in range(i + 1, 6):
+                xj, yj = pos[d, j, 0], pos[d, j, 1]
+                dx = abs(xi) - abs(xj)
+                dd = math.hypot(dx, yi - yj)
+                simp = 2 * abs(dx) / (math.sqrt(lam) * dd ** 1.5 * math.sqrt(xi * xj))
+                assert abs(G[d, i, j]) == pytest.approx(simp, rel=1e-12)
+                # phase: sgn(dx) (2 pi d/lambda - pi/4), Eq. (6)
+                ph = (1 if dx > 0 else -1) * (2 * math.pi * dd / lam - math.pi / 4)
+                assert abs(np.angle(G[d, i, j] / abs(G[d, i, j]) * complex(math.cos(ph), -math.sin(ph)))) < 1e-8
+
+
+def test_closed_form_degenerate_and_k1(orc):
+    arr = orc.array("ula", n_y=1024, fc_hz=100e9)
+    lam = orc.wavelength(arr)
+    pos = np.array([[[2.0, 0.0, 0.0], [2.0 + 0.5 * lam, 1.0, 0.0], [5.0, -1.0, 0.0]]])
+    G, fl = orc.gram_closed_form(arr, pos)
+    assert fl[0] & 8  # |dx| < lambda
+    pos1 = np.array([[[3.0, 1.0, 0.0]]])
+    G1, fl1 = orc.gram_closed_form(arr, pos1)
+    assert fl1[0] == 0 and G1[0, 0, 0].real == orc.power_eq4(1024, lam, 1.0, 3.0, 1.0)
+    # K=1 rate = log2(1 + rho Eq.4) (P5)
+    r, _ = orc.sum_rate(G1, [10.0], orc.RECV_ZF)
+    assert r[0, 0, 0] == pytest.approx(math.log2(1 + 10 * orc.power_eq4(1024, lam, 1.0, 3.0, 1.0)), rel=1e-14)
+
+
+def test_closed_form_regime_cfg3(orc):
+    """P15 (regime, not parity): at cfg3 geometry the closed form is within a few % of the exact
+    Gram (median relative Frobenius ~0.6 %)."""
+    arr = orc.array("ula", n_y=16384, fc_hz=100e9)
+    pos = orc.gen_drops(orc.users(r=(2.0, 20.0), az=(-75.0, 75.0)), 16, 4, seed=0)
+    Ge = orc.gram_exact(arr, pos)
+    Gc, _ = orc.gram_closed_form(arr, pos)
+    rel = [np.linalg.norm(Gc[d] - Ge[d]) / np.linalg.norm(Ge[d]) for d in range(4)]
+    assert np.median(rel) < 0.03
+
+
+# --------------------------------------------------------------------------- a5: receivers
+def _first_principles_rates(H, rho):
+    """Combiner SINRs from H itself (P7): MRC w=h_i; ZF W=(H^H H)^{-1} H^H;
+    MMSE SINR_i = rho h_i^H (I + rho sum_{j!=i} h_j h_j^H)^{-1} h_i; CAP via LAPACK slogdet."""
+    M, K = H.shape
+    G = H.conj().T @ H
+    cap = np.linalg.slogdet(np.eye(K) + rho * G)[1] / math.log(2)
+    mrc = zf = mmse = 0.0
+    W = np.linalg.inv(G) @ H.conj().T
+    for i in range(K):
+        w = H[:, i]
+        sig = rho * abs(w.conj() @ H[:, i]) ** 2
+        intf = rho * sum(abs(w.conj() @ H[:, j]) ** 2 for j in range(K) if j != i)
+        mrc += math.log2(1 + sig / (intf + np.linalg.norm(w) ** 2))
+        zf += math.log2(1 + rho / np.linalg.norm(W[i]) ** 2)
+        R = np.eye(M) + rho * sum(np.outer(H[:, j], H[:, j].conj()) for j in range(K) if j != i)
+        mmse += math.log2(1 + (rho * H[:, i].conj() @ np.linalg.solve(R, H[:, i])).real)
+    return cap, zf, mmse, mrc
+
+
+def test_receivers_vs_first_principles(orc):
+    arr = orc.array("ula", n_y=48, fc_hz=28e9)
+    pos = orc.gen_drops(orc.users(r=(3.0, 30.0)), 5, 3, seed=4)
+    G = orc.gram_exact(arr, pos)
+    allr = orc.RECV_CAP | orc.RECV_ZF | orc.RECV_MMSE | orc.RECV_MRC
+    snr = [0.0, 10.0, 20.0]
+    rates, fl = orc.sum_rate(G, snr, allr)
+    assert np.all(fl == 0)
+    for d in range(3):
+        H = orc.channel_matrix(arr, pos[d])
+        for s, sdb in enumerate(snr):
+            ref = _first_principles_rates(H, 10 ** (sdb / 10))
+            assert np.allclose(rates[d, s], ref, rtol=1e-10, atol=1e-10)
+
+
+def test_receivers_k1_k2_and_diagonal(orc):
+    """P5, P6: K=1 all receivers = log2(1+rho g); K=2 hand formulas; diagonal G => all equal."""
+    rho = 10.0
+    g = np.array([[[3.5 + 0j]]])
+    r, _ = orc.sum_rate(g, [10.0], 15)
+    assert np.allclose(r[0, 0], math.log2(1 + rho * 3.5), rtol=1e-15)
+    a, c, b = 2.0, 3.0, 0.7 - 0.4j
+    G2 = np.array([[[a, b], [np.conj(b), c]]])
+    r, _ = orc.sum_rate(G2, [10.0], 15)
+    det = (1 + rho * a) * (1 + rho * c) - rho ** 2 * abs(b) ** 2
+    zf = math.log2(1 + rho * (a * c - abs(b) ** 2) / c) + math.log2(1 + rho * (a * c - abs(b) ** 2) / a)
+    inv11 = (1 + rho * c) / det
+    inv22 = (1 + rho * a) / det
+    mmse = math.log2(1 / inv11) + math.log2(1 / inv22)
+    mrc = math.log2(1 + rho * a * a / (a + rho * abs(b) ** 2)) + math.log2(1 + rho * c * c / (c + rho * abs(b) ** 2))
+    assert np.allclose(r[0, 0], [math.log2(det), zf, mmse, mrc], rtol=1e-13)
+    Gd = np.array([np.diag([1.0, 2.0, 0.5]).astype(complex)])
+    r, _ = orc.sum_rate(Gd, [3.0], 15)
+    assert np.ptp(r[0, 0]) < 1e-13
+
+
+def test_receiver_ordering_and_flags(orc):
+    """P7: CAP >= MMSE >= max(ZF, MRC); singular G => ZF NaN + flag bit 0."""
+    arr = orc.array("ula", n_y=128, fc_hz=28e9)
+    pos = orc.gen_drops(orc.users(r=(5.0, 50.0)), 4, 40, seed=9)
+    G = orc.gram_exact(arr, pos)
+    r, fl = orc.sum_rate(G, [0.0, 10.0, 30.0], 15)
+    ok = np.all(np.isfinite(r), axis=(1, 2))
+    rr = r[ok]
+    assert np.all(rr[..., 0] >= rr[..., 2] - 1e-9)
+    assert np.all(rr[..., 2] >= np.maximum(rr[..., 1], rr[..., 3]) - 1e-9)
+    pos2 = np.array([[[3.0, 1.0, 0.0], [3.0, 1.0, 0.0]]])
+    G2 = orc.gram_exact(arr, pos2)
+    r2, fl2 = orc.sum_rate(G2, [10.0], orc.RECV_ZF | orc.RECV_CAP)
+    assert fl2[0] & 1 and np.isnan(r2[0, 0, 1]) and np.isfinite(r2[0, 0, 0])
+    gbad = np.array([[[np.nan, 0], [0, 1.0]]], dtype=complex)
+    r3, fl3 = orc.sum_rate(gbad, [10.0], 15)
+    assert fl3[0] & 16 and np.all(np.isnan(r3))
+
+
+# --------------------------------------------------------------------------- a6: saturation
+@pytest.mark.parametrize("ex", GOLD["multiuser_bounds"])
+def test_multiuser_bounds_spec_examples(orc, ex):
+    pos = np.array([[[u[0], u[1], 0.0] for u in ex["users"]]])
+    up, dn = orc.saturation_coords(pos, ex["t"])
+    assert up[0] == pytest.approx(ex["y_up"], abs=ex["tol"])
+    assert dn[0] == pytest.approx(ex["y_down"], abs=ex["tol"])
+    # translation equivariance y -> y + 5
+    pos[..., 1] += 5.0
+    up2, dn2 = orc.saturation_coords(pos, ex["t"])
+    assert up2[0] - up[0] == pytest.approx(5.0, abs=1e-12) and dn2[0] - dn[0] == pytest.approx(5.0, abs=1e-12)
+
+
+def _eq17_paper(x_min, x_max, y_min, y_max, t, K):
+    """Eq. (17) with the undefined '(2N+1)' read as (2K+1) (R16) and
+    B(x; a, b) the non-regularised incomplete beta (R17) = betainc * beta."""
+    from scipy.special import beta, betainc
+    s = t / math.sqrt(1 - t * t)
+    L1 = x_min * s + y_min
+    R1 = min(x_min * s + y_max, x_max * s + y_min)
+    L2 = max(x_min * s + y_max, x_max * s + y_min)
+    R2 = x_max * s + y_max
+    a = (L2 - 2 * R1 + R2) / (2 * (R2 - R1))
+    b = (R1 - L1) / (2 * (R2 - R1))
+    xb = (R1 - L1) / (2 * (R2 - R1))
+    B = betainc(1.5, K, xb) * beta(1.5, K)
+    return (R2 - a ** K * (L2 - 2 * R1 + R2) / (2 * (K + 1)) - a ** K * (R1 - L1)
+            - b ** K * (R1 - L1) / (2 * (K + 1) * (2 * K + 1))
+            - math.sqrt(2) * K * math.sqrt((R1 - L1) * (R2 - R1)) * B)
+
+
+@pytest.mark.parametrize("rect", [(1.0, 10.0, -7.5, 7.5), (1.0, 2.0, -7.5, 7.5)])
+@pytest.mark.parametrize("K", [1, 2, 10, 100, 1000])
+def test_appendix_b_quadrature_equals_eq17(orc, rect, K):
+    """P9: the Appendix B pipeline (oracle quadrature of F_z^K) equals Eq. (17) with (2K+1)."""
+    q = orc.ergodic_y_up_rect(*rect, 0.9, K)
+    assert q == pytest.approx(_eq17_paper(*rect, 0.9, K), abs=1e-9)
+    # Eq. (18): E[y_up] + E[y_down] = y_min + y_max
+    assert q + orc.ergodic_y_down_rect(*rect, 0.9, K) == pytest.approx(rect[2] + rect[3], abs=1e-12)
+
+
+def test_appendix_b_limits_and_paper_numbers(orc):
+    """Eqs. (19)-(20): K -> inf gives the corner points; P10: the E2 setting saturates
+    'around 10^4 antennas'; K_list monotone."""
+    s = orc.slope(0.9)
+    R2 = 10 * s + 7.5
+    assert orc.ergodic_y_up_rect(1, 10, -7.5, 7.5, 0.9, 10 ** 4) == pytest.approx(R2, rel=0.01)
+    vals = [orc.ergodic_y_up_rect(1, 10, -7.5, 7.5, 0.9, K) for K in (1, 2, 5, 10, 100, 1000)]
+    assert all(b >= a for a, b in zip(vals, vals[1:])) and vals[-1] <= R2
+    # K = 1: mean of z = s (x_min+x_max)/2 + (y_min+y_max)/2
+    assert vals[0] == pytest.approx(s * 5.5, abs=1e-9)
+    lam = C / 100e9
+    e2 = GOLD["paper_settings"]["E2_capacity_vs_ant"]
+    up = orc.ergodic_y_up_rect(*e2["x"], *e2["y"], 0.9, e2["K"])
+    dn = orc.ergodic_y_down_rect(*e2["x"], *e2["y"], 0.9, e2["K"])
+    M = math.ceil((up - dn) / (lam / 2))
+    assert 0.5 * e2["M_sat_order"] < M < 2 * e2["M_sat_order"]
+    # App. C envelope dominates the beta term
+    from scipy.special import beta, betainc
+    L1, R1, L2, R2b = orc.trapezoid_breakpoints(1, 10, -7.5, 7.5, 0.9)
+    for K in (2, 10, 100, 1000):
+        xb = (R1 - L1) / (2 * (R2b - R1))
+        term = math.sqrt(2) * K * math.sqrt((R1 - L1) * (R2b - R1)) * betainc(1.5, K, xb) * beta(1.5, K)
+        env = math.sqrt(2) * math.sqrt((R1 - L1) * (R2b - R1)) * math.gamma(1.5) * K ** -0.5
+        assert term <= env * 1.05  # '~' asymptotic, Gamma(b)/Gamma(a+b) ~ b^-a
+
+
+def test_hexagonal_packing_numbers():
+    """P11: App. A arithmetic."""
+    ex = GOLD["hexagonal_packing"][0]
+    dens = 2 / (math.sqrt(3) * ex["d"] ** 2)
+    assert dens == pytest.approx(ex["density"], abs=5e-4)
+    assert round(ex["area_m2"] * dens) == ex["cap"]
+
+
+def test_polar_saturation_quadrature_vs_monte_carlo(orc):
+    """R15: the oracle's polar-law Appendix B quadrature agrees with the Monte Carlo mean of
+    the per-drop Eqs. (13)-(16) (oracle drops) within 4 standard errors, cfg2 law."""
+    u = orc.users(r=(3.0, 30.0), az=(-60.0, 60.0))
+    pos = orc.gen_drops(u, 8, 20000, seed=123)
+    up, dn = orc.saturation_coords(pos, 0.9)
+    lam = C / 28e9
+    Eup, Edn, M = orc.ergodic_saturation_polar(3.0, 30.0, -60.0, 60.0, 0.9, 8, lam / 2)
+    assert abs(up.mean() - Eup) < 4 * up.std() / math.sqrt(up.size)
+    assert abs(dn.mean() - Edn) < 4 * dn.std() / math.sqrt(dn.size)
+    assert M == pytest.approx(20383, rel=0.01)
+
+
+def test_capacity_saturates_in_n(orc):
+    """P8 (north_star): per-drop capacity is non-decreasing in N for nested centred arrays and
+    levels off at the analytic saturation point (cfg2 geometry; fewer drops)."""
+    w_nl = [2 ** k for k in range(8, 17)]
+    arr = orc.array("ula", n_y=65536, fc_hz=28e9)
+    pos = orc.gen_drops(orc.users(r=(3.0, 30.0)), 8, 12, seed=0)
+    erg, nv, sat, pd = orc.saturation_sweep(arr, w_nl, pos, [0.0, 10.0, 20.0], orc.RECV_CAP, per_drop=True)
+    cap = pd[..., 0]                                 # (D, nN, S)
+    assert np.all(np.diff(cap, axis=1) >= -1e-9)
+    norm = erg[:, :, 0] / erg[-1:, :, 0]             # (nN, S)
+    msat = 20383
+    for n, N in enumerate(w_nl):
+        if N >= msat:
+            assert np.all(norm[n] >= 0.99)
+        if N <= msat / 5:
+            assert np.all(norm[n] <= 0.95)
+    # faster convergence at higher SNR
+    assert norm[4, 2] >= norm[4, 0]
+    assert sat[2] == math.ceil((sat[0] - sat[1]) / (C / 28e9 / 2))
+
+
+def test_upa_diagonal_solid_angle(orc):
+    """P17 / R5: UPA diagonal = (4 beta0/lambda^2) * solid angle of the array rectangle."""
+    fc = 100e9
+    lam = C / fc
+    for (ny, nz) in [(64, 64), (128, 32)]:
+        arr = orc.array("upa", n_y=ny, n_z=nz, fc_hz=fc)
+        pos = orc.gen_drops(orc.users(r=(2.0, 20.0), az=(-60, 60), el=(-30, 30)), 3, 1, seed=ny)
+        G = orc.gram_exact(arr, pos)[0]
+        for i in range(3):
+            x, y, z = pos[0, i]
+            Y, Z = ny * lam / 4, nz * lam / 4
+            om = 0.0
+            for sy, yc in ((1, Y), (-1, -Y)):
+                for sz, zc in ((1, Z), (-1, -Z)):
+                    u, v = yc - y, zc - z
+                    om += sy * sz * math.atan(u * v / (x * math.sqrt(x * x + u * u + v * v)))
+            assert G[i, i].real == pytest.approx(4 / lam ** 2 * om, rel=1e-5)
