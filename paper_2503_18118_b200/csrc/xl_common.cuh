@@ -1,0 +1,212 @@
+// xl_common.cuh -- device helpers shared by the xlmimo kernels (sm_100a).
+//
+// Product code: shares nothing with oracle/.  See include/xlmimo.h for the ABI
+// and DESIGN.md for the kernel designs and the readings R1..R23.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/xlmimo.h"
+
+namespace xl {
+
+constexpr double kC = 299792458.0;  // m/s, exact (R2)
+constexpr int kMaxK = 64;           // fused paths: K <= 64
+constexpr int kMaxSnr = 16;
+
+// ---------------------------------------------------------------------------
+// Philox4x64-10 (Salmon et al., SC'11), device implementation (R19).
+// ---------------------------------------------------------------------------
+struct u64x4 { uint64_t v[4]; };
+
+__device__ __forceinline__ u64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                                               uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi0 = __umul64hi(M0, c0), lo0 = M0 * c0;
+    const uint64_t hi1 = __umul64hi(M1, c2), lo1 = M1 * c2;
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += W0; k1 += W1;
+  }
+  u64x4 o; o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+  return o;
+}
+
+__device__ __forceinline__ double u01_53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
+
+// ---------------------------------------------------------------------------
+// sin/cos of 2*pi*f for f in [-1/2, 1/2] (the fp64-reduced phase fraction).
+// Quadrant split k = rint(4f), g = f - k/4 (exact), |2 pi g| <= pi/4, then the
+// Taylor series of sin to theta^15 and cos to theta^16 in g with the (2pi)^n/n!
+// folded into the coefficients: truncation < 5e-17 absolute (K2).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sincos2pi_reduced(double f, double &s, double &c) {
+  const double k = rint(4.0 * f);
+  const double g = fma(-0.25, k, f);
+  const double g2 = g * g;
+  double ps = -7.1812230177850051223e-1;
+  ps = fma(ps, g2, 3.8199525848482821277);
+  ps = fma(ps, g2, -1.5094642576822990392e+1);
+  ps = fma(ps, g2, 4.2058693944897653145e+1);
+  ps = fma(ps, g2, -7.6705859753061385842e+1);
+  ps = fma(ps, g2, 8.1605249276075054203e+1);
+  ps = fma(ps, g2, -4.1341702240399760234e+1);
+  ps = fma(ps, g2, 6.2831853071795864769);
+  const double sn = ps * g;
+  double pc = 0.28200596845579121507;
+  pc = fma(pc, g2, -1.7143907110886720654);
+  pc = fma(pc, g2, 7.9035363713184688042);
+  pc = fma(pc, g2, -26.426256783374397453);
+  pc = fma(pc, g2, 60.244641371876660363);
+  pc = fma(pc, g2, -85.456817206693727736);
+  pc = fma(pc, g2, 64.939394022668291491);
+  pc = fma(pc, g2, -19.739208802178717238);
+  const double cs = fma(pc, g2, 1.0);
+  const int q = ((int)k) & 3;  // 2 pi f = 2 pi g + q pi/2
+  // q=0: (cs, sn); q=1: (-sn, cs); q=2: (-cs, -sn); q=3: (sn, -cs)  -> (cos, sin)
+  const double c1 = (q & 1) ? sn : cs;
+  const double s1 = (q & 1) ? cs : sn;
+  c = (q == 1 || q == 2) ? -c1 : c1;
+  s = (q >= 2) ? -s1 : s1;
+}
+
+// fp32 variant for the XLMIMO_FP32 path: f is the fp64-reduced fraction cast to
+// fp32 (R13); MUFU sin/cos after the same exact quadrant split.
+__device__ __forceinline__ void sincos2pi_reduced_f32(float f, float &s, float &c) {
+  __sincosf(6.28318530717958647692f * f, &s, &c);
+}
+
+// ---------------------------------------------------------------------------
+// Per-user constants of Eq. (3) for the fused generator.
+//   ULA: r^2 = xz2 + (y_user - y_m)^2 with xz2 = x^2 + z^2 (R21), amplitude
+//        sqrt(beta0) sqrt(x_eff) r^{-3/2} with x_eff = sqrt(xz2).
+//   UPA: r^2 = x^2 + (y - y_p)^2 + (z - z_q)^2, x_eff = |x| (R5).
+// ---------------------------------------------------------------------------
+struct UserC {
+  double xz2;   // ULA: x^2+z^2 ; UPA: x^2
+  double y, z;  // user y (and z for UPA)
+  double amp;   // sqrt(beta0) * sqrt(x_eff)
+};
+
+__device__ __forceinline__ UserC make_user(const double *p, int kind, double sqrt_beta0) {
+  UserC u;
+  const double x = p[0], y = p[1], z = p[2];
+  if (kind == XLMIMO_ULA) {
+    u.xz2 = fma(x, x, z * z);
+    u.z = 0.0;
+    u.amp = sqrt_beta0 * sqrt(sqrt(u.xz2));
+  } else {
+    u.xz2 = x * x;
+    u.z = z;
+    u.amp = sqrt_beta0 * sqrt(fabs(x));
+  }
+  u.y = y;
+  return u;
+}
+
+// h = amp * r^{-3/2} * e^{-j 2 pi frac(r/lambda)}  (Eq. 3), fp64.
+// r2 = distance^2.  r is refined to ~0.5 ulp with one residual step so the
+// phase fraction keeps ~1e-11 rad at r/lambda ~ 1e5 (north_star: fp64 range reduction).
+__device__ __forceinline__ void coef_from_r2(double r2, double amp, double inv_lambda, double &re,
+                                             double &im) {
+  const double ir = rsqrt(r2);
+  double r = r2 * ir;
+  r = fma(0.5 * ir, fma(-r, r, r2), r);  // Newton/residual correction of sqrt(r2)
+  const double q = r * inv_lambda;
+  const double f = q - rint(q);
+  double s, c;
+  sincos2pi_reduced(f, s, c);
+  const double a = amp * ir * rsqrt(r);  // r^{-3/2}
+  re = a * c;
+  im = -a * s;
+}
+
+// fp32 phasor and amplitude from fp64 distance / phase reduction (XLMIMO_FP32, K3).
+__device__ __forceinline__ void coef_from_r2_f32(double r2, double amp, double inv_lambda, float &re,
+                                                 float &im) {
+  const double ir = rsqrt(r2);
+  double r = r2 * ir;
+  r = fma(0.5 * ir, fma(-r, r, r2), r);
+  const double q = r * inv_lambda;
+  const float f = (float)(q - rint(q));
+  float s, c;
+  sincos2pi_reduced_f32(f, s, c);
+  const float rf = (float)r;
+  const float a = (float)amp * rsqrtf(rf) / rf;
+  re = a * c;
+  im = -a * s;
+}
+
+// Element coordinate of the "centred order" index t used by every exact-Gram
+// kernel (ULA): for N even, t -> pair p = t>>1 at y = +-(p + 1/2) pitch; for N
+// odd, t = 0 is the centre and t >= 1 -> +-(((t-1)>>1) + 1) pitch.  The first
+// N' indices of this order are exactly the centred N'-element array of the same
+// parity, which makes nested N a prefix (R18, saturation sweep).
+__device__ __forceinline__ double ula_y_centred(int64_t t, bool n_odd, double pitch) {
+  if (n_odd) {
+    if (t == 0) return 0.0;
+    const int64_t p = (t - 1) >> 1;
+    const double y = (double)(p + 1) * pitch;
+    return (t & 1) ? y : -y;
+  }
+  const int64_t p = t >> 1;
+  const double y = ((double)p + 0.5) * pitch;
+  return (t & 1) ? -y : y;
+}
+
+}  // namespace xl
+
+// ---------------------------------------------------------------------------
+// Host-side internal interface between the ABI layer and the kernel files.
+// ---------------------------------------------------------------------------
+namespace xlh {
+
+struct ArrayP {
+  int kind;
+  int64_t n_y, n_z;
+  double lambda, pitch, sqrt_beta0;
+};
+
+void count_launch(uint64_t n = 1);
+
+// Event bracket for the profiling hooks (no-op unless xlmimo_timing_enable(1)).
+struct KTimer {
+  void *rec = nullptr;
+  KTimer(cudaStream_t s, const char *name);
+  void stop(cudaStream_t s);
+};
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+
+// xl_drops.cu
+int launch_gen_drops(const xlmimo_users_t &u, int K, int64_t n_drops, uint64_t seed, uint64_t first_drop,
+                     double *pos, cudaStream_t s);
+
+// xl_gram.cu
+// Exact Gram over element indices [0, N) in the "centred order", with snapshots
+// at the level ends lvl_end[0..n_lvl-1] (ascending, last = N).  Output:
+// out[drop][lvl][K][K][2] full Hermitian.  Scratch: gram_ws_bytes().
+size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode);
+int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
+                      int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
+                      cudaStream_t s);
+
+// xl_closed.cu : out[drop][lvl][K][K][2] for M = n_list[lvl]
+int launch_closed_form(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *m_list,
+                       int n_lvl, double *out, uint32_t *flags, cudaStream_t s);
+
+// xl_rates.cu : problems = n_prob Grams [n_prob][K][K][2]; flags per problem
+int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr_db, int n_snr,
+                    uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s);
+
+// xl_sweep.cu reductions
+int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, int64_t *count,
+                          cudaStream_t s);
+int launch_saturation_stats(const double *pos, int K, int64_t n_drops, double t, double pitch, double *sat,
+                            cudaStream_t s);
+
+}  // namespace xlh

@@ -1,0 +1,42 @@
+// xl_drops.cu -- a1: seeded user drops (R3, R5, R19).
+#include "xl_common.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(256) gen_drops_kernel(xlmimo_users_t u, int K, int64_t n_total,
+                                                        uint64_t seed, uint64_t first_drop, double *pos) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_total) return;
+  const int64_t d = idx / K;
+  const int k = (int)(idx - d * K);
+  const xl::u64x4 w = xl::philox4x64_10(first_drop + (uint64_t)d, (uint64_t)k, 0, 0, seed, 0);
+  const double deg = 3.14159265358979323846 / 180.0;
+  const double r = u.r_min_m + (u.r_max_m - u.r_min_m) * xl::u01_53(w.v[0]);
+  const double az = (u.az_min_deg + (u.az_max_deg - u.az_min_deg) * xl::u01_53(w.v[1])) * deg;
+  const double el = (u.el_min_deg + (u.el_max_deg - u.el_min_deg) * xl::u01_53(w.v[2])) * deg;
+  double sa, ca, se, ce;
+  sincos(az, &sa, &ca);
+  sincos(el, &se, &ce);
+  double *p = pos + idx * 3;
+  p[0] = r * ce * ca;
+  p[1] = r * ce * sa;
+  p[2] = r * se;
+}
+
+}  // namespace
+
+namespace xlh {
+
+int launch_gen_drops(const xlmimo_users_t &u, int K, int64_t n_drops, uint64_t seed, uint64_t first_drop,
+                     double *pos, cudaStream_t s) {
+  const int64_t n = n_drops * (int64_t)K;
+  if (n == 0) return XLMIMO_OK;
+  const int64_t blocks = (n + 255) / 256;
+  KTimer tm(s, "gen_drops");
+  gen_drops_kernel<<<(unsigned)blocks, 256, 0, s>>>(u, K, n, seed, first_drop, pos);
+  tm.stop(s);
+  count_launch();
+  return check_launch("gen_drops_kernel");
+}
+
+}  // namespace xlh

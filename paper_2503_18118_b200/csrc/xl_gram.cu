@@ -1,0 +1,423 @@
+// xl_gram.cu -- a2+a3: exact Gram G = H^H H of the PNUSW channel (Eq. 3),
+// generated on the fly (fused; never materialised), fp64 or fp32 phasors.
+//
+// PAPER.md:240 names "the inner product calculation for elements in H^H H" as
+// the dominant cost; these kernels are that step.  Design (K2/K3):
+//  * grid = n_drops x n_split blocks; a block owns one drop and a contiguous
+//    range of element indices in the "centred order" (xl::ula_y_centred), so the
+//    N' < N arrays of a saturation sweep are prefixes (R18);
+//  * segment ends (level boundaries of the sweep, or N) emit a block-reduced
+//    partial upper triangle to the workspace -- deterministic, no atomics;
+//  * gram_reduce_kernel sums partials in fixed (level, split) order into the
+//    full Hermitian K x K per (drop, level), Im diag = 0 (R20).
+//  Small K (<= 8): every thread owns all K(K+1)/2 accumulators in registers and
+//  generates the K coefficients of its element (kernel A).  Larger K (<= 64):
+//  tiles of 32 elements are generated into shared memory as interleaved complex,
+//  then each thread accumulates one 4x4 register block of the upper triangle
+//  over a subset of the tile's elements (kernel B).
+#include <cstdio>
+#include <type_traits>
+
+#include "xl_common.cuh"
+
+namespace {
+
+constexpr int kMaxLvl = 32;
+
+struct GramParams {
+  const double *pos;
+  double *ws;          // partials [drop][split][lvl][NP][2]
+  int K;
+  int kind;
+  int64_t n_y, n_z;
+  int64_t N;           // total elements (last level end)
+  int64_t chunk;       // elements per split
+  int n_split;
+  int n_lvl;
+  int64_t lvl_end[kMaxLvl];
+  double inv_lambda, pitch, sqrt_beta0;
+};
+
+struct ElemPos {
+  double y, z;
+};
+
+__device__ __forceinline__ ElemPos element_pos(const GramParams &P, int64_t t) {
+  ElemPos e;
+  if (P.kind == XLMIMO_ULA) {
+    e.y = xl::ula_y_centred(t, (P.N & 1) != 0, P.pitch);
+    e.z = 0.0;
+  } else {
+    const int64_t q = t / P.n_y, p = t - q * P.n_y;
+    e.y = ((double)p - 0.5 * (double)(P.n_y - 1)) * P.pitch;
+    e.z = ((double)q - 0.5 * (double)(P.n_z - 1)) * P.pitch;
+  }
+  return e;
+}
+
+__device__ __forceinline__ double dist2(const xl::UserC &u, const ElemPos &e, int kind) {
+  const double dy = e.y - u.y;
+  double r2 = fma(dy, dy, u.xz2);
+  if (kind != XLMIMO_ULA) {
+    const double dz = e.z - u.z;
+    r2 = fma(dz, dz, r2);
+  }
+  return r2;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ kernel A
+template <int KT, int NT, bool FP32>
+__global__ void __launch_bounds__(NT, 1) gram_small_kernel(GramParams P) {
+  constexpr int NP = KT * (KT + 1) / 2;
+  constexpr int NV = 2 * NP;
+  constexpr int NW = NT / 32;
+  __shared__ xl::UserC su[KT];
+  __shared__ double red[NW][NV];
+
+  const int64_t drop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < KT) su[tid] = xl::make_user(P.pos + (drop * KT + tid) * 3, P.kind, P.sqrt_beta0);
+  __syncthreads();
+
+  const int64_t s0 = (int64_t)split * P.chunk;
+  const int64_t s1 = min(P.N, s0 + P.chunk);
+  int64_t lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int64_t lv1 = P.lvl_end[l];
+    const int64_t a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+    for (int64_t t = a + tid; t < b; t += NT) {
+      const ElemPos e = element_pos(P, t);
+      double hr[KT], hi[KT];
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        const xl::UserC u = su[i];
+        const double r2 = dist2(u, e, P.kind);
+        if (FP32) {
+          float fr, fi;
+          xl::coef_from_r2_f32(r2, u.amp, P.inv_lambda, fr, fi);
+          hr[i] = fr; hi[i] = fi;
+        } else {
+          xl::coef_from_r2(r2, u.amp, P.inv_lambda, hr[i], hi[i]);
+        }
+      }
+      int v = 0;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+#pragma unroll
+        for (int j = i; j < KT; ++j) {
+          if (i == j) {
+            acc[v] = fma(hr[i], hr[i], fma(hi[i], hi[i], acc[v]));
+          } else {
+            // conj(h_i) h_j = (ar br + ai bi) + j (ar bi - ai br)
+            acc[v] = fma(hr[i], hr[j], fma(hi[i], hi[j], acc[v]));
+            acc[v + 1] = fma(hr[i], hi[j], fma(-hi[i], hr[j], acc[v + 1]));
+          }
+          v += 2;
+        }
+      }
+    }
+    // block reduction, fixed order
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double s = warp_sum(acc[v]);
+      if (lane == 0) red[warp][v] = s;
+    }
+    __syncthreads();
+    double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * NV;
+    for (int v = tid; v < NV; v += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[w][v];
+      out[v] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ kernel B
+template <int KP>
+struct TiledCfg {
+  static constexpr int NB = KP / 4;
+  static constexpr int NBP = NB * (NB + 1) / 2;
+  // smallest power-of-two group count with NBP * G >= 256 (G <= 32 lanes of one warp)
+  static constexpr int G = (NBP >= 256) ? 1 : (NBP * 2 >= 256) ? 2 : (NBP * 4 >= 256) ? 4 : (NBP * 8 >= 256) ? 8 : (NBP * 16 >= 256) ? 16 : 32;
+  static constexpr int NTASK = NBP * G;
+  static constexpr int NT = (NTASK + 31) / 32 * 32;
+  static constexpr int T = 32;  // elements per tile
+};
+
+template <typename CT>
+struct Cplx;
+template <>
+struct Cplx<double> { using T2 = double2; };
+template <>
+struct Cplx<float> { using T2 = float2; };
+
+template <int KP, bool FP32>
+__global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramParams P) {
+  using Cfg = TiledCfg<KP>;
+  using RT = typename std::conditional<FP32, float, double>::type;
+  using RT2 = typename Cplx<RT>::T2;
+  constexpr int T = Cfg::T, G = Cfg::G, NT = Cfg::NT, EPT = T / G;
+  __shared__ xl::UserC su[KP];
+  __shared__ RT2 hs[T][KP];
+
+  const int64_t drop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int tid = threadIdx.x;
+  const int K = P.K;
+  if (tid < KP) {
+    if (tid < K) su[tid] = xl::make_user(P.pos + (drop * K + tid) * 3, P.kind, P.sqrt_beta0);
+    else su[tid] = xl::UserC{1.0, 0.0, 0.0, 0.0};  // padded user: zero amplitude
+  }
+  // task -> (block pair I <= J, group g)
+  const bool active = tid < Cfg::NTASK;
+  const int bp = tid / G, g = tid - (tid / G) * G;
+  int I = 0, J = 0;
+  {
+    int rem = bp;
+    while (rem >= Cfg::NB - I) { rem -= Cfg::NB - I; ++I; }
+    J = I + rem;
+    if (!active) { I = 0; J = 0; }
+  }
+  __syncthreads();
+
+  const int64_t s0 = (int64_t)split * P.chunk;
+  const int64_t s1 = min(P.N, s0 + P.chunk);
+  int64_t lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int64_t lv1 = P.lvl_end[l];
+    const int64_t a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int64_t t0 = a; t0 < b; t0 += T) {
+      // generation: T x KP coefficients, element-major interleaved complex
+      for (int c = tid; c < T * KP; c += NT) {
+        const int e = c / KP, row = c - (c / KP) * KP;
+        const int64_t t = t0 + e;
+        RT2 h;
+        h.x = 0; h.y = 0;
+        if (t < b) {
+          const ElemPos ep = element_pos(P, t);
+          const xl::UserC u = su[row];
+          const double r2 = dist2(u, ep, P.kind);
+          if (FP32) {
+            float fr, fi;
+            xl::coef_from_r2_f32(r2, u.amp, P.inv_lambda, fr, fi);
+            h.x = fr; h.y = fi;
+          } else {
+            double dr, di;
+            xl::coef_from_r2(r2, u.amp, P.inv_lambda, dr, di);
+            h.x = (RT)dr; h.y = (RT)di;
+          }
+        }
+        hs[e][row] = h;
+      }
+      __syncthreads();
+      if (active) {
+        RT tacc[4][4][2];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) tacc[x][y][0] = tacc[x][y][1] = 0;
+#pragma unroll 4
+        for (int ee = 0; ee < EPT; ++ee) {
+          const int e = g + ee * G;
+          RT2 hiv[4], hjv[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) hiv[x] = hs[e][4 * I + x];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) hjv[y] = hs[e][4 * J + y];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              tacc[x][y][0] = fma(hiv[x].x, hjv[y].x, fma(hiv[x].y, hjv[y].y, tacc[x][y][0]));
+              tacc[x][y][1] = fma(hiv[x].x, hjv[y].y, fma(-hiv[x].y, hjv[y].x, tacc[x][y][1]));
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            acc[x][y][0] += (double)tacc[x][y][0];
+            acc[x][y][1] += (double)tacc[x][y][1];
+          }
+      }
+      __syncthreads();
+    }
+    // reduce over the G lanes of each block pair (contiguous, inside one warp)
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          double v = acc[x][y][c];
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G > 1 ? G : 1);
+          acc[x][y][c] = v;
+        }
+    if (active && g == 0) {
+      double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * (size_t)(K * (K + 1));
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int i = 4 * I + x, j = 4 * J + y;
+          if (i <= j && j < K) {
+            const int p = i * K - i * (i - 1) / 2 + (j - i);
+            out[2 * p] = acc[x][y][0];
+            out[2 * p + 1] = acc[x][y][1];
+          }
+        }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ reduce
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const double *ws, int K, int64_t n_drops, int n_split,
+                                                          int n_lvl, double *out) {
+  const int NP = K * (K + 1) / 2;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_drops * NP) return;
+  const int64_t drop = idx / NP;
+  const int p = (int)(idx - drop * NP);
+  int i = 0, rem = p;
+  while (rem >= K - i) { rem -= K - i; ++i; }
+  const int j = i + rem;
+  double re = 0.0, im = 0.0;
+  for (int l = 0; l < n_lvl; ++l) {
+    for (int s = 0; s < n_split; ++s) {
+      const double *w = ws + (((size_t)drop * n_split + s) * n_lvl + l) * (size_t)(2 * NP) + 2 * p;
+      re += w[0];
+      im += w[1];
+    }
+    double *g = out + ((size_t)drop * n_lvl + l) * (size_t)K * K * 2;
+    g[(i * K + j) * 2] = re;
+    g[(i * K + j) * 2 + 1] = (i == j) ? 0.0 : im;
+    g[(j * K + i) * 2] = re;
+    g[(j * K + i) * 2 + 1] = (i == j) ? 0.0 : -im;
+  }
+}
+
+int choose_split(int64_t n_drops, int64_t N) {
+  const int64_t target_blocks = 148 * 8;
+  int64_t s = (target_blocks + n_drops - 1) / (n_drops > 0 ? n_drops : 1);
+  const int64_t max_s = N / 4096 > 1 ? N / 4096 : 1;
+  if (s > max_s) s = max_s;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+template <int KT, bool FP32>
+void launch_small(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  gram_small_kernel<KT, 256, FP32><<<(unsigned)n_blocks, 256, 0, s>>>(P);
+}
+
+template <bool FP32>
+void launch_small_k(int K, const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  switch (K) {
+    case 1: launch_small<1, FP32>(P, n_blocks, s); break;
+    case 2: launch_small<2, FP32>(P, n_blocks, s); break;
+    case 3: launch_small<3, FP32>(P, n_blocks, s); break;
+    case 4: launch_small<4, FP32>(P, n_blocks, s); break;
+    case 5: launch_small<5, FP32>(P, n_blocks, s); break;
+    case 6: launch_small<6, FP32>(P, n_blocks, s); break;
+    case 7: launch_small<7, FP32>(P, n_blocks, s); break;
+    default: launch_small<8, FP32>(P, n_blocks, s); break;
+  }
+}
+
+template <int KP, bool FP32>
+void launch_tiled(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  gram_tiled_kernel<KP, FP32><<<(unsigned)n_blocks, TiledCfg<KP>::NT, 0, s>>>(P);
+}
+
+template <bool FP32>
+void launch_tiled_k(int K, const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  if (K <= 16) launch_tiled<16, FP32>(P, n_blocks, s);
+  else if (K <= 32) launch_tiled<32, FP32>(P, n_blocks, s);
+  else if (K <= 48) launch_tiled<48, FP32>(P, n_blocks, s);
+  else launch_tiled<64, FP32>(P, n_blocks, s);
+}
+
+}  // namespace
+
+namespace xlh {
+
+size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
+  (void)precision;
+  (void)mode;
+  const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
+  const int n_split = choose_split(n_drops, N);
+  const size_t np = (size_t)K * (K + 1) / 2;
+  return (size_t)n_drops * n_split * n_lvl * np * 2 * sizeof(double);
+}
+
+int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
+                      int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
+                      cudaStream_t s) {
+  if (mode != XLMIMO_FUSED) return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: only XLMIMO_FUSED is provided");
+  if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
+  if (n_drops == 0) return XLMIMO_OK;
+  const int64_t N = lvl_end[n_lvl - 1];
+  const size_t need = gram_ws_bytes(a, K, n_drops, n_lvl, precision, mode);
+  if (ws_bytes < need || (need && !ws))
+    return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+  GramParams P;
+  P.pos = pos;
+  P.ws = (double *)ws;
+  P.K = K;
+  P.kind = a.kind;
+  P.n_y = a.n_y;
+  P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+  P.N = N;
+  P.n_split = choose_split(n_drops, N);
+  const int64_t T = 256;
+  P.chunk = ((N + P.n_split - 1) / P.n_split + T - 1) / T * T;
+  P.n_lvl = n_lvl;
+  for (int l = 0; l < kMaxLvl; ++l) P.lvl_end[l] = l < n_lvl ? lvl_end[l] : N;
+  P.inv_lambda = 1.0 / a.lambda;
+  P.pitch = a.pitch;
+  P.sqrt_beta0 = a.sqrt_beta0;
+  const int64_t n_blocks = n_drops * P.n_split;
+  const bool fp32 = precision == XLMIMO_FP32;
+  KTimer tm(s, K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
+                      : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
+  if (K <= 8) {
+    if (fp32) launch_small_k<true>(K, P, n_blocks, s);
+    else launch_small_k<false>(K, P, n_blocks, s);
+  } else {
+    if (fp32) launch_tiled_k<true>(K, P, n_blocks, s);
+    else launch_tiled_k<false>(K, P, n_blocks, s);
+  }
+  tm.stop(s);
+  count_launch();
+  int rc = check_launch("gram_exact kernel");
+  if (rc) return rc;
+  const int64_t n_items = n_drops * (int64_t)K * (K + 1) / 2;
+  KTimer tr(s, "gram_reduce");
+  gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops, P.n_split,
+                                                                      n_lvl, out);
+  tr.stop(s);
+  count_launch();
+  return check_launch("gram_reduce_kernel");
+}
+
+}  // namespace xlh

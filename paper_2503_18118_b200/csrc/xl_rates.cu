@@ -1,0 +1,260 @@
+// xl_rates.cu -- a5: per-drop receivers on a K x K Gram (Eq. (9) PAPER.md:117-122,
+// Eq. (21); SINR definitions, R12).
+//
+// One warp per Gram.  The matrix lives in shared memory column-major
+// (As[col][row]) so lane = row accesses are conflict-free; lanes own rows
+// (Cholesky) and columns of L^{-1} (diag of the inverse).  For every SNR:
+//   I + rho G = L L^H -> CAP = 2 sum log2 L_kk, [(I+rho G)^{-1}]_ii = sum_k |(L^{-1})_ki|^2;
+//   G = L L^H once     -> [G^{-1}]_ii for ZF;  MRC straight from G.
+// A pivot that is not > 0 (or not finite) marks the factorisation failed (R10).
+#include "xl_common.cuh"
+
+namespace {
+
+struct RateParams {
+  const double *gram;
+  double *rates;
+  uint32_t *flags;
+  int K;
+  int64_t n_prob;
+  int n_snr;
+  uint32_t receivers;
+  int n_recv;
+  double rho[xl::kMaxSnr];
+};
+
+// In-place lower Cholesky of As (column-major, K x K complex) by one warp.
+// Returns true on success (uniform across the warp).
+template <int RPL>
+__device__ bool warp_cholesky(double2 *As, int K, int lane) {
+  for (int j = 0; j < K; ++j) {
+    __syncwarp();
+    const double piv = As[j * K + j].x;
+    if (!(piv > 0.0) || !isfinite(piv)) return false;
+    const double ljj = sqrt(piv), inv = 1.0 / ljj;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i > j && i < K) {
+        double2 v = As[j * K + i];
+        v.x *= inv;
+        v.y *= inv;
+        As[j * K + i] = v;
+      } else if (i == j) {
+        As[j * K + j] = make_double2(ljj, 0.0);
+      }
+    }
+    __syncwarp();
+    // trailing update: A[i][k] -= L[i][j] conj(L[k][j]) for j < k <= i
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i > j && i < K) {
+        const double2 lij = As[j * K + i];
+        for (int k = j + 1; k <= i; ++k) {
+          const double2 lkj = As[j * K + k];
+          double2 a = As[k * K + i];
+          // lij * conj(lkj) = (lr kr + li ki) + j (li kr - lr ki)
+          a.x -= lij.x * lkj.x + lij.y * lkj.y;
+          a.y -= lij.y * lkj.x - lij.x * lkj.y;
+          As[k * K + i] = a;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+// dinv[c] = [A^{-1}]_cc = sum_k |(L^{-1})_kc|^2 for the lane's columns c, with L in
+// As (column-major).  Xs: per-column scratch, Xs[k*K + c].
+template <int RPL>
+__device__ void warp_inv_diag(const double2 *As, double2 *Xs, int K, int lane, double *dinv) {
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) dinv[r] = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double2 lkk = As[k * K + k];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int c = lane + 32 * r;
+      if (c >= K) continue;
+      double2 x = make_double2(0.0, 0.0);
+      if (k >= c) {
+        double xr = (k == c) ? 1.0 : 0.0, xi = 0.0;
+        for (int j = c; j < k; ++j) {
+          const double2 l = As[j * K + k];  // L[k][j]
+          const double2 xj = Xs[j * K + c];
+          xr -= l.x * xj.x - l.y * xj.y;
+          xi -= l.x * xj.y + l.y * xj.x;
+        }
+        x.x = xr / lkk.x;
+        x.y = xi / lkk.x;
+        dinv[r] += x.x * x.x + x.y * x.y;
+      }
+      Xs[k * K + c] = x;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
+  extern __shared__ double2 smem[];
+  const int K = P.K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double2 *As = smem + (size_t)warp * 2 * K * K;
+  double2 *Xs = As + K * K;
+  const int64_t prob = (int64_t)blockIdx.x * nw + warp;
+  if (prob >= P.n_prob) return;
+  const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)prob * K * K;
+  double *out = P.rates + (size_t)prob * P.n_snr * P.n_recv;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  uint32_t fl = 0;
+
+  // non-finite input -> all NaN (flag bit 4)
+  bool fin = true;
+  for (int e = lane; e < K * K; e += 32) fin &= isfinite(G[e].x) && isfinite(G[e].y);
+  fin = __all_sync(0xffffffffu, fin);
+  if (!fin) {
+    for (int e = lane; e < P.n_snr * P.n_recv; e += 32) out[e] = nan;
+    if (lane == 0 && P.flags) P.flags[prob] |= XLMIMO_FLAG_NONFINITE;
+    return;
+  }
+
+  double zf_dinv[RPL];
+  bool zf_ok = false;
+  if (P.receivers & XLMIMO_RECV_ZF) {
+    // As[col j][row i] = G[i][j] = conj(G[j][i])
+    for (int e = lane; e < K * K; e += 32) {
+      const int j = e / K, i = e - (e / K) * K;
+      const double2 g = G[j * K + i];
+      As[e] = make_double2(g.x, -g.y);
+    }
+    zf_ok = warp_cholesky<RPL>(As, K, lane);
+    if (zf_ok) warp_inv_diag<RPL>(As, Xs, K, lane, zf_dinv);
+    else fl |= XLMIMO_FLAG_G_NOT_PD;
+  }
+  bool mrc_ok = true;
+  for (int i = lane; i < K; i += 32) mrc_ok &= G[i * K + i].x > 0.0;
+  mrc_ok = __all_sync(0xffffffffu, mrc_ok);
+  if ((P.receivers & XLMIMO_RECV_MRC) && !mrc_ok) fl |= XLMIMO_FLAG_MRC_UNDEF;
+
+  for (int s = 0; s < P.n_snr; ++s) {
+    const double rho = P.rho[s];
+    int r = 0;
+    bool a_ok = false;
+    double dinv[RPL];
+    double cap_part = 0.0;
+    if (P.receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) {
+      __syncwarp();
+      for (int e = lane; e < K * K; e += 32) {
+        const int j = e / K, i = e - (e / K) * K;
+        const double2 g = G[j * K + i];
+        As[e] = make_double2((i == j ? 1.0 : 0.0) + rho * g.x, -rho * g.y);
+      }
+      a_ok = warp_cholesky<RPL>(As, K, lane);
+      if (!a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
+      if (a_ok) {
+#pragma unroll
+        for (int rr = 0; rr < RPL; ++rr) {
+          const int k = lane + 32 * rr;
+          if (k < K) cap_part += 2.0 * log2(As[k * K + k].x);
+        }
+        if (P.receivers & XLMIMO_RECV_MMSE) warp_inv_diag<RPL>(As, Xs, K, lane, dinv);
+      }
+    }
+    if (P.receivers & XLMIMO_RECV_CAP) {
+      const double c = warp_sum(cap_part);
+      if (lane == 0) out[s * P.n_recv + r] = a_ok ? c : nan;
+      ++r;
+    }
+    if (P.receivers & XLMIMO_RECV_ZF) {
+      double part = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int i = lane + 32 * rr;
+        if (zf_ok && i < K) part += log2(1.0 + rho / zf_dinv[rr]);
+      }
+      const double c = warp_sum(part);
+      if (lane == 0) out[s * P.n_recv + r] = zf_ok ? c : nan;
+      ++r;
+    }
+    if (P.receivers & XLMIMO_RECV_MMSE) {
+      double part = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int i = lane + 32 * rr;
+        if (a_ok && i < K) part += log2(1.0 + (1.0 / dinv[rr] - 1.0));
+      }
+      const double c = warp_sum(part);
+      if (lane == 0) out[s * P.n_recv + r] = a_ok ? c : nan;
+      ++r;
+    }
+    if (P.receivers & XLMIMO_RECV_MRC) {
+      double part = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int i = lane + 32 * rr;
+        if (i < K) {
+          const double gii = G[i * K + i].x;
+          double intf = 0.0;
+          for (int j = 0; j < K; ++j)
+            if (j != i) {
+              const double2 g = G[i * K + j];
+              intf += g.x * g.x + g.y * g.y;
+            }
+          part += log2(1.0 + rho * gii * gii / (gii + rho * intf));
+        }
+      }
+      const double c = warp_sum(part);
+      if (lane == 0) out[s * P.n_recv + r] = mrc_ok ? c : nan;
+      ++r;
+    }
+  }
+  if (lane == 0 && P.flags) P.flags[prob] |= fl;
+}
+
+}  // namespace
+
+namespace xlh {
+
+int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr_db, int n_snr,
+                    uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s) {
+  if (n_prob == 0) return XLMIMO_OK;
+  RateParams P;
+  P.gram = gram;
+  P.rates = rates;
+  P.flags = flags;
+  P.K = K;
+  P.n_prob = n_prob;
+  P.n_snr = n_snr;
+  P.receivers = receivers;
+  P.n_recv = __builtin_popcount(receivers & 15u);
+  for (int i = 0; i < xl::kMaxSnr; ++i) P.rho[i] = i < n_snr ? pow(10.0, snr_db[i] / 10.0) : 0.0;
+  const size_t per_warp = 2 * (size_t)K * K * sizeof(double2);
+  int nw = (int)((96 * 1024) / per_warp);
+  if (nw > 8) nw = 8;
+  if (nw < 1) nw = 1;
+  const size_t smem = per_warp * nw;
+  const int64_t blocks = (n_prob + nw - 1) / nw;
+  KTimer tm(s, "sum_rate");
+  if (K <= 32) {
+    cudaFuncSetAttribute(rates_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rates_kernel<1><<<(unsigned)blocks, 32 * nw, smem, s>>>(P);
+  } else {
+    cudaFuncSetAttribute(rates_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rates_kernel<2><<<(unsigned)blocks, 32 * nw, smem, s>>>(P);
+  }
+  tm.stop(s);
+  count_launch();
+  return check_launch("rates_kernel");
+}
+
+}  // namespace xlh

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, on the same
+seeded inputs (oracle consumes the GPU-drawn positions for Gram/rate parity;
+the draws themselves are compared separately).
+
+Tolerances (north_star): Gram normalized error
+|dG_ij| / sqrt(G_ii G_jj) <= 1e-9 (fp64) / 1e-4 (fp32); per-drop rates <= 1e-6
+bits/s/Hz (fp64) / 1e-3 (fp32); flags and integer outputs exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from tests._util import normalized_err
+from workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def xl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests.conftest import build_product
+    build_product()
+    import paper_2503_18118_b200 as xl
+    return xl
+
+
+def _arr(xl, orc, kind, n_y, n_z, fc):
+    if kind == "ula":
+        return xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+    return xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+
+
+def _users(xl, orc, r, az, el=(0.0, 0.0)):
+    return xl.Users.polar(r, az, el), orc.users(r=r, az=az, el=el)
+
+
+# --------------------------------------------------------------------------- a1
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_drops_match_oracle(xl, orc, cfg):
+    w = CONFIGS[cfg]
+    ug, uo = _users(xl, orc, w.r, w.az, w.el)
+    n = min(w.n_drops, 2000)
+    pg = xl.gen_drops(ug, w.K, n, seed=w.seed).cpu().numpy()
+    po = orc.gen_drops(uo, w.K, n, seed=w.seed)
+    assert np.max(np.abs(pg - po)) <= 4e-15 * max(1.0, w.r[1])
+    # first_drop addressing
+    pg2 = xl.gen_drops(ug, w.K, 10, seed=w.seed, first_drop=n - 10).cpu().numpy()
+    assert np.array_equal(pg2, pg[n - 10:])
+
+
+def test_drops_empty(xl):
+    u = xl.Users.polar((5.0, 50.0), (-60, 60))
+    assert xl.gen_drops(u, 4, 0).shape == (0, 4, 3)
+
+
+# --------------------------------------------------------------------------- a2 + a3
+CASES = [
+    # kind, n_y, n_z, fc, K, drops, r, az, el
+    ("ula", 256, 1, 28e9, 4, 1000, (5.0, 50.0), (-60.0, 60.0), (0.0, 0.0)),     # cfg1 all drops
+    ("ula", 1000, 1, 28e9, 8, 7, (3.0, 30.0), (-60.0, 60.0), (0.0, 0.0)),       # ragged even N, K=8
+    ("ula", 999, 1, 100e9, 5, 5, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),       # odd N
+    ("ula", 1, 1, 28e9, 3, 3, (5.0, 50.0), (-60.0, 60.0), (0.0, 0.0)),          # N = 1
+    ("ula", 777, 1, 100e9, 1, 4, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),       # K = 1
+    ("ula", 4133, 1, 100e9, 9, 3, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),      # K = 9 (tiled, padded)
+    ("ula", 16384, 1, 100e9, 16, 6, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),    # cfg3 geometry
+    ("ula", 3001, 1, 140e9, 33, 2, (5.0, 100.0), (-60.0, 60.0), (0.0, 0.0)),    # K = 33 (KP = 48)
+    ("ula", 5000, 1, 140e9, 64, 2, (5.0, 100.0), (-60.0, 60.0), (0.0, 0.0)),    # K = 64
+    ("upa", 37, 23, 100e9, 6, 3, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),    # UPA ragged, small K
+    ("upa", 64, 64, 100e9, 32, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # UPA K = 32
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}_K{c[4]}_D{c[5]}")
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_gram_exact_parity(xl, orc, case, prec):
+    kind, n_y, n_z, fc, K, D, r, az, el = case
+    ag, ao = _arr(xl, orc, kind, n_y, n_z, fc)
+    ug, _ = _users(xl, orc, r, az, el)
+    pos = xl.gen_drops(ug, K, D, seed=17)
+    G = xl.gram_exact(ag, pos, precision=xl.FP64 if prec == "fp64" else xl.FP32).cpu().numpy()
+    Go = orc.gram_exact(ao, pos.cpu().numpy())
+    tol = 1e-9 if prec == "fp64" else 1e-4
+    assert normalized_err(G, Go) <= tol
+    assert np.array_equal(G, np.conj(np.swapaxes(G, 1, 2)))   # exactly Hermitian
+    assert np.all(np.imag(np.diagonal(G, axis1=1, axis2=2)) == 0)
+
+
+def test_gram_exact_empty_and_determinism(xl):
+    a = xl.Array.ula(4096, 100e9)
+    u = xl.Users.polar((2.0, 20.0), (-75, 75))
+    assert xl.gram_exact(a, xl.gen_drops(u, 16, 0)).shape == (0, 16, 16)
+    pos = xl.gen_drops(u, 16, 33, seed=3)
+    g1 = xl.gram_exact(a, pos)
+    g2 = xl.gram_exact(a, pos)
+    assert torch.equal(g1, g2)
+
+
+def test_gram_cfg5_full_size_sampled(xl, orc):
+    """cfg5 at full size (N = 2^20, K = 64) in the bench launch configuration; the oracle
+    recomputes sampled user pairs one by one (a K=2 Gram of the pair)."""
+    w = CONFIGS[5]
+    ag, ao = _arr(xl, orc, "ula", w.n_y, 1, w.fc_hz)
+    ug, _ = _users(xl, orc, w.r, w.az)
+    pos = xl.gen_drops(ug, w.K, 4, seed=w.seed)
+    G = xl.gram_exact(ag, pos).cpu().numpy()
+    P = pos.cpu().numpy()
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        d = int(rng.integers(4))
+        i, j = (int(v) for v in rng.choice(w.K, 2, replace=False))
+        sub = P[d:d + 1, [i, j]]
+        Go = orc.gram_exact(ao, sub)[0]
+        Gs = G[d][np.ix_([i, j], [i, j])]
+        assert normalized_err(Gs, Go) <= 1e-9
+    # properties at any size: PSD, |rho| <= 1, diag vs Eq. (4) (P1: <= 3e-11 for N >= 65536)
+    lam = 299792458.0 / w.fc_hz
+    for d in range(4):
+        ev = np.linalg.eigvalsh(G[d])
+        assert ev.min() > 0
+        for i in range(w.K):
+            x, y = P[d, i, 0], P[d, i, 1]
+            assert abs(G[d, i, i].real / orc.power_eq4(w.n_y, lam, 1.0, x, y) - 1) < 1e-9
+
+
+# --------------------------------------------------------------------------- a4
+@pytest.mark.parametrize("cfg", [1, 3, 5])
+def test_closed_form_parity(xl, orc, cfg):
+    w = CONFIGS[cfg]
+    ag, ao = _arr(xl, orc, "ula", w.n_y, 1, w.fc_hz)
+    ug, _ = _users(xl, orc, w.r, w.az)
+    D = min(w.n_drops, 1000)
+    pos = xl.gen_drops(ug, w.K, D, seed=w.seed)
+    G, fl = xl.gram_closed_form(ag, pos)
+    Go, flo = orc.gram_closed_form(ao, pos.cpu().numpy())
+    assert normalized_err(G.cpu().numpy(), Go) <= 1e-9
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+
+
+def test_closed_form_upa_unsupported(xl):
+    a = xl.Array.upa(8, 8, 100e9)
+    pos = xl.gen_drops(xl.Users.polar((2, 20), (-60, 60)), 4, 2)
+    with pytest.raises(xl.XlmimoError):
+        xl.gram_closed_form(a, pos)
+
+
+# --------------------------------------------------------------------------- a5
+@pytest.mark.parametrize("which", ["exact_cfg1", "closed_cfg1", "exact_K16", "exact_K64", "singular"])
+def test_sum_rate_parity(xl, orc, which):
+    allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    snr = [0.0, 10.0, 20.0]
+    if which.endswith("cfg1"):
+        w = CONFIGS[1]
+        a = xl.Array.ula(w.n_y, w.fc_hz)
+        pos = xl.gen_drops(xl.Users.polar(w.r, w.az), w.K, w.n_drops, seed=w.seed)
+        if which.startswith("exact"):
+            G = xl.gram_exact(a, pos)
+            fl0 = None
+        else:
+            G, fl0 = xl.gram_closed_form(a, pos)   # ~40 % of drops not PD (R10)
+    elif which == "singular":
+        a = xl.Array.ula(64, 28e9)
+        p = np.array([[[3.0, 1.0, 0.0], [3.0, 1.0, 0.0], [5.0, -2.0, 0.0]]] * 3)
+        pos = torch.tensor(p, device="cuda")
+        G = xl.gram_exact(a, pos)
+        fl0 = None
+    else:
+        K = 16 if which == "exact_K16" else 64
+        a = xl.Array.ula(2048, 100e9)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-75, 75)), K, 20, seed=5)
+        G = xl.gram_exact(a, pos)
+        fl0 = None
+    Gh = G.cpu().numpy()
+    rates, fl = xl.sum_rate(G, snr, allr, flags=fl0.clone() if fl0 is not None else None)
+    ro, flo = orc.sum_rate(Gh, snr, allr, flags_in=fl0.cpu().numpy() if fl0 is not None else None)
+    rg = rates.cpu().numpy()
+    assert np.array_equal(np.isnan(rg), np.isnan(ro))
+    ok = ~np.isnan(ro)
+    assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    if which == "closed_cfg1":
+        assert np.any(flo & 1) and np.any(flo & 8)   # the flags really fire here
+
+
+# --------------------------------------------------------------------------- a1..a6 sweep
+def test_sweep_parity_reduced_cfg2(xl, orc):
+    """cfg2 grid, SNRs and receivers on the first 48 drops: ergodic means, counts, M_sat and
+    per-drop rates vs the oracle, which computes every N independently (no shells)."""
+    w = CONFIGS[2]
+    D = 48
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ao = orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, D, w.snr_db, w.receivers, users=ug, seed=w.seed, per_drop=True)
+    pos = xl.gen_drops(ug, w.K, D, seed=w.seed).cpu().numpy()
+    erg, nv, sat, pd = orc.saturation_sweep(ao, w.n_list, pos, w.snr_db, w.receivers, per_drop=True)
+    assert np.max(np.abs(res["per_drop"].cpu().numpy() - pd)) <= 1e-6
+    assert np.max(np.abs(res["ergodic"] - erg)) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
+    assert res["sat"][2] == sat[2]
+    assert np.allclose(res["sat"][[0, 1, 3]], sat[[0, 1, 3]], rtol=1e-12, atol=1e-12)
+
+
+def test_sweep_closed_form_parity(xl, orc):
+    w = CONFIGS[2]
+    D = 200
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ao = orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, D, w.snr_db, 15, users=ug, seed=1, gram_kind=xl.GRAM_CLOSED_FORM,
+                              per_drop=True)
+    pos = xl.gen_drops(ug, w.K, D, seed=1).cpu().numpy()
+    erg, nv, sat, pd = orc.saturation_sweep(ao, w.n_list, pos, w.snr_db, 15, gram_kind=1, per_drop=True)
+    g = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(pd))
+    ok = ~np.isnan(pd)
+    assert np.max(np.abs(g[ok] - pd[ok])) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
+    assert np.allclose(res["ergodic"], erg, atol=1e-6, equal_nan=True)
+
+
+def test_sweep_full_cfg2_properties_and_sampled_drops(xl, orc):
+    """Full cfg2 (10^4 drops, N = 2^8..2^16) in the bench configuration: capacity per drop
+    non-decreasing in N, saturated at the analytic point (P8), M_sat identical to the oracle's
+    per-drop Eqs. (13)-(16) on the same drops and within 1 % of the Appendix B quadrature (R15);
+    sampled drops recomputed by the oracle."""
+    w = CONFIGS[2]
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, w.n_drops, w.snr_db, w.receivers, users=ug, seed=w.seed,
+                              per_drop=True)
+    pd = res["per_drop"].cpu().numpy()          # [D, nN, S, R], R = CAP, ZF, MMSE
+    cap = pd[..., 0]
+    assert np.all(np.diff(cap, axis=1) >= -1e-9)
+    norm = res["ergodic"][:, :, 0] / res["ergodic"][-1:, :, 0]
+    Ms = res["sat"][2]
+    for n, N in enumerate(w.n_list):
+        if N >= Ms:
+            assert np.all(norm[n] >= 0.99)
+        if N <= Ms / 5:
+            assert np.all(norm[n] <= 0.95)
+    lam = 299792458.0 / w.fc_hz
+    _, _, Mq = orc.ergodic_saturation_polar(w.r[0], w.r[1], w.az[0], w.az[1], w.t, w.K, lam / 2)
+    assert abs(Ms - Mq) / Mq < 0.01
+    pos = xl.gen_drops(ug, w.K, w.n_drops, seed=w.seed).cpu().numpy()
+    up, dn = orc.saturation_coords(pos, w.t)
+    assert Ms == math.ceil((up.mean() - dn.mean()) / (lam / 2))
+    idx = np.array([0, 1234, 5678, 9999])
+    ao = orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz)
+    _, _, _, pdo = orc.saturation_sweep(ao, w.n_list, pos[idx], w.snr_db, w.receivers, per_drop=True)
+    assert np.max(np.abs(pd[idx] - pdo)) <= 1e-6
+    # host-buffer entry == device entry on the same drops (bitwise)
+    ph = torch.tensor(pos).pin_memory()
+    rh = xl.saturation_sweep_host(ag, w.n_list, ph, w.snr_db, w.receivers)
+    assert np.array_equal(rh["ergodic"], res["ergodic"]) and np.array_equal(rh["sat"], res["sat"])
+
+
+def test_launch_counter_moves(xl):
+    n0 = xl.launch_count()
+    xl.gen_drops(xl.Users.polar((5, 50), (-60, 60)), 4, 8)
+    assert xl.launch_count() > n0
