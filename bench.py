@@ -39,7 +39,9 @@ if ROOT not in sys.path:
 from workloads import CONFIGS, cmac_per_drop  # noqa: E402
 
 W = CONFIGS[2]
-FP64_OPS_PER_COEF = 40  # algorithmic FP64-pipe work model per channel coefficient (roofline)
+# Fixed FP64-pipe work model per channel coefficient ("Roofline"): distance^2 2,
+# 1/r 5, r 1, quarter-cycle range reduction 4, sin+cos minimax 13, r^{-3/2} 7, phasor 2.
+FP64_OPS_PER_COEF = 34
 
 
 def parse():
@@ -284,7 +286,8 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (fused fp64 Gram, FP64 pipe bound)
     cmac_step = cmac_per_drop(W) * D            # per rank
     N = max(W.n_list)
-    kname = "gram_fused_small_fp64"
+    gram_k = [k for k in ktimes if k.startswith("gram_fused")]
+    kname = max(gram_k, key=lambda k: ktimes[k][1]) if gram_k else "gram_fused"
     kcount, kms = ktimes.get(kname, (0, 0.0))
     roof = None
     if kcount:

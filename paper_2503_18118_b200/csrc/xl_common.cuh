@@ -108,29 +108,85 @@ __device__ __forceinline__ UserC make_user(const double *p, int kind, double sqr
   return u;
 }
 
-// h = amp * r^{-3/2} * e^{-j 2 pi frac(r/lambda)}  (Eq. 3), fp64.
-// r2 = distance^2.  r is refined to ~0.5 ulp with one residual step so the
-// phase fraction keeps ~1e-11 rad at r/lambda ~ 1e5 (north_star: fp64 range reduction).
+// 1/sqrt(x) for positive normal x: MUFU.RSQ64H (no special-case branches with
+// .ftz; it reads only the high word of x, so its error reaches ~1e-6 relative)
+// + one third-order Householder step y (1 + e/2 + 3e^2/8), e = 1 - x y^2:
+// error O(e^3) -> ~1 ulp.  (A plain Newton step leaves 1.5 e^2 ~ 4e-13, which
+// moves the phase 2 pi r/lambda by ~1e-8 rad at r/lambda ~ 5e3: measured parity
+// failure, so the cubic term is required.)  5 FP64 instructions.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  return fma(y * e, p, y);
+}
+
+// Near-minimax polynomials (Chebyshev-node least squares, fitted in 50-digit
+// arithmetic) in u = g^2 for g in [-1/2, 1/2]:
+//   sin(pi/2 g) = g * S(u)  (degree 5, |err| <= 3.4e-15),
+//   cos(pi/2 g) = C(u)      (degree 6, |err| <= 1.1e-16).
+__constant__ double kSinPoly[6] = {1.5707963267948898981, -0.64596409750431005807, 0.079692626155777645619,
+                                   -0.0046817525918122076931, 0.0001604292666631208935,
+                                   -3.5563888496214387972e-6};
+__constant__ double kCosPoly[7] = {0.99999999999999995287, -1.2337005501361513498, 0.25366950789986513871,
+                                   -0.020863480734953519901, 0.0009192599500952791151,
+                                   -0.000025200135454917479526, 4.6552987291490935821e-7};
+
+// h = amp * r^{-3/2} * e^{-j 2 pi r/lambda}  (Eq. 3), fp64, the fused generator's
+// coefficient.  Phase: q4 = 4 r/lambda (quarter cycles), k = rint(q4) by the
+// 1.5*2^52 magic add (k's low bits = quadrant), g = q4 - k in [-1/2, 1/2] exactly,
+// angle = (pi/2)(k + g): the fp64 range reduction of the north_star.  ~32 FP64
+// pipe instructions per coefficient, no branches.  c4 = 4 / lambda.
+__device__ __forceinline__ void coef_fast(double r2, double amp, double c4, double &re, double &im) {
+  const double ir = rsqrt_nr(r2);
+  const double r = r2 * ir;
+  const double q4 = r * c4;
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double kd = q4 + magic;
+  const int qd = __double2loint(kd);
+  const double g = q4 - (kd - magic);
+  const double u = g * g;
+  double ps = kSinPoly[5];
+  ps = fma(ps, u, kSinPoly[4]);
+  ps = fma(ps, u, kSinPoly[3]);
+  ps = fma(ps, u, kSinPoly[2]);
+  ps = fma(ps, u, kSinPoly[1]);
+  ps = fma(ps, u, kSinPoly[0]);
+  const double sn = ps * g;
+  double pc = kCosPoly[6];
+  pc = fma(pc, u, kCosPoly[5]);
+  pc = fma(pc, u, kCosPoly[4]);
+  pc = fma(pc, u, kCosPoly[3]);
+  pc = fma(pc, u, kCosPoly[2]);
+  pc = fma(pc, u, kCosPoly[1]);
+  const double cs = fma(pc, u, kCosPoly[0]);
+  const double a = amp * ir * rsqrt_nr(r);  // r^{-3/2}
+  // quadrant q: (cos, sin) of (pi/2)(q + g) = q0 (cs, sn), q1 (-sn, cs), q2 (-cs, -sn), q3 (sn, -cs);
+  // h = a (cos - j sin)  =>  re = a*c, im = a*(-s)
+  const int q = qd & 3;
+  const bool sw = q & 1;
+  double c = sw ? sn : cs;
+  double s = sw ? cs : sn;
+  const int negc = ((q + 1) >> 1) & 1;  // q = 1, 2
+  const int negs = (q >> 1) ^ 1;        // -s: flip unless q = 2, 3
+  c = __hiloint2double(__double2hiint(c) ^ (negc << 31), __double2loint(c));
+  s = __hiloint2double(__double2hiint(s) ^ (negs << 31), __double2loint(s));
+  re = a * c;
+  im = a * s;
+}
+
+// Previous generator (kept for the general-K kernels until they move to coef_fast).
 __device__ __forceinline__ void coef_from_r2(double r2, double amp, double inv_lambda, double &re,
                                              double &im) {
-  const double ir = rsqrt(r2);
-  double r = r2 * ir;
-  r = fma(0.5 * ir, fma(-r, r, r2), r);  // Newton/residual correction of sqrt(r2)
-  const double q = r * inv_lambda;
-  const double f = q - rint(q);
-  double s, c;
-  sincos2pi_reduced(f, s, c);
-  const double a = amp * ir * rsqrt(r);  // r^{-3/2}
-  re = a * c;
-  im = -a * s;
+  coef_fast(r2, amp, 4.0 * inv_lambda, re, im);
 }
 
 // fp32 phasor and amplitude from fp64 distance / phase reduction (XLMIMO_FP32, K3).
 __device__ __forceinline__ void coef_from_r2_f32(double r2, double amp, double inv_lambda, float &re,
                                                  float &im) {
-  const double ir = rsqrt(r2);
-  double r = r2 * ir;
-  r = fma(0.5 * ir, fma(-r, r, r2), r);
+  const double ir = rsqrt_nr(r2);
+  const double r = r2 * ir;
   const double q = r * inv_lambda;
   const float f = (float)(q - rint(q));
   float s, c;

@@ -16,6 +16,7 @@
 //  then each thread accumulates one 4x4 register block of the upper triangle
 //  over a subset of the tile's elements (kernel B).
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "xl_common.cuh"
@@ -142,6 +143,142 @@ __global__ void __launch_bounds__(NT, 1) gram_small_kernel(GramParams P) {
       out[v] = s;
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ kernel A2
+// K = 2*KH (KH in {2, 4}), ULA.  Two threads (lanes 2s, 2s+1) share each element:
+// thread h generates users [h*KH, (h+1)*KH) (no duplicated generation), the two
+// exchange their coefficients with one shuffle per value, and each accumulates
+// its own-half triangle plus half of the cross block, so the K(K+1)/2 complex
+// accumulators are split evenly and the register budget allows 2 blocks/SM.
+// Cross block split: thread h sees theirs'[b] = partner.mine[(b + h) % KH] and
+// takes the pairs (a, (a + d) % KH) for even d -- thread 0 covers the even
+// diagonals of the cross block, thread 1 (whose view is rotated by one) the odd
+// ones; split_map() inverts this for the output.
+template <int KH>
+__device__ __forceinline__ void split_map(int i, int j, int &parity, int &slot, bool &conj) {
+  constexpr int NOWN = KH * (KH + 1) / 2, ND = KH / 2;
+  if (j < KH) {
+    parity = 0; slot = i * KH - i * (i - 1) / 2 + (j - i); conj = false;
+  } else if (i >= KH) {
+    const int a = i - KH, b = j - KH;
+    parity = 1; slot = a * KH - a * (a - 1) / 2 + (b - a); conj = false;
+  } else {
+    const int a0 = i, b0 = j - KH;
+    const int d = ((b0 - a0) % KH + KH) % KH;
+    if ((d & 1) == 0) {
+      parity = 0; slot = NOWN + a0 * ND + d / 2; conj = false;
+    } else {
+      const int d1 = ((a0 - b0 - 1) % KH + KH) % KH;
+      parity = 1; slot = NOWN + b0 * ND + d1 / 2; conj = true;
+    }
+  }
+}
+
+template <int KH, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
+  constexpr int K = 2 * KH;
+  constexpr int NOWN = KH * (KH + 1) / 2;
+  constexpr int ND = KH / 2;
+  constexpr int NS = NOWN + KH * ND;  // complex accumulators per thread
+  constexpr int NV = 2 * NS;
+  constexpr int NW = NT / 32;
+  constexpr int NSLOT = NT / 2;
+  __shared__ double4 su[K];  // (xz2, y, amp, -)
+  __shared__ double red[NW][2][NV];
+
+  const int64_t drop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = tid & 1, eslot = tid >> 1;
+  if (tid < K) {
+    const xl::UserC u = xl::make_user(P.pos + (drop * K + tid) * 3, XLMIMO_ULA, P.sqrt_beta0);
+    su[tid] = make_double4(u.xz2, u.y, u.amp, 0.0);
+  }
+  __syncthreads();
+  const double c4 = 4.0 * P.inv_lambda;
+  const bool n_odd = (P.N & 1) != 0;
+
+  const int64_t s0 = (int64_t)split * P.chunk;
+  const int64_t s1 = min(P.N, s0 + P.chunk);
+  int64_t lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int64_t lv1 = P.lvl_end[l];
+    const int64_t a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+    for (int64_t t0 = a; t0 < b; t0 += NSLOT) {  // warp-uniform trip count (shuffles below)
+      const int64_t t = t0 + eslot;
+      const bool valid = t < b;
+      const double ey = xl::ula_y_centred(valid ? t : a, n_odd, P.pitch);
+      double mr[KH], mi[KH];
+#pragma unroll
+      for (int q = 0; q < KH; ++q) {
+        const double4 u = su[h * KH + q];
+        const double dy = ey - u.y;
+        xl::coef_fast(fma(dy, dy, u.x), valid ? u.z : 0.0, c4, mr[q], mi[q]);
+      }
+      double tr[KH], ti[KH];
+#pragma unroll
+      for (int q = 0; q < KH; ++q) {
+        const double sr = h ? mr[q] : mr[(q + 1) % KH];
+        const double si = h ? mi[q] : mi[(q + 1) % KH];
+        tr[q] = __shfl_xor_sync(0xffffffffu, sr, 1);
+        ti[q] = __shfl_xor_sync(0xffffffffu, si, 1);
+      }
+      int v = 0;
+#pragma unroll
+      for (int p = 0; p < KH; ++p) {
+#pragma unroll
+        for (int q = p; q < KH; ++q) {
+          if (p == q) {
+            acc[v] = fma(mr[p], mr[p], fma(mi[p], mi[p], acc[v]));
+          } else {
+            acc[v] = fma(mr[p], mr[q], fma(mi[p], mi[q], acc[v]));
+            acc[v + 1] = fma(mr[p], mi[q], fma(-mi[p], mr[q], acc[v + 1]));
+          }
+          v += 2;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < KH; ++p) {
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          const int q = (p + 2 * dd) % KH;
+          acc[v] = fma(mr[p], tr[q], fma(mi[p], ti[q], acc[v]));
+          acc[v + 1] = fma(mr[p], ti[q], fma(-mi[p], tr[q], acc[v + 1]));
+          v += 2;
+        }
+      }
+    }
+    // reduce lanes of equal parity inside the warp; each warp writes its own
+    // partial (standard upper-triangle layout) -- no block barrier in the level
+    // loop, gram_reduce_kernel sums the NW partials in fixed order.
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double x = acc[v];
+#pragma unroll
+      for (int o = 2; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane < 2) red[warp][lane][v] = x;
+    }
+    __syncwarp();
+    constexpr int NP = K * (K + 1) / 2;
+    double *out = P.ws + ((((size_t)drop * P.n_split + split) * P.n_lvl + l) * NW + warp) * (2 * NP);
+    for (int p = lane; p < NP; p += 32) {
+      int i = 0, rem = p;
+      while (rem >= K - i) { rem -= K - i; ++i; }
+      const int j = i + rem;
+      int par, slot;
+      bool cj;
+      split_map<KH>(i, j, par, slot, cj);
+      const double re = red[warp][par][2 * slot], im = red[warp][par][2 * slot + 1];
+      out[2 * p] = re;
+      out[2 * p + 1] = (i == j) ? 0.0 : (cj ? -im : im);
+    }
+    __syncwarp();
   }
 }
 
@@ -291,8 +428,10 @@ __global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramPar
 }
 
 // ------------------------------------------------------------------ reduce
+// ws layout [drop][split][lvl][part][NP][2]; sums (split, part) in fixed order per
+// level and accumulates across levels (nested-N prefix sums).
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const double *ws, int K, int64_t n_drops, int n_split,
-                                                          int n_lvl, double *out) {
+                                                          int n_lvl, int n_part, double *out) {
   const int NP = K * (K + 1) / 2;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_drops * NP) return;
@@ -304,9 +443,11 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double *ws, int 
   double re = 0.0, im = 0.0;
   for (int l = 0; l < n_lvl; ++l) {
     for (int s = 0; s < n_split; ++s) {
-      const double *w = ws + (((size_t)drop * n_split + s) * n_lvl + l) * (size_t)(2 * NP) + 2 * p;
-      re += w[0];
-      im += w[1];
+      const double *w = ws + ((((size_t)drop * n_split + s) * n_lvl + l) * n_part) * (size_t)(2 * NP) + 2 * p;
+      for (int q = 0; q < n_part; ++q) {
+        re += w[(size_t)q * 2 * NP];
+        im += w[(size_t)q * 2 * NP + 1];
+      }
     }
     double *g = out + ((size_t)drop * n_lvl + l) * (size_t)K * K * 2;
     g[(i * K + j) * 2] = re;
@@ -361,13 +502,30 @@ void launch_tiled_k(int K, const GramParams &P, int64_t n_blocks, cudaStream_t s
 
 namespace xlh {
 
+// Which kernel runs, and how many partials per (drop, split, level) it writes.
+struct KernelChoice {
+  bool split;     // kernel A2 (K in {4, 8}, ULA, fp64): one partial per warp
+  int nt;         // threads per block of the split kernel
+  int parts;
+};
+
+KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
+  KernelChoice c;
+  c.split = precision == XLMIMO_FP64 && a.kind == XLMIMO_ULA && (K == 8 || K == 4);
+  static const int cfg = getenv("XLMIMO_SPLIT_CFG") ? atoi(getenv("XLMIMO_SPLIT_CFG")) : 0;
+  c.nt = 256;
+  if (c.split && K == 8) c.nt = (cfg == 1 || cfg == 3) ? 128 : (cfg == 2) ? 192 : (cfg == 4) ? 64 : 256;
+  c.parts = c.split ? c.nt / 32 : 1;
+  return c;
+}
+
 size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
-  (void)precision;
   (void)mode;
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
-  return (size_t)n_drops * n_split * n_lvl * np * 2 * sizeof(double);
+  const KernelChoice kc = choose_kernel(a, K, precision);
+  return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
 }
 
 int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
@@ -398,9 +556,22 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   P.sqrt_beta0 = a.sqrt_beta0;
   const int64_t n_blocks = n_drops * P.n_split;
   const bool fp32 = precision == XLMIMO_FP32;
-  KTimer tm(s, K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
-                      : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
-  if (K <= 8) {
+  const KernelChoice kc = choose_kernel(a, K, precision);
+  KTimer tm(s, kc.split ? "gram_fused_split_fp64"
+                        : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
+                                 : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
+  if (kc.split) {
+    if (K == 8) {
+      switch (kc.nt) {
+        case 64: gram_split_kernel<4, 64, 8><<<(unsigned)n_blocks, 64, 0, s>>>(P); break;
+        case 128: gram_split_kernel<4, 128, 4><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;
+        case 192: gram_split_kernel<4, 192, 2><<<(unsigned)n_blocks, 192, 0, s>>>(P); break;
+        default: gram_split_kernel<4, 256, 2><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+      }
+    } else {
+      gram_split_kernel<2, 256, 2><<<(unsigned)n_blocks, 256, 0, s>>>(P);
+    }
+  } else if (K <= 8) {
     if (fp32) launch_small_k<true>(K, P, n_blocks, s);
     else launch_small_k<false>(K, P, n_blocks, s);
   } else {
@@ -414,7 +585,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   const int64_t n_items = n_drops * (int64_t)K * (K + 1) / 2;
   KTimer tr(s, "gram_reduce");
   gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops, P.n_split,
-                                                                      n_lvl, out);
+                                                                      n_lvl, kc.parts, out);
   tr.stop(s);
   count_launch();
   return check_launch("gram_reduce_kernel");
