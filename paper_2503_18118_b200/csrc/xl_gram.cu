@@ -17,6 +17,7 @@
 //  over a subset of the tile's elements (kernel B).
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "xl_common.cuh"
@@ -282,6 +283,131 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
   }
 }
 
+// ------------------------------------------------------------------ kernel M
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) Gram, warp-independent, K <= 8G.
+// A warp covers 4 elements x 8 users per step: lane l computes the coefficient of
+// user l/4 (+ 8g for group g) at element l%4 -- exactly the m8n8k4 A-fragment
+// (row = user, k = element) and, for the same register, the B-fragment
+// (k = element, col = user).  Per step and group pair (g1 <= g2):
+//   RR += re_g1^T re_g2,  II += im_g1^T im_g2,  RI += re_g1^T im_g2  (+ IR for g1 < g2),
+// so that Re G = RR + II and Im G(i,j) = RI(i,j) - RI(j,i) (diagonal group) or
+// RI(i,j) - IR(i,j) (cross).  DMMA shares the FP64 pipe with DFMA on B200
+// (tools/pipes.cu) and computes the redundant lower halves, but leaves each
+// lane with one short coefficient chain and a handful of accumulator registers,
+// so occupancy (latency hiding) is high and no shuffles are needed.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int G>
+struct MmaCfg {
+  static constexpr int NDIAG = G;                 // RR, II, RI
+  static constexpr int NCROSS = G * (G - 1) / 2;  // RR, II, RI, IR
+  static constexpr int NMMA = 3 * NDIAG + 4 * NCROSS;
+};
+
+template <int G, int NT, int MINB, int KIND>
+__global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
+  using Cfg = MmaCfg<G>;
+  constexpr int NW = NT / 32;
+  constexpr int NMMA = Cfg::NMMA;
+  __shared__ double4 su[8 * G];            // (xz2, y, z, amp) per user
+  __shared__ double cs[NW][NMMA][8][8];    // per-warp fragment staging at level ends
+
+  const int64_t drop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = P.K;
+  for (int u = tid; u < 8 * G; u += NT) {
+    if (u < K) {
+      const xl::UserC uc = xl::make_user(P.pos + (drop * K + u) * 3, KIND, P.sqrt_beta0);
+      su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+    } else {
+      su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: zero amplitude
+    }
+  }
+  __syncthreads();
+  const double c4 = 4.0 * P.inv_lambda;
+  const bool n_odd = (P.N & 1) != 0;
+  const int ue = lane & 3, uu = lane >> 2;
+
+  const int64_t s0 = (int64_t)split * P.chunk;
+  const int64_t s1 = min(P.N, s0 + P.chunk);
+  int64_t lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int64_t lv1 = P.lvl_end[l];
+    const int64_t a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[NMMA][2];
+#pragma unroll
+    for (int m = 0; m < NMMA; ++m) acc[m][0] = acc[m][1] = 0.0;
+    for (int64_t t0 = a + 4 * warp; t0 < b; t0 += 4 * NW) {  // warp-uniform trip count
+      const int64_t t = t0 + ue;
+      const bool valid = t < b;
+      ElemPos ep = element_pos(P, valid ? t : a);
+      double hr[G], hi[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double4 u = su[uu + 8 * g];
+        const double dy = ep.y - u.y;
+        double r2 = fma(dy, dy, u.x);
+        if (KIND != XLMIMO_ULA) {
+          const double dz = ep.z - u.z;
+          r2 = fma(dz, dz, r2);
+        }
+        xl::coef_fast(r2, valid ? u.w : 0.0, c4, hr[g], hi[g]);
+      }
+      int m = 0;
+#pragma unroll
+      for (int g1 = 0; g1 < G; ++g1) {
+        dmma(acc[m++], hr[g1], hr[g1]);
+        dmma(acc[m++], hi[g1], hi[g1]);
+        dmma(acc[m++], hr[g1], hi[g1]);
+#pragma unroll
+        for (int g2 = g1 + 1; g2 < G; ++g2) {
+          dmma(acc[m++], hr[g1], hr[g2]);
+          dmma(acc[m++], hi[g1], hi[g2]);
+          dmma(acc[m++], hr[g1], hi[g2]);
+          dmma(acc[m++], hi[g1], hr[g2]);
+        }
+      }
+    }
+    // stage the fragments (row = lane/4, cols 2(lane%4) + {0,1}) and assemble this
+    // warp's partial upper triangle in the standard layout -- no block barrier.
+#pragma unroll
+    for (int mm = 0; mm < NMMA; ++mm) {
+      cs[warp][mm][uu][2 * ue] = acc[mm][0];
+      cs[warp][mm][uu][2 * ue + 1] = acc[mm][1];
+    }
+    __syncwarp();
+    const int NP = K * (K + 1) / 2;
+    double *out = P.ws + ((((size_t)drop * P.n_split + split) * P.n_lvl + l) * NW + warp) * (size_t)(2 * NP);
+    for (int p = lane; p < NP; p += 32) {
+      int i = 0, rem = p;
+      while (rem >= K - i) { rem -= K - i; ++i; }
+      const int j = i + rem;
+      const int g1 = i >> 3, g2 = j >> 3, ii = i & 7, jj = j & 7;
+      // job index of the (g1, g2) block: diagonal blocks take 3 slots, cross blocks 4
+      int base = 0;
+      for (int g = 0; g < g1; ++g) base += 3 + 4 * (G - 1 - g);
+      double re, im;
+      if (g1 == g2) {
+        re = cs[warp][base][ii][jj] + cs[warp][base + 1][ii][jj];
+        im = cs[warp][base + 2][ii][jj] - cs[warp][base + 2][jj][ii];
+      } else {
+        const int c = base + 3 + 4 * (g2 - g1 - 1);
+        re = cs[warp][c][ii][jj] + cs[warp][c + 1][ii][jj];
+        im = cs[warp][c + 2][ii][jj] - cs[warp][c + 3][ii][jj];
+      }
+      out[2 * p] = re;
+      out[2 * p + 1] = (i == j) ? 0.0 : im;
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ kernel B
 template <int KP>
 struct TiledCfg {
@@ -503,20 +629,57 @@ void launch_tiled_k(int K, const GramParams &P, int64_t n_blocks, cudaStream_t s
 namespace xlh {
 
 // Which kernel runs, and how many partials per (drop, split, level) it writes.
+// Block shapes of the DMMA kernel (XLMIMO_GRAM_VARIANT selects for tuning):
+//   G = 1: 0 -> 256 thr x 4 blocks/SM (<= 64 regs), 1 -> 256 x 6 (<= 40), 2 -> 128 x 8, 3 -> 256 x 2
+//   G = 2: 0 -> 256 x 2, 1 -> 256 x 3, 2 -> 128 x 4, 3 -> 256 x 2
+int mma_variant() {
+  static const int v = getenv("XLMIMO_GRAM_VARIANT") ? atoi(getenv("XLMIMO_GRAM_VARIANT")) : 0;
+  return v;
+}
+int mma_nt(int G) { return (mma_variant() == 2) ? 128 : 256; }
+
 struct KernelChoice {
-  bool split;     // kernel A2 (K in {4, 8}, ULA, fp64): one partial per warp
-  int nt;         // threads per block of the split kernel
-  int parts;
+  int which;      // 0 = small/tiled (kernel A / B), 1 = split (A2), 2 = DMMA (M)
+  int nt;         // threads per block
+  int parts;      // partials per (drop, split, level)
 };
 
+// XLMIMO_GRAM_KERNEL=split|mma|legacy overrides the default (tuning / A-B tests);
+// XLMIMO_GRAM_NT overrides the block size of the split / DMMA kernels.
 KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
+  static const char *env_k = getenv("XLMIMO_GRAM_KERNEL");
+  static const int env_nt = getenv("XLMIMO_GRAM_NT") ? atoi(getenv("XLMIMO_GRAM_NT")) : 0;
   KernelChoice c;
-  c.split = precision == XLMIMO_FP64 && a.kind == XLMIMO_ULA && (K == 8 || K == 4);
-  static const int cfg = getenv("XLMIMO_SPLIT_CFG") ? atoi(getenv("XLMIMO_SPLIT_CFG")) : 0;
+  const bool fp64 = precision == XLMIMO_FP64;
+  const bool split_ok = fp64 && a.kind == XLMIMO_ULA && (K == 8 || K == 4);
+  const bool mma_ok = fp64 && K <= 16;
+  c.which = mma_ok ? 2 : 0;
+  if (env_k && !strcmp(env_k, "split") && split_ok) c.which = 1;
+  if (env_k && !strcmp(env_k, "legacy")) c.which = 0;
   c.nt = 256;
-  if (c.split && K == 8) c.nt = (cfg == 1 || cfg == 3) ? 128 : (cfg == 2) ? 192 : (cfg == 4) ? 64 : 256;
-  c.parts = c.split ? c.nt / 32 : 1;
+  if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = env_nt;
+  if (c.which == 2) c.nt = mma_nt(K <= 8 ? 1 : 2);
+  c.parts = c.which >= 1 ? c.nt / 32 : 1;
   return c;
+}
+
+template <int G, int KIND>
+void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  const int v = mma_variant();
+  if (G == 1) {
+    switch (v) {
+      case 1: gram_mma_kernel<G, 256, 6, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+      case 2: gram_mma_kernel<G, 128, 8, KIND><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;
+      case 3: gram_mma_kernel<G, 256, 2, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+      default: gram_mma_kernel<G, 256, 4, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+    }
+  } else {
+    switch (v) {
+      case 1: gram_mma_kernel<G, 256, 3, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+      case 2: gram_mma_kernel<G, 128, 4, KIND><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;
+      default: gram_mma_kernel<G, 256, 2, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
+    }
+  }
 }
 
 size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
@@ -557,10 +720,20 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   const int64_t n_blocks = n_drops * P.n_split;
   const bool fp32 = precision == XLMIMO_FP32;
   const KernelChoice kc = choose_kernel(a, K, precision);
-  KTimer tm(s, kc.split ? "gram_fused_split_fp64"
-                        : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
-                                 : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
-  if (kc.split) {
+  KTimer tm(s, kc.which == 1 ? "gram_fused_split_fp64"
+               : kc.which == 2 ? "gram_fused_dmma_fp64"
+               : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
+                        : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
+  if (kc.which == 2) {
+    const bool ula = a.kind == XLMIMO_ULA;
+    if (K <= 8) {
+      if (ula) launch_mma<1, XLMIMO_ULA>(P, n_blocks, s);
+      else launch_mma<1, XLMIMO_UPA>(P, n_blocks, s);
+    } else {
+      if (ula) launch_mma<2, XLMIMO_ULA>(P, n_blocks, s);
+      else launch_mma<2, XLMIMO_UPA>(P, n_blocks, s);
+    }
+  } else if (kc.which == 1) {
     if (K == 8) {
       switch (kc.nt) {
         case 64: gram_split_kernel<4, 64, 8><<<(unsigned)n_blocks, 64, 0, s>>>(P); break;
