@@ -221,6 +221,161 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
   if (lane == 0 && P.flags) P.flags[prob] |= fl;
 }
 
+// ---------------------------------------------------------------------------
+// Small K (<= 8): one thread per Gram, the factor in registers (fully unrolled),
+// G re-read from global/L1 whenever I + rho G is formed.  Same definitions and
+// failure rule as the warp kernel.
+template <int K>
+__device__ __forceinline__ void load_a(const double2 *G, double rho, double diag, double (&ar)[K][K],
+                                       double (&ai)[K][K]) {
+  // lower triangle of diag*I + rho*G: A(i,j) = rho conj(G(j,i)) for i > j
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int i = j; i < K; ++i) {
+      const double2 g = __ldg(G + j * K + i);
+      ar[i][j] = (i == j ? diag : 0.0) + rho * g.x;
+      ai[i][j] = -rho * g.y;
+    }
+}
+
+// in-place lower Cholesky; linv = 1/L_jj
+template <int K>
+__device__ __forceinline__ bool chol_reg(double (&ar)[K][K], double (&ai)[K][K], double (&linv)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = ar[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= ar[j][k] * ar[j][k] + ai[j][k] * ai[j][k];
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double ljj = sqrt(d), inv = 1.0 / ljj;
+    ar[j][j] = ljj;
+    ai[j][j] = 0.0;
+    linv[j] = inv;
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double sr = ar[i][j], si = ai[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) {  // - L_ik conj(L_jk)
+        sr -= ar[i][k] * ar[j][k] + ai[i][k] * ai[j][k];
+        si -= ai[i][k] * ar[j][k] - ar[i][k] * ai[j][k];
+      }
+      ar[i][j] = sr * inv;
+      ai[i][j] = si * inv;
+    }
+  }
+  return true;
+}
+
+template <int K>
+__device__ __forceinline__ void inv_diag_reg(const double (&lr)[K][K], const double (&li)[K][K],
+                                             const double (&linv)[K], double (&dinv)[K]) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    double xr[K], xi[K];
+    xr[c] = linv[c];
+    xi[c] = 0.0;
+    double s = xr[c] * xr[c];
+#pragma unroll
+    for (int k = c + 1; k < K; ++k) {
+      double tr = 0.0, ti = 0.0;
+#pragma unroll
+      for (int j = c; j < k; ++j) {
+        tr += lr[k][j] * xr[j] - li[k][j] * xi[j];
+        ti += lr[k][j] * xi[j] + li[k][j] * xr[j];
+      }
+      xr[k] = -tr * linv[k];
+      xi[k] = -ti * linv[k];
+      s += xr[k] * xr[k] + xi[k] * xi[k];
+    }
+    dinv[c] = s;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) rates_thread_kernel(RateParams P) {
+  const int64_t prob = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (prob >= P.n_prob) return;
+  const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)prob * K * K;
+  double *out = P.rates + (size_t)prob * P.n_snr * P.n_recv;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  bool fin = true, mrc_ok = true;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int i = j; i < K; ++i) {
+      const double2 g = __ldg(G + j * K + i);
+      fin &= isfinite(g.x) && isfinite(g.y);
+      if (i == j) mrc_ok &= g.x > 0.0;
+    }
+  uint32_t fl = 0;
+  if (!fin) {
+    for (int e = 0; e < P.n_snr * P.n_recv; ++e) out[e] = nan;
+    if (P.flags) P.flags[prob] |= XLMIMO_FLAG_NONFINITE;
+    return;
+  }
+  double ar[K][K], ai[K][K], linv[K], zf_dinv[K];
+  bool zf_ok = false;
+  if (P.receivers & XLMIMO_RECV_ZF) {
+    load_a<K>(G, 1.0, 0.0, ar, ai);
+    zf_ok = chol_reg<K>(ar, ai, linv);
+    if (zf_ok) inv_diag_reg<K>(ar, ai, linv, zf_dinv);
+    else fl |= XLMIMO_FLAG_G_NOT_PD;
+  }
+  if ((P.receivers & XLMIMO_RECV_MRC) && !mrc_ok) fl |= XLMIMO_FLAG_MRC_UNDEF;
+  for (int s = 0; s < P.n_snr; ++s) {
+    const double rho = P.rho[s];
+    int r = 0;
+    bool a_ok = false;
+    double cap = 0.0, mmse = 0.0;
+    if (P.receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) {
+      load_a<K>(G, rho, 1.0, ar, ai);
+      a_ok = chol_reg<K>(ar, ai, linv);
+      if (!a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
+      if (a_ok) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) cap += 2.0 * log2(ar[k][k]);
+        if (P.receivers & XLMIMO_RECV_MMSE) {
+          double dinv[K];
+          inv_diag_reg<K>(ar, ai, linv, dinv);
+#pragma unroll
+          for (int i = 0; i < K; ++i) mmse += log2(1.0 + (1.0 / dinv[i] - 1.0));
+        }
+      }
+    }
+    if (P.receivers & XLMIMO_RECV_CAP) out[s * P.n_recv + r++] = a_ok ? cap : nan;
+    if (P.receivers & XLMIMO_RECV_ZF) {
+      double c = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) c += log2(1.0 + rho / zf_dinv[i]);
+      out[s * P.n_recv + r++] = zf_ok ? c : nan;
+    }
+    if (P.receivers & XLMIMO_RECV_MMSE) out[s * P.n_recv + r++] = a_ok ? mmse : nan;
+    if (P.receivers & XLMIMO_RECV_MRC) {
+      double c = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double intf = 0.0;
+        const double gii = __ldg(G + i * K + i).x;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (j != i) {
+            const double2 g = __ldg(G + i * K + j);
+            intf += g.x * g.x + g.y * g.y;
+          }
+        c += log2(1.0 + rho * gii * gii / (gii + rho * intf));
+      }
+      out[s * P.n_recv + r++] = mrc_ok ? c : nan;
+    }
+  }
+  if (P.flags) P.flags[prob] |= fl;
+}
+
+template <int K>
+void launch_rates_thread(const RateParams &P, cudaStream_t s) {
+  rates_thread_kernel<K><<<(unsigned)((P.n_prob + 127) / 128), 128, 0, s>>>(P);
+}
+
 }  // namespace
 
 namespace xlh {
@@ -245,7 +400,18 @@ int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr
   const size_t smem = per_warp * nw;
   const int64_t blocks = (n_prob + nw - 1) / nw;
   KTimer tm(s, "sum_rate");
-  if (K <= 32) {
+  if (K <= 8) {
+    switch (K) {
+      case 1: launch_rates_thread<1>(P, s); break;
+      case 2: launch_rates_thread<2>(P, s); break;
+      case 3: launch_rates_thread<3>(P, s); break;
+      case 4: launch_rates_thread<4>(P, s); break;
+      case 5: launch_rates_thread<5>(P, s); break;
+      case 6: launch_rates_thread<6>(P, s); break;
+      case 7: launch_rates_thread<7>(P, s); break;
+      default: launch_rates_thread<8>(P, s); break;
+    }
+  } else if (K <= 32) {
     cudaFuncSetAttribute(rates_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     rates_kernel<1><<<(unsigned)blocks, 32 * nw, smem, s>>>(P);
   } else {
