@@ -38,6 +38,8 @@ struct GramParams {
   int n_lvl;
   int64_t lvl_end[kMaxLvl];
   double inv_lambda, pitch, sqrt_beta0;
+  const float *hmat;   // materialised H (FROM_H kernels): [drop - h_drop0][K][2][N]
+  int64_t h_drop0;     // first drop of the current batch (materialised mode; 0 otherwise)
 };
 
 struct ElemPos {
@@ -73,6 +75,37 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// K4a: write H as planar complex64 [drop - h_drop0][K][2][N] (re plane, im plane,
+// N contiguous) for a batch of drops, in the centred element order.  fp64 distance
+// and phase reduction, fp32 phasor (XLMIMO_FP32).  Thread per element, coalesced
+// stores along N.  Optionally rounds to TF32 (round-to-nearest-away) for the
+// tensor-core stream (V8: hardware truncation would bias the diagonal by -7e-4).
+__global__ void __launch_bounds__(256) h_materialise_kernel(GramParams P, float *H, int n_batch, int tf32) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = P.N;
+  if (idx >= per * n_batch) return;
+  const int bd = (int)(idx / per);
+  const int64_t t = idx - (int64_t)bd * per;
+  const int64_t drop = P.h_drop0 + bd;
+  const int K = P.K;
+  const ElemPos ep = element_pos(P, t);
+  float *Hd = H + (size_t)bd * K * 2 * per;
+  for (int k = 0; k < K; ++k) {
+    const xl::UserC u = xl::make_user(P.pos + (drop * K + k) * 3, P.kind, P.sqrt_beta0);
+    float fr, fi;
+    xl::coef_from_r2_f32(dist2(u, ep, P.kind), u.amp, P.inv_lambda, fr, fi);
+    if (tf32) {
+      uint32_t a, b;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(fr));
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(fi));
+      fr = __uint_as_float(a);
+      fi = __uint_as_float(b);
+    }
+    __stcs(Hd + ((size_t)k * 2) * per + t, fr);
+    __stcs(Hd + ((size_t)k * 2 + 1) * per + t, fi);
+  }
+}
+
 // ------------------------------------------------------------------ kernel A
 template <int KT, int NT, bool FP32>
 __global__ void __launch_bounds__(NT, 1) gram_small_kernel(GramParams P) {
@@ -82,8 +115,9 @@ __global__ void __launch_bounds__(NT, 1) gram_small_kernel(GramParams P) {
   __shared__ xl::UserC su[KT];
   __shared__ double red[NW][NV];
 
-  const int64_t drop = blockIdx.x / P.n_split;
-  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < KT) su[tid] = xl::make_user(P.pos + (drop * KT + tid) * 3, P.kind, P.sqrt_beta0);
   __syncthreads();
@@ -189,8 +223,9 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
   __shared__ double4 su[K];  // (xz2, y, amp, -)
   __shared__ double red[NW][2][NV];
 
-  const int64_t drop = blockIdx.x / P.n_split;
-  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = tid & 1, eslot = tid >> 1;
   if (tid < K) {
@@ -316,8 +351,9 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
   __shared__ double4 su[8 * G];            // (xz2, y, z, amp) per user
   __shared__ double cs[NW][NMMA][8][8];    // per-warp fragment staging at level ends
 
-  const int64_t drop = blockIdx.x / P.n_split;
-  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = P.K;
   for (int u = tid; u < 8 * G; u += NT) {
@@ -427,7 +463,7 @@ struct Cplx<double> { using T2 = double2; };
 template <>
 struct Cplx<float> { using T2 = float2; };
 
-template <int KP, bool FP32>
+template <int KP, bool FP32, bool FROM_H = false>
 __global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramParams P) {
   using Cfg = TiledCfg<KP>;
   using RT = typename std::conditional<FP32, float, double>::type;
@@ -436,8 +472,9 @@ __global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramPar
   __shared__ xl::UserC su[KP];
   __shared__ RT2 hs[T][KP];
 
-  const int64_t drop = blockIdx.x / P.n_split;
-  const int split = blockIdx.x - (int)(drop * P.n_split);
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
   const int tid = threadIdx.x;
   const int K = P.K;
   if (tid < KP) {
@@ -469,8 +506,23 @@ __global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramPar
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     for (int64_t t0 = a; t0 < b; t0 += T) {
+      if (FROM_H) {
+        // materialised planar fp32 H[drop][K][2][N]: coalesced along elements
+        const float *Hd = P.hmat + (size_t)(drop - P.h_drop0) * K * 2 * P.N;
+        for (int c = tid; c < T * KP; c += NT) {
+          const int row = c / T, e = c - (c / T) * T;
+          const int64_t t = t0 + e;
+          RT2 h;
+          h.x = 0; h.y = 0;
+          if (t < b && row < K) {
+            h.x = __ldcs(Hd + ((size_t)row * 2) * P.N + t);
+            h.y = __ldcs(Hd + ((size_t)row * 2 + 1) * P.N + t);
+          }
+          hs[e][row] = h;
+        }
+      }
       // generation: T x KP coefficients, element-major interleaved complex
-      for (int c = tid; c < T * KP; c += NT) {
+      for (int c = tid; c < (FROM_H ? 0 : T * KP); c += NT) {
         const int e = c / KP, row = c - (c / KP) * KP;
         const int64_t t = t0 + e;
         RT2 h;
@@ -684,19 +736,100 @@ void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   }
 }
 
+// Materialised mode: drops per batch so that the planar complex64 H of a batch
+// fits a 2 GiB slice of the workspace (cfg5: 4 drops of 512 MiB; cfg3: 1024).
+int64_t materialised_batch(int64_t N, int K, int64_t n_drops) {
+  const int64_t per = (int64_t)N * K * 2 * (int64_t)sizeof(float);
+  int64_t b = ((int64_t)2 << 30) / (per > 0 ? per : 1);
+  if (b < 1) b = 1;
+  return b < n_drops ? b : n_drops;
+}
+
 size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
-  (void)mode;
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
+  if (mode == XLMIMO_MATERIALIZED) {
+    const size_t part = ((size_t)n_drops * n_split * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
+    return part + (size_t)materialised_batch(N, K, n_drops) * N * K * 2 * sizeof(float);
+  }
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
+}
+
+template <int KP>
+void launch_tiled_from_h(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  gram_tiled_kernel<KP, true, true><<<(unsigned)n_blocks, TiledCfg<KP>::NT, 0, s>>>(P);
+}
+
+// XLMIMO_MATERIALIZED (fp32 only): per batch of drops, K4a writes H to HBM and the
+// streaming kernel reads it back; partials reduced in fp64 as in the fused path.
+int launch_materialised(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *out,
+                        void *ws, size_t ws_bytes, cudaStream_t s) {
+  const size_t need = gram_ws_bytes(a, K, n_drops, 1, XLMIMO_FP32, XLMIMO_MATERIALIZED);
+  if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+  GramParams P;
+  memset(&P, 0, sizeof(P));
+  P.pos = pos;
+  P.ws = (double *)ws;
+  P.K = K;
+  P.kind = a.kind;
+  P.n_y = a.n_y;
+  P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+  P.N = N;
+  P.n_split = choose_split(n_drops, N);
+  P.chunk = ((N + P.n_split - 1) / P.n_split + 255) / 256 * 256;
+  P.n_lvl = 1;
+  for (int l = 0; l < kMaxLvl; ++l) P.lvl_end[l] = N;
+  P.inv_lambda = 1.0 / a.lambda;
+  P.pitch = a.pitch;
+  P.sqrt_beta0 = a.sqrt_beta0;
+  const size_t np = (size_t)K * (K + 1) / 2;
+  const size_t part = ((size_t)n_drops * P.n_split * np * 2 * sizeof(double) + 255) / 256 * 256;
+  float *H = (float *)((char *)ws + part);
+  P.hmat = H;
+  const int64_t B = materialised_batch(N, K, n_drops);
+  for (int64_t d0 = 0; d0 < n_drops; d0 += B) {
+    const int nb = (int)(d0 + B <= n_drops ? B : n_drops - d0);
+    P.h_drop0 = d0;
+    const int64_t n_el = N * nb;
+    {
+      KTimer tm(s, "h_materialise");
+      h_materialise_kernel<<<(unsigned)((n_el + 255) / 256), 256, 0, s>>>(P, H, nb, 0);
+      tm.stop(s);
+      count_launch();
+    }
+    KTimer tm(s, "gram_stream_fp32");
+    const int64_t n_blocks = (int64_t)nb * P.n_split;
+    if (K <= 16) launch_tiled_from_h<16>(P, n_blocks, s);
+    else if (K <= 32) launch_tiled_from_h<32>(P, n_blocks, s);
+    else if (K <= 48) launch_tiled_from_h<48>(P, n_blocks, s);
+    else launch_tiled_from_h<64>(P, n_blocks, s);
+    tm.stop(s);
+    count_launch();
+    int rc = check_launch("materialised gram");
+    if (rc) return rc;
+  }
+  const int64_t n_items = n_drops * (int64_t)np;
+  KTimer tr(s, "gram_reduce");
+  gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops, P.n_split, 1,
+                                                                      1, out);
+  tr.stop(s);
+  count_launch();
+  return check_launch("gram_reduce_kernel");
 }
 
 int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s) {
-  if (mode != XLMIMO_FUSED) return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: only XLMIMO_FUSED is provided");
+  if (mode == XLMIMO_MATERIALIZED) {
+    if (precision != XLMIMO_FP32)
+      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: XLMIMO_MATERIALIZED is complex64 (XLMIMO_FP32) only");
+    if (n_lvl != 1) return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: materialised mode has no nested levels");
+    if (n_drops == 0) return XLMIMO_OK;
+    return launch_materialised(a, pos, K, n_drops, lvl_end[0], out, ws, ws_bytes, s);
+  }
+  if (mode != XLMIMO_FUSED) return set_error(XLMIMO_EINVAL, "gram_exact: mode");
   if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
   if (n_drops == 0) return XLMIMO_OK;
   const int64_t N = lvl_end[n_lvl - 1];
@@ -704,6 +837,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   if (ws_bytes < need || (need && !ws))
     return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
   GramParams P;
+  memset(&P, 0, sizeof(P));
   P.pos = pos;
   P.ws = (double *)ws;
   P.K = K;

@@ -76,13 +76,14 @@ CASES = [
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}_K{c[4]}_D{c[5]}")
-@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "mat32"])
 def test_gram_exact_parity(xl, orc, case, prec):
     kind, n_y, n_z, fc, K, D, r, az, el = case
     ag, ao = _arr(xl, orc, kind, n_y, n_z, fc)
     ug, _ = _users(xl, orc, r, az, el)
     pos = xl.gen_drops(ug, K, D, seed=17)
-    G = xl.gram_exact(ag, pos, precision=xl.FP64 if prec == "fp64" else xl.FP32).cpu().numpy()
+    mode = xl.MATERIALIZED if prec == "mat32" else xl.FUSED
+    G = xl.gram_exact(ag, pos, precision=xl.FP64 if prec == "fp64" else xl.FP32, mode=mode).cpu().numpy()
     Go = orc.gram_exact(ao, pos.cpu().numpy())
     tol = 1e-9 if prec == "fp64" else 1e-4
     assert normalized_err(G, Go) <= tol
@@ -125,6 +126,21 @@ def test_gram_cfg5_full_size_sampled(xl, orc):
         for i in range(w.K):
             x, y = P[d, i, 0], P[d, i, 1]
             assert abs(G[d, i, i].real / orc.power_eq4(w.n_y, lam, 1.0, x, y) - 1) < 1e-9
+
+
+def test_gram_cfg5_materialised_and_fp32_full_size(xl, orc):
+    """cfg5 full size: the materialised complex64 H path and the fused fp32 path vs the
+    oracle on sampled pairs (1e-4 normalized, fp32 tolerance)."""
+    w = CONFIGS[5]
+    ag, ao = _arr(xl, orc, "ula", w.n_y, 1, w.fc_hz)
+    pos = xl.gen_drops(xl.Users.polar(w.r, w.az), w.K, 2, seed=w.seed)
+    P = pos.cpu().numpy()
+    Gm = xl.gram_exact(ag, pos, precision=xl.FP32, mode=xl.MATERIALIZED).cpu().numpy()
+    Gf = xl.gram_exact(ag, pos, precision=xl.FP32).cpu().numpy()
+    for d, (i, j) in [(0, (3, 41)), (1, (0, 63)), (1, (17, 18))]:
+        Go = orc.gram_exact(ao, P[d:d + 1, [i, j]])[0]
+        for G in (Gm, Gf):
+            assert normalized_err(G[d][np.ix_([i, j], [i, j])], Go) <= 1e-4
 
 
 # --------------------------------------------------------------------------- a4
