@@ -251,6 +251,12 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s);
 
+// xl_stream_tc.cu : tcgen05 TF32 streaming Gram over a materialised batch
+bool stream_tc_supported(int K, int64_t N);
+int stream_tc_chunks(int64_t N);
+int stream_tc_parts(int K);
+int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s);
+
 // xl_closed.cu : out[drop][lvl][K][K][2] for M = n_list[lvl]
 int launch_closed_form(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *m_list,
                        int n_lvl, double *out, uint32_t *flags, cudaStream_t s);

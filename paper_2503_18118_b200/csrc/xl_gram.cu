@@ -80,20 +80,27 @@ __device__ __forceinline__ double warp_sum(double v) {
 // and phase reduction, fp32 phasor (XLMIMO_FP32).  Thread per element, coalesced
 // stores along N.  Optionally rounds to TF32 (round-to-nearest-away) for the
 // tensor-core stream (V8: hardware truncation would bias the diagonal by -7e-4).
-__global__ void __launch_bounds__(256) h_materialise_kernel(GramParams P, float *H, int n_batch, int tf32) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t per = P.N;
-  if (idx >= per * n_batch) return;
-  const int bd = (int)(idx / per);
-  const int64_t t = idx - (int64_t)bd * per;
+// Layouts: planar  H[d][k][c][N]                    (CUDA-core stream)
+//          tiled32 H[d][N32/32][k][c][32], N32 = n_pad (tcgen05 stream: one TMA box =
+//                  2K rows x 128 B contiguous; padded elements are written as 0).
+// grid = (ceil(n_pad / 256), n_batch): one drop per blockIdx.y, users staged in smem.
+__global__ void __launch_bounds__(256) h_materialise_kernel(GramParams P, float *H, int64_t n_pad, int tiled,
+                                                            int tf32) {
+  __shared__ xl::UserC su[xl::kMaxK];
+  const int bd = blockIdx.y;
   const int64_t drop = P.h_drop0 + bd;
   const int K = P.K;
-  const ElemPos ep = element_pos(P, t);
-  float *Hd = H + (size_t)bd * K * 2 * per;
+  if (threadIdx.x < K) su[threadIdx.x] = xl::make_user(P.pos + (drop * K + threadIdx.x) * 3, P.kind, P.sqrt_beta0);
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pad) return;
+  const bool valid = t < P.N;
+  const ElemPos ep = element_pos(P, valid ? t : 0);
+  float *Hd = H + (size_t)bd * K * 2 * n_pad;
   for (int k = 0; k < K; ++k) {
-    const xl::UserC u = xl::make_user(P.pos + (drop * K + k) * 3, P.kind, P.sqrt_beta0);
-    float fr, fi;
-    xl::coef_from_r2_f32(dist2(u, ep, P.kind), u.amp, P.inv_lambda, fr, fi);
+    const xl::UserC u = su[k];
+    float fr = 0.f, fi = 0.f;
+    if (valid) xl::coef_from_r2_f32(dist2(u, ep, P.kind), u.amp, P.inv_lambda, fr, fi);
     if (tf32) {
       uint32_t a, b;
       asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(fr));
@@ -101,8 +108,17 @@ __global__ void __launch_bounds__(256) h_materialise_kernel(GramParams P, float 
       fr = __uint_as_float(a);
       fi = __uint_as_float(b);
     }
-    __stcs(Hd + ((size_t)k * 2) * per + t, fr);
-    __stcs(Hd + ((size_t)k * 2 + 1) * per + t, fi);
+    size_t o_re, o_im;
+    if (tiled) {
+      const size_t tile = (size_t)(t >> 5);
+      o_re = ((tile * K + k) * 2) * 32 + (t & 31);
+      o_im = o_re + 32;
+    } else {
+      o_re = ((size_t)k * 2) * n_pad + t;
+      o_im = o_re + n_pad;
+    }
+    __stcs(Hd + o_re, fr);
+    __stcs(Hd + o_im, fi);
   }
 }
 
@@ -444,6 +460,177 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
   }
 }
 
+// ------------------------------------------------------------------ kernel MT
+// DMMA Gram for K = 17..64 (G = 3..8 user groups of 8), shared generation.
+// Per tile of 4*S elements all threads generate the 8G x 4S coefficients into
+// shared memory already in m8n8k4 fragment order (frag[s][g][lane], lane =
+// 4*(user%8) + element%4, re and im planes), then each warp runs the DMMAs of its
+// share of the group pairs (g1 <= g2): 3 per diagonal pair (RR, II, RI), 4 per
+// cross pair (RR, II, RI, IR), loading 4 fragments (one LDS.64 per lane each) per
+// pair.  At the level end the warps stage their fragments and the block writes
+// one partial in the standard layout.
+constexpr int kMtMaxPairs = 8;  // group pairs per warp (G = 8: 36 pairs over 8 warps)
+struct MtPlan {
+  int npairs[8];
+  int g1[8][kMtMaxPairs], g2[8][kMtMaxPairs];
+};
+
+template <int G, int S>
+__global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, MtPlan plan) {
+  constexpr int NT = 256, NW = 8, NPAIR = G * (G + 1) / 2;
+  extern __shared__ __align__(16) double dsm[];
+  double *fre = dsm;                  // [S][G][32]
+  double *fim = dsm + S * G * 32;     // [S][G][32]
+  double *stage = dsm;                // [NPAIR][4][8][8] at level ends (aliases the tiles)
+  __shared__ double4 su[8 * G];
+
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = P.K;
+  for (int u = tid; u < 8 * G; u += NT) {
+    if (u < K) {
+      const xl::UserC uc = xl::make_user(P.pos + (drop * K + u) * 3, P.kind, P.sqrt_beta0);
+      su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+    } else {
+      su[u] = make_double4(1.0, 0.0, 0.0, 0.0);
+    }
+  }
+  constexpr int MAXP = (NPAIR + 7) / 8 + 1;  // bound used by make_mt_plan
+  const int np = plan.npairs[warp];
+  int pg1[MAXP], pg2[MAXP];
+#pragma unroll
+  for (int k = 0; k < MAXP; ++k) {
+    pg1[k] = plan.g1[warp][k];
+    pg2[k] = plan.g2[warp][k];
+  }
+  __syncthreads();
+  const double c4 = 4.0 * P.inv_lambda;
+  const int ulocal = lane >> 2, elocal = lane & 3;
+
+  const int64_t s0 = (int64_t)split * P.chunk;
+  const int64_t s1 = min(P.N, s0 + P.chunk);
+  int64_t lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int64_t lv1 = P.lvl_end[l];
+    const int64_t a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[MAXP][4][2];
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+    for (int64_t t0 = a; t0 < b; t0 += 4 * S) {
+      // generation: S*G*32 coefficients, fragment order
+      for (int c = tid; c < S * G * 32; c += NT) {
+        const int s = c / (G * 32), rem = c - s * (G * 32), g = rem >> 5, ln = rem & 31;
+        const int64_t t = t0 + 4 * s + (ln & 3);
+        const int u = (ln >> 2) + 8 * g;
+        const bool valid = t < b;
+        const ElemPos ep = element_pos(P, valid ? t : a);
+        const double4 uc = su[u];
+        const double dy = ep.y - uc.y;
+        double r2 = fma(dy, dy, uc.x);
+        if (P.kind != XLMIMO_ULA) {
+          const double dz = ep.z - uc.z;
+          r2 = fma(dz, dz, r2);
+        }
+        double hr, hi;
+        xl::coef_fast(r2, valid ? uc.w : 0.0, c4, hr, hi);
+        fre[c] = hr;
+        fim[c] = hi;
+      }
+      __syncthreads();
+      for (int s = 0; s < S; ++s) {
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k) {
+          if (k < np) {
+            const int g1 = pg1[k], g2 = pg2[k];
+            const double ar = fre[(s * G + g1) * 32 + lane], ai = fim[(s * G + g1) * 32 + lane];
+            const double br = fre[(s * G + g2) * 32 + lane], bi = fim[(s * G + g2) * 32 + lane];
+            dmma(acc[k][0], ar, br);
+            dmma(acc[k][1], ai, bi);
+            dmma(acc[k][2], ar, bi);
+            if (g1 != g2) dmma(acc[k][3], ai, br);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // stage fragments: pair index p(g1,g2) in row-major (g1 <= g2) order
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) {
+      if (k < np) {
+        const int g1 = pg1[k], g2 = pg2[k];
+        const int p =g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          stage[((p * 4 + m) * 8 + ulocal) * 8 + 2 * elocal] = acc[k][m][0];
+          stage[((p * 4 + m) * 8 + ulocal) * 8 + 2 * elocal + 1] = acc[k][m][1];
+        }
+      }
+    }
+    __syncthreads();
+    const int NP = K * (K + 1) / 2;
+    double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * (size_t)(2 * NP);
+    for (int q = tid; q < NP; q += NT) {
+      int i = 0, rem = q;
+      while (rem >= K - i) { rem -= K - i; ++i; }
+      const int j = i + rem;
+      const int g1 = i >> 3, g2 = j >> 3, ii = i & 7, jj = j & 7;
+      const int p = g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
+      const double *st = stage + (size_t)p * 4 * 64;
+      const double re = st[0 * 64 + ii * 8 + jj] + st[1 * 64 + ii * 8 + jj];
+      const double im = (g1 == g2) ? st[2 * 64 + ii * 8 + jj] - st[2 * 64 + jj * 8 + ii]
+                                   : st[2 * 64 + ii * 8 + jj] - st[3 * 64 + ii * 8 + jj];
+      out[2 * q] = re;
+      out[2 * q + 1] = (i == j) ? 0.0 : im;
+    }
+    __syncthreads();
+    (void)NPAIR;
+  }
+}
+
+// Balanced assignment of the G(G+1)/2 group pairs (row-major) to 8 warps by DMMA count.
+MtPlan make_mt_plan(int G) {
+  MtPlan pl;
+  memset(&pl, 0, sizeof(pl));
+  const int maxp = (G * (G + 1) / 2 + 7) / 8 + 1;
+  // longest-processing-time greedy: cross pairs (4 DMMAs) first, then diagonal (3)
+  int load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int pass = 0; pass < 2; ++pass)
+    for (int g1 = 0; g1 < G; ++g1)
+      for (int g2 = g1; g2 < G; ++g2) {
+        if ((g1 == g2) != (pass == 1)) continue;
+        int w = -1;
+        for (int c = 0; c < 8; ++c)
+          if (pl.npairs[c] < maxp && (w < 0 || load[c] < load[w])) w = c;
+        pl.g1[w][pl.npairs[w]] = g1;
+        pl.g2[w][pl.npairs[w]] = g2;
+        ++pl.npairs[w];
+        load[w] += (g1 == g2) ? 3 : 4;
+      }
+  return pl;
+}
+
+constexpr int kMtS = 8;  // 4-element steps per tile (32 elements)
+
+template <int G>
+size_t mt_smem_bytes() {
+  const size_t tiles = 2 * (size_t)kMtS * G * 32 * sizeof(double);
+  const size_t stage = (size_t)(G * (G + 1) / 2) * 4 * 64 * sizeof(double);
+  return tiles > stage ? tiles : stage;
+}
+
+template <int G>
+void launch_mt(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  static const MtPlan plan = make_mt_plan(G);
+  const size_t smem = mt_smem_bytes<G>();
+  cudaFuncSetAttribute(gram_mma_tiled_kernel<G, kMtS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_mma_tiled_kernel<G, kMtS><<<(unsigned)n_blocks, 256, smem, s>>>(P, plan);
+}
+
 // ------------------------------------------------------------------ kernel B
 template <int KP>
 struct TiledCfg {
@@ -706,14 +893,14 @@ KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
   const bool split_ok = fp64 && a.kind == XLMIMO_ULA && (K == 8 || K == 4);
   const bool mma_ok = fp64 && K <= 16;
   // measured on B200 (cfg2, K = 8): split 20.4 ms < DMMA 23.6 ms < register kernel A 37.7 ms
-  c.which = split_ok ? 1 : mma_ok ? 2 : 0;
+  c.which = split_ok ? 1 : mma_ok ? 2 : fp64 ? 3 : 0;
   if (env_k && !strcmp(env_k, "split") && split_ok) c.which = 1;
   if (env_k && !strcmp(env_k, "mma") && mma_ok) c.which = 2;
   if (env_k && !strcmp(env_k, "legacy")) c.which = 0;
   c.nt = 256;
   if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = env_nt;
   if (c.which == 2) c.nt = mma_nt(K <= 8 ? 1 : 2);
-  c.parts = c.which >= 1 ? c.nt / 32 : 1;
+  c.parts = (c.which == 1 || c.which == 2) ? c.nt / 32 : 1;
   return c;
 }
 
@@ -736,11 +923,24 @@ void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   }
 }
 
+// Materialised streaming on tcgen05 (TF32, RNA-pre-rounded H) unless disabled by
+// XLMIMO_STREAM=cuda (CUDA-core fp32 tiled kernel, also the fallback for shapes
+// the TMA path does not take: K < 9, N % 4 != 0).
+bool materialised_use_tc(int K, int64_t N) {
+  static const char *e = getenv("XLMIMO_STREAM");
+  if (e && !strcmp(e, "cuda")) return false;
+  return stream_tc_supported(K, N);
+}
+
 // Materialised mode: drops per batch so that the planar complex64 H of a batch
-// fits a 2 GiB slice of the workspace (cfg5: 4 drops of 512 MiB; cfg3: 1024).
+// fits an 8 GiB slice of the workspace (cfg5: 16 drops of 512 MiB; cfg3: 4096), so
+// one persistent streaming launch has >= ~14 waves of work items.
+// elements per drop as stored: the tiled32 (tcgen05) layout pads N to whole groups of 4 tiles
+int64_t mat_npad(int K, int64_t N) { return materialised_use_tc(K, N) ? (N + 127) / 128 * 128 : N; }
+
 int64_t materialised_batch(int64_t N, int K, int64_t n_drops) {
-  const int64_t per = (int64_t)N * K * 2 * (int64_t)sizeof(float);
-  int64_t b = ((int64_t)2 << 30) / (per > 0 ? per : 1);
+  const int64_t per = mat_npad(K, N) * K * 2 * (int64_t)sizeof(float);
+  int64_t b = ((int64_t)8 << 30) / (per > 0 ? per : 1);
   if (b < 1) b = 1;
   return b < n_drops ? b : n_drops;
 }
@@ -750,8 +950,9 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
   if (mode == XLMIMO_MATERIALIZED) {
-    const size_t part = ((size_t)n_drops * n_split * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
-    return part + (size_t)materialised_batch(N, K, n_drops) * N * K * 2 * sizeof(float);
+    const int parts = materialised_use_tc(K, N) ? stream_tc_chunks(N) * stream_tc_parts(K) : n_split;
+    const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
+    return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
@@ -785,35 +986,47 @@ int launch_materialised(const ArrayP &a, const double *pos, int K, int64_t n_dro
   P.pitch = a.pitch;
   P.sqrt_beta0 = a.sqrt_beta0;
   const size_t np = (size_t)K * (K + 1) / 2;
-  const size_t part = ((size_t)n_drops * P.n_split * np * 2 * sizeof(double) + 255) / 256 * 256;
+  const bool tc = materialised_use_tc(K, N);
+  const int parts = tc ? stream_tc_chunks(N) : P.n_split;
+  const int subparts = tc ? stream_tc_parts(K) : 1;
+  const size_t part = ((size_t)n_drops * parts * subparts * np * 2 * sizeof(double) + 255) / 256 * 256;
   float *H = (float *)((char *)ws + part);
   P.hmat = H;
   const int64_t B = materialised_batch(N, K, n_drops);
   for (int64_t d0 = 0; d0 < n_drops; d0 += B) {
     const int nb = (int)(d0 + B <= n_drops ? B : n_drops - d0);
     P.h_drop0 = d0;
-    const int64_t n_el = N * nb;
+    const int64_t n_pad = mat_npad(K, N);
     {
       KTimer tm(s, "h_materialise");
-      h_materialise_kernel<<<(unsigned)((n_el + 255) / 256), 256, 0, s>>>(P, H, nb, 0);
+      h_materialise_kernel<<<dim3((unsigned)((n_pad + 255) / 256), (unsigned)nb), 256, 0, s>>>(P, H, n_pad, tc ? 1 : 0,
+                                                                                             tc ? 1 : 0);
       tm.stop(s);
       count_launch();
     }
-    KTimer tm(s, "gram_stream_fp32");
-    const int64_t n_blocks = (int64_t)nb * P.n_split;
-    if (K <= 16) launch_tiled_from_h<16>(P, n_blocks, s);
-    else if (K <= 32) launch_tiled_from_h<32>(P, n_blocks, s);
-    else if (K <= 48) launch_tiled_from_h<48>(P, n_blocks, s);
-    else launch_tiled_from_h<64>(P, n_blocks, s);
-    tm.stop(s);
-    count_launch();
-    int rc = check_launch("materialised gram");
+    int rc;
+    if (tc) {
+      KTimer tm(s, "gram_stream_tc_tf32");
+      rc = launch_stream_tc(H, K, n_pad, d0, nb, (double *)ws, s);
+      tm.stop(s);
+      count_launch();
+    } else {
+      KTimer tm(s, "gram_stream_fp32");
+      const int64_t n_blocks = (int64_t)nb * P.n_split;
+      if (K <= 16) launch_tiled_from_h<16>(P, n_blocks, s);
+      else if (K <= 32) launch_tiled_from_h<32>(P, n_blocks, s);
+      else if (K <= 48) launch_tiled_from_h<48>(P, n_blocks, s);
+      else launch_tiled_from_h<64>(P, n_blocks, s);
+      tm.stop(s);
+      count_launch();
+      rc = check_launch("materialised gram");
+    }
     if (rc) return rc;
   }
   const int64_t n_items = n_drops * (int64_t)np;
   KTimer tr(s, "gram_reduce");
-  gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops, P.n_split, 1,
-                                                                      1, out);
+  gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops, parts, 1,
+                                                                      subparts, out);
   tr.stop(s);
   count_launch();
   return check_launch("gram_reduce_kernel");
@@ -858,9 +1071,19 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   const KernelChoice kc = choose_kernel(a, K, precision);
   KTimer tm(s, kc.which == 1 ? "gram_fused_split_fp64"
                : kc.which == 2 ? "gram_fused_dmma_fp64"
+               : kc.which == 3 ? "gram_fused_dmma_tiled_fp64"
                : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
                         : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
-  if (kc.which == 2) {
+  if (kc.which == 3) {
+    switch ((K + 7) / 8) {
+      case 3: launch_mt<3>(P, n_blocks, s); break;
+      case 4: launch_mt<4>(P, n_blocks, s); break;
+      case 5: launch_mt<5>(P, n_blocks, s); break;
+      case 6: launch_mt<6>(P, n_blocks, s); break;
+      case 7: launch_mt<7>(P, n_blocks, s); break;
+      default: launch_mt<8>(P, n_blocks, s); break;
+    }
+  } else if (kc.which == 2) {
     const bool ula = a.kind == XLMIMO_ULA;
     if (K <= 8) {
       if (ula) launch_mma<1, XLMIMO_ULA>(P, n_blocks, s);

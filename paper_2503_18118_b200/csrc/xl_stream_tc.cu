@@ -1,0 +1,350 @@
+// xl_stream_tc.cu -- K4b on the 5th-generation tensor cores: G = H^H H streamed
+// from HBM (XLMIMO_MATERIALIZED), tcgen05.mma kind::tf32 with the accumulator in
+// TMEM, operands staged by TMA (SWIZZLE_128B) through an mbarrier ring.
+//
+// Real-ified Gram: H is stored planar [drop][K][2][N] (rows = (user, re/im)), so
+// the 2K x N row block of a drop is the K-major operand A, and R = A A^T (M = 128
+// rows, rows >= 2K zero in shared memory; MMA N = 2K rounded up to 16) gives
+//   Re G(i,j) = R(2i,2j) + R(2i+1,2j+1),   Im G(i,j) = R(2i,2j+1) - R(2i+1,2j).
+// TF32 products of the RNA-pre-rounded H (K4a, tf32 = 1) accumulate in fp32 over
+// a chunk of kChunk elements; chunk partials are combined in fp64 by
+// gram_reduce_kernel (fp32 in-tile, fp64 across tiles).
+//
+// Persistent kernel, one CTA per SM, warp roles: warp 0 TMA producer, warp 1 TMEM
+// allocator + MMA issuer (one elected lane), warps 4..7 epilogue (TMEM lane
+// quadrants 0..3), double-buffered TMEM accumulator so the epilogue of one chunk
+// overlaps the MMAs of the next.  Bounded mbarrier waits trap instead of hanging.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "xl_common.cuh"
+
+namespace {
+
+constexpr int kStages = 12;
+constexpr int kRows = 128;             // MMA M (rows >= 2K stay zero)
+constexpr int kBoxK = 32;              // fp32 elements per row per stage (128 B, one swizzle atom)
+constexpr int kStageBytes = kRows * kBoxK * 4;  // 16 KiB
+constexpr int kChunk = 8192;           // elements accumulated in TMEM per partial
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  uint32_t done = 0;
+  for (uint32_t it = 0; it < (1u << 26); ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();  // a lost arrival: abort the kernel rather than hang the GPU
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, void *dst, uint64_t *bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, void *dst, uint64_t *bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05): start >> 4,
+// LBO = 16 B (unused for swizzled K-major), SBO = 1024 B (8 rows x 128 B),
+// version 1 (bit 46), layout type 2 = SWIZZLE_128B (bits 61..63).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct StreamParams {
+  double *ws;        // partials [drop][chunk][blk][NP][2] (absolute drop index)
+  int K;
+  int rb;            // rows per element block in a stage (32, 64 or 128; >= 2K)
+  int nblk;          // element blocks stacked in the 128 MMA rows (128 / rb)
+  int n_mma;         // MMA N
+  int64_t N;
+  int n_chunks;      // per drop
+  int64_t drop0;     // first drop of this batch
+  int nb;            // drops in this batch
+  uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                    StreamParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned stage ring
+  uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *stages = base;
+  uint64_t *full = (uint64_t *)(base + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = P.K, R = 2 * K;
+  const int64_t n_items = (int64_t)P.nb * P.n_chunks;
+
+  // zero the ring once: rows >= 2K are never written by TMA and must read as 0
+  for (int i = tid; i < kStages * kStageBytes / 16; i += kThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_sh;
+  const int kb_per_chunk = kChunk / (kBoxK * P.nblk);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int d = (int)(it / P.n_chunks), c = (int)(it - (int64_t)d * P.n_chunks);
+        const int64_t x0 = (int64_t)c * kChunk;
+        for (int kb = 0; kb < kb_per_chunk; ++kb) {
+          const int64_t x = x0 + (int64_t)kb * kBoxK * P.nblk;
+          if (x >= P.N) break;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], (uint32_t)(P.nblk * R * kBoxK * 4));
+          // one contiguous 2K x 128 B tile per element block (tiled32 layout, N padded by K4a)
+          const int64_t tile0 = (int64_t)d * (P.N / kBoxK) + x / kBoxK;
+          for (int b = 0; b < P.nblk; ++b)
+            tma_load_3d(&tmap, stages + stage * kStageBytes + b * P.rb * kBoxK * 4, &full[stage], 0, 0,
+                        (int)(tile0 + b));
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = tf32_idesc(kRows, P.n_mma);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+        const int d = (int)(it / P.n_chunks), c = (int)(it - (int64_t)d * P.n_chunks);
+        (void)d;
+        const int64_t x0 = (int64_t)c * kChunk;
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
+        for (int kb = 0; kb < kb_per_chunk; ++kb) {
+          if (x0 + (int64_t)kb * kBoxK * P.nblk >= P.N) break;
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stages + stage * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < kBoxK / 8; ++k) {  // 8 tf32 (32 B) per MMA along K
+            const uint64_t desc = sw128_desc(sa + 32 * k);
+            mma_tf32(tmem_d, desc, desc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue: TMEM lanes 32q..32q+31
+    const int q = warp - 4;
+    const int row = 32 * q + lane;
+    const int blk = (32 * q) / P.rb;                 // element block of this quadrant
+    const int lr = row - blk * P.rb;                 // row within the block
+    const int i = lr >> 1, plane = lr & 1;
+    const int col0 = blk * P.rb;                     // the block's diagonal columns
+    const bool has_users = 32 * q - blk * P.rb < R;
+    const int NP = K * (K + 1) / 2;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      const int d = (int)(it / P.n_chunks), c = (int)(it - (int64_t)d * P.n_chunks);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double *out = P.ws + (((size_t)(P.drop0 + d) * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
+      if (has_users) {
+        for (int cb = 0; cb < (R + 31) / 32; ++cb) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + col0 + 32 * cb), v);
+          float x[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+          // even lane (re row 2i): j-pairs 0..7 of this 32-column group; odd lane (im row): 8..15
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int jj = plane * 8 + h;
+            const int j = 16 * cb + jj;
+            float rr, rr2, ri, ir;  // R(2i,2j), R(2i+1,2j+1), R(2i,2j+1), R(2i+1,2j)
+            if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
+            else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
+            if (i < K && j < K && j >= i) {
+              const int p = i * K - i * (i - 1) / 2 + (j - i);
+              out[2 * p] = (double)rr + (double)rr2;
+              out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+}  // namespace
+
+namespace xlh {
+
+bool stream_tc_supported(int K, int64_t N) { return K >= 9 && K <= 64 && (N % 4) == 0 && N >= kBoxK; }
+
+int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
+
+// element blocks stacked per stage: 2K <= 32 -> 4, <= 64 -> 2, else 1
+static int rows_per_block(int K) { return 2 * K <= 32 ? 32 : 2 * K <= 64 ? 64 : 128; }
+int stream_tc_parts(int K) { return kRows / rows_per_block(K); }
+
+// One batch: H in the tiled32 layout [nb][N/32][2K][32] fp32 (TF32-rounded, N a
+// multiple of 128), partials for drops [drop0, drop0+nb).
+int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s) {
+  auto enc = encode_fn();
+  if (!enc) return set_error(XLMIMO_ECUDA, "stream_tc: cuTensorMapEncodeTiled unavailable");
+  if (N % 128) return set_error(XLMIMO_EINVAL, "stream_tc: padded N must be a multiple of 128");
+  CUtensorMap map;
+  const cuuint64_t gdim[3] = {(cuuint64_t)kBoxK, (cuuint64_t)(2 * K), (cuuint64_t)(N / kBoxK) * nb};
+  const cuuint64_t gstride[2] = {(cuuint64_t)kBoxK * 4, (cuuint64_t)kBoxK * 4 * 2 * K};
+  const cuuint32_t box[3] = {(cuuint32_t)kBoxK, (cuuint32_t)(2 * K), 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)H, gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(XLMIMO_ECUDA, "stream_tc: tensor map encode failed (%d)", (int)r);
+  StreamParams P;
+  P.ws = ws;
+  P.K = K;
+  P.rb = rows_per_block(K);
+  P.nblk = kRows / P.rb;
+  P.n_mma = P.nblk > 1 ? kRows : (2 * K + 15) / 16 * 16;
+  P.N = N;
+  P.n_chunks = stream_tc_chunks(N);
+  P.drop0 = drop0;
+  P.nb = nb;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * P.n_mma)) cols <<= 1;
+  P.tmem_cols = cols;
+  const size_t smem = 1024 + (size_t)kStages * kStageBytes + (2 * kStages + 4) * 8 + 16;
+  cudaFuncSetAttribute(gram_stream_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = (int64_t)nb * P.n_chunks;
+  const int grid = (int)(items < sms ? items : sms);
+  gram_stream_tc_kernel<<<grid, kThreads, smem, s>>>(map, P);
+  return check_launch("gram_stream_tc_kernel");
+}
+
+}  // namespace xlh
