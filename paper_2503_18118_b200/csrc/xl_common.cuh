@@ -132,20 +132,34 @@ __constant__ double kSinPoly[6] = {1.5707963267948898981, -0.6459640975043100580
 __constant__ double kCosPoly[7] = {0.99999999999999995287, -1.2337005501361513498, 0.25366950789986513871,
                                    -0.020863480734953519901, 0.0009192599500952791151,
                                    -0.000025200135454917479526, 4.6552987291490935821e-7};
+//   cos(pi/2 g) = C5(u) (degree 5, |err| <= 5.6e-14): used by coef_fast.
+__constant__ double kCosPoly5[6] = {0.99999999999994445739, -1.23370055012016865, 0.25366950715400581474,
+                                    -0.020863468005621057384, 0.00091916175238771112641,
+                                    -0.000024850988050231297507};
+
+// 1/sqrt(x) to ~3e-13 relative (MUFU seed + one Newton step, 4 FP64 instructions):
+// enough for the amplitude r^{-3/2}, not for the phase (see rsqrt_nr).
+__device__ __forceinline__ double rsqrt_newton(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
 
 // h = amp * r^{-3/2} * e^{-j 2 pi r/lambda}  (Eq. 3), fp64, the fused generator's
-// coefficient.  Phase: q4 = 4 r/lambda (quarter cycles), k = rint(q4) by the
-// 1.5*2^52 magic add (k's low bits = quadrant), g = q4 - k in [-1/2, 1/2] exactly,
-// angle = (pi/2)(k + g): the fp64 range reduction of the north_star.  ~32 FP64
-// pipe instructions per coefficient, no branches.  c4 = 4 / lambda.
+// coefficient.  Phase: q4 = 4 r/lambda (quarter cycles), k = rint(q4) (FRND),
+// quadrant = k mod 4 (F2I, XU pipe), g = q4 - k in [-1/2, 1/2] exactly, angle =
+// (pi/2)(k + g): the fp64 range reduction of the north_star.  1/r to ~1 ulp
+// (Householder), r^{-3/2} to ~3e-13 (Newton), sin 3.4e-15 / cos 5.6e-14 abs:
+// 29 FP64-pipe instructions + 2 MUFU + 1 F2I per coefficient, no branches.
+// c4 = 4 / lambda.
 __device__ __forceinline__ void coef_fast(double r2, double amp, double c4, double &re, double &im) {
   const double ir = rsqrt_nr(r2);
   const double r = r2 * ir;
   const double q4 = r * c4;
-  const double magic = 6755399441055744.0;  // 1.5 * 2^52
-  const double kd = q4 + magic;
-  const int qd = __double2loint(kd);
-  const double g = q4 - (kd - magic);
+  const double k = rint(q4);       // FRND.F64
+  const int qd = (int)k;           // F2I on the XU pipe (q4 < 2^31)
+  const double g = q4 - k;         // exact, |g| <= 1/2
   const double u = g * g;
   double ps = kSinPoly[5];
   ps = fma(ps, u, kSinPoly[4]);
@@ -154,14 +168,13 @@ __device__ __forceinline__ void coef_fast(double r2, double amp, double c4, doub
   ps = fma(ps, u, kSinPoly[1]);
   ps = fma(ps, u, kSinPoly[0]);
   const double sn = ps * g;
-  double pc = kCosPoly[6];
-  pc = fma(pc, u, kCosPoly[5]);
-  pc = fma(pc, u, kCosPoly[4]);
-  pc = fma(pc, u, kCosPoly[3]);
-  pc = fma(pc, u, kCosPoly[2]);
-  pc = fma(pc, u, kCosPoly[1]);
-  const double cs = fma(pc, u, kCosPoly[0]);
-  const double a = amp * ir * rsqrt_nr(r);  // r^{-3/2}
+  double pc = kCosPoly5[5];
+  pc = fma(pc, u, kCosPoly5[4]);
+  pc = fma(pc, u, kCosPoly5[3]);
+  pc = fma(pc, u, kCosPoly5[2]);
+  pc = fma(pc, u, kCosPoly5[1]);
+  const double cs = fma(pc, u, kCosPoly5[0]);
+  const double a = amp * ir * rsqrt_newton(r);  // r^{-3/2}, ~3e-13 relative
   // quadrant q: (cos, sin) of (pi/2)(q + g) = q0 (cs, sn), q1 (-sn, cs), q2 (-cs, -sn), q3 (sn, -cs);
   // h = a (cos - j sin)  =>  re = a*c, im = a*(-s)
   const int q = qd & 3;

@@ -227,7 +227,7 @@ __device__ __forceinline__ void split_map(int i, int j, int &parity, int &slot, 
   }
 }
 
-template <int KH, int NT, int MINB>
+template <int KH, int NT, int MINB, int UNR = 1>
 __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
   constexpr int K = 2 * KH;
   constexpr int NOWN = KH * (KH + 1) / 2;
@@ -262,47 +262,53 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
     double acc[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-    for (int64_t t0 = a; t0 < b; t0 += NSLOT) {  // warp-uniform trip count (shuffles below)
-      const int64_t t = t0 + eslot;
-      const bool valid = t < b;
-      const double ey = xl::ula_y_centred(valid ? t : a, n_odd, P.pitch);
-      double mr[KH], mi[KH];
+    for (int64_t t0 = a; t0 < b; t0 += NSLOT * UNR) {  // warp-uniform trip count (shuffles below)
+      double mr[UNR][KH], mi[UNR][KH];
 #pragma unroll
-      for (int q = 0; q < KH; ++q) {
-        const double4 u = su[h * KH + q];
-        const double dy = ey - u.y;
-        xl::coef_fast(fma(dy, dy, u.x), valid ? u.z : 0.0, c4, mr[q], mi[q]);
-      }
-      double tr[KH], ti[KH];
+      for (int w = 0; w < UNR; ++w) {
+        const int64_t t = t0 + w * NSLOT + eslot;
+        const bool valid = t < b;
+        const double ey = xl::ula_y_centred(valid ? t : a, n_odd, P.pitch);
 #pragma unroll
-      for (int q = 0; q < KH; ++q) {
-        const double sr = h ? mr[q] : mr[(q + 1) % KH];
-        const double si = h ? mi[q] : mi[(q + 1) % KH];
-        tr[q] = __shfl_xor_sync(0xffffffffu, sr, 1);
-        ti[q] = __shfl_xor_sync(0xffffffffu, si, 1);
-      }
-      int v = 0;
-#pragma unroll
-      for (int p = 0; p < KH; ++p) {
-#pragma unroll
-        for (int q = p; q < KH; ++q) {
-          if (p == q) {
-            acc[v] = fma(mr[p], mr[p], fma(mi[p], mi[p], acc[v]));
-          } else {
-            acc[v] = fma(mr[p], mr[q], fma(mi[p], mi[q], acc[v]));
-            acc[v + 1] = fma(mr[p], mi[q], fma(-mi[p], mr[q], acc[v + 1]));
-          }
-          v += 2;
+        for (int q = 0; q < KH; ++q) {
+          const double4 u = su[h * KH + q];
+          const double dy = ey - u.y;
+          xl::coef_fast(fma(dy, dy, u.x), valid ? u.z : 0.0, c4, mr[w][q], mi[w][q]);
         }
       }
 #pragma unroll
-      for (int p = 0; p < KH; ++p) {
+      for (int w = 0; w < UNR; ++w) {
+        double tr[KH], ti[KH];
 #pragma unroll
-        for (int dd = 0; dd < ND; ++dd) {
-          const int q = (p + 2 * dd) % KH;
-          acc[v] = fma(mr[p], tr[q], fma(mi[p], ti[q], acc[v]));
-          acc[v + 1] = fma(mr[p], ti[q], fma(-mi[p], tr[q], acc[v + 1]));
-          v += 2;
+        for (int q = 0; q < KH; ++q) {
+          const double sr = h ? mr[w][q] : mr[w][(q + 1) % KH];
+          const double si = h ? mi[w][q] : mi[w][(q + 1) % KH];
+          tr[q] = __shfl_xor_sync(0xffffffffu, sr, 1);
+          ti[q] = __shfl_xor_sync(0xffffffffu, si, 1);
+        }
+        int v = 0;
+#pragma unroll
+        for (int p = 0; p < KH; ++p) {
+#pragma unroll
+          for (int q = p; q < KH; ++q) {
+            if (p == q) {
+              acc[v] = fma(mr[w][p], mr[w][p], fma(mi[w][p], mi[w][p], acc[v]));
+            } else {
+              acc[v] = fma(mr[w][p], mr[w][q], fma(mi[w][p], mi[w][q], acc[v]));
+              acc[v + 1] = fma(mr[w][p], mi[w][q], fma(-mi[w][p], mr[w][q], acc[v + 1]));
+            }
+            v += 2;
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < KH; ++p) {
+#pragma unroll
+          for (int dd = 0; dd < ND; ++dd) {
+            const int q = (p + 2 * dd) % KH;
+            acc[v] = fma(mr[w][p], tr[q], fma(mi[w][p], ti[q], acc[v]));
+            acc[v + 1] = fma(mr[w][p], ti[q], fma(-mi[w][p], tr[q], acc[v + 1]));
+            v += 2;
+          }
         }
       }
     }
@@ -897,10 +903,14 @@ KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
   if (env_k && !strcmp(env_k, "split") && split_ok) c.which = 1;
   if (env_k && !strcmp(env_k, "mma") && mma_ok) c.which = 2;
   if (env_k && !strcmp(env_k, "legacy")) c.which = 0;
-  c.nt = 256;
+  // split variants (XLMIMO_GRAM_NT selects; "nt" is a variant id, threads in kSplitThreads)
+  // split default: variant 192 = 128 threads x 3 blocks/SM, two elements per iteration
+  // (19.45 ms vs 19.77 for 256 x 2 on cfg2, B200)
+  c.nt = (c.which == 1 && K == 8) ? 192 : 256;
   if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = env_nt;
   if (c.which == 2) c.nt = mma_nt(K <= 8 ? 1 : 2);
-  c.parts = (c.which == 1 || c.which == 2) ? c.nt / 32 : 1;
+  const int threads = (c.which == 1 && (c.nt == 64)) ? 256 : (c.which == 1 && c.nt == 192) ? 128 : c.nt;
+  c.parts = (c.which == 1 || c.which == 2) ? threads / 32 : 1;
   return c;
 }
 
@@ -1095,9 +1105,9 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   } else if (kc.which == 1) {
     if (K == 8) {
       switch (kc.nt) {
-        case 64: gram_split_kernel<4, 64, 8><<<(unsigned)n_blocks, 64, 0, s>>>(P); break;
+        case 64: gram_split_kernel<4, 256, 1, 2><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
         case 128: gram_split_kernel<4, 128, 4><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;
-        case 192: gram_split_kernel<4, 192, 2><<<(unsigned)n_blocks, 192, 0, s>>>(P); break;
+        case 192: gram_split_kernel<4, 128, 3, 2><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;
         default: gram_split_kernel<4, 256, 2><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
       }
     } else {
