@@ -39,9 +39,11 @@ if ROOT not in sys.path:
 from workloads import CONFIGS, cmac_per_drop  # noqa: E402
 
 W = CONFIGS[2]
-# Fixed FP64-pipe work model per channel coefficient ("Roofline"): distance^2 2,
-# 1/r 5, r 1, quarter-cycle range reduction 4, sin+cos minimax 13, r^{-3/2} 7, phasor 2.
-FP64_OPS_PER_COEF = 34
+# FP64-pipe work model per channel coefficient ("Roofline"): the cheapest fp64
+# evaluation found (coef_fast): distance^2 2, 1/r 5, r 1, quarter-cycle reduction 3,
+# sin+cos minimax 12, r^{-3/2} 6, phasor 2 (MUFU seeds and the quadrant F2I are off the
+# FP64 pipe).  With this model frac ~ the FP64 pipe utilisation against the nominal peak.
+FP64_OPS_PER_COEF = 31
 
 
 def parse():

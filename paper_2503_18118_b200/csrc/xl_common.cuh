@@ -268,6 +268,9 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
 bool stream_tc_supported(int K, int64_t N);
 int stream_tc_chunks(int64_t N);
 int stream_tc_parts(int K);
+bool fused_tc_supported(const ArrayP &a, int K);
+int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                    cudaStream_t s);
 int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s);
 
 // xl_closed.cu : out[drop][lvl][K][K][2] for M = n_list[lvl]

@@ -945,6 +945,13 @@ bool materialised_use_tc(int K, int64_t N) {
 // Materialised mode: drops per batch so that the planar complex64 H of a batch
 // fits an 8 GiB slice of the workspace (cfg5: 16 drops of 512 MiB; cfg3: 4096), so
 // one persistent streaming launch has >= ~14 waves of work items.
+// fused fp32 exact Gram on tcgen05 (generate -> TF32 smem tiles -> TMEM), single level only
+bool use_fused_tc(const ArrayP &a, int K, int precision, int n_lvl) {
+  static const char *e = getenv("XLMIMO_GRAM_KERNEL");
+  if (e && !strcmp(e, "legacy")) return false;
+  return precision == XLMIMO_FP32 && n_lvl == 1 && fused_tc_supported(a, K);
+}
+
 // elements per drop as stored: the tiled32 (tcgen05) layout pads N to whole groups of 4 tiles
 int64_t mat_npad(int K, int64_t N) { return materialised_use_tc(K, N) ? (N + 127) / 128 * 128 : N; }
 
@@ -964,6 +971,7 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
+  if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
 }
@@ -1059,6 +1067,23 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   const size_t need = gram_ws_bytes(a, K, n_drops, n_lvl, precision, mode);
   if (ws_bytes < need || (need && !ws))
     return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+  if (use_fused_tc(a, K, precision, n_lvl)) {
+    int rc;
+    {
+      KTimer tm(s, "gram_fused_tc_tf32");
+      rc = launch_fused_tc(a, pos, K, n_drops, N, (double *)ws, s);
+      tm.stop(s);
+      count_launch();
+    }
+    if (rc) return rc;
+    const int64_t n_items = n_drops * (int64_t)K * (K + 1) / 2;
+    KTimer tr(s, "gram_reduce");
+    gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops,
+                                                                        stream_tc_chunks(N), 1, 1, out);
+    tr.stop(s);
+    count_launch();
+    return check_launch("gram_reduce_kernel");
+  }
   GramParams P;
   memset(&P, 0, sizeof(P));
   P.pos = pos;

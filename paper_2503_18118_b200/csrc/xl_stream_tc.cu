@@ -284,6 +284,243 @@ __global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __gri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused fp32 path (XLMIMO_FP32, XLMIMO_FUSED, K >= 9): the same tcgen05 TF32
+// Gram, but the operand tiles are GENERATED into the swizzled shared-memory ring
+// by 4 generator warps instead of being loaded by TMA -- H never touches HBM.
+// Generator task = (user u, 4 consecutive elements): the fp64 anchor at the first
+// element (distance, 1/r, phase reduced as frac(r/lambda) in fp64, north_star),
+// then for the 4 elements an fp32 delta: Delta(r^2) = dd (2 dy + dd),
+// delta = Delta / r_c^2, Delta r = r_c delta (1/2 - delta/8 + delta^2/16),
+// phase = frac_c + Delta r / lambda (fp32, re-reduced), sin/cos by MUFU,
+// amplitude a_c (1 + delta)^{-3/4} ~ a_c (1 - 3/4 delta + 21/32 delta^2); each
+// row chunk of 4 TF32 (RNA) values is one 16-byte store.  Elements are taken in
+// natural spatial order (the sum is order-free; no nested levels on this path).
+struct FusedParams {
+  const double *pos;
+  double *ws;        // partials [drop][chunk][NP][2]
+  int K, kind;
+  int64_t n_y, n_z, N;
+  double lambda, pitch, sqrt_beta0;
+  int n_mma;
+  int n_chunks;
+  int64_t n_drops;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// byte offset of the 16-B chunk c (0..7) of row r in a SWIZZLE_128B K-major tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+constexpr int kGenWarps = 1;       // warps per generator group (arrivals per full barrier)
+constexpr int kGenGroups = 12;     // groups take stages round-robin (stage k -> group k % 12)
+constexpr int kGenThreads = 32 * kGenWarps;
+constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 12: warps 12..15 = TMEM lane quadrants 0..3
+constexpr int kMmaWarp = kEpiWarp0 + 4;            // 16
+constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 544
+
+__global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *stages = base;
+  uint64_t *full = (uint64_t *)(base + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
+  double4 *su_all = (double4 *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][64]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = P.K, R = 2 * K;
+  const int64_t n_items = P.n_drops * P.n_chunks;
+  for (int i = tid; i < kStages * kStageBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kGenWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_sh;
+  const int kb_per_chunk = kChunk / kBoxK;
+
+  if (warp < kEpiWarp0) {  // ---------------- generators: warp g owns ring slot g
+    // kStages == kGenGroups: the global stage sequence k (same order as the MMA issuer)
+    // maps to slot k % 12, so generator warp g handles exactly the stages k = g (mod 12),
+    // always in slot g, with phase (k / 12) & 1.
+    const int grp = warp;
+    double4 *su = su_all + grp * 64;
+    const double inv_lambda = 1.0 / P.lambda;
+    const float inv_lambda_f = (float)inv_lambda;
+    const float pitch_f = (float)P.pitch;
+    const int n_tasks = K * 8;
+    const uint32_t slot_base = smem_u32(stages + grp * kStageBytes);
+    int64_t kstart = 0;  // global index of the item's first stage
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t d = it / P.n_chunks;
+      const int c = (int)(it - d * P.n_chunks);
+      const int64_t x0 = (int64_t)c * kChunk;
+      const int64_t rem = P.N - x0;
+      const int ns = (int)(((rem < kChunk ? rem : kChunk) + kBoxK - 1) / kBoxK);
+      int64_t k = kstart + (((int64_t)grp - kstart) % kGenGroups + kGenGroups) % kGenGroups;
+      kstart += ns;
+      if (k >= kstart) continue;  // no stage of this item for this warp
+      __syncwarp();
+      for (int u = lane; u < K; u += 32) {
+        const double *p = P.pos + (d * K + u) * 3;
+        const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
+        su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+      }
+      __syncwarp();
+      for (; k < kstart; k += kGenGroups) {
+        const int64_t xs = x0 + (k - (kstart - ns)) * kBoxK;
+        mbar_wait(&empty[grp], ((uint32_t)(k / kGenGroups) & 1) ^ 1);
+#pragma unroll 2
+        for (int task = lane; task < n_tasks; task += 32) {
+          const int u = task >> 3, g4 = task & 7;
+          const int64_t t0 = xs + 4 * g4;
+          const double4 uc = su[u];
+          // fp64 anchor at element t0 (natural order: ULA y = (t - (N-1)/2) pitch; UPA t = q n_y + p)
+          double ey, ez = 0.0;
+          if (P.kind == XLMIMO_ULA) {
+            ey = ((double)t0 - 0.5 * (double)(P.N - 1)) * P.pitch;
+          } else {
+            const int64_t q = t0 / P.n_y, pp = t0 - q * P.n_y;
+            ey = ((double)pp - 0.5 * (double)(P.n_y - 1)) * P.pitch;
+            ez = ((double)q - 0.5 * (double)(P.n_z - 1)) * P.pitch;
+          }
+          const double dy = ey - uc.y, dz = ez - uc.z;
+          const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
+          const double ir = xl::rsqrt_nr(r2);
+          const double rc = r2 * ir;
+          const double qc = rc * inv_lambda;
+          const float fc = (float)(qc - rint(qc));
+          const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
+          const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
+          uint32_t vr[4], vi[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const float dd = (float)m * pitch_f;
+            const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
+            const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
+            float cyc = fmaf(dr, inv_lambda_f, fc);
+            cyc -= rintf(cyc);
+            float sn, co;
+            __sincosf(6.28318530717958647692f * cyc, &sn, &co);
+            const float a = ((t0 + m) < P.N) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
+            vr[m] = tf32_rna(a * co);
+            vi[m] = tf32_rna(-a * sn);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(2 * u, g4)),
+                       "r"(vr[0]), "r"(vr[1]), "r"(vr[2]), "r"(vr[3])
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(2 * u + 1, g4)),
+                       "r"(vi[0]), "r"(vi[1]), "r"(vi[2]), "r"(vi[3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[grp]);
+      }
+    }
+  } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = tf32_idesc(kRows, P.n_mma);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+        const int64_t d = it / P.n_chunks;
+        const int c = (int)(it - d * P.n_chunks);
+        const int64_t x0 = (int64_t)c * kChunk;
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
+        for (int kb = 0; kb < kb_per_chunk; ++kb) {
+          if (x0 + (int64_t)kb * kBoxK >= P.N) break;
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stages + stage * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < kBoxK / 8; ++k) {
+            const uint64_t desc = sw128_desc(sa + 32 * k);
+            mma_tf32(tmem_d, desc, desc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue, warps 12..15 = TMEM lane quadrants 0..3
+    const int q = warp - kEpiWarp0;
+    const int row = 32 * q + lane;
+    const int i = row >> 1, plane = row & 1;
+    const int NP = K * (K + 1) / 2;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      const int64_t d = it / P.n_chunks;
+      const int c = (int)(it - d * P.n_chunks);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double *out = P.ws + ((size_t)d * P.n_chunks + c) * (size_t)(2 * NP);
+      if (32 * q < R) {
+        for (int cb = 0; cb < (R + 31) / 32; ++cb) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + 32 * cb), v);
+          float x[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int jj = plane * 8 + h;
+            const int j = 16 * cb + jj;
+            float rr, rr2, ri, ir;
+            if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
+            else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
+            if (i < K && j < K && j >= i) {
+              const int p = i * K - i * (i - 1) / 2 + (j - i);
+              out[2 * p] = (double)rr + (double)rr2;
+              out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -303,6 +540,41 @@ namespace xlh {
 bool stream_tc_supported(int K, int64_t N) { return K >= 9 && K <= 64 && (N % 4) == 0 && N >= kBoxK; }
 
 int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
+
+bool fused_tc_supported(const ArrayP &a, int K) {
+  return K >= 9 && K <= 64 && (a.kind == XLMIMO_ULA || (a.n_y % 4) == 0);
+}
+
+// Fused fp32 Gram on tcgen05: partials [drop][chunk][NP][2] into ws (stream_tc_chunks(N) per drop).
+int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                    cudaStream_t s) {
+  FusedParams P;
+  P.pos = pos;
+  P.ws = ws;
+  P.K = K;
+  P.kind = a.kind;
+  P.n_y = a.n_y;
+  P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+  P.N = N;
+  P.lambda = a.lambda;
+  P.pitch = a.pitch;
+  P.sqrt_beta0 = a.sqrt_beta0;
+  P.n_mma = (2 * K + 15) / 16 * 16;
+  P.n_chunks = stream_tc_chunks(N);
+  P.n_drops = n_drops;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * P.n_mma)) cols <<= 1;
+  P.tmem_cols = cols;
+  const size_t smem = 1024 + (size_t)kStages * kStageBytes + (2 * kStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
+  cudaFuncSetAttribute(gram_fused_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = n_drops * P.n_chunks;
+  const int grid = (int)(items < sms ? items : sms);
+  gram_fused_tc_kernel<<<grid, kFusedThreads, smem, s>>>(P);
+  return check_launch("gram_fused_tc_kernel");
+}
 
 // element blocks stacked per stage: 2K <= 32 -> 4, <= 64 -> 2, else 1
 static int rows_per_block(int K) { return 2 * K <= 32 ? 32 : 2 * K <= 64 ? 64 : 128; }

@@ -46,7 +46,7 @@ def main(cfgs):
         pos = xl.gen_drops(xl.Users.polar(w.r, w.az, w.el), w.K, D, seed=w.seed)
         N, K = w.N, w.K
         coef = N * K * D
-        ops = D * N * (K * 34 + 4 * K * (K - 1) // 2 + 2 * K)
+        ops = D * N * (K * 31 + 4 * K * (K - 1) // 2 + 2 * K)  # bench.py FP64_OPS_PER_COEF model
         cmac = D * N * K * (K + 1) // 2
         res = {"cfg": c, "workload": w.name, "drops_timed": D, "drops_config": w.n_drops}
         t = timed(lambda: xl.gram_exact(arr, pos, precision=xl.FP64))
