@@ -31,6 +31,9 @@ constexpr int kStageBytes = kRows * kBoxK * 4;  // 16 KiB
 constexpr int kChunk = 8192;           // elements accumulated in TMEM per partial
 constexpr int kThreads = 256;
 
+// element blocks stacked per stage in the 128 MMA rows: 2K <= 32 -> 4 blocks, <= 64 -> 2, else 1
+int rows_per_block(int K) { return 2 * K <= 32 ? 32 : 2 * K <= 64 ? 64 : 128; }
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
@@ -302,6 +305,7 @@ struct FusedParams {
   int K, kind;
   int64_t n_y, n_z, N;
   double lambda, pitch, sqrt_beta0;
+  int rb, nblk;      // rows per element block, blocks stacked per stage (as StreamParams)
   int n_mma;
   int n_chunks;
   int64_t n_drops;
@@ -317,20 +321,22 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 // byte offset of the 16-B chunk c (0..7) of row r in a SWIZZLE_128B K-major tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-constexpr int kGenWarps = 1;       // warps per generator group (arrivals per full barrier)
-constexpr int kGenGroups = 12;     // groups take stages round-robin (stage k -> group k % 12)
+constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
+constexpr int kGenGroups = 8;      // group g owns ring slot g (stage k -> slot k % 8)
+constexpr int kFStages = kGenGroups;
 constexpr int kGenThreads = 32 * kGenWarps;
-constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 12: warps 12..15 = TMEM lane quadrants 0..3
-constexpr int kMmaWarp = kEpiWarp0 + 4;            // 16
-constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 544
+constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
+constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
+constexpr int kMmaWarp = kEpiWarp0 + 4;            // 20
+constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 672
 
 __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *stages = base;
-  uint64_t *full = (uint64_t *)(base + kStages * kStageBytes);
-  uint64_t *empty = full + kStages;
-  uint64_t *tfull = empty + kStages;
+  uint64_t *full = (uint64_t *)(base + kFStages * kStageBytes);
+  uint64_t *empty = full + kFStages;
+  uint64_t *tfull = empty + kFStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
   double4 *su_all = (double4 *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][64]
@@ -338,9 +344,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = P.K, R = 2 * K;
   const int64_t n_items = P.n_drops * P.n_chunks;
-  for (int i = tid; i < kStages * kStageBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < kFStages * kStageBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kFStages; ++s) {
       mbar_init(&full[s], kGenWarps);
       mbar_init(&empty[s], 1);
     }
@@ -361,18 +367,21 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
-  const int kb_per_chunk = kChunk / kBoxK;
+  const int kb_per_chunk = kChunk / (kBoxK * P.nblk);
 
   if (warp < kEpiWarp0) {  // ---------------- generators: warp g owns ring slot g
-    // kStages == kGenGroups: the global stage sequence k (same order as the MMA issuer)
+    // kFStages == kGenGroups: the global stage sequence k (same order as the MMA issuer)
     // maps to slot k % 12, so generator warp g handles exactly the stages k = g (mod 12),
     // always in slot g, with phase (k / 12) & 1.
-    const int grp = warp;
+    const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
     double4 *su = su_all + grp * 64;
     const double inv_lambda = 1.0 / P.lambda;
     const float inv_lambda_f = (float)inv_lambda;
     const float pitch_f = (float)P.pitch;
-    const int n_tasks = K * 8;
+    // element blocks stacked in the 128 rows (as in the stream kernel): block b of a
+    // stage covers elements xs + 32 b .. + 31 in rows rb*b .. rb*b + 2K - 1
+    const int n_tasks = P.nblk * K * (kBoxK / kTaskE);
+    const int tpb = K * (kBoxK / kTaskE);  // tasks per block
     const uint32_t slot_base = smem_u32(stages + grp * kStageBytes);
     int64_t kstart = 0;  // global index of the item's first stage
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -380,24 +389,26 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int c = (int)(it - d * P.n_chunks);
       const int64_t x0 = (int64_t)c * kChunk;
       const int64_t rem = P.N - x0;
-      const int ns = (int)(((rem < kChunk ? rem : kChunk) + kBoxK - 1) / kBoxK);
+      const int spb = kBoxK * P.nblk;  // elements per stage
+      const int ns = (int)(((rem < kChunk ? rem : kChunk) + spb - 1) / spb);
       int64_t k = kstart + (((int64_t)grp - kstart) % kGenGroups + kGenGroups) % kGenGroups;
       kstart += ns;
-      if (k >= kstart) continue;  // no stage of this item for this warp
-      __syncwarp();
-      for (int u = lane; u < K; u += 32) {
+      if (k >= kstart) continue;  // no stage of this item for this group
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
+      for (int u = gtid; u < K; u += kGenThreads) {
         const double *p = P.pos + (d * K + u) * 3;
         const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
         su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
       }
-      __syncwarp();
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
       for (; k < kstart; k += kGenGroups) {
-        const int64_t xs = x0 + (k - (kstart - ns)) * kBoxK;
+        const int64_t xs = x0 + (k - (kstart - ns)) * spb;
         mbar_wait(&empty[grp], ((uint32_t)(k / kGenGroups) & 1) ^ 1);
-#pragma unroll 2
-        for (int task = lane; task < n_tasks; task += 32) {
-          const int u = task >> 3, g4 = task & 7;
-          const int64_t t0 = xs + 4 * g4;
+        for (int task = gtid; task < n_tasks; task += kGenThreads) {
+          const int blk = task / tpb, tb = task - blk * tpb;
+          const int u = tb / (kBoxK / kTaskE), g8 = tb % (kBoxK / kTaskE);
+          const int row0 = blk * P.rb + 2 * u;
+          const int64_t t0 = xs + kBoxK * blk + kTaskE * g8;
           const double4 uc = su[u];
           // fp64 anchor at element t0 (natural order: ULA y = (t - (N-1)/2) pitch; UPA t = q n_y + p)
           double ey, ez = 0.0;
@@ -416,9 +427,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
           const float fc = (float)(qc - rint(qc));
           const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
           const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
-          uint32_t vr[4], vi[4];
+          uint32_t vr[kTaskE], vi[kTaskE];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
+          for (int m = 0; m < kTaskE; ++m) {
             const float dd = (float)m * pitch_f;
             const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
             const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
@@ -430,16 +441,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
             vr[m] = tf32_rna(a * co);
             vi[m] = tf32_rna(-a * sn);
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(2 * u, g4)),
-                       "r"(vr[0]), "r"(vr[1]), "r"(vr[2]), "r"(vr[3])
-                       : "memory");
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(2 * u + 1, g4)),
-                       "r"(vi[0]), "r"(vi[1]), "r"(vi[2]), "r"(vi[3])
-                       : "memory");
+#pragma unroll
+          for (int h = 0; h < kTaskE / 4; ++h) {
+            const int chunk = (kTaskE / 4) * g8 + h;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0, chunk)),
+                         "r"(vr[4 * h]), "r"(vr[4 * h + 1]), "r"(vr[4 * h + 2]), "r"(vr[4 * h + 3])
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0 + 1, chunk)),
+                         "r"(vi[4 * h]), "r"(vi[4 * h + 1]), "r"(vi[4 * h + 2]), "r"(vi[4 * h + 3])
+                         : "memory");
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[grp]);
+        if (lane == 0) mbar_arrive(&full[grp]);  // kGenWarps arrivals complete the stage
       }
     }
   } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
@@ -458,7 +473,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
         for (int kb = 0; kb < kb_per_chunk; ++kb) {
-          if (x0 + (int64_t)kb * kBoxK >= P.N) break;
+          if (x0 + (int64_t)kb * kBoxK * P.nblk >= P.N) break;
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(stages + stage * kStageBytes);
@@ -468,15 +483,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
             mma_tf32(tmem_d, desc, desc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == kFStages) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
       }
     }
-  } else {  // ---------------- epilogue, warps 12..15 = TMEM lane quadrants 0..3
+  } else {  // ---------------- epilogue, warps kEpiWarp0..+3 = TMEM lane quadrants 0..3
     const int q = warp - kEpiWarp0;
     const int row = 32 * q + lane;
-    const int i = row >> 1, plane = row & 1;
+    const int blk = (32 * q) / P.rb;
+    const int lr = row - blk * P.rb;
+    const int i = lr >> 1, plane = lr & 1;
+    const int col0 = blk * P.rb;
+    const bool has_users = 32 * q - blk * P.rb < R;
     const int NP = K * (K + 1) / 2;
     int local = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
@@ -486,11 +505,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      double *out = P.ws + ((size_t)d * P.n_chunks + c) * (size_t)(2 * NP);
-      if (32 * q < R) {
+      double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
+      if (has_users) {
         for (int cb = 0; cb < (R + 31) / 32; ++cb) {
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + 32 * cb), v);
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + col0 + 32 * cb), v);
           float x[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
@@ -559,13 +578,15 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   P.lambda = a.lambda;
   P.pitch = a.pitch;
   P.sqrt_beta0 = a.sqrt_beta0;
-  P.n_mma = (2 * K + 15) / 16 * 16;
+  P.rb = rows_per_block(K);
+  P.nblk = kRows / P.rb;
+  P.n_mma = P.nblk > 1 ? kRows : (2 * K + 15) / 16 * 16;
   P.n_chunks = stream_tc_chunks(N);
   P.n_drops = n_drops;
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * P.n_mma)) cols <<= 1;
   P.tmem_cols = cols;
-  const size_t smem = 1024 + (size_t)kStages * kStageBytes + (2 * kStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
+  const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
   cudaFuncSetAttribute(gram_fused_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -576,8 +597,6 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   return check_launch("gram_fused_tc_kernel");
 }
 
-// element blocks stacked per stage: 2K <= 32 -> 4, <= 64 -> 2, else 1
-static int rows_per_block(int K) { return 2 * K <= 32 ? 32 : 2 * K <= 64 ? 64 : 128; }
 int stream_tc_parts(int K) { return kRows / rows_per_block(K); }
 
 // One batch: H in the tiled32 layout [nb][N/32][2K][32] fp32 (TF32-rounded, N a
