@@ -275,6 +275,40 @@ def test_sweep_full_cfg2_properties_and_sampled_drops(xl, orc):
     assert np.array_equal(rh["ergodic"], res["ergodic"]) and np.array_equal(rh["sat"], res["sat"])
 
 
+def test_sweep_fp32_parity(xl, orc):
+    """The fp32 sweep (fp32 phasors, fp64 accumulation) vs the fp64 oracle: rates within the
+    fp32 tolerance 1e-3 bits/s/Hz (north_star)."""
+    w = CONFIGS[2]
+    D = 24
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ao = orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, D, w.snr_db, w.receivers, users=ug, seed=3, precision=xl.FP32,
+                              per_drop=True)
+    pos = xl.gen_drops(ug, w.K, D, seed=3).cpu().numpy()
+    _, nv, sat, pd = orc.saturation_sweep(ao, w.n_list, pos, w.snr_db, w.receivers, per_drop=True)
+    assert np.max(np.abs(res["per_drop"].cpu().numpy() - pd)) <= 1e-3
+    assert np.array_equal(res["n_valid"], nv) and res["sat"][2] == sat[2]
+
+
+@pytest.mark.parametrize("K,N,prec,mode", [(8, 1000, "fp64", "fused"), (16, 2048, "fp64", "fused"),
+                                           (33, 1500, "fp64", "fused"), (16, 4096, "fp32", "fused"),
+                                           (40, 1024, "fp32", "fused"), (16, 4096, "fp32", "mat"),
+                                           (5, 1001, "fp32", "mat")])
+def test_determinism_all_paths(xl, K, N, prec, mode):
+    """T3: identical inputs give bitwise-identical outputs on every path (fixed reduction
+    orders, static work assignment in the persistent tensor-core kernels, no float atomics)."""
+    a = xl.Array.ula(N, 100e9)
+    pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60.0, 60.0)), K, 7, seed=K)
+    kw = dict(precision=xl.FP64 if prec == "fp64" else xl.FP32, mode=xl.MATERIALIZED if mode == "mat" else xl.FUSED)
+    g1 = xl.gram_exact(a, pos, **kw)
+    g2 = xl.gram_exact(a, pos, **kw)
+    assert torch.equal(g1, g2)
+    r1, f1 = xl.sum_rate(g1, [0.0, 10.0], 15)
+    r2, f2 = xl.sum_rate(g2, [0.0, 10.0], 15)
+    assert torch.equal(r1.view(torch.int64), r2.view(torch.int64)) and torch.equal(f1, f2)
+
+
 def test_launch_counter_moves(xl):
     n0 = xl.launch_count()
     xl.gen_drops(xl.Users.polar((5, 50), (-60, 60)), 4, 8)
