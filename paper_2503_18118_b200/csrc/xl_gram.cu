@@ -52,7 +52,16 @@ __device__ __forceinline__ ElemPos element_pos(const GramParams &P, int64_t t) {
     e.y = xl::ula_y_centred(t, (P.N & 1) != 0, P.pitch);
     e.z = 0.0;
   } else {
-    const int64_t q = t / P.n_y, p = t - q * P.n_y;
+    int64_t q, p;
+    if (P.N < ((int64_t)1 << 31)) {  // 32-bit division (no 64-bit division subroutine)
+      const uint32_t tt = (uint32_t)t, ny = (uint32_t)P.n_y;
+      const uint32_t q32 = tt / ny;
+      q = q32;
+      p = tt - q32 * ny;
+    } else {
+      q = t / P.n_y;
+      p = t - q * P.n_y;
+    }
     e.y = ((double)p - 0.5 * (double)(P.n_y - 1)) * P.pitch;
     e.z = ((double)q - 0.5 * (double)(P.n_z - 1)) * P.pitch;
   }
@@ -262,18 +271,39 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
     double acc[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-    for (int64_t t0 = a; t0 < b; t0 += NSLOT * UNR) {  // warp-uniform trip count (shuffles below)
+    // Even N: the centred order puts index t at y = +-(t/2 + 1/2) pitch with the sign set
+    // by t's parity, which is fixed per thread (NSLOT is even), so y is one FMA of an
+    // exactly incremented pair index: fma(p, +-pitch, +-pitch/2) == ((p + 1/2) pitch)
+    // rounded once, bitwise what ula_y_centred gives.
+    const int64_t ta = a + eslot;
+    const double sgn = (ta & 1) ? -1.0 : 1.0;
+    const double sp = sgn * P.pitch, sh = 0.5 * sgn * P.pitch;
+    double pd = (double)(ta >> 1);
+    for (int64_t t0 = a; t0 < b; t0 += NSLOT * UNR, pd += (double)(NSLOT * UNR / 2)) {  // warp-uniform trips
       double mr[UNR][KH], mi[UNR][KH];
+      if (!n_odd && t0 + NSLOT * UNR <= b) {  // full iteration: no masking (uniform branch)
 #pragma unroll
-      for (int w = 0; w < UNR; ++w) {
-        const int64_t t = t0 + w * NSLOT + eslot;
-        const bool valid = t < b;
-        const double ey = xl::ula_y_centred(valid ? t : a, n_odd, P.pitch);
+        for (int w = 0; w < UNR; ++w) {
+          const double ey = fma(pd + (double)(w * NSLOT / 2), sp, sh);
 #pragma unroll
-        for (int q = 0; q < KH; ++q) {
-          const double4 u = su[h * KH + q];
-          const double dy = ey - u.y;
-          xl::coef_fast(fma(dy, dy, u.x), valid ? u.z : 0.0, c4, mr[w][q], mi[w][q]);
+          for (int q = 0; q < KH; ++q) {
+            const double4 u = su[h * KH + q];
+            const double dy = ey - u.y;
+            xl::coef_fast(fma(dy, dy, u.x), u.z, c4, mr[w][q], mi[w][q]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < UNR; ++w) {
+          const int64_t t = t0 + w * NSLOT + eslot;
+          const bool valid = t < b;
+          const double ey = xl::ula_y_centred(valid ? t : a, n_odd, P.pitch);
+#pragma unroll
+          for (int q = 0; q < KH; ++q) {
+            const double4 u = su[h * KH + q];
+            const double dy = ey - u.y;
+            xl::coef_fast(fma(dy, dy, u.x), valid ? u.z : 0.0, c4, mr[w][q], mi[w][q]);
+          }
         }
       }
 #pragma unroll
@@ -477,13 +507,18 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
 // one partial in the standard layout.
 constexpr int kMtMaxPairs = 8;  // group pairs per warp (G = 8: 36 pairs over 8 warps)
 struct MtPlan {
-  int npairs[8];
-  int g1[8][kMtMaxPairs], g2[8][kMtMaxPairs];
+  int npairs[16];
+  int g1[16][kMtMaxPairs], g2[16][kMtMaxPairs];
 };
 
-template <int G, int S>
-__global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, MtPlan plan) {
-  constexpr int NT = 256, NW = 8, NPAIR = G * (G + 1) / 2;
+// jobs per G: G <= 4 splits cross pairs into two half-jobs (see make_mt_plan)
+__host__ __device__ constexpr int mt_jobs(int G) { return G <= 4 ? G + G * (G - 1) : G * (G + 1) / 2; }
+__host__ __device__ constexpr int mt_maxp(int G, int NW) { return (mt_jobs(G) + NW - 1) / NW + 1; }
+
+template <int G, int S, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) gram_mma_tiled_kernel(GramParams P, MtPlan plan) {
+  constexpr int NT = 32 * NW, NPAIR = G * (G + 1) / 2;
+  constexpr bool HALVE = G <= 4;
   extern __shared__ __align__(16) double dsm[];
   double *fre = dsm;                  // [S][G][32]
   double *fim = dsm + S * G * 32;     // [S][G][32]
@@ -503,7 +538,7 @@ __global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, Mt
       su[u] = make_double4(1.0, 0.0, 0.0, 0.0);
     }
   }
-  constexpr int MAXP = (NPAIR + 7) / 8 + 1;  // bound used by make_mt_plan
+  constexpr int MAXP = mt_maxp(G, NW);  // bound used by make_mt_plan
   const int np = plan.npairs[warp];
   int pg1[MAXP], pg2[MAXP];
 #pragma unroll
@@ -552,13 +587,18 @@ __global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, Mt
 #pragma unroll
         for (int k = 0; k < MAXP; ++k) {
           if (k < np) {
-            const int g1 = pg1[k], g2 = pg2[k];
+            // part: 0 all, 1 RR+II, 2 RI+IR (compile-time 0 unless HALVE)
+            const int g1 = pg1[k], g2 = pg2[k] & 255, part = HALVE ? (pg2[k] >> 8) : 0;
             const double ar = fre[(s * G + g1) * 32 + lane], ai = fim[(s * G + g1) * 32 + lane];
             const double br = fre[(s * G + g2) * 32 + lane], bi = fim[(s * G + g2) * 32 + lane];
-            dmma(acc[k][0], ar, br);
-            dmma(acc[k][1], ai, bi);
-            dmma(acc[k][2], ar, bi);
-            if (g1 != g2) dmma(acc[k][3], ai, br);
+            if (part != 2) {
+              dmma(acc[k][0], ar, br);
+              dmma(acc[k][1], ai, bi);
+            }
+            if (part != 1) {
+              dmma(acc[k][2], ar, bi);
+              if (g1 != g2) dmma(acc[k][3], ai, br);
+            }
           }
         }
       }
@@ -568,10 +608,11 @@ __global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, Mt
 #pragma unroll
     for (int k = 0; k < MAXP; ++k) {
       if (k < np) {
-        const int g1 = pg1[k], g2 = pg2[k];
-        const int p =g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
+        const int g1 = pg1[k], g2 = pg2[k] & 255, part = HALVE ? (pg2[k] >> 8) : 0;
+        const int p = g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
+          if ((m < 2 && part == 2) || (m >= 2 && part == 1)) continue;  // the other half-job's slots
           stage[((p * 4 + m) * 8 + ulocal) * 8 + 2 * elocal] = acc[k][m][0];
           stage[((p * 4 + m) * 8 + ulocal) * 8 + 2 * elocal + 1] = acc[k][m][1];
         }
@@ -599,24 +640,37 @@ __global__ void __launch_bounds__(256, 1) gram_mma_tiled_kernel(GramParams P, Mt
 }
 
 // Balanced assignment of the G(G+1)/2 group pairs (row-major) to 8 warps by DMMA count.
-MtPlan make_mt_plan(int G) {
+MtPlan make_mt_plan(int G, int nw) {
   MtPlan pl;
   memset(&pl, 0, sizeof(pl));
-  const int maxp = (G * (G + 1) / 2 + 7) / 8 + 1;
-  // longest-processing-time greedy: cross pairs (4 DMMAs) first, then diagonal (3)
-  int load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int pass = 0; pass < 2; ++pass)
-    for (int g1 = 0; g1 < G; ++g1)
-      for (int g2 = g1; g2 < G; ++g2) {
-        if ((g1 == g2) != (pass == 1)) continue;
-        int w = -1;
-        for (int c = 0; c < 8; ++c)
-          if (pl.npairs[c] < maxp && (w < 0 || load[c] < load[w])) w = c;
-        pl.g1[w][pl.npairs[w]] = g1;
-        pl.g2[w][pl.npairs[w]] = g2;
-        ++pl.npairs[w];
-        load[w] += (g1 == g2) ? 3 : 4;
+  const int maxp = mt_maxp(G, nw);
+  // longest-processing-time greedy over jobs: diagonal pairs (3 DMMAs) and cross pairs
+  // (4 DMMAs, or for G <= 4 -- fewer pairs than warps can balance -- two half-jobs
+  // RR+II / RI+IR of 2 DMMAs each, encoded as g2 | part << 8).
+  int load[16] = {0};
+  const bool halve = G <= 4;
+  auto place = [&](int g1, int g2code, int cost) {
+    int w = -1;
+    for (int c = 0; c < nw; ++c)
+      if (pl.npairs[c] < maxp && (w < 0 || load[c] < load[w])) w = c;
+    pl.g1[w][pl.npairs[w]] = g1;
+    pl.g2[w][pl.npairs[w]] = g2code;
+    ++pl.npairs[w];
+    load[w] += cost;
+  };
+  if (halve)  // costliest first: diagonal (3) before the half-jobs (2)
+    for (int g = 0; g < G; ++g) place(g, g, 3);
+  for (int g1 = 0; g1 < G; ++g1)
+    for (int g2 = g1 + 1; g2 < G; ++g2) {
+      if (halve) {
+        place(g1, g2 | (1 << 8), 2);
+        place(g1, g2 | (2 << 8), 2);
+      } else {
+        place(g1, g2, 4);
       }
+    }
+  if (!halve)
+    for (int g = 0; g < G; ++g) place(g, g, 3);
   return pl;
 }
 
@@ -629,12 +683,14 @@ size_t mt_smem_bytes() {
   return tiles > stage ? tiles : stage;
 }
 
+// 16 warps for G >= 5 (more latency hiding, half the accumulators per warp), 8 below
 template <int G>
 void launch_mt(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
-  static const MtPlan plan = make_mt_plan(G);
+  constexpr int NW = 16;
+  static const MtPlan plan = make_mt_plan(G, NW);
   const size_t smem = mt_smem_bytes<G>();
-  cudaFuncSetAttribute(gram_mma_tiled_kernel<G, kMtS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  gram_mma_tiled_kernel<G, kMtS><<<(unsigned)n_blocks, 256, smem, s>>>(P, plan);
+  cudaFuncSetAttribute(gram_mma_tiled_kernel<G, kMtS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_mma_tiled_kernel<G, kMtS, NW><<<(unsigned)n_blocks, 32 * NW, smem, s>>>(P, plan);
 }
 
 // ------------------------------------------------------------------ kernel B
