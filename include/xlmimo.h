@@ -170,6 +170,31 @@ XLMIMO_API int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const i
                                  int32_t precision, double t, double *ergodic, int64_t *n_valid, double *sat,
                                  void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------- NEXT-1
+ * Effective ("mismatched") rate of the paper's modified ZF:
+ * the ZF equalizer of Eq. (21) built from the closed-form Gram G~,
+ * W = G~^{-1} H^H, applied to the TRUE channel y = H x + n (Eq. (1)).  With
+ * A = G~^{-1} G and noise covariance G~^{-1} G G~^{-1} / rho (G~ Hermitian):
+ *   SINR_i = |A_ii|^2 / (sum_{j!=i} |A_ij|^2 + [G~^{-1} G G~^{-1}]_ii / rho),
+ *   rate = sum_i log2(1 + SINR_i)   (reading R11; "worse ... at the beginning").
+ * gram (true G) and gram_model (G~): dev [n_drops][K][K][2]; snr_db host [n_snr] (<= 16);
+ * rates dev [n_drops][n_snr]; flags dev [n_drops] or NULL, OR-ed with
+ * XLMIMO_FLAG_MODEL_SINGULAR when G~ has an exactly zero pivot (rates NaN).  G~ is
+ * inverted by complex Gauss-Jordan with partial pivoting.  K <= 64. */
+enum { XLMIMO_FLAG_MODEL_SINGULAR = 32 };
+XLMIMO_API int xlmimo_sum_rate_mismatched(const double *gram, const double *gram_model, int32_t K, int64_t n_drops,
+                                          const double *snr_db, int32_t n_snr, double *rates, uint32_t *flags,
+                                          void *stream);
+
+/* ------------------------------------------------------------------------- NEXT-4
+ * Seeded drops from the paper's own user field: x ~ U[x_min,
+ * x_max] (0 < x_min <= x_max), y ~ U[y_min, y_max], z = 0 -- the rectangle on the right
+ * of the array behind Eq. (17) and Figs. norm_cap / Capacity_vs_number_of_ant.  Same
+ * Philox stream as xlmimo_gen_drops (word 0 -> x, word 1 -> y).  pos dev [n_drops][K][3].
+ * EINVAL: K < 1, n_drops < 0, x_min <= 0, x_min > x_max, y_min > y_max, pos NULL. */
+XLMIMO_API int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max, int32_t K,
+                                     int64_t n_drops, uint64_t seed, uint64_t first_drop, double *pos, void *stream);
+
 /* Thread-local text of the last non-zero return on this thread ("" if none). */
 XLMIMO_API const char *xlmimo_last_error(void);
 

@@ -83,6 +83,8 @@ def lib():
         L.or_corr_limit_eq8.argtypes = [d, d, d, d, d, P(d), P(d)]
         L.or_sum_rate.argtypes = [vp, i32, i64, vp, i32, u32, vp, vp]
         L.or_saturation_coords.argtypes = [vp, i32, i64, d, vp, vp]
+        L.or_sum_rate_mismatched.argtypes = [vp, vp, i32, i64, vp, i32, vp, vp]
+        L.or_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp]
         L.or_saturation_sweep.argtypes = [P(OrArray), vp, i32, vp, i32, i64, vp, i32, u32, i32, d,
                                           vp, vp, vp, vp, i32]
         _lib = L
@@ -194,6 +196,27 @@ def sum_rate(gram: np.ndarray, snr_db, receivers: int, flags_in=None):
     fl = np.zeros(D, dtype=np.uint32) if flags_in is None else np.array(flags_in, dtype=np.uint32)
     lib().or_sum_rate(_ptr(g), K, D, _ptr(snr), snr.size, receivers, _ptr(rates), _ptr(fl))
     return rates, fl
+
+
+def sum_rate_mismatched(gram: np.ndarray, gram_model: np.ndarray, snr_db):
+    """Effective rate of the modified-ZF equalizer G~^{-1} H^H on the true channel (NEXT-1).
+    Returns rates (D, S) and flags (D,) (bit 5: G~ singular)."""
+    g = np.ascontiguousarray(np.stack([gram.real, gram.imag], axis=-1), dtype=np.float64)
+    gm = np.ascontiguousarray(np.stack([gram_model.real, gram_model.imag], axis=-1), dtype=np.float64)
+    D, K = g.shape[0], g.shape[1]
+    snr = np.ascontiguousarray(np.atleast_1d(snr_db), dtype=np.float64)
+    rates = np.zeros((D, snr.size))
+    fl = np.zeros(D, dtype=np.uint32)
+    lib().or_sum_rate_mismatched(_ptr(g), _ptr(gm), K, D, _ptr(snr), snr.size, _ptr(rates), _ptr(fl))
+    return rates, fl
+
+
+def gen_drops_rect(x, y, K: int, n_drops: int, seed: int = 0, first_drop: int = 0) -> np.ndarray:
+    """The paper's rectangle user field x ~ U[x0, x1], y ~ U[y0, y1]."""
+    pos = np.zeros((n_drops, K, 3), dtype=np.float64)
+    lib().or_gen_drops_rect(float(x[0]), float(x[1]), float(y[0]), float(y[1]), K, n_drops, seed, first_drop,
+                            _ptr(pos))
+    return pos
 
 
 def saturation_coords(pos: np.ndarray, t: float):

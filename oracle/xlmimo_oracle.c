@@ -102,6 +102,25 @@ void or_gen_drops(const or_users_t *u, int32_t K, int64_t n_drops, uint64_t seed
     }
 }
 
+/* The paper's own user field: x ~ U[x_min, x_max],
+ * y ~ U[y_min, y_max] (a rectangle on the right of the y-axis), z = 0.  Same
+ * Philox stream as or_gen_drops: word 0 -> x, word 1 -> y. */
+void or_gen_drops_rect(double x_min, double x_max, double y_min, double y_max, int32_t K, int64_t n_drops,
+                       uint64_t seed, uint64_t first_drop, double *pos)
+{
+    for (int64_t d = 0; d < n_drops; ++d)
+        for (int32_t k = 0; k < K; ++k) {
+            uint64_t ctr[4] = {first_drop + (uint64_t)d, (uint64_t)k, 0, 0};
+            uint64_t key[2] = {seed, 0};
+            uint64_t w[4];
+            or_philox4x64_10(ctr, key, w);
+            double *p = pos + ((size_t)d * K + k) * 3;
+            p[0] = x_min + (x_max - x_min) * or_u01(w[0]);
+            p[1] = y_min + (y_max - y_min) * or_u01(w[1]);
+            p[2] = 0.0;
+        }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Geometry (R1, R5).                                                        */
 /* ------------------------------------------------------------------------ */
@@ -453,6 +472,118 @@ void or_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double *s
         if (flags) flags[d] = fl;
     }
     free(A); free(L); free(dinv); free(x);
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: effective rate of the "modified ZF": the ZF      */
+/* equalizer of Eq. (21) built from the closed-form Gram G~,   */
+/* W = G~^{-1} H^H, applied to the true channel y = H x + n (Eq. 1):          */
+/*   W y = A x + W n,  A = G~^{-1} G,  cov(W n) = sigma^2 G~^{-1} G G~^{-1},  */
+/*   SINR_i = |A_ii|^2 / (sum_{j!=i} |A_ij|^2 + [G~^{-1} G G~^{-1}]_ii / rho). */
+/* "worse performance ... at the beginning" is this rate below */
+/* saturation (reading R11).                                                  */
+/* ------------------------------------------------------------------------ */
+
+/* In-place complex Gauss-Jordan inverse with partial pivoting (plain loops).
+ * Returns 0, or -1 if a pivot is exactly zero (singular). */
+static int or_cinv(double *M, int K)
+{
+    int *perm = (int *)malloc(sizeof(int) * K);
+    for (int k = 0; k < K; ++k) {
+        int p = k;
+        double best = -1.0;
+        for (int i = k; i < K; ++i) {
+            const double v = hypot(M[(i * K + k) * 2], M[(i * K + k) * 2 + 1]);
+            if (v > best) { best = v; p = i; }
+        }
+        perm[k] = p;
+        if (!(best > 0.0)) { free(perm); return -1; }
+        if (p != k)
+            for (int j = 0; j < K; ++j)
+                for (int c = 0; c < 2; ++c) {
+                    const double t = M[(k * K + j) * 2 + c];
+                    M[(k * K + j) * 2 + c] = M[(p * K + j) * 2 + c];
+                    M[(p * K + j) * 2 + c] = t;
+                }
+        /* 1 / pivot */
+        const double pr = M[(k * K + k) * 2], pi = M[(k * K + k) * 2 + 1];
+        const double den = pr * pr + pi * pi;
+        const double ir = pr / den, ii = -pi / den;
+        M[(k * K + k) * 2] = 1.0;
+        M[(k * K + k) * 2 + 1] = 0.0;
+        for (int j = 0; j < K; ++j) { /* row k *= 1/pivot */
+            const double ar = M[(k * K + j) * 2], ai = M[(k * K + j) * 2 + 1];
+            M[(k * K + j) * 2] = ar * ir - ai * ii;
+            M[(k * K + j) * 2 + 1] = ar * ii + ai * ir;
+        }
+        for (int i = 0; i < K; ++i) {
+            if (i == k) continue;
+            const double fr = M[(i * K + k) * 2], fi = M[(i * K + k) * 2 + 1];
+            M[(i * K + k) * 2] = 0.0;
+            M[(i * K + k) * 2 + 1] = 0.0;
+            for (int j = 0; j < K; ++j) { /* row i -= f * row k */
+                const double br = M[(k * K + j) * 2], bi = M[(k * K + j) * 2 + 1];
+                M[(i * K + j) * 2] -= fr * br - fi * bi;
+                M[(i * K + j) * 2 + 1] -= fr * bi + fi * br;
+            }
+        }
+    }
+    for (int k = K - 1; k >= 0; --k) /* undo the row swaps as column swaps */
+        if (perm[k] != k)
+            for (int i = 0; i < K; ++i)
+                for (int c = 0; c < 2; ++c) {
+                    const double t = M[(i * K + k) * 2 + c];
+                    M[(i * K + k) * 2 + c] = M[(i * K + perm[k]) * 2 + c];
+                    M[(i * K + perm[k]) * 2 + c] = t;
+                }
+    free(perm);
+    return 0;
+}
+
+/* rates[d][s] (bits/s/Hz); flags bit 5 (32) when G~ is singular (rates NaN). */
+void or_sum_rate_mismatched(const double *gram, const double *gram_model, int32_t K, int64_t n_drops,
+                            const double *snr_db, int32_t n_snr, double *rates, uint32_t *flags)
+{
+    double *B = (double *)malloc(sizeof(double) * 2 * K * K);
+    double *A = (double *)malloc(sizeof(double) * 2 * K * K);
+    for (int64_t d = 0; d < n_drops; ++d) {
+        const double *G = gram + (size_t)d * K * K * 2;
+        memcpy(B, gram_model + (size_t)d * K * K * 2, sizeof(double) * 2 * K * K);
+        if (or_cinv(B, K) != 0) {
+            for (int s = 0; s < n_snr; ++s) rates[d * n_snr + s] = NAN;
+            if (flags) flags[d] |= 32u;
+            continue;
+        }
+        for (int i = 0; i < K; ++i) /* A = B G */
+            for (int j = 0; j < K; ++j) {
+                double sr = 0.0, si = 0.0;
+                for (int k = 0; k < K; ++k) {
+                    const double br = B[(i * K + k) * 2], bi = B[(i * K + k) * 2 + 1];
+                    const double gr = G[(k * K + j) * 2], gi = G[(k * K + j) * 2 + 1];
+                    sr += br * gr - bi * gi;
+                    si += br * gi + bi * gr;
+                }
+                A[(i * K + j) * 2] = sr;
+                A[(i * K + j) * 2 + 1] = si;
+            }
+        for (int s = 0; s < n_snr; ++s) {
+            const double rho = pow(10.0, snr_db[s] / 10.0);
+            double c = 0.0;
+            for (int i = 0; i < K; ++i) {
+                double sig = 0.0, intf = 0.0, noise = 0.0;
+                for (int j = 0; j < K; ++j) {
+                    const double p = A[(i * K + j) * 2] * A[(i * K + j) * 2] + A[(i * K + j) * 2 + 1] * A[(i * K + j) * 2 + 1];
+                    if (j == i) sig = p; else intf += p;
+                }
+                for (int k = 0; k < K; ++k) { /* [A B]_ii = sum_k A_ik B_ki, real for Hermitian PSD G */
+                    noise += A[(i * K + k) * 2] * B[(k * K + i) * 2] - A[(i * K + k) * 2 + 1] * B[(k * K + i) * 2 + 1];
+                }
+                c += log2(1.0 + sig / (intf + noise / rho));
+            }
+            rates[d * n_snr + s] = c;
+        }
+    }
+    free(A); free(B);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -88,6 +88,10 @@ def _load():
                                           vp, vp, vp, vp, vp, sz, vp]
     L.xlmimo_saturation_sweep_host.argtypes = [P(Array), vp, i32, vp, i32, i64, vp, i32, u32, i32, i32, d,
                                                vp, vp, vp, vp, sz, vp]
+    L.xlmimo_sum_rate_mismatched.argtypes = [vp, vp, i32, i64, vp, i32, vp, vp, vp]
+    L.xlmimo_sum_rate_mismatched.restype = ctypes.c_int
+    L.xlmimo_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp, vp]
+    L.xlmimo_gen_drops_rect.restype = ctypes.c_int
     L.xlmimo_timing_enable.argtypes = [i32]
     L.xlmimo_timing_read.argtypes = [i32, ctypes.c_char_p, vp, vp]
     L.xlmimo_last_error.restype = ctypes.c_char_p
@@ -194,6 +198,33 @@ def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | N
     _check(_L.xlmimo_sum_rate(_dptr(g), K, D, _hptr(snr), snr.size, receivers, _dptr(rates), _dptr(fl),
                               _stream(stream)), "xlmimo_sum_rate")
     return rates, fl
+
+
+def sum_rate_mismatched(gram: torch.Tensor, gram_model: torch.Tensor, snr_db, flags: torch.Tensor | None = None,
+                        stream=None):
+    """NEXT-1: effective rate of the modified-ZF equalizer G~^{-1} H^H on the true channel.
+    Returns rates [D, n_snr] and flags [D] (bit 5: G~ singular)."""
+    _need_cuda()
+    g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
+    gm = torch.view_as_real(gram_model).contiguous() if gram_model.is_complex() else gram_model.contiguous()
+    D, K = g.shape[0], g.shape[1]
+    snr = _f64_host(snr_db)
+    rates = torch.empty((D, snr.size), dtype=torch.float64, device=g.device)
+    fl = flags if flags is not None else torch.zeros(D, dtype=torch.int32, device=g.device)
+    _check(_L.xlmimo_sum_rate_mismatched(_dptr(g), _dptr(gm), K, D, _hptr(snr), snr.size, _dptr(rates), _dptr(fl),
+                                         _stream(stream)), "xlmimo_sum_rate_mismatched")
+    return rates, fl
+
+
+def gen_drops_rect(x, y, K: int, n_drops: int, seed: int = 0, first_drop: int = 0, device=None,
+                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """NEXT-4: drops from the paper's rectangle user field x ~ U[x0,x1], y ~ U[y0,y1]."""
+    _need_cuda()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    pos = out if out is not None else torch.empty((n_drops, K, 3), dtype=torch.float64, device=dev)
+    _check(_L.xlmimo_gen_drops_rect(float(x[0]), float(x[1]), float(y[0]), float(y[1]), K, n_drops, seed,
+                                    first_drop, _dptr(pos), _stream(stream)), "xlmimo_gen_drops_rect")
+    return pos
 
 
 # --------------------------------------------------------------------------- a1..a6

@@ -309,6 +309,30 @@ int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double
   return xlh::launch_sum_rate(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, (cudaStream_t)stream);
 }
 
+int xlmimo_sum_rate_mismatched(const double *gram, const double *gram_model, int32_t K, int64_t n_drops,
+                               const double *snr_db, int32_t n_snr, double *rates, uint32_t *flags, void *stream) {
+  g_err[0] = 0;
+  if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "sum_rate_mismatched: K=%d", K);
+  if (K > xl::kMaxK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate_mismatched: K=%d > %d", K, xl::kMaxK);
+  if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr)
+    return xlh::set_error(XLMIMO_EINVAL, "sum_rate_mismatched: n_snr out of [1,16]");
+  if (n_drops > 0 && (!gram || !gram_model || !rates))
+    return xlh::set_error(XLMIMO_EINVAL, "sum_rate_mismatched: null pointer");
+  return xlh::launch_sum_rate_mismatched(gram, gram_model, K, n_drops, snr_db, n_snr, rates, flags,
+                                         (cudaStream_t)stream);
+}
+
+int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max, int32_t K, int64_t n_drops,
+                          uint64_t seed, uint64_t first_drop, double *pos, void *stream) {
+  g_err[0] = 0;
+  if (!(x_min > 0.0) || !(x_min <= x_max) || !(y_min <= y_max) || !std::isfinite(x_max) || !std::isfinite(y_min) ||
+      !std::isfinite(y_max))
+    return xlh::set_error(XLMIMO_EINVAL, "gen_drops_rect: invalid rectangle");
+  if (K < 1 || n_drops < 0 || (!pos && n_drops > 0)) return xlh::set_error(XLMIMO_EINVAL, "gen_drops_rect: K/n/pos");
+  return xlh::launch_gen_drops_rect(x_min, x_max, y_min, y_max, K, n_drops, seed, first_drop, pos,
+                                    (cudaStream_t)stream);
+}
+
 size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, int32_t K,
                                          int64_t n_drops, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
                                          int32_t precision) {

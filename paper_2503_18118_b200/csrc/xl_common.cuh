@@ -255,6 +255,12 @@ int check_launch(const char *what);
 int launch_gen_drops(const xlmimo_users_t &u, int K, int64_t n_drops, uint64_t seed, uint64_t first_drop,
                      double *pos, cudaStream_t s);
 
+int launch_gen_drops_rect(double x0, double x1, double y0, double y1, int K, int64_t n_drops, uint64_t seed,
+                          uint64_t first_drop, double *pos, cudaStream_t s);
+// xl_rates.cu : NEXT-1 modified-ZF effective rate, rates [n_prob][n_snr]
+int launch_sum_rate_mismatched(const double *gram, const double *gram_model, int K, int64_t n_prob,
+                               const double *snr_db, int n_snr, double *rates, uint32_t *flags, cudaStream_t s);
+
 // xl_gram.cu
 // Exact Gram over element indices [0, N) in the "centred order", with snapshots
 // at the level ends lvl_end[0..n_lvl-1] (ascending, last = N).  Output:

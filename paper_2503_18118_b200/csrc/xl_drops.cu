@@ -23,9 +23,35 @@ __global__ void __launch_bounds__(256) gen_drops_kernel(xlmimo_users_t u, int K,
   p[2] = r * se;
 }
 
+// NEXT-4: the paper's rectangle user field x ~ U[x0, x1], y ~ U[y0, y1].
+__global__ void __launch_bounds__(256) gen_drops_rect_kernel(double x0, double x1, double y0, double y1, int K,
+                                                             int64_t n_total, uint64_t seed, uint64_t first_drop,
+                                                             double *pos) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_total) return;
+  const int64_t d = idx / K;
+  const int k = (int)(idx - d * K);
+  const xl::u64x4 w = xl::philox4x64_10(first_drop + (uint64_t)d, (uint64_t)k, 0, 0, seed, 0);
+  double *p = pos + idx * 3;
+  p[0] = x0 + (x1 - x0) * xl::u01_53(w.v[0]);
+  p[1] = y0 + (y1 - y0) * xl::u01_53(w.v[1]);
+  p[2] = 0.0;
+}
+
 }  // namespace
 
 namespace xlh {
+
+int launch_gen_drops_rect(double x0, double x1, double y0, double y1, int K, int64_t n_drops, uint64_t seed,
+                          uint64_t first_drop, double *pos, cudaStream_t s) {
+  const int64_t n = n_drops * (int64_t)K;
+  if (n == 0) return XLMIMO_OK;
+  KTimer tm(s, "gen_drops_rect");
+  gen_drops_rect_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x0, x1, y0, y1, K, n, seed, first_drop, pos);
+  tm.stop(s);
+  count_launch();
+  return check_launch("gen_drops_rect_kernel");
+}
 
 int launch_gen_drops(const xlmimo_users_t &u, int K, int64_t n_drops, uint64_t seed, uint64_t first_drop,
                      double *pos, cudaStream_t s) {

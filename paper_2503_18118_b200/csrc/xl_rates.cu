@@ -7,6 +7,8 @@
 //   I + rho G = L L^H -> CAP = 2 sum log2 L_kk, [(I+rho G)^{-1}]_ii = sum_k |(L^{-1})_ki|^2;
 //   G = L L^H once     -> [G^{-1}]_ii for ZF;  MRC straight from G.
 // A pivot that is not > 0 (or not finite) marks the factorisation failed (R10).
+#include <cstring>
+
 #include "xl_common.cuh"
 
 namespace {
@@ -371,6 +373,115 @@ __global__ void __launch_bounds__(128) rates_thread_kernel(RateParams P) {
   if (P.flags) P.flags[prob] |= fl;
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-1: modified-ZF effective rate.  Block per Gram pair, thread per row:
+// in-place complex Gauss-Jordan with partial pivoting for B = G~^{-1} (pivot
+// search by thread 0, first maximal |.|, as the oracle), A = B G, then per row
+// SINR_i = |A_ii|^2 / (sum_{j!=i}|A_ij|^2 + Re[A B]_ii / rho); rates summed in
+// row order by thread 0 (deterministic).
+__global__ void __launch_bounds__(64) mismatched_kernel(const double *gram, const double *gram_model, int K,
+                                                        int n_snr, RateParams P) {
+  extern __shared__ double2 sm[];
+  double2 *B = sm, *Gs = sm + K * K, *A = sm + 2 * K * K;
+  __shared__ int singular;
+  __shared__ int perm[xl::kMaxK];
+  __shared__ double terms[xl::kMaxSnr][64];
+  const int64_t prob = blockIdx.x;
+  const int t = threadIdx.x;
+  const double2 *Gm = reinterpret_cast<const double2 *>(gram_model) + (size_t)prob * K * K;
+  const double2 *Gt = reinterpret_cast<const double2 *>(gram) + (size_t)prob * K * K;
+  for (int e = t; e < K * K; e += blockDim.x) {
+    B[e] = Gm[e];
+    Gs[e] = Gt[e];
+  }
+  if (t == 0) singular = 0;
+  __syncthreads();
+  for (int k = 0; k < K; ++k) {
+    if (t == 0) {
+      int p = k;
+      double best = -1.0;
+      for (int i = k; i < K; ++i) {
+        const double v = hypot(B[i * K + k].x, B[i * K + k].y);
+        if (v > best) { best = v; p = i; }
+      }
+      if (!(best > 0.0)) singular = 1;
+      perm[k] = p;
+      if (p != k)
+        for (int j = 0; j < K; ++j) {
+          const double2 tmp = B[k * K + j];
+          B[k * K + j] = B[p * K + j];
+          B[p * K + j] = tmp;
+        }
+    }
+    __syncthreads();
+    if (singular) break;
+    const double2 pv = B[k * K + k];
+    const double den = pv.x * pv.x + pv.y * pv.y;
+    const double ir = pv.x / den, ii = -pv.y / den;
+    __syncthreads();
+    for (int j = t; j < K; j += blockDim.x) {  // row k *= 1/pivot (B[k][k] := 1 first)
+      const double2 a = (j == k) ? make_double2(1.0, 0.0) : B[k * K + j];
+      B[k * K + j] = make_double2(a.x * ir - a.y * ii, a.x * ii + a.y * ir);
+    }
+    __syncthreads();
+    if (t < K && t != k) {  // row t -= f * row k
+      const double2 f = B[t * K + k];
+      B[t * K + k] = make_double2(0.0, 0.0);
+      for (int j = 0; j < K; ++j) {
+        const double2 b = B[k * K + j];
+        double2 a = B[t * K + j];
+        a.x -= f.x * b.x - f.y * b.y;
+        a.y -= f.x * b.y + f.y * b.x;
+        B[t * K + j] = a;
+      }
+    }
+    __syncthreads();
+  }
+  double *out = P.rates + (size_t)prob * n_snr;
+  if (singular) {
+    if (t < n_snr) out[t] = __longlong_as_double(0x7ff8000000000000LL);
+    if (t == 0 && P.flags) P.flags[prob] |= XLMIMO_FLAG_MODEL_SINGULAR;
+    return;
+  }
+  // undo the row swaps as column swaps (each thread its own row)
+  if (t < K)
+    for (int k = K - 1; k >= 0; --k) {
+      const int p = perm[k];
+      if (p != k) {
+        const double2 tmp = B[t * K + k];
+        B[t * K + k] = B[t * K + p];
+        B[t * K + p] = tmp;
+      }
+    }
+  __syncthreads();
+  double sig = 0.0, intf = 0.0, noise = 0.0;
+  if (t < K) {
+    for (int j = 0; j < K; ++j) {  // A = B G, row t
+      double sr = 0.0, si = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const double2 b = B[t * K + k], g = Gs[k * K + j];
+        sr += b.x * g.x - b.y * g.y;
+        si += b.x * g.y + b.y * g.x;
+      }
+      A[t * K + j] = make_double2(sr, si);
+      const double p = sr * sr + si * si;
+      if (j == t) sig = p;
+      else intf += p;
+    }
+    for (int k = 0; k < K; ++k) {  // Re [A B]_tt
+      const double2 a = A[t * K + k], b = B[k * K + t];
+      noise += a.x * b.x - a.y * b.y;
+    }
+    for (int s = 0; s < n_snr; ++s) terms[s][t] = log2(1.0 + sig / (intf + noise / P.rho[s]));
+  }
+  __syncthreads();
+  if (t < n_snr) {
+    double c = 0.0;
+    for (int i = 0; i < K; ++i) c += terms[t][i];
+    out[t] = c;
+  }
+}
+
 template <int K>
 void launch_rates_thread(const RateParams &P, cudaStream_t s) {
   rates_thread_kernel<K><<<(unsigned)((P.n_prob + 127) / 128), 128, 0, s>>>(P);
@@ -379,6 +490,26 @@ void launch_rates_thread(const RateParams &P, cudaStream_t s) {
 }  // namespace
 
 namespace xlh {
+
+int launch_sum_rate_mismatched(const double *gram, const double *gram_model, int K, int64_t n_prob,
+                               const double *snr_db, int n_snr, double *rates, uint32_t *flags, cudaStream_t s) {
+  if (n_prob == 0) return XLMIMO_OK;
+  RateParams P;
+  memset(&P, 0, sizeof(P));
+  P.rates = rates;
+  P.flags = flags;
+  P.K = K;
+  P.n_prob = n_prob;
+  P.n_snr = n_snr;
+  for (int i = 0; i < xl::kMaxSnr; ++i) P.rho[i] = i < n_snr ? pow(10.0, snr_db[i] / 10.0) : 0.0;
+  const size_t smem = 3 * (size_t)K * K * sizeof(double2);
+  cudaFuncSetAttribute(mismatched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  KTimer tm(s, "sum_rate_mismatched");
+  mismatched_kernel<<<(unsigned)n_prob, 64, smem, s>>>(gram, gram_model, K, n_snr, P);
+  tm.stop(s);
+  count_launch();
+  return check_launch("mismatched_kernel");
+}
 
 int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr_db, int n_snr,
                     uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s) {

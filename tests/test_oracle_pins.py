@@ -511,3 +511,69 @@ def test_upa_diagonal_solid_angle(orc):
                     u, v = yc - y, zc - z
                     om += sy * sz * math.atan(u * v / (x * math.sqrt(x * x + u * u + v * v)))
             assert G[i, i].real == pytest.approx(4 / lam ** 2 * om, rel=1e-5)
+
+
+# --------------------------------------------------------------------------- NEXT-1 / NEXT-4
+def _first_principles_mismatched(H, Gt, rho):
+    """W = G~^{-1} H^H applied to the true H (numpy/LAPACK inverse): T = W H, noise W W^H / rho."""
+    W = np.linalg.inv(Gt) @ H.conj().T
+    T = W @ H
+    c = 0.0
+    for i in range(T.shape[0]):
+        sig = abs(T[i, i]) ** 2
+        intf = sum(abs(T[i, j]) ** 2 for j in range(T.shape[0]) if j != i)
+        c += math.log2(1 + sig / (intf + np.linalg.norm(W[i]) ** 2 / rho))
+    return c
+
+
+def test_mismatched_rate_first_principles_and_zf_limit(orc):
+    """NEXT-1 (R11): the modified-ZF effective rate equals the first-principles SINR of
+    W = G~^{-1} H^H on H; with G~ = G it is exactly the ZF rate (A = I)."""
+    arr = orc.array("ula", n_y=40, fc_hz=100e9)
+    lam = orc.wavelength(arr)
+    pos = orc.gen_drops_rect((1.0, 2.0), (-7.5, 7.5), 5, 3, seed=8)
+    G = orc.gram_exact(arr, pos)
+    Gt, _ = orc.gram_closed_form(arr, pos)
+    snr = [0.0, 10.0, 30.0]
+    r, fl = orc.sum_rate_mismatched(G, Gt, snr)
+    for d in range(3):
+        H = orc.channel_matrix(arr, pos[d])
+        for s, sdb in enumerate(snr):
+            assert r[d, s] == pytest.approx(_first_principles_mismatched(H, Gt[d], 10 ** (sdb / 10)), rel=1e-9)
+    rz, _ = orc.sum_rate_mismatched(G, G, snr)
+    zf, _ = orc.sum_rate(G, snr, orc.RECV_ZF)
+    assert np.allclose(rz, zf[..., 0], rtol=1e-11)
+    # singular model Gram -> NaN + flag bit 5
+    Gs = Gt.copy()
+    Gs[0] = 0.0
+    rs, fls = orc.sum_rate_mismatched(G, Gs, snr)
+    assert np.all(np.isnan(rs[0])) and fls[0] & 32 and np.all(np.isfinite(rs[1:]))
+
+
+def test_modified_zf_worse_below_saturation_equal_after(orc):
+    """PAPER.md:273-275 (E2 setting: K = 10, x ~ U(1,2), y ~ U[-7.5,7.5] m, 100 GHz, transmit
+    SNR set for a 33 dB limit at (1.5 m, 0)): the modified ZF is worse than ZF well below the
+    saturation point and reaches it beyond."""
+    lam = C / 100e9
+    rho_db = 10 * math.log10(10 ** 3.3 * lam * 1.5 / 4)  # P * 4 beta0/(lambda x) / sigma^2 = 33 dB at x = 1.5 (Eq. 5)
+    pos = orc.gen_drops_rect((1.0, 2.0), (-7.5, 7.5), 10, 4, seed=2)
+    out = {}
+    for N in (256, 25000):
+        arr = orc.array("ula", n_y=N, fc_hz=100e9)
+        G = orc.gram_exact(arr, pos)
+        Gt, _ = orc.gram_closed_form(arr, pos)
+        zf, _ = orc.sum_rate(G, [rho_db], orc.RECV_ZF)
+        mz, _ = orc.sum_rate_mismatched(G, Gt, [rho_db])
+        out[N] = (zf[:, 0, 0], mz[:, 0])
+    zf, mz = out[256]
+    assert np.all(mz < zf)                                  # "worse performance ... at the beginning"
+    zf, mz = out[25000]
+    assert np.all(np.abs(mz - zf) / zf < 0.01)              # same capacity after the saturation point
+
+
+def test_rect_drops_law(orc):
+    pos = orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 8, 5000, seed=4)
+    assert pos[..., 0].min() >= 1.0 and pos[..., 0].max() <= 10.0 and np.all(pos[..., 2] == 0)
+    assert abs(pos[..., 0].mean() - 5.5) < 4 * 9 / math.sqrt(12) / math.sqrt(pos[..., 0].size)
+    assert abs(pos[..., 1].mean()) < 4 * 15 / math.sqrt(12) / math.sqrt(pos[..., 1].size)
+    assert np.array_equal(orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 8, 10, seed=4, first_drop=7), pos[7:17])
