@@ -226,6 +226,16 @@ __device__ __forceinline__ double ula_y_centred(int64_t t, bool n_odd, double pi
   const double y = ((double)p + 0.5) * pitch;
   return (t & 1) ? -y : y;
 }
+// the same for 0 <= t < 2^31 in 32-bit integer arithmetic
+__device__ __forceinline__ double ula_y_centred(int t, bool n_odd, double pitch) {
+  if (n_odd) {
+    if (t == 0) return 0.0;
+    const double y = (double)(((t - 1) >> 1) + 1) * pitch;
+    return (t & 1) ? y : -y;
+  }
+  const double y = ((double)(t >> 1) + 0.5) * pitch;
+  return (t & 1) ? -y : y;
+}
 
 }  // namespace xl
 

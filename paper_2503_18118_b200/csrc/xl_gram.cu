@@ -520,8 +520,7 @@ __global__ void __launch_bounds__(32 * NW, 1) gram_mma_tiled_kernel(GramParams P
   constexpr int NT = 32 * NW, NPAIR = G * (G + 1) / 2;
   constexpr bool HALVE = G <= 4;
   extern __shared__ __align__(16) double dsm[];
-  double *fre = dsm;                  // [S][G][32]
-  double *fim = dsm + S * G * 32;     // [S][G][32]
+  double *fre = dsm;                  // 2 buffers x {re [S][G][32], im [S][G][32]}
   double *stage = dsm;                // [NPAIR][4][8][8] at level ends (aliases the tiles)
   __shared__ double4 su[8 * G];
 
@@ -562,8 +561,10 @@ __global__ void __launch_bounds__(32 * NW, 1) gram_mma_tiled_kernel(GramParams P
     for (int k = 0; k < MAXP; ++k)
 #pragma unroll
       for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
-    for (int64_t t0 = a; t0 < b; t0 += 4 * S) {
-      // generation: S*G*32 coefficients, fragment order
+    // double-buffered tiles: generation of tile i+1 and the DMMAs of tile i run between
+    // the same pair of barriers (one __syncthreads per tile)
+    auto generate = [&](int64_t t0, int buf) {
+      double *gre = fre + buf * (2 * S * G * 32), *gim = gre + S * G * 32;
       for (int c = tid; c < S * G * 32; c += NT) {
         const int s = c / (G * 32), rem = c - s * (G * 32), g = rem >> 5, ln = rem & 31;
         const int64_t t = t0 + 4 * s + (ln & 3);
@@ -579,18 +580,25 @@ __global__ void __launch_bounds__(32 * NW, 1) gram_mma_tiled_kernel(GramParams P
         }
         double hr, hi;
         xl::coef_fast(r2, valid ? uc.w : 0.0, c4, hr, hi);
-        fre[c] = hr;
-        fim[c] = hi;
+        gre[c] = hr;
+        gim[c] = hi;
       }
-      __syncthreads();
+    };
+    if (a < b) generate(a, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t t0 = a; t0 < b; t0 += 4 * S, buf ^= 1) {
+      if (t0 + 4 * S < b) generate(t0 + 4 * S, buf ^ 1);
+      const double *fre_c = fre + buf * (2 * S * G * 32);
+      const double *fim_c = fre_c + S * G * 32;
       for (int s = 0; s < S; ++s) {
 #pragma unroll
         for (int k = 0; k < MAXP; ++k) {
           if (k < np) {
             // part: 0 all, 1 RR+II, 2 RI+IR (compile-time 0 unless HALVE)
             const int g1 = pg1[k], g2 = pg2[k] & 255, part = HALVE ? (pg2[k] >> 8) : 0;
-            const double ar = fre[(s * G + g1) * 32 + lane], ai = fim[(s * G + g1) * 32 + lane];
-            const double br = fre[(s * G + g2) * 32 + lane], bi = fim[(s * G + g2) * 32 + lane];
+            const double ar = fre_c[(s * G + g1) * 32 + lane], ai = fim_c[(s * G + g1) * 32 + lane];
+            const double br = fre_c[(s * G + g2) * 32 + lane], bi = fim_c[(s * G + g2) * 32 + lane];
             if (part != 2) {
               dmma(acc[k][0], ar, br);
               dmma(acc[k][1], ai, bi);
@@ -678,7 +686,7 @@ constexpr int kMtS = 8;  // 4-element steps per tile (32 elements)
 
 template <int G>
 size_t mt_smem_bytes() {
-  const size_t tiles = 2 * (size_t)kMtS * G * 32 * sizeof(double);
+  const size_t tiles = 4 * (size_t)kMtS * G * 32 * sizeof(double);  // double-buffered re/im tiles
   const size_t stage = (size_t)(G * (G + 1) / 2) * 4 * 64 * sizeof(double);
   return tiles > stage ? tiles : stage;
 }
@@ -691,6 +699,211 @@ void launch_mt(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const size_t smem = mt_smem_bytes<G>();
   cudaFuncSetAttribute(gram_mma_tiled_kernel<G, kMtS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   gram_mma_tiled_kernel<G, kMtS, NW><<<(unsigned)n_blocks, 32 * NW, smem, s>>>(P, plan);
+}
+
+// ------------------------------------------------------------------ kernel MT2
+// DMMA Gram for K = 17..64 with a branch-free inner loop (the default for fp64
+// K > 16).  The real-ified Gram R = A A^T (A = the 2K x N real matrix of re/im
+// rows, one m8n8k4 fragment "plane" per 8 users) is covered by the G(G+1)/2
+// 2x2 plane blocks (g1 <= g2); every block is one job of exactly four DMMAs
+// (RR, II, RI, IR) on four fragment loads -- diagonal blocks included, whose
+// IR = RI^T is redundant (G of the 2G(G+1) DMMAs per step, 6-11%) but keeps the
+// loop uniform: Re G = RR + II, Im G = RI - IR for every (i <= j).  Warps are
+// (job group jg, step group sg): JPW jobs per warp over the steps s == sg mod SG
+// of each tile; the SG partial accumulators meet in shared memory at level ends.
+// The NW = (J/JPW)*SG warps are a multiple of 4 so that each SM sub-partition
+// (warp % 4) gets the same DMMA and generation load.  Tiles of 4S elements are
+// generated (one 32-lane fragment row = 4 elements x 8 users per warp-iteration)
+// into a double buffer, so one barrier per tile separates generation of tile i+1
+// from the DMMAs of tile i.
+template <int G>
+struct Mt2Cfg;
+template <> struct Mt2Cfg<3> { static constexpr int JPW = 1, SG = 2, S = 8; };   // NW 12
+template <> struct Mt2Cfg<4> { static constexpr int JPW = 1, SG = 2, S = 8; };   // NW 20
+template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };   // NW 20
+template <> struct Mt2Cfg<6> { static constexpr int JPW = 7, SG = 4, S = 8; };   // NW 12
+template <> struct Mt2Cfg<7> { static constexpr int JPW = 7, SG = 3, S = 12; };  // NW 12
+template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 8; };   // NW 12
+
+template <int G>
+struct Mt2 {
+  static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = Mt2Cfg<G>::S;
+  static constexpr int JG = J / JPW, NW = JG * SG, NT = 32 * NW;
+  static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
+  static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
+  static_assert(J % JPW == 0 && S % SG == 0 && NW % 4 == 0, "Mt2Cfg");
+  static constexpr size_t tiles_bytes = 4ull * PLANE * sizeof(double);        // 2 buffers x re/im
+  static constexpr size_t stage_bytes = (size_t)J * 4 * SG * 64 * sizeof(double);
+  static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
+};
+
+struct FastDiv {  // q = (umulhi(m, t) + t) >> sh == t / d for 0 <= t < 2^31
+  uint32_t m;
+  int sh;
+};
+
+FastDiv make_fastdiv(uint32_t d) {
+  int l = 0;
+  while ((1ull << l) < d) ++l;
+  FastDiv f;
+  f.m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+  f.sh = l;
+  return f;
+}
+
+template <int KIND>
+__device__ __forceinline__ ElemPos element_pos32(const GramParams &P, int t, FastDiv fd, bool n_odd) {
+  ElemPos e;
+  if (KIND == XLMIMO_ULA) {
+    e.y = xl::ula_y_centred(t, n_odd, P.pitch);
+    e.z = 0.0;
+  } else {
+    const uint32_t tt = (uint32_t)t;
+    const uint32_t q = (__umulhi(fd.m, tt) + tt) >> fd.sh;
+    const uint32_t p = tt - q * (uint32_t)P.n_y;
+    e.y = ((double)p - 0.5 * (double)(P.n_y - 1)) * P.pitch;
+    e.z = ((double)q - 0.5 * (double)(P.n_z - 1)) * P.pitch;
+  }
+  return e;
+}
+
+template <int G, int KIND>
+__global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd) {
+  using C = Mt2<G>;
+  constexpr int JPW = C::JPW, SG = C::SG, S = C::S, NW = C::NW, NT = C::NT, JG = C::JG;
+  constexpr int PLANE = C::PLANE, ROWS = C::ROWS;
+  extern __shared__ __align__(16) double dsm[];  // tiles [2][re|im][S][G][32]; stage at level ends
+  __shared__ double4 su[8 * G];
+
+  const int64_t bdrop = blockIdx.x / P.n_split;
+  const int split = blockIdx.x - (int)(bdrop * P.n_split);
+  const int64_t drop = P.h_drop0 + bdrop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = P.K;
+  for (int u = tid; u < 8 * G; u += NT) {
+    if (u < K) {
+      const xl::UserC uc = xl::make_user(P.pos + (drop * K + u) * 3, KIND, P.sqrt_beta0);
+      su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+    } else {
+      su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: zero amplitude
+    }
+  }
+  const int jg = warp % JG, sg = warp / JG;
+  int aoff[JPW], boff[JPW];  // fragment offsets of the job's two planes (row-major g1 <= g2 order)
+#pragma unroll
+  for (int k = 0; k < JPW; ++k) {
+    int q = jg * JPW + k, g1 = 0;
+    while (q >= G - g1) { q -= G - g1; ++g1; }
+    aoff[k] = g1 * 32 + lane;
+    boff[k] = (g1 + q) * 32 + lane;
+  }
+  __syncthreads();
+  const double c4 = 4.0 * P.inv_lambda;
+  const bool n_odd = (P.N & 1) != 0;
+
+  const int s0 = (int)min((int64_t)split * P.chunk, P.N);
+  const int s1 = (int)min(P.N, (int64_t)s0 + P.chunk);
+  int lv0 = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int lv1 = (int)P.lvl_end[l];
+    const int a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[JPW][4][2];
+#pragma unroll
+    for (int k = 0; k < JPW; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+    auto generate = [&](int t0, int buf) {
+      double *gre = dsm + buf * (2 * PLANE), *gim = gre + PLANE;
+#pragma unroll
+      for (int i = 0; i < (ROWS + NW - 1) / NW; ++i) {
+        const int row = warp + i * NW;  // row = s * G + g
+        if (ROWS % NW == 0 || row < ROWS) {
+          const int s = row / G, g = row - s * G;
+          const int t = t0 + 4 * s + (lane & 3);
+          const bool valid = t < b;
+          const ElemPos ep = element_pos32<KIND>(P, valid ? t : a, fd, n_odd);
+          const double4 uc = su[8 * g + (lane >> 2)];
+          const double dy = ep.y - uc.y;
+          double r2 = fma(dy, dy, uc.x);
+          if (KIND != XLMIMO_ULA) {
+            const double dz = ep.z - uc.z;
+            r2 = fma(dz, dz, r2);
+          }
+          double hr, hi;
+          xl::coef_fast(r2, valid ? uc.w : 0.0, c4, hr, hi);
+          gre[row * 32 + lane] = hr;
+          gim[row * 32 + lane] = hi;
+        }
+      }
+    };
+    if (a < b) generate(a, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int t0 = a; t0 < b; t0 += 4 * S, buf ^= 1) {
+      if (t0 + 4 * S < b) generate(t0 + 4 * S, buf ^ 1);
+      const double *cre = dsm + buf * (2 * PLANE) + sg * (G * 32), *cim = cre + PLANE;
+#pragma unroll
+      for (int si = 0; si < S / SG; ++si) {
+        const int so = si * SG * G * 32;
+#pragma unroll
+        for (int k = 0; k < JPW; ++k) {
+          const double ar = cre[so + aoff[k]], ai = cim[so + aoff[k]];
+          const double br = cre[so + boff[k]], bi = cim[so + boff[k]];
+          dmma(acc[k][0], ar, br);
+          dmma(acc[k][1], ai, bi);
+          dmma(acc[k][2], ar, bi);
+          dmma(acc[k][3], ai, br);
+        }
+      }
+      __syncthreads();
+    }
+    // stage [q][m][sg][8][8] (C fragment: row lane/4, cols 2(lane%4) + {0,1})
+#pragma unroll
+    for (int k = 0; k < JPW; ++k) {
+      const int q = jg * JPW + k;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double *st = dsm + ((q * 4 + m) * SG + sg) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
+        st[0] = acc[k][m][0];
+        st[1] = acc[k][m][1];
+      }
+    }
+    __syncthreads();
+    const int NP = K * (K + 1) / 2;
+    double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * (size_t)(2 * NP);
+    for (int p = tid; p < NP; p += NT) {
+      int i = 0, rem = p;
+      while (rem >= K - i) { rem -= K - i; ++i; }
+      const int j = i + rem;
+      const int g1 = i >> 3, g2 = j >> 3, e = (i & 7) * 8 + (j & 7);
+      const int q = g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
+      const double *st = dsm + (size_t)q * 4 * SG * 64 + e;
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int g = 0; g < SG; ++g) {
+        re += st[(0 * SG + g) * 64] + st[(1 * SG + g) * 64];
+        im += st[(2 * SG + g) * 64] - st[(3 * SG + g) * 64];
+      }
+      out[2 * p] = re;
+      out[2 * p + 1] = (i == j) ? 0.0 : im;
+    }
+    __syncthreads();
+  }
+}
+
+template <int G, int KIND>
+void launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  using C = Mt2<G>;
+  const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
+  cudaFuncSetAttribute(gram_mt2_kernel<G, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+  gram_mt2_kernel<G, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd);
+}
+
+template <int G>
+void launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+  if (P.kind == XLMIMO_ULA) launch_mt2_k<G, XLMIMO_ULA>(P, n_blocks, s);
+  else launch_mt2_k<G, XLMIMO_UPA>(P, n_blocks, s);
 }
 
 // ------------------------------------------------------------------ kernel B
@@ -1165,7 +1378,9 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                : kc.which == 3 ? "gram_fused_dmma_tiled_fp64"
                : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
                         : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
-  if (kc.which == 3) {
+  static const char *env_mt = getenv("XLMIMO_GRAM_KERNEL");
+  const bool mt1 = (env_mt && !strcmp(env_mt, "mt1")) || N >= ((int64_t)1 << 31);
+  if (kc.which == 3 && mt1) {
     switch ((K + 7) / 8) {
       case 3: launch_mt<3>(P, n_blocks, s); break;
       case 4: launch_mt<4>(P, n_blocks, s); break;
@@ -1173,6 +1388,15 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       case 6: launch_mt<6>(P, n_blocks, s); break;
       case 7: launch_mt<7>(P, n_blocks, s); break;
       default: launch_mt<8>(P, n_blocks, s); break;
+    }
+  } else if (kc.which == 3) {
+    switch ((K + 7) / 8) {
+      case 3: launch_mt2<3>(P, n_blocks, s); break;
+      case 4: launch_mt2<4>(P, n_blocks, s); break;
+      case 5: launch_mt2<5>(P, n_blocks, s); break;
+      case 6: launch_mt2<6>(P, n_blocks, s); break;
+      case 7: launch_mt2<7>(P, n_blocks, s); break;
+      default: launch_mt2<8>(P, n_blocks, s); break;
     }
   } else if (kc.which == 2) {
     const bool ula = a.kind == XLMIMO_ULA;
