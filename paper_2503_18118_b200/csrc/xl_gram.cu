@@ -722,19 +722,20 @@ template <> struct Mt2Cfg<3> { static constexpr int JPW = 1, SG = 2, S = 8; };  
 template <> struct Mt2Cfg<4> { static constexpr int JPW = 1, SG = 2, S = 8; };   // NW 20
 template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };   // NW 20
 template <> struct Mt2Cfg<6> { static constexpr int JPW = 7, SG = 4, S = 8; };   // NW 12
-template <> struct Mt2Cfg<7> { static constexpr int JPW = 7, SG = 3, S = 12; };  // NW 12
+template <> struct Mt2Cfg<7> { static constexpr int JPW = 7, SG = 2, S = 8; };   // NW 8
 template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 8; };   // NW 12
 
-template <int G>
+template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::S; NBUF tile buffers
 struct Mt2 {
-  static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = Mt2Cfg<G>::S;
+  static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
   static constexpr int JG = J / JPW, NW = JG * SG, NT = 32 * NW;
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
   static_assert(J % JPW == 0 && S % SG == 0 && NW % 4 == 0, "Mt2Cfg");
-  static constexpr size_t tiles_bytes = 4ull * PLANE * sizeof(double);        // 2 buffers x re/im
+  static constexpr size_t tiles_bytes = 2ull * NBUF * PLANE * sizeof(double);  // NBUF buffers x re/im
   static constexpr size_t stage_bytes = (size_t)J * 4 * SG * 64 * sizeof(double);
   static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
+  static_assert(smem <= 220 * 1024, "Mt2 shared memory");
 };
 
 struct FastDiv {  // q = (umulhi(m, t) + t) >> sh == t / d for 0 <= t < 2^31
@@ -767,13 +768,41 @@ __device__ __forceinline__ ElemPos element_pos32(const GramParams &P, int t, Fas
   return e;
 }
 
-template <int G, int KIND>
-__global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd) {
-  using C = Mt2<G>;
+__device__ __forceinline__ uint32_t mt_smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// bounded parity wait (a broken protocol traps instead of hanging the GPU)
+__device__ __forceinline__ void mt_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = mt_smem_u32(bar);
+  for (uint32_t it = 0; it < (1u << 28); ++it) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();
+}
+__device__ __forceinline__ void mt_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mt_smem_u32(bar)) : "memory");
+}
+
+// NBUF = 2: one __syncthreads per tile (generation of tile i+1 and the DMMAs of
+// tile i between the same pair of barriers).  NBUF = 3: a ring with per-buffer
+// full/empty mbarriers (every thread arrives), so warps drift up to a tile apart
+// instead of draining the FP64 pipe at every tile boundary.
+template <int G, int SM, int NBUF, int KIND>
+__global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd) {
+  using C = Mt2<G, SM, NBUF>;
   constexpr int JPW = C::JPW, SG = C::SG, S = C::S, NW = C::NW, NT = C::NT, JG = C::JG;
   constexpr int PLANE = C::PLANE, ROWS = C::ROWS;
-  extern __shared__ __align__(16) double dsm[];  // tiles [2][re|im][S][G][32]; stage at level ends
+  extern __shared__ __align__(16) double dsm[];  // tiles [NBUF][re|im][S][G][32]; stage at level ends
   __shared__ double4 su[8 * G];
+  __shared__ __align__(8) uint64_t mb_full[NBUF], mb_empty[NBUF];
 
   const int64_t bdrop = blockIdx.x / P.n_split;
   const int split = blockIdx.x - (int)(bdrop * P.n_split);
@@ -787,6 +816,13 @@ __global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, F
     } else {
       su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: zero amplitude
     }
+  }
+  if (NBUF > 2 && tid == 0) {
+    for (int i = 0; i < NBUF; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mt_smem_u32(&mb_full[i])), "r"(NT));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mt_smem_u32(&mb_empty[i])), "r"(NT));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int jg = warp % JG, sg = warp / JG;
   int aoff[JPW], boff[JPW];  // fragment offsets of the job's two planes (row-major g1 <= g2 order)
@@ -804,6 +840,7 @@ __global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, F
   const int s0 = (int)min((int64_t)split * P.chunk, P.N);
   const int s1 = (int)min(P.N, (int64_t)s0 + P.chunk);
   int lv0 = 0;
+  uint32_t T = 0;  // tiles issued so far (ring position, uniform)
   for (int l = 0; l < P.n_lvl; ++l) {
     const int lv1 = (int)P.lvl_end[l];
     const int a = max(lv0, s0), b = min(lv1, s1);
@@ -837,11 +874,7 @@ __global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, F
         }
       }
     };
-    if (a < b) generate(a, 0);
-    __syncthreads();
-    int buf = 0;
-    for (int t0 = a; t0 < b; t0 += 4 * S, buf ^= 1) {
-      if (t0 + 4 * S < b) generate(t0 + 4 * S, buf ^ 1);
+    auto consume = [&](int buf) {
       const double *cre = dsm + buf * (2 * PLANE) + sg * (G * 32), *cim = cre + PLANE;
 #pragma unroll
       for (int si = 0; si < S / SG; ++si) {
@@ -856,7 +889,38 @@ __global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, F
           dmma(acc[k][3], ai, br);
         }
       }
+    };
+    if (NBUF == 2) {
+      if (a < b) generate(a, 0);
       __syncthreads();
+      int buf = 0;
+      for (int t0 = a; t0 < b; t0 += 4 * S, buf ^= 1) {
+        if (t0 + 4 * S < b) generate(t0 + 4 * S, buf ^ 1);
+        consume(buf);
+        __syncthreads();
+      }
+    } else {
+      const int n = b > a ? (b - a + 4 * S - 1) / (4 * S) : 0;
+      auto produce = [&](int i) {
+        const uint32_t tt = T + i;
+        const int bb = (int)(tt % NBUF);
+        if (tt >= NBUF) mt_wait(&mb_empty[bb], (tt / NBUF - 1) & 1);  // tile tt - NBUF consumed
+        generate(a + i * 4 * S, bb);
+        mt_arrive(&mb_full[bb]);
+      };
+#pragma unroll
+      for (int i = 0; i < NBUF - 1; ++i)
+        if (i < n) produce(i);
+      for (int i = 0; i < n; ++i) {
+        if (i + NBUF - 1 < n) produce(i + NBUF - 1);
+        const uint32_t tt = T + i;
+        const int bb = (int)(tt % NBUF);
+        mt_wait(&mb_full[bb], (tt / NBUF) & 1);
+        consume(bb);
+        mt_arrive(&mb_empty[bb]);
+      }
+      T += n;
+      __syncthreads();  // every warp's DMMAs done before the stage aliases the tiles
     }
     // stage [q][m][sg][8][8] (C fragment: row lane/4, cols 2(lane%4) + {0,1})
 #pragma unroll
@@ -892,18 +956,24 @@ __global__ void __launch_bounds__(Mt2<G>::NT, 1) gram_mt2_kernel(GramParams P, F
   }
 }
 
-template <int G, int KIND>
+template <int G, int SM, int NBUF, int KIND>
 void launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
-  using C = Mt2<G>;
+  using C = Mt2<G, SM, NBUF>;
   const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
-  cudaFuncSetAttribute(gram_mt2_kernel<G, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-  gram_mt2_kernel<G, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd);
+  cudaFuncSetAttribute(gram_mt2_kernel<G, SM, NBUF, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+  gram_mt2_kernel<G, SM, NBUF, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd);
 }
 
+// Tiles of 2*Mt2Cfg<G>::S steps.  Buffers: 2 (one barrier per tile) for G <= 4, the
+// 3-deep mbarrier ring above (measured on B200: cfg4 K=32 17.65 vs 18.50 ms with the
+// ring; cfg5 K=64 25.24 vs 25.79 ms).  XLMIMO_MT2=2|3 overrides.
 template <int G>
 void launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
-  if (P.kind == XLMIMO_ULA) launch_mt2_k<G, XLMIMO_ULA>(P, n_blocks, s);
-  else launch_mt2_k<G, XLMIMO_UPA>(P, n_blocks, s);
+  static const int env = getenv("XLMIMO_MT2") ? atoi(getenv("XLMIMO_MT2")) : 0;
+  const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
+  const bool ula = P.kind == XLMIMO_ULA;
+  if (nbuf == 2) ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
+  else ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
 }
 
 // ------------------------------------------------------------------ kernel B

@@ -72,6 +72,9 @@ CASES = [
     ("ula", 5000, 1, 140e9, 64, 2, (5.0, 100.0), (-60.0, 60.0), (0.0, 0.0)),    # K = 64
     ("upa", 37, 23, 100e9, 6, 3, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),    # UPA ragged, small K
     ("upa", 64, 64, 100e9, 32, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # UPA K = 32
+    ("ula", 2049, 1, 100e9, 20, 3, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),     # K = 20 (3 groups, odd N)
+    ("upa", 51, 29, 100e9, 45, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # K = 45 (6 groups, ragged UPA)
+    ("ula", 1500, 1, 140e9, 52, 2, (5.0, 100.0), (-60.0, 60.0), (0.0, 0.0)),    # K = 52 (7 groups)
 ]
 
 
@@ -219,6 +222,23 @@ def test_sweep_parity_reduced_cfg2(xl, orc):
     assert np.array_equal(res["n_valid"], nv)
     assert res["sat"][2] == sat[2]
     assert np.allclose(res["sat"][[0, 1, 3]], sat[[0, 1, 3]], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("K", [24, 40])
+def test_sweep_parity_many_users(xl, orc, K):
+    """Nested levels on the K > 16 DMMA kernel (level ends inside tiles, ring carried
+    across levels): per-drop rates vs the oracle's independent per-N Grams."""
+    n_list = [96, 200, 1000, 1536, 4000]
+    ag, ao = xl.Array.ula(4000, 100e9), orc.array("ula", n_y=4000, fc_hz=100e9)
+    ug = xl.Users.polar((2.0, 20.0), (-60.0, 60.0))
+    res = xl.saturation_sweep(ag, n_list, K, 4, [10.0], xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE, users=ug, seed=5,
+                              per_drop=True)
+    pos = xl.gen_drops(ug, K, 4, seed=5).cpu().numpy()
+    _, nv, _, pd = orc.saturation_sweep(ao, n_list, pos, [10.0], xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE, per_drop=True)
+    got = res["per_drop"].cpu().numpy()
+    both = np.isfinite(pd)
+    assert np.array_equal(np.isfinite(got), both) and np.array_equal(res["n_valid"], nv)
+    assert np.max(np.abs(got[both] - pd[both])) <= 1e-6
 
 
 def test_sweep_closed_form_parity(xl, orc):
