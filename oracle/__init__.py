@@ -84,6 +84,7 @@ def lib():
         L.or_sum_rate.argtypes = [vp, i32, i64, vp, i32, u32, vp, vp]
         L.or_saturation_coords.argtypes = [vp, i32, i64, d, vp, vp]
         L.or_sum_rate_mismatched.argtypes = [vp, vp, i32, i64, vp, i32, vp, vp]
+        L.or_bounds_app_a.argtypes = [vp, i32, i64, vp, i32, vp, vp, vp, vp, i32]
         L.or_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp]
         L.or_saturation_sweep.argtypes = [P(OrArray), vp, i32, vp, i32, i64, vp, i32, u32, i32, d,
                                           vp, vp, vp, vp, i32]
@@ -209,6 +210,39 @@ def sum_rate_mismatched(gram: np.ndarray, gram_model: np.ndarray, snr_db):
     fl = np.zeros(D, dtype=np.uint32)
     lib().or_sum_rate_mismatched(_ptr(g), _ptr(gm), K, D, _ptr(snr), snr.size, _ptr(rates), _ptr(fl))
     return rates, fl
+
+
+def gram_exact_blas(arr: OrArray, pos: np.ndarray) -> np.ndarray:
+    """Exact Gram for large K (Appendix A at K up to 1000): H from the oracle's own
+    Eq. (3) coefficients (channel_matrix), then G = H^H H by one library matmul
+    (PAPER.md:74).  Same definition as gram_exact (pinned equal at small sizes);
+    only the summation order differs."""
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    out = []
+    for d in range(pos.shape[0]):
+        H = channel_matrix(arr, pos[d])
+        G = H.conj().T @ H
+        G = 0.5 * (G + G.conj().T)  # exact Hermitian symmetry (R20); Im diag = 0
+        np.fill_diagonal(G, G.diagonal().real)
+        out.append(G)
+    return np.stack(out)
+
+
+def bounds_app_a(gram: np.ndarray, snr_db, eig: bool = False, nthreads: int = 0):
+    """Appendix A per drop, NEXT-3.
+    Returns rstat (D, 2) = (log2 det R, gap = -(1/K) log2 det R), bounds (D, S, 3) =
+    (log2 U, log2 det(I + rho G), log2 L), eigenvalues of R (D, K) ascending (cyclic
+    Jacobi) or None, flags (D,)."""
+    g = np.ascontiguousarray(np.stack([gram.real, gram.imag], axis=-1), dtype=np.float64)
+    D, K = g.shape[0], g.shape[1]
+    snr = np.ascontiguousarray(np.atleast_1d(snr_db), dtype=np.float64)
+    rstat = np.zeros((D, 2))
+    bounds = np.zeros((D, snr.size, 3))
+    ev = np.zeros((D, K)) if eig else None
+    fl = np.zeros(D, dtype=np.uint32)
+    lib().or_bounds_app_a(_ptr(g), K, D, _ptr(snr), snr.size, _ptr(rstat), _ptr(bounds),
+                          _ptr(ev) if ev is not None else None, _ptr(fl), nthreads)
+    return rstat, bounds, ev, fl
 
 
 def gen_drops_rect(x, y, K: int, n_drops: int, seed: int = 0, first_drop: int = 0) -> np.ndarray:

@@ -666,3 +666,157 @@ void or_saturation_sweep(const or_array_t *a_in, const int64_t *n_list, int32_t 
     sat[3] = sqrt(var > 0 ? var : 0.0) / sqrt(D);
     free(up); free(dn); free(g); free(rt); free(fl);
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-3: Appendix A, per drop, in the paper's order.    */
+/*   a_i  = rho G_ii, the diagonal of (P/sigma_n^2) H^H H;    */
+/*   U    = prod_i (1 + a_i), Hadamard's upper bound;    */
+/*   R_ij = G_ij / (||h_i|| ||h_j||), the correlation matrix; */
+/*   L    = det(R) prod_i (1 + a_i), the Schur-Horn lower bound; */
+/*   C    = log2 det(I + rho G), the capacity they bracket (Eq. 9);          */
+/*   gap  = -log2 det(R) / sum_i log2(1 + 1) = -(1/K) log2 det R, the        */
+/*          maximised normalised gap of Eq. (eq9), whose   */
+/*          last line is -E_K[log2 lambda^R] (same number; pinned by the     */
+/*          eigenvalues below).                                             */
+/*   rstat[d][2]     = { log2 det R, gap }                                  */
+/*   bounds[d][s][3] = { log2 U, C, log2 L } for rho = 10^(snr_db[s]/10)     */
+/*   eig[d][K] (optional) = eigenvalues of R ascending, by cyclic Jacobi.    */
+/* flags: bit0 R (= G scaled) not PD -> log2 det R, gap, log2 L NaN; bit1    */
+/* I + rho G not PD -> C NaN; bit2 some G_ii <= 0 -> everything NaN (R is    */
+/* undefined); bit4 non-finite G -> everything NaN.                          */
+/* ------------------------------------------------------------------------ */
+
+/* Eigenvalues of a Hermitian K x K matrix A ([K][K][2], destroyed) by the cyclic
+ * Jacobi method: for each (p < q) with A_pq != 0, make A_pq real by the phase
+ * rotation S = diag(.., e^{-j phi} at q, ..), then zero it with the real plane
+ * rotation of Numerical Recipes 11.1 (theta = (a_qq - a_pp) / (2|a_pq|),
+ * t = sgn(theta) / (|theta| + sqrt(theta^2 + 1))).  Sweeps until the off-diagonal
+ * mass is below 1e-30 of the total.  ev ascending. */
+static void or_jacobi_eig(double *A, int K, double *ev)
+{
+#define OR_A(i, j) (A + ((size_t)(i) * K + (j)) * 2)
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j) {
+                const double m = OR_A(i, j)[0] * OR_A(i, j)[0] + OR_A(i, j)[1] * OR_A(i, j)[1];
+                tot += m;
+                if (i != j) off += m;
+            }
+        if (off <= 1e-30 * tot) break;
+        for (int p = 0; p < K - 1; ++p)
+            for (int q = p + 1; q < K; ++q) {
+                const double br = OR_A(p, q)[0], bi = OR_A(p, q)[1];
+                const double b = sqrt(br * br + bi * bi);
+                if (b == 0.0) continue;
+                /* phase: column q times e^{-j phi}, row q times e^{+j phi}, phi = arg A_pq */
+                const double cr = br / b, ci = -bi / b; /* e^{-j phi} */
+                for (int r = 0; r < K; ++r) {
+                    double *x = OR_A(r, q); /* x *= e^{-j phi} */
+                    const double xr = x[0] * cr - x[1] * ci, xi = x[0] * ci + x[1] * cr;
+                    x[0] = xr; x[1] = xi;
+                }
+                for (int r = 0; r < K; ++r) {
+                    double *x = OR_A(q, r); /* x *= e^{+j phi} */
+                    const double xr = x[0] * cr + x[1] * ci, xi = -x[0] * ci + x[1] * cr;
+                    x[0] = xr; x[1] = xi;
+                }
+                /* now A_pq = b (real); the real rotation */
+                const double app = OR_A(p, p)[0], aqq = OR_A(q, q)[0];
+                const double theta = (aqq - app) / (2.0 * b);
+                double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+                if (theta < 0.0) t = -t;
+                const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int r = 0; r < K; ++r) {
+                    if (r == p || r == q) continue;
+                    double *xp = OR_A(r, p), *xq = OR_A(r, q);
+                    const double pr = c * xp[0] - s * xq[0], pi = c * xp[1] - s * xq[1];
+                    const double qr = s * xp[0] + c * xq[0], qi = s * xp[1] + c * xq[1];
+                    xp[0] = pr; xp[1] = pi; xq[0] = qr; xq[1] = qi;
+                    OR_A(p, r)[0] = pr; OR_A(p, r)[1] = -pi; /* Hermitian mirror */
+                    OR_A(q, r)[0] = qr; OR_A(q, r)[1] = -qi;
+                }
+                OR_A(p, p)[0] = app - t * b; OR_A(p, p)[1] = 0.0;
+                OR_A(q, q)[0] = aqq + t * b; OR_A(q, q)[1] = 0.0;
+                OR_A(p, q)[0] = OR_A(p, q)[1] = 0.0;
+                OR_A(q, p)[0] = OR_A(q, p)[1] = 0.0;
+            }
+    }
+    for (int i = 0; i < K; ++i) ev[i] = OR_A(i, i)[0];
+    for (int i = 1; i < K; ++i) { /* insertion sort, ascending */
+        const double v = ev[i];
+        int j = i - 1;
+        while (j >= 0 && ev[j] > v) { ev[j + 1] = ev[j]; --j; }
+        ev[j + 1] = v;
+    }
+#undef OR_A
+}
+
+void or_bounds_app_a(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
+                     double *rstat, double *bounds, double *eig, uint32_t *flags, int32_t nthreads)
+{
+    int nt = or_threads(nthreads);
+    (void)nt;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+    for (int64_t d = 0; d < n_drops; ++d) {
+        const double *G = gram + (size_t)d * K * K * 2;
+        double *rs = rstat + (size_t)d * 2, *bo = bounds + (size_t)d * n_snr * 3;
+        double *ev = eig ? eig + (size_t)d * K : NULL;
+        uint32_t fl = 0;
+        int finite = 1, diag_ok = 1;
+        for (int e = 0; e < 2 * K * K; ++e) finite &= isfinite(G[e]) ? 1 : 0;
+        for (int i = 0; i < K && finite; ++i) diag_ok &= G[(i * K + i) * 2] > 0.0;
+        if (!finite || !diag_ok) {
+            fl |= finite ? 4u : 16u;
+            rs[0] = rs[1] = NAN;
+            for (int e = 0; e < 3 * n_snr; ++e) bo[e] = NAN;
+            if (ev) for (int i = 0; i < K; ++i) ev[i] = NAN;
+            if (flags) flags[d] = fl;
+            continue;
+        }
+        double *R = (double *)malloc(sizeof(double) * 2 * K * K);
+        double *Lf = (double *)malloc(sizeof(double) * 2 * K * K);
+        double *A = (double *)malloc(sizeof(double) * 2 * K * K);
+        /* R_ij = G_ij / sqrt(G_ii G_jj); ||h_i||^2 = G_ii */
+        for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j) {
+                const double s = sqrt(G[(i * K + i) * 2] * G[(j * K + j) * 2]);
+                R[(i * K + j) * 2] = (i == j) ? 1.0 : G[(i * K + j) * 2] / s;
+                R[(i * K + j) * 2 + 1] = (i == j) ? 0.0 : G[(i * K + j) * 2 + 1] / s;
+            }
+        double ldr = NAN;
+        if (or_cholesky(R, K, Lf) == 0) {
+            ldr = 0.0; /* log2 det R = 2 sum log2 L_kk */
+            for (int k = 0; k < K; ++k) ldr += 2.0 * log2(Lf[(k * K + k) * 2]);
+        } else {
+            fl |= 1u;
+        }
+        rs[0] = ldr;
+        rs[1] = -ldr / (double)K; /* -log2 det R / sum_i log2(1 + 1)  (Eq. eq9) */
+        for (int s = 0; s < n_snr; ++s) {
+            const double rho = pow(10.0, snr_db[s] / 10.0);
+            double lu = 0.0;
+            for (int i = 0; i < K; ++i) lu += log2(1.0 + rho * G[(i * K + i) * 2]); /* log2 U */
+            for (int i = 0; i < K; ++i)
+                for (int j = 0; j < K; ++j) {
+                    A[(i * K + j) * 2] = (i == j ? 1.0 : 0.0) + rho * G[(i * K + j) * 2];
+                    A[(i * K + j) * 2 + 1] = rho * G[(i * K + j) * 2 + 1];
+                }
+            double cap = NAN;
+            if (or_cholesky(A, K, Lf) == 0) {
+                cap = 0.0;
+                for (int k = 0; k < K; ++k) cap += 2.0 * log2(Lf[(k * K + k) * 2]);
+            } else {
+                fl |= 2u;
+            }
+            bo[3 * s + 0] = lu;
+            bo[3 * s + 1] = cap;
+            bo[3 * s + 2] = ldr + lu; /* log2 L = log2 det R + log2 U */
+        }
+        if (ev) or_jacobi_eig(R, K, ev); /* R is not needed after this */
+        free(R);
+        free(Lf);
+        free(A);
+        if (flags) flags[d] = fl;
+    }
+}

@@ -577,3 +577,138 @@ def test_rect_drops_law(orc):
     assert abs(pos[..., 0].mean() - 5.5) < 4 * 9 / math.sqrt(12) / math.sqrt(pos[..., 0].size)
     assert abs(pos[..., 1].mean()) < 4 * 15 / math.sqrt(12) / math.sqrt(pos[..., 1].size)
     assert np.array_equal(orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 8, 10, seed=4, first_drop=7), pos[7:17])
+
+
+# --------------------------------------------------------------------------- NEXT-3: Appendix A
+def _app_a_grams(orc):
+    """Exact Grams of the paper's E1/E3 user field, 100 GHz, a few K and M."""
+    out = []
+    for K, M, seed in [(3, 512, 1), (8, 4096, 2), (16, 2048, 3), (5, 64, 4)]:
+        pos = orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 6, seed=seed)
+        out.append(orc.gram_exact(orc.array("ula", n_y=M, fc_hz=100e9), pos))
+    return out
+
+
+def test_gram_exact_blas_equals_compensated_loops(orc):
+    """The large-K oracle Gram (library matmul of the Eq. (3) H) is the same definition
+    as the Neumaier loops."""
+    a = orc.array("ula", n_y=700, fc_hz=100e9)
+    pos = orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 12, 3, seed=5)
+    assert normalized_err(orc.gram_exact_blas(a, pos), orc.gram_exact(a, pos)) < 1e-14
+
+
+def test_app_a_bounds_bracket_capacity(orc):
+    """Hadamard U >= det(I + rho G) >= det(R) prod(1 + a_i) = L, for
+    every drop and received SNR (the paper's range 0..30 dB and beyond)."""
+    snr = [-10.0, 0.0, 10.0, 30.0, 60.0]
+    for G in _app_a_grams(orc):
+        rs, bo, _, fl = orc.bounds_app_a(G, snr)
+        assert np.all(fl == 0)
+        lu, cap, ll = bo[..., 0], bo[..., 1], bo[..., 2]
+        assert np.all(lu >= cap - 1e-12) and np.all(cap >= ll - 1e-12)
+        # log2 L - log2 U = log2 det R <= 0 (Hadamard on R)
+        assert np.all(rs[:, 0] <= 1e-14)
+
+
+def test_app_a_against_lapack_and_determinant_identity(orc):
+    """Each output against numpy.linalg (LAPACK): log2 U from the diagonal, C by slogdet,
+    log2 det R by slogdet of D^{-1/2} G D^{-1/2}, and the decomposition of PAPER.md:300-305,
+    det(rho G) = det(P) det(R) with P = Diag(a_i)."""
+    snr = [0.0, 20.0]
+    for G in _app_a_grams(orc):
+        rs, bo, _, _ = orc.bounds_app_a(G, snr)
+        K = G.shape[1]
+        for d in range(G.shape[0]):
+            g = G[d]
+            dg = np.real(np.diag(g))
+            R = g / np.sqrt(np.outer(dg, dg))
+            ldr = np.linalg.slogdet(R)[1] / math.log(2)
+            assert abs(rs[d, 0] - ldr) < 1e-10 * max(1.0, abs(ldr))
+            assert abs(rs[d, 1] + ldr / K) < 1e-10
+            for s, sdb in enumerate(snr):
+                rho = 10 ** (sdb / 10)
+                cap = np.linalg.slogdet(np.eye(K) + rho * g)[1] / math.log(2)
+                lu = np.sum(np.log2(1 + rho * dg))
+                assert abs(bo[d, s, 0] - lu) < 1e-12 * lu
+                assert abs(bo[d, s, 1] - cap) < 1e-10 * cap
+                assert abs(bo[d, s, 2] - (ldr + lu)) < 1e-10 * lu
+                ldp = np.linalg.slogdet(rho * g)[1] / math.log(2)
+                assert abs(ldp - (np.sum(np.log2(rho * dg)) + rs[d, 0])) < 1e-9 * abs(ldp)
+
+
+def test_app_a_two_users_and_subset_expansion(orc):
+    """K = 2 by hand: det R = 1 - |r_12|^2, U = (1+a1)(1+a2), L = (1-|r|^2)(1+a1)(1+a2),
+    C = 1 + a1 + a2 + a1 a2 (1 - |r|^2).  K = 3: det(I + P^1/2 R P^1/2) is the sum over
+    subsets S of prod_{i in S} a_i det R_S (principal minors), so C >= L term by term."""
+    a = orc.array("ula", n_y=300, fc_hz=100e9)
+    pos = orc.gen_drops_rect((1.0, 3.0), (-1.0, 1.0), 2, 10, seed=11)
+    G = orc.gram_exact(a, pos)
+    rs, bo, _, _ = orc.bounds_app_a(G, [3.0])
+    rho = 10 ** 0.3
+    for d in range(10):
+        a1, a2 = rho * G[d, 0, 0].real, rho * G[d, 1, 1].real
+        r2 = abs(G[d, 0, 1]) ** 2 / (G[d, 0, 0].real * G[d, 1, 1].real)
+        assert abs(2 ** rs[d, 0] - (1 - r2)) < 1e-12
+        assert abs(2 ** bo[d, 0, 0] - (1 + a1) * (1 + a2)) < 1e-12 * (1 + a1) * (1 + a2)
+        assert abs(2 ** bo[d, 0, 1] - (1 + a1 + a2 + a1 * a2 * (1 - r2))) < 1e-11 * (1 + a1) * (1 + a2)
+        assert abs(2 ** bo[d, 0, 2] - (1 - r2) * (1 + a1) * (1 + a2)) < 1e-11 * (1 + a1) * (1 + a2)
+    pos3 = orc.gen_drops_rect((1.0, 3.0), (-1.0, 1.0), 3, 5, seed=12)
+    G3 = orc.gram_exact(a, pos3)
+    _, bo3, _, _ = orc.bounds_app_a(G3, [0.0])
+    import itertools
+    for d in range(5):
+        dg = G3[d].diagonal().real
+        R = G3[d] / np.sqrt(np.outer(dg, dg))
+        tot = 0.0
+        for n in range(4):
+            for S in itertools.combinations(range(3), n):
+                minor = np.linalg.det(R[np.ix_(S, S)]).real if S else 1.0
+                tot += np.prod(dg[list(S)]) * minor
+        assert abs(2 ** bo3[d, 0, 1] - tot) < 1e-11 * tot
+
+
+def test_app_a_eigenvalues_jacobi(orc):
+    """-E_K[log2 lambda^R]: the Jacobi eigenvalues of R equal LAPACK's
+    eigvalsh, sum to tr R = K, and their mean log2 is minus the gap (from Cholesky)."""
+    for G in _app_a_grams(orc):
+        rs, _, ev, _ = orc.bounds_app_a(G, [0.0], eig=True)
+        dg = np.real(np.diagonal(G, axis1=1, axis2=2))
+        R = G / np.sqrt(dg[:, :, None] * dg[:, None, :])
+        K = G.shape[1]
+        assert np.max(np.abs(ev - np.linalg.eigvalsh(R))) < 1e-12
+        assert np.max(np.abs(ev.sum(1) - K)) < 1e-12 * K
+        assert np.max(np.abs(-np.mean(np.log2(ev), axis=1) - rs[:, 1])) < 1e-12
+        assert np.all(np.diff(ev, axis=1) >= 0)
+
+
+def test_app_a_diagonal_gram_and_flags(orc):
+    """Orthogonal users (diagonal G): R = I, det R = 1, gap 0, L = U = C.  A zero
+    diagonal or non-finite entry gives NaN + flag; an indefinite G flags bit 0."""
+    G = np.zeros((3, 4, 4), complex)
+    G[0] = np.diag([1.0, 2.0, 3.0, 4.0])
+    G[1] = np.diag([1.0, 0.0, 3.0, 4.0])
+    G[2] = np.diag([1.0, 2.0, np.inf, 4.0])
+    rs, bo, ev, fl = orc.bounds_app_a(G, [10.0], eig=True)
+    assert rs[0, 0] == 0.0 and rs[0, 1] == 0.0 and np.allclose(ev[0], 1.0)
+    assert abs(bo[0, 0, 0] - bo[0, 0, 1]) < 1e-13 and bo[0, 0, 2] == bo[0, 0, 0]
+    assert fl[1] == 4 and np.all(np.isnan(bo[1])) and fl[2] == 16 and np.all(np.isnan(rs[2]))
+    Gi = np.array([[[1.0, 2.0], [2.0, 1.0]]], complex)  # |r| = 2: not a correlation matrix
+    rs, bo, _, fl = orc.bounds_app_a(Gi, [0.0])
+    assert fl[0] & 1 and np.isnan(rs[0, 0]) and np.isnan(bo[0, 0, 2]) and np.isfinite(bo[0, 0, 0])
+
+
+def test_app_a_paper_gap_k1000(orc):
+    """PAPER.md:331-335 (Fig. K_vs_E): with the Sec. IV-C user field (x ~ U[1, 10] m,
+    y ~ U[-7.5, 7.5] m, 100 GHz) the negative empirical expectation
+    -E_K[log2 lambda^R] grows with K and reaches 0.064 at K = 1000.  Array: M = 35 000
+    elements (the E1 ergodic saturation size; the paper does not state M).
+    One drop at K = 1000 (the mean over 1000 eigenvalues is already self-averaging)."""
+    a = orc.array("ula", n_y=35000, fc_hz=100e9)
+    gaps = {}
+    for K, D in [(10, 4), (100, 4), (1000, 1)]:
+        pos = orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=0)
+        rs, _, _, fl = orc.bounds_app_a(orc.gram_exact_blas(a, pos), [0.0])
+        assert np.all(fl == 0)
+        gaps[K] = float(np.mean(rs[:, 1]))
+    assert gaps[10] < gaps[100] < gaps[1000]
+    assert abs(gaps[1000] - 0.064) < 1.0e-3, gaps
