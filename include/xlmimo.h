@@ -40,7 +40,7 @@ extern "C" {
 typedef enum {
     XLMIMO_OK = 0,
     XLMIMO_EINVAL = -1,        /* bad argument (null pointer, K<1, N<1, fc<=0, |az|>=90, t not in (0,1), ...) */
-    XLMIMO_EUNSUPPORTED = -2,  /* valid but not provided (closed form for a UPA; K > 64 on a fused path) */
+    XLMIMO_EUNSUPPORTED = -2,  /* valid but not provided (closed form for a UPA; K beyond a path's limit) */
     XLMIMO_EWORKSPACE = -3,    /* workspace smaller than the matching *_workspace() query */
     XLMIMO_ECUDA = -4          /* CUDA launch / runtime error (text in xlmimo_last_error) */
 } xlmimo_status_t;
@@ -101,9 +101,11 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  *   mode XLMIMO_FUSED: H is never materialised.  XLMIMO_MATERIALIZED: H is
  *     written to the workspace as planar complex64 and streamed back (fp32 only).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
- * Im G(i,i) = 0.  K <= 64.  ws may be NULL iff the query returns 0.
- * EINVAL: bad array/arguments; EUNSUPPORTED: K > 64, or FP64 + MATERIALIZED;
- * EWORKSPACE: ws_bytes too small. */
+ * Im G(i,i) = 0.  K <= 1024: K <= 64 on every precision/mode; 64 < K <= 1024 fused
+ * fp64 only (block pairs of 64 users on DMMA; NEXT-3/E1-E3 user counts, PAPER.md:228,
+ * 331-335).  ws may be NULL iff the query returns 0.
+ * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 not fused fp64, or
+ * FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
 XLMIMO_API size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops,
                                    int32_t precision, int32_t mode);
 XLMIMO_API int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,
@@ -133,9 +135,43 @@ XLMIMO_API int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double
  * gram (dev [n_drops][K][K][2]); snr_db (host [n_snr], n_snr <= 16);
  * rates (dev [n_drops][n_snr][popcount(receivers)]); flags (dev [n_drops] or NULL):
  * OR-ed with the XLMIMO_FLAG_* bits (so a closed-form DEGENERATE bit survives).
- * A failed Cholesky gives NaN for the receivers it feeds (R10).  K <= 64. */
+ * A failed Cholesky gives NaN for the receivers it feeds (R10).  K <= 64 (no
+ * workspace); for 64 < K <= 1024 use xlmimo_sum_rate_ws (CAP and MRC only). */
 XLMIMO_API int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
                     uint32_t receivers, double *rates, uint32_t *flags, void *stream);
+
+/* The same receivers with a caller workspace, for K up to 1024.  For K > 64 CAP
+ * comes from a tiled Cholesky of I + rho G in the workspace (one CTA per matrix,
+ * 32 x 32 complex tiles) and MRC straight from G; ZF/MMSE (diagonal of an
+ * inverse) return EUNSUPPORTED for K > 64.  The workspace query returns 0 when
+ * none is needed (K <= 64, or no CAP); ws may then be NULL.
+ * EWORKSPACE: ws_bytes below the query. */
+XLMIMO_API size_t xlmimo_sum_rate_workspace(int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers);
+XLMIMO_API int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const double *snr_db,
+                                  int32_t n_snr, uint32_t receivers, double *rates, uint32_t *flags, void *ws,
+                                  size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------- NEXT-3
+ * Appendix A per drop: with a_i = rho G_ii (the diagonal of
+ * (P/sigma_n^2) H^H H) and R_ij = G_ij / sqrt(G_ii G_jj),
+ *   rstat  (dev [n_drops][2])        = { log2 det R, gap = -log2 det(R) / K }  -- the
+ *            maximised normalised gap (U - L)/U of Eq. (eq9), = -E_K[log2 lambda^R]
+ *            (PAPER.md:318-327);
+ *   bounds (dev [n_drops][n_snr][3]) = { log2 U, log2 det(I + rho G), log2 L } with
+ *            U = prod(1 + a_i) (Hadamard) and L = det(R) U
+ *            (Schur-Horn), so log2 U >= C >= log2 L;
+ *   eig    (dev [n_drops][K] or NULL, K <= 64) = eigenvalues of R ascending (cyclic
+ *            Jacobi), whose mean log2 is -gap;
+ *   flags  (dev [n_drops] or NULL, SET): G_NOT_PD (R not PD: log2 det R, gap, log2 L
+ *            NaN), A_NOT_PD (I + rho G not PD for some SNR: that C NaN), MRC_UNDEF
+ *            (some G_ii <= 0: R undefined, all NaN), NONFINITE (all NaN).
+ * gram dev [n_drops][K][K][2]; snr_db host [n_snr] (<= 16).  K <= 1024; K > 64 needs
+ * the workspace of the query (tiled Cholesky slots), K <= 64 none.
+ * EUNSUPPORTED: K > 1024, or eig with K > 64.  EWORKSPACE: ws_bytes below the query. */
+XLMIMO_API size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr);
+XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const double *snr_db,
+                                   int32_t n_snr, double *rstat, double *bounds, double *eig, uint32_t *flags,
+                                   void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------- a1..a6
  * Capacity-vs-N saturation sweep.  ULA only.  For every N in
@@ -150,6 +186,8 @@ XLMIMO_API int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, c
  *            PAPER.md:228) and M_sat = ceil((E[y_up]-E[y_down]) / pitch) (R15),
  *   per_drop (dev [n_drops][n_n][n_snr][n_recv] or NULL).
  * array->n_y is ignored (the grid is n_list).  Synchronises `stream` before return.
+ * K <= 1024; for K > 64 the exact Gram is fp64 and the receivers CAP/MRC only
+ * (EUNSUPPORTED otherwise) -- the paper's K = 100 curves.
  * EINVAL also for n_list not ascending / mixed parity, t not in (0,1). */
 XLMIMO_API size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                                          int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers,

@@ -9,7 +9,9 @@ There is no CPU fallback: importing this package without the built library,
 or calling it without a CUDA device, raises.
 
 Function names follow the ABI: gen_drops, gram_exact, gram_closed_form,
-sum_rate, saturation_sweep (+ saturation_sweep_host, the host-buffer entry).
+sum_rate, saturation_sweep (+ saturation_sweep_host, the host-buffer entry),
+and the widened rows sum_rate_mismatched (NEXT-1), app_a_bounds (NEXT-3),
+gen_drops_rect (NEXT-4).
 """
 from __future__ import annotations
 
@@ -18,7 +20,8 @@ import os
 
 import torch
 
-__all__ = ["Array", "Users", "gen_drops", "gram_exact", "gram_closed_form", "sum_rate", "saturation_sweep",
+__all__ = ["Array", "Users", "gen_drops", "gram_exact", "gram_closed_form", "sum_rate", "sum_rate_mismatched",
+           "gen_drops_rect", "app_a_bounds", "saturation_sweep",
            "saturation_sweep_host", "launch_count", "lib_path", "XlmimoError",
            "ULA", "UPA", "FP64", "FP32", "FUSED", "MATERIALIZED", "GRAM_EXACT", "GRAM_CLOSED_FORM",
            "RECV_CAP", "RECV_ZF", "RECV_MMSE", "RECV_MRC", "n_recv"]
@@ -82,6 +85,12 @@ def _load():
     L.xlmimo_gram_exact.argtypes = [P(Array), vp, i32, i64, i32, i32, vp, vp, sz, vp]
     L.xlmimo_gram_closed_form.argtypes = [P(Array), vp, i32, i64, vp, vp, vp]
     L.xlmimo_sum_rate.argtypes = [vp, i32, i64, vp, i32, u32, vp, vp, vp]
+    L.xlmimo_sum_rate_workspace.argtypes = [i32, i64, i32, u32]
+    L.xlmimo_sum_rate_workspace.restype = sz
+    L.xlmimo_sum_rate_ws.argtypes = [vp, i32, i64, vp, i32, u32, vp, vp, vp, sz, vp]
+    L.xlmimo_app_a_bounds_workspace.argtypes = [i32, i64, i32]
+    L.xlmimo_app_a_bounds_workspace.restype = sz
+    L.xlmimo_app_a_bounds.argtypes = [vp, i32, i64, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.xlmimo_saturation_sweep_workspace.argtypes = [P(Array), vp, i32, i32, i64, i32, u32, i32, i32]
     L.xlmimo_saturation_sweep_workspace.restype = sz
     L.xlmimo_saturation_sweep.argtypes = [P(Array), vp, i32, P(Users), vp, i32, i64, u64, vp, i32, u32, i32, i32, d,
@@ -97,7 +106,8 @@ def _load():
     L.xlmimo_last_error.restype = ctypes.c_char_p
     L.xlmimo_launch_count.restype = u64
     for name in ("xlmimo_gen_drops", "xlmimo_gram_exact", "xlmimo_gram_closed_form", "xlmimo_sum_rate",
-                 "xlmimo_saturation_sweep", "xlmimo_saturation_sweep_host"):
+                 "xlmimo_sum_rate_ws", "xlmimo_app_a_bounds", "xlmimo_saturation_sweep",
+                 "xlmimo_saturation_sweep_host"):
         getattr(L, name).restype = ctypes.c_int
     return L
 
@@ -187,17 +197,44 @@ def gram_closed_form(array: Array, pos: torch.Tensor, stream=None):
 
 
 # --------------------------------------------------------------------------- a5
-def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | None = None, stream=None):
-    """Receivers per drop: rates [D, n_snr, n_recv] (bits/s/Hz) and flags [D] (OR-ed into `flags`)."""
+def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | None = None,
+             ws: torch.Tensor | None = None, stream=None):
+    """Receivers per drop: rates [D, n_snr, n_recv] (bits/s/Hz) and flags [D] (OR-ed into `flags`).
+    K <= 64: all receivers; 64 < K <= 1024: CAP and MRC (tiled Cholesky in a workspace)."""
     _need_cuda()
     g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
     D, K = g.shape[0], g.shape[1]
     snr = _f64_host(snr_db)
     rates = torch.empty((D, snr.size, n_recv(receivers)), dtype=torch.float64, device=g.device)
     fl = flags if flags is not None else torch.zeros(D, dtype=torch.int32, device=g.device)
-    _check(_L.xlmimo_sum_rate(_dptr(g), K, D, _hptr(snr), snr.size, receivers, _dptr(rates), _dptr(fl),
-                              _stream(stream)), "xlmimo_sum_rate")
+    need = int(_L.xlmimo_sum_rate_workspace(K, D, snr.size, receivers))
+    if need and (ws is None or ws.numel() < need):
+        ws = _workspace(need, g.device)
+    _check(_L.xlmimo_sum_rate_ws(_dptr(g), K, D, _hptr(snr), snr.size, receivers, _dptr(rates), _dptr(fl),
+                                 _dptr(ws) if need else None, ws.numel() if need else 0, _stream(stream)),
+           "xlmimo_sum_rate_ws")
     return rates, fl
+
+
+def app_a_bounds(gram: torch.Tensor, snr_db, eig: bool = False, ws: torch.Tensor | None = None, stream=None):
+    """NEXT-3, Appendix A per drop.  Returns rstat [D, 2] = (log2 det R,
+    gap = -log2 det(R)/K), bounds [D, n_snr, 3] = (log2 U, log2 det(I + rho G), log2 L),
+    eigenvalues of R [D, K] ascending (K <= 64) or None, flags [D]."""
+    _need_cuda()
+    g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
+    D, K = g.shape[0], g.shape[1]
+    snr = _f64_host(snr_db)
+    rstat = torch.empty((D, 2), dtype=torch.float64, device=g.device)
+    bounds = torch.empty((D, snr.size, 3), dtype=torch.float64, device=g.device)
+    ev = torch.empty((D, K), dtype=torch.float64, device=g.device) if eig else None
+    fl = torch.zeros(D, dtype=torch.int32, device=g.device)
+    need = int(_L.xlmimo_app_a_bounds_workspace(K, D, snr.size))
+    if need and (ws is None or ws.numel() < need):
+        ws = _workspace(need, g.device)
+    _check(_L.xlmimo_app_a_bounds(_dptr(g), K, D, _hptr(snr), snr.size, _dptr(rstat), _dptr(bounds),
+                                  _dptr(ev) if ev is not None else None, _dptr(fl), _dptr(ws) if need else None,
+                                  ws.numel() if need else 0, _stream(stream)), "xlmimo_app_a_bounds")
+    return rstat, bounds, ev, fl
 
 
 def sum_rate_mismatched(gram: torch.Tensor, gram_model: torch.Tensor, snr_db, flags: torch.Tensor | None = None,

@@ -67,8 +67,8 @@ struct SweepWs {
   double *pos, *grams, *rates, *erg, *sat;
   int64_t *nval;
   uint32_t *flags;
-  void *gws;
-  size_t gws_bytes;
+  void *gws, *rws;
+  size_t gws_bytes, rws_bytes;
   size_t total;
 };
 
@@ -91,6 +91,9 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
     w.gws_bytes = xlh::gram_ws_bytes(big, K, D, n_n, precision, XLMIMO_FUSED);
   }
   w.gws = c.take(w.gws_bytes);
+  // K > 64: receivers through the large-K path (CAP by Cholesky slots, MRC)
+  w.rws_bytes = (K > xl::kMaxK && (receivers & XLMIMO_RECV_CAP)) ? xlh::large_k_ws_bytes(K, D * n_n, n_snr) : 0;
+  w.rws = c.take(w.rws_bytes);
   w.total = c.off;
   return w;
 }
@@ -105,7 +108,12 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
     if (i && n_list[i] <= n_list[i - 1]) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_list not ascending");
     if ((n_list[i] & 1) != (n_list[0] & 1)) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_list mixed parity");
   }
-  if (K < 1 || K > xl::kMaxK) return xlh::set_error(K < 1 ? XLMIMO_EINVAL : XLMIMO_EUNSUPPORTED, "sweep: K=%d", K);
+  if (K < 1 || K > xl::kMaxKLarge)
+    return xlh::set_error(K < 1 ? XLMIMO_EINVAL : XLMIMO_EUNSUPPORTED, "sweep: K=%d", K);
+  if (K > xl::kMaxK && (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)))
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: ZF/MMSE need K <= %d (K=%d)", xl::kMaxK, K);
+  if (K > xl::kMaxK && gram_kind == XLMIMO_GRAM_EXACT && precision != XLMIMO_FP64)
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: K=%d > %d is fp64 only", K, xl::kMaxK);
   if (n_drops < 1) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_drops < 1");
   if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_snr out of [1,16]");
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sweep: receivers");
@@ -148,7 +156,12 @@ int run_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, c
   double *rates = per_drop ? per_drop : w.rates;
   if (cudaMemsetAsync(w.flags, 0, (size_t)n_drops * n_n * sizeof(uint32_t), s) != cudaSuccess)
     return xlh::check_launch("sweep: memset flags");
-  if ((rc = xlh::launch_sum_rate(w.grams, K, n_drops * n_n, snr_db, n_snr, receivers, rates, w.flags, s))) return rc;
+  if (K > xl::kMaxK)
+    rc = xlh::launch_sum_rate_large(w.grams, K, n_drops * n_n, snr_db, n_snr, receivers, rates, w.flags, w.rws,
+                                    w.rws_bytes, s);
+  else
+    rc = xlh::launch_sum_rate(w.grams, K, n_drops * n_n, snr_db, n_snr, receivers, rates, w.flags, s);
+  if (rc) return rc;
   const int n_out = n_n * n_snr * n_recv_of(receivers);
   if ((rc = xlh::launch_ergodic_reduce(rates, n_drops, n_out, w.erg, w.nval, s))) return rc;
   if ((rc = xlh::launch_saturation_stats(P, K, n_drops, t, ap.pitch, w.sat, s))) return rc;
@@ -267,7 +280,8 @@ int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t n_drops, ui
 
 size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops, int32_t precision,
                                    int32_t mode) {
-  if (bad_array(array) || K < 1 || K > xl::kMaxK || n_drops < 0) return 0;
+  if (bad_array(array) || K < 1 || K > xl::kMaxKLarge || n_drops < 0) return 0;
+  if (K > xl::kMaxK && (precision != XLMIMO_FP64 || mode != XLMIMO_FUSED)) return 0;
   return xlh::gram_ws_bytes(to_params(array), K, n_drops, 1, precision, mode);
 }
 
@@ -276,7 +290,7 @@ int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K,
   g_err[0] = 0;
   if (bad_array(array)) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: invalid array");
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: K=%d n_drops=%lld", K, (long long)n_drops);
-  if (K > xl::kMaxK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d", K, xl::kMaxK);
+  if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d", K, xl::kMaxKLarge);
   if (precision != XLMIMO_FP64 && precision != XLMIMO_FP32) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: precision");
   if (mode != XLMIMO_FUSED && mode != XLMIMO_MATERIALIZED) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: mode");
   if (n_drops > 0 && (!pos || !gram)) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: null pointer");
@@ -298,15 +312,52 @@ int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double *pos, int3
   return xlh::launch_closed_form(ap, pos, K, n_drops, &M, 1, gram, flags, (cudaStream_t)stream);
 }
 
-int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
-                    uint32_t receivers, double *rates, uint32_t *flags, void *stream) {
+size_t xlmimo_sum_rate_workspace(int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers) {
+  if (K < 1 || K > xl::kMaxKLarge || n_drops < 0 || n_snr < 1 || n_snr > xl::kMaxSnr) return 0;
+  if (K <= xl::kMaxK || !(receivers & XLMIMO_RECV_CAP)) return 0;
+  return xlh::large_k_ws_bytes(K, n_drops, n_snr);
+}
+
+int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
+                       uint32_t receivers, double *rates, uint32_t *flags, void *ws, size_t ws_bytes, void *stream) {
   g_err[0] = 0;
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: K=%d", K);
-  if (K > xl::kMaxK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: K=%d > %d", K, xl::kMaxK);
+  if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: K=%d > %d", K, xl::kMaxKLarge);
   if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: n_snr out of [1,16]");
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: receivers");
   if (n_drops > 0 && (!gram || !rates)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: null pointer");
+  if (K > xl::kMaxK) {
+    if (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE))
+      return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: ZF/MMSE need K <= %d (K=%d)", xl::kMaxK, K);
+    return xlh::launch_sum_rate_large(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, ws, ws_bytes,
+                                      (cudaStream_t)stream);
+  }
   return xlh::launch_sum_rate(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, (cudaStream_t)stream);
+}
+
+int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
+                    uint32_t receivers, double *rates, uint32_t *flags, void *stream) {
+  return xlmimo_sum_rate_ws(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, nullptr, 0, stream);
+}
+
+size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr) {
+  if (K < 1 || K > xl::kMaxKLarge || n_drops < 0 || n_snr < 1 || n_snr > xl::kMaxSnr) return 0;
+  return xlh::large_k_ws_bytes(K, n_drops, 1 + n_snr);
+}
+
+int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
+                        double *rstat, double *bounds, double *eig, uint32_t *flags, void *ws, size_t ws_bytes,
+                        void *stream) {
+  g_err[0] = 0;
+  if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: K=%d", K);
+  if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "app_a_bounds: K=%d > %d", K, xl::kMaxKLarge);
+  if (eig && K > xl::kMaxK)
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "app_a_bounds: eigenvalues need K <= %d", xl::kMaxK);
+  if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr)
+    return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: n_snr out of [1,16]");
+  if (n_drops > 0 && (!gram || !rstat || !bounds)) return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: null pointer");
+  return xlh::launch_bounds(gram, K, n_drops, snr_db, n_snr, rstat, bounds, eig, flags, ws, ws_bytes,
+                            (cudaStream_t)stream);
 }
 
 int xlmimo_sum_rate_mismatched(const double *gram, const double *gram_model, int32_t K, int64_t n_drops,
@@ -336,7 +387,7 @@ int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max
 size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, int32_t K,
                                          int64_t n_drops, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
                                          int32_t precision) {
-  if (bad_array(array) || !n_list || n_n < 1 || n_n > 32 || K < 1 || K > xl::kMaxK || n_drops < 1) return 0;
+  if (bad_array(array) || !n_list || n_n < 1 || n_n > 32 || K < 1 || K > xl::kMaxKLarge || n_drops < 1) return 0;
   return sweep_layout(nullptr, to_params(array), n_list, n_n, K, n_drops, n_snr, receivers, gram_kind, precision)
       .total;
 }

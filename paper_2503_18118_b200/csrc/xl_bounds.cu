@@ -1,0 +1,738 @@
+// xl_bounds.cu -- NEXT-3: Appendix A per drop, the large-K
+// (K > 64) log-determinant path shared with the receivers, and the eigenvalues of
+// the correlation matrix R.
+//
+// Per drop, with a_i = rho G_ii (the diagonal of (P/sigma_n^2) H^H H):
+//   log2 U = sum_i log2(1 + a_i)              Hadamard upper bound
+//   R_ij   = G_ij / sqrt(G_ii G_jj)           correlation matrix
+//   log2 L = log2 det R + log2 U              Schur-Horn lower bound
+//   C      = log2 det(I + rho G)              the capacity they bracket (Eq. (9))
+//   gap    = -log2 det(R) / K                 max normalised gap, Eq. (eq9)
+// log2 det comes from a Cholesky factor (2 sum log2 L_kk); a pivot that is not > 0
+// marks the matrix not positive definite (R10).
+//
+// Kernels
+//  * bounds_warp_kernel (K <= 64): one warp per drop, the matrix in shared memory,
+//    the same warp Cholesky as the receivers.
+//  * chol_smem_kernel (64 < K <= 160): one CTA per matrix, packed lower triangle in
+//    shared memory, unblocked right-looking Cholesky.
+//  * chol_tiled_kernel (K > 160): one CTA per matrix in a global workspace slot,
+//    right-looking tiled Cholesky with 32 x 32 complex tiles and a register-blocked
+//    trailing update.  O(K^3/6) complex MACs per matrix.
+//  * finish kernels: one CTA per drop; scan G (finite, positive diagonal), log2 U /
+//    MRC from G, assemble outputs and flags.
+//  * eig_jacobi_kernel (K <= 64): eigenvalues of R by the parallel (round-robin)
+//    cyclic Jacobi method, one warp per drop, lane = one disjoint (p, q) pair per
+//    round; each rotation first makes A_pq real by a phase on column/row q, then
+//    zeroes it with the real plane rotation (t = sgn(theta)/(|theta| + sqrt(theta^2+1)),
+//    theta = (a_qq - a_pp)/(2|a_pq|)).
+#include <cstring>
+
+#include "xl_common.cuh"
+#include "xl_linalg.cuh"
+
+namespace {
+
+constexpr int kTile = 32;
+constexpr int kCtaThreads = 256;
+constexpr double kNaN = __builtin_nan("");
+
+struct BoundsParams {
+  const double *gram;
+  double *rstat;   // [D][2]
+  double *bounds;  // [D][S][3]
+  uint32_t *flags;
+  int K;
+  int64_t n_drops;
+  int n_snr;
+  double rho[xl::kMaxSnr];
+};
+
+// ------------------------------------------------------------------ K <= 64
+template <int RPL>
+__global__ void __launch_bounds__(256) bounds_warp_kernel(BoundsParams P) {
+  extern __shared__ double2 smem[];
+  const int K = P.K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double2 *As = smem + (size_t)warp * K * K;
+  const int64_t d = (int64_t)blockIdx.x * nw + warp;
+  if (d >= P.n_drops) return;
+  const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
+  double *rs = P.rstat + 2 * d, *bo = P.bounds + (size_t)d * P.n_snr * 3;
+  uint32_t fl = 0;
+
+  bool fin = true, dpos = true;
+  for (int e = lane; e < K * K; e += 32) fin &= isfinite(G[e].x) && isfinite(G[e].y);
+  for (int i = lane; i < K; i += 32) dpos &= G[i * K + i].x > 0.0;
+  fin = __all_sync(0xffffffffu, fin);
+  dpos = __all_sync(0xffffffffu, dpos);
+  if (!fin || !dpos) {
+    if (lane < 2) rs[lane] = kNaN;
+    for (int e = lane; e < 3 * P.n_snr; e += 32) bo[e] = kNaN;
+    if (lane == 0 && P.flags) P.flags[d] = fin ? XLMIMO_FLAG_MRC_UNDEF : XLMIMO_FLAG_NONFINITE;
+    return;
+  }
+  // R (column-major: As[j*K + i] = R_ij = conj(R_ji)), unit diagonal
+  for (int e = lane; e < K * K; e += 32) {
+    const int j = e / K, i = e - j * K;
+    const double2 g = G[j * K + i];
+    const double s = rsqrt(G[i * K + i].x) * rsqrt(G[j * K + j].x);
+    As[e] = (i == j) ? make_double2(1.0, 0.0) : make_double2(g.x * s, -g.y * s);
+  }
+  double ldr = kNaN;
+  if (xlk::warp_cholesky<RPL>(As, K, lane)) {
+    double part = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int k = lane + 32 * r;
+      if (k < K) part += 2.0 * log2(As[k * K + k].x);
+    }
+    ldr = xlk::warp_sum(part);
+  } else {
+    fl |= XLMIMO_FLAG_G_NOT_PD;
+  }
+  if (lane == 0) {
+    rs[0] = ldr;
+    rs[1] = -ldr / (double)K;
+  }
+  for (int s = 0; s < P.n_snr; ++s) {
+    const double rho = P.rho[s];
+    double lu = 0.0;
+    for (int i = lane; i < K; i += 32) lu += log2(1.0 + rho * G[i * K + i].x);
+    lu = xlk::warp_sum(lu);
+    __syncwarp();
+    for (int e = lane; e < K * K; e += 32) {
+      const int j = e / K, i = e - j * K;
+      const double2 g = G[j * K + i];
+      As[e] = make_double2((i == j ? 1.0 : 0.0) + rho * g.x, (i == j) ? 0.0 : -rho * g.y);
+    }
+    double cap = kNaN;
+    if (xlk::warp_cholesky<RPL>(As, K, lane)) {
+      double part = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int k = lane + 32 * r;
+        if (k < K) part += 2.0 * log2(As[k * K + k].x);
+      }
+      cap = xlk::warp_sum(part);
+    } else {
+      fl |= XLMIMO_FLAG_A_NOT_PD;
+    }
+    if (lane == 0) {
+      bo[3 * s + 0] = lu;
+      bo[3 * s + 1] = cap;
+      bo[3 * s + 2] = ldr + lu;
+    }
+  }
+  if (lane == 0 && P.flags) P.flags[d] = fl;
+}
+
+// ------------------------------------------------------------------ K > 64: log-determinants
+// Problem p = (drop d, matrix m): m = 0 .. n_mat-1.  first_is_r: m == 0 builds R (App. A);
+// every other m builds I + rho_m G.  log2det[p] = log2 det (NaN if not PD / not built).
+struct CholParams {
+  const double *gram;
+  double2 *ws;       // tiled kernel: [n_slots][Kp][Kp]
+  double *log2det;   // [n_prob]
+  int K, Kp, nt;
+  int64_t n_prob;
+  int n_mat;         // matrices per drop
+  int first_is_r;    // matrix 0 of each drop is R
+  double rho[xl::kMaxSnr + 1];  // rho of matrix m (unused for R)
+};
+
+// value (i, j) of problem matrix (R or I + rho G), i, j < K
+__device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, int j, bool is_r, double rho,
+                                              bool &good) {
+  const double2 g = G[(size_t)i * K + j];
+  good &= isfinite(g.x) && isfinite(g.y);
+  if (is_r) {
+    const double gi = G[(size_t)i * K + i].x, gj = G[(size_t)j * K + j].x;
+    good &= gi > 0.0 && gj > 0.0;
+    if (i == j) return make_double2(1.0, 0.0);
+    const double s = rsqrt(gi) * rsqrt(gj);
+    return make_double2(g.x * s, g.y * s);
+  }
+  return (i == j) ? make_double2(1.0 + rho * g.x, 0.0) : make_double2(rho * g.x, rho * g.y);
+}
+
+// 64 < K <= kSmemK: one CTA per matrix, the packed lower triangle resident in shared
+// memory (column-major packed: column j holds rows j..K-1 at off(j) = jK - j(j-1)/2),
+// unblocked right-looking Cholesky: per column j the pivot, the column scaled by
+// 1/L_jj, and the rank-1 update of the trailing triangle with warps over columns and
+// lanes over rows (contiguous, conflict-free).
+constexpr int kSmemK = 160;
+
+__global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
+  extern __shared__ double2 Ls[];
+  __shared__ int s_ok;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kCtaThreads / 32;
+  const int K = P.K;
+  auto off = [K](int j) { return j * K - j * (j - 1) / 2; };
+  for (int64_t prob = blockIdx.x; prob < P.n_prob; prob += gridDim.x) {
+    const int64_t d = prob / P.n_mat;
+    const int m = (int)(prob - d * P.n_mat);
+    const bool is_r = P.first_is_r && m == 0;
+    const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
+    bool good = true;
+    // column j of the lower triangle = conj of row j of G (coalesced reads)
+    for (int j = warp; j < K; j += NW)
+      for (int i = j + lane; i < K; i += 32) {
+        const double2 v = chol_entry(G, K, j, i, is_r, P.rho[m], good);
+        Ls[off(j) + i - j] = make_double2(v.x, -v.y);
+      }
+    const int ok0 = __syncthreads_and(good ? 1 : 0);
+    double ld = 0.0;
+    bool ok = ok0 != 0;
+    for (int j = 0; j < K && ok; ++j) {
+      const int oj = off(j);
+      const double piv = Ls[oj].x;  // every thread reads the same value: uniform branch
+      if (!(piv > 0.0) || !isfinite(piv)) {
+        ok = false;
+        break;
+      }
+      const double ljj = sqrt(piv), inv = 1.0 / ljj;
+      if (tid == 0) ld += 2.0 * log2(ljj);
+      __syncthreads();  // all pivot reads done before the column is rescaled
+      for (int i = j + tid; i < K; i += kCtaThreads) {
+        double2 v = Ls[oj + i - j];
+        Ls[oj + i - j] = (i == j) ? make_double2(ljj, 0.0) : make_double2(v.x * inv, v.y * inv);
+      }
+      __syncthreads();
+      // A_ic -= L_ij conj(L_cj), j < c <= i
+      for (int c = j + 1 + warp; c < K; c += NW) {
+        const double2 lc = Ls[oj + c - j];
+        const int oc = off(c);
+        for (int i = c + lane; i < K; i += 32) {
+          const double2 li = Ls[oj + i - j];
+          double2 a = Ls[oc + i - c];
+          a.x -= li.x * lc.x + li.y * lc.y;
+          a.y -= li.y * lc.x - li.x * lc.y;
+          Ls[oc + i - c] = a;
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) P.log2det[prob] = ok ? ld : kNaN;
+    __syncthreads();
+  }
+}
+
+// K > kSmemK: one CTA per matrix in a global workspace slot (K_pad = 32 nt, row-major,
+// lower triangle used), right-looking tiled Cholesky with 32 x 32 complex tiles:
+//  (1) warp 0 factors the diagonal tile in shared memory;
+//  (2) every thread solves one panel row x L_kk^H = a in registers;
+//  (3) trailing update A_ij -= L_ik L_jk^H: L_jk staged once per j for all warps, each
+//      warp stages its L_ik and computes the tile with a 4 x 8 register block per lane
+//      (32 independent complex accumulators; 12 shared loads per 32 complex MACs).
+constexpr int kLd = kTile + 1;  // padded row stride (conflict-free 16-byte column reads)
+constexpr size_t kTiledSmem = (size_t)(1 + kCtaThreads / 32) * kTile * kLd * sizeof(double2);
+
+__global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P) {
+  extern __shared__ double2 tsm[];       // S [32][33] then per-warp W [8][32][33]
+  __shared__ double2 T[kTile * kTile];   // diagonal tile, column-major T[c*32 + r]
+  __shared__ int s_ok;
+  __shared__ double s_ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kCtaThreads / 32;
+  const int K = P.K, Kp = P.Kp, nt = P.nt;
+  double2 *A = P.ws + (size_t)blockIdx.x * Kp * Kp;
+  double2 *S = tsm, *W = tsm + (1 + warp) * kTile * kLd;
+  const int lr = lane >> 2, lc = lane & 3;  // micro-tile: rows 4 lr .. +3, cols 8 lc .. +7
+
+  for (int64_t prob = blockIdx.x; prob < P.n_prob; prob += gridDim.x) {
+    const int64_t d = prob / P.n_mat;
+    const int m = (int)(prob - d * P.n_mat);
+    const bool is_r = P.first_is_r && m == 0;
+    const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
+    bool good = true;
+    for (int i = warp; i < Kp; i += NW)  // lower triangle, identity padding
+      for (int j = lane; j <= i; j += 32) {
+        double2 v = make_double2(i == j ? 1.0 : 0.0, 0.0);
+        if (i < K) v = chol_entry(G, K, i, j, is_r, P.rho[m], good);
+        A[(size_t)i * Kp + j] = v;
+      }
+    const int ok0 = __syncthreads_and(good ? 1 : 0);
+    if (tid == 0) {
+      s_ok = ok0;
+      s_ld = 0.0;
+    }
+    __syncthreads();
+    // s_ok is only read right after the barrier that follows its one writer (step 1),
+    // so every warp sees the same value and leaves the loop together.
+    for (int k = 0; k < nt && ok0; ++k) {
+      const int k0 = k * kTile;
+      if (warp == 0) {  // (1)
+        for (int c = 0; c < kTile; ++c) {
+          const double2 v = A[(size_t)(k0 + lane) * Kp + k0 + c];
+          T[c * kTile + lane] = (lane >= c) ? v : make_double2(0.0, 0.0);
+        }
+        const bool okf = xlk::warp_cholesky<1>(T, kTile, lane);
+        const double part = okf ? 2.0 * log2(T[lane * kTile + lane].x) : 0.0;
+        const double sum = xlk::warp_sum(part);
+        if (lane == 0) {
+          if (okf) s_ld += sum;
+          else s_ok = 0;
+        }
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj
+      for (int row = k0 + kTile + tid; row < Kp; row += kCtaThreads) {
+        // keep the 528 L_kk reads inside the iteration (hoisting them out of the row
+        // loop would need ~1000 registers)
+        asm volatile("" ::: "memory");
+        double2 *ar = A + (size_t)row * Kp + k0;
+        double2 x[kTile];
+#pragma unroll
+        for (int j = 0; j < kTile; ++j) x[j] = ar[j];
+#pragma unroll
+        for (int j = 0; j < kTile; ++j) {
+          double xr = x[j].x, xi = x[j].y;
+#pragma unroll
+          for (int mm = 0; mm < j; ++mm) {
+            const double2 l = T[mm * kTile + j];  // L_jm
+            xr -= x[mm].x * l.x + x[mm].y * l.y;
+            xi -= x[mm].y * l.x - x[mm].x * l.y;
+          }
+          const double inv = 1.0 / T[j * kTile + j].x;
+          x[j] = make_double2(xr * inv, xi * inv);
+        }
+#pragma unroll
+        for (int j = 0; j < kTile; ++j) ar[j] = x[j];
+      }
+      __syncthreads();
+      // (3)
+      for (int j = k + 1; j < nt; ++j) {
+        const int j0 = j * kTile;
+        for (int e = tid; e < kTile * kTile; e += kCtaThreads) {  // S[c][mm] = L_jk[c][mm]
+          const int c = e >> 5, mm = e & 31;
+          S[c * kLd + mm] = A[(size_t)(j0 + c) * Kp + k0 + mm];
+        }
+        __syncthreads();
+        for (int i = j + warp; i < nt; i += NW) {
+          const int i0 = i * kTile;
+          for (int r = 0; r < kTile; ++r) W[r * kLd + lane] = A[(size_t)(i0 + r) * Kp + k0 + lane];
+          __syncwarp();
+          double2 acc[4][8];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = A[(size_t)(i0 + 4 * lr + a) * Kp + j0 + 8 * lc + b];
+#pragma unroll 1
+          for (int mm = 0; mm < kTile; ++mm) {
+            double2 wa[4], sb[8];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) wa[a] = W[(4 * lr + a) * kLd + mm];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) sb[b] = S[(8 * lc + b) * kLd + mm];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 8; ++b) {
+                // wa conj(sb) = (wr sr + wi si) + j (wi sr - wr si)
+                acc[a][b].x -= wa[a].x * sb[b].x + wa[a].y * sb[b].y;
+                acc[a][b].y -= wa[a].y * sb[b].x - wa[a].x * sb[b].y;
+              }
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) A[(size_t)(i0 + 4 * lr + a) * Kp + j0 + 8 * lc + b] = acc[a][b];
+          __syncwarp();
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) P.log2det[prob] = s_ok ? s_ld : kNaN;
+    __syncthreads();
+  }
+}
+
+// scan one drop's Gram: finite entries and positive diagonal (block-wide)
+__device__ void scan_gram(const double2 *G, int K, bool &fin, bool &dpos) {
+  bool f = true, p = true;
+  for (int64_t e = threadIdx.x; e < (int64_t)K * K; e += blockDim.x) f &= isfinite(G[e].x) && isfinite(G[e].y);
+  for (int i = threadIdx.x; i < K; i += blockDim.x) p &= G[(size_t)i * K + i].x > 0.0;
+  fin = __syncthreads_and(f ? 1 : 0) != 0;
+  dpos = __syncthreads_and(p ? 1 : 0) != 0;
+}
+
+__device__ double block_sum(double v, double *red) {
+  v = xlk::warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];  // fixed order
+  return s;
+}
+
+// App. A outputs from the tiled log-dets (matrix 0 = R, 1 + s = I + rho_s G)
+__global__ void __launch_bounds__(kCtaThreads) bounds_finish_kernel(BoundsParams P, const double *log2det) {
+  __shared__ double red[kCtaThreads / 32];
+  const int64_t d = blockIdx.x;
+  const int K = P.K;
+  const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
+  double *rs = P.rstat + 2 * d, *bo = P.bounds + (size_t)d * P.n_snr * 3;
+  bool fin, dpos;
+  scan_gram(G, K, fin, dpos);
+  if (!fin || !dpos) {
+    if (threadIdx.x < 2) rs[threadIdx.x] = kNaN;
+    for (int e = threadIdx.x; e < 3 * P.n_snr; e += blockDim.x) bo[e] = kNaN;
+    if (threadIdx.x == 0 && P.flags) P.flags[d] = fin ? XLMIMO_FLAG_MRC_UNDEF : XLMIMO_FLAG_NONFINITE;
+    return;
+  }
+  const double *ld = log2det + d * (1 + P.n_snr);
+  uint32_t fl = 0;
+  const double ldr = ld[0];
+  if (isnan(ldr)) fl |= XLMIMO_FLAG_G_NOT_PD;
+  for (int s = 0; s < P.n_snr; ++s) {
+    double lu = 0.0;
+    for (int i = threadIdx.x; i < K; i += blockDim.x) lu += log2(1.0 + P.rho[s] * G[(size_t)i * K + i].x);
+    lu = block_sum(lu, red);
+    const double cap = ld[1 + s];
+    if (isnan(cap)) fl |= XLMIMO_FLAG_A_NOT_PD;
+    if (threadIdx.x == 0) {
+      bo[3 * s + 0] = lu;
+      bo[3 * s + 1] = cap;
+      bo[3 * s + 2] = ldr + lu;
+    }
+  }
+  if (threadIdx.x == 0) {
+    rs[0] = ldr;
+    rs[1] = -ldr / (double)K;
+    if (P.flags) P.flags[d] = fl;
+  }
+}
+
+// Large-K receivers (CAP from the tiled log-dets, MRC from G), same
+// output order and flag rules as the warp receivers (xl_rates.cu).
+struct LargeRateParams {
+  const double *gram;
+  double *rates;
+  uint32_t *flags;
+  int K;
+  int n_snr, n_recv;
+  uint32_t receivers;
+  double rho[xl::kMaxSnr];
+};
+
+__global__ void __launch_bounds__(kCtaThreads) rates_large_finish_kernel(LargeRateParams P, const double *log2det) {
+  __shared__ double red[kCtaThreads / 32];
+  const int64_t d = blockIdx.x;
+  const int K = P.K;
+  const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
+  double *out = P.rates + (size_t)d * P.n_snr * P.n_recv;
+  bool fin, dpos;
+  scan_gram(G, K, fin, dpos);
+  if (!fin) {
+    for (int e = threadIdx.x; e < P.n_snr * P.n_recv; e += blockDim.x) out[e] = kNaN;
+    if (threadIdx.x == 0 && P.flags) P.flags[d] |= XLMIMO_FLAG_NONFINITE;
+    return;
+  }
+  uint32_t fl = 0;
+  const bool mrc = (P.receivers & XLMIMO_RECV_MRC) != 0;
+  if (mrc && !dpos) fl |= XLMIMO_FLAG_MRC_UNDEF;
+  for (int s = 0; s < P.n_snr; ++s) {
+    int r = 0;
+    if (P.receivers & XLMIMO_RECV_CAP) {
+      const double cap = log2det[d * P.n_snr + s];
+      if (isnan(cap)) fl |= XLMIMO_FLAG_A_NOT_PD;
+      if (threadIdx.x == 0) out[s * P.n_recv + r] = cap;
+      ++r;
+    }
+    if (mrc) {
+      const double rho = P.rho[s];
+      double part = 0.0;
+      for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        const double gii = G[(size_t)i * K + i].x;
+        double intf = 0.0;
+        for (int j = 0; j < K; ++j)
+          if (j != i) {
+            const double2 g = G[(size_t)i * K + j];
+            intf += g.x * g.x + g.y * g.y;
+          }
+        part += log2(1.0 + rho * gii * gii / (gii + rho * intf));
+      }
+      const double c = block_sum(part, red);
+      if (threadIdx.x == 0) out[s * P.n_recv + r] = dpos ? c : kNaN;
+      ++r;
+    }
+  }
+  if (threadIdx.x == 0 && P.flags) P.flags[d] |= fl;
+}
+
+// ------------------------------------------------------------------ eigenvalues of R (K <= 64)
+__global__ void __launch_bounds__(128) eig_jacobi_kernel(const double *gram, int K, int64_t n_drops, double *eig) {
+  extern __shared__ double2 smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int Kp = K + (K & 1), ld = Kp + 1, npair = Kp / 2;
+  double2 *A = smem + (size_t)warp * Kp * ld;  // column-major A[c*ld + r]
+  const int64_t d = (int64_t)blockIdx.x * nw + warp;
+  if (d >= n_drops) return;
+  const double2 *G = reinterpret_cast<const double2 *>(gram) + (size_t)d * K * K;
+  double *ev = eig + (size_t)d * K;
+  bool ok = true;
+  for (int e = lane; e < K * K; e += 32) ok &= isfinite(G[e].x) && isfinite(G[e].y);
+  for (int i = lane; i < K; i += 32) ok &= G[i * K + i].x > 0.0;
+  if (!__all_sync(0xffffffffu, ok)) {
+    for (int i = lane; i < K; i += 32) ev[i] = kNaN;
+    return;
+  }
+  for (int e = lane; e < Kp * Kp; e += 32) {
+    const int c = e / Kp, r = e - c * Kp;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < K && c < K) {
+      if (r == c) {
+        v.x = 1.0;
+      } else {
+        const double2 g = G[r * K + c];
+        const double s = rsqrt(G[r * K + r].x) * rsqrt(G[c * K + c].x);
+        v = make_double2(g.x * s, g.y * s);
+      }
+    }
+    A[c * ld + r] = v;
+  }
+  __syncwarp();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int e = lane; e < Kp * Kp; e += 32) {
+      const int c = e / Kp, r = e - c * Kp;
+      const double2 v = A[c * ld + r];
+      const double m = v.x * v.x + v.y * v.y;
+      tot += m;
+      if (r != c) off += m;
+    }
+    off = xlk::warp_sum(off);
+    tot = xlk::warp_sum(tot);
+    if (off <= 1e-30 * tot) break;
+    for (int round = 0; round < Kp - 1; ++round) {
+      // round-robin pairing: position 0 fixed, the others rotate
+      int p = 0, q = 0;
+      const bool act = lane < npair;
+      if (act) {
+        const int a = lane, b = Kp - 1 - lane;
+        p = (a == 0) ? 0 : (a - 1 + round) % (Kp - 1) + 1;
+        q = (b - 1 + round) % (Kp - 1) + 1;
+      }
+      double c = 1.0, s = 0.0, er = 1.0, ei = 0.0, t = 0.0, bmag = 0.0;
+      if (act) {
+        const double2 apq = A[q * ld + p];
+        bmag = sqrt(apq.x * apq.x + apq.y * apq.y);
+        if (bmag > 0.0) {
+          er = apq.x / bmag;  // e^{-j phi} = conj(A_pq) / |A_pq|
+          ei = -apq.y / bmag;
+          const double theta = (A[q * ld + q].x - A[p * ld + p].x) / (2.0 * bmag);
+          t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+          if (theta < 0.0) t = -t;
+          c = rsqrt(t * t + 1.0);
+          s = t * c;
+        }
+      }
+      const bool rot = act && bmag > 0.0;
+      __syncwarp();
+      // columns: col_p' = c col_p - s e col_q ; col_q' = s col_p + c e col_q   (e = e^{-j phi})
+      if (rot) {
+        double2 *cp = A + p * ld, *cq = A + q * ld;
+        for (int r = 0; r < Kp; ++r) {
+          const double2 xp = cp[r], xq0 = cq[r];
+          const double2 xq = make_double2(xq0.x * er - xq0.y * ei, xq0.x * ei + xq0.y * er);
+          cp[r] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
+          cq[r] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+        }
+      }
+      __syncwarp();
+      // rows: row_p' = c row_p - s conj(e) row_q ; row_q' = s row_p + c conj(e) row_q
+      if (rot) {
+        for (int cc = 0; cc < Kp; ++cc) {
+          double2 *col = A + cc * ld;
+          const double2 xp = col[p], xq0 = col[q];
+          const double2 xq = make_double2(xq0.x * er + xq0.y * ei, -xq0.x * ei + xq0.y * er);
+          col[p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
+          col[q] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+        }
+      }
+      __syncwarp();
+      if (rot) {
+        A[q * ld + p] = make_double2(0.0, 0.0);
+        A[p * ld + q] = make_double2(0.0, 0.0);
+        A[p * ld + p].y = 0.0;
+        A[q * ld + q].y = 0.0;
+      }
+      __syncwarp();
+    }
+  }
+  // ascending: rank of each of the first K diagonal entries (ties by index);
+  // the padded index (odd K) holds an exact 0 that is never coupled and is skipped.
+  for (int i = lane; i < K; i += 32) {
+    const double v = A[i * ld + i].x;
+    int rank = 0;
+    for (int j = 0; j < K; ++j) {
+      const double w = A[j * ld + j].x;
+      rank += (w < v) || (w == v && j < i);
+    }
+    ev[rank] = v;
+  }
+}
+
+int n_chol_slots(int64_t n_prob) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+    cudaGetLastError();  // a failed query (no device) must not leak into check_launch
+  }
+  return (int)(n_prob < sms ? n_prob : sms);
+}
+
+int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool first_is_r, const double *rho,
+                double *log2det, void *ws, size_t ws_bytes, cudaStream_t s) {
+  CholParams C;
+  memset(&C, 0, sizeof(C));
+  C.gram = gram;
+  C.K = K;
+  C.nt = (K + kTile - 1) / kTile;
+  C.Kp = C.nt * kTile;
+  C.n_prob = n_drops * n_mat;
+  C.n_mat = n_mat;
+  C.first_is_r = first_is_r ? 1 : 0;
+  for (int m = 0; m < n_mat; ++m) C.rho[m] = rho[m];
+  C.log2det = log2det;
+  C.ws = (double2 *)ws;
+  xlh::KTimer tm(s, "chol_logdet");
+  if (K <= kSmemK) {
+    const size_t smem = (size_t)K * (K + 1) / 2 * sizeof(double2);
+    const int per_sm = (int)((220 * 1024) / smem);
+    const int64_t grid = (int64_t)n_chol_slots(C.n_prob) * (per_sm > 1 ? per_sm : 1);
+    cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    chol_smem_kernel<<<(unsigned)(grid < C.n_prob ? grid : C.n_prob), kCtaThreads, smem, s>>>(C);
+  } else {
+    const int slots = n_chol_slots(C.n_prob);
+    if ((size_t)slots * C.Kp * C.Kp * sizeof(double2) > ws_bytes)
+      return xlh::set_error(XLMIMO_EWORKSPACE, "large-K Cholesky: workspace too small");
+    cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmem);
+    chol_tiled_kernel<<<slots, kCtaThreads, kTiledSmem, s>>>(C);
+  }
+  tm.stop(s);
+  xlh::count_launch();
+  return xlh::check_launch("chol_logdet kernel");
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t chol_slot_bytes(int K, int64_t n_prob) {
+  if (K <= kSmemK) return 0;
+  const int Kp = (K + kTile - 1) / kTile * kTile;
+  return align256((size_t)n_chol_slots(n_prob) * Kp * Kp * sizeof(double2));
+}
+
+}  // namespace
+
+namespace xlh {
+
+// Scratch for the large-K path: Cholesky slots + per-problem log-dets.
+size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat) {
+  if (K <= xl::kMaxK || n_drops == 0) return 0;
+  return chol_slot_bytes(K, n_drops * n_mat) + align256((size_t)n_drops * n_mat * sizeof(double));
+}
+
+int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr, double *rstat,
+                  double *bounds, double *eig, uint32_t *flags, void *ws, size_t ws_bytes, cudaStream_t s) {
+  if (n_drops == 0) return XLMIMO_OK;
+  BoundsParams P;
+  memset(&P, 0, sizeof(P));
+  P.gram = gram;
+  P.rstat = rstat;
+  P.bounds = bounds;
+  P.flags = flags;
+  P.K = K;
+  P.n_drops = n_drops;
+  P.n_snr = n_snr;
+  for (int i = 0; i < n_snr; ++i) P.rho[i] = pow(10.0, snr_db[i] / 10.0);
+  int rc = XLMIMO_OK;
+  if (K <= xl::kMaxK) {
+    const size_t per_warp = (size_t)K * K * sizeof(double2);
+    int nw = (int)((96 * 1024) / per_warp);
+    nw = nw > 8 ? 8 : (nw < 1 ? 1 : nw);
+    const int64_t blocks = (n_drops + nw - 1) / nw;
+    KTimer tm(s, "app_a_bounds");
+    if (K <= 32) {
+      cudaFuncSetAttribute(bounds_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * nw));
+      bounds_warp_kernel<1><<<(unsigned)blocks, 32 * nw, per_warp * nw, s>>>(P);
+    } else {
+      cudaFuncSetAttribute(bounds_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * nw));
+      bounds_warp_kernel<2><<<(unsigned)blocks, 32 * nw, per_warp * nw, s>>>(P);
+    }
+    tm.stop(s);
+    count_launch();
+    rc = check_launch("bounds_warp_kernel");
+  } else {
+    const int n_mat = 1 + n_snr;
+    const int64_t n_prob = n_drops * n_mat;
+    const size_t chol_b = chol_slot_bytes(K, n_prob);
+    if (ws_bytes < large_k_ws_bytes(K, n_drops, n_mat) || !ws)
+      return set_error(XLMIMO_EWORKSPACE, "app_a_bounds: workspace %zu < %zu", ws_bytes,
+                       large_k_ws_bytes(K, n_drops, n_mat));
+    double *log2det = (double *)((char *)ws + chol_b);
+    double rho[xl::kMaxSnr + 1];
+    rho[0] = 0.0;
+    for (int i = 0; i < n_snr; ++i) rho[1 + i] = P.rho[i];
+    rc = launch_chol(gram, K, n_drops, n_mat, true, rho, log2det, ws, chol_b, s);
+    if (rc) return rc;
+    KTimer tm(s, "app_a_finish");
+    bounds_finish_kernel<<<(unsigned)n_drops, kCtaThreads, 0, s>>>(P, log2det);
+    tm.stop(s);
+    count_launch();
+    rc = check_launch("bounds_finish_kernel");
+  }
+  if (rc || !eig) return rc;
+  const int Kp = K + (K & 1);
+  const size_t per_warp = (size_t)Kp * (Kp + 1) * sizeof(double2);
+  int nw = (int)((100 * 1024) / per_warp);
+  nw = nw > 4 ? 4 : (nw < 1 ? 1 : nw);
+  KTimer tm(s, "eig_jacobi");
+  cudaFuncSetAttribute(eig_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * nw));
+  eig_jacobi_kernel<<<(unsigned)((n_drops + nw - 1) / nw), 32 * nw, per_warp * nw, s>>>(gram, K, n_drops, eig);
+  tm.stop(s);
+  count_launch();
+  return check_launch("eig_jacobi_kernel");
+}
+
+int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr,
+                          uint32_t receivers, double *rates, uint32_t *flags, void *ws, size_t ws_bytes,
+                          cudaStream_t s) {
+  if (n_drops == 0) return XLMIMO_OK;
+  LargeRateParams P;
+  memset(&P, 0, sizeof(P));
+  P.gram = gram;
+  P.rates = rates;
+  P.flags = flags;
+  P.K = K;
+  P.n_snr = n_snr;
+  P.receivers = receivers;
+  P.n_recv = __builtin_popcount(receivers & 15u);
+  for (int i = 0; i < n_snr; ++i) P.rho[i] = pow(10.0, snr_db[i] / 10.0);
+  double *log2det = nullptr;
+  if (receivers & XLMIMO_RECV_CAP) {
+    const int64_t n_prob = n_drops * n_snr;
+    const size_t chol_b = chol_slot_bytes(K, n_prob);
+    if (ws_bytes < large_k_ws_bytes(K, n_drops, n_snr) || !ws)
+      return set_error(XLMIMO_EWORKSPACE, "sum_rate (K > 64): workspace %zu < %zu", ws_bytes,
+                       large_k_ws_bytes(K, n_drops, n_snr));
+    log2det = (double *)((char *)ws + chol_b);
+    const int rc = launch_chol(gram, K, n_drops, n_snr, false, P.rho, log2det, ws, chol_b, s);
+    if (rc) return rc;
+  }
+  KTimer tm(s, "sum_rate_large_finish");
+  rates_large_finish_kernel<<<(unsigned)n_drops, kCtaThreads, 0, s>>>(P, log2det);
+  tm.stop(s);
+  count_launch();
+  return check_launch("rates_large_finish_kernel");
+}
+
+}  // namespace xlh

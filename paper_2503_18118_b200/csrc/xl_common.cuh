@@ -13,6 +13,7 @@ namespace xl {
 
 constexpr double kC = 299792458.0;  // m/s, exact (R2)
 constexpr int kMaxK = 64;           // fused paths: K <= 64
+constexpr int kMaxKLarge = 1024;    // large-K paths (tiled Cholesky, block-pair Gram)
 constexpr int kMaxSnr = 16;
 
 // ---------------------------------------------------------------------------
@@ -296,6 +297,14 @@ int launch_closed_form(const ArrayP &a, const double *pos, int K, int64_t n_drop
 // xl_rates.cu : problems = n_prob Grams [n_prob][K][K][2]; flags per problem
 int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr_db, int n_snr,
                     uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s);
+
+// xl_bounds.cu : Appendix A (NEXT-3) and the large-K (K > 64) receivers
+size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat);
+int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr, double *rstat,
+                  double *bounds, double *eig, uint32_t *flags, void *ws, size_t ws_bytes, cudaStream_t s);
+int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr,
+                          uint32_t receivers, double *rates, uint32_t *flags, void *ws, size_t ws_bytes,
+                          cudaStream_t s);
 
 // xl_sweep.cu reductions
 int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, int64_t *count,

@@ -976,6 +976,232 @@ void launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   else ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
 }
 
+// ------------------------------------------------------------------ kernel BLK
+// DMMA Gram for 64 < K <= 1024 (NEXT-3 / E1-E3 user counts).  Users in blocks of 64
+// (8 fragment planes).  A CTA owns (drop, block pair bi <= bj, element split) and
+// computes the 64 x 64 block G[bi][bj] as 64 jobs (ga, gb) of four DMMAs (RR, II,
+// RI, IR) per 4-element step, exactly the MT2 arithmetic.  For bi < bj both blocks'
+// coefficients are generated per tile (16 planes: A = bi, B = bj); for bi == bj the 8
+// planes serve as both operands and the lower-half jobs are computed but not written
+// (the diagonal blocks are nb of the nb(nb+1)/2 pairs).  A warp owns one ga and four
+// gb: one A fragment load per step feeds four jobs; jobs on padded planes and
+// lower-half diagonal jobs skip their DMMAs.  Tiles of 32
+// elements are generated into a 3-deep mbarrier ring (as MT2, NBUF = 3).  Level ends
+// stage the 64 jobs' accumulators in shared memory and write the block's entries of
+// the packed upper triangle [K(K+1)/2] of this (drop, split, level) partial.
+constexpr int kBlkU = 64, kBlkG = 8, kBlkNW = 16, kBlkNT = 32 * kBlkNW, kBlkS = 8, kBlkNBUF = 3;
+constexpr int kBlkPlane = kBlkS * 2 * kBlkG * 32;  // doubles per (re|im) tile plane set, 16 planes
+constexpr size_t kBlkTiles = 2ull * kBlkNBUF * kBlkPlane * sizeof(double);
+constexpr size_t kBlkStage = 64ull * 4 * 64 * sizeof(double);
+constexpr size_t kBlkSmem = kBlkTiles > kBlkStage ? kBlkTiles : kBlkStage;
+static_assert(kBlkSmem <= 220 * 1024, "BLK shared memory");
+
+template <int KIND>
+__global__ void __launch_bounds__(kBlkNT, 1) gram_blk_kernel(GramParams P, FastDiv fd, int n_pairs, int nb) {
+  extern __shared__ __align__(16) double dsm[];  // tiles [NBUF][re|im][S][16][32]; stage at level ends
+  __shared__ double4 su[2 * kBlkU];
+  __shared__ __align__(8) uint64_t mb_full[kBlkNBUF], mb_empty[kBlkNBUF];
+  constexpr int S = kBlkS, NT = kBlkNT, NW = kBlkNW, PLANE = kBlkPlane, GP = 2 * kBlkG;
+
+  const int64_t bdrop = blockIdx.x / ((int64_t)P.n_split * n_pairs);
+  const int rem = (int)(blockIdx.x - bdrop * P.n_split * n_pairs);
+  const int pair = rem / P.n_split, split = rem - pair * P.n_split;
+  int bi = 0, q0 = pair;
+  while (q0 >= nb - bi) { q0 -= nb - bi; ++bi; }
+  const int bj = bi + q0;
+  const bool diag = bi == bj;
+  const int64_t drop = bdrop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = P.K;
+  for (int u = tid; u < 2 * kBlkU; u += NT) {
+    const int gu = (u < kBlkU ? bi * kBlkU + u : bj * kBlkU + (u - kBlkU));
+    if (gu < K) {
+      const xl::UserC uc = xl::make_user(P.pos + (drop * K + gu) * 3, KIND, P.sqrt_beta0);
+      su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+    } else {
+      su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: zero amplitude
+    }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kBlkNBUF; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mt_smem_u32(&mb_full[i])), "r"(NT));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mt_smem_u32(&mb_empty[i])), "r"(NT));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // warp w on sub-partition s = w % 4, j = w / 4: ga = s or 7 - s, gb = 4 (j / 2) + k.
+  // Jobs on planes that hold only padded users, and the lower-half jobs of a diagonal
+  // block, issue no DMMAs: a warp's active jobs are a contiguous k range [klo, khi)
+  // dispatched to a compile-time loop (a predicated-off DMMA would still hold the
+  // pipe).  ga in {s, 7 - s} gives every sub-partition 9 of the 36 diagonal jobs.
+  const int sp = warp & 3, wj = warp >> 2;
+  const int ga = (wj & 1) ? 7 - sp : sp, gb0 = 4 * (wj >> 1);
+  const int aoff = ga * 32 + lane;
+  const int pa = min(kBlkG, (K - bi * kBlkU + 7) >> 3), pb = min(kBlkG, (K - bj * kBlkU + 7) >> 3);
+  int boff[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) boff[k] = ((diag ? 0 : kBlkG) + gb0 + k) * 32 + lane;
+  const int klo = (ga >= pa) ? 4 : (diag ? max(0, ga - gb0) : 0);
+  const int khi = min(4, pb - gb0);
+  const int kcase = (klo < khi) ? klo * 5 + khi : 0;  // 0: no active job
+  const int rows = S * (diag ? kBlkG : GP);  // generated 32-lane rows per tile
+  __syncthreads();
+  const double c4 = 4.0 * P.inv_lambda;
+  const bool n_odd = (P.N & 1) != 0;
+
+  const int s0 = (int)min((int64_t)split * P.chunk, P.N);
+  const int s1 = (int)min(P.N, (int64_t)s0 + P.chunk);
+  const int NP = K * (K + 1) / 2;
+  int lv0 = 0;
+  uint32_t T = 0;
+  for (int l = 0; l < P.n_lvl; ++l) {
+    const int lv1 = (int)P.lvl_end[l];
+    const int a = max(lv0, s0), b = min(lv1, s1);
+    lv0 = lv1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+    auto generate = [&](int t0, int buf) {
+      double *gre = dsm + buf * (2 * PLANE), *gim = gre + PLANE;
+#pragma unroll
+      for (int i = 0; i < (S * GP) / NW; ++i) {
+        const int row = warp + i * NW;  // row = s * GP + g
+        if (row < rows) {
+          const int g = diag ? (row % kBlkG) : (row % GP);
+          const int st = diag ? (row / kBlkG) : (row / GP);
+          const int t = t0 + 4 * st + (lane & 3);
+          const bool valid = t < b;
+          const ElemPos ep = element_pos32<KIND>(P, valid ? t : a, fd, n_odd);
+          const double4 uc = su[8 * g + (lane >> 2)];
+          const double dy = ep.y - uc.y;
+          double r2 = fma(dy, dy, uc.x);
+          if (KIND != XLMIMO_ULA) {
+            const double dz = ep.z - uc.z;
+            r2 = fma(dz, dz, r2);
+          }
+          double hr, hi;
+          xl::coef_fast(r2, valid ? uc.w : 0.0, c4, hr, hi);
+          const int orow = st * GP + g;  // storage row: step-major, 16 planes per step
+          gre[orow * 32 + lane] = hr;
+          gim[orow * 32 + lane] = hi;
+        }
+      }
+    };
+    auto consume_r = [&](auto kl, auto kh, int buf) {
+      constexpr int KL = decltype(kl)::value, KH = decltype(kh)::value;
+      const double *cre = dsm + buf * (2 * PLANE), *cim = cre + PLANE;
+#pragma unroll
+      for (int si = 0; si < S; ++si) {
+        const int so = si * GP * 32;
+        const double ar = cre[so + aoff], ai = cim[so + aoff];
+#pragma unroll
+        for (int k = KL; k < KH; ++k) {
+          const double br = cre[so + boff[k]], bim = cim[so + boff[k]];
+          dmma(acc[k][0], ar, br);
+          dmma(acc[k][1], ai, bim);
+          dmma(acc[k][2], ar, bim);
+          dmma(acc[k][3], ai, br);
+        }
+      }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using I4 = std::integral_constant<int, 4>;
+    auto consume = [&](int buf) {
+      switch (kcase) {  // klo * 5 + khi, warp-uniform
+        case 4: consume_r(I0{}, I4{}, buf); break;
+        case 1: consume_r(I0{}, I1{}, buf); break;
+        case 2: consume_r(I0{}, I2{}, buf); break;
+        case 3: consume_r(I0{}, I3{}, buf); break;
+        case 7: consume_r(I1{}, I2{}, buf); break;
+        case 8: consume_r(I1{}, I3{}, buf); break;
+        case 9: consume_r(I1{}, I4{}, buf); break;
+        case 13: consume_r(I2{}, I3{}, buf); break;
+        case 14: consume_r(I2{}, I4{}, buf); break;
+        case 19: consume_r(I3{}, I4{}, buf); break;
+        default: break;
+      }
+    };
+    const int n = b > a ? (b - a + 4 * S - 1) / (4 * S) : 0;
+    auto produce = [&](int i) {
+      const uint32_t tt = T + i;
+      const int bb = (int)(tt % kBlkNBUF);
+      if (tt >= kBlkNBUF) mt_wait(&mb_empty[bb], (tt / kBlkNBUF - 1) & 1);
+      generate(a + i * 4 * S, bb);
+      mt_arrive(&mb_full[bb]);
+    };
+#pragma unroll
+    for (int i = 0; i < kBlkNBUF - 1; ++i)
+      if (i < n) produce(i);
+    for (int i = 0; i < n; ++i) {
+      if (i + kBlkNBUF - 1 < n) produce(i + kBlkNBUF - 1);
+      const uint32_t tt = T + i;
+      const int bb = (int)(tt % kBlkNBUF);
+      mt_wait(&mb_full[bb], (tt / kBlkNBUF) & 1);
+      consume(bb);
+      mt_arrive(&mb_empty[bb]);
+    }
+    T += n;
+    __syncthreads();  // every warp's DMMAs done before the stage aliases the tiles
+    // stage [job q = ga*8 + gb][m][8][8] (C fragment: row lane/4, cols 2(lane%4) + {0,1})
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = ga * kBlkG + gb0 + k;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double *st = dsm + (q * 4 + m) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
+        st[0] = acc[k][m][0];
+        st[1] = acc[k][m][1];
+      }
+    }
+    __syncthreads();
+    double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * (size_t)(2 * NP);
+    for (int e = tid; e < kBlkU * kBlkU; e += NT) {
+      const int ua = e >> 6, ub = e & 63;
+      const int i = bi * kBlkU + ua, j = bj * kBlkU + ub;
+      if (i >= K || j >= K || (diag && ub < ua)) continue;
+      const int q = (ua >> 3) * kBlkG + (ub >> 3), f = (ua & 7) * 8 + (ub & 7);
+      const double *st = dsm + q * 4 * 64 + f;
+      const double re = st[0] + st[64];
+      const double im = st[128] - st[192];
+      const int64_t p = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
+      out[2 * p] = re;
+      out[2 * p + 1] = (i == j) ? 0.0 : im;
+    }
+    __syncthreads();
+  }
+}
+
+// Row-wise reduce for large K: block (drop, row i), threads over j >= i; sums splits in
+// fixed order per level, prefix over levels, Hermitian mirror, Im diag = 0.
+__global__ void __launch_bounds__(256) gram_reduce_rows_kernel(const double *ws, int K, int n_split, int n_lvl,
+                                                               double *out) {
+  const int64_t drop = blockIdx.x / K;
+  const int i = (int)(blockIdx.x - drop * K);
+  const int64_t NP = (int64_t)K * (K + 1) / 2;
+  const int64_t base = (int64_t)i * K - (int64_t)i * (i - 1) / 2 - i;
+  for (int j = i + threadIdx.x; j < K; j += blockDim.x) {
+    const int64_t p = base + j;
+    double re = 0.0, im = 0.0;
+    for (int l = 0; l < n_lvl; ++l) {
+      for (int s = 0; s < n_split; ++s) {
+        const double *w = ws + (((size_t)drop * n_split + s) * n_lvl + l) * (size_t)(2 * NP) + 2 * p;
+        re += w[0];
+        im += w[1];
+      }
+      double *g = out + ((size_t)drop * n_lvl + l) * (size_t)K * K * 2;
+      g[((size_t)i * K + j) * 2] = re;
+      g[((size_t)i * K + j) * 2 + 1] = (i == j) ? 0.0 : im;
+      g[((size_t)j * K + i) * 2] = re;
+      g[((size_t)j * K + i) * 2 + 1] = (i == j) ? 0.0 : -im;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel B
 template <int KP>
 struct TiledCfg {
@@ -1176,6 +1402,21 @@ int choose_split(int64_t n_drops, int64_t N) {
   return (int)s;
 }
 
+// BLK kernel (K > 64): one CTA per SM (192 KB of tiles), so aim for >= 2 waves of
+// (drop, block pair, split) CTAs; splits keep >= 4096 elements each.
+int blk_pairs(int K) {
+  const int nb = (K + kBlkU - 1) / kBlkU;
+  return nb * (nb + 1) / 2;
+}
+int choose_split_blk(int64_t n_drops, int K, int64_t N) {
+  const int64_t target = 148 * 2, have = n_drops * blk_pairs(K);
+  int64_t s = (target + have - 1) / (have > 0 ? have : 1);
+  const int64_t max_s = N / 4096 > 1 ? N / 4096 : 1;
+  if (s > max_s) s = max_s;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
 template <int KT, bool FP32>
 void launch_small(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   gram_small_kernel<KT, 256, FP32><<<(unsigned)n_blocks, 256, 0, s>>>(P);
@@ -1310,6 +1551,7 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
+  if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
@@ -1389,9 +1631,63 @@ int launch_materialised(const ArrayP &a, const double *pos, int K, int64_t n_dro
   return check_launch("gram_reduce_kernel");
 }
 
+// K > 64: block-pair DMMA kernel (fp64, fused), then the row-wise reduce.
+int launch_gram_blk(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end, int n_lvl,
+                    double *out, void *ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t N = lvl_end[n_lvl - 1];
+  if (N >= ((int64_t)1 << 31)) return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K > 64 needs N < 2^31");
+  const size_t need = gram_ws_bytes(a, K, n_drops, n_lvl, XLMIMO_FP64, XLMIMO_FUSED);
+  if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+  GramParams P;
+  memset(&P, 0, sizeof(P));
+  P.pos = pos;
+  P.ws = (double *)ws;
+  P.K = K;
+  P.kind = a.kind;
+  P.n_y = a.n_y;
+  P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+  P.N = N;
+  P.n_split = choose_split_blk(n_drops, K, N);
+  P.chunk = ((N + P.n_split - 1) / P.n_split + 255) / 256 * 256;
+  P.n_lvl = n_lvl;
+  for (int l = 0; l < kMaxLvl; ++l) P.lvl_end[l] = l < n_lvl ? lvl_end[l] : N;
+  P.inv_lambda = 1.0 / a.lambda;
+  P.pitch = a.pitch;
+  P.sqrt_beta0 = a.sqrt_beta0;
+  const int nb = (K + kBlkU - 1) / kBlkU, n_pairs = blk_pairs(K);
+  const int64_t n_blocks = n_drops * n_pairs * P.n_split;
+  const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
+  {
+    KTimer tm(s, "gram_fused_dmma_blk_fp64");
+    if (a.kind == XLMIMO_ULA) {
+      cudaFuncSetAttribute(gram_blk_kernel<XLMIMO_ULA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlkSmem);
+      gram_blk_kernel<XLMIMO_ULA><<<(unsigned)n_blocks, kBlkNT, kBlkSmem, s>>>(P, fd, n_pairs, nb);
+    } else {
+      cudaFuncSetAttribute(gram_blk_kernel<XLMIMO_UPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlkSmem);
+      gram_blk_kernel<XLMIMO_UPA><<<(unsigned)n_blocks, kBlkNT, kBlkSmem, s>>>(P, fd, n_pairs, nb);
+    }
+    tm.stop(s);
+    count_launch();
+  }
+  int rc = check_launch("gram_blk_kernel");
+  if (rc) return rc;
+  KTimer tr(s, "gram_reduce");
+  gram_reduce_rows_kernel<<<(unsigned)(n_drops * K), 256, 0, s>>>((const double *)ws, K, P.n_split, n_lvl, out);
+  tr.stop(s);
+  count_launch();
+  return check_launch("gram_reduce_rows_kernel");
+}
+
 int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s) {
+  if (K > xl::kMaxK) {
+    if (mode != XLMIMO_FUSED || precision != XLMIMO_FP64)
+      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d is fused fp64 only", K, xl::kMaxK);
+    if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
+    if (n_drops == 0) return XLMIMO_OK;
+    return launch_gram_blk(a, pos, K, n_drops, lvl_end, n_lvl, out, ws, ws_bytes, s);
+  }
   if (mode == XLMIMO_MATERIALIZED) {
     if (precision != XLMIMO_FP32)
       return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: XLMIMO_MATERIALIZED is complex64 (XLMIMO_FP32) only");

@@ -10,6 +10,7 @@
 #include <cstring>
 
 #include "xl_common.cuh"
+#include "xl_linalg.cuh"
 
 namespace {
 
@@ -24,50 +25,6 @@ struct RateParams {
   int n_recv;
   double rho[xl::kMaxSnr];
 };
-
-// In-place lower Cholesky of As (column-major, K x K complex) by one warp.
-// Returns true on success (uniform across the warp).
-template <int RPL>
-__device__ bool warp_cholesky(double2 *As, int K, int lane) {
-  for (int j = 0; j < K; ++j) {
-    __syncwarp();
-    const double piv = As[j * K + j].x;
-    if (!(piv > 0.0) || !isfinite(piv)) return false;
-    const double ljj = sqrt(piv), inv = 1.0 / ljj;
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const int i = lane + 32 * r;
-      if (i > j && i < K) {
-        double2 v = As[j * K + i];
-        v.x *= inv;
-        v.y *= inv;
-        As[j * K + i] = v;
-      } else if (i == j) {
-        As[j * K + j] = make_double2(ljj, 0.0);
-      }
-    }
-    __syncwarp();
-    // trailing update: A[i][k] -= L[i][j] conj(L[k][j]) for j < k <= i
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const int i = lane + 32 * r;
-      if (i > j && i < K) {
-        const double2 lij = As[j * K + i];
-        for (int k = j + 1; k <= i; ++k) {
-          const double2 lkj = As[j * K + k];
-          double2 a = As[k * K + i];
-          // lij * conj(lkj) = (lr kr + li ki) + j (li kr - lr ki)
-          a.x -= lij.x * lkj.x + lij.y * lkj.y;
-          a.y -= lij.y * lkj.x - lij.x * lkj.y;
-          As[k * K + i] = a;
-        }
-      }
-    }
-  }
-  __syncwarp();
-  return true;
-}
 
 // dinv[c] = [A^{-1}]_cc = sum_k |(L^{-1})_kc|^2 for the lane's columns c, with L in
 // As (column-major).  Xs: per-column scratch, Xs[k*K + c].
@@ -98,12 +55,6 @@ __device__ void warp_inv_diag(const double2 *As, double2 *Xs, int K, int lane, d
     }
   }
   __syncwarp();
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
 }
 
 template <int RPL>
@@ -139,7 +90,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
       const double2 g = G[j * K + i];
       As[e] = make_double2(g.x, -g.y);
     }
-    zf_ok = warp_cholesky<RPL>(As, K, lane);
+    zf_ok = xlk::warp_cholesky<RPL>(As, K, lane);
     if (zf_ok) warp_inv_diag<RPL>(As, Xs, K, lane, zf_dinv);
     else fl |= XLMIMO_FLAG_G_NOT_PD;
   }
@@ -161,7 +112,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
         const double2 g = G[j * K + i];
         As[e] = make_double2((i == j ? 1.0 : 0.0) + rho * g.x, -rho * g.y);
       }
-      a_ok = warp_cholesky<RPL>(As, K, lane);
+      a_ok = xlk::warp_cholesky<RPL>(As, K, lane);
       if (!a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
       if (a_ok) {
 #pragma unroll
@@ -173,7 +124,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
       }
     }
     if (P.receivers & XLMIMO_RECV_CAP) {
-      const double c = warp_sum(cap_part);
+      const double c = xlk::warp_sum(cap_part);
       if (lane == 0) out[s * P.n_recv + r] = a_ok ? c : nan;
       ++r;
     }
@@ -184,7 +135,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
         const int i = lane + 32 * rr;
         if (zf_ok && i < K) part += log2(1.0 + rho / zf_dinv[rr]);
       }
-      const double c = warp_sum(part);
+      const double c = xlk::warp_sum(part);
       if (lane == 0) out[s * P.n_recv + r] = zf_ok ? c : nan;
       ++r;
     }
@@ -195,7 +146,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
         const int i = lane + 32 * rr;
         if (a_ok && i < K) part += log2(1.0 + (1.0 / dinv[rr] - 1.0));
       }
-      const double c = warp_sum(part);
+      const double c = xlk::warp_sum(part);
       if (lane == 0) out[s * P.n_recv + r] = a_ok ? c : nan;
       ++r;
     }
@@ -215,7 +166,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
           part += log2(1.0 + rho * gii * gii / (gii + rho * intf));
         }
       }
-      const double c = warp_sum(part);
+      const double c = xlk::warp_sum(part);
       if (lane == 0) out[s * P.n_recv + r] = mrc_ok ? c : nan;
       ++r;
     }

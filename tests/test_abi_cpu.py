@@ -63,8 +63,12 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     upa = xl.Array.upa(8, 8, 100e9)
     assert L.xlmimo_gram_closed_form(ctypes.byref(upa), ctypes.c_void_p(8), 4, 1, ctypes.c_void_p(8), None, None) == -2
     ula = xl.Array.ula(256, 28e9)
-    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 0, 0, ctypes.c_void_p(8), None, 0,
+    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 1025, 1, 0, 0, ctypes.c_void_p(8), None, 0,
                                None) == -2
+    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 1, 0, ctypes.c_void_p(8), None, 0,
+                               None) == -2  # K > 64 is fused fp64 only
+    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 0, 0, ctypes.c_void_p(8), None, 0,
+                               None) == -3  # needs its workspace
     bad = xl.Array.ula(256, -1.0)
     assert L.xlmimo_gram_exact(ctypes.byref(bad), ctypes.c_void_p(8), 4, 1, 0, 0, ctypes.c_void_p(8), None, 0,
                                None) == -1
@@ -72,6 +76,19 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     snr = np.zeros(1)
     assert L.xlmimo_sum_rate(ctypes.c_void_p(8), 4, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 0,
                              ctypes.c_void_p(8), None, None) == -1  # no receivers
+    # Appendix A / large K: eigenvalues only for K <= 64, K <= 1024, workspace for K > 64
+    rs = ctypes.c_void_p(8)
+    assert L.xlmimo_app_a_bounds(rs, 65, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, rs, None, None, 0,
+                                 None) == -2
+    assert L.xlmimo_app_a_bounds(rs, 1025, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, None, None, None, 0,
+                                 None) == -2
+    assert L.xlmimo_app_a_bounds(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, None, None, None, 0,
+                                 None) == -3
+    assert L.xlmimo_app_a_bounds(rs, 8, 1, None, 1, rs, rs, None, None, None, 0, None) == -1
+    assert L.xlmimo_app_a_bounds_workspace(8, 100, 1) == 0 < L.xlmimo_app_a_bounds_workspace(100, 100, 1)
+    assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # ZF, K>64
+    assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 1, rs, None, None) == -3  # CAP: ws
+    assert L.xlmimo_sum_rate_workspace(100, 4, 1, 8) == 0 < L.xlmimo_sum_rate_workspace(100, 4, 1, 1)
     nl = np.array([256, 512, 1023], dtype=np.int64)  # mixed parity
     erg = np.zeros(16)
     nv = np.zeros(16, dtype=np.int64)
@@ -96,7 +113,9 @@ def test_workspace_queries_are_pure(lib):
     w1 = xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 64, 1000, 0, 0)
     w2 = xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 64, 1000, 0, 0)
     assert w1 == w2 > 0
-    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 0, 0) == 0
+    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 1025, 1000, 0, 0) == 0
+    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 1, 0) == 0
+    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 0, 0) > 0
 
 
 def test_product_path_has_no_oracle_dependency():

@@ -1,0 +1,124 @@
+"""GPU parity for NEXT-3 (Appendix A) and the large-K (K > 64)
+receivers: the CUDA path through the C ABI vs the CPU oracle on the same Grams.
+
+Tolerances: log2-determinants, log2 U / C / log2 L and rates <= 1e-6 bits
+(the north_star's fp64 rate bar; measured ~1e-12), gap <= 1e-9, eigenvalues of R
+<= 1e-10 absolute (R has unit diagonal); flags exact.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SNR = [0.0, 10.0, 30.0]
+
+
+@pytest.fixture(scope="module")
+def xl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests.conftest import build_product
+    build_product()
+    import paper_2503_18118_b200 as xl
+    return xl
+
+
+def _rect_gram_gpu(xl, K, N, D, seed, fc=100e9):
+    """E1/E3 user field at K <= 64: positions and Gram from the GPU path."""
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=seed)
+    return xl.gram_exact(xl.Array.ula(N, fc), pos)
+
+
+def _rect_gram_oracle(orc, K, N, D, seed, fc=100e9):
+    pos = orc.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=seed)
+    return orc.gram_exact_blas(orc.array("ula", n_y=N, fc_hz=fc), pos)
+
+
+def _compare(xl, orc, Gh, G, eig):
+    rs, bo, ev, fl = xl.app_a_bounds(G, SNR, eig=eig)
+    rso, boo, evo, flo = orc.bounds_app_a(Gh, SNR, eig=eig)
+    rs, bo = rs.cpu().numpy(), bo.cpu().numpy()
+    assert np.array_equal(np.isnan(rs), np.isnan(rso)) and np.array_equal(np.isnan(bo), np.isnan(boo))
+    ok = ~np.isnan(rso)
+    assert np.max(np.abs(rs[ok] - rso[ok]), initial=0.0) <= 1e-6
+    assert np.max(np.abs(rs[:, 1][ok[:, 1]] - rso[:, 1][ok[:, 1]]), initial=0.0) <= 1e-9
+    ok = ~np.isnan(boo)
+    assert np.max(np.abs(bo[ok] - boo[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    if eig:
+        ev = ev.cpu().numpy()
+        assert np.array_equal(np.isnan(ev), np.isnan(evo))
+        ok = ~np.isnan(evo)
+        assert np.max(np.abs(ev[ok] - evo[ok]), initial=0.0) <= 1e-10
+    return rs, bo
+
+
+@pytest.mark.parametrize("K,N,D", [(1, 64, 5), (2, 300, 7), (3, 512, 9), (8, 4096, 40), (16, 2048, 33),
+                                   (33, 4096, 11), (64, 8192, 6)])
+def test_app_a_parity_small_k(xl, orc, K, N, D):
+    G = _rect_gram_gpu(xl, K, N, D, seed=K)
+    rs, bo = _compare(xl, orc, G.cpu().numpy(), G, eig=True)
+    # the paper's sandwich on the GPU's own outputs
+    assert np.all(bo[..., 0] >= bo[..., 1] - 1e-9) and np.all(bo[..., 1] >= bo[..., 2] - 1e-9)
+
+
+@pytest.mark.parametrize("K,N,D", [(65, 2000, 3), (100, 35000, 2), (129, 4096, 2), (160, 3000, 2), (161, 3000, 2),
+                                   (200, 1000, 2), (333, 2000, 1)])
+def test_app_a_parity_large_k(xl, orc, K, N, D):
+    """K > 64: the shared-memory Cholesky (K <= 160) and the tiled one (K > 160, ragged
+    last tile for 161, 200, 333)."""
+    Gh = _rect_gram_oracle(orc, K, N, D, seed=K)
+    G = torch.view_as_complex(torch.tensor(np.stack([Gh.real, Gh.imag], -1), device="cuda").contiguous())
+    _compare(xl, orc, Gh, G, eig=False)
+
+
+def test_app_a_flags_and_edges(xl, orc):
+    G = np.zeros((4, 4, 4), complex)
+    G[0] = np.diag([1.0, 2.0, 3.0, 4.0])
+    G[1] = np.diag([1.0, 0.0, 3.0, 4.0])
+    G[2] = np.diag([1.0, 2.0, np.inf, 4.0])
+    G[3] = np.array([[1, 2, 0, 0], [2, 1, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]], complex)
+    Gd = torch.view_as_complex(torch.tensor(np.stack([G.real, G.imag], -1), device="cuda").contiguous())
+    _compare(xl, orc, G, Gd, eig=True)
+    # the same four at K = 100 and 200 through the large-K paths (padded with identity blocks)
+    for KL in (100, 200):
+        Gl = np.zeros((4, KL, KL), complex)
+        for d in range(4):
+            Gl[d] = np.eye(KL)
+            Gl[d, :4, :4] = G[d]
+        Gld = torch.view_as_complex(torch.tensor(np.stack([Gl.real, Gl.imag], -1), device="cuda").contiguous())
+        _compare(xl, orc, Gl, Gld, eig=False)
+    # empty batch
+    e = torch.zeros((0, 8, 8), dtype=torch.complex128, device="cuda")
+    rs, bo, _, _ = xl.app_a_bounds(e, SNR)
+    assert rs.shape == (0, 2) and bo.shape == (0, 3, 3)
+    with pytest.raises(xl.XlmimoError):
+        xl.app_a_bounds(Gld, SNR, eig=True)  # eigenvalues need K <= 64
+
+
+@pytest.mark.parametrize("K,N,D", [(65, 3000, 3), (100, 20000, 2), (160, 500, 2), (250, 4000, 2)])
+def test_sum_rate_large_k_parity(xl, orc, K, N, D):
+    """CAP (tiled Cholesky of I + rho G) and MRC for K > 64; ZF/MMSE are refused there."""
+    Gh = _rect_gram_oracle(orc, K, N, D, seed=3 * K)
+    G = torch.view_as_complex(torch.tensor(np.stack([Gh.real, Gh.imag], -1), device="cuda").contiguous())
+    rec = xl.RECV_CAP | xl.RECV_MRC
+    rates, fl = xl.sum_rate(G, SNR, rec)
+    ro, flo = orc.sum_rate(Gh, SNR, rec)
+    rg = rates.cpu().numpy()
+    assert np.array_equal(np.isnan(rg), np.isnan(ro))
+    ok = ~np.isnan(ro)
+    assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    with pytest.raises(xl.XlmimoError):
+        xl.sum_rate(G, SNR, xl.RECV_ZF)
+
+
+def test_app_a_paper_gap_k1000_gpu(xl, orc):
+    """-E_K[log2 lambda^R] = 0.064 at K = 1000 (E1 user field, M = 35 000):
+    GPU log2 det R of the oracle's Gram equals the oracle's, and the paper's number."""
+    Gh = _rect_gram_oracle(orc, 1000, 35000, 1, seed=0)
+    G = torch.view_as_complex(torch.tensor(np.stack([Gh.real, Gh.imag], -1), device="cuda").contiguous())
+    rs, _ = _compare(xl, orc, Gh, G, eig=False)
+    assert abs(rs[0, 1] - 0.064) < 1e-3

@@ -1,0 +1,78 @@
+"""GPU parity for the large-K (64 < K <= 1024) exact Gram (block-pair DMMA kernel):
+the CUDA path through the C ABI vs the oracle on the same GPU-drawn positions.
+
+Tolerance: |dG_ij| / sqrt(G_ii G_jj) <= 1e-9 (fp64 path, reading R9).
+"""
+import numpy as np
+import pytest
+
+from tests._util import normalized_err
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def xl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests.conftest import build_product
+    build_product()
+    import paper_2503_18118_b200 as xl
+    return xl
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 700, 1, 65, 3), ("ula", 1001, 1, 100, 2),
+                                              ("ula", 640, 1, 128, 2), ("ula", 333, 1, 129, 2),
+                                              ("ula", 500, 1, 200, 1), ("upa", 24, 20, 80, 2),
+                                              ("ula", 50, 1, 100, 2)])
+def test_gram_large_k_parity(xl, orc, kind, n_y, n_z, K, D):
+    """Block pairs of 64 users: full (K = 128), ragged (65, 100, 129, 200), UPA, and
+    N < K (rank-deficient G, N = 50)."""
+    fc = 100e9
+    if kind == "ula":
+        a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+    else:
+        a, ao = xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+    if kind == "ula":
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=K)
+    else:
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, D, seed=K)
+    G = xl.gram_exact(a, pos).cpu().numpy()
+    Go = orc.gram_exact(ao, pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-9
+    assert np.all(G.diagonal(axis1=1, axis2=2).imag == 0)
+    assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
+
+
+def test_gram_large_k_e3_full_size(xl, orc):
+    """The E3 point of the paper (K = 1000 users of the Sec. IV-C field, M = 35 000,
+    100 GHz) at full size: GPU Gram vs the oracle's Eq. (3) H and
+    one library matmul, then Appendix A on the GPU's own Gram -> 0.064."""
+    a = xl.Array.ula(35000, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 1000, 1, seed=0)
+    G = xl.gram_exact(a, pos)
+    Go = orc.gram_exact_blas(orc.array("ula", n_y=35000, fc_hz=100e9), pos.cpu().numpy())
+    assert normalized_err(G.cpu().numpy(), Go) <= 1e-9
+    rs, _, _, fl = xl.app_a_bounds(G, [0.0])
+    assert int(fl[0]) == 0 and abs(float(rs[0, 1]) - 0.064) < 1e-3
+
+
+def test_gram_large_k_unsupported_modes(xl):
+    a = xl.Array.ula(256, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 70, 1, seed=1)
+    with pytest.raises(xl.XlmimoError):
+        xl.gram_exact(a, pos, precision=xl.FP32)
+    with pytest.raises(xl.XlmimoError):
+        xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED)
+    e = torch.zeros((0, 70, 3), dtype=torch.float64, device="cuda")
+    assert xl.gram_exact(a, e).shape == (0, 70, 70)
+
+
+def test_gram_large_k_determinism(xl):
+    a = xl.Array.ula(3000, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 150, 3, seed=9)
+    g1 = xl.gram_exact(a, pos)
+    g2 = xl.gram_exact(a, pos)
+    assert torch.equal(g1, g2)
