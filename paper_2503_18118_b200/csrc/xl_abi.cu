@@ -64,7 +64,7 @@ struct Carve {
 
 // Layout of the saturation-sweep workspace (shared by the size query and the call).
 struct SweepWs {
-  double *pos, *grams, *rates, *erg, *sat;
+  double *pos, *grams, *rates, *erg, *sat, *satp;
   int64_t *nval;
   uint32_t *flags;
   void *gws, *rws;
@@ -84,6 +84,7 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
   w.erg = (double *)c.take((size_t)n_n * n_snr * R * sizeof(double));
   w.nval = (int64_t *)c.take((size_t)n_n * n_snr * R * sizeof(int64_t));
   w.sat = (double *)c.take(4 * sizeof(double));
+  w.satp = (double *)c.take(xlh::saturation_stats_scratch(D));
   w.gws_bytes = 0;
   if (gram_kind == XLMIMO_GRAM_EXACT) {
     xlh::ArrayP big = ap;
@@ -164,7 +165,7 @@ int run_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, c
   if (rc) return rc;
   const int n_out = n_n * n_snr * n_recv_of(receivers);
   if ((rc = xlh::launch_ergodic_reduce(rates, n_drops, n_out, w.erg, w.nval, s))) return rc;
-  if ((rc = xlh::launch_saturation_stats(P, K, n_drops, t, ap.pitch, w.sat, s))) return rc;
+  if ((rc = xlh::launch_saturation_stats(P, K, n_drops, t, ap.pitch, w.sat, w.satp, s))) return rc;
   cudaMemcpyAsync(ergodic, w.erg, (size_t)n_out * sizeof(double), cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(n_valid, w.nval, (size_t)n_out * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(sat, w.sat, 4 * sizeof(double), cudaMemcpyDeviceToHost, s);

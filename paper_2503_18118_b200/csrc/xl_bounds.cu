@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
   const int K = P.K, Kp = P.Kp, nt = P.nt;
   double2 *A = P.ws + (size_t)blockIdx.x * Kp * Kp;
   double2 *S = tsm, *W = tsm + (1 + warp) * kTile * kLd;
-  const int lr = lane >> 2, lc = lane & 3;  // micro-tile: rows 4 lr .. +3, cols 8 lc .. +7
+  // micro-tile: rows lr + 8a (a < 4), cols lc + 4b (b < 8).  With the 33-element row
+  // stride the 8 row groups and the 4 column groups hit distinct 16-byte bank slots.
+  const int lr = lane >> 2, lc = lane & 3;
 
   for (int64_t prob = blockIdx.x; prob < P.n_prob; prob += gridDim.x) {
     const int64_t d = prob / P.n_mat;
@@ -319,14 +321,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 8; ++b) acc[a][b] = A[(size_t)(i0 + 4 * lr + a) * Kp + j0 + 8 * lc + b];
+            for (int b = 0; b < 8; ++b) acc[a][b] = A[(size_t)(i0 + lr + 8 * a) * Kp + j0 + lc + 4 * b];
 #pragma unroll 1
           for (int mm = 0; mm < kTile; ++mm) {
             double2 wa[4], sb[8];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) wa[a] = W[(4 * lr + a) * kLd + mm];
+            for (int a = 0; a < 4; ++a) wa[a] = W[(lr + 8 * a) * kLd + mm];
 #pragma unroll
-            for (int b = 0; b < 8; ++b) sb[b] = S[(8 * lc + b) * kLd + mm];
+            for (int b = 0; b < 8; ++b) sb[b] = S[(lc + 4 * b) * kLd + mm];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 8; ++b) A[(size_t)(i0 + 4 * lr + a) * Kp + j0 + 8 * lc + b] = acc[a][b];
+            for (int b = 0; b < 8; ++b) A[(size_t)(i0 + lr + 8 * a) * Kp + j0 + lc + 4 * b] = acc[a][b];
           __syncwarp();
         }
         __syncthreads();

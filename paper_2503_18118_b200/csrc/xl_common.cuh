@@ -309,7 +309,8 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
 // xl_sweep.cu reductions
 int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, int64_t *count,
                           cudaStream_t s);
+size_t saturation_stats_scratch(int64_t n_drops);
 int launch_saturation_stats(const double *pos, int K, int64_t n_drops, double t, double pitch, double *sat,
-                            cudaStream_t s);
+                            double *scratch, cudaStream_t s);
 
 }  // namespace xlh

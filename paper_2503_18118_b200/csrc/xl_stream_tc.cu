@@ -312,11 +312,10 @@ struct FusedParams {
   uint32_t tmem_cols;
 };
 
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
+// TF32 round-to-nearest, ties away from zero, as integer ALU work (sign-magnitude:
+// add half a TF32 ulp to the magnitude, drop the 13 low mantissa bits) -- the same
+// bits as cvt.rna.tf32.f32 for finite x, without its XU-pipe conversion.
+__device__ __forceinline__ uint32_t tf32_rna(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
 
 // byte offset of the 16-B chunk c (0..7) of row r in a SWIZZLE_128B K-major tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
@@ -427,6 +426,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
           const float fc = (float)(qc - rint(qc));
           const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
           const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
+          const int64_t nv64 = P.N - t0;  // valid elements of this task (padding past N is 0)
+          const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
           uint32_t vr[kTaskE], vi[kTaskE];
 #pragma unroll
           for (int m = 0; m < kTaskE; ++m) {
@@ -434,10 +435,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
             const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
             const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
             float cyc = fmaf(dr, inv_lambda_f, fc);
-            cyc -= rintf(cyc);
+            // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
+            // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
+            cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);
             float sn, co;
             __sincosf(6.28318530717958647692f * cyc, &sn, &co);
-            const float a = ((t0 + m) < P.N) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
+            const float a = (m < nv) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
             vr[m] = tf32_rna(a * co);
             vi[m] = tf32_rna(-a * sn);
           }

@@ -1,7 +1,7 @@
 // xl_sweep.cu -- a6: ergodic reductions of the saturation sweep.
 //  * ergodic_reduce_kernel: mean over drops of each (N, SNR, receiver) column,
 //    excluding NaN, with the valid count (R10); fixed-order block reduction.
-//  * saturation_stats_kernel: per-drop Eqs. (13)-(16)
+//  * sat_partial_kernel + sat_final_kernel: per-drop Eqs. (13)-(16)
 //      y_up = max_i (x_i t/sqrt(1-t^2) + y_i),  y_down = min_i (-x_i t/sqrt(1-t^2) + y_i),
 //    their means over drops, M_sat = ceil((E[y_up] - E[y_down]) / pitch) (R15) and
 //    the standard error of the per-drop extent / pitch.
@@ -39,12 +39,15 @@ __global__ void __launch_bounds__(kRedThreads) ergodic_reduce_kernel(const doubl
   }
 }
 
-__global__ void __launch_bounds__(kRedThreads) saturation_stats_kernel(const double *pos, int K, int64_t n_drops,
-                                                                       double t, double pitch, double *sat) {
-  __shared__ double s_up[kRedThreads], s_dn[kRedThreads], s_e[kRedThreads], s_e2[kRedThreads];
-  const double sl = t / sqrt(1.0 - t * t);
-  double su = 0.0, sd = 0.0, se = 0.0, se2 = 0.0;
-  for (int64_t d = threadIdx.x; d < n_drops; d += kRedThreads) {
+// Two stages, both deterministic: sat_partial_kernel -- a thread per drop (Eqs. (13)-(16)
+// over its K users), fixed-order tree sums of (y_up, y_down, e, e^2) per block into
+// part[block][4]; sat_final_kernel -- one warp adds the block partials in block order.
+__global__ void __launch_bounds__(kRedThreads) sat_partial_kernel(const double *pos, int K, int64_t n_drops, double sl,
+                                                                  double pitch, double *part) {
+  __shared__ double sm[4][kRedThreads];
+  const int64_t d = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (d < n_drops) {
     double up = -INFINITY, dn = INFINITY;
     for (int i = 0; i < K; ++i) {
       const double *p = pos + (d * K + i) * 3;
@@ -52,35 +55,36 @@ __global__ void __launch_bounds__(kRedThreads) saturation_stats_kernel(const dou
       up = fmax(up, fma(x, sl, p[1]));    // Eqs. (13), (15)
       dn = fmin(dn, fma(-x, sl, p[1]));   // Eqs. (14), (16)
     }
-    su += up;
-    sd += dn;
     const double e = (up - dn) / pitch;
-    se += e;
-    se2 += e * e;
+    v[0] = up;
+    v[1] = dn;
+    v[2] = e;
+    v[3] = e * e;
   }
-  s_up[threadIdx.x] = su;
-  s_dn[threadIdx.x] = sd;
-  s_e[threadIdx.x] = se;
-  s_e2[threadIdx.x] = se2;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sm[q][threadIdx.x] = v[q];
   __syncthreads();
   for (int o = kRedThreads / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      s_up[threadIdx.x] += s_up[threadIdx.x + o];
-      s_dn[threadIdx.x] += s_dn[threadIdx.x + o];
-      s_e[threadIdx.x] += s_e[threadIdx.x + o];
-      s_e2[threadIdx.x] += s_e2[threadIdx.x + o];
-    }
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sm[q][threadIdx.x] += sm[q][threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const double D = (double)n_drops;
-    const double eu = s_up[0] / D, ed = s_dn[0] / D, me = s_e[0] / D;
-    const double var = n_drops > 1 ? (s_e2[0] - D * me * me) / (D - 1.0) : 0.0;
-    sat[0] = eu;
-    sat[1] = ed;
-    sat[2] = ceil((eu - ed) / pitch);
-    sat[3] = sqrt(var > 0.0 ? var : 0.0) / sqrt(D);
-  }
+  if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+__global__ void sat_final_kernel(const double *part, int nb, int64_t n_drops, double pitch, double *sat) {
+  if (threadIdx.x != 0) return;
+  double t[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b = 0; b < nb; ++b)
+    for (int q = 0; q < 4; ++q) t[q] += part[b * 4 + q];
+  const double D = (double)n_drops;
+  const double eu = t[0] / D, ed = t[1] / D, me = t[2] / D;
+  const double var = n_drops > 1 ? (t[3] - D * me * me) / (D - 1.0) : 0.0;
+  sat[0] = eu;
+  sat[1] = ed;
+  sat[2] = ceil((eu - ed) / pitch);
+  sat[3] = sqrt(var > 0.0 ? var : 0.0) / sqrt(D);
 }
 
 }  // namespace
@@ -97,13 +101,19 @@ int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, do
   return check_launch("ergodic_reduce_kernel");
 }
 
+size_t saturation_stats_scratch(int64_t n_drops) {
+  return (size_t)((n_drops + kRedThreads - 1) / kRedThreads) * 4 * sizeof(double);
+}
+
 int launch_saturation_stats(const double *pos, int K, int64_t n_drops, double t, double pitch, double *sat,
-                            cudaStream_t s) {
+                            double *scratch, cudaStream_t s) {
+  const int nb = (int)((n_drops + kRedThreads - 1) / kRedThreads);
   KTimer tm(s, "saturation_stats");
-  saturation_stats_kernel<<<1, kRedThreads, 0, s>>>(pos, K, n_drops, t, pitch, sat);
+  sat_partial_kernel<<<nb, kRedThreads, 0, s>>>(pos, K, n_drops, t / sqrt(1.0 - t * t), pitch, scratch);
+  sat_final_kernel<<<1, 32, 0, s>>>(scratch, nb, n_drops, pitch, sat);
   tm.stop(s);
-  count_launch();
-  return check_launch("saturation_stats_kernel");
+  count_launch(2);
+  return check_launch("saturation_stats kernels");
 }
 
 }  // namespace xlh
