@@ -322,7 +322,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(
 
 constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
 constexpr int kGenGroups = 8;      // group g owns ring slot g (stage k -> slot k % 8)
-constexpr int kFStages = kGenGroups;
+constexpr int kFStages = 12;      // ring slots: stage k -> slot k % 12, generated by group k % 8
 constexpr int kGenThreads = 32 * kGenWarps;
 constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
 constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
@@ -368,10 +368,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   const uint32_t tmem = *tmem_base_sh;
   const int kb_per_chunk = kChunk / (kBoxK * P.nblk);
 
-  if (warp < kEpiWarp0) {  // ---------------- generators: warp g owns ring slot g
-    // kFStages == kGenGroups: the global stage sequence k (same order as the MMA issuer)
-    // maps to slot k % 12, so generator warp g handles exactly the stages k = g (mod 12),
-    // always in slot g, with phase (k / 12) & 1.
+  if (warp < kEpiWarp0) {  // ---------------- generators: group g makes stages k = g (mod 8)
+    // The global stage sequence k (the MMA issuer's order) lives in slot k % 12 with
+    // phase (k / 12) & 1; 12 slots for 8 groups let a group start its next stage
+    // while the MMA still holds its previous one.
     const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
     double4 *su = su_all + grp * 64;
     const double inv_lambda = 1.0 / P.lambda;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     // stage covers elements xs + 32 b .. + 31 in rows rb*b .. rb*b + 2K - 1
     const int n_tasks = P.nblk * K * (kBoxK / kTaskE);
     const int tpb = K * (kBoxK / kTaskE);  // tasks per block
-    const uint32_t slot_base = smem_u32(stages + grp * kStageBytes);
+    const uint32_t stages_base = smem_u32(stages);
     int64_t kstart = 0;  // global index of the item's first stage
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / P.n_chunks;
@@ -402,9 +402,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
       for (; k < kstart; k += kGenGroups) {
         const int64_t xs = x0 + (k - (kstart - ns)) * spb;
-        mbar_wait(&empty[grp], ((uint32_t)(k / kGenGroups) & 1) ^ 1);
-        for (int task = gtid; task < n_tasks; task += kGenThreads) {
-          const int blk = task / tpb, tb = task - blk * tpb;
+        // more slots than groups: a group's next stage reuses a slot freed 4 stages ago,
+        // so generation never waits on the MMA of its own previous stage
+        const int slot = (int)(k % kFStages);
+        const uint32_t slot_base = stages_base + slot * kStageBytes;
+        mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
+        // (blk, tb) = divmod(task, tpb), stepped without a division (tpb = 4K >= 36 > 64/2)
+        int blk = gtid / tpb, tb = gtid - blk * tpb;
+        for (int task = gtid; task < n_tasks; task += kGenThreads, tb += kGenThreads) {
+          while (tb >= tpb) { tb -= tpb; ++blk; }
           const int u = tb / (kBoxK / kTaskE), g8 = tb % (kBoxK / kTaskE);
           const int row0 = blk * P.rb + 2 * u;
           const int64_t t0 = xs + kBoxK * blk + kTaskE * g8;
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[grp]);  // kGenWarps arrivals complete the stage
+        if (lane == 0) mbar_arrive(&full[slot]);  // kGenWarps arrivals complete the stage
       }
     }
   } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
