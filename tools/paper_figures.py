@@ -1,0 +1,125 @@
+"""The paper's own figure workloads (NEXT-4, NEXT-3) end to end on one GPU, through the
+public API; prints one JSON object per figure (data + device time).  Synthetic seeded
+drops with the paper's user fields; nothing here reads the oracle.
+
+    python tools/paper_figures.py [--drops-e1 D] [--drops-e2 D] [--drops-e3 D]
+
+E1  Fig. norm_cap: 100 GHz, x ~ U[1,10] m, y ~ U[-7.5,7.5] m, K = 100,
+    SNR 0 and 200 dB, t = 0.9: ergodic capacity vs M on nested arrays, normalised by the
+    largest M, and the per-drop Eqs. (13)-(16) saturation estimate.
+E2  Fig. Capacity_vs_number_of_ant: x ~ U(1,2) m, K = 10, transmit SNR
+    for a 33 dB received-SNR limit at (1.5 m, 0) (Eq. (5)): CAP, ZF, MMSE, MRC on the exact
+    Gram, modified ZF nominal (closed-form Gram) and effective (closed-form equalizer on the
+    true channel) vs M.
+E3  Fig. K_vs_E: -E_K[log2 lambda^R] (Appendix A gap) vs K at M = 35 000
+    (reading R25), E1 user field.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2503_18118_b200 as xl  # noqa: E402
+
+C = 299792458.0
+
+
+def dev_ms(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1)
+
+
+def e1(D):
+    nl = [2048, 4096, 8192, 12288, 16384, 24576, 34774, 49152, 65536, 98304, 131072]
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 100, D, seed=11)
+    res, ms = dev_ms(lambda: xl.saturation_sweep(xl.Array.ula(max(nl), 100e9), nl, 100, D, [0.0, 200.0],
+                                                 xl.RECV_CAP, pos=pos))
+    erg = res["ergodic"][:, :, 0]
+    return {"figure": "E1 norm_cap", "K": 100, "drops": D, "M": nl, "snr_db": [0.0, 200.0],
+            "capacity_bits": erg.tolist(), "normalized": (erg / erg[-1]).tolist(),
+            "n_valid": res["n_valid"][:, :, 0].tolist(),
+            "sat_mc": {"E_y_up": res["sat"][0], "E_y_down": res["sat"][1], "M_sat": res["sat"][2],
+                       "stderr": res["sat"][3]},
+            "note": "red line of the paper = Eq. (17)-(18) with (2K+1): 34 774 elements (oracle, R16)",
+            "device_ms": ms}
+
+
+def e2(D):
+    lam = C / 100e9
+    rho_db = 10 * math.log10(10 ** 3.3 * lam * 1.5 / 4)
+    Ms = [256, 512, 1024, 2048, 4096, 8192, 12460, 16384, 32768, 65536]
+    pos = xl.gen_drops_rect((1.0, 2.0), (-7.5, 7.5), 10, D, seed=12)
+    rows = []
+    t_ms = 0.0
+    for M in Ms:
+        a = xl.Array.ula(M, 100e9)
+
+        def run():
+            G = xl.gram_exact(a, pos)
+            Gt, _ = xl.gram_closed_form(a, pos)
+            r, _ = xl.sum_rate(G, [rho_db], xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC)
+            rn, _ = xl.sum_rate(Gt, [rho_db], xl.RECV_ZF)
+            mz, _ = xl.sum_rate_mismatched(G, Gt, [rho_db])
+            return r, rn, mz
+        (r, rn, mz), ms = dev_ms(run)
+        t_ms += ms
+        r, rn, mz = r[:, 0].cpu().numpy(), rn[:, 0, 0].cpu().numpy(), mz[:, 0].cpu().numpy()
+        rows.append({"M": M, "CAP": float(np.nanmean(r[:, 0])), "ZF": float(np.nanmean(r[:, 1])),
+                     "MMSE": float(np.nanmean(r[:, 2])), "MRC": float(np.nanmean(r[:, 3])),
+                     "modified_ZF_nominal": float(np.nanmean(rn)), "modified_ZF_nominal_valid": int(np.sum(~np.isnan(rn))),
+                     "modified_ZF_effective": float(np.nanmean(mz))})
+    return {"figure": "E2 Capacity_vs_number_of_ant", "K": 10, "drops": D, "rho_db": rho_db, "curves": rows,
+            "device_ms": t_ms}
+
+
+def e3(D):
+    Ks = [10, 50, 100, 200, 400, 700, 1000]
+    a = xl.Array.ula(35000, 100e9)
+    out = []
+    t_ms = 0.0
+    for K in Ks:
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=13)
+
+        def run():
+            G = xl.gram_exact(a, pos)
+            return xl.app_a_bounds(G, [0.0, 30.0])
+        (rs, bo, _, fl), ms = dev_ms(run)
+        t_ms += ms
+        gap = rs[:, 1].cpu().numpy()
+        bo = bo.cpu().numpy()
+        out.append({"K": K, "gap_mean": float(np.nanmean(gap)), "gap_std": float(np.nanstd(gap)),
+                    "flagged": int((fl != 0).sum()), "log2U_minus_C_0dB": float(np.mean(bo[:, 0, 0] - bo[:, 0, 1])),
+                    "C_minus_log2L_0dB": float(np.mean(bo[:, 0, 1] - bo[:, 0, 2])), "device_ms": ms})
+    return {"figure": "E3 K_vs_E", "M": 35000, "drops": D, "points": out,
+            "paper": "0.064 at K = 1000 (PAPER.md:335)", "device_ms": t_ms}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--drops-e1", type=int, default=1000)
+    ap.add_argument("--drops-e2", type=int, default=2000)
+    ap.add_argument("--drops-e3", type=int, default=32)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    for f, d in ((e1, args.drops_e1), (e2, args.drops_e2), (e3, args.drops_e3)):
+        t0 = time.perf_counter()
+        rec = f(d)
+        rec["wall_s"] = time.perf_counter() - t0
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()
