@@ -119,6 +119,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(kname: str, n_drops: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    newest committed ncu --set full capture of the same launch (profiles/r*/ncu_traffic_bench.json),
+    or None.  The fused kernel is ALU-bound: this is positions in + Gram partials out."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_bench.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if d.get("kernel") == kname and d.get("n_drops") == n_drops:
+            return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+    return None
+
+
 # ----------------------------------------------------------------------------- oracle timing
 def oracle_sample(n_drops_sample: int, seed: int, nthreads: int = 0):
     """Time the oracle (as it stands) on a bounded sample of the workload."""
@@ -300,7 +316,7 @@ def run_ours(args):
         clk = ck.get("sm_max_mhz") or 1965.0
         peak = 148 * 64 * clk * 1e6 / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "FP64 Top/s", "frac": achieved / peak,
-                "traffic": None, "kernel": kname, "launch_ms": per_launch_ms,
+                "traffic": ncu_traffic(kname, D), "kernel": kname, "launch_ms": per_launch_ms,
                 "work_model": f"per element-user coefficient {FP64_OPS_PER_COEF} FP64 ops, 4 DFMA per off-diagonal "
                               "cMAC, 2 per diagonal; peak = 148 SM x 64 FP64 lanes/clk x sm_max clock",
                 "share_of_step": kms / t_ms}
