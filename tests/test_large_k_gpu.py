@@ -76,3 +76,24 @@ def test_gram_large_k_determinism(xl):
     g1 = xl.gram_exact(a, pos)
     g2 = xl.gram_exact(a, pos)
     assert torch.equal(g1, g2)
+
+
+def test_closed_form_and_sweep_large_k(xl, orc):
+    """Closed-form (modified-ZF) Gram at K = 100 (O(K^2), no N loop) and the closed-form
+    saturation sweep at K > 64 (CAP + MRC) against the oracle on the same drops."""
+    pos = xl.gen_drops_rect((1.0, 2.0), (-7.5, 7.5), 100, 4, seed=21)
+    ph = pos.cpu().numpy()
+    a, ao = xl.Array.ula(12460, 100e9), orc.array("ula", n_y=12460, fc_hz=100e9)
+    Gt, fl = xl.gram_closed_form(a, pos)
+    Gto, flo = orc.gram_closed_form(ao, ph)
+    assert np.max(np.abs(Gt.cpu().numpy() - Gto)) <= 1e-9 * np.max(np.abs(Gto))
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    nl = [1024, 4096, 12460]
+    rec = xl.RECV_CAP | xl.RECV_MRC
+    res = xl.saturation_sweep(a, nl, 100, 4, [3.5], rec, pos=pos, gram_kind=xl.GRAM_CLOSED_FORM, per_drop=True)
+    _, nv, _, pd = orc.saturation_sweep(ao, nl, ph, [3.5], rec, gram_kind=1, per_drop=True)
+    g = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(pd))
+    ok = ~np.isnan(pd)
+    assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
