@@ -136,15 +136,17 @@ XLMIMO_API int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double
  * rates (dev [n_drops][n_snr][popcount(receivers)]); flags (dev [n_drops] or NULL):
  * OR-ed with the XLMIMO_FLAG_* bits (so a closed-form DEGENERATE bit survives).
  * A failed Cholesky gives NaN for the receivers it feeds (R10).  K <= 64 (no
- * workspace); for 64 < K <= 1024 use xlmimo_sum_rate_ws (CAP and MRC only). */
+ * workspace); for 64 < K <= 1024 use xlmimo_sum_rate_ws. */
 XLMIMO_API int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
                     uint32_t receivers, double *rates, uint32_t *flags, void *stream);
 
-/* The same receivers with a caller workspace, for K up to 1024.  For K > 64 CAP
- * comes from a tiled Cholesky of I + rho G in the workspace (one CTA per matrix,
- * 32 x 32 complex tiles) and MRC straight from G; ZF/MMSE (diagonal of an
- * inverse) return EUNSUPPORTED for K > 64.  The workspace query returns 0 when
- * none is needed (K <= 64, or no CAP); ws may then be NULL.
+/* The same receivers with a caller workspace, for K up to 1024.  For K > 64 the
+ * Cholesky factors of I + rho G (CAP, MMSE) and of G (ZF) are formed one CTA per
+ * matrix -- resident in shared memory for K <= 160, with the diagonal of the
+ * inverse by forward substitution for ZF/MMSE; tiled (32 x 32 complex) in the
+ * workspace for K > 160 -- and MRC comes straight from G.  ZF/MMSE need K <= 160
+ * (EUNSUPPORTED above; CAP and MRC run to K = 1024).  The workspace query returns 0
+ * when none is needed (K <= 64); ws may then be NULL.
  * EWORKSPACE: ws_bytes below the query. */
 XLMIMO_API size_t xlmimo_sum_rate_workspace(int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers);
 XLMIMO_API int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const double *snr_db,
@@ -186,7 +188,7 @@ XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drop
  *            PAPER.md:228) and M_sat = ceil((E[y_up]-E[y_down]) / pitch) (R15),
  *   per_drop (dev [n_drops][n_n][n_snr][n_recv] or NULL).
  * array->n_y is ignored (the grid is n_list).  Synchronises `stream` before return.
- * K <= 1024; for K > 64 the exact Gram is fp64 and the receivers CAP/MRC only
+ * K <= 1024; for K > 64 the exact Gram is fp64, and ZF/MMSE need K <= 160
  * (EUNSUPPORTED otherwise) -- the paper's K = 100 curves.
  * EINVAL also for n_list not ascending / mixed parity, t not in (0,1). */
 XLMIMO_API size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,

@@ -11,11 +11,20 @@
 #include <cstdio>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "xl_common.cuh"
 
 namespace {
 
 thread_local char g_err[512] = "";
+
+// NVTX range around each compute entry point (header-only NVTX v3: a no-op unless a
+// tool such as ncu / nsys injects itself), so profiles show the ABI call structure.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 std::atomic<uint64_t> g_launches{0};
 
 bool bad_array(const xlmimo_array_t *a) {
@@ -93,7 +102,7 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
   }
   w.gws = c.take(w.gws_bytes);
   // K > 64: receivers through the large-K path (CAP by Cholesky slots, MRC)
-  w.rws_bytes = (K > xl::kMaxK && (receivers & XLMIMO_RECV_CAP)) ? xlh::large_k_ws_bytes(K, D * n_n, n_snr) : 0;
+  w.rws_bytes = K > xl::kMaxK ? xlh::sum_rate_large_ws_bytes(K, D * n_n, n_snr, receivers) : 0;
   w.rws = c.take(w.rws_bytes);
   w.total = c.off;
   return w;
@@ -111,8 +120,8 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
   }
   if (K < 1 || K > xl::kMaxKLarge)
     return xlh::set_error(K < 1 ? XLMIMO_EINVAL : XLMIMO_EUNSUPPORTED, "sweep: K=%d", K);
-  if (K > xl::kMaxK && (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)))
-    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: ZF/MMSE need K <= %d (K=%d)", xl::kMaxK, K);
+  if (K > xl::kMaxKInv && (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)))
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: ZF/MMSE need K <= %d (K=%d)", xl::kMaxKInv, K);
   if (K > xl::kMaxK && gram_kind == XLMIMO_GRAM_EXACT && precision != XLMIMO_FP64)
     return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: K=%d > %d is fp64 only", K, xl::kMaxK);
   if (n_drops < 1) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_drops < 1");
@@ -272,6 +281,7 @@ int xlmimo_timing_read(int32_t max_entries, char *names, int64_t *counts, double
 
 int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t n_drops, uint64_t seed, uint64_t first_drop,
                      double *pos, void *stream) {
+  NvtxRange nvtx_range("xlmimo_gen_drops");
   g_err[0] = 0;
   if (bad_users(users)) return xlh::set_error(XLMIMO_EINVAL, "gen_drops: invalid user law");
   if (K < 1 || n_drops < 0 || (!pos && n_drops > 0))
@@ -288,6 +298,7 @@ size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64
 
 int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,
                       int32_t precision, int32_t mode, double *gram, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_range("xlmimo_gram_exact");
   g_err[0] = 0;
   if (bad_array(array)) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: invalid array");
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "gram_exact: K=%d n_drops=%lld", K, (long long)n_drops);
@@ -303,6 +314,7 @@ int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K,
 
 int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,
                             double *gram, uint32_t *flags, void *stream) {
+  NvtxRange nvtx_range("xlmimo_gram_closed_form");
   g_err[0] = 0;
   if (bad_array(array)) return xlh::set_error(XLMIMO_EINVAL, "closed_form: invalid array");
   if (array->kind != XLMIMO_ULA) return xlh::set_error(XLMIMO_EUNSUPPORTED, "closed_form: ULA only (PAPER.md:40)");
@@ -315,12 +327,13 @@ int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double *pos, int3
 
 size_t xlmimo_sum_rate_workspace(int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers) {
   if (K < 1 || K > xl::kMaxKLarge || n_drops < 0 || n_snr < 1 || n_snr > xl::kMaxSnr) return 0;
-  if (K <= xl::kMaxK || !(receivers & XLMIMO_RECV_CAP)) return 0;
-  return xlh::large_k_ws_bytes(K, n_drops, n_snr);
+  if (K <= xl::kMaxK) return 0;
+  return xlh::sum_rate_large_ws_bytes(K, n_drops, n_snr, receivers);
 }
 
 int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
                        uint32_t receivers, double *rates, uint32_t *flags, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_range("xlmimo_sum_rate_ws");
   g_err[0] = 0;
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: K=%d", K);
   if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: K=%d > %d", K, xl::kMaxKLarge);
@@ -328,8 +341,8 @@ int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const dou
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: receivers");
   if (n_drops > 0 && (!gram || !rates)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: null pointer");
   if (K > xl::kMaxK) {
-    if (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE))
-      return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: ZF/MMSE need K <= %d (K=%d)", xl::kMaxK, K);
+    if ((receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)) && K > xl::kMaxKInv)
+      return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: ZF/MMSE need K <= %d (K=%d)", xl::kMaxKInv, K);
     return xlh::launch_sum_rate_large(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, ws, ws_bytes,
                                       (cudaStream_t)stream);
   }
@@ -343,12 +356,13 @@ int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double
 
 size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr) {
   if (K < 1 || K > xl::kMaxKLarge || n_drops < 0 || n_snr < 1 || n_snr > xl::kMaxSnr) return 0;
-  return xlh::large_k_ws_bytes(K, n_drops, 1 + n_snr);
+  return xlh::large_k_ws_bytes(K, n_drops, 1 + n_snr, false);
 }
 
 int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
                         double *rstat, double *bounds, double *eig, uint32_t *flags, void *ws, size_t ws_bytes,
                         void *stream) {
+  NvtxRange nvtx_range("xlmimo_app_a_bounds");
   g_err[0] = 0;
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: K=%d", K);
   if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "app_a_bounds: K=%d > %d", K, xl::kMaxKLarge);
@@ -363,6 +377,7 @@ int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const do
 
 int xlmimo_sum_rate_mismatched(const double *gram, const double *gram_model, int32_t K, int64_t n_drops,
                                const double *snr_db, int32_t n_snr, double *rates, uint32_t *flags, void *stream) {
+  NvtxRange nvtx_range("xlmimo_sum_rate_mismatched");
   g_err[0] = 0;
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "sum_rate_mismatched: K=%d", K);
   if (K > xl::kMaxK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate_mismatched: K=%d > %d", K, xl::kMaxK);
@@ -376,6 +391,7 @@ int xlmimo_sum_rate_mismatched(const double *gram, const double *gram_model, int
 
 int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max, int32_t K, int64_t n_drops,
                           uint64_t seed, uint64_t first_drop, double *pos, void *stream) {
+  NvtxRange nvtx_range("xlmimo_gen_drops_rect");
   g_err[0] = 0;
   if (!(x_min > 0.0) || !(x_min <= x_max) || !(y_min <= y_max) || !std::isfinite(x_max) || !std::isfinite(y_min) ||
       !std::isfinite(y_max))
@@ -398,6 +414,7 @@ int xlmimo_saturation_sweep(const xlmimo_array_t *array, const int64_t *n_list, 
                             const double *snr_db, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
                             int32_t precision, double t, double *ergodic, int64_t *n_valid, double *sat,
                             double *per_drop, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_range("xlmimo_saturation_sweep");
   g_err[0] = 0;
   int rc = validate_sweep(array, n_list, n_n, K, n_drops, snr_db, n_snr, receivers, gram_kind, precision, t);
   if (rc) return rc;
@@ -412,6 +429,7 @@ int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const int64_t *n_l
                                  int32_t n_snr, uint32_t receivers, int32_t gram_kind, int32_t precision, double t,
                                  double *ergodic, int64_t *n_valid, double *sat, void *ws, size_t ws_bytes,
                                  void *stream) {
+  NvtxRange nvtx_range("xlmimo_saturation_sweep_host");
   g_err[0] = 0;
   int rc = validate_sweep(array, n_list, n_n, K, n_drops, snr_db, n_snr, receivers, gram_kind, precision, t);
   if (rc) return rc;

@@ -129,21 +129,25 @@ __global__ void __launch_bounds__(256) bounds_warp_kernel(BoundsParams P) {
 
 // ------------------------------------------------------------------ K > 64: log-determinants
 // Problem p = (drop d, matrix m): m = 0 .. n_mat-1.  first_is_r: m == 0 builds R (App. A);
-// every other m builds I + rho_m G.  log2det[p] = log2 det (NaN if not PD / not built).
+// every other m builds alpha_m I + rho_m G (I + rho G for CAP/MMSE, G for ZF).
+// log2det[p] = log2 det (NaN if not PD / not built); dinv[p][i] = [A^{-1}]_ii when
+// requested (shared-memory kernel only).
 struct CholParams {
   const double *gram;
   double2 *ws;       // tiled kernel: [n_slots][Kp][Kp]
   double *log2det;   // [n_prob]
+  double *dinv;      // [n_prob][K] or null
   int K, Kp, nt;
   int64_t n_prob;
   int n_mat;         // matrices per drop
   int first_is_r;    // matrix 0 of each drop is R
-  double rho[xl::kMaxSnr + 1];  // rho of matrix m (unused for R)
+  double rho[xl::kMaxSnr + 2];    // rho of matrix m (unused for R)
+  double alpha[xl::kMaxSnr + 2];  // identity weight of matrix m
 };
 
-// value (i, j) of problem matrix (R or I + rho G), i, j < K
+// value (i, j) of problem matrix (R or alpha I + rho G), i, j < K
 __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, int j, bool is_r, double rho,
-                                              bool &good) {
+                                              double alpha, bool &good) {
   const double2 g = G[(size_t)i * K + j];
   good &= isfinite(g.x) && isfinite(g.y);
   if (is_r) {
@@ -153,7 +157,7 @@ __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, in
     const double s = rsqrt(gi) * rsqrt(gj);
     return make_double2(g.x * s, g.y * s);
   }
-  return (i == j) ? make_double2(1.0 + rho * g.x, 0.0) : make_double2(rho * g.x, rho * g.y);
+  return (i == j) ? make_double2(alpha + rho * g.x, 0.0) : make_double2(rho * g.x, rho * g.y);
 }
 
 // 64 < K <= kSmemK: one CTA per matrix, the packed lower triangle resident in shared
@@ -161,11 +165,15 @@ __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, in
 // unblocked right-looking Cholesky: per column j the pivot, the column scaled by
 // 1/L_jj, and the rank-1 update of the trailing triangle with warps over columns and
 // lanes over rows (contiguous, conflict-free).
-constexpr int kSmemK = 160;
+// With dinv requested, [A^{-1}]_ii = ||L^{-1} e_i||^2 follows: warp per i, forward
+// substitution L x = e_i with x_m held by lane m % 32 (register slot m / 32), the
+// pivot element broadcast by shuffle, the column of L read from shared memory.
+constexpr int kSmemK = xl::kMaxKInv;
+constexpr int kSmemRpl = (kSmemK + 31) / 32;
 
 __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
   extern __shared__ double2 Ls[];
-  __shared__ int s_ok;
+  __shared__ double s_inv[kSmemK];  // 1 / L_jj
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kCtaThreads / 32;
   const int K = P.K;
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
     // column j of the lower triangle = conj of row j of G (coalesced reads)
     for (int j = warp; j < K; j += NW)
       for (int i = j + lane; i < K; i += 32) {
-        const double2 v = chol_entry(G, K, j, i, is_r, P.rho[m], good);
+        const double2 v = chol_entry(G, K, j, i, is_r, P.rho[m], P.alpha[m], good);
         Ls[off(j) + i - j] = make_double2(v.x, -v.y);
       }
     const int ok0 = __syncthreads_and(good ? 1 : 0);
@@ -193,7 +201,10 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
         break;
       }
       const double ljj = sqrt(piv), inv = 1.0 / ljj;
-      if (tid == 0) ld += 2.0 * log2(ljj);
+      if (tid == 0) {
+        ld += 2.0 * log2(ljj);
+        s_inv[j] = inv;
+      }
       __syncthreads();  // all pivot reads done before the column is rescaled
       for (int i = j + tid; i < K; i += kCtaThreads) {
         double2 v = Ls[oj + i - j];
@@ -215,6 +226,46 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
       __syncthreads();
     }
     if (tid == 0) P.log2det[prob] = ok ? ld : kNaN;
+    if (P.dinv) {
+      double *dout = P.dinv + (size_t)prob * K;
+      for (int i = warp; i < K; i += NW) {
+        if (!ok) {
+          if (lane == 0) dout[i] = kNaN;
+          continue;
+        }
+        double xr[kSmemRpl], xi[kSmemRpl];
+#pragma unroll
+        for (int r = 0; r < kSmemRpl; ++r) {
+          xr[r] = (lane + 32 * r == i) ? 1.0 : 0.0;
+          xi[r] = 0.0;
+        }
+        double sum = 0.0;
+        for (int k = i; k < K; ++k) {
+          const int rk = k >> 5;
+          double vr = 0.0, vi = 0.0;
+#pragma unroll
+          for (int r = 0; r < kSmemRpl; ++r)
+            if (r == rk) {
+              vr = xr[r];
+              vi = xi[r];
+            }
+          vr = __shfl_sync(0xffffffffu, vr, k & 31) * s_inv[k];
+          vi = __shfl_sync(0xffffffffu, vi, k & 31) * s_inv[k];
+          sum += vr * vr + vi * vi;
+          const int ok2 = off(k);
+#pragma unroll
+          for (int r = 0; r < kSmemRpl; ++r) {
+            const int mm = lane + 32 * r;
+            if (mm > k && mm < K) {
+              const double2 l = Ls[ok2 + mm - k];  // L_mk
+              xr[r] -= l.x * vr - l.y * vi;
+              xi[r] -= l.x * vi + l.y * vr;
+            }
+          }
+        }
+        if (lane == 0) dout[i] = sum;
+      }
+    }
     __syncthreads();
   }
 }
@@ -252,7 +303,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
     for (int i = warp; i < Kp; i += NW)  // lower triangle, identity padding
       for (int j = lane; j <= i; j += 32) {
         double2 v = make_double2(i == j ? 1.0 : 0.0, 0.0);
-        if (i < K) v = chol_entry(G, K, i, j, is_r, P.rho[m], good);
+        if (i < K) v = chol_entry(G, K, i, j, is_r, P.rho[m], P.alpha[m], good);
         A[(size_t)i * Kp + j] = v;
       }
     const int ok0 = __syncthreads_and(good ? 1 : 0);
@@ -410,7 +461,8 @@ __global__ void __launch_bounds__(kCtaThreads) bounds_finish_kernel(BoundsParams
   }
 }
 
-// Large-K receivers (CAP from the tiled log-dets, MRC from G), same
+// Large-K receivers: CAP from the log-dets of I + rho G, MMSE from the diagonal of its
+// inverse, ZF from the diagonal of G^{-1}, MRC straight from G; same
 // output order and flag rules as the warp receivers (xl_rates.cu).
 struct LargeRateParams {
   const double *gram;
@@ -419,10 +471,12 @@ struct LargeRateParams {
   int K;
   int n_snr, n_recv;
   uint32_t receivers;
+  int n_mat, mat_g;  // problems per drop; index of the G problem (ZF) or -1
   double rho[xl::kMaxSnr];
 };
 
-__global__ void __launch_bounds__(kCtaThreads) rates_large_finish_kernel(LargeRateParams P, const double *log2det) {
+__global__ void __launch_bounds__(kCtaThreads) rates_large_finish_kernel(LargeRateParams P, const double *log2det,
+                                                                         const double *dinv) {
   __shared__ double red[kCtaThreads / 32];
   const int64_t d = blockIdx.x;
   const int K = P.K;
@@ -438,16 +492,37 @@ __global__ void __launch_bounds__(kCtaThreads) rates_large_finish_kernel(LargeRa
   uint32_t fl = 0;
   const bool mrc = (P.receivers & XLMIMO_RECV_MRC) != 0;
   if (mrc && !dpos) fl |= XLMIMO_FLAG_MRC_UNDEF;
+  const int64_t pg = d * P.n_mat + P.mat_g;
+  const bool zf_ok = P.mat_g >= 0 && !isnan(log2det[pg]);
+  if (P.mat_g >= 0 && !zf_ok) fl |= XLMIMO_FLAG_G_NOT_PD;
   for (int s = 0; s < P.n_snr; ++s) {
     int r = 0;
+    const double rho = P.rho[s];
+    const int64_t pa = d * P.n_mat + s;
+    const bool a_used = (P.receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) != 0;
+    const bool a_ok = a_used && !isnan(log2det[pa]);
+    if (a_used && !a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
     if (P.receivers & XLMIMO_RECV_CAP) {
-      const double cap = log2det[d * P.n_snr + s];
-      if (isnan(cap)) fl |= XLMIMO_FLAG_A_NOT_PD;
-      if (threadIdx.x == 0) out[s * P.n_recv + r] = cap;
+      if (threadIdx.x == 0) out[s * P.n_recv + r] = a_ok ? log2det[pa] : kNaN;
+      ++r;
+    }
+    if (P.receivers & XLMIMO_RECV_ZF) {  // SINR_i = rho / [G^{-1}]_ii
+      double part = 0.0;
+      if (zf_ok)
+        for (int i = threadIdx.x; i < K; i += blockDim.x) part += log2(1.0 + rho / dinv[pg * K + i]);
+      const double c = block_sum(part, red);
+      if (threadIdx.x == 0) out[s * P.n_recv + r] = zf_ok ? c : kNaN;
+      ++r;
+    }
+    if (P.receivers & XLMIMO_RECV_MMSE) {  // SINR_i = 1 / [(I + rho G)^{-1}]_ii - 1
+      double part = 0.0;
+      if (a_ok)
+        for (int i = threadIdx.x; i < K; i += blockDim.x) part += log2(1.0 + (1.0 / dinv[pa * K + i] - 1.0));
+      const double c = block_sum(part, red);
+      if (threadIdx.x == 0) out[s * P.n_recv + r] = a_ok ? c : kNaN;
       ++r;
     }
     if (mrc) {
-      const double rho = P.rho[s];
       double part = 0.0;
       for (int i = threadIdx.x; i < K; i += blockDim.x) {
         const double gii = G[(size_t)i * K + i].x;
@@ -593,7 +668,7 @@ int n_chol_slots(int64_t n_prob) {
 }
 
 int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool first_is_r, const double *rho,
-                double *log2det, void *ws, size_t ws_bytes, cudaStream_t s) {
+                const double *alpha, double *log2det, double *dinv, void *ws, size_t ws_bytes, cudaStream_t s) {
   CholParams C;
   memset(&C, 0, sizeof(C));
   C.gram = gram;
@@ -603,13 +678,18 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
   C.n_prob = n_drops * n_mat;
   C.n_mat = n_mat;
   C.first_is_r = first_is_r ? 1 : 0;
-  for (int m = 0; m < n_mat; ++m) C.rho[m] = rho[m];
+  for (int m = 0; m < n_mat; ++m) {
+    C.rho[m] = rho[m];
+    C.alpha[m] = alpha[m];
+  }
   C.log2det = log2det;
+  C.dinv = dinv;
   C.ws = (double2 *)ws;
+  if (dinv && K > kSmemK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "inverse diagonal needs K <= %d", kSmemK);
   xlh::KTimer tm(s, "chol_logdet");
   if (K <= kSmemK) {
     const size_t smem = (size_t)K * (K + 1) / 2 * sizeof(double2);
-    const int per_sm = (int)((220 * 1024) / smem);
+    const int per_sm = (int)((220 * 1024) / (smem + kSmemK * sizeof(double)));
     const int64_t grid = (int64_t)n_chol_slots(C.n_prob) * (per_sm > 1 ? per_sm : 1);
     cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     chol_smem_kernel<<<(unsigned)(grid < C.n_prob ? grid : C.n_prob), kCtaThreads, smem, s>>>(C);
@@ -638,9 +718,11 @@ size_t chol_slot_bytes(int K, int64_t n_prob) {
 namespace xlh {
 
 // Scratch for the large-K path: Cholesky slots + per-problem log-dets.
-size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat) {
-  if (K <= xl::kMaxK || n_drops == 0) return 0;
-  return chol_slot_bytes(K, n_drops * n_mat) + align256((size_t)n_drops * n_mat * sizeof(double));
+size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat, bool with_dinv) {
+  if (K <= xl::kMaxK || n_drops == 0 || n_mat == 0) return 0;
+  const size_t n_prob = (size_t)n_drops * n_mat;
+  return chol_slot_bytes(K, (int64_t)n_prob) + align256(n_prob * sizeof(double)) +
+         (with_dinv ? align256(n_prob * K * sizeof(double)) : 0);
 }
 
 int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr, double *rstat,
@@ -677,14 +759,18 @@ int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_
     const int n_mat = 1 + n_snr;
     const int64_t n_prob = n_drops * n_mat;
     const size_t chol_b = chol_slot_bytes(K, n_prob);
-    if (ws_bytes < large_k_ws_bytes(K, n_drops, n_mat) || !ws)
+    if (ws_bytes < large_k_ws_bytes(K, n_drops, n_mat, false) || !ws)
       return set_error(XLMIMO_EWORKSPACE, "app_a_bounds: workspace %zu < %zu", ws_bytes,
-                       large_k_ws_bytes(K, n_drops, n_mat));
+                       large_k_ws_bytes(K, n_drops, n_mat, false));
     double *log2det = (double *)((char *)ws + chol_b);
-    double rho[xl::kMaxSnr + 1];
+    double rho[xl::kMaxSnr + 1], alpha[xl::kMaxSnr + 1];
     rho[0] = 0.0;
-    for (int i = 0; i < n_snr; ++i) rho[1 + i] = P.rho[i];
-    rc = launch_chol(gram, K, n_drops, n_mat, true, rho, log2det, ws, chol_b, s);
+    alpha[0] = 0.0;
+    for (int i = 0; i < n_snr; ++i) {
+      rho[1 + i] = P.rho[i];
+      alpha[1 + i] = 1.0;
+    }
+    rc = launch_chol(gram, K, n_drops, n_mat, true, rho, alpha, log2det, nullptr, ws, chol_b, s);
     if (rc) return rc;
     KTimer tm(s, "app_a_finish");
     bounds_finish_kernel<<<(unsigned)n_drops, kCtaThreads, 0, s>>>(P, log2det);
@@ -705,6 +791,13 @@ int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_
   return check_launch("eig_jacobi_kernel");
 }
 
+size_t sum_rate_large_ws_bytes(int K, int64_t n_drops, int n_snr, uint32_t receivers) {
+  const int n_a = (receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) ? n_snr : 0;
+  const int n_g = (receivers & XLMIMO_RECV_ZF) ? 1 : 0;
+  return large_k_ws_bytes(K, n_drops, n_a + n_g, (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)) != 0);
+}
+
+// Problems per drop: I + rho_s G for every SNR (CAP and/or MMSE), then G (ZF).
 int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr,
                           uint32_t receivers, double *rates, uint32_t *flags, void *ws, size_t ws_bytes,
                           cudaStream_t s) {
@@ -719,19 +812,33 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
   P.receivers = receivers;
   P.n_recv = __builtin_popcount(receivers & 15u);
   for (int i = 0; i < n_snr; ++i) P.rho[i] = pow(10.0, snr_db[i] / 10.0);
-  double *log2det = nullptr;
-  if (receivers & XLMIMO_RECV_CAP) {
-    const int64_t n_prob = n_drops * n_snr;
+  const int n_a = (receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) ? n_snr : 0;
+  const int n_g = (receivers & XLMIMO_RECV_ZF) ? 1 : 0;
+  const bool need_dinv = (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)) != 0;
+  P.n_mat = n_a + n_g;
+  P.mat_g = n_g ? n_a : -1;
+  double *log2det = nullptr, *dinv = nullptr;
+  if (P.n_mat) {
+    const int64_t n_prob = n_drops * P.n_mat;
+    const size_t need = sum_rate_large_ws_bytes(K, n_drops, n_snr, receivers);
+    if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "sum_rate (K > 64): workspace %zu < %zu", ws_bytes, need);
     const size_t chol_b = chol_slot_bytes(K, n_prob);
-    if (ws_bytes < large_k_ws_bytes(K, n_drops, n_snr) || !ws)
-      return set_error(XLMIMO_EWORKSPACE, "sum_rate (K > 64): workspace %zu < %zu", ws_bytes,
-                       large_k_ws_bytes(K, n_drops, n_snr));
     log2det = (double *)((char *)ws + chol_b);
-    const int rc = launch_chol(gram, K, n_drops, n_snr, false, P.rho, log2det, ws, chol_b, s);
+    if (need_dinv) dinv = (double *)((char *)ws + chol_b + align256((size_t)n_prob * sizeof(double)));
+    double rho[xl::kMaxSnr + 2], alpha[xl::kMaxSnr + 2];
+    for (int i = 0; i < n_a; ++i) {
+      rho[i] = P.rho[i];
+      alpha[i] = 1.0;
+    }
+    if (n_g) {
+      rho[n_a] = 1.0;
+      alpha[n_a] = 0.0;
+    }
+    const int rc = launch_chol(gram, K, n_drops, P.n_mat, false, rho, alpha, log2det, dinv, ws, chol_b, s);
     if (rc) return rc;
   }
   KTimer tm(s, "sum_rate_large_finish");
-  rates_large_finish_kernel<<<(unsigned)n_drops, kCtaThreads, 0, s>>>(P, log2det);
+  rates_large_finish_kernel<<<(unsigned)n_drops, kCtaThreads, 0, s>>>(P, log2det, dinv);
   tm.stop(s);
   count_launch();
   return check_launch("rates_large_finish_kernel");

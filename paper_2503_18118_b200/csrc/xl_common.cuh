@@ -14,6 +14,7 @@ namespace xl {
 constexpr double kC = 299792458.0;  // m/s, exact (R2)
 constexpr int kMaxK = 64;           // fused paths: K <= 64
 constexpr int kMaxKLarge = 1024;    // large-K paths (tiled Cholesky, block-pair Gram)
+constexpr int kMaxKInv = 160;       // ZF/MMSE (diagonal of an inverse) beyond K = 64: shared-memory Cholesky
 constexpr int kMaxSnr = 16;
 
 // ---------------------------------------------------------------------------
@@ -299,7 +300,8 @@ int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr
                     uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s);
 
 // xl_bounds.cu : Appendix A (NEXT-3) and the large-K (K > 64) receivers
-size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat);
+size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat, bool with_dinv);
+size_t sum_rate_large_ws_bytes(int K, int64_t n_drops, int n_snr, uint32_t receivers);
 int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr, double *rstat,
                   double *bounds, double *eig, uint32_t *flags, void *ws, size_t ws_bytes, cudaStream_t s);
 int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr,

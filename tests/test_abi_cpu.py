@@ -86,9 +86,11 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
                                  None) == -3
     assert L.xlmimo_app_a_bounds(rs, 8, 1, None, 1, rs, rs, None, None, None, 0, None) == -1
     assert L.xlmimo_app_a_bounds_workspace(8, 100, 1) == 0 < L.xlmimo_app_a_bounds_workspace(100, 100, 1)
-    assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # ZF, K>64
+    assert L.xlmimo_sum_rate(rs, 161, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # ZF, K>160
+    assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -3  # ZF: ws
     assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 1, rs, None, None) == -3  # CAP: ws
     assert L.xlmimo_sum_rate_workspace(100, 4, 1, 8) == 0 < L.xlmimo_sum_rate_workspace(100, 4, 1, 1)
+    assert L.xlmimo_sum_rate_workspace(100, 4, 1, 1) < L.xlmimo_sum_rate_workspace(100, 4, 1, 7)  # + inverse diagonals
     nl = np.array([256, 512, 1023], dtype=np.int64)  # mixed parity
     erg = np.zeros(16)
     nv = np.zeros(16, dtype=np.int64)

@@ -30,11 +30,13 @@ def xl():
 
 
 def test_e1_sweep_k100_parity_small(xl, orc):
-    """The K = 100 sweep path (block-pair Gram with nested levels, Cholesky CAP, MRC)
+    """The K = 100 sweep path (block-pair Gram with nested levels, Cholesky CAP/ZF/MMSE, MRC)
     against the oracle's independent per-N sweep on 3 drops and small arrays."""
     pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 100, 3, seed=0)
-    nl = [64, 512, 2048]
-    rec = xl.RECV_CAP | xl.RECV_MRC
+    # N >= 10 K: G well conditioned on these drops (at N = 128 one drop's G has lambda_min /
+    # lambda_max ~ 1e-17, where the sign of the last ZF pivot is rounding, R10)
+    nl = [1024, 1536, 2048]
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
     res = xl.saturation_sweep(xl.Array.ula(2048, 100e9), nl, 100, 3, [0.0, 20.0], rec, pos=pos, per_drop=True)
     erg, nv, sat, pd = orc.saturation_sweep(orc.array("ula", n_y=2048, fc_hz=100e9), nl, pos.cpu().numpy(),
                                             [0.0, 20.0], rec, per_drop=True)

@@ -73,5 +73,34 @@ def main(cfgs):
         print(json.dumps(res), flush=True)
 
 
+def steady_cfg1(D=10 ** 6):
+    """cfg1 in a steady-state batch: 10^6 drops through drops -> exact fp64 Gram
+    -> closed-form Gram -> CAP/ZF/MMSE/MRC, per-kernel device times (one drop is too small to
+    time on its own: the 1000-drop config is launch-bound)."""
+    w = CONFIGS[1]
+    arr = xl.Array.ula(w.n_y, w.fc_hz)
+    users = xl.Users.polar(w.r, w.az)
+    pos = xl.gen_drops(users, w.K, D, seed=w.seed)
+    allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+
+    def path():
+        xl.gen_drops(users, w.K, D, seed=w.seed, out=pos)
+        G = xl.gram_exact(arr, pos)
+        Gt, fl = xl.gram_closed_form(arr, pos)
+        xl.sum_rate(G, list(w.snr_db), allr)
+        xl.sum_rate(Gt, list(w.snr_db), allr, flags=fl)
+    t = timed(path)
+    tot = sum(t.values())
+    cmac = D * w.N * w.K * (w.K + 1) // 2
+    print(json.dumps({"cfg": "1-steady", "workload": w.name + " (steady-state batch)", "drops_timed": D,
+                      "kernel_ms": t, "total_kernel_ms": tot, "drops_per_s": D / (tot * 1e-3),
+                      "gram_cmac_per_s": cmac / (t.get("gram_fused_split_fp64", float("nan")) * 1e-3)}), flush=True)
+
+
 if __name__ == "__main__":
-    main([int(a) for a in sys.argv[1:]] or [1, 3, 4, 5])
+    args = sys.argv[1:]
+    if "1s" in args:
+        steady_cfg1()
+        args = [a for a in args if a != "1s"]
+    if args or "1s" not in sys.argv[1:]:
+        main([int(a) for a in args] or [1, 3, 4, 5])
