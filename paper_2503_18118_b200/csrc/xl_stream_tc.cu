@@ -569,8 +569,11 @@ bool stream_tc_supported(int K, int64_t N) { return K >= 9 && K <= 64 && (N % 4)
 
 int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
 
+// UPA: a generator task (kTaskE consecutive elements off one fp64 anchor, the delta
+// along y) must not cross a row of the n_y x n_z grid, so n_y must be a multiple of
+// kTaskE; other UPAs take the CUDA-core fp32 kernel.
 bool fused_tc_supported(const ArrayP &a, int K) {
-  return K >= 9 && K <= 64 && (a.kind == XLMIMO_ULA || (a.n_y % 4) == 0);
+  return K >= 9 && K <= 64 && (a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0);
 }
 
 // Fused fp32 Gram on tcgen05: partials [drop][chunk][NP][2] into ws (stream_tc_chunks(N) per drop).

@@ -75,6 +75,8 @@ CASES = [
     ("ula", 2049, 1, 100e9, 20, 3, (2.0, 20.0), (-75.0, 75.0), (0.0, 0.0)),     # K = 20 (3 groups, odd N)
     ("upa", 51, 29, 100e9, 45, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # K = 45 (6 groups, ragged UPA)
     ("ula", 1500, 1, 140e9, 52, 2, (5.0, 100.0), (-60.0, 60.0), (0.0, 0.0)),    # K = 52 (7 groups)
+    ("upa", 12, 10, 100e9, 16, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # UPA rows not a multiple of 8
+    ("upa", 24, 11, 100e9, 12, 2, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0)),   # UPA rows a multiple of 8
 ]
 
 
