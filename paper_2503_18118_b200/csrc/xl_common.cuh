@@ -290,6 +290,9 @@ bool fused_tc_supported(const ArrayP &a, int K);
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
                     cudaStream_t s);
 int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s);
+bool materialise_tc_supported(const ArrayP &a);
+int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
+                            int nb, float *H, cudaStream_t s);
 
 // xl_closed.cu : out[drop][lvl][K][K][2] for M = n_list[lvl]
 int launch_closed_form(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *m_list,

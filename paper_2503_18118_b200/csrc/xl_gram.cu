@@ -1598,8 +1598,13 @@ int launch_materialised(const ArrayP &a, const double *pos, int K, int64_t n_dro
     const int64_t n_pad = mat_npad(K, N);
     {
       KTimer tm(s, "h_materialise");
-      h_materialise_kernel<<<dim3((unsigned)((n_pad + 255) / 256), (unsigned)nb), 256, 0, s>>>(P, H, n_pad, tc ? 1 : 0,
-                                                                                             tc ? 1 : 0);
+      if (tc && materialise_tc_supported(a)) {  // anchor + fp32-delta generator, TF32 tiles
+        const int rc = launch_h_materialise_tc(a, pos, K, N, n_pad, d0, nb, H, s);
+        if (rc) return rc;
+      } else {
+        h_materialise_kernel<<<dim3((unsigned)((n_pad + 255) / 256), (unsigned)nb), 256, 0, s>>>(P, H, n_pad,
+                                                                                               tc ? 1 : 0, tc ? 1 : 0);
+      }
       tm.stop(s);
       count_launch();
     }

@@ -320,11 +320,57 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) { return (__float_as_uint(
 // byte offset of the 16-B chunk c (0..7) of row r in a SWIZZLE_128B K-major tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
+
+// One generator task: the TF32 (RNA) coefficients h = a e^{-j 2 pi r / lambda} (Eq. 3) of
+// one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7, from an fp64
+// anchor at t0 (distance, 1/r, phase reduced as frac(r / lambda) in fp64) and fp32
+// deltas along y: Delta(r^2) = dd (2 dy + dd), delta = Delta / r_c^2,
+// Delta r = r_c delta (1/2 - delta/8 + delta^2/16), phase re-reduced in fp32, MUFU
+// sin/cos, amplitude a_c (1 - 3/4 delta + 21/32 delta^2).  Elements past N are 0.
+// uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
+__device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
+                                              int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
+                                              float pitch_f, uint32_t (&vr)[kTaskE], uint32_t (&vi)[kTaskE]) {
+  double ey, ez = 0.0;
+  if (kind == XLMIMO_ULA) {
+    ey = ((double)t0 - 0.5 * (double)(N - 1)) * pitch;
+  } else {
+    const int64_t q = t0 / n_y, pp = t0 - q * n_y;
+    ey = ((double)pp - 0.5 * (double)(n_y - 1)) * pitch;
+    ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
+  }
+  const double dy = ey - uc.y, dz = ez - uc.z;
+  const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
+  const double ir = xl::rsqrt_nr(r2);
+  const double rc = r2 * ir;
+  const double qc = rc * inv_lambda;
+  const float fc = (float)(qc - rint(qc));
+  const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
+  const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
+  const int64_t nv64 = N - t0;  // valid elements of this task (padding past N is 0)
+  const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
+#pragma unroll
+  for (int m = 0; m < kTaskE; ++m) {
+    const float dd = (float)m * pitch_f;
+    const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
+    const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
+    float cyc = fmaf(dr, inv_lambda_f, fc);
+    // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
+    // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
+    cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);
+    float sn, co;
+    __sincosf(6.28318530717958647692f * cyc, &sn, &co);
+    const float a = (m < nv) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
+    vr[m] = tf32_rna(a * co);
+    vi[m] = tf32_rna(-a * sn);
+  }
+}
+
 constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
 constexpr int kGenGroups = 8;      // group g owns ring slot g (stage k -> slot k % 8)
 constexpr int kFStages = 12;      // ring slots: stage k -> slot k % 12, generated by group k % 8
 constexpr int kGenThreads = 32 * kGenWarps;
-constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
 constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
 constexpr int kMmaWarp = kEpiWarp0 + 4;            // 20
 constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 672
@@ -414,42 +460,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
           const int u = tb / (kBoxK / kTaskE), g8 = tb % (kBoxK / kTaskE);
           const int row0 = blk * P.rb + 2 * u;
           const int64_t t0 = xs + kBoxK * blk + kTaskE * g8;
-          const double4 uc = su[u];
-          // fp64 anchor at element t0 (natural order: ULA y = (t - (N-1)/2) pitch; UPA t = q n_y + p)
-          double ey, ez = 0.0;
-          if (P.kind == XLMIMO_ULA) {
-            ey = ((double)t0 - 0.5 * (double)(P.N - 1)) * P.pitch;
-          } else {
-            const int64_t q = t0 / P.n_y, pp = t0 - q * P.n_y;
-            ey = ((double)pp - 0.5 * (double)(P.n_y - 1)) * P.pitch;
-            ez = ((double)q - 0.5 * (double)(P.n_z - 1)) * P.pitch;
-          }
-          const double dy = ey - uc.y, dz = ez - uc.z;
-          const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
-          const double ir = xl::rsqrt_nr(r2);
-          const double rc = r2 * ir;
-          const double qc = rc * inv_lambda;
-          const float fc = (float)(qc - rint(qc));
-          const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
-          const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
-          const int64_t nv64 = P.N - t0;  // valid elements of this task (padding past N is 0)
-          const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
           uint32_t vr[kTaskE], vi[kTaskE];
-#pragma unroll
-          for (int m = 0; m < kTaskE; ++m) {
-            const float dd = (float)m * pitch_f;
-            const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
-            const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
-            float cyc = fmaf(dr, inv_lambda_f, fc);
-            // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
-            // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
-            cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);
-            float sn, co;
-            __sincosf(6.28318530717958647692f * cyc, &sn, &co);
-            const float a = (m < nv) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
-            vr[m] = tf32_rna(a * co);
-            vi[m] = tf32_rna(-a * sn);
-          }
+          gen_task_tf32(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
 #pragma unroll
           for (int h = 0; h < kTaskE / 4; ++h) {
             const int chunk = (kTaskE / 4) * g8 + h;
@@ -549,6 +561,35 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   }
 }
 
+// K4a for the tcgen05 stream: H of a batch of drops written straight into the tiled32
+// TF32 layout [drop - drop0][N_pad / 32][2K][32] (row 2k = Re h_k, 2k + 1 = Im h_k) with
+// the task generator above: a warp covers one 32-element tile for 8 users, lane =
+// (user u = lane / 4, elements 8 (lane % 4) .. +7), so each lane stores 2 x 32 B and a
+// warp writes sixteen full 128-B rows.  Block = 8 warps = 8 consecutive tiles; grid =
+// (ceil(N_pad / 256), batch drops x ceil(K / 8) user groups).  Elements past N are 0.
+__global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos, int K, int kind, int64_t N,
+                                                               int64_t n_pad, int64_t n_y, int64_t n_z, double pitch,
+                                                               double lambda, double sqrt_beta0, int64_t drop0,
+                                                               int n_ugrp, float *H) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bd = blockIdx.y / n_ugrp, ug = blockIdx.y - bd * n_ugrp;
+  const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
+  if (tile * 32 >= n_pad) return;
+  const int u = 8 * ug + (lane >> 2);
+  if (u >= K) return;
+  const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
+  const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
+  const int64_t t0 = tile * 32 + 8 * (lane & 3);
+  const double inv_lambda = 1.0 / lambda;
+  uint32_t vr[kTaskE], vi[kTaskE];
+  gen_task_tf32(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch, vr, vi);
+  float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * K) + 2 * u) * 32 + 8 * (lane & 3);
+  __stcs(reinterpret_cast<uint4 *>(row), make_uint4(vr[0], vr[1], vr[2], vr[3]));
+  __stcs(reinterpret_cast<uint4 *>(row) + 1, make_uint4(vr[4], vr[5], vr[6], vr[7]));
+  __stcs(reinterpret_cast<uint4 *>(row + 32), make_uint4(vi[0], vi[1], vi[2], vi[3]));
+  __stcs(reinterpret_cast<uint4 *>(row + 32) + 1, make_uint4(vi[4], vi[5], vi[6], vi[7]));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -613,6 +654,18 @@ int stream_tc_parts(int K) { return kRows / rows_per_block(K); }
 
 // One batch: H in the tiled32 layout [nb][N/32][2K][32] fp32 (TF32-rounded, N a
 // multiple of 128), partials for drops [drop0, drop0+nb).
+// UPA rows must hold whole generator tasks (see fused_tc_supported).
+bool materialise_tc_supported(const ArrayP &a) { return a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0; }
+
+int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
+                            int nb, float *H, cudaStream_t s) {
+  const int n_ugrp = (K + 7) / 8;
+  const dim3 grid((unsigned)((n_pad + 255) / 256), (unsigned)(nb * n_ugrp));
+  h_materialise_tc_kernel<<<grid, 256, 0, s>>>(pos, K, a.kind, N, n_pad, a.n_y, a.kind == XLMIMO_ULA ? 1 : a.n_z,
+                                               a.pitch, a.lambda, a.sqrt_beta0, drop0, n_ugrp, H);
+  return check_launch("h_materialise_tc_kernel");
+}
+
 int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s) {
   auto enc = encode_fn();
   if (!enc) return set_error(XLMIMO_ECUDA, "stream_tc: cuTensorMapEncodeTiled unavailable");
