@@ -513,6 +513,30 @@ def test_upa_diagonal_solid_angle(orc):
             assert G[i, i].real == pytest.approx(4 / lam ** 2 * om, rel=1e-5)
 
 
+def test_upa_reduces_to_ula_and_rotates(orc):
+    """R5 pins of the UPA off-diagonal (beyond the tiny-array mpmath check): a UPA with one
+    row (n_z = 1) IS the centred ULA of PAPER.md:52 for users in the z = 0 plane (same
+    element coordinates, x_eff = |x|); a single column (n_y = 1) is the same ULA along z,
+    so users mirrored (y, z) -> (z, y) see the identical Gram; and the 180-degree rotation
+    (y, z) -> (-y, -z) of the users about the array axis maps the centred grid onto itself,
+    leaving G unchanged.  The ULA path is pinned independently (mpmath, Eq. (4))."""
+    fc = 100e9
+    pos = orc.gen_drops(orc.users(r=(2.0, 20.0), az=(-60, 60)), 5, 3, seed=31)   # z = 0
+    G_upa = orc.gram_exact(orc.array("upa", n_y=300, n_z=1, fc_hz=fc), pos)
+    G_ula = orc.gram_exact(orc.array("ula", n_y=300, fc_hz=fc), pos)
+    assert normalized_err(G_upa, G_ula) < 1e-13
+    pz = orc.gen_drops(orc.users(r=(2.0, 20.0), az=(-60, 60), el=(-30, 30)), 5, 3, seed=32)
+    swapped = pz[..., [0, 2, 1]].copy()
+    G_col = orc.gram_exact(orc.array("upa", n_y=1, n_z=257, fc_hz=fc), pz)
+    G_row = orc.gram_exact(orc.array("upa", n_y=257, n_z=1, fc_hz=fc), swapped)
+    # (the distance sums dy^2 + dz^2 in the other order: 1-ulp r, the fp64 phase floor)
+    assert normalized_err(G_col, G_row) < 1e-11
+    arr = orc.array("upa", n_y=20, n_z=13, fc_hz=fc)
+    rot = pz.copy()
+    rot[..., 1:] *= -1.0
+    assert normalized_err(orc.gram_exact(arr, rot), orc.gram_exact(arr, pz)) < 1e-11
+
+
 # --------------------------------------------------------------------------- NEXT-1 / NEXT-4
 def _first_principles_mismatched(H, Gt, rho):
     """W = G~^{-1} H^H applied to the true H (numpy/LAPACK inverse): T = W H, noise W W^H / rho."""
