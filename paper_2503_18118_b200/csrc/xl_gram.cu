@@ -850,16 +850,26 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     for (int k = 0; k < JPW; ++k)
 #pragma unroll
       for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+    // warp w generates the consecutive rows [w R, (w+1) R) (row = s * G + g, g fastest),
+    // so runs of up to G rows share one element step s and decode its coordinates once
+    // (a UPA decode costs 4 FP64 ops, a ULA one 2: otherwise repeated for every group)
+    constexpr int R = (ROWS + NW - 1) / NW;
     auto generate = [&](int t0, int buf) {
       double *gre = dsm + buf * (2 * PLANE), *gim = gre + PLANE;
+      int s_cur = -1;
+      bool valid = false;
+      ElemPos ep;
 #pragma unroll
-      for (int i = 0; i < (ROWS + NW - 1) / NW; ++i) {
-        const int row = warp + i * NW;  // row = s * G + g
+      for (int i = 0; i < R; ++i) {
+        const int row = warp * R + i;
         if (ROWS % NW == 0 || row < ROWS) {
           const int s = row / G, g = row - s * G;
-          const int t = t0 + 4 * s + (lane & 3);
-          const bool valid = t < b;
-          const ElemPos ep = element_pos32<KIND>(P, valid ? t : a, fd, n_odd);
+          if (s != s_cur) {  // warp-uniform
+            s_cur = s;
+            const int t = t0 + 4 * s + (lane & 3);
+            valid = t < b;
+            ep = element_pos32<KIND>(P, valid ? t : a, fd, n_odd);
+          }
           const double4 uc = su[8 * g + (lane >> 2)];
           const double dy = ep.y - uc.y;
           double r2 = fma(dy, dy, uc.x);
