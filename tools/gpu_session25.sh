@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -p no:cacheprovider -k "fp64 or sweep_parity_many" > gpurun_out/pytest_s25.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_s25.log
+timeout 600 python tools/bench_configs.py 4 5 > gpurun_out/bc25.jsonl 2>&1; python -c "
+import json
+for l in open('gpurun_out/bc25.jsonl'):
+    d=json.loads(l); print(d['cfg'], d['fused_fp64']['ms'], d['fused_fp64']['fp64_frac_of_nominal'])"
