@@ -367,3 +367,26 @@ def test_sum_rate_mismatched_parity(xl, orc, K, N, fc):
     rz, _ = xl.sum_rate_mismatched(G, G, snr)
     zf, _ = xl.sum_rate(G, snr, xl.RECV_ZF)
     assert torch.allclose(rz, zf[..., 0], rtol=1e-10, atol=1e-10)
+
+
+def test_resume_by_first_drop_equals_one_run(xl):
+    """Checkpoint/resume: drops are addressed by (seed, drop index), so a sweep
+    run as two batches (first_drop = 0 and D/2) and combined with the multi-rank combine
+    (paper_2503_18118_b200.parallel) reproduces the one-batch sweep."""
+    from paper_2503_18118_b200 import parallel
+    w = CONFIGS[2]
+    D = 400
+    nl = [256, 512, 1024, 2048]
+    arr = xl.Array.ula(2048, w.fc_hz)
+    u = xl.Users.polar(w.r, w.az)
+    pitch = 0.5 * 299792458.0 / w.fc_hz
+    full = xl.saturation_sweep(arr, nl, w.K, D, list(w.snr_db), w.receivers,
+                               pos=xl.gen_drops(u, w.K, D, seed=3))
+    parts = [xl.saturation_sweep(arr, nl, w.K, D // 2, list(w.snr_db), w.receivers,
+                                 pos=xl.gen_drops(u, w.K, D // 2, seed=3, first_drop=f)) for f in (0, D // 2)]
+    v = sum(parallel.pack_sweep(p, D // 2, pitch) for p in parts)
+    comb = parallel.unpack_sweep(v, full["ergodic"].shape, pitch)
+    assert np.array_equal(comb["n_valid"], full["n_valid"])
+    assert np.nanmax(np.abs(comb["ergodic"] - full["ergodic"])) <= 1e-10
+    assert comb["sat"][2] == full["sat"][2]
+    assert abs(comb["sat"][0] - full["sat"][0]) <= 1e-12 * abs(full["sat"][0])
