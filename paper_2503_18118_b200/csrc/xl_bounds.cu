@@ -12,8 +12,8 @@
 // marks the matrix not positive definite (R10).
 //
 // Kernels
-//  * bounds_warp_kernel (K <= 64): one warp per drop, the matrix in shared memory,
-//    the same warp Cholesky as the receivers.
+//  * bounds_warp_kernel (K <= 64): one warp per drop, the packed lower triangle in
+//    shared memory, the same warp Cholesky as the receivers.
 //  * chol_smem_kernel (64 < K <= 160): one CTA per matrix, packed lower triangle in
 //    shared memory, unblocked right-looking Cholesky.
 //  * chol_tiled_kernel (K > 160): one CTA per matrix in a global workspace slot,
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) bounds_warp_kernel(BoundsParams P) {
   extern __shared__ double2 smem[];
   const int K = P.K;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double2 *As = smem + (size_t)warp * K * K;
+  double2 *As = smem + (size_t)warp * (K * (K + 1) / 2);  // packed lower triangle (xl_linalg.cuh)
   const int64_t d = (int64_t)blockIdx.x * nw + warp;
   if (d >= P.n_drops) return;
   const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
@@ -72,20 +72,23 @@ __global__ void __launch_bounds__(256) bounds_warp_kernel(BoundsParams P) {
     if (lane == 0 && P.flags) P.flags[d] = fin ? XLMIMO_FLAG_MRC_UNDEF : XLMIMO_FLAG_NONFINITE;
     return;
   }
-  // R (column-major: As[j*K + i] = R_ij = conj(R_ji)), unit diagonal
-  for (int e = lane; e < K * K; e += 32) {
-    const int j = e / K, i = e - j * K;
-    const double2 g = G[j * K + i];
-    const double s = rsqrt(G[i * K + i].x) * rsqrt(G[j * K + j].x);
-    As[e] = (i == j) ? make_double2(1.0, 0.0) : make_double2(g.x * s, -g.y * s);
+  // R, packed lower: R_ij = conj(R_ji) = conj(G_ji) / sqrt(G_ii G_jj), unit diagonal
+  for (int j = 0; j < K; ++j) {
+    const int oj = xlk::poff(K, j);
+    for (int i = j + lane; i < K; i += 32) {
+      const double2 g = G[j * K + i];
+      const double s = rsqrt(G[i * K + i].x) * rsqrt(G[j * K + j].x);
+      As[oj + i - j] = (i == j) ? make_double2(1.0, 0.0) : make_double2(g.x * s, -g.y * s);
+    }
   }
+  __syncwarp();
   double ldr = kNaN;
-  if (xlk::warp_cholesky<RPL>(As, K, lane)) {
+  if (xlk::warp_cholesky_packed<RPL>(As, K, lane)) {
     double part = 0.0;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int k = lane + 32 * r;
-      if (k < K) part += 2.0 * log2(As[k * K + k].x);
+      if (k < K) part += 2.0 * log2(As[xlk::poff(K, k)].x);
     }
     ldr = xlk::warp_sum(part);
   } else {
@@ -101,18 +104,21 @@ __global__ void __launch_bounds__(256) bounds_warp_kernel(BoundsParams P) {
     for (int i = lane; i < K; i += 32) lu += log2(1.0 + rho * G[i * K + i].x);
     lu = xlk::warp_sum(lu);
     __syncwarp();
-    for (int e = lane; e < K * K; e += 32) {
-      const int j = e / K, i = e - j * K;
-      const double2 g = G[j * K + i];
-      As[e] = make_double2((i == j ? 1.0 : 0.0) + rho * g.x, (i == j) ? 0.0 : -rho * g.y);
+    for (int j = 0; j < K; ++j) {
+      const int oj = xlk::poff(K, j);
+      for (int i = j + lane; i < K; i += 32) {
+        const double2 g = G[j * K + i];
+        As[oj + i - j] = (i == j) ? make_double2(1.0 + rho * g.x, 0.0) : make_double2(rho * g.x, -rho * g.y);
+      }
     }
+    __syncwarp();
     double cap = kNaN;
-    if (xlk::warp_cholesky<RPL>(As, K, lane)) {
+    if (xlk::warp_cholesky_packed<RPL>(As, K, lane)) {
       double part = 0.0;
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
         const int k = lane + 32 * r;
-        if (k < K) part += 2.0 * log2(As[k * K + k].x);
+        if (k < K) part += 2.0 * log2(As[xlk::poff(K, k)].x);
       }
       cap = xlk::warp_sum(part);
     } else {
@@ -740,7 +746,7 @@ int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_
   for (int i = 0; i < n_snr; ++i) P.rho[i] = pow(10.0, snr_db[i] / 10.0);
   int rc = XLMIMO_OK;
   if (K <= xl::kMaxK) {
-    const size_t per_warp = (size_t)K * K * sizeof(double2);
+    const size_t per_warp = (size_t)K * (K + 1) / 2 * sizeof(double2);
     int nw = (int)((96 * 1024) / per_warp);
     nw = nw > 8 ? 8 : (nw < 1 ? 1 : nw);
     const int64_t blocks = (n_drops + nw - 1) / nw;

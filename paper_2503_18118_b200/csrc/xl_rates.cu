@@ -1,9 +1,11 @@
 // xl_rates.cu -- a5: per-drop receivers on a K x K Gram (Eq. (9) PAPER.md:117-122,
 // Eq. (21); SINR definitions, R12).
 //
-// One warp per Gram.  The matrix lives in shared memory column-major
-// (As[col][row]) so lane = row accesses are conflict-free; lanes own rows
-// (Cholesky) and columns of L^{-1} (diag of the inverse).  For every SNR:
+// One warp per Gram.  The factor lives in shared memory as a packed column-major
+// lower triangle (K(K+1)/2 complex, xl_linalg.cuh) so lane = row accesses are
+// conflict-free and up to 3 warps (K = 64) share 100 KB; lanes own rows for the
+// Cholesky and for the in-place inverse X = L^{-1} whose column norms are the
+// diagonal of the inverse.  For every SNR:
 //   I + rho G = L L^H -> CAP = 2 sum log2 L_kk, [(I+rho G)^{-1}]_ii = sum_k |(L^{-1})_ki|^2;
 //   G = L L^H once     -> [G^{-1}]_ii for ZF;  MRC straight from G.
 // A pivot that is not > 0 (or not finite) marks the factorisation failed (R10).
@@ -26,32 +28,16 @@ struct RateParams {
   double rho[xl::kMaxSnr];
 };
 
-// dinv[c] = [A^{-1}]_cc = sum_k |(L^{-1})_kc|^2 for the lane's columns c, with L in
-// As (column-major).  Xs: per-column scratch, Xs[k*K + c].
+// Packed lower triangle per warp (K(K+1)/2 complex): column j of A = conj of row j of G
+// (coalesced reads).  alpha I + rho G.
 template <int RPL>
-__device__ void warp_inv_diag(const double2 *As, double2 *Xs, int K, int lane, double *dinv) {
-#pragma unroll
-  for (int r = 0; r < RPL; ++r) dinv[r] = 0.0;
-  for (int k = 0; k < K; ++k) {
-    const double2 lkk = As[k * K + k];
-#pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const int c = lane + 32 * r;
-      if (c >= K) continue;
-      double2 x = make_double2(0.0, 0.0);
-      if (k >= c) {
-        double xr = (k == c) ? 1.0 : 0.0, xi = 0.0;
-        for (int j = c; j < k; ++j) {
-          const double2 l = As[j * K + k];  // L[k][j]
-          const double2 xj = Xs[j * K + c];
-          xr -= l.x * xj.x - l.y * xj.y;
-          xi -= l.x * xj.y + l.y * xj.x;
-        }
-        x.x = xr / lkk.x;
-        x.y = xi / lkk.x;
-        dinv[r] += x.x * x.x + x.y * x.y;
-      }
-      Xs[k * K + c] = x;
+__device__ __forceinline__ void load_packed(double2 *Ls, const double2 *G, int K, int lane, double alpha,
+                                            double rho) {
+  for (int j = 0; j < K; ++j) {
+    const int oj = xlk::poff(K, j);
+    for (int i = j + lane; i < K; i += 32) {
+      const double2 g = G[j * K + i];
+      Ls[oj + i - j] = (i == j) ? make_double2(alpha + rho * g.x, 0.0) : make_double2(rho * g.x, -rho * g.y);
     }
   }
   __syncwarp();
@@ -62,8 +48,7 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
   extern __shared__ double2 smem[];
   const int K = P.K;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double2 *As = smem + (size_t)warp * 2 * K * K;
-  double2 *Xs = As + K * K;
+  double2 *Ls = smem + (size_t)warp * (K * (K + 1) / 2);
   const int64_t prob = (int64_t)blockIdx.x * nw + warp;
   if (prob >= P.n_prob) return;
   const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)prob * K * K;
@@ -84,14 +69,9 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
   double zf_dinv[RPL];
   bool zf_ok = false;
   if (P.receivers & XLMIMO_RECV_ZF) {
-    // As[col j][row i] = G[i][j] = conj(G[j][i])
-    for (int e = lane; e < K * K; e += 32) {
-      const int j = e / K, i = e - (e / K) * K;
-      const double2 g = G[j * K + i];
-      As[e] = make_double2(g.x, -g.y);
-    }
-    zf_ok = xlk::warp_cholesky<RPL>(As, K, lane);
-    if (zf_ok) warp_inv_diag<RPL>(As, Xs, K, lane, zf_dinv);
+    load_packed<RPL>(Ls, G, K, lane, 0.0, 1.0);
+    zf_ok = xlk::warp_cholesky_packed<RPL>(Ls, K, lane);
+    if (zf_ok) xlk::warp_inv_diag_packed<RPL>(Ls, K, lane, zf_dinv);
     else fl |= XLMIMO_FLAG_G_NOT_PD;
   }
   bool mrc_ok = true;
@@ -107,20 +87,16 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
     double cap_part = 0.0;
     if (P.receivers & (XLMIMO_RECV_CAP | XLMIMO_RECV_MMSE)) {
       __syncwarp();
-      for (int e = lane; e < K * K; e += 32) {
-        const int j = e / K, i = e - (e / K) * K;
-        const double2 g = G[j * K + i];
-        As[e] = make_double2((i == j ? 1.0 : 0.0) + rho * g.x, -rho * g.y);
-      }
-      a_ok = xlk::warp_cholesky<RPL>(As, K, lane);
+      load_packed<RPL>(Ls, G, K, lane, 1.0, rho);
+      a_ok = xlk::warp_cholesky_packed<RPL>(Ls, K, lane);
       if (!a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
       if (a_ok) {
 #pragma unroll
         for (int rr = 0; rr < RPL; ++rr) {
           const int k = lane + 32 * rr;
-          if (k < K) cap_part += 2.0 * log2(As[k * K + k].x);
+          if (k < K) cap_part += 2.0 * log2(Ls[xlk::poff(K, k)].x);
         }
-        if (P.receivers & XLMIMO_RECV_MMSE) warp_inv_diag<RPL>(As, Xs, K, lane, dinv);
+        if (P.receivers & XLMIMO_RECV_MMSE) xlk::warp_inv_diag_packed<RPL>(Ls, K, lane, dinv);
       }
     }
     if (P.receivers & XLMIMO_RECV_CAP) {
@@ -475,8 +451,8 @@ int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr
   P.receivers = receivers;
   P.n_recv = __builtin_popcount(receivers & 15u);
   for (int i = 0; i < xl::kMaxSnr; ++i) P.rho[i] = i < n_snr ? pow(10.0, snr_db[i] / 10.0) : 0.0;
-  const size_t per_warp = 2 * (size_t)K * K * sizeof(double2);
-  int nw = (int)((96 * 1024) / per_warp);
+  const size_t per_warp = (size_t)K * (K + 1) / 2 * sizeof(double2);  // packed factor per warp
+  int nw = (int)((100 * 1024) / per_warp);
   if (nw > 8) nw = 8;
   if (nw < 1) nw = 1;
   const size_t smem = per_warp * nw;

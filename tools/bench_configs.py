@@ -97,7 +97,47 @@ def steady_cfg1(D=10 ** 6):
                       "gram_cmac_per_s": cmac / (t.get("gram_fused_split_fp64", float("nan")) * 1e-3)}), flush=True)
 
 
+def full_size(cfgs=(1, 3, 4, 5)):
+    """Every config at its own full drop count through the whole per-drop path on one GPU:
+    drops -> exact Gram (fused fp64; for cfg3 also fused fp32 and materialised) -> the
+    config's receivers (-> closed form + receivers where the config asks for it), all drops
+    in one batch.  Whole-job device time (CUDA events) and drops/s."""
+    for c in cfgs:
+        w = CONFIGS[c]
+        arr = xl.Array.ula(w.n_y, w.fc_hz) if w.kind == "ula" else xl.Array.upa(w.n_y, w.n_z, w.fc_hz)
+        users = xl.Users.polar(w.r, w.az, w.el)
+        B = w.n_drops  # one batch: every path's workspace fits (cfg3 fused fp32: 1.7 GB)
+        paths = ["fp64"] + (["fp32", "mat32"] if c in (3, 5) else []) + (["closed"] if w.kind == "ula" else [])
+        out = {"cfg": c, "workload": w.name, "drops": w.n_drops, "batch": B}
+        for path in paths:
+            pos = torch.empty((B, w.K, 3), dtype=torch.float64, device="cuda")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for warm in (True, False):  # one untimed batch first (module load, workspace, attributes)
+              torch.cuda.synchronize()
+              e0.record()
+              for d0 in range(0, B if warm else w.n_drops, B):
+                nb = min(B, w.n_drops - d0)
+                p = xl.gen_drops(users, w.K, nb, seed=w.seed, first_drop=d0, out=pos[:nb])
+                if path == "closed":
+                    G, fl = xl.gram_closed_form(arr, p)
+                    xl.sum_rate(G, list(w.snr_db), w.receivers, flags=fl)
+                else:
+                    G = xl.gram_exact(arr, p, precision=xl.FP64 if path == "fp64" else xl.FP32,
+                                      mode=xl.MATERIALIZED if path == "mat32" else xl.FUSED)
+                    xl.sum_rate(G, list(w.snr_db), w.receivers)
+              e1.record()
+              torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            cmac = w.n_drops * w.N * w.K * (w.K + 1) // 2
+            out[path] = {"ms": ms, "drops_per_s": w.n_drops / (ms * 1e-3),
+                         "gram_cmac_per_s": None if path == "closed" else cmac / (ms * 1e-3)}
+        print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["full"]:
+        full_size()
+        sys.exit(0)
     args = sys.argv[1:]
     if "1s" in args:
         steady_cfg1()
