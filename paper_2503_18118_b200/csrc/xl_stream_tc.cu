@@ -323,15 +323,20 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(
 constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
 
 // One generator task: the TF32 (RNA) coefficients h = a e^{-j 2 pi r / lambda} (Eq. 3) of
-// one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7, from an fp64
-// anchor at t0 (distance, 1/r, phase reduced as frac(r / lambda) in fp64) and fp32
-// deltas along y: Delta(r^2) = dd (2 dy + dd), delta = Delta / r_c^2,
-// Delta r = r_c delta (1/2 - delta/8 + delta^2/16), phase re-reduced in fp32, MUFU
-// sin/cos, amplitude a_c (1 - 3/4 delta + 21/32 delta^2).  Elements past N are 0.
+// one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7 (offset d = m pitch
+// along y), from an fp64 anchor at t0: distance r_c, phase reduced as frac(r_c / lambda)
+// in fp64, and the Taylor coefficients of r(d) = sqrt(r_c^2 + 2 dy d + d^2) about d = 0,
+//   r = r_c + u d + (w/2) d^2 - (u w / (2 r_c)) d^3,  u = dy / r_c,  w = (1 - u^2) / r_c,
+// turned into a cubic in m for the phase (cycles) and a quadratic for the amplitude
+// a_c (r / r_c)^{-3/2}; per element only fp32 FMAs, the FMA-pipe rint, MUFU sin/cos and
+// integer RNA rounding remain.  Truncation over 7 pitches at r >= 2 m, 100 GHz: phase
+// ~5e-7 cycles, amplitude ~2e-7 relative (fp32 tier tolerance 1e-4).  Elements past N are 0.
 // uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
 __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
                                               int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
                                               float pitch_f, uint32_t (&vr)[kTaskE], uint32_t (&vi)[kTaskE]) {
+  (void)inv_lambda_f;
+  (void)pitch_f;
   double ey, ez = 0.0;
   if (kind == XLMIMO_ULA) {
     ey = ((double)t0 - 0.5 * (double)(N - 1)) * pitch;
@@ -346,22 +351,28 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
   const double rc = r2 * ir;
   const double qc = rc * inv_lambda;
   const float fc = (float)(qc - rint(qc));
-  const float irc2 = (float)(ir * ir), rcf = (float)rc, tdy = (float)(2.0 * dy);
-  const float ac = (float)(uc.w * ir) * rsqrtf(rcf);
+  const double u = dy * ir, w = fma(-u, u, 1.0) * ir;
+  const double pl = pitch * inv_lambda, p1 = pitch * ir;   // pitch / lambda, pitch / r_c
+  const float ca = (float)(u * pl);                          // cycles per element, linear
+  const float cb = (float)(0.5 * w * pitch * pl);            // quadratic
+  const float cg = (float)(-0.5 * u * w * p1 * pitch * pl);  // cubic
+  const double ac = uc.w * ir * xl::rsqrt_nr(rc);            // a_c = amp r_c^{-3/2}
+  // (r / r_c)^{-3/2} = 1 - 3/2 D + 15/8 D^2, D = (r - r_c) / r_c = u p1 m + (w/2) p1 pitch m^2
+  const float a0 = (float)ac;
+  const float a1 = (float)(ac * (-1.5 * u * p1));
+  const float a2 = (float)(ac * (-0.75 * w * p1 * pitch + 1.875 * u * u * p1 * p1));
   const int64_t nv64 = N - t0;  // valid elements of this task (padding past N is 0)
   const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
 #pragma unroll
   for (int m = 0; m < kTaskE; ++m) {
-    const float dd = (float)m * pitch_f;
-    const float dl = dd * (tdy + dd) * irc2;                  // delta = Delta(r^2) / r_c^2
-    const float dr = rcf * dl * fmaf(dl, fmaf(dl, 0.0625f, -0.125f), 0.5f);
-    float cyc = fmaf(dr, inv_lambda_f, fc);
+    const float fm = (float)m;
+    float cyc = fmaf(fmaf(fmaf(cg, fm, cb), fm, ca), fm, fc);
     // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
     // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
     cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);
     float sn, co;
     __sincosf(6.28318530717958647692f * cyc, &sn, &co);
-    const float a = (m < nv) ? ac * fmaf(dl, fmaf(dl, 0.65625f, -0.75f), 1.0f) : 0.0f;
+    const float a = (m < nv) ? fmaf(fmaf(a2, fm, a1), fm, a0) : 0.0f;
     vr[m] = tf32_rna(a * co);
     vi[m] = tf32_rna(-a * sn);
   }
