@@ -142,11 +142,11 @@ XLMIMO_API int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, c
 
 /* The same receivers with a caller workspace, for K up to 1024.  For K > 64 the
  * Cholesky factors of I + rho G (CAP, MMSE) and of G (ZF) are formed one CTA per
- * matrix -- resident in shared memory for K <= 160, with the diagonal of the
- * inverse by forward substitution for ZF/MMSE; tiled (32 x 32 complex) in the
- * workspace for K > 160 -- and MRC comes straight from G.  ZF/MMSE need K <= 160
- * (EUNSUPPORTED above; CAP and MRC run to K = 1024).  The workspace query returns 0
- * when none is needed (K <= 64); ws may then be NULL.
+ * matrix -- resident in shared memory for K <= 160, tiled (32 x 32 complex) in the
+ * workspace above -- and the ZF/MMSE diagonals of the inverse follow from X = L^{-1}
+ * (in place for K <= 160; blocked forward substitution, diagonal-tile inverses and
+ * per-warp column panels in the workspace above); MRC comes straight from G.  The
+ * workspace query returns 0 when none is needed (K <= 64); ws may then be NULL.
  * EWORKSPACE: ws_bytes below the query. */
 XLMIMO_API size_t xlmimo_sum_rate_workspace(int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers);
 XLMIMO_API int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const double *snr_db,
@@ -188,8 +188,8 @@ XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drop
  *            PAPER.md:228) and M_sat = ceil((E[y_up]-E[y_down]) / pitch) (R15),
  *   per_drop (dev [n_drops][n_n][n_snr][n_recv] or NULL).
  * array->n_y is ignored (the grid is n_list).  Synchronises `stream` before return.
- * K <= 1024; for K > 64 the exact Gram is fp64, and ZF/MMSE need K <= 160
- * (EUNSUPPORTED otherwise) -- the paper's K = 100 curves.
+ * K <= 1024; for K > 64 the exact Gram is fp64 (EUNSUPPORTED otherwise) -- the
+ * paper's K = 100 curves.
  * EINVAL also for n_list not ascending / mixed parity, t not in (0,1). */
 XLMIMO_API size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                                          int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers,

@@ -120,8 +120,6 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
   }
   if (K < 1 || K > xl::kMaxKLarge)
     return xlh::set_error(K < 1 ? XLMIMO_EINVAL : XLMIMO_EUNSUPPORTED, "sweep: K=%d", K);
-  if (K > xl::kMaxKInv && (receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)))
-    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: ZF/MMSE need K <= %d (K=%d)", xl::kMaxKInv, K);
   if (K > xl::kMaxK && gram_kind == XLMIMO_GRAM_EXACT && precision != XLMIMO_FP64)
     return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: K=%d > %d is fp64 only", K, xl::kMaxK);
   if (n_drops < 1) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_drops < 1");
@@ -341,8 +339,6 @@ int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops, const dou
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: receivers");
   if (n_drops > 0 && (!gram || !rates)) return xlh::set_error(XLMIMO_EINVAL, "sum_rate: null pointer");
   if (K > xl::kMaxK) {
-    if ((receivers & (XLMIMO_RECV_ZF | XLMIMO_RECV_MMSE)) && K > xl::kMaxKInv)
-      return xlh::set_error(XLMIMO_EUNSUPPORTED, "sum_rate: ZF/MMSE need K <= %d (K=%d)", xl::kMaxKInv, K);
     return xlh::launch_sum_rate_large(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, ws, ws_bytes,
                                       (cudaStream_t)stream);
   }

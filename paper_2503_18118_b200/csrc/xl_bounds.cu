@@ -143,6 +143,8 @@ struct CholParams {
   double2 *ws;       // tiled kernel: [n_slots][Kp][Kp]
   double *log2det;   // [n_prob]
   double *dinv;      // [n_prob][K] or null
+  double2 *xscr;     // tiled + dinv: per slot [8 warps][Kp][32] column panels of L^{-1}
+  double2 *dvs;      // tiled + dinv: per slot [nt][32][32] inverses of the diagonal tiles
   int K, Kp, nt;
   int64_t n_prob;
   int n_mat;         // matrices per drop
@@ -174,7 +176,7 @@ __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, in
 // With dinv requested, [A^{-1}]_ii = ||L^{-1} e_i||^2 follows: warp per i, forward
 // substitution L x = e_i with x_m held by lane m % 32 (register slot m / 32), the
 // pivot element broadcast by shuffle, the column of L read from shared memory.
-constexpr int kSmemK = xl::kMaxKInv;
+constexpr int kSmemK = 160;
 constexpr int kSmemRpl = (kSmemK + 31) / 32;
 
 __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
@@ -328,6 +330,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           T[c * kTile + lane] = (lane >= c) ? v : make_double2(0.0, 0.0);
         }
         const bool okf = xlk::warp_cholesky<1>(T, kTile, lane);
+        if (okf && P.dinv)  // the inverse phase reads L_kk back from the slot
+          for (int c = 0; c <= lane; ++c) A[(size_t)(k0 + lane) * Kp + k0 + c] = T[c * kTile + lane];
         const double part = okf ? 2.0 * log2(T[lane * kTile + lane].x) : 0.0;
         const double sum = xlk::warp_sum(part);
         if (lane == 0) {
@@ -405,6 +409,138 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
       }
     }
     if (tid == 0) P.log2det[prob] = s_ok ? s_ld : kNaN;
+    if (P.dinv) {
+      // ---- [A^{-1}]_cc = sum_i |X_ic|^2, X = L^{-1}, by blocked forward substitution:
+      // (a) Dinv_i = L_ii^{-1} for every diagonal tile (warp per tile, lane = column);
+      // (b) warp per column block j: X_jj = Dinv_j, X_ij = -Dinv_i sum_{k=j}^{i-1} L_ik X_kj,
+      //     the panel X_{.j} kept in the warp's global scratch, column norms accumulated.
+      double *dout = P.dinv + (size_t)prob * K;
+      const bool fact = s_ok != 0;
+      double2 *Dv = P.dvs + (size_t)blockIdx.x * nt * kTile * kTile;
+      for (int i = warp; i < nt && fact; i += NW) {
+        const int i0 = i * kTile;
+        for (int r = 0; r < kTile; ++r)
+          W[r * kLd + lane] = (lane <= r) ? A[(size_t)(i0 + r) * Kp + i0 + lane] : make_double2(0.0, 0.0);
+        __syncwarp();
+        asm volatile("" ::: "memory");
+        double2 x[kTile];
+#pragma unroll
+        for (int k = 0; k < kTile; ++k) {
+          double xr = (k == lane) ? 1.0 : 0.0, xi = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < k; ++mm) {
+            const double2 l = W[k * kLd + mm];  // L_k,mm
+            xr -= l.x * x[mm].x - l.y * x[mm].y;
+            xi -= l.x * x[mm].y + l.y * x[mm].x;
+          }
+          const double inv = 1.0 / W[k * kLd + k].x;
+          x[k] = make_double2(xr * inv, xi * inv);
+        }
+#pragma unroll
+        for (int k = 0; k < kTile; ++k) Dv[((size_t)i * kTile + k) * kTile + lane] = x[k];  // row k, col lane
+        __syncwarp();
+      }
+      __syncthreads();
+      double2 *Xp = P.xscr + ((size_t)blockIdx.x * NW + warp) * Kp * kTile;  // [row - j0][32]
+      for (int j = warp; j < nt; j += NW) {
+        const int j0 = j * kTile;
+        if (!fact) {
+          if (j0 + lane < K) dout[j0 + lane] = kNaN;
+          continue;
+        }
+        // X_jj = Dinv_j; lane c: column c norm
+        double nrm = 0.0;
+        for (int r = 0; r < kTile; ++r) {
+          const double2 v = Dv[((size_t)j * kTile + r) * kTile + lane];
+          Xp[(size_t)r * kTile + lane] = v;
+          nrm += v.x * v.x + v.y * v.y;
+        }
+        double part[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) part[b] = 0.0;
+        __syncwarp();
+        for (int i = j + 1; i < nt; ++i) {
+          const int i0 = i * kTile;
+          double2 acc[4][8];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
+          for (int k = j; k < i; ++k) {  // Y += L_ik X_kj
+            const double2 *lrow = A + (size_t)i0 * Kp + (size_t)k * kTile;
+            const double2 *xk = Xp + (size_t)(k - j) * kTile * kTile;
+#pragma unroll 1
+            for (int mm = 0; mm < kTile; ++mm) {
+              double2 wa[4], sb[8];
+#pragma unroll
+              for (int a = 0; a < 4; ++a) wa[a] = lrow[(size_t)(lr + 8 * a) * Kp + mm];
+#pragma unroll
+              for (int b = 0; b < 8; ++b) sb[b] = xk[mm * kTile + lc + 4 * b];
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                  acc[a][b].x += wa[a].x * sb[b].x - wa[a].y * sb[b].y;
+                  acc[a][b].y += wa[a].x * sb[b].y + wa[a].y * sb[b].x;
+                }
+            }
+          }
+          // Y -> shared (W), then X_ij = -Dinv_i Y
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) W[(lr + 8 * a) * kLd + lc + 4 * b] = acc[a][b];
+          __syncwarp();
+          const double2 *dvi = Dv + (size_t)i * kTile * kTile;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
+#pragma unroll 1
+          for (int mm = 0; mm < kTile; ++mm) {
+            double2 wa[4], sb[8];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) wa[a] = dvi[(lr + 8 * a) * kTile + mm];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) sb[b] = W[mm * kLd + lc + 4 * b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 8; ++b) {
+                acc[a][b].x -= wa[a].x * sb[b].x - wa[a].y * sb[b].y;
+                acc[a][b].y -= wa[a].x * sb[b].y + wa[a].y * sb[b].x;
+              }
+          }
+          double2 *xo = Xp + (size_t)(i - j) * kTile * kTile;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              xo[(lr + 8 * a) * kTile + lc + 4 * b] = acc[a][b];
+              part[b] += acc[a][b].x * acc[a][b].x + acc[a][b].y * acc[a][b].y;
+            }
+          __syncwarp();
+        }
+        // column c = lc + 4 b: add the 8 row groups (lanes lr * 4 + lc), then the X_jj part
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          double v = part[b];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          part[b] = v;
+        }
+        // lane c gathers column c's sum from lane lc = c % 4 (any lr), slot b = c / 4
+        double tot = 0.0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const double v = __shfl_sync(0xffffffffu, part[b], lane & 3);
+          if ((lane >> 2) == b) tot = v;
+        }
+        if (j0 + lane < K) dout[j0 + lane] = nrm + tot;
+        __syncwarp();
+      }
+    }
     __syncthreads();
   }
 }
@@ -673,6 +809,17 @@ int n_chol_slots(int64_t n_prob) {
   return (int)(n_prob < sms ? n_prob : sms);
 }
 
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t chol_slot_bytes(int K, int64_t n_prob, bool with_dinv) {
+  if (K <= kSmemK) return 0;
+  const int Kp = (K + kTile - 1) / kTile * kTile;
+  const size_t slots = (size_t)n_chol_slots(n_prob);
+  size_t b = align256(slots * Kp * Kp * sizeof(double2));
+  if (with_dinv) b += align256(slots * ((kCtaThreads / 32) * (size_t)Kp * kTile + (size_t)Kp * kTile) * sizeof(double2));
+  return b;
+}
+
 int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool first_is_r, const double *rho,
                 const double *alpha, double *log2det, double *dinv, void *ws, size_t ws_bytes, cudaStream_t s) {
   CholParams C;
@@ -691,7 +838,6 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
   C.log2det = log2det;
   C.dinv = dinv;
   C.ws = (double2 *)ws;
-  if (dinv && K > kSmemK) return xlh::set_error(XLMIMO_EUNSUPPORTED, "inverse diagonal needs K <= %d", kSmemK);
   xlh::KTimer tm(s, "chol_logdet");
   if (K <= kSmemK) {
     const size_t smem = (size_t)K * (K + 1) / 2 * sizeof(double2);
@@ -701,8 +847,12 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
     chol_smem_kernel<<<(unsigned)(grid < C.n_prob ? grid : C.n_prob), kCtaThreads, smem, s>>>(C);
   } else {
     const int slots = n_chol_slots(C.n_prob);
-    if ((size_t)slots * C.Kp * C.Kp * sizeof(double2) > ws_bytes)
+    if (chol_slot_bytes(K, C.n_prob, dinv != nullptr) > ws_bytes)
       return xlh::set_error(XLMIMO_EWORKSPACE, "large-K Cholesky: workspace too small");
+    if (dinv) {  // slot matrices, then the L^{-1} panels, then the diagonal-tile inverses
+      C.xscr = (double2 *)((char *)ws + align256((size_t)slots * C.Kp * C.Kp * sizeof(double2)));
+      C.dvs = C.xscr + (size_t)slots * (kCtaThreads / 32) * C.Kp * kTile;
+    }
     cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmem);
     chol_tiled_kernel<<<slots, kCtaThreads, kTiledSmem, s>>>(C);
   }
@@ -711,13 +861,6 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
   return xlh::check_launch("chol_logdet kernel");
 }
 
-size_t align256(size_t x) { return (x + 255) / 256 * 256; }
-
-size_t chol_slot_bytes(int K, int64_t n_prob) {
-  if (K <= kSmemK) return 0;
-  const int Kp = (K + kTile - 1) / kTile * kTile;
-  return align256((size_t)n_chol_slots(n_prob) * Kp * Kp * sizeof(double2));
-}
 
 }  // namespace
 
@@ -727,7 +870,7 @@ namespace xlh {
 size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat, bool with_dinv) {
   if (K <= xl::kMaxK || n_drops == 0 || n_mat == 0) return 0;
   const size_t n_prob = (size_t)n_drops * n_mat;
-  return chol_slot_bytes(K, (int64_t)n_prob) + align256(n_prob * sizeof(double)) +
+  return chol_slot_bytes(K, (int64_t)n_prob, with_dinv) + align256(n_prob * sizeof(double)) +
          (with_dinv ? align256(n_prob * K * sizeof(double)) : 0);
 }
 
@@ -764,7 +907,7 @@ int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_
   } else {
     const int n_mat = 1 + n_snr;
     const int64_t n_prob = n_drops * n_mat;
-    const size_t chol_b = chol_slot_bytes(K, n_prob);
+    const size_t chol_b = chol_slot_bytes(K, n_prob, false);
     if (ws_bytes < large_k_ws_bytes(K, n_drops, n_mat, false) || !ws)
       return set_error(XLMIMO_EWORKSPACE, "app_a_bounds: workspace %zu < %zu", ws_bytes,
                        large_k_ws_bytes(K, n_drops, n_mat, false));
@@ -828,7 +971,7 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
     const int64_t n_prob = n_drops * P.n_mat;
     const size_t need = sum_rate_large_ws_bytes(K, n_drops, n_snr, receivers);
     if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "sum_rate (K > 64): workspace %zu < %zu", ws_bytes, need);
-    const size_t chol_b = chol_slot_bytes(K, n_prob);
+    const size_t chol_b = chol_slot_bytes(K, n_prob, need_dinv);
     log2det = (double *)((char *)ws + chol_b);
     if (need_dinv) dinv = (double *)((char *)ws + chol_b + align256((size_t)n_prob * sizeof(double)));
     double rho[xl::kMaxSnr + 2], alpha[xl::kMaxSnr + 2];

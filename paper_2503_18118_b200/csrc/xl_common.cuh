@@ -14,7 +14,6 @@ namespace xl {
 constexpr double kC = 299792458.0;  // m/s, exact (R2)
 constexpr int kMaxK = 64;           // fused paths: K <= 64
 constexpr int kMaxKLarge = 1024;    // large-K paths (tiled Cholesky, block-pair Gram)
-constexpr int kMaxKInv = 160;       // ZF/MMSE (diagonal of an inverse) beyond K = 64: shared-memory Cholesky
 constexpr int kMaxSnr = 16;
 
 // ---------------------------------------------------------------------------

@@ -86,7 +86,8 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
                                  None) == -3
     assert L.xlmimo_app_a_bounds(rs, 8, 1, None, 1, rs, rs, None, None, None, 0, None) == -1
     assert L.xlmimo_app_a_bounds_workspace(8, 100, 1) == 0 < L.xlmimo_app_a_bounds_workspace(100, 100, 1)
-    assert L.xlmimo_sum_rate(rs, 161, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # ZF, K>160
+    assert L.xlmimo_sum_rate(rs, 1025, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # K>1024
+    assert L.xlmimo_sum_rate(rs, 333, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -3  # ZF: ws
     assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -3  # ZF: ws
     assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 1, rs, None, None) == -3  # CAP: ws
     assert L.xlmimo_sum_rate_workspace(100, 4, 1, 8) == 0 < L.xlmimo_sum_rate_workspace(100, 4, 1, 1)

@@ -57,6 +57,9 @@ def main():
                           "app_a_ms": t, "chol_cmac_per_s": cmac / (chol * 1e-3),
                           "chol_frac_fp64_nominal": 4 * cmac / (chol * 1e-3) / PEAK_FP64,
                           "gap_mean": float(xl.app_a_bounds(G, snr)[0][:, 1].mean())}), flush=True)
+        allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+        tr = timed(lambda: xl.sum_rate(G, snr, allr), reps=1)
+        print(json.dumps({"K": K, "drops": D, "sum_rate_all_receivers_ms": tr}), flush=True)
 
 
 if __name__ == "__main__":
