@@ -102,10 +102,11 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  *     written to the workspace as planar complex64 and streamed back (fp32 only).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
  * Im G(i,i) = 0.  K <= 1024: K <= 64 on every precision/mode; 64 < K <= 1024 fused
- * fp64 only (block pairs of 64 users on DMMA; NEXT-3/E1-E3 user counts, PAPER.md:228,
- * 331-335).  ws may be NULL iff the query returns 0.
- * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 not fused fp64, or
- * FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
+ * only, in blocks of 64 users (fp64 on DMMA; fp32 on tcgen05, a UPA needing rows that
+ * are a multiple of 8) -- NEXT-3/E1-E3 user counts.  ws may be
+ * NULL iff the query returns 0.
+ * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 materialised (or fp32 on
+ * an unsupported UPA), or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
 XLMIMO_API size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops,
                                    int32_t precision, int32_t mode);
 XLMIMO_API int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,

@@ -286,9 +286,13 @@ bool stream_tc_supported(int K, int64_t N);
 int stream_tc_chunks(int64_t N);
 int stream_tc_parts(int K);
 bool fused_tc_supported(const ArrayP &a, int K);
+bool fused_tc_supported_geometry(const ArrayP &a);
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
                     cudaStream_t s);
 int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s);
+int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                         cudaStream_t s);
+int fused_tc_pair_chunks(int64_t N);
 bool materialise_tc_supported(const ArrayP &a);
 int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
                             int nb, float *H, cudaStream_t s);

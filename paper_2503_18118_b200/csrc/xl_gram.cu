@@ -1563,6 +1563,8 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
+  if (K > xl::kMaxK && precision == XLMIMO_FP32)  // fused tcgen05 block pairs: one partial per chunk
+    return (size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double);
   if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
@@ -1699,9 +1701,32 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s) {
   if (K > xl::kMaxK) {
-    if (mode != XLMIMO_FUSED || precision != XLMIMO_FP64)
-      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d is fused fp64 only", K, xl::kMaxK);
+    if (mode != XLMIMO_FUSED)
+      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d is fused only", K, xl::kMaxK);
     if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
+    if (precision == XLMIMO_FP32) {
+      if (n_lvl != 1 || !fused_tc_supported_geometry(a))
+        return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d fp32 needs one level and a ULA or a UPA with "
+                                              "rows a multiple of 8", K);
+      if (n_drops == 0) return XLMIMO_OK;
+      const int64_t N = lvl_end[0];
+      const size_t need = gram_ws_bytes(a, K, n_drops, 1, precision, mode);
+      if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+      int rc;
+      {
+        KTimer tm(s, "gram_fused_tc_pair_tf32");
+        rc = launch_fused_tc_pair(a, pos, K, n_drops, N, (double *)ws, s);
+        tm.stop(s);
+        count_launch();
+      }
+      if (rc) return rc;
+      KTimer tr(s, "gram_reduce");
+      gram_reduce_rows_kernel<<<(unsigned)(n_drops * K), 256, 0, s>>>((const double *)ws, K,
+                                                                      fused_tc_pair_chunks(N), 1, out);
+      tr.stop(s);
+      count_launch();
+      return check_launch("gram_reduce_rows_kernel");
+    }
     if (n_drops == 0) return XLMIMO_OK;
     return launch_gram_blk(a, pos, K, n_drops, lvl_end, n_lvl, out, ws, ws_bytes, s);
   }

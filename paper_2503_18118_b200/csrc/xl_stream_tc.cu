@@ -572,6 +572,229 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   }
 }
 
+// ------------------------------------------------------------------ K > 64, fp32
+// Fused fp32 Gram for 64 < K <= 1024 on tcgen05: the block-pair decomposition of the
+// fp64 BLK kernel with the machinery above.  A work item is (drop, user-block pair
+// bi <= bj, 8192-element chunk); a stage holds the A tile (block bi: 64 users x re/im =
+// 128 rows x 32 elements) and, for bi < bj, the B tile (block bj) behind it in the same
+// 32 KB slot; the MMA computes A B^T (M = N = 128, K = 8, four per stage) into a
+// double-buffered TMEM accumulator, the epilogue writes the block's entries of the
+// packed upper triangle of the (drop, chunk) partial (the fp64 combine over chunks is
+// gram_reduce_rows_kernel).  Six 32 KB slots; su holds the pair's 128 users per group.
+constexpr int kPSlots = 6;
+constexpr int kPGroups = kPSlots;  // a group may not lap a slot: groups <= slots (parity waits)
+constexpr int kPSlotBytes = 2 * kStageBytes;
+constexpr int kPUsers = 64;
+// Elements accumulated in fp32 TMEM per partial: the tensor core's fp32 accumulation
+// drifts by ~6e-8 per MMA (1024 per 8192 elements: 1.1e-4 normalised at K = 1000,
+// M = 35 000, over the fp32-tier tolerance), so the pair kernel closes a partial every
+// 4096 elements (half the drift) and combines partials in fp64.
+constexpr int kPChunk = 4096;
+
+struct FusedPairParams {
+  const double *pos;
+  double *ws;        // partials [drop][chunk][NP][2], NP = K(K+1)/2 over all K users
+  int K, kind, nb, n_pairs;
+  int64_t n_y, n_z, N;
+  double lambda, pitch, sqrt_beta0;
+  int n_chunks;
+  int64_t n_drops;
+};
+
+__device__ __forceinline__ void pair_of(int pair, int nb, int &bi, int &bj) {
+  bi = 0;
+  while (pair >= nb - bi) { pair -= nb - bi; ++bi; }
+  bj = bi + pair;
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(FusedPairParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *stages = base;
+  uint64_t *full = (uint64_t *)(base + kPSlots * kPSlotBytes);
+  uint64_t *empty = full + kPSlots;
+  uint64_t *tfull = empty + kPSlots;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
+  double4 *su_all = (double4 *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][128]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = P.K;
+  const int64_t per_drop = (int64_t)P.n_pairs * P.n_chunks;
+  const int64_t n_items = P.n_drops * per_drop;
+  for (int i = tid; i < kPSlots * kPSlotBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (int s = 0; s < kPSlots; ++s) {
+      mbar_init(&full[s], kGenWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_sh;
+  constexpr int kSpb = kBoxK;  // elements per stage
+
+  if (warp < kPGroups * kGenWarps) {  // ---------------- generators: group g makes stages k = g (mod 6)
+    // (warps 12..15 idle: with 6 slots of 32 KB, more groups could lap a slot and pass a
+    // parity wait one phase early)
+    const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
+    double4 *su = su_all + grp * (2 * kPUsers);
+    const double inv_lambda = 1.0 / P.lambda;
+    const float inv_lambda_f = (float)inv_lambda;
+    const float pitch_f = (float)P.pitch;
+    const uint32_t stages_base = smem_u32(stages);
+    int64_t kstart = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t d = it / per_drop;
+      const int rem2 = (int)(it - d * per_drop);
+      const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
+      int bi, bj;
+      pair_of(pair, P.nb, bi, bj);
+      const bool diag = bi == bj;
+      const int64_t x0 = (int64_t)c * kPChunk;
+      const int64_t rem = P.N - x0;
+      const int ns = (int)(((rem < kPChunk ? rem : kPChunk) + kSpb - 1) / kSpb);
+      int64_t k = kstart + (((int64_t)grp - kstart) % kPGroups + kPGroups) % kPGroups;
+      kstart += ns;
+      if (k >= kstart) continue;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
+      for (int u = gtid; u < 2 * kPUsers; u += kGenThreads) {
+        const int gu = (u < kPUsers ? bi : bj) * kPUsers + (u & (kPUsers - 1));
+        if (gu < K) {
+          const xl::UserC uc = xl::make_user(P.pos + (d * K + gu) * 3, P.kind, P.sqrt_beta0);
+          su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+        } else {
+          su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: amplitude 0
+        }
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
+      const int n_tasks = (diag ? kPUsers : 2 * kPUsers) * (kBoxK / kTaskE);
+      for (; k < kstart; k += kPGroups) {
+        const int64_t xs = x0 + (k - (kstart - ns)) * kSpb;
+        const int slot = (int)(k % kPSlots);
+        const uint32_t slot_base = stages_base + slot * kPSlotBytes;
+        mbar_wait(&empty[slot], ((uint32_t)(k / kPSlots) & 1) ^ 1);
+        for (int task = gtid; task < n_tasks; task += kGenThreads) {
+          const int u = task >> 2, g8 = task & 3;  // u < 64: A tile (rows 2u), else B tile (rows 128 + ...)
+          const int row0 = 2 * u;
+          const int64_t t0 = xs + kTaskE * g8;
+          uint32_t vr[kTaskE], vi[kTaskE];
+          gen_task_tf32(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
+#pragma unroll
+          for (int h = 0; h < kTaskE / 4; ++h) {
+            const int chunk = (kTaskE / 4) * g8 + h;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0, chunk)),
+                         "r"(vr[4 * h]), "r"(vr[4 * h + 1]), "r"(vr[4 * h + 2]), "r"(vr[4 * h + 3])
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0 + 1, chunk)),
+                         "r"(vi[4 * h]), "r"(vi[4 * h + 1]), "r"(vi[4 * h + 2]), "r"(vi[4 * h + 3])
+                         : "memory");
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[slot]);
+      }
+    }
+  } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = tf32_idesc(kRows, kRows);
+      // (the original kernel's 12 slots over 8 groups satisfy the same groups <= slots rule)
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+        const int64_t d = it / per_drop;
+        const int rem2 = (int)(it - d * per_drop);
+        const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
+        int bi, bj;
+        pair_of(pair, P.nb, bi, bj);
+        const bool diag = bi == bj;
+        const int64_t x0 = (int64_t)c * kPChunk;
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * kRows);
+        for (int kb = 0; kb < kPChunk / kSpb; ++kb) {
+          if (x0 + (int64_t)kb * kSpb >= P.N) break;
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stages + stage * kPSlotBytes);
+          const uint32_t sb = diag ? sa : sa + kStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBoxK / 8; ++kk)
+            mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+          if (++stage == kPSlots) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= kEpiWarp0) {  // ---------------- epilogue, warps kEpiWarp0..+3 = TMEM lane quadrants
+    const int q = warp - kEpiWarp0;
+    const int row = 32 * q + lane;
+    const int il = row >> 1, plane = row & 1;
+    const int64_t NP = (int64_t)K * (K + 1) / 2;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      const int64_t d = it / per_drop;
+      const int rem2 = (int)(it - d * per_drop);
+      const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
+      int bi, bj;
+      pair_of(pair, P.nb, bi, bj);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double *out = P.ws + ((size_t)d * P.n_chunks + c) * (size_t)(2 * NP);
+      const int i = bi * kPUsers + il;
+      for (int cb = 0; cb < kRows / 32; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kRows + 32 * cb), v);
+        float x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int jj = plane * 8 + h;
+          const int jl = 16 * cb + jj;
+          const int j = bj * kPUsers + jl;
+          float rr, rr2, ri, ir;
+          if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
+          else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
+          if (i < K && j < K && j >= i) {
+            const int64_t pp = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
+            out[2 * pp] = (double)rr + (double)rr2;
+            out[2 * pp + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+  }
+}
+
 // K4a for the tcgen05 stream: H of a batch of drops written straight into the tiled32
 // TF32 layout [drop - drop0][N_pad / 32][2K][32] (row 2k = Re h_k, 2k + 1 = Im h_k) with
 // the task generator above: a warp covers one 32-element tile for 8 users, lane =
@@ -624,9 +847,8 @@ int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
 // UPA: a generator task (kTaskE consecutive elements off one fp64 anchor, the delta
 // along y) must not cross a row of the n_y x n_z grid, so n_y must be a multiple of
 // kTaskE; other UPAs take the CUDA-core fp32 kernel.
-bool fused_tc_supported(const ArrayP &a, int K) {
-  return K >= 9 && K <= 64 && (a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0);
-}
+bool fused_tc_supported_geometry(const ArrayP &a) { return a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0; }
+bool fused_tc_supported(const ArrayP &a, int K) { return K >= 9 && K <= 64 && fused_tc_supported_geometry(a); }
 
 // Fused fp32 Gram on tcgen05: partials [drop][chunk][NP][2] into ws (stream_tc_chunks(N) per drop).
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
@@ -675,6 +897,38 @@ int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N
   h_materialise_tc_kernel<<<grid, 256, 0, s>>>(pos, K, a.kind, N, n_pad, a.n_y, a.kind == XLMIMO_ULA ? 1 : a.n_z,
                                                a.pitch, a.lambda, a.sqrt_beta0, drop0, n_ugrp, H);
   return check_launch("h_materialise_tc_kernel");
+}
+
+int fused_tc_pair_chunks(int64_t N) { return (int)((N + kPChunk - 1) / kPChunk); }
+
+// K > 64 fused fp32: partials [drop][chunk][K(K+1)/2][2] into ws (fused_tc_pair_chunks(N) per drop).
+int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                         cudaStream_t s) {
+  FusedPairParams P;
+  P.pos = pos;
+  P.ws = ws;
+  P.K = K;
+  P.kind = a.kind;
+  P.nb = (K + kPUsers - 1) / kPUsers;
+  P.n_pairs = P.nb * (P.nb + 1) / 2;
+  P.n_y = a.n_y;
+  P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+  P.N = N;
+  P.lambda = a.lambda;
+  P.pitch = a.pitch;
+  P.sqrt_beta0 = a.sqrt_beta0;
+  P.n_chunks = fused_tc_pair_chunks(N);
+  P.n_drops = n_drops;
+  const size_t smem = 1024 + (size_t)kPSlots * kPSlotBytes + (2 * kPSlots + 4) * 8 + 16 + 64 +
+                      (size_t)kPGroups * 2 * kPUsers * 32;
+  cudaFuncSetAttribute(gram_fused_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = n_drops * P.n_pairs * P.n_chunks;
+  const int grid = (int)(items < sms ? items : sms);
+  gram_fused_tc_pair_kernel<<<grid, kFusedThreads, smem, s>>>(P);
+  return check_launch("gram_fused_tc_pair_kernel");
 }
 
 int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, double *ws, cudaStream_t s) {

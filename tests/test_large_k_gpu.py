@@ -63,11 +63,44 @@ def test_gram_large_k_unsupported_modes(xl):
     a = xl.Array.ula(256, 100e9)
     pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 70, 1, seed=1)
     with pytest.raises(xl.XlmimoError):
-        xl.gram_exact(a, pos, precision=xl.FP32)
-    with pytest.raises(xl.XlmimoError):
         xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED)
+    upa = xl.Array.upa(20, 10, 100e9)  # rows not a multiple of the 8-element generator task
+    with pytest.raises(xl.XlmimoError):
+        xl.gram_exact(upa, pos, precision=xl.FP32)
     e = torch.zeros((0, 70, 3), dtype=torch.float64, device="cuda")
     assert xl.gram_exact(a, e).shape == (0, 70, 70)
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 4099, 1, 65, 3), ("ula", 20000, 1, 100, 2),
+                                              ("ula", 3000, 1, 129, 2), ("ula", 777, 1, 200, 1),
+                                              ("upa", 24, 40, 80, 2)])
+def test_gram_large_k_fp32_parity(xl, orc, kind, n_y, n_z, K, D):
+    """fp32 tier (1e-4 normalised) for K > 64: block pairs of 64 users on tcgen05 (TF32,
+    RNA-rounded generated operands, fp32 TMEM accumulation per 8192-element chunk, fp64
+    across chunks); ragged users and elements, a chunk boundary (N = 20000), UPA."""
+    fc = 100e9
+    if kind == "ula":
+        a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=K)
+    else:
+        a, ao = xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, D, seed=K)
+    G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+    Go = orc.gram_exact_blas(ao, pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-4
+    assert np.all(G.diagonal(axis1=1, axis2=2).imag == 0)
+    assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
+
+
+def test_gram_large_k_fp32_e3(xl, orc):
+    """E3 size in fp32: K = 1000, M = 35 000 against the oracle (1e-4) and the paper's gap."""
+    a = xl.Array.ula(35000, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 1000, 1, seed=0)
+    G = xl.gram_exact(a, pos, precision=xl.FP32)
+    Go = orc.gram_exact_blas(orc.array("ula", n_y=35000, fc_hz=100e9), pos.cpu().numpy())
+    assert normalized_err(G.cpu().numpy(), Go) <= 1e-4
+    rs, _, _, fl = xl.app_a_bounds(G, [0.0])
+    assert int(fl[0]) == 0 and abs(float(rs[0, 1]) - 0.064) < 1e-3
 
 
 def test_gram_large_k_determinism(xl):
