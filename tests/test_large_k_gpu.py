@@ -130,3 +130,29 @@ def test_closed_form_and_sweep_large_k(xl, orc):
     ok = ~np.isnan(pd)
     assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= 1e-6
     assert np.array_equal(res["n_valid"], nv)
+
+
+def test_max_k_1024_end_to_end(xl, orc):
+    """The largest supported K (1024 = 16 full blocks, K_pad = K): exact fp64 and fp32
+    Grams, all four receivers (tiled Cholesky + blocked inverse) and Appendix A against
+    the oracle on one drop."""
+    K, N = 1024, 3000  # N ~ 3 K: G well conditioned (at N ~ K, R is numerically singular on both sides)
+    a, ao = xl.Array.ula(N, 100e9), orc.array("ula", n_y=N, fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 1, seed=77)
+    G = xl.gram_exact(a, pos)
+    Go = orc.gram_exact_blas(ao, pos.cpu().numpy())
+    assert normalized_err(G.cpu().numpy(), Go) <= 1e-9
+    assert normalized_err(xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy(), Go) <= 1e-4
+    snr = [10.0]
+    allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    r, fl = xl.sum_rate(G, snr, allr)
+    ro, flo = orc.sum_rate(G.cpu().numpy(), snr, allr)
+    rg = r.cpu().numpy()
+    assert np.array_equal(np.isnan(rg), np.isnan(ro))
+    ok = ~np.isnan(ro)
+    assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    rs, bo, _, fa = xl.app_a_bounds(G, snr)
+    rso, boo, _, fao = orc.bounds_app_a(G.cpu().numpy(), snr)
+    assert np.array_equal(fa.cpu().numpy().astype(np.uint32), fao) and int(fao[0]) == 0
+    assert np.max(np.abs(rs.cpu().numpy() - rso)) <= 1e-6 and np.max(np.abs(bo.cpu().numpy() - boo)) <= 1e-6
