@@ -418,7 +418,6 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
   }
   __syncthreads();
   const double c4 = 4.0 * P.inv_lambda;
-  const bool n_odd = (P.N & 1) != 0;
   const int ue = lane & 3, uu = lane >> 2;
 
   const int64_t s0 = (int64_t)split * P.chunk;
