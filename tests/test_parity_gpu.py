@@ -390,3 +390,26 @@ def test_resume_by_first_drop_equals_one_run(xl):
     assert np.nanmax(np.abs(comb["ergodic"] - full["ergodic"])) <= 1e-10
     assert comb["sat"][2] == full["sat"][2]
     assert abs(comb["sat"][0] - full["sat"][0]) <= 1e-12 * abs(full["sat"][0])
+
+
+@pytest.mark.slow
+def test_sweep_full_cfg2_every_drop_vs_oracle(xl, orc):
+    """The bench workload at full size with nothing sampled: all 10^4 cfg2 drops, all nine N
+    (each N recomputed independently by the oracle, no nesting), three SNRs, CAP/ZF/MMSE:
+    every per-drop rate within 1e-6 bits/s/Hz, every ergodic mean within 1e-6, the valid
+    counts and M_sat identical (the oracle runs ~1 min on the GPU box's host cores)."""
+    w = CONFIGS[2]
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, w.n_drops, w.snr_db, w.receivers, users=ug, seed=w.seed,
+                              per_drop=True)
+    pos = xl.gen_drops(ug, w.K, w.n_drops, seed=w.seed).cpu().numpy()
+    erg, nv, sat, pdo = orc.saturation_sweep(orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz), w.n_list, pos, w.snr_db,
+                                             w.receivers, per_drop=True)
+    pd = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(pd), np.isnan(pdo))
+    ok = ~np.isnan(pdo)
+    assert np.max(np.abs(pd[ok] - pdo[ok])) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
+    assert np.nanmax(np.abs(res["ergodic"] - erg)) <= 1e-6
+    assert res["sat"][2] == sat[2]
