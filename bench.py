@@ -335,7 +335,10 @@ def run_ours(args):
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                "gpu_launches": int(launches), "clocks": ck, "roofline": roof,
                "kernel_ms_per_step": {k: v[1] / args.steps for k, v in ktimes.items()},
-               "sat_M": float(res["sat"][2])}
+               "sat_M": float(res["sat"][2]),
+               "run": {"gpu": torch.cuda.get_device_name(dev), "seeds": f"1000 + step (drops of rank r from {D} r)",
+                       "nan_rates_last_step": int(np.asarray(res["n_valid"]).size * D * world
+                                                  - int(np.asarray(res["n_valid"]).sum()))}}
     if dist:
         dist.barrier()
         dist.destroy_process_group()
