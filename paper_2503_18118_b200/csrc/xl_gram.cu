@@ -1527,10 +1527,17 @@ void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 // Materialised streaming on tcgen05 (TF32, RNA-pre-rounded H) unless disabled by
 // XLMIMO_STREAM=cuda (CUDA-core fp32 tiled kernel, also the fallback for shapes
 // the TMA path does not take: K < 9, N % 4 != 0).
+// The tensor-core fp32 paths round each coefficient to TF32 (RNA, 2^-11 relative): a
+// Gram entry's normalised error is ~5.6e-4 / sqrt(N) (per-product errors average over
+// the N elements), inside the fp32-tier 1e-4 for all K^2 entries only from N ~ 1000 on
+// (measured 8.8e-4 at N = 1, 1.7e-4 at N = 33).  Below kTcMinN the CUDA-core fp32
+// kernels (or, for K > 64, the fp64 DMMA kernel) run instead.
+constexpr int64_t kTcMinN = 1024;
+
 bool materialised_use_tc(int K, int64_t N) {
   static const char *e = getenv("XLMIMO_STREAM");
   if (e && !strcmp(e, "cuda")) return false;
-  return stream_tc_supported(K, N);
+  return N >= kTcMinN && stream_tc_supported(K, N);
 }
 
 // Materialised mode: drops per batch so that the planar complex64 H of a batch
@@ -1540,7 +1547,8 @@ bool materialised_use_tc(int K, int64_t N) {
 bool use_fused_tc(const ArrayP &a, int K, int precision, int n_lvl) {
   static const char *e = getenv("XLMIMO_GRAM_KERNEL");
   if (e && !strcmp(e, "legacy")) return false;
-  return precision == XLMIMO_FP32 && n_lvl == 1 && fused_tc_supported(a, K);
+  const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
+  return precision == XLMIMO_FP32 && n_lvl == 1 && N >= kTcMinN && fused_tc_supported(a, K);
 }
 
 // elements per drop as stored: the tiled32 (tcgen05) layout pads N to whole groups of 4 tiles
@@ -1562,7 +1570,7 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
-  if (K > xl::kMaxK && precision == XLMIMO_FP32)  // fused tcgen05 block pairs: one partial per chunk
+  if (K > xl::kMaxK && precision == XLMIMO_FP32 && N >= kTcMinN)  // fused tcgen05 block pairs
     return (size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double);
   if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
@@ -1703,7 +1711,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
     if (mode != XLMIMO_FUSED)
       return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d is fused only", K, xl::kMaxK);
     if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
-    if (precision == XLMIMO_FP32) {
+    if (precision == XLMIMO_FP32 && lvl_end[n_lvl - 1] >= kTcMinN) {
       if (n_lvl != 1 || !fused_tc_supported_geometry(a))
         return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d fp32 needs one level and a ULA or a UPA with "
                                               "rows a multiple of 8", K);

@@ -64,7 +64,7 @@ def test_gram_large_k_unsupported_modes(xl):
     pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 70, 1, seed=1)
     with pytest.raises(xl.XlmimoError):
         xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED)
-    upa = xl.Array.upa(20, 10, 100e9)  # rows not a multiple of the 8-element generator task
+    upa = xl.Array.upa(36, 30, 100e9)  # N >= 1024 (tensor-core tier), rows not a multiple of 8
     with pytest.raises(xl.XlmimoError):
         xl.gram_exact(upa, pos, precision=xl.FP32)
     e = torch.zeros((0, 70, 3), dtype=torch.float64, device="cuda")
@@ -156,3 +156,19 @@ def test_max_k_1024_end_to_end(xl, orc):
     rso, boo, _, fao = orc.bounds_app_a(G.cpu().numpy(), snr)
     assert np.array_equal(fa.cpu().numpy().astype(np.uint32), fao) and int(fao[0]) == 0
     assert np.max(np.abs(rs.cpu().numpy() - rso)) <= 1e-6 and np.max(np.abs(bo.cpu().numpy() - boo)) <= 1e-6
+
+
+@pytest.mark.parametrize("N", [1, 2, 31, 33])
+def test_gram_large_k_tiny_arrays(xl, orc, N):
+    """Degenerate element counts on the large-K paths (fewer elements than one 32-element
+    tile, a single element: G = h h^H of rank 1) in fp64 and fp32 (below 1024 elements
+    the fp32 request runs on the fp64 kernel: TF32 rounding would not average out)."""
+    K = 70
+    a, ao = xl.Array.ula(N, 100e9), orc.array("ula", n_y=N, fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 2, seed=N)
+    Go = orc.gram_exact(ao, pos.cpu().numpy())
+    assert normalized_err(xl.gram_exact(a, pos).cpu().numpy(), Go) <= 1e-9
+    assert normalized_err(xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy(), Go) <= 1e-4
+    if N == 1:
+        h = orc.channel_matrix(ao, pos.cpu().numpy()[0])[0]
+        assert normalized_err(Go[0][None], np.outer(h.conj(), h)[None]) <= 1e-14
