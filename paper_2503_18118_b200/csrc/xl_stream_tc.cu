@@ -318,11 +318,13 @@ constexpr int kTaskE = 8;          // elements per generator task (one fp64 anch
 // one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7 (offset d = m pitch
 // along y), from an fp64 anchor at t0: distance r_c, phase reduced as frac(r_c / lambda)
 // in fp64, and the Taylor coefficients of r(d) = sqrt(r_c^2 + 2 dy d + d^2) about d = 0,
-//   r = r_c + u d + (w/2) d^2 - (u w / (2 r_c)) d^3,  u = dy / r_c,  w = (1 - u^2) / r_c,
-// turned into a cubic in m for the phase (cycles) and a quadratic for the amplitude
+//   r = r_c + u d + (w/2) d^2 - (u w / (2 r_c)) d^3 + (w (5u^2 - 1) / (8 r_c^2)) d^4,
+//   u = dy / r_c,  w = (1 - u^2) / r_c,
+// turned into a quartic in m for the phase (cycles) and a quadratic for the amplitude
 // a_c (r / r_c)^{-3/2}; per element only fp32 FMAs, the FMA-pipe rint, MUFU sin/cos and
-// integer RNA rounding remain.  Truncation over 7 pitches at r >= 2 m, 100 GHz: phase
-// ~5e-7 cycles, amplitude ~2e-7 relative (fp32 tier tolerance 1e-4).  Elements past N are 0.
+// integer RNA rounding remain.  Truncation over 7 pitches at 100 GHz: phase d^5/r^4 ~
+// 7e-7 cycles even at r_c = 0.3 m (the cubic alone left 4e-5 cycles of systematic error
+// there), amplitude O((d/r)^3) ~ 4e-5 at 0.3 m (fp32 tier 1e-4).  Elements past N are 0.
 // uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
 __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
                                               int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
@@ -348,6 +350,7 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
   const float ca = (float)(u * pl);                          // cycles per element, linear
   const float cb = (float)(0.5 * w * pitch * pl);            // quadratic
   const float cg = (float)(-0.5 * u * w * p1 * pitch * pl);  // cubic
+  const float cq = (float)(0.125 * w * fma(5.0 * u, u, -1.0) * p1 * p1 * pitch * pl);  // quartic
   const double ac = uc.w * ir * xl::rsqrt_nr(rc);            // a_c = amp r_c^{-3/2}
   // (r / r_c)^{-3/2} = 1 - 3/2 D + 15/8 D^2, D = (r - r_c) / r_c = u p1 m + (w/2) p1 pitch m^2
   const float a0 = (float)ac;
@@ -358,7 +361,7 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
 #pragma unroll
   for (int m = 0; m < kTaskE; ++m) {
     const float fm = (float)m;
-    float cyc = fmaf(fmaf(fmaf(cg, fm, cb), fm, ca), fm, fc);
+    float cyc = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
     // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
     // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
     cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);

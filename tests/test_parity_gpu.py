@@ -413,3 +413,19 @@ def test_sweep_full_cfg2_every_drop_vs_oracle(xl, orc):
     assert np.array_equal(res["n_valid"], nv)
     assert np.nanmax(np.abs(res["ergodic"] - erg)) <= 1e-6
     assert res["sat"][2] == sat[2]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mat32"])
+def test_gram_fp32_user_close_to_the_array(xl, orc, prec):
+    """Users 0.3-0.6 m from a 100 GHz ULA (x well below the configs' 0.52 m minimum): the
+    fp32 tensor-core generators' Taylor steps stay inside the 1e-4 tier where the phase
+    curvature is largest."""
+    K, N = 16, 8192
+    rng = np.random.default_rng(5)
+    p = np.zeros((2, K, 3))
+    p[..., 0] = rng.uniform(0.3, 0.6, (2, K))
+    p[..., 1] = rng.uniform(-5.0, 5.0, (2, K))
+    pos = torch.tensor(p, device="cuda")
+    a, ao = xl.Array.ula(N, 100e9), orc.array("ula", n_y=N, fc_hz=100e9)
+    G = xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED if prec == "mat32" else xl.FUSED)
+    assert normalized_err(G.cpu().numpy(), orc.gram_exact(ao, p)) <= 1e-4
