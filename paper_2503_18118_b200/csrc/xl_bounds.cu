@@ -282,25 +282,132 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
 // lower triangle used), right-looking tiled Cholesky with 32 x 32 complex tiles:
 //  (1) warp 0 factors the diagonal tile in shared memory;
 //  (2) every thread solves one panel row x L_kk^H = a in registers;
-//  (3) trailing update A_ij -= L_ik L_jk^H: L_jk staged once per j for all warps, each
-//      warp stages its L_ik and computes the tile with a 4 x 8 register block per lane
-//      (32 independent complex accumulators; 12 shared loads per 32 complex MACs).
-constexpr int kLd = kTile + 1;  // padded row stride (conflict-free 16-byte column reads)
-constexpr size_t kTiledSmem = (size_t)(1 + kCtaThreads / 32) * kTile * kLd * sizeof(double2);
+//  (3) trailing update A_ij -= L_ik L_jk^H over the tiles k < j <= i, flattened over the
+//      warps (no per-column barrier), each tile on the FP64 tensor path: 8 k-steps of
+//      4 x 4 fragment pairs x 4 real DMMA m8n8k4 (RR, II, IR, RI), the 64 accumulator
+//      registers of the complex tile resident, both operands read as fragments straight
+//      from the slot (L2: the panel is 32 rows x K_pad per matrix).
+// DMMA and DFMA share the FP64 pipe at the same FMA rate; the tensor
+// path needs 1 instruction per 256 FMAs and no shared-memory operand traffic.
+constexpr int kGrp = 4;         // panels per trailing update
+constexpr int kLdY = kTile + 2;  // per-warp Y tile row stride (conflict-free B-fragment reads)
+constexpr size_t kTiledSmem = (size_t)(kCtaThreads / 32) * kTile * kLdY * sizeof(double2);
+
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double negd(double x) {  // sign flip on the integer pipe
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+
+// complex 32 x 32 tile in DMMA accumulator fragments: [mb][nb] covers rows 8 mb + lane/4,
+// columns 8 nb + 2 (lane % 4) + {0, 1}
+struct CTile {
+  double r[4][4][2], i[4][4][2];
+};
+__device__ __forceinline__ void ctile_zero(CTile &c) {
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) c.r[mb][nb][e] = c.i[mb][nb][e] = 0.0;
+}
+// one k-step (4 columns of A / rows of B): a[mb] = A(8 mb + lane/4, 4 kb + lane%4),
+// b[nb] = B(4 kb + lane%4, 8 nb + lane/4);  C += A B  (conj_b: C += A conj(B))
+template <bool CONJ_B, bool NEG>
+__device__ __forceinline__ void ctile_step(CTile &c, const double2 (&a)[4], const double2 (&b)[4]) {
+  // C += s A op(B), s = -1 if NEG: Re += s(ar br -+ ai bi), Im += s(ai br +- ar bi)
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) {
+    const double ar = NEG ? negd(a[mb].x) : a[mb].x;
+    const double ai = NEG ? negd(a[mb].y) : a[mb].y;
+    const double nai = negd(ai);
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_f64(c.r[mb][nb], ar, b[nb].x);
+      dmma_f64(c.r[mb][nb], CONJ_B ? ai : nai, b[nb].y);
+      dmma_f64(c.i[mb][nb], ai, b[nb].x);
+      dmma_f64(c.i[mb][nb], CONJ_B ? negd(ar) : ar, b[nb].y);
+    }
+  }
+}
+template <bool B_NT>
+__device__ __forceinline__ void frag_load(double2 (&a)[4], double2 (&b)[4], const double2 *__restrict__ Am, size_t lda,
+                                          const double2 *__restrict__ Bm, size_t ldb, int kb, int lane) {
+  const int qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) a[mb] = Am[(size_t)(8 * mb + qr) * lda + 4 * kb + qc];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb)
+    b[nb] = B_NT ? Bm[(size_t)(8 * nb + qr) * ldb + 4 * kb + qc] : Bm[(size_t)(4 * kb + qc) * ldb + 8 * nb + qr];
+}
+// C op= A (32 x 4 nkb, row-major, stride lda) * B (4 nkb x 32), B row-major (ldb) or, with
+// B_NT, B(k, n) = Bt(n, k) from a row-major Bt (stride ldb); C -= when NEG.  The
+// fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run (operands come from L2).
+template <bool B_NT, bool CONJ_B, bool NEG>
+__device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ Am, size_t lda,
+                                          const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
+  double2 a[4], b[4];
+  frag_load<B_NT>(a, b, Am, lda, Bm, ldb, 0, lane);
+#pragma unroll 1
+  for (int kb = 0; kb < nkb; ++kb) {
+    double2 an[4], bn[4];
+    frag_load<B_NT>(an, bn, Am, lda, Bm, ldb, kb + 1 < nkb ? kb + 1 : kb, lane);
+    ctile_step<CONJ_B, NEG>(c, a, b);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q] = an[q];
+      b[q] = bn[q];
+    }
+  }
+}
+// pull a 32 x 32 complex tile (32 rows of 512 B) into L2 ahead of its use
+__device__ __forceinline__ void tile_prefetch_l2(const double2 *src, size_t ld, int lane) {
+  const char *p = reinterpret_cast<const char *>(src + (size_t)lane * ld);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * q));
+}
+__device__ __forceinline__ void ctile_load(CTile &c, const double2 *src, size_t ld, int lane) {
+  const int qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      const double2 *p = src + (size_t)(8 * mb + qr) * ld + 8 * nb + 2 * qc;
+      const double2 v0 = p[0], v1 = p[1];
+      c.r[mb][nb][0] = v0.x;
+      c.i[mb][nb][0] = v0.y;
+      c.r[mb][nb][1] = v1.x;
+      c.i[mb][nb][1] = v1.y;
+    }
+}
+template <bool NEG>
+__device__ __forceinline__ void ctile_store(const CTile &c, double2 *dst, size_t ld, int lane) {
+  const int qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      double2 *p = dst + (size_t)(8 * mb + qr) * ld + 8 * nb + 2 * qc;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        p[e] = NEG ? make_double2(-c.r[mb][nb][e], -c.i[mb][nb][e]) : make_double2(c.r[mb][nb][e], c.i[mb][nb][e]);
+    }
+}
 
 __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P) {
-  extern __shared__ double2 tsm[];       // S [32][33] then per-warp W [8][32][33]
+  extern __shared__ double2 tsm[];       // per-warp Y tiles [8][32][kLdY]
   __shared__ double2 T[kTile * kTile];   // diagonal tile, column-major T[c*32 + r]
-  __shared__ int s_ok;
+  __shared__ int s_ok, s_next;
   __shared__ double s_ld;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kCtaThreads / 32;
   const int K = P.K, Kp = P.Kp, nt = P.nt;
   double2 *A = P.ws + (size_t)blockIdx.x * Kp * Kp;
-  double2 *S = tsm, *W = tsm + (1 + warp) * kTile * kLd;
-  // micro-tile: rows lr + 8a (a < 4), cols lc + 4b (b < 8).  With the 33-element row
-  // stride the 8 row groups and the 4 column groups hit distinct 16-byte bank slots.
-  const int lr = lane >> 2, lc = lane & 3;
+  double2 *W = tsm + warp * kTile * kLdY;
 
   for (int64_t prob = blockIdx.x; prob < P.n_prob; prob += gridDim.x) {
     const int64_t d = prob / P.n_mat;
@@ -318,109 +425,118 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
     if (tid == 0) {
       s_ok = ok0;
       s_ld = 0.0;
+      s_next = 0;
     }
     __syncthreads();
     // s_ok is only read right after the barrier that follows its one writer (step 1),
     // so every warp sees the same value and leaves the loop together.
-    for (int k = 0; k < nt && ok0; ++k) {
-      const int k0 = k * kTile;
-      if (warp == 0) {  // (1)
-        for (int c = 0; c < kTile; ++c) {
-          const double2 v = A[(size_t)(k0 + lane) * Kp + k0 + c];
-          T[c * kTile + lane] = (lane >= c) ? v : make_double2(0.0, 0.0);
+    // Panels in groups of kGrp: column k of a group first takes the updates of the
+    // group's earlier panels (left-looking), is factored (1) and solved (2); the
+    // trailing tiles then take the whole group at once (3), so each trailing tile is
+    // read and written once per group, with an inner dimension of 32 kGrp.
+    for (int g0 = 0; g0 < nt && ok0; g0 += kGrp) {
+      const int g1 = min(g0 + kGrp, nt);
+      for (int k = g0; k < g1; ++k) {
+        const int k0 = k * kTile;
+        if (k > g0) {  // tiles (i, k), i >= k: A_ik -= L_i,[g0,k) L_k,[g0,k)^H
+          const int nkb = (k - g0) * (kTile / 4);
+          for (int i = k + warp; i < nt; i += NW) {
+            const int i0 = i * kTile;
+            if (i + NW < nt) tile_prefetch_l2(A + (size_t)(i0 + NW * kTile) * Kp + k0, Kp, lane);
+            CTile c;
+            ctile_load(c, A + (size_t)i0 * Kp + k0, Kp, lane);
+            ctile_mma<true, true, true>(c, A + (size_t)i0 * Kp + g0 * kTile, Kp, A + (size_t)k0 * Kp + g0 * kTile,
+                                        Kp, nkb, lane);
+            ctile_store<false>(c, A + (size_t)i0 * Kp + k0, Kp, lane);
+          }
+          __syncthreads();
         }
-        const bool okf = xlk::warp_cholesky<1>(T, kTile, lane);
-        if (okf && P.dinv)  // the inverse phase reads L_kk back from the slot
-          for (int c = 0; c <= lane; ++c) A[(size_t)(k0 + lane) * Kp + k0 + c] = T[c * kTile + lane];
-        const double part = okf ? 2.0 * log2(T[lane * kTile + lane].x) : 0.0;
-        const double sum = xlk::warp_sum(part);
-        if (lane == 0) {
-          if (okf) s_ld += sum;
-          else s_ok = 0;
+        if (warp == 0) {  // (1)
+          for (int c = 0; c < kTile; ++c) {
+            const double2 v = A[(size_t)(k0 + lane) * Kp + k0 + c];
+            T[c * kTile + lane] = (lane >= c) ? v : make_double2(0.0, 0.0);
+          }
+          const bool okf = xlk::warp_cholesky<1>(T, kTile, lane);
+          if (okf && P.dinv)  // the inverse phase reads L_kk back from the slot
+            for (int c = 0; c <= lane; ++c) A[(size_t)(k0 + lane) * Kp + k0 + c] = T[c * kTile + lane];
+          const double part = okf ? 2.0 * log2(T[lane * kTile + lane].x) : 0.0;
+          const double sum = xlk::warp_sum(part);
+          if (lane == 0) {
+            if (okf) s_ld += sum;
+            else s_ok = 0;
+          }
         }
+        __syncthreads();
+        if (!s_ok) break;
+        // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj
+        for (int row = k0 + kTile + tid; row < Kp; row += kCtaThreads) {
+          // keep the 528 L_kk reads inside the iteration (hoisting them out of the row
+          // loop would need ~1000 registers)
+          asm volatile("" ::: "memory");
+          double2 *ar = A + (size_t)row * Kp + k0;
+          double2 x[kTile];
+#pragma unroll
+          for (int j = 0; j < kTile; ++j) x[j] = ar[j];
+#pragma unroll
+          for (int j = 0; j < kTile; ++j) {
+            double xr = x[j].x, xi = x[j].y;
+#pragma unroll
+            for (int mm = 0; mm < j; ++mm) {
+              const double2 l = T[mm * kTile + j];  // L_jm
+              xr -= x[mm].x * l.x + x[mm].y * l.y;
+              xi -= x[mm].y * l.x - x[mm].x * l.y;
+            }
+            const double inv = 1.0 / T[j * kTile + j].x;
+            x[j] = make_double2(xr * inv, xi * inv);
+          }
+#pragma unroll
+          for (int j = 0; j < kTile; ++j) ar[j] = x[j];
+        }
+        __syncthreads();
       }
-      __syncthreads();
       if (!s_ok) break;
-      // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj
-      for (int row = k0 + kTile + tid; row < Kp; row += kCtaThreads) {
-        // keep the 528 L_kk reads inside the iteration (hoisting them out of the row
-        // loop would need ~1000 registers)
-        asm volatile("" ::: "memory");
-        double2 *ar = A + (size_t)row * Kp + k0;
-        double2 x[kTile];
-#pragma unroll
-        for (int j = 0; j < kTile; ++j) x[j] = ar[j];
-#pragma unroll
-        for (int j = 0; j < kTile; ++j) {
-          double xr = x[j].x, xi = x[j].y;
-#pragma unroll
-          for (int mm = 0; mm < j; ++mm) {
-            const double2 l = T[mm * kTile + j];  // L_jm
-            xr -= x[mm].x * l.x + x[mm].y * l.y;
-            xi -= x[mm].y * l.x - x[mm].x * l.y;
-          }
-          const double inv = 1.0 / T[j * kTile + j].x;
-          x[j] = make_double2(xr * inv, xi * inv);
+      // (3) tiles (i, j) = (g1+ii, g1+jj), jj <= ii, row by row (warps that run together
+      // share L_i,G): A_ij -= L_i,G L_j,G^H over the group's columns G = [g0, g1)
+      const int nrem = nt - g1;
+      const int npair = nrem * (nrem + 1) / 2;
+      const int nkb = (g1 - g0) * (kTile / 4);
+      auto decode = [&](int p, int &i0, int &j0) {
+        int ii = (int)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
+        while ((ii + 1) * (ii + 2) / 2 <= p) ++ii;
+        while (ii * (ii + 1) / 2 > p) --ii;
+        i0 = (g1 + ii) * kTile;
+        j0 = (g1 + p - ii * (ii + 1) / 2) * kTile;
+      };
+      for (int p = warp; p < npair; p += NW) {
+        int i0, j0;
+        decode(p, i0, j0);
+        if (p + NW < npair) {
+          int pi0, pj0;
+          decode(p + NW, pi0, pj0);
+          tile_prefetch_l2(A + (size_t)pi0 * Kp + pj0, Kp, lane);
         }
-#pragma unroll
-        for (int j = 0; j < kTile; ++j) ar[j] = x[j];
+        CTile c;
+        ctile_load(c, A + (size_t)i0 * Kp + j0, Kp, lane);
+        ctile_mma<true, true, true>(c, A + (size_t)i0 * Kp + g0 * kTile, Kp, A + (size_t)j0 * Kp + g0 * kTile, Kp,
+                                    nkb, lane);
+        ctile_store<false>(c, A + (size_t)i0 * Kp + j0, Kp, lane);
       }
       __syncthreads();
-      // (3)
-      for (int j = k + 1; j < nt; ++j) {
-        const int j0 = j * kTile;
-        for (int e = tid; e < kTile * kTile; e += kCtaThreads) {  // S[c][mm] = L_jk[c][mm]
-          const int c = e >> 5, mm = e & 31;
-          S[c * kLd + mm] = A[(size_t)(j0 + c) * Kp + k0 + mm];
-        }
-        __syncthreads();
-        for (int i = j + warp; i < nt; i += NW) {
-          const int i0 = i * kTile;
-          for (int r = 0; r < kTile; ++r) W[r * kLd + lane] = A[(size_t)(i0 + r) * Kp + k0 + lane];
-          __syncwarp();
-          double2 acc[4][8];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) acc[a][b] = A[(size_t)(i0 + lr + 8 * a) * Kp + j0 + lc + 4 * b];
-#pragma unroll 1
-          for (int mm = 0; mm < kTile; ++mm) {
-            double2 wa[4], sb[8];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) wa[a] = W[(lr + 8 * a) * kLd + mm];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) sb[b] = S[(lc + 4 * b) * kLd + mm];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 8; ++b) {
-                // wa conj(sb) = (wr sr + wi si) + j (wi sr - wr si)
-                acc[a][b].x -= wa[a].x * sb[b].x + wa[a].y * sb[b].y;
-                acc[a][b].y -= wa[a].y * sb[b].x - wa[a].x * sb[b].y;
-              }
-          }
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) A[(size_t)(i0 + lr + 8 * a) * Kp + j0 + lc + 4 * b] = acc[a][b];
-          __syncwarp();
-        }
-        __syncthreads();
-      }
     }
     if (tid == 0) P.log2det[prob] = s_ok ? s_ld : kNaN;
     if (P.dinv) {
       // ---- [A^{-1}]_cc = sum_i |X_ic|^2, X = L^{-1}, by blocked forward substitution:
       // (a) Dinv_i = L_ii^{-1} for every diagonal tile (warp per tile, lane = column);
-      // (b) warp per column block j: X_jj = Dinv_j, X_ij = -Dinv_i sum_{k=j}^{i-1} L_ik X_kj,
-      //     the panel X_{.j} kept in the warp's global scratch, column norms accumulated.
+      // (b) column blocks j handed out largest first by a shared counter:
+      //     X_jj = Dinv_j, X_ij = -Dinv_i sum_{k=j}^{i-1} L_ik X_kj (DMMA tiles), the panel
+      //     X_{.j} kept in the warp's global scratch, column norms accumulated.
       double *dout = P.dinv + (size_t)prob * K;
       const bool fact = s_ok != 0;
       double2 *Dv = P.dvs + (size_t)blockIdx.x * nt * kTile * kTile;
       for (int i = warp; i < nt && fact; i += NW) {
         const int i0 = i * kTile;
         for (int r = 0; r < kTile; ++r)
-          W[r * kLd + lane] = (lane <= r) ? A[(size_t)(i0 + r) * Kp + i0 + lane] : make_double2(0.0, 0.0);
+          W[r * kLdY + lane] = (lane <= r) ? A[(size_t)(i0 + r) * Kp + i0 + lane] : make_double2(0.0, 0.0);
         __syncwarp();
         asm volatile("" ::: "memory");
         double2 x[kTile];
@@ -429,11 +545,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           double xr = (k == lane) ? 1.0 : 0.0, xi = 0.0;
 #pragma unroll
           for (int mm = 0; mm < k; ++mm) {
-            const double2 l = W[k * kLd + mm];  // L_k,mm
+            const double2 l = W[k * kLdY + mm];  // L_k,mm
             xr -= l.x * x[mm].x - l.y * x[mm].y;
             xi -= l.x * x[mm].y + l.y * x[mm].x;
           }
-          const double inv = 1.0 / W[k * kLd + k].x;
+          const double inv = 1.0 / W[k * kLdY + k].x;
           x[k] = make_double2(xr * inv, xi * inv);
         }
 #pragma unroll
@@ -442,7 +558,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
       }
       __syncthreads();
       double2 *Xp = P.xscr + ((size_t)blockIdx.x * NW + warp) * Kp * kTile;  // [row - j0][32]
-      for (int j = warp; j < nt; j += NW) {
+      for (;;) {
+        int j = 0;
+        if (lane == 0) j = atomicAdd(&s_next, 1);
+        j = __shfl_sync(0xffffffffu, j, 0);
+        if (j >= nt) break;
         const int j0 = j * kTile;
         if (!fact) {
           if (j0 + lane < K) dout[j0 + lane] = kNaN;
@@ -455,88 +575,50 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           Xp[(size_t)r * kTile + lane] = v;
           nrm += v.x * v.x + v.y * v.y;
         }
-        double part[8];
+        double part[4][2];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) part[b] = 0.0;
+        for (int nb = 0; nb < 4; ++nb) part[nb][0] = part[nb][1] = 0.0;
         __syncwarp();
         for (int i = j + 1; i < nt; ++i) {
           const int i0 = i * kTile;
-          double2 acc[4][8];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
-          for (int k = j; k < i; ++k) {  // Y += L_ik X_kj
-            const double2 *lrow = A + (size_t)i0 * Kp + (size_t)k * kTile;
-            const double2 *xk = Xp + (size_t)(k - j) * kTile * kTile;
-#pragma unroll 1
-            for (int mm = 0; mm < kTile; ++mm) {
-              double2 wa[4], sb[8];
-#pragma unroll
-              for (int a = 0; a < 4; ++a) wa[a] = lrow[(size_t)(lr + 8 * a) * Kp + mm];
-#pragma unroll
-              for (int b = 0; b < 8; ++b) sb[b] = xk[mm * kTile + lc + 4 * b];
-#pragma unroll
-              for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                  acc[a][b].x += wa[a].x * sb[b].x - wa[a].y * sb[b].y;
-                  acc[a][b].y += wa[a].x * sb[b].y + wa[a].y * sb[b].x;
-                }
-            }
-          }
-          // Y -> shared (W), then X_ij = -Dinv_i Y
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) W[(lr + 8 * a) * kLd + lc + 4 * b] = acc[a][b];
+          CTile c;
+          ctile_zero(c);
+          // Y = sum_{k=j}^{i-1} L_ik X_kj: L_i,[j,i) is contiguous in the row, X_[j,i),j in the panel
+          ctile_mma<false, false, false>(c, A + (size_t)i0 * Kp + j0, Kp, Xp, kTile, (i - j) * (kTile / 4), lane);
+          ctile_store<false>(c, W, kLdY, lane);  // Y -> shared
           __syncwarp();
-          const double2 *dvi = Dv + (size_t)i * kTile * kTile;
+          ctile_zero(c);  // X_ij = -Dinv_i Y
+          ctile_mma<false, false, true>(c, Dv + (size_t)i * kTile * kTile, kTile, W, kLdY, kTile / 4, lane);
+          ctile_store<false>(c, Xp + (size_t)(i - j) * kTile * kTile, kTile, lane);
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-            for (int b = 0; b < 8; ++b) acc[a][b] = make_double2(0.0, 0.0);
-#pragma unroll 1
-          for (int mm = 0; mm < kTile; ++mm) {
-            double2 wa[4], sb[8];
+            for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-            for (int a = 0; a < 4; ++a) wa[a] = dvi[(lr + 8 * a) * kTile + mm];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) sb[b] = W[mm * kLd + lc + 4 * b];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 8; ++b) {
-                acc[a][b].x -= wa[a].x * sb[b].x - wa[a].y * sb[b].y;
-                acc[a][b].y -= wa[a].x * sb[b].y + wa[a].y * sb[b].x;
-              }
-          }
-          double2 *xo = Xp + (size_t)(i - j) * kTile * kTile;
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              xo[(lr + 8 * a) * kTile + lc + 4 * b] = acc[a][b];
-              part[b] += acc[a][b].x * acc[a][b].x + acc[a][b].y * acc[a][b].y;
-            }
+              for (int e = 0; e < 2; ++e)
+                part[nb][e] += c.r[mb][nb][e] * c.r[mb][nb][e] + c.i[mb][nb][e] * c.i[mb][nb][e];
           __syncwarp();
         }
-        // column c = lc + 4 b: add the 8 row groups (lanes lr * 4 + lc), then the X_jj part
+        // column c = 8 nb + 2 qc + e: add the 8 row groups (lanes 4 qr + qc), then X_jj's part
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          double v = part[b];
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          v += __shfl_xor_sync(0xffffffffu, v, 8);
-          v += __shfl_xor_sync(0xffffffffu, v, 16);
-          part[b] = v;
-        }
-        // lane c gathers column c's sum from lane lc = c % 4 (any lr), slot b = c / 4
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double v = part[nb][e];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            part[nb][e] = v;
+          }
+        // lane c gathers its column from lane qc = (c / 2) % 4, slot (nb, e) = (c / 8, c % 2)
         double tot = 0.0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const double v = __shfl_sync(0xffffffffu, part[b], lane & 3);
-          if ((lane >> 2) == b) tot = v;
-        }
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double v = __shfl_sync(0xffffffffu, part[nb][e], (lane >> 1) & 3);
+            if ((lane >> 3) == nb && (lane & 1) == e) tot = v;
+          }
         if (j0 + lane < K) dout[j0 + lane] = nrm + tot;
         __syncwarp();
       }
