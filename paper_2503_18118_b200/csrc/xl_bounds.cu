@@ -316,21 +316,19 @@ __device__ __forceinline__ void ctile_zero(CTile &c) {
       for (int e = 0; e < 2; ++e) c.r[mb][nb][e] = c.i[mb][nb][e] = 0.0;
 }
 // one k-step (4 columns of A / rows of B): a[mb] = A(8 mb + lane/4, 4 kb + lane%4),
-// b[nb] = B(4 kb + lane%4, 8 nb + lane/4);  C += A B  (conj_b: C += A conj(B))
-template <bool CONJ_B, bool NEG>
+// b[nb] = B(4 kb + lane%4, 8 nb + lane/4);  C += A B, or C += A conj(B) with CONJ_B:
+// Re += ar br -+ ai bi, Im += ai br +- ar bi (one sign flip per fragment of A)
+template <bool CONJ_B>
 __device__ __forceinline__ void ctile_step(CTile &c, const double2 (&a)[4], const double2 (&b)[4]) {
-  // C += s A op(B), s = -1 if NEG: Re += s(ar br -+ ai bi), Im += s(ai br +- ar bi)
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb) {
-    const double ar = NEG ? negd(a[mb].x) : a[mb].x;
-    const double ai = NEG ? negd(a[mb].y) : a[mb].y;
-    const double nai = negd(ai);
+    const double n = CONJ_B ? negd(a[mb].x) : negd(a[mb].y);
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) {
-      dmma_f64(c.r[mb][nb], ar, b[nb].x);
-      dmma_f64(c.r[mb][nb], CONJ_B ? ai : nai, b[nb].y);
-      dmma_f64(c.i[mb][nb], ai, b[nb].x);
-      dmma_f64(c.i[mb][nb], CONJ_B ? negd(ar) : ar, b[nb].y);
+      dmma_f64(c.r[mb][nb], a[mb].x, b[nb].x);
+      dmma_f64(c.r[mb][nb], CONJ_B ? a[mb].y : n, b[nb].y);
+      dmma_f64(c.i[mb][nb], a[mb].y, b[nb].x);
+      dmma_f64(c.i[mb][nb], CONJ_B ? n : a[mb].x, b[nb].y);
     }
   }
 }
@@ -344,19 +342,33 @@ __device__ __forceinline__ void frag_load(double2 (&a)[4], double2 (&b)[4], cons
   for (int nb = 0; nb < 4; ++nb)
     b[nb] = B_NT ? Bm[(size_t)(8 * nb + qr) * ldb + 4 * kb + qc] : Bm[(size_t)(4 * kb + qc) * ldb + 8 * nb + qr];
 }
-// C op= A (32 x 4 nkb, row-major, stride lda) * B (4 nkb x 32), B row-major (ldb) or, with
-// B_NT, B(k, n) = Bt(n, k) from a row-major Bt (stride ldb); C -= when NEG.  The
-// fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run (operands come from L2).
-template <bool B_NT, bool CONJ_B, bool NEG>
+// L2 prefetch of the operand lines of k-steps q, q + 1 (q even): A row lane, 128 B; B the
+// same (B_NT) or rows 4q .. 4q + 7 (row-major B, 32-wide)
+template <bool B_NT>
+__device__ __forceinline__ void frag_prefetch_l2(const double2 *Am, size_t lda, const double2 *Bm, size_t ldb, int q,
+                                                 int lane) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(Am + (size_t)lane * lda + 4 * q));
+  const double2 *pb = B_NT ? Bm + (size_t)lane * ldb + 4 * q : Bm + (size_t)(4 * q + (lane >> 2)) * ldb + 8 * (lane & 3);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(pb));
+}
+// C += A (32 x 4 nkb, row-major, stride lda) * B (4 nkb x 32), B row-major (ldb) or, with
+// B_NT, B(k, n) = Bt(n, k) from a row-major Bt (stride ldb) (conjugated with CONJ_B).  The
+// fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run, and (PF, operands in
+// global memory) the lines of k-step kb + kPfDist are pulled into L2 meanwhile.
+constexpr int kPfDist = 8;
+template <bool B_NT, bool CONJ_B, bool PF>
 __device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ Am, size_t lda,
                                           const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
+  if (PF)
+    for (int q = 0; q < kPfDist && q < nkb; q += 2) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, q, lane);
   double2 a[4], b[4];
   frag_load<B_NT>(a, b, Am, lda, Bm, ldb, 0, lane);
 #pragma unroll 1
   for (int kb = 0; kb < nkb; ++kb) {
+    if (PF && !(kb & 1) && kb + kPfDist < nkb) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, kb + kPfDist, lane);
     double2 an[4], bn[4];
     frag_load<B_NT>(an, bn, Am, lda, Bm, ldb, kb + 1 < nkb ? kb + 1 : kb, lane);
-    ctile_step<CONJ_B, NEG>(c, a, b);
+    ctile_step<CONJ_B>(c, a, b);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       a[q] = an[q];
@@ -370,6 +382,7 @@ __device__ __forceinline__ void tile_prefetch_l2(const double2 *src, size_t ld, 
 #pragma unroll
   for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * q));
 }
+template <bool NEG>
 __device__ __forceinline__ void ctile_load(CTile &c, const double2 *src, size_t ld, int lane) {
   const int qr = lane >> 2, qc = lane & 3;
 #pragma unroll
@@ -378,10 +391,10 @@ __device__ __forceinline__ void ctile_load(CTile &c, const double2 *src, size_t 
     for (int nb = 0; nb < 4; ++nb) {
       const double2 *p = src + (size_t)(8 * mb + qr) * ld + 8 * nb + 2 * qc;
       const double2 v0 = p[0], v1 = p[1];
-      c.r[mb][nb][0] = v0.x;
-      c.i[mb][nb][0] = v0.y;
-      c.r[mb][nb][1] = v1.x;
-      c.i[mb][nb][1] = v1.y;
+      c.r[mb][nb][0] = NEG ? -v0.x : v0.x;
+      c.i[mb][nb][0] = NEG ? -v0.y : v0.y;
+      c.r[mb][nb][1] = NEG ? -v1.x : v1.x;
+      c.i[mb][nb][1] = NEG ? -v1.y : v1.y;
     }
 }
 template <bool NEG>
@@ -444,10 +457,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
             const int i0 = i * kTile;
             if (i + NW < nt) tile_prefetch_l2(A + (size_t)(i0 + NW * kTile) * Kp + k0, Kp, lane);
             CTile c;
-            ctile_load(c, A + (size_t)i0 * Kp + k0, Kp, lane);
+            ctile_load<true>(c, A + (size_t)i0 * Kp + k0, Kp, lane);  // -A_ik += L L^H
             ctile_mma<true, true, true>(c, A + (size_t)i0 * Kp + g0 * kTile, Kp, A + (size_t)k0 * Kp + g0 * kTile,
                                         Kp, nkb, lane);
-            ctile_store<false>(c, A + (size_t)i0 * Kp + k0, Kp, lane);
+            ctile_store<true>(c, A + (size_t)i0 * Kp + k0, Kp, lane);
           }
           __syncthreads();
         }
@@ -468,29 +481,44 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
         }
         __syncthreads();
         if (!s_ok) break;
-        // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj
+        // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj, in two halves of 16 columns
+        // (the second half re-reads the first from the row it was just written to)
         for (int row = k0 + kTile + tid; row < Kp; row += kCtaThreads) {
-          // keep the 528 L_kk reads inside the iteration (hoisting them out of the row
-          // loop would need ~1000 registers)
           asm volatile("" ::: "memory");
           double2 *ar = A + (size_t)row * Kp + k0;
-          double2 x[kTile];
 #pragma unroll
-          for (int j = 0; j < kTile; ++j) x[j] = ar[j];
+          for (int h = 0; h < 2; ++h) {
+            constexpr int HW = kTile / 2;
+            double2 x[HW];
 #pragma unroll
-          for (int j = 0; j < kTile; ++j) {
-            double xr = x[j].x, xi = x[j].y;
+            for (int j = 0; j < HW; ++j) x[j] = ar[h * HW + j];
+            if (h) {
+#pragma unroll 4
+              for (int mm = 0; mm < HW; ++mm) {
+                const double2 xm = ar[mm];
 #pragma unroll
-            for (int mm = 0; mm < j; ++mm) {
-              const double2 l = T[mm * kTile + j];  // L_jm
-              xr -= x[mm].x * l.x + x[mm].y * l.y;
-              xi -= x[mm].y * l.x - x[mm].x * l.y;
+                for (int j = 0; j < HW; ++j) {
+                  const double2 l = T[mm * kTile + HW + j];  // L_jm
+                  x[j].x -= xm.x * l.x + xm.y * l.y;
+                  x[j].y -= xm.y * l.x - xm.x * l.y;
+                }
+              }
             }
-            const double inv = 1.0 / T[j * kTile + j].x;
-            x[j] = make_double2(xr * inv, xi * inv);
-          }
 #pragma unroll
-          for (int j = 0; j < kTile; ++j) ar[j] = x[j];
+            for (int j = 0; j < HW; ++j) {
+              double xr = x[j].x, xi = x[j].y;
+#pragma unroll
+              for (int mm = 0; mm < j; ++mm) {
+                const double2 l = T[(h * HW + mm) * kTile + h * HW + j];  // L_jm
+                xr -= x[mm].x * l.x + x[mm].y * l.y;
+                xi -= x[mm].y * l.x - x[mm].x * l.y;
+              }
+              const double inv = 1.0 / T[(h * HW + j) * kTile + h * HW + j].x;
+              x[j] = make_double2(xr * inv, xi * inv);
+            }
+#pragma unroll
+            for (int j = 0; j < HW; ++j) ar[h * HW + j] = x[j];
+          }
         }
         __syncthreads();
       }
@@ -516,10 +544,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           tile_prefetch_l2(A + (size_t)pi0 * Kp + pj0, Kp, lane);
         }
         CTile c;
-        ctile_load(c, A + (size_t)i0 * Kp + j0, Kp, lane);
+        ctile_load<true>(c, A + (size_t)i0 * Kp + j0, Kp, lane);  // -A_ij += L L^H
         ctile_mma<true, true, true>(c, A + (size_t)i0 * Kp + g0 * kTile, Kp, A + (size_t)j0 * Kp + g0 * kTile, Kp,
                                     nkb, lane);
-        ctile_store<false>(c, A + (size_t)i0 * Kp + j0, Kp, lane);
+        ctile_store<true>(c, A + (size_t)i0 * Kp + j0, Kp, lane);
       }
       __syncthreads();
     }
@@ -584,12 +612,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           CTile c;
           ctile_zero(c);
           // Y = sum_{k=j}^{i-1} L_ik X_kj: L_i,[j,i) is contiguous in the row, X_[j,i),j in the panel
-          ctile_mma<false, false, false>(c, A + (size_t)i0 * Kp + j0, Kp, Xp, kTile, (i - j) * (kTile / 4), lane);
+          ctile_mma<false, false, true>(c, A + (size_t)i0 * Kp + j0, Kp, Xp, kTile, (i - j) * (kTile / 4), lane);
           ctile_store<false>(c, W, kLdY, lane);  // Y -> shared
           __syncwarp();
           ctile_zero(c);  // X_ij = -Dinv_i Y
-          ctile_mma<false, false, true>(c, Dv + (size_t)i * kTile * kTile, kTile, W, kLdY, kTile / 4, lane);
-          ctile_store<false>(c, Xp + (size_t)(i - j) * kTile * kTile, kTile, lane);
+          ctile_mma<false, false, false>(c, Dv + (size_t)i * kTile * kTile, kTile, W, kLdY, kTile / 4, lane);
+          ctile_store<true>(c, Xp + (size_t)(i - j) * kTile * kTile, kTile, lane);
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
