@@ -16,9 +16,10 @@
 //    shared memory, the same warp Cholesky as the receivers.
 //  * chol_smem_kernel (64 < K <= 160): one CTA per matrix, packed lower triangle in
 //    shared memory, unblocked right-looking Cholesky.
-//  * chol_tiled_kernel (K > 160): one CTA per matrix in a global workspace slot,
-//    right-looking tiled Cholesky with 32 x 32 complex tiles and a register-blocked
-//    trailing update.  O(K^3/6) complex MACs per matrix.
+//  * chol_tiled_kernel (K > 160): one CTA per matrix in a global workspace slot, two
+//    CTAs per SM, tiled Cholesky with 32 x 32 complex tiles on DMMA (panel groups of
+//    4, inverted diagonal tiles).  O(K^3/6) complex MACs per matrix; with dinv the
+//    blocked inverse L^{-1} (another K^3/6) on the same tile products.
 //  * finish kernels: one CTA per drop; scan G (finite, positive diagonal), log2 U /
 //    MRC from G, assemble outputs and flags.
 //  * eig_jacobi_kernel (K <= 64): eigenvalues of R by the parallel (round-robin)
@@ -26,6 +27,7 @@
 //    round; each rotation first makes A_pq real by a phase on column/row q, then
 //    zeroes it with the real plane rotation (t = sgn(theta)/(|theta| + sqrt(theta^2+1)),
 //    theta = (a_qq - a_pp)/(2|a_pq|)).
+#include <cstdio>
 #include <cstring>
 
 #include "xl_common.cuh"
@@ -279,19 +281,27 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
 }
 
 // K > kSmemK: one CTA per matrix in a global workspace slot (K_pad = 32 nt, row-major,
-// lower triangle used), right-looking tiled Cholesky with 32 x 32 complex tiles:
-//  (1) warp 0 factors the diagonal tile in shared memory;
-//  (2) every thread solves one panel row x L_kk^H = a in registers;
-//  (3) trailing update A_ij -= L_ik L_jk^H over the tiles k < j <= i, flattened over the
-//      warps (no per-column barrier), each tile on the FP64 tensor path: 8 k-steps of
-//      4 x 4 fragment pairs x 4 real DMMA m8n8k4 (RR, II, IR, RI), the 64 accumulator
-//      registers of the complex tile resident, both operands read as fragments straight
-//      from the slot (L2: the panel is 32 rows x K_pad per matrix).
-// DMMA and DFMA share the FP64 pipe at the same FMA rate; the tensor
-// path needs 1 instruction per 256 FMAs and no shared-memory operand traffic.
-constexpr int kGrp = 4;         // panels per trailing update
+// lower triangle used), tiled Cholesky with 32 x 32 complex tiles, panels in groups of
+// kGrp = 4 (left-looking inside a group, right-looking between groups):
+//  (0) the tiles of column k take the group's earlier panels: A_ik -= L_i,G' L_k,G'^H;
+//  (1) warp 0 factors the diagonal tile in shared memory and inverts it (lane = column);
+//  (2) panel X_ik = A_ik L_kk^{-H}, one tile product per warp;
+//  (3) after the group, every trailing tile A_ij -= L_i,G L_j,G^H once (inner dimension
+//      128), tiles flattened over the warps (no per-column barrier).
+// Every tile product runs on the FP64 tensor path: per 4-wide k-step 4 x 4 fragment
+// pairs x 4 real DMMA m8n8k4 (RR, II, IR, RI), the 64 accumulator registers of the
+// complex tile resident, operand fragments read straight from the slot (L2, prefetched
+// kPfDist k-steps ahead) with a one-step register double buffer.  DMMA and DFMA share
+// the FP64 pipe at the same FMA rate; the tensor path needs one
+// instruction per 256 FMAs and no shared-memory operand traffic.
+constexpr int kGrp = 4;          // panels per trailing update
 constexpr int kLdY = kTile + 2;  // per-warp Y tile row stride (conflict-free B-fragment reads)
-constexpr size_t kTiledSmem = (size_t)(kCtaThreads / 32) * kTile * kLdY * sizeof(double2);
+constexpr int kLdI = kTile + 4;  // L_kk^{-1} row stride (conflict-free B_NT fragment reads)
+// Two CTAs of 4 warps per SM, each on its own matrix: one CTA's serial steps (diagonal
+// factor, barriers) overlap the other's tensor work.
+constexpr int kTiledThreads = 128;
+constexpr int kTiledPerSm = 2;
+constexpr size_t kTiledSmem = (size_t)(kTiledThreads / 32) * kTile * kLdY * sizeof(double2);
 
 __device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -320,14 +330,20 @@ __device__ __forceinline__ void ctile_zero(CTile &c) {
 // Re += ar br -+ ai bi, Im += ai br +- ar bi (one sign flip per fragment of A)
 template <bool CONJ_B>
 __device__ __forceinline__ void ctile_step(CTile &c, const double2 (&a)[4], const double2 (&b)[4]) {
+  // the two DMMAs into one accumulator are 32 instructions apart
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_f64(c.r[mb][nb], a[mb].x, b[nb].x);
+      dmma_f64(c.i[mb][nb], a[mb].y, b[nb].x);
+    }
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb) {
     const double n = CONJ_B ? negd(a[mb].x) : negd(a[mb].y);
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) {
-      dmma_f64(c.r[mb][nb], a[mb].x, b[nb].x);
       dmma_f64(c.r[mb][nb], CONJ_B ? a[mb].y : n, b[nb].y);
-      dmma_f64(c.i[mb][nb], a[mb].y, b[nb].x);
       dmma_f64(c.i[mb][nb], CONJ_B ? n : a[mb].x, b[nb].y);
     }
   }
@@ -411,16 +427,28 @@ __device__ __forceinline__ void ctile_store(const CTile &c, double2 *dst, size_t
     }
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P) {
+__global__ void __launch_bounds__(kTiledThreads, kTiledPerSm) chol_tiled_kernel(CholParams P) {
   extern __shared__ double2 tsm[];       // per-warp Y tiles [8][32][kLdY]
   __shared__ double2 T[kTile * kTile];   // diagonal tile, column-major T[c*32 + r]
+  __shared__ double2 LI[kTile * kLdI];   // its inverse, row-major
   __shared__ int s_ok, s_next;
   __shared__ double s_ld;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kCtaThreads / 32;
+  constexpr int NW = kTiledThreads / 32;
   const int K = P.K, Kp = P.Kp, nt = P.nt;
   double2 *A = P.ws + (size_t)blockIdx.x * Kp * Kp;
   double2 *W = tsm + warp * kTile * kLdY;
+#ifdef XB_PROF
+  long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tl = clock64();
+#define XB_T(i)                      \
+  if (tid == 0) {                    \
+    const long long t_ = clock64();  \
+    pt[i] += t_ - tl;                \
+    tl = t_;                         \
+  }
+#else
+#define XB_T(i)
+#endif
 
   for (int64_t prob = blockIdx.x; prob < P.n_prob; prob += gridDim.x) {
     const int64_t d = prob / P.n_mat;
@@ -428,12 +456,47 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
     const bool is_r = P.first_is_r && m == 0;
     const double2 *G = reinterpret_cast<const double2 *>(P.gram) + (size_t)d * K * K;
     bool good = true;
-    for (int i = warp; i < Kp; i += NW)  // lower triangle, identity padding
-      for (int j = lane; j <= i; j += 32) {
-        double2 v = make_double2(i == j ? 1.0 : 0.0, 0.0);
-        if (i < K) v = chol_entry(G, K, i, j, is_r, P.rho[m], P.alpha[m], good);
-        A[(size_t)i * Kp + j] = v;
+    // lower triangle of the problem matrix (identity padding), 8 row loads in flight per
+    // lane; R scales by 1/sqrt(G_ii G_jj) from a table in the (idle) Y-tile memory
+    double *sd = reinterpret_cast<double *>(tsm);
+    if (is_r) {
+      for (int j = tid; j < K; j += kTiledThreads) {
+        const double g = G[(size_t)j * K + j].x;
+        good &= g > 0.0;
+        sd[j] = rsqrt(g);
       }
+      __syncthreads();
+    }
+    const double rho = P.rho[m], alpha = P.alpha[m];
+    for (int i = warp; i < Kp; i += NW) {
+      const double si = (is_r && i < K) ? sd[i] : 0.0;
+      for (int j0 = 0; j0 <= i; j0 += 256) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + 32 * u + lane;
+          v[u] = (i < K && j <= i) ? G[(size_t)i * K + j] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + 32 * u + lane;
+          if (j > i) continue;
+          double2 w = v[u];
+          if (i >= K) {
+            w = make_double2(i == j ? 1.0 : 0.0, 0.0);
+          } else {
+            good &= isfinite(w.x) && isfinite(w.y);
+            if (is_r) {
+              const double sc = si * sd[j];
+              w = (i == j) ? make_double2(1.0, 0.0) : make_double2(w.x * sc, w.y * sc);
+            } else {
+              w = (i == j) ? make_double2(alpha + rho * w.x, 0.0) : make_double2(rho * w.x, rho * w.y);
+            }
+          }
+          A[(size_t)i * Kp + j] = w;
+        }
+      }
+    }
     const int ok0 = __syncthreads_and(good ? 1 : 0);
     if (tid == 0) {
       s_ok = ok0;
@@ -441,6 +504,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
       s_next = 0;
     }
     __syncthreads();
+    XB_T(0)
     // s_ok is only read right after the barrier that follows its one writer (step 1),
     // so every warp sees the same value and leaves the loop together.
     // Panels in groups of kGrp: column k of a group first takes the updates of the
@@ -463,16 +527,42 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
             ctile_store<true>(c, A + (size_t)i0 * Kp + k0, Kp, lane);
           }
           __syncthreads();
+          XB_T(1)
         }
         if (warp == 0) {  // (1)
-          for (int c = 0; c < kTile; ++c) {
-            const double2 v = A[(size_t)(k0 + lane) * Kp + k0 + c];
-            T[c * kTile + lane] = (lane >= c) ? v : make_double2(0.0, 0.0);
+          {
+            double2 v[kTile];  // all 32 loads in flight (the tile is in L2)
+#pragma unroll
+            for (int c = 0; c < kTile; ++c) v[c] = A[(size_t)(k0 + lane) * Kp + k0 + c];
+#pragma unroll
+            for (int c = 0; c < kTile; ++c) T[c * kTile + lane] = (lane >= c) ? v[c] : make_double2(0.0, 0.0);
           }
           const bool okf = xlk::warp_cholesky<1>(T, kTile, lane);
           if (okf && P.dinv)  // the inverse phase reads L_kk back from the slot
             for (int c = 0; c <= lane; ++c) A[(size_t)(k0 + lane) * Kp + k0 + c] = T[c * kTile + lane];
-          const double part = okf ? 2.0 * log2(T[lane * kTile + lane].x) : 0.0;
+          if (okf) {  // L_kk^{-1} by lane = column c: x_r = (delta_rc - sum_{m<r} L_rm x_m) / L_rr
+            double2 x[kTile];
+#pragma unroll
+            for (int r = 0; r < kTile; ++r) {
+              double xr = (r == lane) ? 1.0 : 0.0, xi = 0.0;
+#pragma unroll
+              for (int mm = 0; mm < r; ++mm) {
+                const double2 l = T[mm * kTile + r];  // L_r,mm
+                xr -= l.x * x[mm].x - l.y * x[mm].y;
+                xi -= l.x * x[mm].y + l.y * x[mm].x;
+              }
+              const double inv = 1.0 / T[r * kTile + r].x;
+              x[r] = make_double2(xr * inv, xi * inv);
+            }
+            double2 *dv = P.dinv ? P.dvs + ((size_t)blockIdx.x * nt + k) * kTile * kTile : nullptr;
+#pragma unroll
+            for (int r = 0; r < kTile; ++r) {
+              LI[r * kLdI + lane] = x[r];
+              if (dv) dv[r * kTile + lane] = x[r];  // row r, col lane (the inverse phase's Dinv_k)
+            }
+          }
+          const double dg = T[lane * kTile + lane].x;
+          const double part = okf ? 2.0 * log2(dg) : 0.0;
           const double sum = xlk::warp_sum(part);
           if (lane == 0) {
             if (okf) s_ld += sum;
@@ -480,47 +570,18 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
           }
         }
         __syncthreads();
+        XB_T(2)
         if (!s_ok) break;
-        // (2) x_j = (a_j - sum_{m<j} x_m conj(L_jm)) / L_jj, in two halves of 16 columns
-        // (the second half re-reads the first from the row it was just written to)
-        for (int row = k0 + kTile + tid; row < Kp; row += kCtaThreads) {
-          asm volatile("" ::: "memory");
-          double2 *ar = A + (size_t)row * Kp + k0;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            constexpr int HW = kTile / 2;
-            double2 x[HW];
-#pragma unroll
-            for (int j = 0; j < HW; ++j) x[j] = ar[h * HW + j];
-            if (h) {
-#pragma unroll 4
-              for (int mm = 0; mm < HW; ++mm) {
-                const double2 xm = ar[mm];
-#pragma unroll
-                for (int j = 0; j < HW; ++j) {
-                  const double2 l = T[mm * kTile + HW + j];  // L_jm
-                  x[j].x -= xm.x * l.x + xm.y * l.y;
-                  x[j].y -= xm.y * l.x - xm.x * l.y;
-                }
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < HW; ++j) {
-              double xr = x[j].x, xi = x[j].y;
-#pragma unroll
-              for (int mm = 0; mm < j; ++mm) {
-                const double2 l = T[(h * HW + mm) * kTile + h * HW + j];  // L_jm
-                xr -= x[mm].x * l.x + x[mm].y * l.y;
-                xi -= x[mm].y * l.x - x[mm].x * l.y;
-              }
-              const double inv = 1.0 / T[(h * HW + j) * kTile + h * HW + j].x;
-              x[j] = make_double2(xr * inv, xi * inv);
-            }
-#pragma unroll
-            for (int j = 0; j < HW; ++j) ar[h * HW + j] = x[j];
-          }
+        // (2) panel X_ik = A_ik L_kk^{-H}, tiles i > k over the warps (DMMA, L_kk^{-1} in LI)
+        for (int i = k + 1 + warp; i < nt; i += NW) {
+          const int i0 = i * kTile;
+          CTile c;
+          ctile_zero(c);
+          ctile_mma<true, true, false>(c, A + (size_t)i0 * Kp + k0, Kp, LI, kLdI, kTile / 4, lane);
+          ctile_store<false>(c, A + (size_t)i0 * Kp + k0, Kp, lane);
         }
         __syncthreads();
+        XB_T(3)
       }
       if (!s_ok) break;
       // (3) tiles (i, j) = (g1+ii, g1+jj), jj <= ii, row by row (warps that run together
@@ -550,41 +611,20 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
         ctile_store<true>(c, A + (size_t)i0 * Kp + j0, Kp, lane);
       }
       __syncthreads();
+      XB_T(4)
     }
     if (tid == 0) P.log2det[prob] = s_ok ? s_ld : kNaN;
     if (P.dinv) {
       // ---- [A^{-1}]_cc = sum_i |X_ic|^2, X = L^{-1}, by blocked forward substitution:
-      // (a) Dinv_i = L_ii^{-1} for every diagonal tile (warp per tile, lane = column);
+      // (a) Dinv_i = L_ii^{-1} for every diagonal tile: written by the factorisation;
       // (b) column blocks j handed out largest first by a shared counter:
       //     X_jj = Dinv_j, X_ij = -Dinv_i sum_{k=j}^{i-1} L_ik X_kj (DMMA tiles), the panel
       //     X_{.j} kept in the warp's global scratch, column norms accumulated.
       double *dout = P.dinv + (size_t)prob * K;
       const bool fact = s_ok != 0;
       double2 *Dv = P.dvs + (size_t)blockIdx.x * nt * kTile * kTile;
-      for (int i = warp; i < nt && fact; i += NW) {
-        const int i0 = i * kTile;
-        for (int r = 0; r < kTile; ++r)
-          W[r * kLdY + lane] = (lane <= r) ? A[(size_t)(i0 + r) * Kp + i0 + lane] : make_double2(0.0, 0.0);
-        __syncwarp();
-        asm volatile("" ::: "memory");
-        double2 x[kTile];
-#pragma unroll
-        for (int k = 0; k < kTile; ++k) {
-          double xr = (k == lane) ? 1.0 : 0.0, xi = 0.0;
-#pragma unroll
-          for (int mm = 0; mm < k; ++mm) {
-            const double2 l = W[k * kLdY + mm];  // L_k,mm
-            xr -= l.x * x[mm].x - l.y * x[mm].y;
-            xi -= l.x * x[mm].y + l.y * x[mm].x;
-          }
-          const double inv = 1.0 / W[k * kLdY + k].x;
-          x[k] = make_double2(xr * inv, xi * inv);
-        }
-#pragma unroll
-        for (int k = 0; k < kTile; ++k) Dv[((size_t)i * kTile + k) * kTile + lane] = x[k];  // row k, col lane
-        __syncwarp();
-      }
       __syncthreads();
+      XB_T(5)
       double2 *Xp = P.xscr + ((size_t)blockIdx.x * NW + warp) * Kp * kTile;  // [row - j0][32]
       for (;;) {
         int j = 0;
@@ -652,7 +692,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) chol_tiled_kernel(CholParams P
       }
     }
     __syncthreads();
+    XB_T(6)
   }
+#ifdef XB_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    printf("chol_tiled phases (Mcycles, CTA 0): init %.2f left %.2f diag %.2f panel %.2f trail %.2f dinv_a %.2f dinv_b %.2f\n",
+           pt[0] * 1e-6, pt[1] * 1e-6, pt[2] * 1e-6, pt[3] * 1e-6, pt[4] * 1e-6, pt[5] * 1e-6, pt[6] * 1e-6);
+#endif
+#undef XB_T
 }
 
 // scan one drop's Gram: finite entries and positive diagonal (block-wide)
@@ -918,15 +965,19 @@ int n_chol_slots(int64_t n_prob) {
   }
   return (int)(n_prob < sms ? n_prob : sms);
 }
+int n_tiled_slots(int64_t n_prob) {
+  const int64_t n = (int64_t)kTiledPerSm * n_chol_slots(INT32_MAX);
+  return (int)(n_prob < n ? n_prob : n);
+}
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 size_t chol_slot_bytes(int K, int64_t n_prob, bool with_dinv) {
   if (K <= kSmemK) return 0;
   const int Kp = (K + kTile - 1) / kTile * kTile;
-  const size_t slots = (size_t)n_chol_slots(n_prob);
+  const size_t slots = (size_t)n_tiled_slots(n_prob);
   size_t b = align256(slots * Kp * Kp * sizeof(double2));
-  if (with_dinv) b += align256(slots * ((kCtaThreads / 32) * (size_t)Kp * kTile + (size_t)Kp * kTile) * sizeof(double2));
+  if (with_dinv) b += align256(slots * ((kTiledThreads / 32) * (size_t)Kp * kTile + (size_t)Kp * kTile) * sizeof(double2));
   return b;
 }
 
@@ -956,15 +1007,15 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
     cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     chol_smem_kernel<<<(unsigned)(grid < C.n_prob ? grid : C.n_prob), kCtaThreads, smem, s>>>(C);
   } else {
-    const int slots = n_chol_slots(C.n_prob);
+    const int slots = n_tiled_slots(C.n_prob);
     if (chol_slot_bytes(K, C.n_prob, dinv != nullptr) > ws_bytes)
       return xlh::set_error(XLMIMO_EWORKSPACE, "large-K Cholesky: workspace too small");
     if (dinv) {  // slot matrices, then the L^{-1} panels, then the diagonal-tile inverses
       C.xscr = (double2 *)((char *)ws + align256((size_t)slots * C.Kp * C.Kp * sizeof(double2)));
-      C.dvs = C.xscr + (size_t)slots * (kCtaThreads / 32) * C.Kp * kTile;
+      C.dvs = C.xscr + (size_t)slots * (kTiledThreads / 32) * C.Kp * kTile;
     }
     cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmem);
-    chol_tiled_kernel<<<slots, kCtaThreads, kTiledSmem, s>>>(C);
+    chol_tiled_kernel<<<slots, kTiledThreads, kTiledSmem, s>>>(C);
   }
   tm.stop(s);
   xlh::count_launch();
