@@ -102,9 +102,11 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  *     written to the workspace as planar complex64 and streamed back (fp32 only).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
  * Im G(i,i) = 0.  K <= 1024: K <= 64 on every precision/mode; 64 < K <= 1024 fused
- * only, in blocks of 64 users (fp64 on DMMA; fp32 on tcgen05, a UPA needing rows that
- * are a multiple of 8) -- NEXT-3/E1-E3 user counts.  ws may be
- * NULL iff the query returns 0.
+ * only -- NEXT-3/E1-E3 user counts: fp64 on DMMA, in blocks of
+ * 64 users below K = 128 and from K = 128 on as a chunked Hermitian rank-k update
+ * (H formed in the workspace a chunk of elements at a time, <= 64 MB so it stays in
+ * L2, never whole); fp32 on tcgen05 in blocks of 64 users (a UPA needing rows that are
+ * a multiple of 8).  ws may be NULL iff the query returns 0.
  * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 materialised (or fp32 on
  * an unsupported UPA), or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
 XLMIMO_API size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops,

@@ -281,6 +281,11 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s);
 
+// xl_gram_syrk.cu : large-K fp64 Gram as a chunked DMMA Hermitian rank-k update
+size_t gram_syrk_ws_bytes(int K, int64_t n_drops, int n_lvl);
+int launch_gram_syrk(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end, int n_lvl,
+                     double *out, void *ws, size_t ws_bytes, cudaStream_t s);
+
 // xl_stream_tc.cu : tcgen05 TF32 streaming Gram over a materialised batch
 bool stream_tc_supported(int K, int64_t N);
 int stream_tc_chunks(int64_t N);

@@ -1419,6 +1419,15 @@ int blk_pairs(int K) {
   const int nb = (K + kBlkU - 1) / kBlkU;
   return nb * (nb + 1) / 2;
 }
+// K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) from kSyrkMinK users on, the
+// block-pair kernel below it; XLMIMO_LARGE_K=blk|syrk overrides (A/B tests).
+constexpr int kSyrkMinK = 128;
+bool use_gram_syrk(int K) {
+  static const char *e = getenv("XLMIMO_LARGE_K");
+  if (e && !strcmp(e, "blk")) return false;
+  if (e && !strcmp(e, "syrk")) return true;
+  return K >= kSyrkMinK;
+}
 int choose_split_blk(int64_t n_drops, int K, int64_t N) {
   const int64_t target = 148 * 2, have = n_drops * blk_pairs(K);
   int64_t s = (target + have - 1) / (have > 0 ? have : 1);
@@ -1572,6 +1581,7 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
   }
   if (K > xl::kMaxK && precision == XLMIMO_FP32 && N >= kTcMinN)  // fused tcgen05 block pairs
     return (size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double);
+  if (K > xl::kMaxK && use_gram_syrk(K)) return gram_syrk_ws_bytes(K, n_drops, n_lvl);
   if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
@@ -1735,6 +1745,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       return check_launch("gram_reduce_rows_kernel");
     }
     if (n_drops == 0) return XLMIMO_OK;
+    if (use_gram_syrk(K)) return launch_gram_syrk(a, pos, K, n_drops, lvl_end, n_lvl, out, ws, ws_bytes, s);
     return launch_gram_blk(a, pos, K, n_drops, lvl_end, n_lvl, out, ws, ws_bytes, s);
   }
   if (mode == XLMIMO_MATERIALIZED) {

@@ -1,4 +1,5 @@
-"""GPU parity for the large-K (64 < K <= 1024) exact Gram (block-pair DMMA kernel):
+"""GPU parity for the large-K (64 < K <= 1024) exact Gram (block-pair DMMA kernel below
+K = 128, chunked DMMA SYRK from 128 on; fp32: tcgen05 block pairs):
 the CUDA path through the C ABI vs the oracle on the same GPU-drawn positions.
 
 Tolerance: |dG_ij| / sqrt(G_ii G_jj) <= 1e-9 (fp64 path, reading R9).
@@ -172,3 +173,64 @@ def test_gram_large_k_tiny_arrays(xl, orc, N):
     if N == 1:
         h = orc.channel_matrix(ao, pos.cpu().numpy()[0])[0]
         assert normalized_err(Go[0][None], np.outer(h.conj(), h)[None]) <= 1e-14
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,K,N_or_D", [("upa", 24, 20, 150, 2), ("ula", 1, 1, 150, 2),
+                                                   ("ula", 31, 1, 160, 1), ("ula", 4500, 1, 128, 3)])
+def test_gram_syrk_parity(xl, orc, kind, n_y, n_z, K, N_or_D):
+    """K >= 128 runs the chunked DMMA SYRK (xl_gram_syrk.cu): UPA, one element, fewer
+    elements than a tile, and a chunk boundary (4500 elements > one 4096-element chunk)."""
+    fc, D = 100e9, N_or_D
+    if kind == "ula":
+        a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=K + n_y)
+    else:
+        a, ao = xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, D, seed=K)
+    G = xl.gram_exact(a, pos).cpu().numpy()
+    assert normalized_err(G, orc.gram_exact(ao, pos.cpu().numpy())) <= 1e-9
+    assert np.all(G.diagonal(axis1=1, axis2=2).imag == 0)
+
+
+def test_exact_sweep_large_k_nested_levels(xl, orc):
+    """Exact fp64 saturation sweep at K = 130 (SYRK path: per-level partials, chunks
+    restarting at each level end, the last level two chunks long) against the oracle's
+    independent per-N Grams."""
+    K, D = 130, 2
+    nl = [700, 2000, 9000]
+    a, ao = xl.Array.ula(max(nl), 100e9), orc.array("ula", n_y=max(nl), fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=5)
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    res = xl.saturation_sweep(a, nl, K, D, [10.0], rec, pos=pos, per_drop=True)
+    _, nv, _, pd = orc.saturation_sweep(ao, nl, pos.cpu().numpy(), [10.0], rec, gram_kind=0, per_drop=True)
+    g = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(pd))
+    ok = ~np.isnan(pd)
+    assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
+
+
+@pytest.mark.parametrize("path,K", [("blk", 200), ("syrk", 100), ("syrk", 65)])
+def test_large_k_paths_outside_their_default_range(xl, path, K):
+    """XLMIMO_LARGE_K forces the block-pair or the SYRK kernel; each must match the
+    oracle outside the K range the default selection gives it (fresh process: the
+    selection is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, oracle as orc, paper_2503_18118_b200 as xl
+from tests._util import normalized_err
+a = xl.Array.ula(1500, 100e9)
+pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), {K}, 2, seed=3)
+G = xl.gram_exact(a, pos).cpu().numpy()
+Go = orc.gram_exact(orc.array("ula", n_y=1500, fc_hz=100e9), pos.cpu().numpy())
+e = normalized_err(G, Go)
+print("ERR", e)
+sys.exit(0 if e <= 1e-9 else 1)
+"""
+    env = dict(os.environ, XLMIMO_LARGE_K=path)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -2,8 +2,8 @@
 
     python tools/bench_app_a.py
 
-Grams: exact fused fp64 (E1/E3 user field, 100 GHz); K > 64 through the block-pair
-DMMA kernel.  Work per drop for the Cholesky path: (1 + n_snr) K^3/6 complex MACs.
+Grams: exact fp64 (E1/E3 user field, 100 GHz); K > 64 through the block-pair DMMA
+kernel (K < 128) or the chunked DMMA SYRK (K >= 128; XLMIMO_LARGE_K=blk|syrk overrides).  Work per drop for the Cholesky path: (1 + n_snr) K^3/6 complex MACs.
 """
 import json
 import os
@@ -47,10 +47,14 @@ def main():
         t = timed(lambda: xl.app_a_bounds(G, snr))
         chol = t.get("chol_logdet", float("nan"))
         cmac = D * 2 * K ** 3 / 6
-        gk = tg.get("gram_fused_dmma_blk_fp64", float("nan"))
+        gk = sum(v for k, v in tg.items() if k.startswith("gram"))  # all kernels of the exact Gram
         gcmac = D * N * K * (K + 1) / 2
         nb = (K + 63) // 64
-        ops = D * N * (nb * (nb + 1) // 2 * 64 * 64 * 4 + (nb * nb) * 64 * 31)  # DMMA FMA + generation model
+        if any(k.startswith("gram_syrk") for k in tg):  # 32x32 tile pairs, each coefficient generated once
+            nt = (K + 31) // 32
+            ops = D * N * (nt * (nt + 1) // 2 * 32 * 32 * 4 + nt * 32 * 31)
+        else:  # 64-user block pairs, both blocks generated per pair
+            ops = D * N * (nb * (nb + 1) // 2 * 64 * 64 * 4 + (nb * nb) * 64 * 31)
         print(json.dumps({"K": K, "N": N, "drops": D, "gram_ms": tg, "gram_cmac_per_s": gcmac / (gk * 1e-3),
                           "gram_frac_fp64_useful": 4 * gcmac / (gk * 1e-3) / PEAK_FP64,
                           "gram_frac_fp64_issued_model": ops / (gk * 1e-3) / PEAK_FP64,
