@@ -1,4 +1,5 @@
-"""One large-K gram_exact call (block-pair DMMA kernel) for ncu captures.
+"""One large-K gram_exact call (block-pair DMMA kernel, or the chunked SYRK for K >= 128)
+for ncu captures.
 
     python tools/prof_blk.py <K> <N> <drops>
 """
