@@ -320,17 +320,20 @@ constexpr int kTaskE = 8;          // elements per generator task (one fp64 anch
 // in fp64, and the Taylor coefficients of r(d) = sqrt(r_c^2 + 2 dy d + d^2) about d = 0,
 //   r = r_c + u d + (w/2) d^2 - (u w / (2 r_c)) d^3 + (w (5u^2 - 1) / (8 r_c^2)) d^4,
 //   u = dy / r_c,  w = (1 - u^2) / r_c,
-// turned into a quartic in m for the phase (cycles) and a quadratic for the amplitude
-// a_c (r / r_c)^{-3/2}; per element only fp32 FMAs, the FMA-pipe rint, MUFU sin/cos and
-// integer RNA rounding remain.  Truncation over 7 pitches at 100 GHz: phase d^5/r^4 ~
-// 7e-7 cycles even at r_c = 0.3 m (the cubic alone left 4e-5 cycles of systematic error
-// there), amplitude O((d/r)^3) ~ 4e-5 at 0.3 m (fp32 tier 1e-4).  Elements past N are 0.
-// uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
+// turned into a quartic in m for the phase and a quadratic for the amplitude
+// a_c (r / r_c)^{-3/2}.  fp64 is kept where the phase needs it -- r_c (1/r to ~1 ulp) and
+// the reduction frac(r_c / lambda) -- and the Taylor coefficients follow in fp32 from u,
+// 1/r_c and r_c (relative 1e-7: < 4e-7 rad at m = 7).  The phase is carried in radians,
+// unreduced past the anchor: |phase| <= pi (1 + 2 pitch/lambda m) < 9 pi, which MUFU
+// sin/cos take directly (their own revolution reduction costs < 1e-6 rad here, far inside
+// the TF32 rounding).  Per element: 4 FFMA, the MUFU pre-scale, 2 MUFU, 2 FFMA + 2 FMUL
+// of amplitude and the integer RNA rounding.  Truncation over 7 pitches at 100 GHz:
+// phase d^5/r^4 ~ 7e-7 cycles even at r_c = 0.3 m (the cubic alone left 4e-5 cycles of
+// systematic error there), amplitude O((d/r)^3) ~ 4e-5 at 0.3 m (fp32 tier 1e-4).
+// Elements past N are 0.  uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
 __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
                                               int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
                                               float pitch_f, uint32_t (&vr)[kTaskE], uint32_t (&vi)[kTaskE]) {
-  (void)inv_lambda_f;
-  (void)pitch_f;
   double ey, ez = 0.0;
   if (kind == XLMIMO_ULA) {
     ey = ((double)t0 - 0.5 * (double)(N - 1)) * pitch;
@@ -344,29 +347,29 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
   const double ir = xl::rsqrt_nr(r2);
   const double rc = r2 * ir;
   const double qc = rc * inv_lambda;
-  const float fc = (float)(qc - rint(qc));
-  const double u = dy * ir, w = fma(-u, u, 1.0) * ir;
-  const double pl = pitch * inv_lambda, p1 = pitch * ir;   // pitch / lambda, pitch / r_c
-  const float ca = (float)(u * pl);                          // cycles per element, linear
-  const float cb = (float)(0.5 * w * pitch * pl);            // quadratic
-  const float cg = (float)(-0.5 * u * w * p1 * pitch * pl);  // cubic
-  const float cq = (float)(0.125 * w * fma(5.0 * u, u, -1.0) * p1 * p1 * pitch * pl);  // quartic
-  const double ac = uc.w * ir * xl::rsqrt_nr(rc);            // a_c = amp r_c^{-3/2}
+  constexpr float k2pi = 6.28318530717958647692f;
+  const float fc = (float)(qc - rint(qc)) * k2pi;  // anchor phase, radians in [-pi, pi]
+  const float irf = (float)ir, u = (float)(dy * ir);
+  const float w = fmaf(-u, u, 1.0f) * irf;
+  const float pl = k2pi * pitch_f * inv_lambda_f;  // radians per pitch of path length
+  const float p1 = pitch_f * irf, pp = pitch_f * pl;
+  const float ca = u * pl;                                             // linear
+  const float cb = 0.5f * w * pp;                                      // quadratic
+  const float cg = -0.5f * u * w * p1 * pp;                            // cubic
+  const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;  // quartic
+  const float ac = (float)uc.w * irf * rsqrtf((float)rc);              // a_c = amp r_c^{-3/2}
   // (r / r_c)^{-3/2} = 1 - 3/2 D + 15/8 D^2, D = (r - r_c) / r_c = u p1 m + (w/2) p1 pitch m^2
-  const float a0 = (float)ac;
-  const float a1 = (float)(ac * (-1.5 * u * p1));
-  const float a2 = (float)(ac * (-0.75 * w * p1 * pitch + 1.875 * u * u * p1 * p1));
+  const float a0 = ac;
+  const float a1 = ac * (-1.5f * u * p1);
+  const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
   const int64_t nv64 = N - t0;  // valid elements of this task (padding past N is 0)
   const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
 #pragma unroll
   for (int m = 0; m < kTaskE; ++m) {
     const float fm = (float)m;
-    float cyc = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
-    // cyc - rint(cyc) on the FMA pipe: |cyc| < 2^22, so adding and subtracting
-    // 1.5 * 2^23 rounds to the nearest integer (ties to even, as rintf)
-    cyc -= __fsub_rn(__fadd_rn(cyc, 12582912.0f), 12582912.0f);
+    const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
     float sn, co;
-    __sincosf(6.28318530717958647692f * cyc, &sn, &co);
+    __sincosf(ph, &sn, &co);
     const float a = (m < nv) ? fmaf(fmaf(a2, fm, a1), fm, a0) : 0.0f;
     vr[m] = tf32_rna(a * co);
     vi[m] = tf32_rna(-a * sn);
