@@ -314,6 +314,12 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(
 
 constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
 
+__device__ __forceinline__ void st_cs_v8(float *p, const uint32_t (&v)[8]) {  // 32-B aligned
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 // One generator task: the TF32 (RNA) coefficients h = a e^{-j 2 pi r / lambda} (Eq. 3) of
 // one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7 (offset d = m pitch
 // along y), from an fp64 anchor at t0: distance r_c, phase reduced as frac(r_c / lambda)
@@ -816,10 +822,10 @@ __global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos
   uint32_t vr[kTaskE], vi[kTaskE];
   gen_task_tf32(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch, vr, vi);
   float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * K) + 2 * u) * 32 + 8 * (lane & 3);
-  __stcs(reinterpret_cast<uint4 *>(row), make_uint4(vr[0], vr[1], vr[2], vr[3]));
-  __stcs(reinterpret_cast<uint4 *>(row) + 1, make_uint4(vr[4], vr[5], vr[6], vr[7]));
-  __stcs(reinterpret_cast<uint4 *>(row + 32), make_uint4(vi[0], vi[1], vi[2], vi[3]));
-  __stcs(reinterpret_cast<uint4 *>(row + 32) + 1, make_uint4(vi[4], vi[5], vi[6], vi[7]));
+  // one 256-bit streaming store per plane and lane: every warp store fills whole
+  // 32-byte sectors (two 128-bit stores left half-sector gaps per instruction)
+  st_cs_v8(row, vr);
+  st_cs_v8(row + 32, vi);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
