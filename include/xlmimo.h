@@ -106,7 +106,9 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  * 64 users below K = 128 and from K = 128 on as a chunked Hermitian rank-k update
  * (H formed in the workspace a chunk of elements at a time, <= 64 MB so it stays in
  * L2, never whole); fp32 on tcgen05 in blocks of 64 users (a UPA needing rows that are
- * a multiple of 8).  ws may be NULL iff the query returns 0.
+ * a multiple of 8), the operands generated in-kernel below K = 128 and from K = 128 on
+ * read by TMA from TF32 chunks of H formed in the workspace (<= 48 MB, never whole).
+ * ws may be NULL iff the query returns 0.
  * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 materialised (or fp32 on
  * an unsupported UPA), or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
 XLMIMO_API size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops,

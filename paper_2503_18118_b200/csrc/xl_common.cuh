@@ -300,7 +300,10 @@ int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_dr
 int fused_tc_pair_chunks(int64_t N);
 bool materialise_tc_supported(const ArrayP &a);
 int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
-                            int nb, float *H, cudaStream_t s);
+                            int nb, float *H, cudaStream_t s, int Kr = 0, int64_t t_first = 0, int l2_keep = 0);
+size_t stream_pair_h_bytes(int K, int64_t n_drops, int64_t N);
+int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                          float *H, cudaStream_t s);
 
 // xl_closed.cu : out[drop][lvl][K][K][2] for M = n_list[lvl]
 int launch_closed_form(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *m_list,

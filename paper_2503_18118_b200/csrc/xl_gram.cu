@@ -1422,6 +1422,16 @@ int blk_pairs(int K) {
 // K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) from kSyrkMinK users on, the
 // block-pair kernel below it; XLMIMO_LARGE_K=blk|syrk overrides (A/B tests).
 constexpr int kSyrkMinK = 128;
+// K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
+// kStreamPairMinK users on (generation once per coefficient instead of once per pair),
+// generated in-kernel below; XLMIMO_PAIR=gen|stream overrides.
+constexpr int kStreamPairMinK = 128;
+bool use_stream_pair(int K) {
+  static const char *e = getenv("XLMIMO_PAIR");
+  if (e && !strcmp(e, "gen")) return false;
+  if (e && !strcmp(e, "stream")) return true;
+  return K >= kStreamPairMinK;
+}
 bool use_gram_syrk(int K) {
   static const char *e = getenv("XLMIMO_LARGE_K");
   if (e && !strcmp(e, "blk")) return false;
@@ -1579,8 +1589,10 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
-  if (K > xl::kMaxK && precision == XLMIMO_FP32 && N >= kTcMinN)  // fused tcgen05 block pairs
-    return (size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double);
+  if (K > xl::kMaxK && precision == XLMIMO_FP32 && N >= kTcMinN) {  // tcgen05 block pairs
+    const size_t part = ((size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double) + 255) / 256 * 256;
+    return part + (use_stream_pair(K) && n_drops > 0 ? stream_pair_h_bytes(K, n_drops, N) : 0);
+  }
   if (K > xl::kMaxK && use_gram_syrk(K)) return gram_syrk_ws_bytes(K, n_drops, n_lvl);
   if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
@@ -1730,7 +1742,12 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       const size_t need = gram_ws_bytes(a, K, n_drops, 1, precision, mode);
       if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
       int rc;
-      {
+      if (use_stream_pair(K)) {  // times and counts its own launches
+        const size_t part =
+            ((size_t)n_drops * fused_tc_pair_chunks(N) * ((size_t)K * (K + 1) / 2) * 2 * sizeof(double) + 255) /
+            256 * 256;
+        rc = launch_stream_tc_pair(a, pos, K, n_drops, N, (double *)ws, (float *)((char *)ws + part), s);
+      } else {
         KTimer tm(s, "gram_fused_tc_pair_tf32");
         rc = launch_fused_tc_pair(a, pos, K, n_drops, N, (double *)ws, s);
         tm.stop(s);

@@ -314,8 +314,13 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) { return (uint32_t)(
 
 constexpr int kTaskE = 8;          // elements per generator task (one fp64 anchor)
 
-__device__ __forceinline__ void st_cs_v8(float *p, const uint32_t (&v)[8]) {  // 32-B aligned
+__device__ __forceinline__ void st_cs_v8(float *p, const uint32_t (&v)[8]) {  // 32-B aligned, evict-first
   asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void st_v8(float *p, const uint32_t (&v)[8]) {  // 32-B aligned, default (L2-resident)
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
@@ -805,27 +810,201 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
 // (user u = lane / 4, elements 8 (lane % 4) .. +7), so each lane stores 2 x 32 B and a
 // warp writes sixteen full 128-B rows.  Block = 8 warps = 8 consecutive tiles; grid =
 // (ceil(N_pad / 256), batch drops x ceil(K / 8) user groups).  Elements past N are 0.
-__global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos, int K, int kind, int64_t N,
-                                                               int64_t n_pad, int64_t n_y, int64_t n_z, double pitch,
-                                                               double lambda, double sqrt_beta0, int64_t drop0,
-                                                               int n_ugrp, float *H) {
+__global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos, int K, int Kr, int kind, int64_t N,
+                                                               int64_t t_first, int64_t n_pad, int64_t n_y,
+                                                               int64_t n_z, double pitch, double lambda,
+                                                               double sqrt_beta0, int64_t drop0, int n_ugrp, float *H,
+                                                               int l2_keep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bd = blockIdx.y / n_ugrp, ug = blockIdx.y - bd * n_ugrp;
   const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
   if (tile * 32 >= n_pad) return;
   const int u = 8 * ug + (lane >> 2);
-  if (u >= K) return;
-  const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
-  const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
-  const int64_t t0 = tile * 32 + 8 * (lane & 3);
-  const double inv_lambda = 1.0 / lambda;
+  if (u >= Kr) return;
+  float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * Kr) + 2 * u) * 32 + 8 * (lane & 3);
   uint32_t vr[kTaskE], vi[kTaskE];
-  gen_task_tf32(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch, vr, vi);
-  float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * K) + 2 * u) * 32 + 8 * (lane & 3);
-  // one 256-bit streaming store per plane and lane: every warp store fills whole
-  // 32-byte sectors (two 128-bit stores left half-sector gaps per instruction)
-  st_cs_v8(row, vr);
-  st_cs_v8(row + 32, vi);
+  if (u < K) {
+    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
+    const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
+    const int64_t t0 = t_first + tile * 32 + 8 * (lane & 3);
+    const double inv_lambda = 1.0 / lambda;
+    gen_task_tf32(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch, vr, vi);
+  } else {  // padded user row (the pair stream reads whole 64-user blocks)
+#pragma unroll
+    for (int m = 0; m < kTaskE; ++m) vr[m] = vi[m] = 0u;
+  }
+  // one 256-bit store per plane and lane: every warp store fills whole 32-byte sectors
+  // (two 128-bit stores left half-sector gaps per instruction); evict-first for the
+  // HBM stream, default for an L2-sized chunk that is read back at once (the pair stream)
+  if (l2_keep) {
+    st_v8(row, vr);
+    st_v8(row + 32, vi);
+  } else {
+    st_cs_v8(row, vr);
+    st_cs_v8(row + 32, vi);
+  }
+}
+
+// K > 64 fp32 from a materialised chunk: the pair kernel's MMA and epilogue, fed by TMA
+// from the tiled32 H of a unit of B drops x C element chunks (kPChunk each, L2-sized)
+// instead of regenerating both 64-user blocks per pair.  tile index in the unit =
+// (b * C + c) * (kPChunk / 32) + kb; rows of block b: [128 b, 128 b + 128).
+struct StreamPairParams {
+  double *ws;        // partials [drop][chunk][NP][2]
+  int K, nb, n_pairs;
+  int64_t N;
+  int64_t drop0;     // first drop of the unit
+  int n_ud, n_uc;    // drops and chunks in the unit
+  int c0;            // first chunk of the unit
+  int n_chunks;      // chunks per drop (partials layout)
+};
+
+__global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                      StreamPairParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *stages = base;
+  uint64_t *full = (uint64_t *)(base + kPSlots * kPSlotBytes);
+  uint64_t *empty = full + kPSlots;
+  uint64_t *tfull = empty + kPSlots;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = P.K;
+  const int64_t per_drop = (int64_t)P.n_pairs * P.n_uc;
+  const int64_t n_items = (int64_t)P.n_ud * per_drop;
+  if (tid == 0) {
+    for (int s = 0; s < kPSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_sh;
+  constexpr int kTilesPerChunk = kPChunk / kBoxK;
+  auto decode = [&](int64_t it, int &bl, int &bi, int &bj, int &cl) {
+    bl = (int)(it / per_drop);
+    const int rem = (int)(it - (int64_t)bl * per_drop);
+    const int pair = rem / P.n_uc;
+    cl = rem - pair * P.n_uc;
+    pair_of(pair, P.nb, bi, bj);
+  };
+  auto n_stages = [&](int cl) {
+    const int64_t x0 = (int64_t)(P.c0 + cl) * kPChunk, rem = P.N - x0;
+    return (int)(((rem < kPChunk ? rem : kPChunk) + kBoxK - 1) / kBoxK);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int bl, bi, bj, cl;
+        decode(it, bl, bi, bj, cl);
+        const bool diag = bi == bj;
+        const int ns = n_stages(cl);
+        const int tile0 = (bl * P.n_uc + cl) * kTilesPerChunk;
+        for (int kb = 0; kb < ns; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], (uint32_t)((diag ? 1 : 2) * kStageBytes));
+          uint8_t *dst = stages + stage * kPSlotBytes;
+          tma_load_3d(&tmap, dst, &full[stage], 0, kRows * bi, tile0 + kb);
+          if (!diag) tma_load_3d(&tmap, dst + kStageBytes, &full[stage], 0, kRows * bj, tile0 + kb);
+          if (++stage == kPSlots) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = tf32_idesc(kRows, kRows);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+        int bl, bi, bj, cl;
+        decode(it, bl, bi, bj, cl);
+        const bool diag = bi == bj;
+        const int ns = n_stages(cl);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * kRows);
+        for (int kb = 0; kb < ns; ++kb) {
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(stages + stage * kPSlotBytes);
+          const uint32_t sb = diag ? sa : sa + kStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBoxK / 8; ++kk)
+            mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+          if (++stage == kPSlots) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue, warps 4..7 = TMEM lane quadrants
+    const int q = warp - 4;
+    const int row = 32 * q + lane;
+    const int il = row >> 1, plane = row & 1;
+    const int64_t NP = (int64_t)K * (K + 1) / 2;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      int bl, bi, bj, cl;
+      decode(it, bl, bi, bj, cl);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double *out = P.ws + ((size_t)(P.drop0 + bl) * P.n_chunks + (P.c0 + cl)) * (size_t)(2 * NP);
+      const int i = bi * kPUsers + il;
+      for (int cb = 0; cb < kRows / 32; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kRows + 32 * cb), v);
+        float x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int jj = plane * 8 + h;
+          const int jl = 16 * cb + jj;
+          const int j = bj * kPUsers + jl;
+          float rr, rr2, ri, ir;
+          if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
+          else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
+          if (i < K && j < K && j >= i) {
+            const int64_t pp = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
+            out[2 * pp] = (double)rr + (double)rr2;
+            out[2 * pp + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -895,15 +1074,103 @@ int stream_tc_parts(int K) { return kRows / rows_per_block(K); }
 bool materialise_tc_supported(const ArrayP &a) { return a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0; }
 
 int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
-                            int nb, float *H, cudaStream_t s) {
-  const int n_ugrp = (K + 7) / 8;
+                            int nb, float *H, cudaStream_t s, int Kr, int64_t t_first, int l2_keep) {
+  if (Kr < K) Kr = K;
+  const int n_ugrp = (Kr + 7) / 8;
   const dim3 grid((unsigned)((n_pad + 255) / 256), (unsigned)(nb * n_ugrp));
-  h_materialise_tc_kernel<<<grid, 256, 0, s>>>(pos, K, a.kind, N, n_pad, a.n_y, a.kind == XLMIMO_ULA ? 1 : a.n_z,
-                                               a.pitch, a.lambda, a.sqrt_beta0, drop0, n_ugrp, H);
+  h_materialise_tc_kernel<<<grid, 256, 0, s>>>(pos, K, Kr, a.kind, N, t_first, n_pad, a.n_y,
+                                               a.kind == XLMIMO_ULA ? 1 : a.n_z, a.pitch, a.lambda, a.sqrt_beta0,
+                                               drop0, n_ugrp, H, l2_keep);
   return check_launch("h_materialise_tc_kernel");
 }
 
 int fused_tc_pair_chunks(int64_t N) { return (int)((N + kPChunk - 1) / kPChunk); }
+
+// K > 64 fp32 from materialised chunks (gram_stream_tc_pair_kernel): units of B drops x
+// C chunks with H (TF32, users padded to 64 nb) <= 48 MB so the pair reads hit L2.
+struct PairUnit {
+  int B, C;
+  int Kp;
+};
+PairUnit stream_pair_unit(int K, int64_t n_drops, int64_t N) {
+  PairUnit u;
+  const int nb = (K + kPUsers - 1) / kPUsers;
+  u.Kp = nb * kPUsers;
+  const int64_t per = (int64_t)kPChunk * 2 * u.Kp * 4;  // one drop-chunk of H
+  const int64_t cap = 48ll << 20;
+  int64_t cells = cap / per;
+  if (cells < 1) cells = 1;
+  const int64_t chunks = fused_tc_pair_chunks(N);
+  u.C = (int)(cells < chunks ? cells : chunks);
+  int64_t b = cells / u.C;
+  if (b > n_drops) b = n_drops;
+  u.B = (int)(b < 1 ? 1 : b);
+  return u;
+}
+size_t stream_pair_h_bytes(int K, int64_t n_drops, int64_t N) {
+  const PairUnit u = stream_pair_unit(K, n_drops, N);
+  return (size_t)u.B * u.C * kPChunk * 2 * u.Kp * 4;
+}
+
+int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
+                          float *H, cudaStream_t s) {
+  auto enc = encode_fn();
+  if (!enc) return set_error(XLMIMO_ECUDA, "stream_tc_pair: cuTensorMapEncodeTiled unavailable");
+  const PairUnit u = stream_pair_unit(K, n_drops, N);
+  const int nbk = u.Kp / kPUsers;
+  const int chunks = fused_tc_pair_chunks(N);
+  StreamPairParams P;
+  P.ws = ws;
+  P.K = K;
+  P.nb = nbk;
+  P.n_pairs = nbk * (nbk + 1) / 2;
+  P.N = N;
+  P.n_chunks = chunks;
+  const size_t smem = 1024 + (size_t)kPSlots * kPSlotBytes + (2 * kPSlots + 4) * 8 + 16;
+  cudaFuncSetAttribute(gram_stream_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int64_t d0 = 0; d0 < n_drops; d0 += u.B) {
+    const int nd = (int)((n_drops - d0) < u.B ? (n_drops - d0) : u.B);
+    for (int c0 = 0; c0 < chunks; c0 += u.C) {
+      const int ncu = (chunks - c0) < u.C ? chunks - c0 : u.C;
+      const int64_t n_pad = (int64_t)ncu * kPChunk;
+      int rc;
+      {
+        KTimer tm(s, "h_materialise");
+        rc = launch_h_materialise_tc(a, pos, K, N, n_pad, d0, nd, H, s, u.Kp, (int64_t)c0 * kPChunk, 1);
+        tm.stop(s);
+        count_launch();
+      }
+      if (rc) return rc;
+      CUtensorMap map;
+      const cuuint64_t gdim[3] = {(cuuint64_t)kBoxK, (cuuint64_t)(2 * u.Kp), (cuuint64_t)nd * (n_pad / kBoxK)};
+      const cuuint64_t gstride[2] = {(cuuint64_t)kBoxK * 4, (cuuint64_t)kBoxK * 4 * 2 * u.Kp};
+      const cuuint32_t box[3] = {(cuuint32_t)kBoxK, (cuuint32_t)kRows, 1};
+      const cuuint32_t estride[3] = {1, 1, 1};
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)H, gdim, gstride, box, estride,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return set_error(XLMIMO_ECUDA, "stream_tc_pair: tensor map encode failed (%d)", (int)r);
+      P.drop0 = d0;
+      P.n_ud = nd;
+      P.n_uc = ncu;
+      P.c0 = c0;
+      const int64_t items = (int64_t)nd * P.n_pairs * ncu;
+      const int grid = (int)(items < sms ? items : sms);
+      {
+        KTimer tm(s, "gram_stream_tc_pair_tf32");
+        gram_stream_tc_pair_kernel<<<grid, 256, smem, s>>>(map, P);
+        tm.stop(s);
+        count_launch();
+      }
+      rc = check_launch("gram_stream_tc_pair_kernel");
+      if (rc) return rc;
+    }
+  }
+  return XLMIMO_OK;
+}
 
 // K > 64 fused fp32: partials [drop][chunk][K(K+1)/2][2] into ws (fused_tc_pair_chunks(N) per drop).
 int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
