@@ -53,7 +53,8 @@ def _ws(nbytes):
                                                 (100, 333, 0, 0, "ula"), (200, 129, 0, 0, "ula"),
                                                 (5, 513, 1, 0, "ula"), (16, 4099, 1, 0, "ula"), (40, 1030, 1, 0, "ula"),
                                                 (16, 4096, 1, 1, "ula"), (5, 1001, 1, 1, "ula"), (12, 300, 0, 0, "upa"),
-                                                (12, 300, 1, 0, "upa"), (70, 300, 0, 0, "upa")])
+                                                (12, 300, 1, 0, "upa"), (70, 300, 0, 0, "upa"),
+                                                (130, 1100, 1, 0, "ula"), (150, 1030, 0, 0, "ula")])
 def test_gram_exact_writes_in_bounds(xl, K, N, prec, mode, kind):
     D = 3
     if kind == "ula":
