@@ -41,38 +41,37 @@ __device__ __forceinline__ void ctile_zero(CTile &c) {
 // one k-step (4 columns of A / rows of B): a[mb] = A(8 mb + lane/4, 4 kb + lane%4),
 // b[nb] = B(4 kb + lane%4, 8 nb + lane/4);  C += A B, or C += A conj(B) with CONJ_B:
 // Re += ar br -+ ai bi, Im += ai br +- ar bi (one sign flip per fragment of A)
-template <bool CONJ_B>
+template <bool CONJ_B, int MB = 4, int NB = 4>
 __device__ __forceinline__ void ctile_step(CTile &c, const double2 (&a)[4], const double2 (&b)[4]) {
-  // the two DMMAs into one accumulator are 32 instructions apart
+  // the two DMMAs into one accumulator are 2 MB NB instructions apart; only the first
+  // MB row / NB column fragments (trimmed tiles at the ragged edge of K)
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb)
+  for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = 0; nb < NB; ++nb) {
       dmma_f64(c.r[mb][nb], a[mb].x, b[nb].x);
       dmma_f64(c.i[mb][nb], a[mb].y, b[nb].x);
     }
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb) {
+  for (int mb = 0; mb < MB; ++mb) {
     const double n = CONJ_B ? negd(a[mb].x) : negd(a[mb].y);
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = 0; nb < NB; ++nb) {
       dmma_f64(c.r[mb][nb], CONJ_B ? a[mb].y : n, b[nb].y);
       dmma_f64(c.i[mb][nb], CONJ_B ? n : a[mb].x, b[nb].y);
     }
   }
 }
-template <bool B_NT>
+template <bool B_NT, int MB = 4, int NB = 4>
 __device__ __forceinline__ void frag_load(double2 (&a)[4], double2 (&b)[4], const double2 *__restrict__ Am, size_t lda,
                                           const double2 *__restrict__ Bm, size_t ldb, int kb, int lane) {
   const int qr = lane >> 2, qc = lane & 3;
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb) a[mb] = Am[(size_t)(8 * mb + qr) * lda + 4 * kb + qc];
+  for (int mb = 0; mb < MB; ++mb) a[mb] = Am[(size_t)(8 * mb + qr) * lda + 4 * kb + qc];
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb)
+  for (int nb = 0; nb < NB; ++nb)
     b[nb] = B_NT ? Bm[(size_t)(8 * nb + qr) * ldb + 4 * kb + qc] : Bm[(size_t)(4 * kb + qc) * ldb + 8 * nb + qr];
 }
-// L2 prefetch of the operand lines of k-steps q, q + 1 (q even): A row lane, 128 B; B the
-// same (B_NT) or rows 4q .. 4q + 7 (row-major B, 32-wide)
 template <bool B_NT>
 __device__ __forceinline__ void frag_prefetch_l2(const double2 *Am, size_t lda, const double2 *Bm, size_t ldb, int q,
                                                  int lane) {
@@ -85,24 +84,23 @@ __device__ __forceinline__ void frag_prefetch_l2(const double2 *Am, size_t lda, 
 // fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run, and (PF, operands in
 // global memory) the lines of k-step kb + kPfDist are pulled into L2 meanwhile.
 constexpr int kPfDist = 8;
-template <bool B_NT, bool CONJ_B, bool PF>
+template <bool B_NT, bool CONJ_B, bool PF, int MB = 4, int NB = 4>
 __device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ Am, size_t lda,
                                           const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
   if (PF)
     for (int q = 0; q < kPfDist && q < nkb; q += 2) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, q, lane);
   double2 a[4], b[4];
-  frag_load<B_NT>(a, b, Am, lda, Bm, ldb, 0, lane);
+  frag_load<B_NT, MB, NB>(a, b, Am, lda, Bm, ldb, 0, lane);
 #pragma unroll 1
   for (int kb = 0; kb < nkb; ++kb) {
     if (PF && !(kb & 1) && kb + kPfDist < nkb) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, kb + kPfDist, lane);
     double2 an[4], bn[4];
-    frag_load<B_NT>(an, bn, Am, lda, Bm, ldb, kb + 1 < nkb ? kb + 1 : kb, lane);
-    ctile_step<CONJ_B>(c, a, b);
+    frag_load<B_NT, MB, NB>(an, bn, Am, lda, Bm, ldb, kb + 1 < nkb ? kb + 1 : kb, lane);
+    ctile_step<CONJ_B, MB, NB>(c, a, b);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      a[q] = an[q];
-      b[q] = bn[q];
-    }
+    for (int q = 0; q < MB; ++q) a[q] = an[q];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) b[q] = bn[q];
   }
 }
 // pull a 32 x 32 complex tile (32 rows of 512 B) into L2 ahead of its use
@@ -111,13 +109,13 @@ __device__ __forceinline__ void tile_prefetch_l2(const double2 *src, size_t ld, 
 #pragma unroll
   for (int q = 0; q < 4; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * q));
 }
-template <bool NEG>
+template <bool NEG, int MB = 4, int NB = 4>
 __device__ __forceinline__ void ctile_load(CTile &c, const double2 *src, size_t ld, int lane) {
   const int qr = lane >> 2, qc = lane & 3;
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb)
+  for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = 0; nb < NB; ++nb) {
       const double2 *p = src + (size_t)(8 * mb + qr) * ld + 8 * nb + 2 * qc;
       const double2 v0 = p[0], v1 = p[1];
       c.r[mb][nb][0] = NEG ? -v0.x : v0.x;
@@ -126,13 +124,13 @@ __device__ __forceinline__ void ctile_load(CTile &c, const double2 *src, size_t 
       c.i[mb][nb][1] = NEG ? -v1.y : v1.y;
     }
 }
-template <bool NEG>
+template <bool NEG, int MB = 4, int NB = 4>
 __device__ __forceinline__ void ctile_store(const CTile &c, double2 *dst, size_t ld, int lane) {
   const int qr = lane >> 2, qc = lane & 3;
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb)
+  for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
+    for (int nb = 0; nb < NB; ++nb) {
       double2 *p = dst + (size_t)(8 * mb + qr) * ld + 8 * nb + 2 * qc;
 #pragma unroll
       for (int e = 0; e < 2; ++e)

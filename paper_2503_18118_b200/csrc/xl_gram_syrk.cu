@@ -15,6 +15,7 @@
 // 64-user blocks of every block pair (17x redundant generation at K = 1000), every
 // coefficient is generated once per drop; the price is the chunk round trip through L2.
 #include <cstring>
+#include <type_traits>
 
 #include "xl_common.cuh"
 #include "xl_dmma_tile.cuh"
@@ -119,8 +120,8 @@ __device__ __forceinline__ void pair_decode(int p, int nt, int &ti, int &tj) {
 // so their A rows coincide.  partial[b][lvl][sub][pair][32][32] (row-major) += H_ti H_tj^H
 // over the chunk's elements [sub CH/nsub, (sub + 1) CH/nsub).
 __global__ void __launch_bounds__(32 * kSyrkWarps, 1)
-    gram_syrk_kernel(const double2 *__restrict__ H, int Kp, int nt, int CH, int nsub, int npairs, int64_t n_items,
-                     int lvl, int n_lvl, double2 *partial) {
+    gram_syrk_kernel(const double2 *__restrict__ H, int K, int Kp, int nt, int CH, int nsub, int npairs,
+                     int64_t n_items, int lvl, int n_lvl, double2 *partial) {
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * kSyrkWarps + (threadIdx.x >> 5);
   if (item >= n_items) return;
@@ -134,10 +135,31 @@ __global__ void __launch_bounds__(32 * kSyrkWarps, 1)
   const double2 *A = H + ((size_t)b * Kp + (size_t)ti * kTile) * CH + (size_t)sub * chs;
   const double2 *Bm = H + ((size_t)b * Kp + (size_t)tj * kTile) * CH + (size_t)sub * chs;
   double2 *pt = partial + ((((size_t)b * n_lvl + lvl) * nsub + sub) * npairs + pair) * (kTile * kTile);
-  CTile c;
-  ctile_load<false>(c, pt, kTile, lane);
-  ctile_mma<true, true, true>(c, A, CH, Bm, CH, chs / 4, lane);
-  ctile_store<false>(c, pt, kTile, lane);
+  // the last tile holds K - 32 (nt - 1) users: only its first v row/column fragments
+  // are computed (8 v >= its users; the rest of the partial stays 0 and is never read)
+  const int v = (K - (nt - 1) * kTile + 7) / 8;
+  const bool lj = tj == nt - 1, li = ti == nt - 1;
+  auto run = [&](auto mb, auto nb) {
+    constexpr int MB = decltype(mb)::value, NB = decltype(nb)::value;
+    CTile c;
+    ctile_load<false, MB, NB>(c, pt, kTile, lane);
+    ctile_mma<true, true, true, MB, NB>(c, A, CH, Bm, CH, chs / 4, lane);
+    ctile_store<false, MB, NB>(c, pt, kTile, lane);
+  };
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using I4 = std::integral_constant<int, 4>;
+  if (!lj || v == 4) run(I4{}, I4{});
+  else if (!li) {
+    if (v == 1) run(I4{}, I1{});
+    else if (v == 2) run(I4{}, I2{});
+    else run(I4{}, I3{});
+  } else {
+    if (v == 1) run(I1{}, I1{});
+    else if (v == 2) run(I2{}, I2{});
+    else run(I3{}, I3{});
+  }
 }
 
 // block (b, row i): threads over j >= i
@@ -222,7 +244,7 @@ int launch_gram_syrk(const ArrayP &a, const double *pos, int K, int64_t n_drops,
           KTimer tm(s, "gram_syrk_dmma_fp64");
           const int64_t n_items = (int64_t)nb * p.nsub * p.npairs;
           gram_syrk_kernel<<<(unsigned)((n_items + kSyrkWarps - 1) / kSyrkWarps), 32 * kSyrkWarps, 0, s>>>(
-              H, p.Kp, p.nt, p.CH, p.nsub, p.npairs, n_items, l, n_lvl, partial);
+              H, K, p.Kp, p.nt, p.CH, p.nsub, p.npairs, n_items, l, n_lvl, partial);
           tm.stop(s);
           count_launch();
         }
