@@ -7,7 +7,9 @@ capacity-vs-N saturation sweep -- ULA N = 2^8..2^16, 28 GHz, K = 8 users,
 r ~ U[3, 30] m, az ~ U[-60, 60] deg, SNR 0/10/20 dB, 10^4 seeded drops, fp64,
 CAP + ZF + MMSE.  One step = the whole hot path on one batch: draw the drops
 (a1), fused exact Gram with nested-N snapshots (a2+a3), per-(drop, N) receivers
-(a5), ergodic means + saturation statistics (a6), result to host.  Each step
+(a5), ergodic means + saturation statistics (a6), and the same sweep on the same drops
+through the closed-form ("modified ZF") Gram (a4: Eqs. (4)/(6)/(22)/(23)), results to
+host.  Each step
 uses a fresh seed (new drops), and a 256 MiB buffer is written between steps to
 flush L2 (126 MB).  N > 1 (torchrun): weak scaling, each rank its own 10^4
 drops (first_drop = rank * 10^4) and a per-step NCCL all-reduce of the ergodic
@@ -145,6 +147,7 @@ def oracle_sample(n_drops_sample: int, seed: int, nthreads: int = 0):
     a = oracle.array("ula", n_y=W.n_y, fc_hz=W.fc_hz)
     t0 = time.perf_counter()
     oracle.saturation_sweep(a, W.n_list, pos, W.snr_db, W.receivers, t=W.t, nthreads=nthreads)
+    oracle.saturation_sweep(a, W.n_list, pos, W.snr_db, W.receivers, gram_kind=1, t=W.t, nthreads=nthreads)
     return time.perf_counter() - t0
 
 
@@ -165,7 +168,8 @@ def cpu_baseline(target_s: float):
     t = oracle_sample(n, seed=1000)
     value = cmac_per_drop(W) * n / t
     return {"value": value, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} drops of cfg2 (all 9 N, 3 SNR, CAP+ZF+MMSE; oracle computes every N independently), "
+            "sample": f"{n} drops of cfg2 (all 9 N, 3 SNR, CAP+ZF+MMSE, exact and closed-form sweeps; the oracle "
+                      f"computes every N independently), "
                       f"{t:.1f} s wall on {cores} OpenMP threads",
             "drops_per_s": n / t}
 
@@ -191,6 +195,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": W.name, "n_drops_per_step": n_step, "K": W.K, "n_list": list(W.n_list),
+                       "step": "drops + exact fp64 sweep + closed-form sweep on the same drops",
                        "snr_db": list(W.snr_db), "fc_hz": W.fc_hz},
             "cpu_baseline": {"value": value, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
                              "sample": f"{n_step} drops per step (of the 10^4-drop workload)"},
@@ -229,8 +234,10 @@ def run_ours(args):
     users = xl.Users.polar(W.r, W.az)
     snr = list(W.snr_db)
     R = xl.n_recv(W.receivers)
-    ws = torch.empty(xl.sweep_workspace_bytes(arr, W.n_list, W.K, D, len(snr), W.receivers), dtype=torch.uint8,
-                     device=dev)
+    ws_bytes = max(xl.sweep_workspace_bytes(arr, W.n_list, W.K, D, len(snr), W.receivers),
+                   xl.sweep_workspace_bytes(arr, W.n_list, W.K, D, len(snr), W.receivers,
+                                            gram_kind=xl.GRAM_CLOSED_FORM))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # the two sweeps run in turn on one stream
     pos = torch.empty((D, W.K, 3), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -239,9 +246,13 @@ def run_ours(args):
         flush.fill_(k & 0xFF)                                      # L2 flush between steps
         xl.gen_drops(users, W.K, D, seed=1000 + k, first_drop=rank * D, out=pos)
         res = xl.saturation_sweep(arr, W.n_list, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws)
+        res_cf = xl.saturation_sweep(arr, W.n_list, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws,
+                                     gram_kind=xl.GRAM_CLOSED_FORM)
         if dist:
-            parallel.allreduce_sweep(res, D, dist, dev, pitch=0.5 * 299792458.0 / W.fc_hz)
-        return res
+            pitch = 0.5 * 299792458.0 / W.fc_hz
+            res = parallel.allreduce_sweep(res, D, dist, dev, pitch=pitch)
+            res_cf = parallel.allreduce_sweep(res_cf, D, dist, dev, pitch=pitch)
+        return res, res_cf
 
     for k in range(args.warmup):
         step(k)
@@ -260,7 +271,7 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):
-        step(args.warmup + k)
+        res, res_cf = step(args.warmup + k)
     e1.record(stream)
     torch.cuda.synchronize()
     xl._L.xlmimo_timing_enable(0)
@@ -276,8 +287,14 @@ def run_ours(args):
     # ---- e2e: the host-buffer C-ABI entry, H2D of positions + D2H of the result every step
     pos_host = torch.empty((D, W.K, 3), dtype=torch.float64).pin_memory()
     pos_host.copy_(xl.gen_drops(users, W.K, D, seed=77, first_drop=rank * D).cpu())
+    def step_host():
+        r = xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws)
+        xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws,
+                                 gram_kind=xl.GRAM_CLOSED_FORM)
+        return r
+
     for _ in range(max(1, args.warmup)):
-        xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws)
+        step_host()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -287,7 +304,7 @@ def run_ours(args):
     f0.record(stream)
     for k in range(args.steps):
         flush.fill_(k & 0xFF)
-        res = xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws)
+        step_host()
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1)
@@ -297,9 +314,9 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = D * W.K * 3 * 8
+    h2d = 2 * D * W.K * 3 * 8  # positions, once per sweep (exact, closed form)
     n_out = len(W.n_list) * len(snr) * R
-    d2h = n_out * 8 + n_out * 8 + 4 * 8
+    d2h = 2 * (n_out * 8 + n_out * 8 + 4 * 8)
 
     # ---- roofline of the dominant kernel (fused fp64 Gram, FP64 pipe bound)
     cmac_step = cmac_per_drop(W) * D            # per rank
@@ -329,6 +346,7 @@ def run_ours(args):
                "config": {"workload": W.name, "n_drops_per_rank": D, "K": W.K, "n_list": list(W.n_list),
                           "snr_db": snr, "fc_hz": W.fc_hz, "receivers": "CAP+ZF+MMSE", "precision": "fp64",
                           "cmac_per_drop": cmac_per_drop(W), "l2": "flushed between steps (256 MiB write)",
+                          "step": "drops + exact fp64 sweep + closed-form sweep on the same drops",
                           "parallelism": f"dp{world} (drops)"},
                "drops_per_s": D * world * args.steps / (t_ms * 1e-3),
                "e2e": {"value": cmac_step * world * args.steps / (e2e_ms * 1e-3), "unit": "cMAC/s",
@@ -338,7 +356,9 @@ def run_ours(args):
                "sat_M": float(res["sat"][2]),
                "run": {"gpu": torch.cuda.get_device_name(dev), "seeds": f"1000 + step (drops of rank r from {D} r)",
                        "nan_rates_last_step": int(np.asarray(res["n_valid"]).size * D * world
-                                                  - int(np.asarray(res["n_valid"]).sum()))}}
+                                                  - int(np.asarray(res["n_valid"]).sum())),
+                       "closed_form_nan_rates_last_step": int(np.asarray(res_cf["n_valid"]).size * D * world
+                                                              - int(np.asarray(res_cf["n_valid"]).sum()))}}
     if dist:
         dist.barrier()
         dist.destroy_process_group()
