@@ -415,6 +415,29 @@ def test_sweep_full_cfg2_every_drop_vs_oracle(xl, orc):
     assert res["sat"][2] == sat[2]
 
 
+def test_sweep_cfg2_closed_form_every_drop_vs_oracle(xl, orc):
+    """The closed-form half of the bench step (a4: the modified-ZF Gram of Eqs. (4)/(6)/
+    (22)/(23) for every N of the sweep) on all 10^4 cfg2 drops: per-drop rates within
+    1e-6 bits/s/Hz, the same flagged (NaN) receivers -- far below saturation the
+    closed-form Gram is indefinite (R10) -- identical valid counts, ergodic means within
+    1e-6."""
+    w = CONFIGS[2]
+    ag = xl.Array.ula(w.n_y, w.fc_hz)
+    ug = xl.Users.polar(w.r, w.az)
+    pos_d = xl.gen_drops(ug, w.K, w.n_drops, seed=w.seed)
+    res = xl.saturation_sweep(ag, w.n_list, w.K, w.n_drops, w.snr_db, w.receivers, pos=pos_d,
+                              gram_kind=xl.GRAM_CLOSED_FORM, per_drop=True)
+    erg, nv, _, pdo = orc.saturation_sweep(orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz), w.n_list,
+                                           pos_d.cpu().numpy(), w.snr_db, w.receivers, gram_kind=1, per_drop=True)
+    pd = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(pd), np.isnan(pdo))
+    assert np.isnan(pdo).any() and (~np.isnan(pdo)).any()
+    ok = ~np.isnan(pdo)
+    assert np.max(np.abs(pd[ok] - pdo[ok])) <= 1e-6
+    assert np.array_equal(res["n_valid"], nv)
+    assert np.nanmax(np.abs(res["ergodic"] - erg)) <= 1e-6
+
+
 @pytest.mark.parametrize("prec", ["fp32", "mat32"])
 def test_gram_fp32_user_close_to_the_array(xl, orc, prec):
     """Users 0.3-0.6 m from a 100 GHz ULA (x well below the configs' 0.52 m minimum): the
