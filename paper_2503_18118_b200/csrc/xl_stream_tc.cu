@@ -349,7 +349,15 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
   if (kind == XLMIMO_ULA) {
     ey = ((double)t0 - 0.5 * (double)(N - 1)) * pitch;
   } else {
-    const int64_t q = t0 / n_y, pp = t0 - q * n_y;
+    int64_t q, pp;
+    if (t0 < ((int64_t)1 << 31)) {  // 32-bit division (a 64-bit one is a long software sequence)
+      const uint32_t q32 = (uint32_t)t0 / (uint32_t)n_y;
+      q = q32;
+      pp = (int64_t)((uint32_t)t0 - q32 * (uint32_t)n_y);
+    } else {
+      q = t0 / n_y;
+      pp = t0 - q * n_y;
+    }
     ey = ((double)pp - 0.5 * (double)(n_y - 1)) * pitch;
     ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
   }
