@@ -101,16 +101,19 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  *   mode XLMIMO_FUSED: H is never materialised.  XLMIMO_MATERIALIZED: H is
  *     written to the workspace as planar complex64 and streamed back (fp32 only).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
- * Im G(i,i) = 0.  K <= 1024: K <= 64 on every precision/mode; 64 < K <= 1024 fused
- * only -- NEXT-3/E1-E3 user counts: fp64 on DMMA, in blocks of
- * 64 users below K = 128 and from K = 128 on as a chunked Hermitian rank-k update
- * (H formed in the workspace a chunk of elements at a time, <= 64 MB so it stays in
- * L2, never whole); fp32 on tcgen05 in blocks of 64 users (a UPA needing rows that are
- * a multiple of 8), the operands generated in-kernel below K = 128 and from K = 128 on
- * read by TMA from TF32 chunks of H formed in the workspace (<= 48 MB, never whole).
+ * Im G(i,i) = 0.  K <= 1024 -- 64 < K <= 1024 are the NEXT-3/E1-E3 user counts,
+ * fp64 on DMMA, in blocks of 64 users below K = 128 and from
+ * K = 128 on as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
+ * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
+ * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
+ * operands generated in-kernel below K = 128 and, from K = 128 on or in MATERIALIZED
+ * mode, read by TMA from complex64 (TF32) chunks of H written to the workspace
+ * (<= 112 MB per unit of drops x 4096-element chunks).  Below 1024 elements an fp32
+ * request with K > 64 runs the fp64 kernels (TF32 rounding would not average out).
  * ws may be NULL iff the query returns 0.
- * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, K > 64 materialised (or fp32 on
- * an unsupported UPA), or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes too small. */
+ * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, fp32 with K > 64 on an
+ * unsupported UPA or with nested levels, or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes
+ * too small. */
 XLMIMO_API size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops,
                                    int32_t precision, int32_t mode);
 XLMIMO_API int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,

@@ -290,7 +290,7 @@ int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t n_drops, ui
 size_t xlmimo_gram_exact_workspace(const xlmimo_array_t *array, int32_t K, int64_t n_drops, int32_t precision,
                                    int32_t mode) {
   if (bad_array(array) || K < 1 || K > xl::kMaxKLarge || n_drops < 0) return 0;
-  if (K > xl::kMaxK && mode != XLMIMO_FUSED) return 0;
+  if (K > xl::kMaxK && mode == XLMIMO_MATERIALIZED && precision != XLMIMO_FP32) return 0;  // unsupported
   return xlh::gram_ws_bytes(to_params(array), K, n_drops, 1, precision, mode);
 }
 

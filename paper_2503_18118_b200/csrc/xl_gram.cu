@@ -1584,17 +1584,20 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
+  if (K > xl::kMaxK) {
+    if (precision == XLMIMO_FP32 && N >= kTcMinN) {  // tcgen05 block pairs (+ H chunks when streamed)
+      const size_t part = ((size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double) + 255) / 256 * 256;
+      const bool stream = use_stream_pair(K) || mode == XLMIMO_MATERIALIZED;
+      return part + (stream && n_drops > 0 ? stream_pair_h_bytes(K, n_drops, N) : 0);
+    }
+    if (use_gram_syrk(K)) return gram_syrk_ws_bytes(K, n_drops, n_lvl);
+    return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
+  }
   if (mode == XLMIMO_MATERIALIZED) {
     const int parts = materialised_use_tc(K, N) ? stream_tc_chunks(N) * stream_tc_parts(K) : n_split;
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
-  if (K > xl::kMaxK && precision == XLMIMO_FP32 && N >= kTcMinN) {  // tcgen05 block pairs
-    const size_t part = ((size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double) + 255) / 256 * 256;
-    return part + (use_stream_pair(K) && n_drops > 0 ? stream_pair_h_bytes(K, n_drops, N) : 0);
-  }
-  if (K > xl::kMaxK && use_gram_syrk(K)) return gram_syrk_ws_bytes(K, n_drops, n_lvl);
-  if (K > xl::kMaxK) return (size_t)n_drops * choose_split_blk(n_drops, K, N) * n_lvl * np * 2 * sizeof(double);
   if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
@@ -1730,8 +1733,9 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s) {
   if (K > xl::kMaxK) {
-    if (mode != XLMIMO_FUSED)
-      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: K=%d > %d is fused only", K, xl::kMaxK);
+    // materialised for K > 64 = the TMA-fed pair stream over complex64 (TF32) chunks of H
+    if (mode == XLMIMO_MATERIALIZED && precision != XLMIMO_FP32)
+      return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: XLMIMO_MATERIALIZED is complex64 (XLMIMO_FP32) only");
     if (n_lvl < 1 || n_lvl > kMaxLvl) return set_error(XLMIMO_EINVAL, "gram: n_lvl=%d out of [1,%d]", n_lvl, kMaxLvl);
     if (precision == XLMIMO_FP32 && lvl_end[n_lvl - 1] >= kTcMinN) {
       if (n_lvl != 1 || !fused_tc_supported_geometry(a))
@@ -1742,7 +1746,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       const size_t need = gram_ws_bytes(a, K, n_drops, 1, precision, mode);
       if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
       int rc;
-      if (use_stream_pair(K)) {  // times and counts its own launches
+      if (use_stream_pair(K) || mode == XLMIMO_MATERIALIZED) {  // times and counts its own launches
         const size_t part =
             ((size_t)n_drops * fused_tc_pair_chunks(N) * ((size_t)K * (K + 1) / 2) * 2 * sizeof(double) + 255) /
             256 * 256;

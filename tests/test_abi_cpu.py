@@ -65,8 +65,8 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     ula = xl.Array.ula(256, 28e9)
     assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 1025, 1, 0, 0, ctypes.c_void_p(8), None, 0,
                                None) == -2
-    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 1, 1, ctypes.c_void_p(8), None, 0,
-                               None) == -2  # K > 64 is fused only
+    assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 0, 1, ctypes.c_void_p(8), None, 0,
+                               None) == -2  # materialised is complex64 (fp32) only
     assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 65, 1, 0, 0, ctypes.c_void_p(8), None, 0,
                                None) == -3  # needs its workspace
     bad = xl.Array.ula(256, -1.0)
@@ -117,7 +117,8 @@ def test_workspace_queries_are_pure(lib):
     w2 = xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 64, 1000, 0, 0)
     assert w1 == w2 > 0
     assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 1025, 1000, 0, 0) == 0
-    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 1, 1) == 0
+    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 0, 1) == 0  # fp64 materialised
+    assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 1, 1) > 0  # fp32 materialised pairs
     assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 1, 0) > 0
     assert xl._L.xlmimo_gram_exact_workspace(ctypes.byref(a), 65, 1000, 0, 0) > 0
 

@@ -60,11 +60,21 @@ def test_gram_large_k_e3_full_size(xl, orc):
     assert int(fl[0]) == 0 and abs(float(rs[0, 1]) - 0.064) < 1e-3
 
 
+def test_gram_large_k_materialised_fp32(xl, orc):
+    """MATERIALIZED at K > 64: the TMA-fed tcgen05 pairs over complex64 (TF32) chunks of H
+    written to the workspace, at a K below the fused path's streaming threshold (fp32
+    tier), across a chunk boundary."""
+    a, ao = xl.Array.ula(5000, 100e9), orc.array("ula", n_y=5000, fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 90, 2, seed=6)
+    G = xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED).cpu().numpy()
+    assert normalized_err(G, orc.gram_exact(ao, pos.cpu().numpy())) <= 1e-4
+
+
 def test_gram_large_k_unsupported_modes(xl):
     a = xl.Array.ula(256, 100e9)
     pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 70, 1, seed=1)
     with pytest.raises(xl.XlmimoError):
-        xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED)
+        xl.gram_exact(a, pos, precision=xl.FP64, mode=xl.MATERIALIZED)
     upa = xl.Array.upa(36, 30, 100e9)  # N >= 1024 (tensor-core tier), rows not a multiple of 8
     with pytest.raises(xl.XlmimoError):
         xl.gram_exact(upa, pos, precision=xl.FP32)
