@@ -857,6 +857,8 @@ __global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos
 // from the tiled32 H of a unit of B drops x C element chunks (kPChunk each, L2-sized)
 // instead of regenerating both 64-user blocks per pair.  tile index in the unit =
 // (b * C + c) * (kPChunk / 32) + kb; rows of block b: [128 b, 128 b + 128).
+constexpr int kSSlots = 4;                       // stream-pair ring: A 16 KB + B 32 KB per stage
+constexpr int kSSlotBytes = 3 * kStageBytes;
 struct StreamPairParams {
   double *ws;        // partials [drop][chunk][NP][2]
   int K, nb, n_pairs;
@@ -872,9 +874,9 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *stages = base;
-  uint64_t *full = (uint64_t *)(base + kPSlots * kPSlotBytes);
-  uint64_t *empty = full + kPSlots;
-  uint64_t *tfull = empty + kPSlots;
+  uint64_t *full = (uint64_t *)(base + kSSlots * kSSlotBytes);
+  uint64_t *empty = full + kSSlots;
+  uint64_t *tfull = empty + kSSlots;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
 
@@ -883,7 +885,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   const int64_t per_drop = (int64_t)P.n_pairs * P.n_uc;
   const int64_t n_items = (int64_t)P.n_ud * per_drop;
   if (tid == 0) {
-    for (int s = 0; s < kPSlots; ++s) {
+    for (int s = 0; s < kSSlots; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -896,7 +898,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
-                 "r"(256)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -905,12 +907,16 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
   constexpr int kTilesPerChunk = kPChunk / kBoxK;
+  // item = (drop, block row bi, column blocks bj, bj + 1 (bj = bi + 2q), chunk): the B
+  // operand is 256 rows (two 64-user blocks; rows past 2 K_pad come in as TMA zero fill)
   auto decode = [&](int64_t it, int &bl, int &bi, int &bj, int &cl) {
     bl = (int)(it / per_drop);
     const int rem = (int)(it - (int64_t)bl * per_drop);
-    const int pair = rem / P.n_uc;
-    cl = rem - pair * P.n_uc;
-    pair_of(pair, P.nb, bi, bj);
+    int w = rem / P.n_uc;
+    cl = rem - w * P.n_uc;
+    bi = 0;
+    while (w >= (P.nb - bi + 1) / 2) { w -= (P.nb - bi + 1) / 2; ++bi; }
+    bj = bi + 2 * w;
   };
   auto n_stages = [&](int cl) {
     const int64_t x0 = (int64_t)(P.c0 + cl) * kPChunk, rem = P.N - x0;
@@ -924,45 +930,44 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         int bl, bi, bj, cl;
         decode(it, bl, bi, bj, cl);
-        const bool diag = bi == bj;
         const int ns = n_stages(cl);
         const int tile0 = (bl * P.n_uc + cl) * kTilesPerChunk;
         for (int kb = 0; kb < ns; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], (uint32_t)((diag ? 1 : 2) * kStageBytes));
-          uint8_t *dst = stages + stage * kPSlotBytes;
+          mbar_expect_tx(&full[stage], (uint32_t)(3 * kStageBytes));
+          uint8_t *dst = stages + stage * kSSlotBytes;
           tma_load_3d(&tmap, dst, &full[stage], 0, kRows * bi, tile0 + kb);
-          if (!diag) tma_load_3d(&tmap, dst + kStageBytes, &full[stage], 0, kRows * bj, tile0 + kb);
-          if (++stage == kPSlots) { stage = 0; phase ^= 1; }
+          tma_load_3d(&tmap, dst + kStageBytes, &full[stage], 0, kRows * bj, tile0 + kb);
+          tma_load_3d(&tmap, dst + 2 * kStageBytes, &full[stage], 0, kRows * (bj + 1), tile0 + kb);
+          if (++stage == kSSlots) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = tf32_idesc(kRows, kRows);
+      const uint32_t idesc = tf32_idesc(kRows, 2 * kRows);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
         int bl, bi, bj, cl;
         decode(it, bl, bi, bj, cl);
-        const bool diag = bi == bj;
         const int ns = n_stages(cl);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tmem_d = tmem + (uint32_t)(acc * kRows);
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * 2 * kRows);
         for (int kb = 0; kb < ns; ++kb) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(stages + stage * kPSlotBytes);
-          const uint32_t sb = diag ? sa : sa + kStageBytes;
+          const uint32_t sa = smem_u32(stages + stage * kSSlotBytes);
+          const uint32_t sb = sa + kStageBytes;  // 256 rows: blocks bj, bj + 1
 #pragma unroll
           for (int kk = 0; kk < kBoxK / 8; ++kk)
             mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&empty[stage]);
-          if (++stage == kPSlots) { stage = 0; phase ^= 1; }
+          if (++stage == kSSlots) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
       }
@@ -982,9 +987,9 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       double *out = P.ws + ((size_t)(P.drop0 + bl) * P.n_chunks + (P.c0 + cl)) * (size_t)(2 * NP);
       const int i = bi * kPUsers + il;
-      for (int cb = 0; cb < kRows / 32; ++cb) {
+      for (int cb = 0; cb < 2 * kRows / 32; ++cb) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kRows + 32 * cb), v);
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 2 * kRows + 32 * cb), v);
         float x[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
@@ -1011,7 +1016,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 
@@ -1131,10 +1136,11 @@ int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_d
   P.ws = ws;
   P.K = K;
   P.nb = nbk;
-  P.n_pairs = nbk * (nbk + 1) / 2;
+  P.n_pairs = 0;  // items per (drop, chunk): block rows x column-block pairs
+  for (int bi = 0; bi < nbk; ++bi) P.n_pairs += (nbk - bi + 1) / 2;
   P.N = N;
   P.n_chunks = chunks;
-  const size_t smem = 1024 + (size_t)kPSlots * kPSlotBytes + (2 * kPSlots + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)kSSlots * kSSlotBytes + (2 * kSSlots + 4) * 8 + 16;
   cudaFuncSetAttribute(gram_stream_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
