@@ -106,7 +106,7 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  * K = 128 on as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
  * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
  * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
- * operands generated in-kernel below K = 128 and, from K = 128 on or in MATERIALIZED
+ * operands generated in-kernel below K = 352 and, from K = 352 on or in MATERIALIZED
  * mode, read by TMA from complex64 (TF32) chunks of H written to the workspace
  * (<= 112 MB per unit of drops x 4096-element chunks).  Below 1024 elements an fp32
  * request with K > 64 runs the fp64 kernels (TF32 rounding would not average out).

@@ -1425,7 +1425,7 @@ constexpr int kSyrkMinK = 128;
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
 // generated in-kernel below; XLMIMO_PAIR=gen|stream overrides.
-constexpr int kStreamPairMinK = 128;
+constexpr int kStreamPairMinK = 352;  // measured crossover (35 000 elements): K = 320 gen 12.2 vs stream 12.8 ms, K = 384 17.4 vs 13.6
 bool use_stream_pair(int K) {
   static const char *e = getenv("XLMIMO_PAIR");
   if (e && !strcmp(e, "gen")) return false;
