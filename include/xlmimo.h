@@ -102,8 +102,8 @@ XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t 
  *     written to the workspace as planar complex64 and streamed back (fp32 only).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
  * Im G(i,i) = 0.  K <= 1024 -- 64 < K <= 1024 are the NEXT-3/E1-E3 user counts,
- * fp64 on DMMA, in blocks of 64 users below K = 128 and from
- * K = 128 on as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
+ * fp64 on DMMA, in blocks of 64 users up to K = 128 and above
+ * it as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
  * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
  * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
  * operands generated in-kernel below K = 352 and, from K = 352 on or in MATERIALIZED

@@ -1419,9 +1419,9 @@ int blk_pairs(int K) {
   const int nb = (K + kBlkU - 1) / kBlkU;
   return nb * (nb + 1) / 2;
 }
-// K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) from kSyrkMinK users on, the
+// K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) above 128 users, the
 // block-pair kernel below it; XLMIMO_LARGE_K=blk|syrk overrides (A/B tests).
-constexpr int kSyrkMinK = 128;
+constexpr int kSyrkMinK = 129;  // measured (35 000 elements): K = 128 blk 61 vs SYRK 66 ms, K = 150 64 vs 57, K = 200 54 vs 49
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
 // generated in-kernel below; XLMIMO_PAIR=gen|stream overrides.

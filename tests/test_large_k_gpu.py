@@ -186,9 +186,9 @@ def test_gram_large_k_tiny_arrays(xl, orc, N):
 
 
 @pytest.mark.parametrize("kind,n_y,n_z,K,N_or_D", [("upa", 24, 20, 150, 2), ("ula", 1, 1, 150, 2),
-                                                   ("ula", 31, 1, 160, 1), ("ula", 4500, 1, 128, 3)])
+                                                   ("ula", 31, 1, 160, 1), ("ula", 4500, 1, 130, 3)])
 def test_gram_syrk_parity(xl, orc, kind, n_y, n_z, K, N_or_D):
-    """K >= 128 runs the chunked DMMA SYRK (xl_gram_syrk.cu): UPA, one element, fewer
+    """K > 128 runs the chunked DMMA SYRK (xl_gram_syrk.cu): UPA, one element, fewer
     elements than a tile, and a chunk boundary (4500 elements > one 4096-element chunk)."""
     fc, D = 100e9, N_or_D
     if kind == "ula":

@@ -3,7 +3,7 @@
     python tools/bench_app_a.py
 
 Grams: exact fp64 (E1/E3 user field, 100 GHz); K > 64 through the block-pair DMMA
-kernel (K < 128) or the chunked DMMA SYRK (K >= 128; XLMIMO_LARGE_K=blk|syrk overrides).  Work per drop for the Cholesky path: (1 + n_snr) K^3/6 complex MACs.
+kernel (K <= 128) or the chunked DMMA SYRK (K > 128; XLMIMO_LARGE_K=blk|syrk overrides).  Work per drop for the Cholesky path: (1 + n_snr) K^3/6 complex MACs.
 """
 import json
 import os

@@ -1,4 +1,4 @@
-"""One large-K gram_exact call (block-pair DMMA kernel, or the chunked SYRK for K >= 128)
+"""One large-K gram_exact call (block-pair DMMA kernel, or the chunked SYRK for K > 128)
 for ncu captures.
 
     python tools/prof_blk.py <K> <N> <drops>

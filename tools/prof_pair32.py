@@ -1,4 +1,4 @@
-"""One large-K fp32 gram_exact call (TMA-fed tcgen05 block pairs for K >= 128) for ncu.
+"""One large-K fp32 gram_exact call (TMA-fed tcgen05 block pairs for K >= 352) for ncu.
 
     python tools/prof_pair32.py <K> <N> <drops>
 """
