@@ -200,7 +200,8 @@ def gram_closed_form(array: Array, pos: torch.Tensor, stream=None):
 def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | None = None,
              ws: torch.Tensor | None = None, stream=None):
     """Receivers per drop: rates [D, n_snr, n_recv] (bits/s/Hz) and flags [D] (OR-ed into `flags`).
-    K <= 64: all receivers; 64 < K <= 1024: CAP and MRC (tiled Cholesky in a workspace)."""
+    K <= 64: warp Cholesky per drop; 64 < K <= 1024: all receivers through a CTA or tiled DMMA
+    Cholesky and blocked inverse in a workspace."""
     _need_cuda()
     g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
     D, K = g.shape[0], g.shape[1]

@@ -452,3 +452,26 @@ def test_gram_fp32_user_close_to_the_array(xl, orc, prec):
     a, ao = xl.Array.ula(N, 100e9), orc.array("ula", n_y=N, fc_hz=100e9)
     G = xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED if prec == "mat32" else xl.FUSED)
     assert normalized_err(G.cpu().numpy(), orc.gram_exact(ao, p)) <= 1e-4
+
+
+@pytest.mark.parametrize("K", [8, 100])
+def test_empty_batches_every_entry_point(xl, K):
+    """Zero drops through every per-drop entry point: empty outputs, no error, no launch
+    touching memory (small and large K paths)."""
+    a = xl.Array.ula(512, 28e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 0)
+    assert pos.shape == (0, K, 3)
+    G = xl.gram_exact(a, pos)
+    assert G.shape == (0, K, K)
+    if K <= 64:
+        assert xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED).shape == (0, K, K)
+    Gt, fl = xl.gram_closed_form(a, pos)
+    assert Gt.shape == (0, K, K) and fl.shape == (0,)
+    allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    r, fl = xl.sum_rate(G, [0.0, 10.0], allr)
+    assert r.shape == (0, 2, 4) and fl.shape == (0,)
+    rs, bo, _, fa = xl.app_a_bounds(G, [0.0])
+    assert rs.shape == (0, 2) and bo.shape == (0, 1, 3) and fa.shape == (0,)
+    if K <= 64:
+        rm, _ = xl.sum_rate_mismatched(G, Gt, [10.0])
+        assert rm.shape == (0, 1)
