@@ -151,53 +151,57 @@ __global__ void __launch_bounds__(256) rates_kernel(RateParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// Small K (<= 8): one thread per Gram, the factor in registers (fully unrolled),
-// G re-read from global/L1 whenever I + rho G is formed.  Same definitions and
-// failure rule as the warp kernel.
+// Small K (<= 8): one thread per Gram, the factor in registers (fully unrolled, packed
+// lower triangle: K(K+1)/2 complex entries, so K = 8 fits the register file instead of
+// a 1 KB local-memory frame), G re-read from global/L1 whenever I + rho G is formed.
+// Same definitions and failure rule as the warp kernel.
+__host__ __device__ constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }  // j <= i
+
 template <int K>
-__device__ __forceinline__ void load_a(const double2 *G, double rho, double diag, double (&ar)[K][K],
-                                       double (&ai)[K][K]) {
+__device__ __forceinline__ void load_a(const double2 *G, double rho, double diag, double (&ar)[K * (K + 1) / 2],
+                                       double (&ai)[K * (K + 1) / 2]) {
   // lower triangle of diag*I + rho*G: A(i,j) = rho conj(G(j,i)) for i > j
 #pragma unroll
   for (int j = 0; j < K; ++j)
 #pragma unroll
     for (int i = j; i < K; ++i) {
       const double2 g = __ldg(G + j * K + i);
-      ar[i][j] = (i == j ? diag : 0.0) + rho * g.x;
-      ai[i][j] = -rho * g.y;
+      ar[tri(i, j)] = (i == j ? diag : 0.0) + rho * g.x;
+      ai[tri(i, j)] = -rho * g.y;
     }
 }
 
 // in-place lower Cholesky; linv = 1/L_jj
 template <int K>
-__device__ __forceinline__ bool chol_reg(double (&ar)[K][K], double (&ai)[K][K], double (&linv)[K]) {
+__device__ __forceinline__ bool chol_reg(double (&ar)[K * (K + 1) / 2], double (&ai)[K * (K + 1) / 2],
+                                         double (&linv)[K]) {
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    double d = ar[j][j];
+    double d = ar[tri(j, j)];
 #pragma unroll
-    for (int k = 0; k < j; ++k) d -= ar[j][k] * ar[j][k] + ai[j][k] * ai[j][k];
+    for (int k = 0; k < j; ++k) d -= ar[tri(j, k)] * ar[tri(j, k)] + ai[tri(j, k)] * ai[tri(j, k)];
     if (!(d > 0.0) || !isfinite(d)) return false;
     const double ljj = sqrt(d), inv = 1.0 / ljj;
-    ar[j][j] = ljj;
-    ai[j][j] = 0.0;
+    ar[tri(j, j)] = ljj;
+    ai[tri(j, j)] = 0.0;
     linv[j] = inv;
 #pragma unroll
     for (int i = j + 1; i < K; ++i) {
-      double sr = ar[i][j], si = ai[i][j];
+      double sr = ar[tri(i, j)], si = ai[tri(i, j)];
 #pragma unroll
       for (int k = 0; k < j; ++k) {  // - L_ik conj(L_jk)
-        sr -= ar[i][k] * ar[j][k] + ai[i][k] * ai[j][k];
-        si -= ai[i][k] * ar[j][k] - ar[i][k] * ai[j][k];
+        sr -= ar[tri(i, k)] * ar[tri(j, k)] + ai[tri(i, k)] * ai[tri(j, k)];
+        si -= ai[tri(i, k)] * ar[tri(j, k)] - ar[tri(i, k)] * ai[tri(j, k)];
       }
-      ar[i][j] = sr * inv;
-      ai[i][j] = si * inv;
+      ar[tri(i, j)] = sr * inv;
+      ai[tri(i, j)] = si * inv;
     }
   }
   return true;
 }
 
 template <int K>
-__device__ __forceinline__ void inv_diag_reg(const double (&lr)[K][K], const double (&li)[K][K],
+__device__ __forceinline__ void inv_diag_reg(const double (&lr)[K * (K + 1) / 2], const double (&li)[K * (K + 1) / 2],
                                              const double (&linv)[K], double (&dinv)[K]) {
 #pragma unroll
   for (int c = 0; c < K; ++c) {
@@ -210,8 +214,8 @@ __device__ __forceinline__ void inv_diag_reg(const double (&lr)[K][K], const dou
       double tr = 0.0, ti = 0.0;
 #pragma unroll
       for (int j = c; j < k; ++j) {
-        tr += lr[k][j] * xr[j] - li[k][j] * xi[j];
-        ti += lr[k][j] * xi[j] + li[k][j] * xr[j];
+        tr += lr[tri(k, j)] * xr[j] - li[tri(k, j)] * xi[j];
+        ti += lr[tri(k, j)] * xi[j] + li[tri(k, j)] * xr[j];
       }
       xr[k] = -tr * linv[k];
       xi[k] = -ti * linv[k];
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(128) rates_thread_kernel(RateParams P) {
     if (P.flags) P.flags[prob] |= XLMIMO_FLAG_NONFINITE;
     return;
   }
-  double ar[K][K], ai[K][K], linv[K], zf_dinv[K];
+  double ar[K * (K + 1) / 2], ai[K * (K + 1) / 2], linv[K], zf_dinv[K];
   bool zf_ok = false;
   if (P.receivers & XLMIMO_RECV_ZF) {
     load_a<K>(G, 1.0, 0.0, ar, ai);
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(128) rates_thread_kernel(RateParams P) {
       if (!a_ok) fl |= XLMIMO_FLAG_A_NOT_PD;
       if (a_ok) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) cap += 2.0 * log2(ar[k][k]);
+        for (int k = 0; k < K; ++k) cap += 2.0 * log2(ar[tri(k, k)]);
         if (P.receivers & XLMIMO_RECV_MMSE) {
           double dinv[K];
           inv_diag_reg<K>(ar, ai, linv, dinv);
