@@ -33,6 +33,8 @@ C = 299792458.0
 
 
 def dev_ms(fn):
+    """Device time of fn() after one untimed call (module loading, workspace allocation)."""
+    fn()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
