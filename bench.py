@@ -167,11 +167,16 @@ def cpu_baseline(target_s: float):
     n = cores * rounds
     t = oracle_sample(n, seed=1000)
     value = cmac_per_drop(W) * n / t
+    # the same oracle on one thread (SURVEY 8(d) oracle timing plan): t1 ~ one drop on one core
+    n1 = max(1, int(target_s / 3 / per_round))
+    t_1 = oracle_sample(n1, seed=2000, nthreads=1)
     return {"value": value, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} drops of cfg2 (all 9 N, 3 SNR, CAP+ZF+MMSE, exact and closed-form sweeps; the oracle "
                       f"computes every N independently), "
                       f"{t:.1f} s wall on {cores} OpenMP threads",
-            "drops_per_s": n / t}
+            "drops_per_s": n / t,
+            "single_thread": {"value": cmac_per_drop(W) * n1 / t_1, "unit": "cMAC/s", "cores": 1,
+                              "sample": f"{n1} drops, {t_1:.1f} s wall on 1 thread"}}
 
 
 def run_reference(args):
