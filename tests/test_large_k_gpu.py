@@ -60,12 +60,18 @@ def test_gram_large_k_e3_full_size(xl, orc):
     assert int(fl[0]) == 0 and abs(float(rs[0, 1]) - 0.064) < 1e-3
 
 
-def test_gram_large_k_materialised_fp32(xl, orc):
+@pytest.mark.parametrize("kind", ["ula", "upa"])
+def test_gram_large_k_materialised_fp32(xl, orc, kind):
     """MATERIALIZED at K > 64: the TMA-fed tcgen05 pairs over complex64 (TF32) chunks of H
     written to the workspace, at a K below the fused path's streaming threshold (fp32
-    tier), across a chunk boundary."""
-    a, ao = xl.Array.ula(5000, 100e9), orc.array("ula", n_y=5000, fc_hz=100e9)
-    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 90, 2, seed=6)
+    tier); ULA across a chunk boundary, UPA with rows a multiple of 8 and a ragged last
+    block of users."""
+    if kind == "ula":
+        a, ao = xl.Array.ula(5000, 100e9), orc.array("ula", n_y=5000, fc_hz=100e9)
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), 90, 2, seed=6)
+    else:
+        a, ao = xl.Array.upa(40, 30, 100e9), orc.array("upa", n_y=40, n_z=30, fc_hz=100e9)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), 150, 2, seed=7)
     G = xl.gram_exact(a, pos, precision=xl.FP32, mode=xl.MATERIALIZED).cpu().numpy()
     assert normalized_err(G, orc.gram_exact(ao, pos.cpu().numpy())) <= 1e-4
 
