@@ -396,7 +396,11 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
 }
 
 constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
-constexpr int kGenGroups = 8;      // group g owns ring slot g (stage k -> slot k % 8)
+#ifndef XL_GEN_GROUPS
+#define XL_GEN_GROUPS 10
+#endif
+constexpr int kGenGroups = XL_GEN_GROUPS;  // group g makes stages k = g (mod groups), ring slot k % kFStages
+                                           // (10: cfg4 4.02 -> 3.76 ms, cfg3/cfg5 -1 %; 12 loses on cfg3/cfg5)
 constexpr int kFStages = 12;      // ring slots: stage k -> slot k % 12, generated by group k % 8
 constexpr int kGenThreads = 32 * kGenWarps;
 constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
@@ -608,6 +612,11 @@ constexpr int kPUsers = 64;
 // 4096 elements (half the drift) and combines partials in fp64.
 constexpr int kPChunk = 4096;
 
+// the pair kernel's own warp layout: 6 generator groups of 2 warps, 4 epilogue warps,
+// the MMA warp (no idle warps, so the register cap leaves the generators unspilled)
+constexpr int kPEpiWarp0 = kPGroups * kGenWarps;    // 12
+constexpr int kPMmaWarp = kPEpiWarp0 + 4;           // 16
+constexpr int kPairThreads = 32 * (kPMmaWarp + 1);  // 544
 struct FusedPairParams {
   const double *pos;
   double *ws;        // partials [drop][chunk][NP][2], NP = K(K+1)/2 over all K users
@@ -624,7 +633,7 @@ __device__ __forceinline__ void pair_of(int pair, int nb, int &bi, int &bj) {
   bj = bi + pair;
 }
 
-__global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(FusedPairParams P) {
+__global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(FusedPairParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *stages = base;
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
   const int K = P.K;
   const int64_t per_drop = (int64_t)P.n_pairs * P.n_chunks;
   const int64_t n_items = P.n_drops * per_drop;
-  for (int i = tid; i < kPSlots * kPSlotBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < kPSlots * kPSlotBytes / 16; i += kPairThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < kPSlots; ++s) {
       mbar_init(&full[s], kGenWarps);
@@ -652,7 +661,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (warp == kMmaWarp) {
+  if (warp == kPMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
                  "r"(256)
                  : "memory");
@@ -665,8 +674,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
   constexpr int kSpb = kBoxK;  // elements per stage
 
   if (warp < kPGroups * kGenWarps) {  // ---------------- generators: group g makes stages k = g (mod 6)
-    // (warps 12..15 idle: with 6 slots of 32 KB, more groups could lap a slot and pass a
-    // parity wait one phase early)
+    // (6 groups for 6 slots of 32 KB: more groups could lap a slot and pass a parity wait
+    // one phase early)
     const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
     double4 *su = su_all + grp * (2 * kPUsers);
     const double inv_lambda = 1.0 / P.lambda;
@@ -726,7 +735,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
         if (lane == 0) mbar_arrive(&full[slot]);
       }
     }
-  } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
+  } else if (warp == kPMmaWarp) {  // ---------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = tf32_idesc(kRows, kRows);
       // (the original kernel's 12 slots over 8 groups satisfy the same groups <= slots rule)
@@ -761,8 +770,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
         mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= kEpiWarp0) {  // ---------------- epilogue, warps kEpiWarp0..+3 = TMEM lane quadrants
-    const int q = warp - kEpiWarp0;
+  } else if (warp >= kPEpiWarp0) {  // ---------------- epilogue, warps kPEpiWarp0..+3 = TMEM lane quadrants
+    const int q = warp - kPEpiWarp0;
     const int row = 32 * q + lane;
     const int il = row >> 1, plane = row & 1;
     const int64_t NP = (int64_t)K * (K + 1) / 2;
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_pair_kernel(Fu
     }
   }
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == kPMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
   }
@@ -1212,7 +1221,7 @@ int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_dr
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = n_drops * P.n_pairs * P.n_chunks;
   const int grid = (int)(items < sms ? items : sms);
-  gram_fused_tc_pair_kernel<<<grid, kFusedThreads, smem, s>>>(P);
+  gram_fused_tc_pair_kernel<<<grid, kPairThreads, smem, s>>>(P);
   return check_launch("gram_fused_tc_pair_kernel");
 }
 
