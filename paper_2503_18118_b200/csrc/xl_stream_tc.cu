@@ -401,7 +401,10 @@ constexpr int kGenWarps = 2;       // warps per generator group (arrivals per fu
 #endif
 constexpr int kGenGroups = XL_GEN_GROUPS;  // group g makes stages k = g (mod groups), ring slot k % kFStages
                                            // (10: cfg4 4.02 -> 3.76 ms, cfg3/cfg5 -1 %; 12 loses on cfg3/cfg5)
-constexpr int kFStages = 12;      // ring slots: stage k -> slot k % 12, generated by group k % 8
+#ifndef XL_FSTAGES
+#define XL_FSTAGES 12
+#endif
+constexpr int kFStages = XL_FSTAGES;  // ring slots: stage k -> slot k % kFStages, generated by group k % kGenGroups
 constexpr int kGenThreads = 32 * kGenWarps;
 constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
 constexpr int kMmaWarp = kEpiWarp0 + 4;            // 20
