@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
 
 // K > kSmemK: one CTA per matrix in a global workspace slot (K_pad = 32 nt, row-major,
 // lower triangle used), tiled Cholesky with 32 x 32 complex tiles, panels in groups of
-// kGrp = 4 (left-looking inside a group, right-looking between groups):
+// kGrp = 8 (left-looking inside a group, right-looking between groups):
 //  (0) the tiles of column k take the group's earlier panels: A_ik -= L_i,G' L_k,G'^H;
 //  (1) warp 0 factors the diagonal tile in shared memory and inverts it (lane = column);
 //  (2) panel X_ik = A_ik L_kk^{-H}, one tile product per warp;
@@ -295,7 +295,10 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
 // kPfDist k-steps ahead) with a one-step register double buffer.  DMMA and DFMA share
 // the FP64 pipe at the same FMA rate; the tensor path needs one
 // instruction per 256 FMAs and no shared-memory operand traffic.
-constexpr int kGrp = 4;          // panels per trailing update
+#ifndef XB_GRP
+#define XB_GRP 8  // measured K = 1000: 2 -> 20.3 ms, 4 -> 18.5, 8 / 12 / 16 -> 17.8
+#endif
+constexpr int kGrp = XB_GRP;     // panels per trailing update
 constexpr int kLdY = kTile + 2;  // per-warp Y tile row stride (conflict-free B-fragment reads)
 constexpr int kLdI = kTile + 4;  // L_kk^{-1} row stride (conflict-free B_NT fragment reads)
 // Two CTAs of 4 warps per SM, each on its own matrix: one CTA's serial steps (diagonal
