@@ -83,7 +83,10 @@ __device__ __forceinline__ void frag_prefetch_l2(const double2 *Am, size_t lda, 
 // B_NT, B(k, n) = Bt(n, k) from a row-major Bt (stride ldb) (conjugated with CONJ_B).  The
 // fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run, and (PF, operands in
 // global memory) the lines of k-step kb + kPfDist are pulled into L2 meanwhile.
-constexpr int kPfDist = 8;
+#ifndef XT_PFDIST
+#define XT_PFDIST 4  // measured: 4 vs 8 vs 16 -> K = 1000 receivers 31.4 / 32.4 / 35.7 ms, SYRK equal
+#endif
+constexpr int kPfDist = XT_PFDIST;
 template <bool B_NT, bool CONJ_B, bool PF, int MB = 4, int NB = 4>
 __device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ Am, size_t lda,
                                           const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
