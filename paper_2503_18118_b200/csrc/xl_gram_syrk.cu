@@ -18,6 +18,7 @@
 #include <type_traits>
 
 #include "xl_common.cuh"
+#define XT_PFDIST 8  // long slices: prefetch further ahead (737 vs 740 ms at E3 with 4)
 #include "xl_dmma_tile.cuh"
 
 namespace {
