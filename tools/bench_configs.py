@@ -9,6 +9,7 @@ algorithmic bytes 8 N K per drop.  Drop counts are reduced for the big configs
 (stated in the output).  Prints one JSON object per line.
 """
 import json
+import statistics
 import os
 import sys
 
@@ -26,16 +27,19 @@ PEAK_FP64 = 148 * 64 * 1965e6
 HBM = 6547.8e9
 
 
-def timed(fn, reps=3):
+def timed(fn, reps=5):
+    """Per-kernel device ms: the median of `reps` separately timed calls after one untimed
+    call (median of >= 5 runs)."""
     fn()
     torch.cuda.synchronize()
-    xl._L.xlmimo_timing_enable(1)
+    runs = []
     for _ in range(reps):
+        xl._L.xlmimo_timing_enable(1)
         fn()
-    torch.cuda.synchronize()
-    xl._L.xlmimo_timing_enable(0)
-    kt = parallel.read_kernel_times(xl)
-    return {k: v[1] / reps for k, v in kt.items()}
+        torch.cuda.synchronize()
+        xl._L.xlmimo_timing_enable(0)
+        runs.append({k: v[1] for k, v in parallel.read_kernel_times(xl).items()})
+    return {k: statistics.median(r.get(k, 0.0) for r in runs) for k in runs[0]}
 
 
 def main(cfgs):
@@ -56,7 +60,7 @@ def main(cfgs):
         t = timed(lambda: xl.gram_exact(arr, pos, precision=xl.FP32))
         k = max((k for k in t if k.startswith("gram_fused")), key=lambda k: t[k])
         res["fused_fp32"] = {"kernel": k, "ms": t[k], "cmac_per_s": cmac / (t[k] * 1e-3)}
-        t = timed(lambda: xl.gram_exact(arr, pos, precision=xl.FP32, mode=xl.MATERIALIZED), reps=2)
+        t = timed(lambda: xl.gram_exact(arr, pos, precision=xl.FP32, mode=xl.MATERIALIZED))
         bytes_h = 8 * N * K * D
         ks = [k for k in t if k.startswith("gram_stream")]
         if ks:
