@@ -129,7 +129,9 @@ XLMIMO_API int xlmimo_gram_exact(const xlmimo_array_t *array, const double *pos,
  *   * exp(j sgn(dx) (2 pi frac(d/lambda) - pi/4)),  dx = |x_i| - |x_j|.
  * O(K^2) per drop, independent of N.  gram as for xlmimo_gram_exact.
  * flags (dev [n_drops] or NULL): set (not OR-ed) to XLMIMO_FLAG_DEGENERATE or 0.
- * EUNSUPPORTED for a UPA (the paper is ULA-only). */
+ * EUNSUPPORTED for a UPA (the paper is ULA-only) and for spacing_wl != 0.5:
+ * Eq. (4)'s aperture M lambda and element density 2/lambda are the paper's lambda/2 array
+ * (PAPER.md:52), so another pitch would silently disagree with the exact Gram. */
 XLMIMO_API int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double *pos, int32_t K, int64_t n_drops,
                             double *gram, uint32_t *flags, void *stream);
 
@@ -188,9 +190,14 @@ XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drop
  * n_list (host, ascending, all of one parity so the centred arrays nest, R18) and
  * the SAME drops (pos if non-NULL, else drawn from users/seed like xlmimo_gen_drops
  * with first_drop = 0): the Gram (exact, fused, computed in one pass over the
- * largest array as nested shells; or closed form per N), the receivers, and
- *   ergodic  (host [n_n][n_snr][n_recv]) = mean over drops excluding NaN,
- *   n_valid  (host, same shape)          = number of drops in each mean,
+ * largest array as nested shells; or closed form per N), the receivers, and (R10)
+ *   ergodic  (host [n_n][n_snr][n_recv]) = the ergodic mean over ALL n_drops drops
+ *             -- NaN for a column in which any drop's rate is
+ *            NaN (a failed Cholesky, e.g. an indefinite closed-form Gram: a mean over
+ *            the surviving drops would be biased, so it is never reported as ergodic),
+ *   n_valid  (host, same shape)          = number of drops whose rate is not NaN,
+ *   ergodic_valid (host, same shape, or NULL) = mean over those n_valid drops only
+ *            (a conditional mean; NaN if n_valid = 0; = ergodic when n_valid = n_drops),
  *   sat      (host [4]) = { E[y_up], E[y_down], M_sat, stderr(M_sat) } with the
  *            per-drop Eqs. (13)-(16) at threshold t (0.9,
  *            PAPER.md:228) and M_sat = ceil((E[y_up]-E[y_down]) / pitch) (R15),
@@ -206,8 +213,8 @@ XLMIMO_API int xlmimo_saturation_sweep(const xlmimo_array_t *array, const int64_
                             const xlmimo_users_t *users, const double *pos, int32_t K, int64_t n_drops,
                             uint64_t seed, const double *snr_db, int32_t n_snr, uint32_t receivers,
                             int32_t gram_kind, int32_t precision, double t,
-                            double *ergodic, int64_t *n_valid, double *sat, double *per_drop,
-                            void *ws, size_t ws_bytes, void *stream);
+                            double *ergodic, int64_t *n_valid, double *ergodic_valid, double *sat,
+                            double *per_drop, void *ws, size_t ws_bytes, void *stream);
 
 /* Same as xlmimo_saturation_sweep with HOST positions (pos_host [n_drops][K][3],
  * pinned for full speed): copies them in, runs the sweep, returns host results.
@@ -215,8 +222,8 @@ XLMIMO_API int xlmimo_saturation_sweep(const xlmimo_array_t *array, const int64_
 XLMIMO_API int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                                  const double *pos_host, int32_t K, int64_t n_drops,
                                  const double *snr_db, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
-                                 int32_t precision, double t, double *ergodic, int64_t *n_valid, double *sat,
-                                 void *ws, size_t ws_bytes, void *stream);
+                                 int32_t precision, double t, double *ergodic, int64_t *n_valid,
+                                 double *ergodic_valid, double *sat, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------- NEXT-1
  * Effective ("mismatched") rate of the paper's modified ZF:

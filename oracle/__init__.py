@@ -87,7 +87,7 @@ def lib():
         L.or_bounds_app_a.argtypes = [vp, i32, i64, vp, i32, vp, vp, vp, vp, i32]
         L.or_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp]
         L.or_saturation_sweep.argtypes = [P(OrArray), vp, i32, vp, i32, i64, vp, i32, u32, i32, d,
-                                          vp, vp, vp, vp, i32]
+                                          vp, vp, vp, vp, vp, i32]
         _lib = L
     return _lib
 
@@ -262,7 +262,9 @@ def saturation_coords(pos: np.ndarray, t: float):
 
 
 def saturation_sweep(arr: OrArray, n_list, pos: np.ndarray, snr_db, receivers: int, gram_kind: int = 0,
-                     t: float = 0.9, per_drop: bool = False, nthreads: int = 0):
+                     t: float = 0.9, per_drop: bool = False, nthreads: int = 0, valid_mean: bool = False):
+    """(ergodic, n_valid, sat, per_drop) -- plus ergodic_valid (the mean over the valid drops
+    only) when valid_mean.  ergodic is NaN for a column with any NaN drop (R10)."""
     pos = np.ascontiguousarray(pos, dtype=np.float64)
     D, K, _ = pos.shape
     nl = np.ascontiguousarray(n_list, dtype=np.int64)
@@ -272,9 +274,12 @@ def saturation_sweep(arr: OrArray, n_list, pos: np.ndarray, snr_db, receivers: i
     nv = np.zeros((nl.size, snr.size, R), dtype=np.int64)
     sat = np.zeros(4)
     pd = np.zeros((D, nl.size, snr.size, R)) if per_drop else None
+    ergv = np.zeros((nl.size, snr.size, R))
     lib().or_saturation_sweep(ctypes.byref(arr), _ptr(nl), nl.size, _ptr(pos), K, D, _ptr(snr), snr.size,
-                              receivers, gram_kind, t, _ptr(erg), _ptr(nv), _ptr(sat),
+                              receivers, gram_kind, t, _ptr(erg), _ptr(nv), _ptr(ergv), _ptr(sat),
                               _ptr(pd) if pd is not None else None, nthreads)
+    if valid_mean:
+        return erg, nv, sat, pd, ergv
     return erg, nv, sat, pd
 
 

@@ -610,14 +610,19 @@ void or_saturation_coords(const double *pos, int32_t K, int64_t n_drops, double 
 }
 
 /* Saturation sweep (ULA): for every N in n_list, independently (no nesting,
- * R18), the Gram of the same drops, the receivers, and the ergodic mean over
- * drops excluding NaN (R10).  sat = {E[y_up], E[y_down], M_sat, stderr(M_sat)}
- * with M_sat = ceil((E[y_up] - E[y_down]) / pitch).
+ * R18), the Gram of the same drops, the receivers, and per (N, SNR, receiver)
+ * column (R10): n_valid = the number of drops whose rate is not NaN;
+ * ergodic = the mean over ALL drops (the expectation of PAPER.md:177-178, 228),
+ * which exists only when every drop is valid, else NaN; ergodic_valid (optional)
+ * = the mean over the valid drops only (a conditional mean, NaN if none).
+ * sat = {E[y_up], E[y_down], M_sat, stderr(M_sat)} with
+ * M_sat = ceil((E[y_up] - E[y_down]) / pitch) and
+ * stderr = sample std (ddof 1) of the per-drop extent (y_up - y_down)/pitch over sqrt(D).
  * gram_kind: 0 exact, 1 closed form.  per_drop (optional) [D][n_n][n_snr][n_recv]. */
 void or_saturation_sweep(const or_array_t *a_in, const int64_t *n_list, int32_t n_n, const double *pos,
                          int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr, uint32_t receivers,
-                         int32_t gram_kind, double t, double *ergodic, int64_t *n_valid, double *sat,
-                         double *per_drop, int32_t nthreads)
+                         int32_t gram_kind, double t, double *ergodic, int64_t *n_valid, double *ergodic_valid,
+                         double *sat, double *per_drop, int32_t nthreads)
 {
     int n_recv = 0;
     for (int b = 0; b < 4; ++b) n_recv += (receivers >> b) & 1u;
@@ -640,7 +645,9 @@ void or_saturation_sweep(const or_array_t *a_in, const int64_t *n_list, int32_t 
                 if (per_drop) per_drop[((size_t)d * n_n + n) * per + e] = v;
                 if (!isnan(v)) { or_nadd(&acc, v); ++cnt; }
             }
-            ergodic[(size_t)n * per + e] = cnt ? (acc.s + acc.c) / (double)cnt : NAN;
+            const double cond = cnt ? (acc.s + acc.c) / (double)cnt : NAN;
+            ergodic[(size_t)n * per + e] = cnt == n_drops ? cond : NAN;
+            if (ergodic_valid) ergodic_valid[(size_t)n * per + e] = cond;
             n_valid[(size_t)n * per + e] = cnt;
         }
     }

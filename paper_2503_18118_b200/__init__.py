@@ -94,9 +94,9 @@ def _load():
     L.xlmimo_saturation_sweep_workspace.argtypes = [P(Array), vp, i32, i32, i64, i32, u32, i32, i32]
     L.xlmimo_saturation_sweep_workspace.restype = sz
     L.xlmimo_saturation_sweep.argtypes = [P(Array), vp, i32, P(Users), vp, i32, i64, u64, vp, i32, u32, i32, i32, d,
-                                          vp, vp, vp, vp, vp, sz, vp]
+                                          vp, vp, vp, vp, vp, vp, sz, vp]
     L.xlmimo_saturation_sweep_host.argtypes = [P(Array), vp, i32, vp, i32, i64, vp, i32, u32, i32, i32, d,
-                                               vp, vp, vp, vp, sz, vp]
+                                               vp, vp, vp, vp, vp, sz, vp]
     L.xlmimo_sum_rate_mismatched.argtypes = [vp, vp, i32, i64, vp, i32, vp, vp, vp]
     L.xlmimo_sum_rate_mismatched.restype = ctypes.c_int
     L.xlmimo_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp, vp]
@@ -135,6 +135,37 @@ def _dptr(t: torch.Tensor):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _check_tensor(t: torch.Tensor, what: str, dtype, shape):
+    """Argument checks before a device pointer crosses the ABI (a wrong dtype or a short
+    tensor would make the kernels read or write out of bounds)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise XlmimoError(f"{what}: expected a CUDA tensor")
+    if t.dtype not in (dtype if isinstance(dtype, tuple) else (dtype,)):
+        raise XlmimoError(f"{what}: dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise XlmimoError(f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise XlmimoError(f"{what}: must be contiguous")
+
+
+def _check_pos(pos: torch.Tensor, K: int, n_drops: int):
+    _check_tensor(pos, "pos", torch.float64, (n_drops, K, 3))
+
+
+def _check_flags(fl: torch.Tensor, n_drops: int):
+    _check_tensor(fl, "flags", (torch.int32, torch.uint32), (n_drops,))
+
+
+def _gram_arg(gram: torch.Tensor, what: str = "gram") -> torch.Tensor:
+    """[D, K, K] complex128 or [D, K, K, 2] float64 -> the contiguous interleaved float64 view."""
+    g = torch.view_as_real(gram) if gram.is_complex() else gram
+    if g.dim() != 4 or g.shape[1] != g.shape[2] or g.shape[3] != 2:
+        raise XlmimoError(f"{what}: shape {tuple(gram.shape)}, expected [D, K, K] complex or [D, K, K, 2]")
+    g = g.contiguous()
+    _check_tensor(g, what, torch.float64, tuple(g.shape))
+    return g
+
+
 def _hptr(a):
     return ctypes.c_void_p(a.data_ptr()) if isinstance(a, torch.Tensor) else a.ctypes.data_as(ctypes.c_void_p)
 
@@ -164,6 +195,7 @@ def gen_drops(users: Users, K: int, n_drops: int, seed: int = 0, first_drop: int
     _need_cuda()
     dev = device or torch.device("cuda", torch.cuda.current_device())
     pos = out if out is not None else torch.empty((n_drops, K, 3), dtype=torch.float64, device=dev)
+    _check_pos(pos, K, n_drops)
     _check(_L.xlmimo_gen_drops(ctypes.byref(users), K, n_drops, seed, first_drop, _dptr(pos), _stream(stream)),
            "xlmimo_gen_drops")
     return pos
@@ -175,7 +207,9 @@ def gram_exact(array: Array, pos: torch.Tensor, precision: int = FP64, mode: int
     """Exact Gram H^H H, complex128 [n_drops, K, K]."""
     _need_cuda()
     D, K, _ = pos.shape
+    _check_pos(pos, K, D)
     g = out if out is not None else torch.empty((D, K, K, 2), dtype=torch.float64, device=pos.device)
+    _check_tensor(g, "out", torch.float64, (D, K, K, 2))
     need = _L.xlmimo_gram_exact_workspace(ctypes.byref(array), K, D, precision, mode)
     if ws is None or ws.numel() < need:
         ws = _workspace(need, pos.device)
@@ -189,6 +223,7 @@ def gram_closed_form(array: Array, pos: torch.Tensor, stream=None):
     """Closed-form (modified-ZF) Gram complex128 [D, K, K] and per-drop flags (uint32 as int32)."""
     _need_cuda()
     D, K, _ = pos.shape
+    _check_pos(pos, K, D)
     g = torch.empty((D, K, K, 2), dtype=torch.float64, device=pos.device)
     fl = torch.zeros(D, dtype=torch.int32, device=pos.device)
     _check(_L.xlmimo_gram_closed_form(ctypes.byref(array), _dptr(pos), K, D, _dptr(g), _dptr(fl), _stream(stream)),
@@ -203,11 +238,12 @@ def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | N
     K <= 64: warp Cholesky per drop; 64 < K <= 1024: all receivers through a CTA or tiled DMMA
     Cholesky and blocked inverse in a workspace."""
     _need_cuda()
-    g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
+    g = _gram_arg(gram)
     D, K = g.shape[0], g.shape[1]
     snr = _f64_host(snr_db)
     rates = torch.empty((D, snr.size, n_recv(receivers)), dtype=torch.float64, device=g.device)
     fl = flags if flags is not None else torch.zeros(D, dtype=torch.int32, device=g.device)
+    _check_flags(fl, D)
     need = int(_L.xlmimo_sum_rate_workspace(K, D, snr.size, receivers))
     if need and (ws is None or ws.numel() < need):
         ws = _workspace(need, g.device)
@@ -222,7 +258,7 @@ def app_a_bounds(gram: torch.Tensor, snr_db, eig: bool = False, ws: torch.Tensor
     gap = -log2 det(R)/K), bounds [D, n_snr, 3] = (log2 U, log2 det(I + rho G), log2 L),
     eigenvalues of R [D, K] ascending (K <= 64) or None, flags [D]."""
     _need_cuda()
-    g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
+    g = _gram_arg(gram)
     D, K = g.shape[0], g.shape[1]
     snr = _f64_host(snr_db)
     rstat = torch.empty((D, 2), dtype=torch.float64, device=g.device)
@@ -243,12 +279,15 @@ def sum_rate_mismatched(gram: torch.Tensor, gram_model: torch.Tensor, snr_db, fl
     """NEXT-1: effective rate of the modified-ZF equalizer G~^{-1} H^H on the true channel.
     Returns rates [D, n_snr] and flags [D] (bit 5: G~ singular)."""
     _need_cuda()
-    g = torch.view_as_real(gram).contiguous() if gram.is_complex() else gram.contiguous()
-    gm = torch.view_as_real(gram_model).contiguous() if gram_model.is_complex() else gram_model.contiguous()
+    g = _gram_arg(gram)
+    gm = _gram_arg(gram_model, "gram_model")
+    if gm.shape != g.shape:
+        raise XlmimoError(f"gram_model: shape {tuple(gm.shape)} != gram {tuple(g.shape)}")
     D, K = g.shape[0], g.shape[1]
     snr = _f64_host(snr_db)
     rates = torch.empty((D, snr.size), dtype=torch.float64, device=g.device)
     fl = flags if flags is not None else torch.zeros(D, dtype=torch.int32, device=g.device)
+    _check_flags(fl, D)
     _check(_L.xlmimo_sum_rate_mismatched(_dptr(g), _dptr(gm), K, D, _hptr(snr), snr.size, _dptr(rates), _dptr(fl),
                                          _stream(stream)), "xlmimo_sum_rate_mismatched")
     return rates, fl
@@ -260,6 +299,7 @@ def gen_drops_rect(x, y, K: int, n_drops: int, seed: int = 0, first_drop: int = 
     _need_cuda()
     dev = device or torch.device("cuda", torch.cuda.current_device())
     pos = out if out is not None else torch.empty((n_drops, K, 3), dtype=torch.float64, device=dev)
+    _check_pos(pos, K, n_drops)
     _check(_L.xlmimo_gen_drops_rect(float(x[0]), float(x[1]), float(y[0]), float(y[1]), K, n_drops, seed,
                                     first_drop, _dptr(pos), _stream(stream)), "xlmimo_gen_drops_rect")
     return pos
@@ -279,7 +319,8 @@ def saturation_sweep(array: Array, n_list, K: int, n_drops: int, snr_db, receive
                      precision: int = FP64, t: float = 0.9, per_drop: bool = False, ws: torch.Tensor | None = None,
                      stream=None, device=None):
     """Capacity-vs-N sweep over nested centred ULAs.  Returns a dict with host numpy arrays
-    ergodic [n_n, n_snr, n_recv], n_valid (same), sat [4] and (optionally) the device
+    ergodic [n_n, n_snr, n_recv] (NaN for a column with any NaN drop, R10), n_valid (same),
+    ergodic_valid (same: the mean over the valid drops), sat [4] and (optionally) the device
     per_drop [n_drops, n_n, n_snr, n_recv]."""
     import numpy as np
     _need_cuda()
@@ -287,7 +328,10 @@ def saturation_sweep(array: Array, n_list, K: int, n_drops: int, snr_db, receive
     nl = np.ascontiguousarray(n_list, dtype=np.int64)
     snr = _f64_host(snr_db)
     R = n_recv(receivers)
+    if pos is not None:
+        _check_pos(pos, K, n_drops)
     erg = np.zeros((nl.size, snr.size, R))
+    ergv = np.zeros((nl.size, snr.size, R))
     nv = np.zeros((nl.size, snr.size, R), dtype=np.int64)
     sat = np.zeros(4)
     pd = torch.empty((n_drops, nl.size, snr.size, R), dtype=torch.float64, device=dev) if per_drop else None
@@ -298,9 +342,9 @@ def saturation_sweep(array: Array, n_list, K: int, n_drops: int, snr_db, receive
                                       ctypes.byref(users) if users is not None else None,
                                       _dptr(pos) if pos is not None else None, K, n_drops, seed, _hptr(snr),
                                       snr.size, receivers, gram_kind, precision, t, _hptr(erg), _hptr(nv),
-                                      _hptr(sat), _dptr(pd) if pd is not None else None, _dptr(ws), ws.numel(),
-                                      _stream(stream)), "xlmimo_saturation_sweep")
-    return {"ergodic": erg, "n_valid": nv, "sat": sat, "per_drop": pd}
+                                      _hptr(ergv), _hptr(sat), _dptr(pd) if pd is not None else None, _dptr(ws),
+                                      ws.numel(), _stream(stream)), "xlmimo_saturation_sweep")
+    return {"ergodic": erg, "n_valid": nv, "ergodic_valid": ergv, "sat": sat, "per_drop": pd}
 
 
 def saturation_sweep_host(array: Array, n_list, pos_host: torch.Tensor, snr_db, receivers: int, *,
@@ -309,13 +353,16 @@ def saturation_sweep_host(array: Array, n_list, pos_host: torch.Tensor, snr_db, 
     """The end-to-end entry: HOST positions (pin them for speed) in, host results out."""
     import numpy as np
     _need_cuda()
-    assert not pos_host.is_cuda and pos_host.dtype == torch.float64 and pos_host.is_contiguous()
+    if pos_host.is_cuda or pos_host.dtype != torch.float64 or not pos_host.is_contiguous() or pos_host.dim() != 3 \
+            or pos_host.shape[2] != 3:
+        raise XlmimoError("pos_host: expected a contiguous host float64 tensor [n_drops, K, 3]")
     dev = device or torch.device("cuda", torch.cuda.current_device())
     n_drops, K, _ = pos_host.shape
     nl = np.ascontiguousarray(n_list, dtype=np.int64)
     snr = _f64_host(snr_db)
     R = n_recv(receivers)
     erg = np.zeros((nl.size, snr.size, R))
+    ergv = np.zeros((nl.size, snr.size, R))
     nv = np.zeros((nl.size, snr.size, R), dtype=np.int64)
     sat = np.zeros(4)
     need = sweep_workspace_bytes(array, nl, K, n_drops, snr.size, receivers, gram_kind, precision)
@@ -323,6 +370,7 @@ def saturation_sweep_host(array: Array, n_list, pos_host: torch.Tensor, snr_db, 
         ws = _workspace(need, dev)
     _check(_L.xlmimo_saturation_sweep_host(ctypes.byref(array), _hptr(nl), nl.size, _hptr(pos_host), K, n_drops,
                                            _hptr(snr), snr.size, receivers, gram_kind, precision, t, _hptr(erg),
-                                           _hptr(nv), _hptr(sat), _dptr(ws), ws.numel(), _stream(stream)),
+                                           _hptr(nv), _hptr(ergv), _hptr(sat), _dptr(ws), ws.numel(),
+                                           _stream(stream)),
            "xlmimo_saturation_sweep_host")
-    return {"ergodic": erg, "n_valid": nv, "sat": sat}
+    return {"ergodic": erg, "n_valid": nv, "ergodic_valid": ergv, "sat": sat}

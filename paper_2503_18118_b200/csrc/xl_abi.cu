@@ -73,7 +73,7 @@ struct Carve {
 
 // Layout of the saturation-sweep workspace (shared by the size query and the call).
 struct SweepWs {
-  double *pos, *grams, *rates, *erg, *sat, *satp;
+  double *pos, *grams, *rates, *erg, *ergv, *sat, *satp;
   int64_t *nval;
   uint32_t *flags;
   void *gws, *rws;
@@ -91,6 +91,7 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
   w.rates = (double *)c.take((size_t)D * n_n * n_snr * R * sizeof(double));
   w.flags = (uint32_t *)c.take((size_t)D * n_n * sizeof(uint32_t));
   w.erg = (double *)c.take((size_t)n_n * n_snr * R * sizeof(double));
+  w.ergv = (double *)c.take((size_t)n_n * n_snr * R * sizeof(double));
   w.nval = (int64_t *)c.take((size_t)n_n * n_snr * R * sizeof(int64_t));
   w.sat = (double *)c.take(4 * sizeof(double));
   w.satp = (double *)c.take(xlh::saturation_stats_scratch(D));
@@ -127,6 +128,8 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sweep: receivers");
   if (gram_kind != XLMIMO_GRAM_EXACT && gram_kind != XLMIMO_GRAM_CLOSED_FORM)
     return xlh::set_error(XLMIMO_EINVAL, "sweep: gram_kind");
+  if (gram_kind == XLMIMO_GRAM_CLOSED_FORM && array->spacing_wl != 0.5)
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: the closed form assumes lambda/2 spacing (PAPER.md:52)");
   if (precision != XLMIMO_FP64 && precision != XLMIMO_FP32) return xlh::set_error(XLMIMO_EINVAL, "sweep: precision");
   if (!(t > 0.0 && t < 1.0)) return xlh::set_error(XLMIMO_EINVAL, "sweep: t not in (0,1)");
   return XLMIMO_OK;
@@ -135,8 +138,8 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
 int run_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, const xlmimo_users_t *users,
               const double *pos, const double *pos_host, int32_t K, int64_t n_drops, uint64_t seed,
               const double *snr_db, int32_t n_snr, uint32_t receivers, int32_t gram_kind, int32_t precision,
-              double t, double *ergodic, int64_t *n_valid, double *sat, double *per_drop, void *ws,
-              size_t ws_bytes, cudaStream_t s) {
+              double t, double *ergodic, int64_t *n_valid, double *ergodic_valid, double *sat, double *per_drop,
+              void *ws, size_t ws_bytes, cudaStream_t s) {
   const xlh::ArrayP ap = to_params(array);
   SweepWs w = sweep_layout(ws, ap, n_list, n_n, K, n_drops, n_snr, receivers, gram_kind, precision);
   if (!ws || ws_bytes < w.total)
@@ -171,11 +174,14 @@ int run_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, c
     rc = xlh::launch_sum_rate(w.grams, K, n_drops * n_n, snr_db, n_snr, receivers, rates, w.flags, s);
   if (rc) return rc;
   const int n_out = n_n * n_snr * n_recv_of(receivers);
-  if ((rc = xlh::launch_ergodic_reduce(rates, n_drops, n_out, w.erg, w.nval, s))) return rc;
+  if ((rc = xlh::launch_ergodic_reduce(rates, n_drops, n_out, w.erg, w.ergv, w.nval, s))) return rc;
   if ((rc = xlh::launch_saturation_stats(P, K, n_drops, t, ap.pitch, w.sat, w.satp, s))) return rc;
-  cudaMemcpyAsync(ergodic, w.erg, (size_t)n_out * sizeof(double), cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(n_valid, w.nval, (size_t)n_out * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(sat, w.sat, 4 * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (cudaMemcpyAsync(ergodic, w.erg, (size_t)n_out * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      (ergodic_valid && cudaMemcpyAsync(ergodic_valid, w.ergv, (size_t)n_out * sizeof(double),
+                                        cudaMemcpyDeviceToHost, s) != cudaSuccess) ||
+      cudaMemcpyAsync(n_valid, w.nval, (size_t)n_out * sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(sat, w.sat, 4 * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return xlh::check_launch("sweep: D2H results");
   if (cudaStreamSynchronize(s) != cudaSuccess) return xlh::check_launch("sweep: synchronize");
   return XLMIMO_OK;
 }
@@ -316,6 +322,8 @@ int xlmimo_gram_closed_form(const xlmimo_array_t *array, const double *pos, int3
   g_err[0] = 0;
   if (bad_array(array)) return xlh::set_error(XLMIMO_EINVAL, "closed_form: invalid array");
   if (array->kind != XLMIMO_ULA) return xlh::set_error(XLMIMO_EUNSUPPORTED, "closed_form: ULA only (PAPER.md:40)");
+  if (array->spacing_wl != 0.5)
+    return xlh::set_error(XLMIMO_EUNSUPPORTED, "closed_form: Eqs. (4)/(6) assume lambda/2 spacing (PAPER.md:52)");
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "closed_form: K=%d", K);
   if (n_drops > 0 && (!pos || !gram)) return xlh::set_error(XLMIMO_EINVAL, "closed_form: null pointer");
   const xlh::ArrayP ap = to_params(array);
@@ -397,10 +405,15 @@ int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max
                                     (cudaStream_t)stream);
 }
 
+static const double kSnrProbe = 0.0;  // validate_sweep wants a non-null SNR list; the query has none
+
 size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, int32_t K,
                                          int64_t n_drops, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
                                          int32_t precision) {
-  if (bad_array(array) || !n_list || n_n < 1 || n_n > 32 || K < 1 || K > xl::kMaxKLarge || n_drops < 1) return 0;
+  if (validate_sweep(array, n_list, n_n, K, n_drops, &kSnrProbe, n_snr, receivers, gram_kind, precision, 0.5)) {
+    g_err[0] = 0;  // a size query reports a bad argument as 0 bytes, not as the thread's last error
+    return 0;
+  }
   return sweep_layout(nullptr, to_params(array), n_list, n_n, K, n_drops, n_snr, receivers, gram_kind, precision)
       .total;
 }
@@ -408,8 +421,8 @@ size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int6
 int xlmimo_saturation_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                             const xlmimo_users_t *users, const double *pos, int32_t K, int64_t n_drops, uint64_t seed,
                             const double *snr_db, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
-                            int32_t precision, double t, double *ergodic, int64_t *n_valid, double *sat,
-                            double *per_drop, void *ws, size_t ws_bytes, void *stream) {
+                            int32_t precision, double t, double *ergodic, int64_t *n_valid, double *ergodic_valid,
+                            double *sat, double *per_drop, void *ws, size_t ws_bytes, void *stream) {
   NvtxRange nvtx_range("xlmimo_saturation_sweep");
   g_err[0] = 0;
   int rc = validate_sweep(array, n_list, n_n, K, n_drops, snr_db, n_snr, receivers, gram_kind, precision, t);
@@ -417,21 +430,21 @@ int xlmimo_saturation_sweep(const xlmimo_array_t *array, const int64_t *n_list, 
   if (!pos && bad_users(users)) return xlh::set_error(XLMIMO_EINVAL, "sweep: no positions and invalid user law");
   if (!ergodic || !n_valid || !sat) return xlh::set_error(XLMIMO_EINVAL, "sweep: null output");
   return run_sweep(array, n_list, n_n, users, pos, nullptr, K, n_drops, seed, snr_db, n_snr, receivers, gram_kind,
-                   precision, t, ergodic, n_valid, sat, per_drop, ws, ws_bytes, (cudaStream_t)stream);
+                   precision, t, ergodic, n_valid, ergodic_valid, sat, per_drop, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                                  const double *pos_host, int32_t K, int64_t n_drops, const double *snr_db,
                                  int32_t n_snr, uint32_t receivers, int32_t gram_kind, int32_t precision, double t,
-                                 double *ergodic, int64_t *n_valid, double *sat, void *ws, size_t ws_bytes,
-                                 void *stream) {
+                                 double *ergodic, int64_t *n_valid, double *ergodic_valid, double *sat, void *ws,
+                                 size_t ws_bytes, void *stream) {
   NvtxRange nvtx_range("xlmimo_saturation_sweep_host");
   g_err[0] = 0;
   int rc = validate_sweep(array, n_list, n_n, K, n_drops, snr_db, n_snr, receivers, gram_kind, precision, t);
   if (rc) return rc;
   if (!pos_host || !ergodic || !n_valid || !sat) return xlh::set_error(XLMIMO_EINVAL, "sweep_host: null pointer");
   return run_sweep(array, n_list, n_n, nullptr, nullptr, pos_host, K, n_drops, 0, snr_db, n_snr, receivers, gram_kind,
-                   precision, t, ergodic, n_valid, sat, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+                   precision, t, ergodic, n_valid, ergodic_valid, sat, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
 // Every tile product runs on the FP64 tensor path: per 4-wide k-step 4 x 4 fragment
 // pairs x 4 real DMMA m8n8k4 (RR, II, IR, RI), the 64 accumulator registers of the
 // complex tile resident, operand fragments read straight from the slot (L2, prefetched
-// kPfDist k-steps ahead) with a one-step register double buffer.  DMMA and DFMA share
+// PFD k-steps ahead) with a one-step register double buffer.  DMMA and DFMA share
 // the FP64 pipe at the same FMA rate; the tensor path needs one
 // instruction per 256 FMAs and no shared-memory operand traffic.
 #ifndef XB_GRP

@@ -323,8 +323,8 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
                           cudaStream_t s);
 
 // xl_sweep.cu reductions
-int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, int64_t *count,
-                          cudaStream_t s);
+int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, double *mean_valid,
+                          int64_t *count, cudaStream_t s);
 size_t saturation_stats_scratch(int64_t n_drops);
 int launch_saturation_stats(const double *pos, int K, int64_t n_drops, double t, double pitch, double *sat,
                             double *scratch, cudaStream_t s);

@@ -5,7 +5,7 @@
 // A complex tile is held as DMMA accumulator fragments (64 registers per lane); a
 // k-step of 4 columns is 4 x 4 fragment pairs x 4 real DMMAs (RR, II, IR, RI).
 // Operand fragments are read straight from global memory (L2) with a one-step register
-// double buffer and an L2 prefetch kPfDist k-steps ahead.  DMMA and DFMA share the
+// double buffer and an L2 prefetch PFD k-steps ahead.  DMMA and DFMA share the
 // FP64 pipe at the same FMA rate; the tensor path needs one
 // instruction per 256 FMAs and no shared-memory operand traffic.
 #pragma once
@@ -82,21 +82,20 @@ __device__ __forceinline__ void frag_prefetch_l2(const double2 *Am, size_t lda, 
 // C += A (32 x 4 nkb, row-major, stride lda) * B (4 nkb x 32), B row-major (ldb) or, with
 // B_NT, B(k, n) = Bt(n, k) from a row-major Bt (stride ldb) (conjugated with CONJ_B).  The
 // fragments of k-step kb + 1 are loaded while kb's 64 DMMAs run, and (PF, operands in
-// global memory) the lines of k-step kb + kPfDist are pulled into L2 meanwhile.
-#ifndef XT_PFDIST
-#define XT_PFDIST 4  // measured: 4 vs 8 vs 16 -> K = 1000 receivers 31.4 / 32.4 / 35.7 ms, SYRK equal
-#endif
-constexpr int kPfDist = XT_PFDIST;
-template <bool B_NT, bool CONJ_B, bool PF, int MB = 4, int NB = 4>
+// global memory) the lines of k-step kb + PFD are pulled into L2 meanwhile.  PFD = 4
+// measured best for the Cholesky (K = 1000 receivers 31.4 / 32.4 / 35.7 ms at 4 / 8 / 16);
+// the SYRK's long slices pass 8 (737 vs 740 ms at E3).  A template parameter, so every
+// instantiation has one definition across translation units.
+template <bool B_NT, bool CONJ_B, bool PF, int MB = 4, int NB = 4, int PFD = 4>
 __device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ Am, size_t lda,
                                           const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
   if (PF)
-    for (int q = 0; q < kPfDist && q < nkb; q += 2) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, q, lane);
+    for (int q = 0; q < PFD && q < nkb; q += 2) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, q, lane);
   double2 a[4], b[4];
   frag_load<B_NT, MB, NB>(a, b, Am, lda, Bm, ldb, 0, lane);
 #pragma unroll 1
   for (int kb = 0; kb < nkb; ++kb) {
-    if (PF && !(kb & 1) && kb + kPfDist < nkb) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, kb + kPfDist, lane);
+    if (PF && !(kb & 1) && kb + PFD < nkb) frag_prefetch_l2<B_NT>(Am, lda, Bm, ldb, kb + PFD, lane);
     double2 an[4], bn[4];
     frag_load<B_NT, MB, NB>(an, bn, Am, lda, Bm, ldb, kb + 1 < nkb ? kb + 1 : kb, lane);
     ctile_step<CONJ_B, MB, NB>(c, a, b);

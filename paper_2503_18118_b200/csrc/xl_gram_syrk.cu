@@ -18,7 +18,6 @@
 #include <type_traits>
 
 #include "xl_common.cuh"
-#define XT_PFDIST 8  // long slices: prefetch further ahead (737 vs 740 ms at E3 with 4)
 #include "xl_dmma_tile.cuh"
 
 namespace {
@@ -144,7 +143,7 @@ __global__ void __launch_bounds__(32 * kSyrkWarps, 1)
     constexpr int MB = decltype(mb)::value, NB = decltype(nb)::value;
     CTile c;
     ctile_load<false, MB, NB>(c, pt, kTile, lane);
-    ctile_mma<true, true, true, MB, NB>(c, A, CH, Bm, CH, chs / 4, lane);
+    ctile_mma<true, true, true, MB, NB, 8>(c, A, CH, Bm, CH, chs / 4, lane);  // long slices: prefetch 8 ahead
     ctile_store<false, MB, NB>(c, pt, kTile, lane);
   };
   using I1 = std::integral_constant<int, 1>;

@@ -1,6 +1,8 @@
 // xl_sweep.cu -- a6: ergodic reductions of the saturation sweep.
-//  * ergodic_reduce_kernel: mean over drops of each (N, SNR, receiver) column,
-//    excluding NaN, with the valid count (R10); fixed-order block reduction.
+//  * ergodic_reduce_kernel: per (N, SNR, receiver) column, fixed-order block reduction
+//    (R10): the valid (non-NaN) count, the mean over the valid drops (conditional mean)
+//    and the ergodic mean over ALL drops -- defined only when every drop is valid, NaN
+//    otherwise (an expectation over a subset of the drops is not the ergodic value).
 //  * sat_partial_kernel + sat_final_kernel: per-drop Eqs. (13)-(16)
 //      y_up = max_i (x_i t/sqrt(1-t^2) + y_i),  y_down = min_i (-x_i t/sqrt(1-t^2) + y_i),
 //    their means over drops, M_sat = ceil((E[y_up] - E[y_down]) / pitch) (R15) and
@@ -12,7 +14,8 @@ namespace {
 constexpr int kRedThreads = 256;
 
 __global__ void __launch_bounds__(kRedThreads) ergodic_reduce_kernel(const double *per_drop, int64_t n_drops,
-                                                                     int n_out, double *mean, int64_t *count) {
+                                                                     int n_out, double *mean, double *mean_valid,
+                                                                     int64_t *count) {
   __shared__ double ss[kRedThreads];
   __shared__ long long sc[kRedThreads];
   const int col = blockIdx.x;
@@ -34,7 +37,9 @@ __global__ void __launch_bounds__(kRedThreads) ergodic_reduce_kernel(const doubl
   }
   if (threadIdx.x == 0) {
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    mean[col] = sc[0] ? ss[0] / (double)sc[0] : nan;
+    const double cond = sc[0] ? ss[0] / (double)sc[0] : nan;
+    mean[col] = sc[0] == n_drops ? cond : nan;
+    mean_valid[col] = cond;
     count[col] = sc[0];
   }
 }
@@ -91,11 +96,11 @@ __global__ void sat_final_kernel(const double *part, int nb, int64_t n_drops, do
 
 namespace xlh {
 
-int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, int64_t *count,
-                          cudaStream_t s) {
+int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, double *mean_valid,
+                          int64_t *count, cudaStream_t s) {
   if (n_out == 0) return XLMIMO_OK;
   KTimer tm(s, "ergodic_reduce");
-  ergodic_reduce_kernel<<<n_out, kRedThreads, 0, s>>>(per_drop, n_drops, n_out, mean, count);
+  ergodic_reduce_kernel<<<n_out, kRedThreads, 0, s>>>(per_drop, n_drops, n_out, mean, mean_valid, count);
   tm.stop(s);
   count_launch();
   return check_launch("ergodic_reduce_kernel");

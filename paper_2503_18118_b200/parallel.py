@@ -28,7 +28,7 @@ def shard_range(total_drops: int, rank: int, world: int):
 def pack_sweep(res: dict, n_drops: int, pitch: float) -> np.ndarray:
     """Per-rank partial sums: [sum_k (mean*count) ..., counts ..., D, D*E_up, D*E_dn,
     sum of extent/pitch, sum of (extent/pitch)^2]."""
-    erg = np.nan_to_num(np.asarray(res["ergodic"], dtype=np.float64), nan=0.0).ravel()
+    erg = np.nan_to_num(np.asarray(res["ergodic_valid"], dtype=np.float64), nan=0.0).ravel()
     cnt = np.asarray(res["n_valid"], dtype=np.float64).ravel()
     sat = np.asarray(res["sat"], dtype=np.float64)
     D = float(n_drops)
@@ -43,11 +43,13 @@ def unpack_sweep(v: np.ndarray, shape, pitch: float) -> dict:
     sums, cnt = v[:n], v[n:2 * n]
     D, su, sd, se, s2 = v[2 * n:2 * n + 5]
     with np.errstate(invalid="ignore", divide="ignore"):
-        erg = np.where(cnt > 0, sums / np.maximum(cnt, 1), np.nan)
+        ergv = np.where(cnt > 0, sums / np.maximum(cnt, 1), np.nan)
+    erg = np.where(cnt == D, ergv, np.nan)      # R10: ergodic only when every drop of every rank is valid
     eu, ed, me = su / D, sd / D, se / D
     var = (s2 - D * me * me) / (D - 1.0) if D > 1 else 0.0
     sat = np.array([eu, ed, math.ceil((eu - ed) / pitch), math.sqrt(max(var, 0.0)) / math.sqrt(D)])
-    return {"ergodic": erg.reshape(shape), "n_valid": cnt.reshape(shape).astype(np.int64), "sat": sat}
+    return {"ergodic": erg.reshape(shape), "ergodic_valid": ergv.reshape(shape),
+            "n_valid": cnt.reshape(shape).astype(np.int64), "sat": sat}
 
 
 def allreduce_sweep(res: dict, n_drops: int, dist, device, pitch: float | None = None) -> dict:

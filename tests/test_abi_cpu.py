@@ -62,6 +62,10 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     assert L.xlmimo_gen_drops(ctypes.byref(u), 0, 10, 0, 0, ctypes.c_void_p(8), None) == -1
     upa = xl.Array.upa(8, 8, 100e9)
     assert L.xlmimo_gram_closed_form(ctypes.byref(upa), ctypes.c_void_p(8), 4, 1, ctypes.c_void_p(8), None, None) == -2
+    ula_wide = xl.Array.ula(256, 28e9, spacing_wl=0.7)   # Eq. (4) is the lambda/2 array's
+    assert L.xlmimo_gram_closed_form(ctypes.byref(ula_wide), ctypes.c_void_p(8), 4, 1, ctypes.c_void_p(8), None,
+                                     None) == -2
+    assert b"lambda/2" in L.xlmimo_last_error()
     ula = xl.Array.ula(256, 28e9)
     assert L.xlmimo_gram_exact(ctypes.byref(ula), ctypes.c_void_p(8), 1025, 1, 0, 0, ctypes.c_void_p(8), None, 0,
                                None) == -2
@@ -98,16 +102,23 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     sat = np.zeros(4)
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
     assert L.xlmimo_saturation_sweep(ctypes.byref(ula), p(nl), 3, ctypes.byref(u), None, 4, 10, 0, p(snr), 1, 1, 0, 0,
-                                     0.9, p(erg), p(nv), p(sat), None, None, 0, None) == -1
+                                     0.9, p(erg), p(nv), None, p(sat), None, None, 0, None) == -1
     nl = np.array([512, 256], dtype=np.int64)  # not ascending
     assert L.xlmimo_saturation_sweep(ctypes.byref(ula), p(nl), 2, ctypes.byref(u), None, 4, 10, 0, p(snr), 1, 1, 0, 0,
-                                     0.9, p(erg), p(nv), p(sat), None, None, 0, None) == -1
+                                     0.9, p(erg), p(nv), None, p(sat), None, None, 0, None) == -1
     nl = np.array([256, 512], dtype=np.int64)
     assert L.xlmimo_saturation_sweep(ctypes.byref(ula), p(nl), 2, ctypes.byref(u), None, 4, 10, 0, p(snr), 1, 1, 0, 0,
-                                     1.0, p(erg), p(nv), p(sat), None, None, 0, None) == -1  # t not in (0,1)
+                                     1.0, p(erg), p(nv), None, p(sat), None, None, 0, None) == -1  # t not in (0,1)
     assert L.xlmimo_saturation_sweep(ctypes.byref(ula), p(nl), 2, ctypes.byref(u), None, 4, 10, 0, p(snr), 1, 1, 0, 0,
-                                     0.9, p(erg), p(nv), p(sat), None, None, 0, None) == -3  # no workspace
+                                     0.9, p(erg), p(nv), None, p(sat), None, None, 0, None) == -3  # no workspace
     assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 1, 1) > 0
+    # the size query validates like the call: bad arguments size to 0, never to a wrapped value
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, -1, 1) == 0          # n_snr < 1
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 17, 1) == 0          # n_snr > 16
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 1, 0) == 0           # no receiver
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 1, 16) == 0          # unknown receiver bit
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 1, 1, gram_kind=7) == 0
+    assert xl.sweep_workspace_bytes(ula, nl, 4, 10, 1, 1, precision=5) == 0
 
 
 def test_workspace_queries_are_pure(lib):

@@ -137,7 +137,7 @@ def test_drops_closed_form_and_sweep_write_in_bounds(xl):
     ws = _ws(need)
     f = lambda arr: arr.ctypes.data_as(ctypes.c_void_p)
     rc = xl._L.xlmimo_saturation_sweep(ctypes.byref(a), f(nl), 3, None, p.ptr(), K, D, 0, f(snr), 3, 7, 0, 0, 0.9,
-                                       f(erg), f(nv), f(sat), pd.ptr(), ws.ptr(), need, None)
+                                       f(erg), f(nv), None, f(sat), pd.ptr(), ws.ptr(), need, None)
     assert rc == 0, xl._L.xlmimo_last_error()
     pd.check()
     ws.check()

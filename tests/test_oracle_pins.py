@@ -57,6 +57,33 @@ def test_gen_drops_law_and_determinism(orc):
     assert np.array_equal(orc.gen_drops(u, 8, 100, seed=7, first_drop=1000), p1[1000:1100])
 
 
+def test_gen_drops_upa_elevation_law(orc):
+    """R3/R5 (UPA users of config 4): |p| = r ~ U[r_min, r_max], elevation asin(z/|p|) ~ U[el_min,
+    el_max], azimuth atan2(y, x) ~ U[az_min, az_max] (x = r cos el cos az, y = r cos el sin az,
+    z = r sin el), each independent.  Asymmetric ranges so a swapped sign, a swapped angle or a
+    degree/radian slip moves a mean by many standard errors; a KS test for the uniform law."""
+    from scipy import stats
+    r_rng, az_rng, el_rng = (2.0, 20.0), (-20.0, 60.0), (-10.0, 40.0)
+    p = orc.gen_drops(orc.users(r=r_rng, az=az_rng, el=el_rng), 32, 2000, seed=5)
+    r = np.sqrt(np.sum(p * p, axis=-1)).ravel()
+    el = np.degrees(np.arcsin(p[..., 2].ravel() / r))
+    az = np.degrees(np.arctan2(p[..., 1], p[..., 0])).ravel()
+    assert r.min() >= r_rng[0] * (1 - 1e-14) and r.max() <= r_rng[1] * (1 + 1e-14)
+    assert el.min() >= el_rng[0] - 1e-9 and el.max() <= el_rng[1] + 1e-9
+    assert az.min() >= az_rng[0] - 1e-9 and az.max() <= az_rng[1] + 1e-9
+    n = r.size
+    for v, (a, b) in ((r, r_rng), (el, el_rng), (az, az_rng)):
+        se = (b - a) / math.sqrt(12) / math.sqrt(n)
+        assert abs(v.mean() - 0.5 * (a + b)) < 4 * se
+        assert stats.kstest(v, "uniform", args=(a, b - a)).pvalue > 1e-4
+    # independence of the three draws (Philox words 0/1/2): correlations within 4 / sqrt(n)
+    c = np.corrcoef(np.stack([r, el, az]))
+    assert np.all(np.abs(c[np.triu_indices(3, 1)]) < 4 / math.sqrt(n))
+    # the elevation plane: cos(el) scales the horizontal projection, x > 0 always (same side)
+    assert np.all(p[..., 0] > 0)
+    np.testing.assert_allclose(np.hypot(p[..., 0], p[..., 1]).ravel(), r * np.cos(np.radians(el)), rtol=1e-12)
+
+
 # --------------------------------------------------------------------------- a2: geometry + channel
 @pytest.mark.parametrize("ex", GOLD["element_y"])
 def test_element_coordinates_spec_examples(orc, ex):
@@ -492,6 +519,61 @@ def test_capacity_saturates_in_n(orc):
     # faster convergence at higher SNR
     assert norm[4, 2] >= norm[4, 0]
     assert sat[2] == math.ceil((sat[0] - sat[1]) / (C / 28e9 / 2))
+
+
+def test_sweep_statistics_with_invalid_drops(orc):
+    """R10 / PAPER.md:177-178, 228: the sweep's reductions, pinned against numpy on its own
+    per-drop table.  cfg1 geometry through the closed-form Gram (SURVEY.md:582 Q10: ~39 % of
+    the drops have an indefinite G~ at N = 256, so their ZF rate is NaN):
+      n_valid       = the count of non-NaN per-drop rates in each (N, SNR, receiver) column;
+      ergodic       = the plain mean over ALL drops when the column has no NaN, else NaN
+                      (an expectation over a subset of the drops is not the ergodic value);
+      ergodic_valid = the mean over the non-NaN drops (conditional mean);
+      sat[0], sat[1]= E[y_up], E[y_down]: means over drops of the per-drop Eqs. (13)-(16),
+                      here re-derived geometrically -- y_up_i is the element coordinate seen
+                      from user i at sin(angle) = t, (y_up_i - y_i)/hypot(x_i, y_up_i - y_i) = t;
+      sat[2]        = ceil((E[y_up] - E[y_down]) / pitch)  (M_sat, PAPER.md:228);
+      sat[3]        = std(extent/pitch, ddof=1)/sqrt(D), extent = y_up - y_down per drop."""
+    lam = C / 28e9
+    pitch = lam / 2
+    t = 0.9
+    D = 300
+    pos = orc.gen_drops(orc.users(r=(5.0, 50.0), az=(-60.0, 60.0)), 4, D, seed=3)
+    nl = [64, 128, 256]
+    rec = orc.RECV_CAP | orc.RECV_ZF | orc.RECV_MMSE
+    arr = orc.array("ula", n_y=256, fc_hz=28e9)
+    erg, nv, sat, pd, ergv = orc.saturation_sweep(arr, nl, pos, [0.0, 10.0], rec, gram_kind=1, t=t,
+                                                  per_drop=True, valid_mean=True)
+    assert pd.shape == (D, 3, 2, 3)
+    ok = ~np.isnan(pd)
+    np.testing.assert_array_equal(nv, ok.sum(axis=0))
+    assert np.any(nv < D)                              # NaN drops are exercised (full columns below)
+    with np.errstate(invalid="ignore"):
+        np.testing.assert_allclose(ergv, np.nanmean(pd, axis=0), rtol=1e-13, atol=0)
+    full = nv == D
+    np.testing.assert_allclose(erg[full], pd.mean(axis=0)[full], rtol=1e-13, atol=0)
+    assert np.all(np.isnan(erg[~full]))
+    # the same per-drop table with the exact Gram has no NaN: ergodic == ergodic_valid == mean
+    erg_x, nv_x, sat_x, pd_x, ergv_x = orc.saturation_sweep(arr, nl, pos[:40], [10.0], rec, t=t, per_drop=True,
+                                                            valid_mean=True)
+    assert np.all(nv_x == 40)
+    np.testing.assert_allclose(erg_x, pd_x.mean(axis=0), rtol=1e-13)
+    np.testing.assert_array_equal(erg_x, ergv_x)
+    # saturation statistics from the geometry
+    x = np.hypot(pos[..., 0], pos[..., 2])
+    y = pos[..., 1]
+    off = x * t / math.sqrt(1 - t * t)
+    up_i, dn_i = y + off, y - off
+    np.testing.assert_allclose((up_i - y) / np.hypot(x, up_i - y), t, rtol=1e-12)
+    np.testing.assert_allclose((y - dn_i) / np.hypot(x, y - dn_i), t, rtol=1e-12)
+    up, dn = up_i.max(axis=1), dn_i.min(axis=1)
+    ext = (up - dn) / pitch
+    assert sat[0] == pytest.approx(up.mean(), rel=1e-13)
+    assert sat[1] == pytest.approx(dn.mean(), rel=1e-13)
+    assert sat[2] == math.ceil((up.mean() - dn.mean()) / pitch)
+    assert sat[3] == pytest.approx(np.std(ext, ddof=1) / math.sqrt(D), rel=1e-9)
+    # sat is geometry only: the exact sweep on the first 40 drops gives their own M_sat
+    assert sat_x[2] == math.ceil((up[:40].mean() - dn[:40].mean()) / pitch)
 
 
 def test_upa_diagonal_solid_angle(orc):

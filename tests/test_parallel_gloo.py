@@ -23,10 +23,11 @@ def _free_port():
     return p
 
 
-def _sweep_result(orc, pos, n_list, snr, recv, lam):
+def _sweep_result(orc, pos, n_list, snr, recv, lam, gram_kind=0):
     a = orc.array("ula", n_y=max(n_list), fc_hz=28e9)
-    erg, nv, sat, _ = orc.saturation_sweep(a, n_list, pos, snr, recv, nthreads=1)
-    return {"ergodic": erg, "n_valid": nv, "sat": sat}
+    erg, nv, sat, _, ergv = orc.saturation_sweep(a, n_list, pos, snr, recv, gram_kind=gram_kind, nthreads=1,
+                                                 valid_mean=True)
+    return {"ergodic": erg, "n_valid": nv, "ergodic_valid": ergv, "sat": sat}
 
 
 def _worker(rank, world, port, out_q):
@@ -37,10 +38,13 @@ def _worker(rank, world, port, out_q):
     first, n = parallel.shard_range(total, rank, world)
     pos = orc.gen_drops(orc.users(r=(3.0, 30.0)), 4, n, seed=5, first_drop=first)
     lam = 299792458.0 / 28e9
-    res = _sweep_result(orc, pos, [64, 128, 256], [0.0, 10.0], 7, lam)
-    comb = parallel.allreduce_sweep(res, n, dist, torch.device("cpu"), pitch=lam / 2)
+    out = {}
+    for gk in (0, 1):   # exact; closed form (cfg1-like drops with NaN ZF rates, R10)
+        res = _sweep_result(orc, pos, [64, 128, 256], [0.0, 10.0], 7, lam, gram_kind=gk)
+        comb = parallel.allreduce_sweep(res, n, dist, torch.device("cpu"), pitch=lam / 2)
+        out[gk] = {k: np.asarray(v) for k, v in comb.items()}
     if rank == 0:
-        out_q.put({k: np.asarray(v) for k, v in comb.items()})
+        out_q.put(out)
     dist.destroy_process_group()
 
 
@@ -60,6 +64,7 @@ def test_pack_unpack_single_rank_identity(orc):
     res = _sweep_result(orc, pos, [64, 128], [10.0], 7, lam)
     back = parallel.unpack_sweep(parallel.pack_sweep(res, 10, lam / 2), res["ergodic"].shape, lam / 2)
     assert np.allclose(back["ergodic"], res["ergodic"], rtol=1e-13)
+    assert np.allclose(back["ergodic_valid"], res["ergodic_valid"], rtol=1e-13)
     assert np.array_equal(back["n_valid"], res["n_valid"])
     assert np.allclose(back["sat"], res["sat"], rtol=1e-10)
 
@@ -77,8 +82,14 @@ def test_two_rank_combine_equals_single_rank(orc):
         assert p.exitcode == 0
     pos = orc.gen_drops(orc.users(r=(3.0, 30.0)), 4, 36, seed=5)
     lam = 299792458.0 / 28e9
-    ref = _sweep_result(orc, pos, [64, 128, 256], [0.0, 10.0], 7, lam)
-    assert np.allclose(comb["ergodic"], ref["ergodic"], rtol=1e-12, atol=1e-12)
-    assert np.array_equal(comb["n_valid"], ref["n_valid"])
-    assert np.allclose(comb["sat"][[0, 1, 3]], ref["sat"][[0, 1, 3]], rtol=1e-9)
-    assert comb["sat"][2] == ref["sat"][2]
+    for gk in (0, 1):
+        ref = _sweep_result(orc, pos, [64, 128, 256], [0.0, 10.0], 7, lam, gram_kind=gk)
+        c = comb[gk]
+        np.testing.assert_array_equal(np.isnan(c["ergodic"]), np.isnan(ref["ergodic"]))
+        assert np.allclose(c["ergodic"], ref["ergodic"], rtol=1e-12, atol=1e-12, equal_nan=True)
+        assert np.allclose(c["ergodic_valid"], ref["ergodic_valid"], rtol=1e-12, atol=1e-12, equal_nan=True)
+        assert np.array_equal(c["n_valid"], ref["n_valid"])
+        assert np.allclose(c["sat"][[0, 1, 3]], ref["sat"][[0, 1, 3]], rtol=1e-9)
+        assert c["sat"][2] == ref["sat"][2]
+        if gk == 1:
+            assert np.any(ref["n_valid"] < 36)       # the strict-NaN rule is exercised across ranks

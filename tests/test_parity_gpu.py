@@ -252,13 +252,17 @@ def test_sweep_closed_form_parity(xl, orc):
     res = xl.saturation_sweep(ag, w.n_list, w.K, D, w.snr_db, 15, users=ug, seed=1, gram_kind=xl.GRAM_CLOSED_FORM,
                               per_drop=True)
     pos = xl.gen_drops(ug, w.K, D, seed=1).cpu().numpy()
-    erg, nv, sat, pd = orc.saturation_sweep(ao, w.n_list, pos, w.snr_db, 15, gram_kind=1, per_drop=True)
+    erg, nv, sat, pd, ergv = orc.saturation_sweep(ao, w.n_list, pos, w.snr_db, 15, gram_kind=1, per_drop=True,
+                                                  valid_mean=True)
     g = res["per_drop"].cpu().numpy()
     assert np.array_equal(np.isnan(g), np.isnan(pd))
     ok = ~np.isnan(pd)
     assert np.max(np.abs(g[ok] - pd[ok])) <= 1e-6
     assert np.array_equal(res["n_valid"], nv)
+    assert np.array_equal(np.isnan(res["ergodic"]), np.isnan(erg))          # R10: NaN iff some drop is NaN
+    assert np.array_equal(np.isnan(res["ergodic"]), nv < D)
     assert np.allclose(res["ergodic"], erg, atol=1e-6, equal_nan=True)
+    assert np.allclose(res["ergodic_valid"], ergv, atol=1e-6, equal_nan=True)
 
 
 def test_sweep_full_cfg2_properties_and_sampled_drops(xl, orc):
@@ -427,15 +431,18 @@ def test_sweep_cfg2_closed_form_every_drop_vs_oracle(xl, orc):
     pos_d = xl.gen_drops(ug, w.K, w.n_drops, seed=w.seed)
     res = xl.saturation_sweep(ag, w.n_list, w.K, w.n_drops, w.snr_db, w.receivers, pos=pos_d,
                               gram_kind=xl.GRAM_CLOSED_FORM, per_drop=True)
-    erg, nv, _, pdo = orc.saturation_sweep(orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz), w.n_list,
-                                           pos_d.cpu().numpy(), w.snr_db, w.receivers, gram_kind=1, per_drop=True)
+    erg, nv, _, pdo, ergv = orc.saturation_sweep(orc.array("ula", n_y=w.n_y, fc_hz=w.fc_hz), w.n_list,
+                                                 pos_d.cpu().numpy(), w.snr_db, w.receivers, gram_kind=1,
+                                                 per_drop=True, valid_mean=True)
     pd = res["per_drop"].cpu().numpy()
     assert np.array_equal(np.isnan(pd), np.isnan(pdo))
     assert np.isnan(pdo).any() and (~np.isnan(pdo)).any()
     ok = ~np.isnan(pdo)
     assert np.max(np.abs(pd[ok] - pdo[ok])) <= 1e-6
     assert np.array_equal(res["n_valid"], nv)
+    assert np.array_equal(np.isnan(res["ergodic"]), np.isnan(erg))
     assert np.nanmax(np.abs(res["ergodic"] - erg)) <= 1e-6
+    assert np.nanmax(np.abs(res["ergodic_valid"] - ergv)) <= 1e-6
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mat32"])
