@@ -250,6 +250,28 @@ XLMIMO_API int xlmimo_sum_rate_mismatched(const double *gram, const double *gram
 XLMIMO_API int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, double y_max, int32_t K,
                                      int64_t n_drops, uint64_t seed, uint64_t first_drop, double *pos, void *stream);
 
+/* ------------------------------------------------------------------------- path options
+ * Kernel-path overrides for A/B tests and tuning.  Process-global, 0 = automatic (the
+ * measured default) for every option; they select WHICH kernel runs, never what is
+ * computed: every choice meets the same parity tier.  Not for concurrent use with
+ * running entry points.  The library reads no environment variables.
+ *   XLMIMO_OPT_LARGE_K      fp64 Gram for 64 < K: 1 block pairs, 2 chunked SYRK
+ *   XLMIMO_OPT_PAIR         fp32 Gram for 64 < K: 1 operands generated in-kernel, 2 TMA-fed chunks
+ *   XLMIMO_OPT_GRAM_KERNEL  fused Gram, K <= 64: 1 split (K in {4,8}, ULA, fp64), 2 DMMA (K <= 16,
+ *                           fp64), 3 CUDA-core register/tile kernels, 4 64-bit-index DMMA (K > 16)
+ *   XLMIMO_OPT_SPLIT_NT     split kernel block variant: 64, 128, 192 (128 x 3/SM) or 256
+ *   XLMIMO_OPT_DMMA_VARIANT DMMA kernel block shape 0..3 (xl_gram.cu, mma_variant)
+ *   XLMIMO_OPT_MT2_BUFFERS  DMMA K = 17..64 tile buffers: 2 or 3
+ *   XLMIMO_OPT_STREAM       materialised fp32 stream: 1 CUDA cores instead of tcgen05
+ * Returns XLMIMO_OK, or EINVAL for an unknown option (value not range-checked: an
+ * out-of-range value means automatic). */
+enum {
+    XLMIMO_OPT_LARGE_K = 0, XLMIMO_OPT_PAIR = 1, XLMIMO_OPT_GRAM_KERNEL = 2, XLMIMO_OPT_SPLIT_NT = 3,
+    XLMIMO_OPT_DMMA_VARIANT = 4, XLMIMO_OPT_MT2_BUFFERS = 5, XLMIMO_OPT_STREAM = 6, XLMIMO_OPT_COUNT = 7
+};
+XLMIMO_API int xlmimo_set_option(int32_t option, int64_t value);
+XLMIMO_API int64_t xlmimo_get_option(int32_t option);
+
 /* Thread-local text of the last non-zero return on this thread ("" if none). */
 XLMIMO_API const char *xlmimo_last_error(void);
 

@@ -24,13 +24,17 @@ __all__ = ["Array", "Users", "gen_drops", "gram_exact", "gram_closed_form", "sum
            "gen_drops_rect", "app_a_bounds", "saturation_sweep",
            "saturation_sweep_host", "launch_count", "lib_path", "XlmimoError",
            "ULA", "UPA", "FP64", "FP32", "FUSED", "MATERIALIZED", "GRAM_EXACT", "GRAM_CLOSED_FORM",
-           "RECV_CAP", "RECV_ZF", "RECV_MMSE", "RECV_MRC", "n_recv"]
+           "RECV_CAP", "RECV_ZF", "RECV_MMSE", "RECV_MRC", "n_recv", "option", "set_option", "get_option",
+           "OPT_LARGE_K", "OPT_PAIR", "OPT_GRAM_KERNEL", "OPT_SPLIT_NT", "OPT_DMMA_VARIANT", "OPT_MT2_BUFFERS",
+           "OPT_STREAM"]
 
 ULA, UPA = 0, 1
 FP64, FP32 = 0, 1
 FUSED, MATERIALIZED = 0, 1
 GRAM_EXACT, GRAM_CLOSED_FORM = 0, 1
 RECV_CAP, RECV_ZF, RECV_MMSE, RECV_MRC = 1, 2, 4, 8
+(OPT_LARGE_K, OPT_PAIR, OPT_GRAM_KERNEL, OPT_SPLIT_NT, OPT_DMMA_VARIANT, OPT_MT2_BUFFERS,
+ OPT_STREAM) = range(7)
 FLAG_G_NOT_PD, FLAG_A_NOT_PD, FLAG_MRC_UNDEF, FLAG_DEGENERATE, FLAG_NONFINITE = 1, 2, 4, 8, 16
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -101,6 +105,10 @@ def _load():
     L.xlmimo_sum_rate_mismatched.restype = ctypes.c_int
     L.xlmimo_gen_drops_rect.argtypes = [d, d, d, d, i32, i64, u64, u64, vp, vp]
     L.xlmimo_gen_drops_rect.restype = ctypes.c_int
+    L.xlmimo_set_option.argtypes = [i32, i64]
+    L.xlmimo_set_option.restype = ctypes.c_int
+    L.xlmimo_get_option.argtypes = [i32]
+    L.xlmimo_get_option.restype = i64
     L.xlmimo_timing_enable.argtypes = [i32]
     L.xlmimo_timing_read.argtypes = [i32, ctypes.c_char_p, vp, vp]
     L.xlmimo_last_error.restype = ctypes.c_char_p
@@ -177,6 +185,31 @@ def _f64_host(x):
 
 def n_recv(receivers: int) -> int:
     return bin(int(receivers) & 15).count("1")
+
+
+def set_option(opt: int, value: int):
+    """Kernel-path override (include/xlmimo.h, "path options"); 0 = automatic."""
+    _check(_L.xlmimo_set_option(opt, int(value)), "xlmimo_set_option")
+
+
+def get_option(opt: int) -> int:
+    return int(_L.xlmimo_get_option(opt))
+
+
+class option:
+    """``with option(OPT_LARGE_K, 2): ...`` -- set a path override for a block, then restore it."""
+
+    def __init__(self, opt: int, value: int):
+        self.opt, self.value = opt, value
+
+    def __enter__(self):
+        self.prev = get_option(self.opt)
+        set_option(self.opt, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.opt, self.prev)
+        return False
 
 
 def launch_count() -> int:

@@ -26,6 +26,7 @@ struct NvtxRange {
   ~NvtxRange() { nvtxRangePop(); }
 };
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int64_t> g_opts[XLMIMO_OPT_COUNT];
 
 bool bad_array(const xlmimo_array_t *a) {
   if (!a) return true;
@@ -447,4 +448,19 @@ int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const int64_t *n_l
                    precision, t, ergodic, n_valid, ergodic_valid, sat, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int xlmimo_set_option(int32_t option, int64_t value) {
+  g_err[0] = 0;
+  if (option < 0 || option >= XLMIMO_OPT_COUNT) return xlh::set_error(XLMIMO_EINVAL, "set_option: %d", option);
+  g_opts[option].store(value);
+  return XLMIMO_OK;
+}
+
+int64_t xlmimo_get_option(int32_t option) {
+  return (option < 0 || option >= XLMIMO_OPT_COUNT) ? 0 : g_opts[option].load();
+}
+
 }  // extern "C"
+
+namespace xlh {
+int64_t option(int id) { return xlmimo_get_option(id); }
+}  // namespace xlh

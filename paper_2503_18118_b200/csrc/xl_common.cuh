@@ -40,48 +40,6 @@ __device__ __forceinline__ u64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_
 __device__ __forceinline__ double u01_53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
 
 // ---------------------------------------------------------------------------
-// sin/cos of 2*pi*f for f in [-1/2, 1/2] (the fp64-reduced phase fraction).
-// Quadrant split k = rint(4f), g = f - k/4 (exact), |2 pi g| <= pi/4, then the
-// Taylor series of sin to theta^15 and cos to theta^16 in g with the (2pi)^n/n!
-// folded into the coefficients: truncation < 5e-17 absolute (K2).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void sincos2pi_reduced(double f, double &s, double &c) {
-  const double k = rint(4.0 * f);
-  const double g = fma(-0.25, k, f);
-  const double g2 = g * g;
-  double ps = -7.1812230177850051223e-1;
-  ps = fma(ps, g2, 3.8199525848482821277);
-  ps = fma(ps, g2, -1.5094642576822990392e+1);
-  ps = fma(ps, g2, 4.2058693944897653145e+1);
-  ps = fma(ps, g2, -7.6705859753061385842e+1);
-  ps = fma(ps, g2, 8.1605249276075054203e+1);
-  ps = fma(ps, g2, -4.1341702240399760234e+1);
-  ps = fma(ps, g2, 6.2831853071795864769);
-  const double sn = ps * g;
-  double pc = 0.28200596845579121507;
-  pc = fma(pc, g2, -1.7143907110886720654);
-  pc = fma(pc, g2, 7.9035363713184688042);
-  pc = fma(pc, g2, -26.426256783374397453);
-  pc = fma(pc, g2, 60.244641371876660363);
-  pc = fma(pc, g2, -85.456817206693727736);
-  pc = fma(pc, g2, 64.939394022668291491);
-  pc = fma(pc, g2, -19.739208802178717238);
-  const double cs = fma(pc, g2, 1.0);
-  const int q = ((int)k) & 3;  // 2 pi f = 2 pi g + q pi/2
-  // q=0: (cs, sn); q=1: (-sn, cs); q=2: (-cs, -sn); q=3: (sn, -cs)  -> (cos, sin)
-  const double c1 = (q & 1) ? sn : cs;
-  const double s1 = (q & 1) ? cs : sn;
-  c = (q == 1 || q == 2) ? -c1 : c1;
-  s = (q >= 2) ? -s1 : s1;
-}
-
-// fp32 variant for the XLMIMO_FP32 path: f is the fp64-reduced fraction cast to
-// fp32 (R13); MUFU sin/cos after the same exact quadrant split.
-__device__ __forceinline__ void sincos2pi_reduced_f32(float f, float &s, float &c) {
-  __sincosf(6.28318530717958647692f * f, &s, &c);
-}
-
-// ---------------------------------------------------------------------------
 // Per-user constants of Eq. (3) for the fused generator.
 //   ULA: r^2 = xz2 + (y_user - y_m)^2 with xz2 = x^2 + z^2 (R21), amplitude
 //        sqrt(beta0) sqrt(x_eff) r^{-3/2} with x_eff = sqrt(xz2).
@@ -126,14 +84,10 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // Near-minimax polynomials (Chebyshev-node least squares, fitted in 50-digit
 // arithmetic) in u = g^2 for g in [-1/2, 1/2]:
 //   sin(pi/2 g) = g * S(u)  (degree 5, |err| <= 3.4e-15),
-//   cos(pi/2 g) = C(u)      (degree 6, |err| <= 1.1e-16).
+//   cos(pi/2 g) = C5(u)     (degree 5, |err| <= 5.6e-14).
 __constant__ double kSinPoly[6] = {1.5707963267948898981, -0.64596409750431005807, 0.079692626155777645619,
                                    -0.0046817525918122076931, 0.0001604292666631208935,
                                    -3.5563888496214387972e-6};
-__constant__ double kCosPoly[7] = {0.99999999999999995287, -1.2337005501361513498, 0.25366950789986513871,
-                                   -0.020863480734953519901, 0.0009192599500952791151,
-                                   -0.000025200135454917479526, 4.6552987291490935821e-7};
-//   cos(pi/2 g) = C5(u) (degree 5, |err| <= 5.6e-14): used by coef_fast.
 __constant__ double kCosPoly5[6] = {0.99999999999994445739, -1.23370055012016865, 0.25366950715400581474,
                                     -0.020863468005621057384, 0.00091916175238771112641,
                                     -0.000024850988050231297507};
@@ -190,13 +144,9 @@ __device__ __forceinline__ void coef_fast(double r2, double amp, double c4, doub
   im = a * s;
 }
 
-// Previous generator (kept for the general-K kernels until they move to coef_fast).
-__device__ __forceinline__ void coef_from_r2(double r2, double amp, double inv_lambda, double &re,
-                                             double &im) {
-  coef_fast(r2, amp, 4.0 * inv_lambda, re, im);
-}
-
-// fp32 phasor and amplitude from fp64 distance / phase reduction (XLMIMO_FP32, K3).
+// fp32 phasor and amplitude from fp64 distance / phase reduction (XLMIMO_FP32, K3):
+// f = frac(r / lambda) in [-1/2, 1/2] reduced in fp64 (R13), then MUFU sin/cos of
+// 2 pi f in fp32 (no quadrant split: MUFU takes the whole [-pi, pi] range).
 __device__ __forceinline__ void coef_from_r2_f32(double r2, double amp, double inv_lambda, float &re,
                                                  float &im) {
   const double ir = rsqrt_nr(r2);
@@ -204,7 +154,7 @@ __device__ __forceinline__ void coef_from_r2_f32(double r2, double amp, double i
   const double q = r * inv_lambda;
   const float f = (float)(q - rint(q));
   float s, c;
-  sincos2pi_reduced_f32(f, s, c);
+  __sincosf(6.28318530717958647692f * f, &s, &c);
   const float rf = (float)r;
   const float a = (float)amp * rsqrtf(rf) / rf;
   re = a * c;
@@ -323,6 +273,7 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
                           cudaStream_t s);
 
 // xl_sweep.cu reductions
+int64_t option(int id);  // xlmimo_set_option value (0 = automatic)
 int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, double *mean_valid,
                           int64_t *count, cudaStream_t s);
 size_t saturation_stats_scratch(int64_t n_drops);

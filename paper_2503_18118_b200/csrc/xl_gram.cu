@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(NT, 1) gram_small_kernel(GramParams P) {
           xl::coef_from_r2_f32(r2, u.amp, P.inv_lambda, fr, fi);
           hr[i] = fr; hi[i] = fi;
         } else {
-          xl::coef_from_r2(r2, u.amp, P.inv_lambda, hr[i], hi[i]);
+          xl::coef_fast(r2, u.amp, 4.0 * P.inv_lambda, hr[i], hi[i]);
         }
       }
       int v = 0;
@@ -977,10 +977,10 @@ void launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 
 // Tiles of 2*Mt2Cfg<G>::S steps.  Buffers: 2 (one barrier per tile) for G <= 4, the
 // 3-deep mbarrier ring above (measured on B200: cfg4 K=32 17.65 vs 18.50 ms with the
-// ring; cfg5 K=64 25.24 vs 25.79 ms).  XLMIMO_MT2=2|3 overrides.
+// ring; cfg5 K=64 25.24 vs 25.79 ms).  XLMIMO_OPT_MT2_BUFFERS = 2|3 overrides.
 template <int G>
 void launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
-  static const int env = getenv("XLMIMO_MT2") ? atoi(getenv("XLMIMO_MT2")) : 0;
+  const int env = (int)xlh::option(XLMIMO_OPT_MT2_BUFFERS);
   const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
   if (nbuf == 2) ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
@@ -1306,7 +1306,7 @@ __global__ void __launch_bounds__(TiledCfg<KP>::NT, 1) gram_tiled_kernel(GramPar
             h.x = fr; h.y = fi;
           } else {
             double dr, di;
-            xl::coef_from_r2(r2, u.amp, P.inv_lambda, dr, di);
+            xl::coef_fast(r2, u.amp, 4.0 * P.inv_lambda, dr, di);
             h.x = (RT)dr; h.y = (RT)di;
           }
         }
@@ -1420,22 +1420,22 @@ int blk_pairs(int K) {
   return nb * (nb + 1) / 2;
 }
 // K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) above 128 users, the
-// block-pair kernel below it; XLMIMO_LARGE_K=blk|syrk overrides (A/B tests).
+// block-pair kernel below it; XLMIMO_OPT_LARGE_K = 1 (blocks) | 2 (SYRK) overrides.
 constexpr int kSyrkMinK = 129;  // measured (35 000 elements): K = 128 blk 61 vs SYRK 66 ms, K = 150 64 vs 57, K = 200 54 vs 49
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
-// generated in-kernel below; XLMIMO_PAIR=gen|stream overrides.
+// generated in-kernel below; XLMIMO_OPT_PAIR = 1 (gen) | 2 (stream) overrides.
 constexpr int kStreamPairMinK = 352;  // measured crossover (35 000 elements): K = 320 gen 12.2 vs stream 12.8 ms, K = 384 17.4 vs 13.6
 bool use_stream_pair(int K) {
-  static const char *e = getenv("XLMIMO_PAIR");
-  if (e && !strcmp(e, "gen")) return false;
-  if (e && !strcmp(e, "stream")) return true;
+  const int64_t o = xlh::option(XLMIMO_OPT_PAIR);
+  if (o == 1) return false;
+  if (o == 2) return true;
   return K >= kStreamPairMinK;
 }
 bool use_gram_syrk(int K) {
-  static const char *e = getenv("XLMIMO_LARGE_K");
-  if (e && !strcmp(e, "blk")) return false;
-  if (e && !strcmp(e, "syrk")) return true;
+  const int64_t o = xlh::option(XLMIMO_OPT_LARGE_K);
+  if (o == 1) return false;
+  if (o == 2) return true;
   return K >= kSyrkMinK;
 }
 int choose_split_blk(int64_t n_drops, int K, int64_t N) {
@@ -1484,12 +1484,12 @@ void launch_tiled_k(int K, const GramParams &P, int64_t n_blocks, cudaStream_t s
 namespace xlh {
 
 // Which kernel runs, and how many partials per (drop, split, level) it writes.
-// Block shapes of the DMMA kernel (XLMIMO_GRAM_VARIANT selects for tuning):
+// Block shapes of the DMMA kernel (XLMIMO_OPT_DMMA_VARIANT selects for tuning):
 //   G = 1: 0 -> 256 thr x 4 blocks/SM (<= 64 regs), 1 -> 256 x 6 (<= 40), 2 -> 128 x 8, 3 -> 256 x 2
 //   G = 2: 0 -> 256 x 2, 1 -> 256 x 3, 2 -> 128 x 4, 3 -> 256 x 2
 int mma_variant() {
-  static const int v = getenv("XLMIMO_GRAM_VARIANT") ? atoi(getenv("XLMIMO_GRAM_VARIANT")) : 0;
-  return v;
+  const int64_t v = option(XLMIMO_OPT_DMMA_VARIANT);
+  return (v >= 0 && v <= 3) ? (int)v : 0;
 }
 int mma_nt(int G) { return (mma_variant() == 2) ? 128 : 256; }
 
@@ -1499,25 +1499,25 @@ struct KernelChoice {
   int parts;      // partials per (drop, split, level)
 };
 
-// XLMIMO_GRAM_KERNEL=split|mma|legacy overrides the default (tuning / A-B tests);
-// XLMIMO_GRAM_NT overrides the block size of the split / DMMA kernels.
+// XLMIMO_OPT_GRAM_KERNEL = 1 split | 2 DMMA | 3 CUDA-core overrides the default (tuning /
+// A-B tests); XLMIMO_OPT_SPLIT_NT selects the split kernel's block variant.
 KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
-  static const char *env_k = getenv("XLMIMO_GRAM_KERNEL");
-  static const int env_nt = getenv("XLMIMO_GRAM_NT") ? atoi(getenv("XLMIMO_GRAM_NT")) : 0;
+  const int64_t env_k = option(XLMIMO_OPT_GRAM_KERNEL);
+  const int64_t env_nt = option(XLMIMO_OPT_SPLIT_NT);
   KernelChoice c;
   const bool fp64 = precision == XLMIMO_FP64;
   const bool split_ok = fp64 && a.kind == XLMIMO_ULA && (K == 8 || K == 4);
   const bool mma_ok = fp64 && K <= 16;
   // measured on B200 (cfg2, K = 8): split 20.4 ms < DMMA 23.6 ms < register kernel A 37.7 ms
   c.which = split_ok ? 1 : mma_ok ? 2 : fp64 ? 3 : 0;
-  if (env_k && !strcmp(env_k, "split") && split_ok) c.which = 1;
-  if (env_k && !strcmp(env_k, "mma") && mma_ok) c.which = 2;
-  if (env_k && !strcmp(env_k, "legacy")) c.which = 0;
-  // split variants (XLMIMO_GRAM_NT selects; "nt" is a variant id, threads in kSplitThreads)
+  if (env_k == 1 && split_ok) c.which = 1;
+  if (env_k == 2 && mma_ok) c.which = 2;
+  if (env_k == 3) c.which = 0;
+  // split variants (XLMIMO_OPT_SPLIT_NT selects; "nt" is a variant id, threads in kSplitThreads)
   // split default: variant 192 = 128 threads x 3 blocks/SM, two elements per iteration
   // (19.45 ms vs 19.77 for 256 x 2 on cfg2, B200)
   c.nt = (c.which == 1 && K == 8) ? 192 : 256;
-  if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = env_nt;
+  if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = (int)env_nt;
   if (c.which == 2) c.nt = mma_nt(K <= 8 ? 1 : 2);
   const int threads = (c.which == 1 && (c.nt == 64)) ? 256 : (c.which == 1 && c.nt == 192) ? 128 : c.nt;
   c.parts = (c.which == 1 || c.which == 2) ? threads / 32 : 1;
@@ -1544,7 +1544,7 @@ void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 }
 
 // Materialised streaming on tcgen05 (TF32, RNA-pre-rounded H) unless disabled by
-// XLMIMO_STREAM=cuda (CUDA-core fp32 tiled kernel, also the fallback for shapes
+// XLMIMO_OPT_STREAM = 1 (CUDA-core fp32 tiled kernel, also the fallback for shapes
 // the TMA path does not take: K < 9, N % 4 != 0).
 // The tensor-core fp32 paths round each coefficient to TF32 (RNA, 2^-11 relative): a
 // Gram entry's normalised error is ~5.6e-4 / sqrt(N) (per-product errors average over
@@ -1554,8 +1554,7 @@ void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 constexpr int64_t kTcMinN = 1024;
 
 bool materialised_use_tc(int K, int64_t N) {
-  static const char *e = getenv("XLMIMO_STREAM");
-  if (e && !strcmp(e, "cuda")) return false;
+  if (option(XLMIMO_OPT_STREAM) == 1) return false;
   return N >= kTcMinN && stream_tc_supported(K, N);
 }
 
@@ -1564,8 +1563,7 @@ bool materialised_use_tc(int K, int64_t N) {
 // one persistent streaming launch has >= ~14 waves of work items.
 // fused fp32 exact Gram on tcgen05 (generate -> TF32 smem tiles -> TMEM), single level only
 bool use_fused_tc(const ArrayP &a, int K, int precision, int n_lvl) {
-  static const char *e = getenv("XLMIMO_GRAM_KERNEL");
-  if (e && !strcmp(e, "legacy")) return false;
+  if (option(XLMIMO_OPT_GRAM_KERNEL) == 3) return false;
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   return precision == XLMIMO_FP32 && n_lvl == 1 && N >= kTcMinN && fused_tc_supported(a, K);
 }
@@ -1825,8 +1823,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
                : kc.which == 3 ? "gram_fused_dmma_tiled_fp64"
                : K <= 8 ? (fp32 ? "gram_fused_small_fp32" : "gram_fused_small_fp64")
                         : (fp32 ? "gram_fused_tiled_fp32" : "gram_fused_tiled_fp64"));
-  static const char *env_mt = getenv("XLMIMO_GRAM_KERNEL");
-  const bool mt1 = (env_mt && !strcmp(env_mt, "mt1")) || N >= ((int64_t)1 << 31);
+  const bool mt1 = option(XLMIMO_OPT_GRAM_KERNEL) == 4 || N >= ((int64_t)1 << 31);
   if (kc.which == 3 && mt1) {
     switch ((K + 7) / 8) {
       case 3: launch_mt<3>(P, n_blocks, s); break;

@@ -144,3 +144,20 @@ def test_product_path_has_no_oracle_dependency():
                 assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
                 assert "or_gram" not in txt and "xlmimo_oracle" not in txt, f
     assert "oracle" not in open(HDR).read().lower()
+
+
+def test_path_options_are_an_abi_knob_not_the_environment(lib):
+    """Kernel-path overrides are the documented xlmimo_set_option knob (include/xlmimo.h);
+    the product sources read no environment variable, so production behaviour cannot change
+    silently."""
+    import glob
+    import paper_2503_18118_b200 as xl
+    for src in glob.glob(os.path.join(os.path.dirname(LIB), "csrc", "*")):
+        assert "getenv" not in open(src).read(), src
+    for opt in range(7):
+        assert xl.get_option(opt) == 0
+    with xl.option(xl.OPT_LARGE_K, 2):
+        assert xl.get_option(xl.OPT_LARGE_K) == 2
+    assert xl.get_option(xl.OPT_LARGE_K) == 0
+    assert xl._L.xlmimo_set_option(7, 1) == -1 and xl._L.xlmimo_set_option(-1, 1) == -1
+    assert xl._L.xlmimo_get_option(99) == 0

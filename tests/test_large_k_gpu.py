@@ -226,53 +226,26 @@ def test_exact_sweep_large_k_nested_levels(xl, orc):
     assert np.array_equal(res["n_valid"], nv)
 
 
-@pytest.mark.parametrize("path,K", [("blk", 200), ("syrk", 100), ("syrk", 65)])
-def test_large_k_paths_outside_their_default_range(xl, path, K):
-    """XLMIMO_LARGE_K forces the block-pair or the SYRK kernel; each must match the
-    oracle outside the K range the default selection gives it (fresh process: the
-    selection is read once)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = f"""
-import sys; sys.path.insert(0, {root!r})
-import numpy as np, oracle as orc, paper_2503_18118_b200 as xl
-from tests._util import normalized_err
-a = xl.Array.ula(1500, 100e9)
-pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), {K}, 2, seed=3)
-G = xl.gram_exact(a, pos).cpu().numpy()
-Go = orc.gram_exact(orc.array("ula", n_y=1500, fc_hz=100e9), pos.cpu().numpy())
-e = normalized_err(G, Go)
-print("ERR", e)
-sys.exit(0 if e <= 1e-9 else 1)
-"""
-    env = dict(os.environ, XLMIMO_LARGE_K=path)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
+@pytest.mark.parametrize("path,K", [(1, 200), (2, 100), (2, 65)])
+def test_large_k_paths_outside_their_default_range(xl, orc, path, K):
+    """XLMIMO_OPT_LARGE_K forces the block-pair (1) or the SYRK (2) kernel; each must match
+    the oracle outside the K range the default selection gives it."""
+    a = xl.Array.ula(1500, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 2, seed=3)
+    with xl.option(xl.OPT_LARGE_K, path):
+        G = xl.gram_exact(a, pos).cpu().numpy()
+    Go = orc.gram_exact(orc.array("ula", n_y=1500, fc_hz=100e9), pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-9
 
 
-@pytest.mark.parametrize("path,K", [("gen", 400), ("stream", 100), ("stream", 200)])
-def test_large_k_fp32_paths_outside_their_default_range(xl, path, K):
-    """XLMIMO_PAIR forces the in-kernel-generation or the TMA-fed (materialised chunk)
-    tcgen05 block-pair kernel at fp32; each must meet the fp32 tier (1e-4 normalised)
+@pytest.mark.parametrize("path,K", [(1, 400), (2, 100), (2, 200)])
+def test_large_k_fp32_paths_outside_their_default_range(xl, orc, path, K):
+    """XLMIMO_OPT_PAIR forces the in-kernel-generation (1) or the TMA-fed materialised-chunk
+    (2) tcgen05 block-pair kernel at fp32; each must meet the fp32 tier (1e-4 normalised)
     outside the K range the default selection gives it, across a chunk boundary."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = f"""
-import sys; sys.path.insert(0, {root!r})
-import numpy as np, oracle as orc, paper_2503_18118_b200 as xl
-from tests._util import normalized_err
-a = xl.Array.ula(5000, 100e9)
-pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), {K}, 2, seed=4)
-G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
-Go = orc.gram_exact(orc.array("ula", n_y=5000, fc_hz=100e9), pos.cpu().numpy())
-e = normalized_err(G, Go)
-print("ERR", e)
-sys.exit(0 if e <= 1e-4 else 1)
-"""
-    env = dict(os.environ, XLMIMO_PAIR=path)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
+    a = xl.Array.ula(5000, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 2, seed=4)
+    with xl.option(xl.OPT_PAIR, path):
+        G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+    Go = orc.gram_exact(orc.array("ula", n_y=5000, fc_hz=100e9), pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-4
