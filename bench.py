@@ -2,31 +2,39 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], the config its metric is quoted on): the
-capacity-vs-N saturation sweep -- ULA N = 2^8..2^16, 28 GHz, K = 8 users,
-r ~ U[3, 30] m, az ~ U[-60, 60] deg, SNR 0/10/20 dB, 10^4 seeded drops, fp64,
-CAP + ZF + MMSE.  One step = the whole hot path on one batch: draw the drops
-(a1), fused exact Gram with nested-N snapshots (a2+a3), per-(drop, N) receivers
-(a5), ergodic means + saturation statistics (a6), and the same sweep on the same drops
-through the closed-form ("modified ZF") Gram (a4: Eqs. (4)/(6)/(22)/(23)), results to
-host.  Each step
-uses a fresh seed (new drops), and a 256 MiB buffer is written between steps to
-flush L2 (126 MB).  N > 1 (torchrun): weak scaling, each rank its own 10^4
-drops (first_drop = rank * 10^4) and a per-step NCCL all-reduce of the ergodic
-sums/counts -- the only exchange the method has.
+Headline workload: BASELINE.json configs[4] (cfg5), the largest single-GPU config --
+ULA N = 2^20, 140 GHz, K = 64 users, r ~ U[5, 100] m, az ~ U[-60, 60] deg, SNR 10 dB,
+1000 seeded drops, fp64.  One step = the whole hot path on one batch: draw the drops
+(a1), the fused exact Gram H^H H with H never materialised (a2+a3, DMMA on the FP64
+pipe), CAP + ZF + MMSE per drop (a5), the ergodic means and saturation statistics (a6),
+and the same receivers through the closed-form ("modified ZF") Gram of Eqs. (4)/(6)/
+(22)/(23) on the same drops (a4).  Each step draws fresh drops (new seed) and a 256 MiB
+buffer is written before it to flush L2 (126 MB).
 
-metric: Gram complex MACs per second, cMAC = N_max K(K+1)/2 per drop (nested
-shells: the algorithmic count of the largest array).
+Sub-records (same run, same clock sampling, each its own W warm-up + K timed steps):
+  cfg5_materialised  the complex64 H written to HBM (K4a) and streamed back by TMA into
+                     tcgen05 (K4b): HBM roofline of the streaming kernel;
+  cfg5_fused_fp32    the fused TF32 tcgen05 Gram (generator in shared memory): MUFU roofline;
+  cfg1_steady        cfg1 in a 10^6-drop steady-state batch (drops, fused fp64 Gram, closed
+                     form, CAP/ZF/MMSE/MRC on both);
+  cfg2_sweep         the capacity-vs-N saturation sweep (10^4 drops, nine nested N, three
+                     SNRs, exact + closed form) -- round 1's headline;
+  cfg3, cfg4         full drop counts (10^5, 10^4), fused fp64 Gram + the config's receivers,
+                     and the fused fp32 Gram.
+N > 1 (torchrun): weak scaling of the headline, each rank its own 1000 drops (first_drop =
+rank * 1000) and one NCCL all-reduce per step of the ergodic sums/counts -- the only
+exchange the method has; the sub-records and the CPU baseline run at N = 1 only.
 
---impl reference: the CPU oracle (oracle/, plain fp64 C) on this box's host
-cores, same workload, each step a bounded sample of drops (the tier's reference
-arm; a deliberately slow program -- parity and roofline are the headline).
+metric: Gram complex MACs per second, N K(K+1)/2 per drop.
+
+--impl reference: the CPU oracle (oracle/, plain fp64 C) on this box's host cores, on
+cfg5 drops, each step a bounded sample (the tier's reference arm; a deliberately slow
+program -- parity and the roofline fraction are the headline).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -40,12 +48,16 @@ if ROOT not in sys.path:
 
 from workloads import CONFIGS, cmac_per_drop  # noqa: E402
 
-W = CONFIGS[2]
-# FP64-pipe work model per channel coefficient ("Roofline"): the cheapest fp64
+W = CONFIGS[5]
+# FP64-pipe work model per channel coefficient: the cheapest fp64
 # evaluation found (coef_fast): distance^2 2, 1/r 5, r 1, quarter-cycle reduction 3,
 # sin+cos minimax 12, r^{-3/2} 6, phasor 2 (MUFU seeds and the quadrant F2I are off the
-# FP64 pipe).  With this model frac ~ the FP64 pipe utilisation against the nominal peak.
+# FP64 pipe); then 4 FP64-pipe ops per off-diagonal complex MAC (DFMA, or a quarter of
+# the four real m8n8k4 DMMAs per 2x2 plane block), 2 per diagonal one.
 FP64_OPS_PER_COEF = 31
+MUFU_PER_COEF_FP32 = 2   # the fused fp32 generator: MUFU sin + cos per coefficient
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6545.3   # B200_PROFILING.md / MEASURED_PEAKS.json copy bandwidth
 
 
 def parse():
@@ -55,6 +67,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="headline only (no per-config sub-records)")
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -66,9 +79,17 @@ def dist_env():
     return rank, world, local
 
 
+def hbm_peak():
+    try:
+        d = json.load(open(PEAKS_FILE))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    except (OSError, ValueError, KeyError):
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback"
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling DURING the timed regions (B200_PROFILING.md clocks line)."""
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
@@ -121,34 +142,40 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kname: str, n_drops: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
-    newest committed ncu --set full capture of the same launch (profiles/r*/ncu_traffic_bench.json),
-    or None.  The fused kernel is ALU-bound: this is positions in + Gram partials out."""
+def ncu_traffic(kname: str, launch: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of a kernel from the newest
+    committed `ncu --set full` capture of the same launch (profiles/r*/ncu_traffic_*.json),
+    or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_bench.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_*.json")))
     for f in reversed(files):
         try:
             d = json.load(open(f))
         except (OSError, ValueError):
             continue
-        if d.get("kernel") == kname and d.get("n_drops") == n_drops:
-            return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+        for e in (d if isinstance(d, list) else [d]):
+            if e.get("kernel") == kname and e.get("launch_key") == launch:
+                return int(e["dram_bytes_read"]) + int(e["dram_bytes_write"])
     return None
 
 
 # ----------------------------------------------------------------------------- oracle timing
+ORACLE_SUB_N = 2 ** 16   # the oracle's cost is linear in N: it runs cfg5 drops on the centred 2^16-element sub-array
+
+
 def oracle_sample(n_drops_sample: int, seed: int, nthreads: int = 0):
-    """Time the oracle (as it stands) on a bounded sample of the workload."""
+    """Time the oracle (as it stands) on a bounded sample of the headline workload: cfg5 drops
+    (K = 64, 140 GHz, same user law), the exact Gram, CAP/ZF/MMSE, ergodic reduction and the
+    closed-form path, on the centred ORACLE_SUB_N-element sub-array.  Returns (seconds, cMACs)."""
     import oracle
     oracle.build()
     u = oracle.users(r=W.r, az=W.az)
     pos = oracle.gen_drops(u, W.K, n_drops_sample, seed=seed)
-    a = oracle.array("ula", n_y=W.n_y, fc_hz=W.fc_hz)
+    a = oracle.array("ula", n_y=ORACLE_SUB_N, fc_hz=W.fc_hz)
     t0 = time.perf_counter()
-    oracle.saturation_sweep(a, W.n_list, pos, W.snr_db, W.receivers, t=W.t, nthreads=nthreads)
-    oracle.saturation_sweep(a, W.n_list, pos, W.snr_db, W.receivers, gram_kind=1, t=W.t, nthreads=nthreads)
-    return time.perf_counter() - t0
+    oracle.saturation_sweep(a, [ORACLE_SUB_N], pos, W.snr_db, W.receivers, t=W.t, nthreads=nthreads)
+    oracle.saturation_sweep(a, [ORACLE_SUB_N], pos, W.snr_db, W.receivers, gram_kind=1, t=W.t, nthreads=nthreads)
+    return time.perf_counter() - t0, ORACLE_SUB_N * W.K * (W.K + 1) // 2 * n_drops_sample
 
 
 def cpu_threads():
@@ -158,24 +185,22 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+SAMPLE_TEXT = (f"cfg5 drops (K = 64, 140 GHz, r ~ U[5,100] m) on the centred {ORACLE_SUB_N}-element sub-array "
+               f"of the 2^20 ULA (the oracle's cost is linear in N): exact fp64 Gram + CAP/ZF/MMSE + ergodic "
+               f"reduction + closed-form Gram and receivers")
+
+
 def cpu_baseline(target_s: float):
     cores = cpu_threads()
-    # calibrate on one drop per thread, then size the sample to ~target_s
-    t1 = oracle_sample(cores, seed=999)
-    per_round = max(t1, 1e-3)
-    rounds = max(1, int(target_s / per_round))
+    t1, _ = oracle_sample(cores, seed=999)               # one drop per thread: calibration
+    rounds = max(1, int(target_s / max(t1, 1e-3)))
     n = cores * rounds
-    t = oracle_sample(n, seed=1000)
-    value = cmac_per_drop(W) * n / t
-    # the same oracle on one thread (SURVEY 8(d) oracle timing plan): t1 ~ one drop on one core
-    n1 = max(1, int(target_s / 3 / per_round))
-    t_1 = oracle_sample(n1, seed=2000, nthreads=1)
-    return {"value": value, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} drops of cfg2 (all 9 N, 3 SNR, CAP+ZF+MMSE, exact and closed-form sweeps; the oracle "
-                      f"computes every N independently), "
-                      f"{t:.1f} s wall on {cores} OpenMP threads",
-            "drops_per_s": n / t,
-            "single_thread": {"value": cmac_per_drop(W) * n1 / t_1, "unit": "cMAC/s", "cores": 1,
+    t, cm = oracle_sample(n, seed=1000)
+    n1 = max(1, int(target_s / 3 / max(t1, 1e-3)))
+    t_1, cm1 = oracle_sample(n1, seed=2000, nthreads=1)
+    return {"value": cm / t, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} {SAMPLE_TEXT}; {t:.1f} s wall on {cores} OpenMP threads (over drops)",
+            "single_thread": {"value": cm1 / t_1, "unit": "cMAC/s", "cores": 1,
                               "sample": f"{n1} drops, {t_1:.1f} s wall on 1 thread"}}
 
 
@@ -184,26 +209,27 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = cpu_threads()
-    t_cal = oracle_sample(cores, seed=999)
-    # size each step so (warmup + steps) fit in ~150 s
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    n_step = max(cores, int(cores * max(1.0, budget / max(t_cal, 1e-3))))
+    t_cal, _ = oracle_sample(cores, seed=999)
+    budget = 150.0 / max(1, args.steps + args.warmup)    # (warmup + steps) in ~150 s
+    n_step = max(cores, cores * int(max(1.0, budget / max(t_cal, 1e-3))))
     for w in range(args.warmup):
         oracle_sample(n_step, seed=10 + w)
-    ts = []
+    ts, cm = [], 0
     for k in range(args.steps):
-        ts.append(oracle_sample(n_step, seed=100 + k))
+        t, c = oracle_sample(n_step, seed=100 + k)
+        ts.append(t)
+        cm += c
     t = sum(ts)
-    value = cmac_per_drop(W) * n_step * args.steps / t
+    value = cm / t
     line = {"metric": "gram_cmac_per_s", "value": value, "unit": "cMAC/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": W.name, "n_drops_per_step": n_step, "K": W.K, "n_list": list(W.n_list),
-                       "step": "drops + exact fp64 sweep + closed-form sweep on the same drops",
+            "config": {"workload": W.name, "n_drops_per_step": n_step, "K": W.K, "N": ORACLE_SUB_N,
+                       "step": "drops + exact fp64 Gram + CAP/ZF/MMSE + ergodic + closed-form path",
                        "snr_db": list(W.snr_db), "fc_hz": W.fc_hz},
             "cpu_baseline": {"value": value, "unit": "cMAC/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{n_step} drops per step (of the 10^4-drop workload)"},
+                             "sample": f"{n_step} {SAMPLE_TEXT} per step"},
             "e2e": {"value": value, "unit": "cMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "drops_per_s": n_step * args.steps / t}
     print(json.dumps(line), flush=True)
@@ -211,6 +237,11 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- ours
+def fp64_ops(D, N, K):
+    """FP64-pipe operations of the fused exact Gram (work model above)."""
+    return D * N * (K * FP64_OPS_PER_COEF + 4 * (K * (K - 1) // 2) + 2 * K)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -222,7 +253,6 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    sys.path.insert(0, ROOT)
     import importlib.util
     spec = importlib.util.spec_from_file_location("_xl_build", os.path.join(ROOT, "paper_2503_18118_b200", "build.py"))
     bmod = importlib.util.module_from_spec(spec)
@@ -234,24 +264,77 @@ def run_ours(args):
     import paper_2503_18118_b200 as xl
     from paper_2503_18118_b200 import parallel
 
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    hbm_gbs, hbm_src = hbm_peak()
+
+    def timed(step, steps, warmup):
+        """W untimed + K timed steps (L2 flushed before each), CUDA events on the launching
+        stream; per-kernel device times from the library's event hooks."""
+        for k in range(warmup):
+            flush.fill_(k & 0xFF)
+            step(k)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        n0 = xl.launch_count()
+        xl._L.xlmimo_timing_enable(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        out = None
+        ms_flush = 0.0
+        e0.record(stream)
+        for k in range(steps):
+            flush.fill_((warmup + k) & 0xFF)
+            out = step(warmup + k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        xl._L.xlmimo_timing_enable(0)
+        kt = parallel.read_kernel_times(xl)
+        t_ms = e0.elapsed_time(e1)
+        # the flush writes are not part of the step: time them alone and subtract
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for k in range(steps):
+            flush.fill_(k & 0xFF)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms_flush = f0.elapsed_time(f1)
+        return max(t_ms - ms_flush, 1e-6), kt, xl.launch_count() - n0, out
+
+    def fp64_roof(kt, names, D, N, K, clk):
+        ks = [k for k in kt if k in names]
+        if not ks:
+            return None
+        kname = max(ks, key=lambda k: kt[k][1])
+        cnt, ms = kt[kname]
+        per_launch = ms / cnt
+        ach = fp64_ops(D, N, K) / (per_launch * 1e-3) / 1e12
+        peak = 148 * 64 * clk * 1e6 / 1e12
+        return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "FP64 Top/s", "frac": ach / peak,
+                "kernel": kname, "launch_ms": per_launch, "launches": cnt,
+                "work_model": f"{FP64_OPS_PER_COEF} FP64-pipe ops per element-user coefficient + 4 per off-diagonal "
+                              f"cMAC + 2 per diagonal, x {D} drops x N = {N} per launch; peak = 148 SM x 64 FP64 "
+                              f"lanes/clk x sm_max clock (B200_PROFILING.md unit counts)"}
+
+    # ------------------------------------------------------------------ headline: cfg5 fp64 step
     D = W.n_drops
-    arr = xl.Array.ula(W.n_y, W.fc_hz)
+    N = W.N
+    arr = xl.Array.ula(N, W.fc_hz)
     users = xl.Users.polar(W.r, W.az)
     snr = list(W.snr_db)
-    R = xl.n_recv(W.receivers)
-    ws_bytes = max(xl.sweep_workspace_bytes(arr, W.n_list, W.K, D, len(snr), W.receivers),
-                   xl.sweep_workspace_bytes(arr, W.n_list, W.K, D, len(snr), W.receivers,
+    nl = [N]
+    ws_bytes = max(xl.sweep_workspace_bytes(arr, nl, W.K, D, len(snr), W.receivers),
+                   xl.sweep_workspace_bytes(arr, nl, W.K, D, len(snr), W.receivers,
                                             gram_kind=xl.GRAM_CLOSED_FORM))
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # the two sweeps run in turn on one stream
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     pos = torch.empty((D, W.K, 3), dtype=torch.float64, device=dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
 
     def step(k):
-        flush.fill_(k & 0xFF)                                      # L2 flush between steps
         xl.gen_drops(users, W.K, D, seed=1000 + k, first_drop=rank * D, out=pos)
-        res = xl.saturation_sweep(arr, W.n_list, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws)
-        res_cf = xl.saturation_sweep(arr, W.n_list, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws,
+        res = xl.saturation_sweep(arr, nl, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws)
+        res_cf = xl.saturation_sweep(arr, nl, W.K, D, snr, W.receivers, pos=pos, t=W.t, ws=ws,
                                      gram_kind=xl.GRAM_CLOSED_FORM)
         if dist:
             pitch = 0.5 * 299792458.0 / W.fc_hz
@@ -259,111 +342,81 @@ def run_ours(args):
             res_cf = parallel.allreduce_sweep(res_cf, D, dist, dev, pitch=pitch)
         return res, res_cf
 
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    n0 = xl.launch_count()
-    xl._L.xlmimo_timing_enable(1)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for k in range(args.steps):
-        res, res_cf = step(args.warmup + k)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    xl._L.xlmimo_timing_enable(0)
-    launches = xl.launch_count() - n0
-    t_ms = e0.elapsed_time(e1)
+    t_ms, ktimes, launches, (res, res_cf) = timed(step, args.steps, args.warmup)
     if dist:
         tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-    ck = clocks.stop()
-    ktimes = parallel.read_kernel_times(xl)
+    clk_guess = 1965.0
 
-    # ---- e2e: the host-buffer C-ABI entry, H2D of positions + D2H of the result every step
+    # ------------------------------------------------------------------ e2e: host-buffer C-ABI entry
     pos_host = torch.empty((D, W.K, 3), dtype=torch.float64).pin_memory()
     pos_host.copy_(xl.gen_drops(users, W.K, D, seed=77, first_drop=rank * D).cpu())
-    def step_host():
-        r = xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws)
-        xl.saturation_sweep_host(arr, W.n_list, pos_host, snr, W.receivers, t=W.t, ws=ws,
-                                 gram_kind=xl.GRAM_CLOSED_FORM)
+
+    def step_host(k):
+        r = xl.saturation_sweep_host(arr, nl, pos_host, snr, W.receivers, t=W.t, ws=ws)
+        xl.saturation_sweep_host(arr, nl, pos_host, snr, W.receivers, t=W.t, ws=ws, gram_kind=xl.GRAM_CLOSED_FORM)
         return r
 
-    for _ in range(max(1, args.warmup)):
-        step_host()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     t0 = time.perf_counter()
-    f0 = torch.cuda.Event(enable_timing=True)
-    f1 = torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for k in range(args.steps):
-        flush.fill_(k & 0xFF)
-        step_host()
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    e2e_wall = (time.perf_counter() - t0) * 1e3
-    e2e_ms = max(e2e_ms, e2e_wall)
+    e2e_ms, _, _, _ = timed(step_host, args.steps, min(args.warmup, 1))
+    e2e_wall = (time.perf_counter() - t0) * 1e3 * args.steps / (args.steps + min(args.warmup, 1))
+    e2e_ms = max(e2e_ms, 0.0)
     if dist:
         tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = 2 * D * W.K * 3 * 8  # positions, once per sweep (exact, closed form)
-    n_out = len(W.n_list) * len(snr) * R
-    d2h = 2 * (n_out * 8 + n_out * 8 + 4 * 8)
+    R = xl.n_recv(W.receivers)
+    h2d = 2 * D * W.K * 3 * 8            # positions, once per sweep (exact, closed form)
+    n_out = len(nl) * len(snr) * R
+    d2h = 2 * (n_out * 8 * 2 + n_out * 8 + 4 * 8)   # ergodic, ergodic_valid, n_valid, sat per sweep
 
-    # ---- roofline of the dominant kernel (fused fp64 Gram, FP64 pipe bound)
-    cmac_step = cmac_per_drop(W) * D            # per rank
-    N = max(W.n_list)
-    gram_k = [k for k in ktimes if k.startswith("gram_fused")]
-    kname = max(gram_k, key=lambda k: ktimes[k][1]) if gram_k else "gram_fused"
-    kcount, kms = ktimes.get(kname, (0, 0.0))
-    roof = None
-    if kcount:
-        per_launch_ms = kms / kcount
-        tri_off = W.K * (W.K - 1) // 2
-        ops = D * N * (W.K * FP64_OPS_PER_COEF + 4 * tri_off + 2 * W.K)   # FP64-pipe ops per launch
-        achieved = ops / (per_launch_ms * 1e-3) / 1e12
-        clk = ck.get("sm_max_mhz") or 1965.0
-        peak = 148 * 64 * clk * 1e6 / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "FP64 Top/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(kname, D), "kernel": kname, "launch_ms": per_launch_ms,
-                "work_model": f"per element-user coefficient {FP64_OPS_PER_COEF} FP64 ops, 4 DFMA per off-diagonal "
-                              "cMAC, 2 per diagonal; peak = 148 SM x 64 FP64 lanes/clk x sm_max clock",
-                "share_of_step": kms / t_ms}
+    # ------------------------------------------------------------------ sub-records (N = 1)
+    sub = {}
+    if world == 1 and not args.no_sub:
+        sub = run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src, clk_guess)
+    ck = clocks.stop()
+    clk = ck.get("sm_max_mhz") or clk_guess
+
+    # ------------------------------------------------------------------ headline roofline
+    roof = fp64_roof(ktimes, ("gram_fused_dmma_tiled_fp64", "gram_fused_dmma_fp64", "gram_fused_split_fp64"),
+                     D, N, W.K, clk)
+    if roof:
+        roof["share_of_step"] = ktimes[roof["kernel"]][1] / t_ms
+        roof["traffic"] = ncu_traffic(roof["kernel"], f"cfg5 fp64 D={D}")
+    cmac_step = cmac_per_drop(W) * D
     out = None
     if rank == 0:
         value = cmac_step * world * args.steps / (t_ms * 1e-3)
         out = {"metric": "gram_cmac_per_s", "value": value, "unit": "cMAC/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": W.name, "n_drops_per_rank": D, "K": W.K, "n_list": list(W.n_list),
-                          "snr_db": snr, "fc_hz": W.fc_hz, "receivers": "CAP+ZF+MMSE", "precision": "fp64",
-                          "cmac_per_drop": cmac_per_drop(W), "l2": "flushed between steps (256 MiB write)",
-                          "step": "drops + exact fp64 sweep + closed-form sweep on the same drops",
+               "config": {"workload": W.name, "n_drops_per_rank": D, "N": N, "K": W.K, "snr_db": snr,
+                          "fc_hz": W.fc_hz, "r_m": list(W.r), "az_deg": list(W.az), "receivers": "CAP+ZF+MMSE",
+                          "precision": "fp64", "gram": "fused (H never materialised), DMMA on the FP64 pipe",
+                          "cmac_per_drop": cmac_per_drop(W),
+                          "l2": "flushed before every timed step (256 MiB write, its time subtracted)",
+                          "step": "drops + exact fp64 Gram + CAP/ZF/MMSE + ergodic/saturation reduce + closed-form "
+                                  "Gram and receivers on the same drops",
                           "parallelism": f"dp{world} (drops)"},
                "drops_per_s": D * world * args.steps / (t_ms * 1e-3),
                "e2e": {"value": cmac_step * world * args.steps / (e2e_ms * 1e-3), "unit": "cMAC/s",
-                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "entry": "xlmimo_saturation_sweep_host (exact + closed form), host positions in, host "
+                                "results out", "wall_ms_per_step": e2e_wall / args.steps},
                "gpu_launches": int(launches), "clocks": ck, "roofline": roof,
                "kernel_ms_per_step": {k: v[1] / args.steps for k, v in ktimes.items()},
-               "sat_M": float(res["sat"][2]),
-               "run": {"gpu": torch.cuda.get_device_name(dev), "seeds": f"1000 + step (drops of rank r from {D} r)",
-                       "nan_rates_last_step": int(np.asarray(res["n_valid"]).size * D * world
-                                                  - int(np.asarray(res["n_valid"]).sum())),
-                       "closed_form_nan_rates_last_step": int(np.asarray(res_cf["n_valid"]).size * D * world
-                                                              - int(np.asarray(res_cf["n_valid"]).sum()))}}
+               "results_last_step": {"ergodic_bits": np.asarray(res["ergodic"]).ravel().tolist(),
+                                     "n_valid": np.asarray(res["n_valid"]).ravel().tolist(),
+                                     "closed_form_ergodic_bits": np.asarray(res_cf["ergodic"]).ravel().tolist(),
+                                     "closed_form_n_valid": np.asarray(res_cf["n_valid"]).ravel().tolist(),
+                                     "M_sat": float(res["sat"][2])},
+               "sub": sub,
+               "run": {"gpu": torch.cuda.get_device_name(dev),
+                       "seeds": f"1000 + step (drops of rank r from {D} r)", "hbm_peak_source": hbm_src}}
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -372,6 +425,170 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(out), flush=True)
     return 0
+
+
+def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src, clk):
+    sub = {}
+    K_, W_ = args.steps, args.warmup
+
+    def rec(w, D, ms, kt, launches, extra):
+        cm = cmac_per_drop(w) * D
+        r = {"workload": w.name, "drops_per_step": D, "ms_per_step": ms / K_, "cmac_per_s": cm * K_ / (ms * 1e-3),
+             "drops_per_s": D * K_ / (ms * 1e-3), "gpu_launches": int(launches),
+             "kernel_ms_per_step": {k: v[1] / K_ for k, v in kt.items()}}
+        r.update(extra)
+        return r
+
+    # ---- cfg5 materialised: K4a write + K4b TMA -> tcgen05 stream, then the receivers
+    w = CONFIGS[5]
+    D = w.n_drops
+    arr = xl.Array.ula(w.N, w.fc_hz)
+    users = xl.Users.polar(w.r, w.az)
+    pos = torch.empty((D, w.K, 3), dtype=torch.float64, device=dev)
+    ws = torch.empty(xl.gram_workspace_bytes(arr, w.K, D, xl.FP32, xl.MATERIALIZED),
+                     dtype=torch.uint8, device=dev)
+    G = torch.empty((D, w.K, w.K, 2), dtype=torch.float64, device=dev)
+
+    def s_mat(k):
+        xl.gen_drops(users, w.K, D, seed=3000 + k, out=pos)
+        g = xl.gram_exact(arr, pos, precision=xl.FP32, mode=xl.MATERIALIZED, out=G, ws=ws)
+        return xl.sum_rate(g, list(w.snr_db), w.receivers)
+    ms, kt, nl_, _ = timed(s_mat, K_, W_)
+    st = kt.get("gram_stream_tc_tf32")
+    wr = kt.get("h_materialise")
+    extra = {"precision": "fp32 (complex64 H, TF32 tensor cores, fp64 across chunks)"}
+    if st:
+        per_launch = st[1] / st[0]
+        drops_per_launch = D / st[0]
+        bytes_launch = 8 * w.N * w.K * drops_per_launch
+        ach = bytes_launch / (per_launch * 1e-3) / 1e9
+        extra["roofline"] = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
+                             "traffic": ncu_traffic("gram_stream_tc_tf32", f"cfg5 mat32 B={int(drops_per_launch)}"),
+                             "kernel": "gram_stream_tc_tf32", "launch_ms": per_launch, "launches": st[0],
+                             "algorithmic_bytes_per_launch": bytes_launch,
+                             "work_model": "8 N K bytes per drop (complex64 H read once) x drops per launch",
+                             "peak_source": hbm_src, "share_of_step": st[1] / ms}
+    if wr:
+        per_launch = wr[1] / wr[0]
+        bytes_launch = 8 * w.N * w.K * D / wr[0]
+        extra["writer"] = {"kernel": "h_materialise (K4a)", "launch_ms": per_launch,
+                           "gbs": bytes_launch / (per_launch * 1e-3) / 1e9,
+                           "frac_of_hbm_peak": bytes_launch / (per_launch * 1e-3) / 1e9 / hbm_gbs}
+    sub["cfg5_materialised"] = rec(w, D, ms, kt, nl_, extra)
+    del ws
+
+    # ---- cfg5 fused fp32 (TF32 tcgen05, generator writes the operand tiles in shared memory)
+    ws = torch.empty(xl.gram_workspace_bytes(arr, w.K, D, xl.FP32, xl.FUSED),
+                     dtype=torch.uint8, device=dev)
+
+    def s_f32(k):
+        xl.gen_drops(users, w.K, D, seed=4000 + k, out=pos)
+        g = xl.gram_exact(arr, pos, precision=xl.FP32, out=G, ws=ws)
+        return xl.sum_rate(g, list(w.snr_db), w.receivers)
+    ms, kt, nl_, _ = timed(s_f32, K_, W_)
+    extra = {"precision": "fp32 (TF32 tensor cores, fp64 distance/phase anchor, fp64 across chunks)"}
+    tc = kt.get("gram_fused_tc_tf32")
+    if tc:
+        per_launch = tc[1] / tc[0]
+        coefs = w.N * w.K * D / tc[0]
+        ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
+        peak = 148 * 16 * clk * 1e6 / 1e12
+        extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s", "frac": ach / peak,
+                             "kernel": "gram_fused_tc_tf32", "launch_ms": per_launch, "launches": tc[0],
+                             "coefficients_per_clk_per_sm": coefs / (per_launch * 1e-3) / (clk * 1e6) / 148,
+                             "traffic": ncu_traffic("gram_fused_tc_tf32", f"cfg5 fp32 D={int(D / tc[0])}"),
+                             "work_model": "2 MUFU (sin, cos) per element-user coefficient; peak = 148 SM x 16 MUFU "
+                                           "lanes/clk x sm_max clock", "share_of_step": tc[1] / ms}
+    sub["cfg5_fused_fp32"] = rec(w, D, ms, kt, nl_, extra)
+    del ws, G, pos
+
+    # ---- cfg1 steady state: 10^6 drops through the whole per-drop path (exact and closed form)
+    w = CONFIGS[1]
+    D = 10 ** 6
+    arr = xl.Array.ula(w.N, w.fc_hz)
+    users = xl.Users.polar(w.r, w.az)
+    pos = torch.empty((D, w.K, 3), dtype=torch.float64, device=dev)
+    allr = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    G = torch.empty((D, w.K, w.K, 2), dtype=torch.float64, device=dev)
+    ws = torch.empty(max(1, xl.gram_workspace_bytes(arr, w.K, D, xl.FP64, xl.FUSED)),
+                     dtype=torch.uint8, device=dev)
+
+    def s_c1(k):
+        xl.gen_drops(users, w.K, D, seed=5000 + k, out=pos)
+        g = xl.gram_exact(arr, pos, out=G, ws=ws)
+        gt, fl = xl.gram_closed_form(arr, pos)
+        xl.sum_rate(g, list(w.snr_db), allr)
+        return xl.sum_rate(gt, list(w.snr_db), allr, flags=fl)
+    ms, kt, nl_, _ = timed(s_c1, K_, W_)
+    sub["cfg1_steady"] = rec(w, D, ms, kt, nl_, {
+        "step": "10^6 drops: drops + fused fp64 Gram + closed-form Gram + CAP/ZF/MMSE/MRC on both",
+        "roofline": fp64_roof(kt, ("gram_fused_split_fp64", "gram_fused_dmma_fp64", "gram_fused_small_fp64",
+                                   "gram_fused_warp_fp64"), D, w.N, w.K, clk)})
+    del pos, G, ws
+
+    # ---- cfg2: the saturation sweep (round 1's headline)
+    w = CONFIGS[2]
+    D = w.n_drops
+    arr = xl.Array.ula(w.n_y, w.fc_hz)
+    users = xl.Users.polar(w.r, w.az)
+    snr = list(w.snr_db)
+    ws = torch.empty(max(xl.sweep_workspace_bytes(arr, w.n_list, w.K, D, len(snr), w.receivers),
+                         xl.sweep_workspace_bytes(arr, w.n_list, w.K, D, len(snr), w.receivers,
+                                                  gram_kind=xl.GRAM_CLOSED_FORM)), dtype=torch.uint8, device=dev)
+    pos = torch.empty((D, w.K, 3), dtype=torch.float64, device=dev)
+
+    def s_c2(k):
+        xl.gen_drops(users, w.K, D, seed=6000 + k, out=pos)
+        r = xl.saturation_sweep(arr, w.n_list, w.K, D, snr, w.receivers, pos=pos, t=w.t, ws=ws)
+        xl.saturation_sweep(arr, w.n_list, w.K, D, snr, w.receivers, pos=pos, t=w.t, ws=ws,
+                            gram_kind=xl.GRAM_CLOSED_FORM)
+        return r
+    ms, kt, nl_, r = timed(s_c2, K_, W_)
+    roof = fp64_roof(kt, ("gram_fused_split_fp64",), D, max(w.n_list), w.K, clk)
+    if roof:
+        roof["traffic"] = ncu_traffic(roof["kernel"], f"cfg2 sweep D={D}")
+    sub["cfg2_sweep"] = rec(w, D, ms, kt, nl_, {
+        "step": "drops + exact fp64 sweep (9 nested N, 3 SNR, CAP/ZF/MMSE) + closed-form sweep", "roofline": roof,
+        "M_sat": float(r["sat"][2])})
+    del ws, pos
+
+    # ---- cfg3, cfg4: full drop counts, fused fp64 Gram + the config's receivers; fused fp32 Gram
+    for c in (3, 4):
+        w = CONFIGS[c]
+        D = w.n_drops
+        arr = xl.Array.ula(w.n_y, w.fc_hz) if w.kind == "ula" else xl.Array.upa(w.n_y, w.n_z, w.fc_hz)
+        users = xl.Users.polar(w.r, w.az, w.el)
+        pos = torch.empty((D, w.K, 3), dtype=torch.float64, device=dev)
+        G = torch.empty((D, w.K, w.K, 2), dtype=torch.float64, device=dev)
+        for prec, tag in ((xl.FP64, "fp64"), (xl.FP32, "fp32")):
+            ws = torch.empty(max(1, xl.gram_workspace_bytes(arr, w.K, D, prec,
+                                                                         xl.FUSED)), dtype=torch.uint8, device=dev)
+
+            def s_c(k):
+                xl.gen_drops(users, w.K, D, seed=7000 + k, out=pos)
+                g = xl.gram_exact(arr, pos, precision=prec, out=G, ws=ws)
+                return xl.sum_rate(g, list(w.snr_db), w.receivers)
+            ms, kt, nl_, _ = timed(s_c, K_, W_)
+            extra = {"precision": tag, "step": "drops + fused exact Gram + " +
+                     "+".join(n for n, b in (("CAP", 1), ("ZF", 2), ("MMSE", 4)) if w.receivers & b)}
+            if prec == xl.FP64:
+                extra["roofline"] = fp64_roof(kt, ("gram_fused_dmma_fp64", "gram_fused_dmma_tiled_fp64"), D, w.N,
+                                              w.K, clk)
+            else:
+                tc = kt.get("gram_fused_tc_tf32")
+                if tc:
+                    per_launch = tc[1] / tc[0]
+                    coefs = w.N * w.K * D / tc[0]
+                    ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
+                    peak = 148 * 16 * clk * 1e6 / 1e12
+                    extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s",
+                                         "frac": ach / peak, "kernel": "gram_fused_tc_tf32", "launch_ms": per_launch,
+                                         "coefficients_per_clk_per_sm": coefs / (per_launch * 1e-3) / (clk * 1e6) / 148}
+            sub[f"cfg{c}_{tag}"] = rec(w, D, ms, kt, nl_, extra)
+            del ws
+        del pos, G
+    torch.cuda.empty_cache()
+    return sub
 
 
 def main():

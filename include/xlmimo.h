@@ -89,6 +89,13 @@ typedef struct {
 XLMIMO_API int xlmimo_gen_drops(const xlmimo_users_t *users, int32_t K, int64_t n_drops, uint64_t seed,
                      uint64_t first_drop, double *pos, void *stream);
 
+/* The raw draws behind xlmimo_gen_drops / xlmimo_gen_drops_rect (R19): words (dev
+ * [n_drops][K][4] uint64) = Philox4x64-10 with key (seed, 0) at counter
+ * (first_drop + d, k, 0, 0).  Exposed so the draws can be audited bit for bit against
+ * any other implementation of the generator.  EINVAL: K < 1, n_drops < 0, words NULL. */
+XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint64_t first_drop, uint64_t *words,
+                                 void *stream);
+
 /* ------------------------------------------------------------------------- a2+a3
  * Exact Gram G = H^H H of the PNUSW channel, Eq. (3):
  *   h_i(m) = sqrt(beta0) e^{-j 2 pi r_im / lambda} / r_im * sqrt(x_i / r_im),

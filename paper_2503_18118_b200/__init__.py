@@ -20,7 +20,7 @@ import os
 
 import torch
 
-__all__ = ["Array", "Users", "gen_drops", "gram_exact", "gram_closed_form", "sum_rate", "sum_rate_mismatched",
+__all__ = ["Array", "Users", "gen_drops", "draw_words", "gram_workspace_bytes", "sweep_workspace_bytes", "gram_exact", "gram_closed_form", "sum_rate", "sum_rate_mismatched",
            "gen_drops_rect", "app_a_bounds", "saturation_sweep",
            "saturation_sweep_host", "launch_count", "lib_path", "XlmimoError",
            "ULA", "UPA", "FP64", "FP32", "FUSED", "MATERIALIZED", "GRAM_EXACT", "GRAM_CLOSED_FORM",
@@ -84,6 +84,8 @@ def _load():
     i32, i64, u32, u64, d, sz = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
                                  ctypes.c_double, ctypes.c_size_t)
     L.xlmimo_gen_drops.argtypes = [P(Users), i32, i64, u64, u64, vp, vp]
+    L.xlmimo_draw_words.argtypes = [i32, i64, u64, u64, vp, vp]
+    L.xlmimo_draw_words.restype = ctypes.c_int
     L.xlmimo_gram_exact_workspace.argtypes = [P(Array), i32, i64, i32, i32]
     L.xlmimo_gram_exact_workspace.restype = sz
     L.xlmimo_gram_exact.argtypes = [P(Array), vp, i32, i64, i32, i32, vp, vp, sz, vp]
@@ -234,7 +236,21 @@ def gen_drops(users: Users, K: int, n_drops: int, seed: int = 0, first_drop: int
     return pos
 
 
+def draw_words(K: int, n_drops: int, seed: int = 0, first_drop: int = 0, device=None, stream=None) -> torch.Tensor:
+    """The raw Philox4x64-10 words behind gen_drops: [n_drops, K, 4] uint64 on the device."""
+    _need_cuda()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    w = torch.empty((n_drops, K, 4), dtype=torch.uint64, device=dev)
+    _check(_L.xlmimo_draw_words(K, n_drops, seed, first_drop, _dptr(w), _stream(stream)), "xlmimo_draw_words")
+    return w
+
+
 # --------------------------------------------------------------------------- a2 + a3
+def gram_workspace_bytes(array: Array, K: int, n_drops: int, precision: int = FP64, mode: int = FUSED) -> int:
+    """xlmimo_gram_exact_workspace: scratch bytes gram_exact needs for this shape (0 = none)."""
+    return int(_L.xlmimo_gram_exact_workspace(ctypes.byref(array), K, n_drops, precision, mode))
+
+
 def gram_exact(array: Array, pos: torch.Tensor, precision: int = FP64, mode: int = FUSED,
                out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Exact Gram H^H H, complex128 [n_drops, K, K]."""

@@ -448,6 +448,14 @@ int xlmimo_saturation_sweep_host(const xlmimo_array_t *array, const int64_t *n_l
                    precision, t, ergodic, n_valid, ergodic_valid, sat, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint64_t first_drop, uint64_t *words,
+                      void *stream) {
+  NvtxRange nvtx_range("xlmimo_draw_words");
+  g_err[0] = 0;
+  if (K < 1 || n_drops < 0 || (!words && n_drops > 0)) return xlh::set_error(XLMIMO_EINVAL, "draw_words: K/n/words");
+  return xlh::launch_draw_words(K, n_drops, seed, first_drop, words, (cudaStream_t)stream);
+}
+
 int xlmimo_set_option(int32_t option, int64_t value) {
   g_err[0] = 0;
   if (option < 0 || option >= XLMIMO_OPT_COUNT) return xlh::set_error(XLMIMO_EINVAL, "set_option: %d", option);

@@ -273,7 +273,8 @@ int launch_sum_rate_large(const double *gram, int K, int64_t n_drops, const doub
                           cudaStream_t s);
 
 // xl_sweep.cu reductions
-int64_t option(int id);  // xlmimo_set_option value (0 = automatic)
+int64_t option(int id);
+int launch_draw_words(int K, int64_t n_drops, uint64_t seed, uint64_t first_drop, uint64_t *words, cudaStream_t s);  // xlmimo_set_option value (0 = automatic)
 int launch_ergodic_reduce(const double *per_drop, int64_t n_drops, int n_out, double *mean, double *mean_valid,
                           int64_t *count, cudaStream_t s);
 size_t saturation_stats_scratch(int64_t n_drops);

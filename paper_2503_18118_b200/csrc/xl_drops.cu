@@ -38,9 +38,31 @@ __global__ void __launch_bounds__(256) gen_drops_rect_kernel(double x0, double x
   p[2] = 0.0;
 }
 
+// The raw counter-based words behind both drop laws (R19), for a bit-exact audit.
+__global__ void __launch_bounds__(256) draw_words_kernel(int K, int64_t n_total, uint64_t seed, uint64_t first_drop,
+                                                         uint64_t *words) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_total) return;
+  const int64_t d = idx / K;
+  const int k = (int)(idx - d * K);
+  const xl::u64x4 w = xl::philox4x64_10(first_drop + (uint64_t)d, (uint64_t)k, 0, 0, seed, 0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) words[idx * 4 + q] = w.v[q];
+}
+
 }  // namespace
 
 namespace xlh {
+
+int launch_draw_words(int K, int64_t n_drops, uint64_t seed, uint64_t first_drop, uint64_t *words, cudaStream_t s) {
+  const int64_t n = n_drops * (int64_t)K;
+  if (n == 0) return XLMIMO_OK;
+  KTimer tm(s, "draw_words");
+  draw_words_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(K, n, seed, first_drop, words);
+  tm.stop(s);
+  count_launch();
+  return check_launch("draw_words_kernel");
+}
 
 int launch_gen_drops_rect(double x0, double x1, double y0, double y1, int K, int64_t n_drops, uint64_t seed,
                           uint64_t first_drop, double *pos, cudaStream_t s) {
