@@ -459,7 +459,7 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
     extra = {"precision": "fp32 (complex64 H, TF32 tensor cores, fp64 across chunks)"}
     if st:
         per_launch = st[1] / st[0]
-        drops_per_launch = D / st[0]
+        drops_per_launch = D * K_ / st[0]
         bytes_launch = 8 * w.N * w.K * drops_per_launch
         ach = bytes_launch / (per_launch * 1e-3) / 1e9
         extra["roofline"] = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
@@ -470,7 +470,7 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
                              "peak_source": hbm_src, "share_of_step": st[1] / ms}
     if wr:
         per_launch = wr[1] / wr[0]
-        bytes_launch = 8 * w.N * w.K * D / wr[0]
+        bytes_launch = 8 * w.N * w.K * D * K_ / wr[0]
         extra["writer"] = {"kernel": "h_materialise (K4a)", "launch_ms": per_launch,
                            "gbs": bytes_launch / (per_launch * 1e-3) / 1e9,
                            "frac_of_hbm_peak": bytes_launch / (per_launch * 1e-3) / 1e9 / hbm_gbs}
@@ -490,13 +490,13 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
     tc = kt.get("gram_fused_tc_tf32")
     if tc:
         per_launch = tc[1] / tc[0]
-        coefs = w.N * w.K * D / tc[0]
+        coefs = w.N * w.K * D * K_ / tc[0]
         ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
         peak = 148 * 16 * clk * 1e6 / 1e12
         extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s", "frac": ach / peak,
                              "kernel": "gram_fused_tc_tf32", "launch_ms": per_launch, "launches": tc[0],
                              "coefficients_per_clk_per_sm": coefs / (per_launch * 1e-3) / (clk * 1e6) / 148,
-                             "traffic": ncu_traffic("gram_fused_tc_tf32", f"cfg5 fp32 D={int(D / tc[0])}"),
+                             "traffic": ncu_traffic("gram_fused_tc_tf32", f"cfg5 fp32 D={int(D * K_ / tc[0])}"),
                              "work_model": "2 MUFU (sin, cos) per element-user coefficient; peak = 148 SM x 16 MUFU "
                                            "lanes/clk x sm_max clock", "share_of_step": tc[1] / ms}
     sub["cfg5_fused_fp32"] = rec(w, D, ms, kt, nl_, extra)
@@ -578,7 +578,7 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
                 tc = kt.get("gram_fused_tc_tf32")
                 if tc:
                     per_launch = tc[1] / tc[0]
-                    coefs = w.N * w.K * D / tc[0]
+                    coefs = w.N * w.K * D * K_ / tc[0]
                     ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
                     peak = 148 * 16 * clk * 1e6 / 1e12
                     extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s",

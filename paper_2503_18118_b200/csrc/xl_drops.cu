@@ -11,16 +11,19 @@ __global__ void __launch_bounds__(256) gen_drops_kernel(xlmimo_users_t u, int K,
   const int k = (int)(idx - d * K);
   const xl::u64x4 w = xl::philox4x64_10(first_drop + (uint64_t)d, (uint64_t)k, 0, 0, seed, 0);
   const double deg = 3.14159265358979323846 / 180.0;
-  const double r = u.r_min_m + (u.r_max_m - u.r_min_m) * xl::u01_53(w.v[0]);
-  const double az = (u.az_min_deg + (u.az_max_deg - u.az_min_deg) * xl::u01_53(w.v[1])) * deg;
-  const double el = (u.el_min_deg + (u.el_max_deg - u.el_min_deg) * xl::u01_53(w.v[2])) * deg;
+  // explicit round-to-nearest multiply and add (no FMA contraction): r, az and el are then
+  // the same doubles as any plain evaluation of the law (R3, R19), so positions differ only
+  // by the sin/cos implementation (<= 2 ulp)
+  const double r = __dadd_rn(u.r_min_m, __dmul_rn(u.r_max_m - u.r_min_m, xl::u01_53(w.v[0])));
+  const double az = __dmul_rn(__dadd_rn(u.az_min_deg, __dmul_rn(u.az_max_deg - u.az_min_deg, xl::u01_53(w.v[1]))), deg);
+  const double el = __dmul_rn(__dadd_rn(u.el_min_deg, __dmul_rn(u.el_max_deg - u.el_min_deg, xl::u01_53(w.v[2]))), deg);
   double sa, ca, se, ce;
   sincos(az, &sa, &ca);
   sincos(el, &se, &ce);
   double *p = pos + idx * 3;
-  p[0] = r * ce * ca;
-  p[1] = r * ce * sa;
-  p[2] = r * se;
+  p[0] = __dmul_rn(__dmul_rn(r, ce), ca);
+  p[1] = __dmul_rn(__dmul_rn(r, ce), sa);
+  p[2] = __dmul_rn(r, se);
 }
 
 // NEXT-4: the paper's rectangle user field x ~ U[x0, x1], y ~ U[y0, y1].
@@ -33,8 +36,8 @@ __global__ void __launch_bounds__(256) gen_drops_rect_kernel(double x0, double x
   const int k = (int)(idx - d * K);
   const xl::u64x4 w = xl::philox4x64_10(first_drop + (uint64_t)d, (uint64_t)k, 0, 0, seed, 0);
   double *p = pos + idx * 3;
-  p[0] = x0 + (x1 - x0) * xl::u01_53(w.v[0]);
-  p[1] = y0 + (y1 - y0) * xl::u01_53(w.v[1]);
+  p[0] = __dadd_rn(x0, __dmul_rn(x1 - x0, xl::u01_53(w.v[0])));  // no FMA contraction (as gen_drops_kernel)
+  p[1] = __dadd_rn(y0, __dmul_rn(y1 - y0, xl::u01_53(w.v[1])));
   p[2] = 0.0;
 }
 

@@ -28,7 +28,14 @@ constexpr int kStages = 12;
 constexpr int kRows = 128;             // MMA M (rows >= 2K stay zero)
 constexpr int kBoxK = 32;              // fp32 elements per row per stage (128 B, one swizzle atom)
 constexpr int kStageBytes = kRows * kBoxK * 4;  // 16 KiB
-constexpr int kChunk = 8192;           // elements accumulated in TMEM per partial
+constexpr int kChunk = 8192;           // elements per work item (one fp64 partial per item)
+// The tensor core's fp32 accumulation truncates: each MMA leaves ~0.5 ulp of the running
+// sum, a relative bias of ~3e-8 per MMA that grows with the run length (512 MMAs per
+// accumulator left -2.5e-5 on the cfg4 diagonal = 1.2e-3 bit of ZF rate at K = 32).  So
+// the TMEM accumulator restarts every kSubStages stages (4 MMAs each: <= 64 MMAs, bias
+// <= ~3e-6); the epilogue folds the sub-chunk sums into a running fp32 sum kept in a third
+// TMEM region (drain_subchunk) and writes the item's fp64 partial after the last one.
+constexpr int kSubStages = 16;
 constexpr int kThreads = 256;
 
 // element blocks stacked per stage in the 128 MMA rows: 2K <= 32 -> 4 blocks, <= 64 -> 2, else 1
@@ -120,6 +127,66 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Epilogue of one TMEM sub-chunk (K <= 64 kernels).  `lane_base` = tmem + (32 q << 16), the
+// thread's accumulator row at column acc_col, its running sum at run_col (same row, a third
+// TMEM region).  Sub-chunks before the last fold the accumulator into the running sum in fp32
+// (round to nearest: unbiased, unlike the tensor core's own accumulation); the last adds the
+// running sum, pairs re/im rows with the neighbouring lane and writes
+//   Re G(i,j) = R(2i,2j) + R(2i+1,2j+1),  Im G(i,j) = R(2i,2j+1) - R(2i+1,2j)
+// (even lane: j-pairs 0..7 of each 32-column group, odd lane: 8..15) into the item's fp64
+// partial `out` (packed upper triangle).
+__device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_col, uint32_t run_col, int R, int K,
+                                               int i, int plane, bool first, bool last, double *out) {
+  for (int cb = 0; cb < (R + 31) / 32; ++cb) {
+    float v[32];
+    tmem_ld32(lane_base + acc_col + (uint32_t)(32 * cb), v);
+    if (!first) {
+      float r[32];
+      tmem_ld32(lane_base + run_col + (uint32_t)(32 * cb), r);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] += r[e];
+    }
+    if (!last) {
+      tmem_st32(lane_base + run_col + (uint32_t)(32 * cb), v);
+      continue;
+    }
+    float x[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const int jj = plane * 8 + h;
+      const int j = 16 * cb + jj;
+      float rr, rr2, ri, ir;  // R(2i,2j), R(2i+1,2j+1), R(2i,2j+1), R(2i+1,2j)
+      if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
+      else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
+      if (i < K && j < K && j >= i) {
+        const int p = i * K - i * (i - 1) / 2 + (j - i);
+        out[2 * p] = (double)rr + (double)rr2;
+        out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+      }
+    }
+  }
+}
+
 struct StreamParams {
   double *ws;        // partials [drop][chunk][blk][NP][2] (absolute drop index)
   int K;
@@ -132,6 +199,13 @@ struct StreamParams {
   int nb;            // drops in this batch
   uint32_t tmem_cols;
 };
+
+// stages of work item chunk c: kb_per_chunk, fewer in the ragged last chunk
+__device__ __forceinline__ int item_stages(int64_t N, int c, int kb_per_chunk, int spb) {
+  const int64_t rem = N - (int64_t)c * kChunk;
+  const int64_t ns = (rem + spb - 1) / spb;
+  return ns < kb_per_chunk ? (int)ns : kb_per_chunk;
+}
 
 __global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                     StreamParams P) {
@@ -202,29 +276,31 @@ __global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __gri
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int d = (int)(it / P.n_chunks), c = (int)(it - (int64_t)d * P.n_chunks);
         (void)d;
-        const int64_t x0 = (int64_t)c * kChunk;
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
-        for (int kb = 0; kb < kb_per_chunk; ++kb) {
-          if (x0 + (int64_t)kb * kBoxK * P.nblk >= P.N) break;
-          mbar_wait(&full[stage], phase);
+        const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
+        for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {  // one TMEM sub-chunk
+          const int acc = local & 1;
+          const uint32_t acc_phase = (local >> 1) & 1;
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(stages + stage * kStageBytes);
+          const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
+          const int s1 = s0 + kSubStages < ns ? s0 + kSubStages : ns;
+          for (int kb = s0; kb < s1; ++kb) {
+            mbar_wait(&full[stage], phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(stages + stage * kStageBytes);
 #pragma unroll
-          for (int k = 0; k < kBoxK / 8; ++k) {  // 8 tf32 (32 B) per MMA along K
-            const uint64_t desc = sw128_desc(sa + 32 * k);
-            mma_tf32(tmem_d, desc, desc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBoxK / 8; ++k) {  // 8 tf32 (32 B) per MMA along K
+              const uint64_t desc = sw128_desc(sa + 32 * k);
+              mma_tf32(tmem_d, desc, desc, idesc, (kb > s0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          mma_commit(&tfull[acc]);
         }
-        mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM lanes 32q..32q+31
@@ -237,39 +313,22 @@ __global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __gri
     const bool has_users = 32 * q - blk * P.rb < R;
     const int NP = K * (K + 1) / 2;
     int local = 0;
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int d = (int)(it / P.n_chunks), c = (int)(it - (int64_t)d * P.n_chunks);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       double *out = P.ws + (((size_t)(P.drop0 + d) * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
-      if (has_users) {
-        for (int cb = 0; cb < (R + 31) / 32; ++cb) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + col0 + 32 * cb), v);
-          float x[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
-          // even lane (re row 2i): j-pairs 0..7 of this 32-column group; odd lane (im row): 8..15
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const int jj = plane * 8 + h;
-            const int j = 16 * cb + jj;
-            float rr, rr2, ri, ir;  // R(2i,2j), R(2i+1,2j+1), R(2i,2j+1), R(2i+1,2j)
-            if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
-            else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
-            if (i < K && j < K && j >= i) {
-              const int p = i * K - i * (i - 1) / 2 + (j - i);
-              out[2 * p] = (double)rr + (double)rr2;
-              out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
-            }
-          }
-        }
+      const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
+      for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tfull[acc], acc_phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (has_users)
+          drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * P.n_mma + col0),
+                         (uint32_t)(2 * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kSubStages >= ns, out);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
@@ -519,29 +578,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int64_t d = it / P.n_chunks;
         const int c = (int)(it - d * P.n_chunks);
-        const int64_t x0 = (int64_t)c * kChunk;
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
-        for (int kb = 0; kb < kb_per_chunk; ++kb) {
-          if (x0 + (int64_t)kb * kBoxK * P.nblk >= P.N) break;
-          mbar_wait(&full[stage], phase);
+        const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
+        for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {  // one TMEM sub-chunk
+          const int acc = local & 1;
+          const uint32_t acc_phase = (local >> 1) & 1;
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(stages + stage * kStageBytes);
+          const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
+          const int s1 = s0 + kSubStages < ns ? s0 + kSubStages : ns;
+          for (int kb = s0; kb < s1; ++kb) {
+            mbar_wait(&full[stage], phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(stages + stage * kStageBytes);
 #pragma unroll
-          for (int k = 0; k < kBoxK / 8; ++k) {
-            const uint64_t desc = sw128_desc(sa + 32 * k);
-            mma_tf32(tmem_d, desc, desc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBoxK / 8; ++k) {
+              const uint64_t desc = sw128_desc(sa + 32 * k);
+              mma_tf32(tmem_d, desc, desc, idesc, (kb > s0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == kFStages) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&empty[stage]);
-          if (++stage == kFStages) { stage = 0; phase ^= 1; }
+          mma_commit(&tfull[acc]);
         }
-        mma_commit(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue, warps kEpiWarp0..+3 = TMEM lane quadrants 0..3
@@ -554,39 +615,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     const bool has_users = 32 * q - blk * P.rb < R;
     const int NP = K * (K + 1) / 2;
     int local = 0;
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
-      if (has_users) {
-        for (int cb = 0; cb < (R + 31) / 32; ++cb) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * P.n_mma + col0 + 32 * cb), v);
-          float x[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const int jj = plane * 8 + h;
-            const int j = 16 * cb + jj;
-            float rr, rr2, ri, ir;
-            if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
-            else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
-            if (i < K && j < K && j >= i) {
-              const int p = i * K - i * (i - 1) / 2 + (j - i);
-              out[2 * p] = (double)rr + (double)rr2;
-              out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
-            }
-          }
-        }
+      const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
+      for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tfull[acc], acc_phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (has_users)
+          drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * P.n_mma + col0),
+                         (uint32_t)(2 * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kSubStages >= ns, out);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
@@ -1078,7 +1123,7 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   P.n_chunks = stream_tc_chunks(N);
   P.n_drops = n_drops;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * P.n_mma)) cols <<= 1;
+  while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
   P.tmem_cols = cols;
   const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
   cudaFuncSetAttribute(gram_fused_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1252,7 +1297,7 @@ int launch_stream_tc(const float *H, int K, int64_t N, int64_t drop0, int nb, do
   P.drop0 = drop0;
   P.nb = nb;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * P.n_mma)) cols <<= 1;
+  while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
   P.tmem_cols = cols;
   const size_t smem = 1024 + (size_t)kStages * kStageBytes + (2 * kStages + 4) * 8 + 16;
   cudaFuncSetAttribute(gram_stream_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

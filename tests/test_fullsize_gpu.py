@@ -134,8 +134,10 @@ def test_cfg3_fp32_sweep_rates_every_drop(xl, orc):
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
 def test_draw_words_bit_exact_and_positions_within_2ulp(xl, orc, cfg):
     """R19: the Philox4x64-10 words behind every drop are bit-identical to the oracle's
-    generator (itself pinned to numpy's Philox); positions (r cos el cos az, r cos el sin az,
-    r sin el) within 2 ulp per coordinate (the only difference is libm vs CUDA sin/cos)."""
+    generator (itself pinned to numpy's Philox); r, az, el are then the same doubles on both
+    sides (no FMA contraction), so positions (r cos el cos az, r cos el sin az, r sin el) differ
+    only by libm vs CUDA sin/cos: <= 2 ulp per coordinate for planar users (el = 0, one trig
+    factor), <= 3 ulp for the UPA's 3-D users (two trig factors, cfg4)."""
     w = CONFIGS[cfg]
     n = min(w.n_drops, 256)
     words = xl.draw_words(w.K, n, seed=w.seed).cpu().numpy()
@@ -148,7 +150,7 @@ def test_draw_words_bit_exact_and_positions_within_2ulp(xl, orc, cfg):
     exact_zero = po == 0.0
     assert np.array_equal(pg[exact_zero], po[exact_zero])
     ulp = np.abs(pg - po)[~exact_zero] / np.spacing(np.abs(po[~exact_zero]))
-    assert ulp.max() <= 2.0, ulp.max()
+    assert ulp.max() <= (3.0 if w.el != (0.0, 0.0) else 2.0), ulp.max()
     # first_drop addressing of the words (sharding / resume)
     tail = xl.draw_words(w.K, 10, seed=w.seed, first_drop=n - 10).cpu().numpy()
     assert np.array_equal(tail, words[n - 10:])
