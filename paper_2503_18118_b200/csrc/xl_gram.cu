@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "xl_common.cuh"
 
@@ -701,30 +702,34 @@ void launch_mt(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ kernel MT2
-// DMMA Gram for K = 17..64 with a branch-free inner loop (the default for fp64
-// K > 16).  The real-ified Gram R = A A^T (A = the 2K x N real matrix of re/im
-// rows, one m8n8k4 fragment "plane" per 8 users) is covered by the G(G+1)/2
-// 2x2 plane blocks (g1 <= g2); every block is one job of exactly four DMMAs
-// (RR, II, RI, IR) on four fragment loads -- diagonal blocks included, whose
-// IR = RI^T is redundant (G of the 2G(G+1) DMMAs per step, 6-11%) but keeps the
-// loop uniform: Re G = RR + II, Im G = RI - IR for every (i <= j).  Warps are
-// (job group jg, step group sg): JPW jobs per warp over the steps s == sg mod SG
-// of each tile; the SG partial accumulators meet in shared memory at level ends.
-// The NW = (J/JPW)*SG warps are a multiple of 4 so that each SM sub-partition
-// (warp % 4) gets the same DMMA and generation load.  Tiles of 4S elements are
-// generated (one 32-lane fragment row = 4 elements x 8 users per warp-iteration)
-// into a double buffer, so one barrier per tile separates generation of tile i+1
-// from the DMMAs of tile i.  The tile length is chosen so the S*G generated rows split
-// evenly over the NW warps (the barrier waits on the busiest one): G = 4, 20 steps
-// (cfg4 17.6 -> 15.8 ms against 16 steps); G = 8, 18 steps (cfg5 25.3 -> 24.3 ms).
+// DMMA Gram for K = 17..64 (the default for fp64 K > 16), three real DMMAs per
+// complex 8 x 8 block.  With A, B the re / im fragment planes of 8 users each (one
+// m8n8k4 fragment per 8 users and 4 elements), the block of plane groups (c, p) is
+//   G(c, p) = sum conj(h_c) h_p:  Re = P1 + P2,  Im = P1 - P2 - P3,
+//   P1 = A_c A_p^T,  P2 = B_c B_p^T,  P3 = (A_c + B_c)(A_p - B_p)^T
+// (the 3M form of the complex product: one DMMA fewer than RR, II, RI, IR, for two
+// fp64 adds on fragments -- its cancellation in Im costs ~eps sqrt(G_ii G_jj), i.e.
+// nothing against the normalised 1e-9 tier, R9).  The G(G+1)/2 blocks g1 <= g2 are
+// dealt to warps as STARS: a warp owns JPW blocks that share one centre group c
+// (c, p_1..p_JPW), so A_c, B_c and A_c + B_c are loaded / formed once per step; a star
+// decomposition exists when the blocks can be oriented so that every group's count of
+// blocks it centres (its own diagonal block included) is a multiple of JPW -- a
+// tournament score condition (Landau), found by a small search on the host
+// (star_plan).  Warps are (star, step group sg): the stars over the steps s == sg mod
+// SG of each tile; the SG partial accumulators meet in shared memory at level ends.
+// NW = stars * SG is a multiple of 4 (same DMMA load per SM sub-partition) except
+// G = 6, 7 (14 warps).  Tiles of 4S elements are generated (one 32-lane fragment row =
+// 4 elements x 8 users per warp-iteration) into a double buffer or a 3-deep mbarrier
+// ring; the tile length splits the S*G generated rows evenly over the warps.
+// Measured (cfg5, K = 64, 1000 drops): 4 DMMAs per block 782 ms -> see DESIGN.md 6.1.
 template <int G>
 struct Mt2Cfg;
-template <> struct Mt2Cfg<3> { static constexpr int JPW = 1, SG = 2, S = 8; };   // NW 12
-template <> struct Mt2Cfg<4> { static constexpr int JPW = 1, SG = 2, S = 10; };  // NW 20, 4 rows/warp
-template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };   // NW 20
-template <> struct Mt2Cfg<6> { static constexpr int JPW = 7, SG = 4, S = 8; };   // NW 12
-template <> struct Mt2Cfg<7> { static constexpr int JPW = 7, SG = 2, S = 8; };   // NW 8
-template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 9; };   // NW 12, 12 rows/warp
+template <> struct Mt2Cfg<3> { static constexpr int JPW = 2, SG = 4, S = 8; };   // 3 stars, NW 12
+template <> struct Mt2Cfg<4> { static constexpr int JPW = 2, SG = 4, S = 10; };  // 5 stars, NW 20
+template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };   // 5 stars, NW 20
+template <> struct Mt2Cfg<6> { static constexpr int JPW = 3, SG = 2, S = 8; };   // 7 stars, NW 14
+template <> struct Mt2Cfg<7> { static constexpr int JPW = 4, SG = 2, S = 8; };   // 7 stars, NW 14
+template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 9; };   // 12 stars, NW 12, 12 rows/warp
 
 template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::S; NBUF tile buffers
 struct Mt2 {
@@ -732,11 +737,20 @@ struct Mt2 {
   static constexpr int JG = J / JPW, NW = JG * SG, NT = 32 * NW;
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
-  static_assert(J % JPW == 0 && S % SG == 0 && NW % 4 == 0, "Mt2Cfg");
+  static_assert(J % JPW == 0 && S % SG == 0, "Mt2Cfg");
   static constexpr size_t tiles_bytes = 2ull * NBUF * PLANE * sizeof(double);  // NBUF buffers x re/im
-  static constexpr size_t stage_bytes = (size_t)J * 4 * SG * 64 * sizeof(double);
+  static constexpr size_t stage_bytes = (size_t)J * 3 * SG * 64 * sizeof(double);
   static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
   static_assert(smem <= 220 * 1024, "Mt2 shared memory");
+};
+
+// Star plan of the MT2 kernel: star s (warp's job group) = centre cen[s] and partners
+// par[s][k]; blk[g1 * 8 + g2] (g1 <= g2) = 2 * (job s * JPW + k) + (1 if the star holds
+// the block as (g2, g1), i.e. transposed).
+struct StarPlan {
+  int8_t cen[16];
+  int8_t par[16][4];
+  int16_t blk[64];
 };
 
 struct FastDiv {  // q = (umulhi(m, t) + t) >> sh == t / d for 0 <= t < 2^31
@@ -797,7 +811,8 @@ __device__ __forceinline__ void mt_arrive(uint64_t *bar) {
 // full/empty mbarriers (every thread arrives), so warps drift up to a tile apart
 // instead of draining the FP64 pipe at every tile boundary.
 template <int G, int SM, int NBUF, int KIND>
-__global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd) {
+__global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd,
+                                                                         const __grid_constant__ StarPlan plan) {
   using C = Mt2<G, SM, NBUF>;
   constexpr int JPW = C::JPW, SG = C::SG, S = C::S, NW = C::NW, NT = C::NT, JG = C::JG;
   constexpr int PLANE = C::PLANE, ROWS = C::ROWS;
@@ -826,14 +841,10 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int jg = warp % JG, sg = warp / JG;
-  int aoff[JPW], boff[JPW];  // fragment offsets of the job's two planes (row-major g1 <= g2 order)
+  const int coff = plan.cen[jg] * 32 + lane;  // the star's centre fragment
+  int poff[JPW];                              // its partners' fragments
 #pragma unroll
-  for (int k = 0; k < JPW; ++k) {
-    int q = jg * JPW + k, g1 = 0;
-    while (q >= G - g1) { q -= G - g1; ++g1; }
-    aoff[k] = g1 * 32 + lane;
-    boff[k] = (g1 + q) * 32 + lane;
-  }
+  for (int k = 0; k < JPW; ++k) poff[k] = plan.par[jg][k] * 32 + lane;
   __syncthreads();
   const double c4 = 4.0 * P.inv_lambda;
   const bool n_odd = (P.N & 1) != 0;
@@ -846,11 +857,11 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     const int lv1 = (int)P.lvl_end[l];
     const int a = max(lv0, s0), b = min(lv1, s1);
     lv0 = lv1;
-    double acc[JPW][4][2];
+    double acc[JPW][3][2];
 #pragma unroll
     for (int k = 0; k < JPW; ++k)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+      for (int m = 0; m < 3; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
     // warp w generates the consecutive rows [w R, (w+1) R) (row = s * G + g, g fastest),
     // so runs of up to G rows share one element step s and decode its coordinates once
     // (a UPA decode costs 4 FP64 ops, a ULA one 2: otherwise repeated for every group)
@@ -890,14 +901,14 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
 #pragma unroll
       for (int si = 0; si < S / SG; ++si) {
         const int so = si * SG * G * 32;
+        const double ar = cre[so + coff], ai = cim[so + coff];
+        const double as = ar + ai;
 #pragma unroll
         for (int k = 0; k < JPW; ++k) {
-          const double ar = cre[so + aoff[k]], ai = cim[so + aoff[k]];
-          const double br = cre[so + boff[k]], bi = cim[so + boff[k]];
-          dmma(acc[k][0], ar, br);
-          dmma(acc[k][1], ai, bi);
-          dmma(acc[k][2], ar, bi);
-          dmma(acc[k][3], ai, br);
+          const double br = cre[so + poff[k]], bi = cim[so + poff[k]];
+          dmma(acc[k][0], ar, br);       // P1
+          dmma(acc[k][1], ai, bi);       // P2
+          dmma(acc[k][2], as, br - bi);  // P3
         }
       }
     };
@@ -938,8 +949,8 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     for (int k = 0; k < JPW; ++k) {
       const int q = jg * JPW + k;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        double *st = dsm + ((q * 4 + m) * SG + sg) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
+      for (int m = 0; m < 3; ++m) {
+        double *st = dsm + ((q * 3 + m) * SG + sg) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
         st[0] = acc[k][m][0];
         st[1] = acc[k][m][1];
       }
@@ -951,40 +962,104 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
       int i = 0, rem = p;
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
-      const int g1 = i >> 3, g2 = j >> 3, e = (i & 7) * 8 + (j & 7);
-      const int q = g1 * G - g1 * (g1 - 1) / 2 + (g2 - g1);
-      const double *st = dsm + (size_t)q * 4 * SG * 64 + e;
-      double re = 0.0, im = 0.0;
+      const int bq = plan.blk[(i >> 3) * 8 + (j >> 3)];
+      const bool tr = bq & 1;  // block held as (g2, g1): read (j, i) and conjugate
+      const int e = tr ? (j & 7) * 8 + (i & 7) : (i & 7) * 8 + (j & 7);
+      const double *st = dsm + (size_t)(bq >> 1) * 3 * SG * 64 + e;
+      double p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
       for (int g = 0; g < SG; ++g) {
-        re += st[(0 * SG + g) * 64] + st[(1 * SG + g) * 64];
-        im += st[(2 * SG + g) * 64] - st[(3 * SG + g) * 64];
+        p1 += st[(0 * SG + g) * 64];
+        p2 += st[(1 * SG + g) * 64];
+        p3 += st[(2 * SG + g) * 64];
       }
-      out[2 * p] = re;
-      out[2 * p + 1] = (i == j) ? 0.0 : im;
+      const double im = p1 - p2 - p3;
+      out[2 * p] = p1 + p2;
+      out[2 * p + 1] = (i == j) ? 0.0 : (tr ? -im : im);
     }
     __syncthreads();
   }
 }
 
+// Star decomposition of the G(G+1)/2 plane blocks into stars of JPW blocks sharing a centre
+// (see kernel MT2): orient every pair {a, b} (a < b) towards one centre so that each group's
+// centred-block count (+1 for its own diagonal block) is a multiple of JPW, by depth-first
+// search over the pairs; then cut each group's list (diagonal first) into stars.
+bool star_plan(int G, int JPW, StarPlan &pl) {
+  int pa[28], pb[28], n = 0;
+  for (int a = 0; a < G; ++a)
+    for (int b = a + 1; b < G; ++b) { pa[n] = a; pb[n] = b; ++n; }
+  int out[8] = {0}, left[8], to[28];
+  for (int v = 0; v < G; ++v) left[v] = G - 1;
+  auto can = [&](int v) {  // some multiple of JPW is still reachable for v
+    for (int d = out[v]; d <= out[v] + left[v]; ++d)
+      if ((d + 1) % JPW == 0) return true;
+    return false;
+  };
+  std::vector<int> st;  // DFS over pairs: choice 0 = a centres, 1 = b centres
+  int k = 0, choice = 0;
+  while (k < n) {
+    bool placed = false;
+    for (; choice < 2; ++choice) {
+      const int c = choice ? pb[k] : pa[k];
+      ++out[c]; --left[pa[k]]; --left[pb[k]];
+      if (can(pa[k]) && can(pb[k])) { to[k] = choice; st.push_back(choice); ++k; choice = 0; placed = true; break; }
+      --out[c]; ++left[pa[k]]; ++left[pb[k]];
+    }
+    if (placed) continue;
+    if (st.empty()) return false;  // no decomposition
+    --k;
+    choice = st.back();
+    st.pop_back();
+    const int c = choice ? pb[k] : pa[k];
+    --out[c]; ++left[pa[k]]; ++left[pb[k]];
+    ++choice;
+  }
+  for (int v = 0; v < G; ++v)
+    if ((out[v] + 1) % JPW) return false;
+  int ns = 0;
+  for (int v = 0; v < G; ++v) {
+    int list[8], m = 0;
+    list[m++] = v;
+    for (int e = 0; e < n; ++e)
+      if ((to[e] ? pb[e] : pa[e]) == v) list[m++] = to[e] ? pa[e] : pb[e];
+    for (int q = 0; q < m; q += JPW, ++ns) {
+      pl.cen[ns] = (int8_t)v;
+      for (int t = 0; t < JPW; ++t) {
+        const int p = list[q + t];
+        pl.par[ns][t] = (int8_t)p;
+        const int job = ns * JPW + t;
+        if (v <= p) pl.blk[v * 8 + p] = (int16_t)(2 * job);
+        else pl.blk[p * 8 + v] = (int16_t)(2 * job + 1);
+      }
+    }
+  }
+  return ns * JPW == G * (G + 1) / 2;
+}
+
 template <int G, int SM, int NBUF, int KIND>
-void launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   using C = Mt2<G, SM, NBUF>;
+  static StarPlan plan;
+  static const bool ok = star_plan(G, C::JPW, plan);
+  if (!ok) return xlh::set_error(XLMIMO_EUNSUPPORTED, "mt2: no star decomposition for G=%d, JPW=%d", G, C::JPW);
   const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
   cudaFuncSetAttribute(gram_mt2_kernel<G, SM, NBUF, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-  gram_mt2_kernel<G, SM, NBUF, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd);
+  gram_mt2_kernel<G, SM, NBUF, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd, plan);
+  return XLMIMO_OK;
 }
 
 // Tiles of 2*Mt2Cfg<G>::S steps.  Buffers: 2 (one barrier per tile) for G <= 4, the
 // 3-deep mbarrier ring above (measured on B200: cfg4 K=32 17.65 vs 18.50 ms with the
 // ring; cfg5 K=64 25.24 vs 25.79 ms).  XLMIMO_OPT_MT2_BUFFERS = 2|3 overrides.
 template <int G>
-void launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
+int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int env = (int)xlh::option(XLMIMO_OPT_MT2_BUFFERS);
   const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
-  if (nbuf == 2) ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
-  else ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
+  if (nbuf == 2)
+    return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
+  return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
 }
 
 // ------------------------------------------------------------------ kernel BLK
@@ -1834,14 +1909,16 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       default: launch_mt<8>(P, n_blocks, s); break;
     }
   } else if (kc.which == 3) {
+    int rc;
     switch ((K + 7) / 8) {
-      case 3: launch_mt2<3>(P, n_blocks, s); break;
-      case 4: launch_mt2<4>(P, n_blocks, s); break;
-      case 5: launch_mt2<5>(P, n_blocks, s); break;
-      case 6: launch_mt2<6>(P, n_blocks, s); break;
-      case 7: launch_mt2<7>(P, n_blocks, s); break;
-      default: launch_mt2<8>(P, n_blocks, s); break;
+      case 3: rc = launch_mt2<3>(P, n_blocks, s); break;
+      case 4: rc = launch_mt2<4>(P, n_blocks, s); break;
+      case 5: rc = launch_mt2<5>(P, n_blocks, s); break;
+      case 6: rc = launch_mt2<6>(P, n_blocks, s); break;
+      case 7: rc = launch_mt2<7>(P, n_blocks, s); break;
+      default: rc = launch_mt2<8>(P, n_blocks, s); break;
     }
+    if (rc) return rc;
   } else if (kc.which == 2) {
     const bool ula = a.kind == XLMIMO_ULA;
     if (K <= 8) {
