@@ -127,20 +127,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
       "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
       "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
       "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
-      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
-      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
-      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
-      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
-      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      "r"(__float_as_uint(v[15]))
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -151,30 +158,30 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 // (round to nearest: unbiased, unlike the tensor core's own accumulation); the last adds the
 // running sum, pairs re/im rows with the neighbouring lane and writes
 //   Re G(i,j) = R(2i,2j) + R(2i+1,2j+1),  Im G(i,j) = R(2i,2j+1) - R(2i+1,2j)
-// (even lane: j-pairs 0..7 of each 32-column group, odd lane: 8..15) into the item's fp64
-// partial `out` (packed upper triangle).
+// (even lane: j-pairs 0..3 of each 16-column slab, odd lane: 4..7) into the item's fp64
+// partial `out` (packed upper triangle).  16-column slabs keep the live set at 32 floats.
 __device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_col, uint32_t run_col, int R, int K,
                                                int i, int plane, bool first, bool last, double *out) {
-  for (int cb = 0; cb < (R + 31) / 32; ++cb) {
-    float v[32];
-    tmem_ld32(lane_base + acc_col + (uint32_t)(32 * cb), v);
+  for (int cb = 0; cb < (R + 15) / 16; ++cb) {
+    float v[16];
+    tmem_ld16(lane_base + acc_col + (uint32_t)(16 * cb), v);
     if (!first) {
-      float r[32];
-      tmem_ld32(lane_base + run_col + (uint32_t)(32 * cb), r);
+      float r[16];
+      tmem_ld16(lane_base + run_col + (uint32_t)(16 * cb), r);
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] += r[e];
+      for (int e = 0; e < 16; ++e) v[e] += r[e];
     }
     if (!last) {
-      tmem_st32(lane_base + run_col + (uint32_t)(32 * cb), v);
+      tmem_st16(lane_base + run_col + (uint32_t)(16 * cb), v);
       continue;
     }
-    float x[32];
+    float x[16];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
+    for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
 #pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const int jj = plane * 8 + h;
-      const int j = 16 * cb + jj;
+    for (int h = 0; h < 4; ++h) {
+      const int jj = plane * 4 + h;
+      const int j = 8 * cb + jj;
       float rr, rr2, ri, ir;  // R(2i,2j), R(2i+1,2j+1), R(2i,2j+1), R(2i+1,2j)
       if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
       else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
@@ -454,6 +461,82 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
   }
 }
 
+
+// The fused kernel's generator task: TE (8 or 16) consecutive elements t0 .. t0 + TE - 1 of
+// one user, from an fp64 anchor at the task's CENTRE (element t0 + (TE - 1)/2, a half-
+// integer position), so the Taylor offsets are |m'| <= (TE - 1)/2 pitches: a 16-element task
+// has the truncation of gen_task_tf32's 8-element one (d^5/r^4 over 7.5 pitches) for half
+// the anchors.  Same expansion as gen_task_tf32 with m' = m - (TE - 1)/2.  The outputs are
+// rounded for the tensor core only: + half a TF32 ulp on the magnitude bits and NO mask --
+// kind::tf32 reads the top 19 bits of each 32-bit operand and ignores the other 13 (that
+// truncation is why raw fp32 would bias the diagonal), so the add alone is round-to-nearest
+// (ties away).  Full tasks (all TE elements < N) skip the per-element padding select.
+template <int TE>
+__device__ __forceinline__ void gen_task_c(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
+                                           int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
+                                           float pitch_f, uint32_t (&vr)[TE], uint32_t (&vi)[TE]) {
+  constexpr double kMid = 0.5 * (TE - 1);
+  double ey, ez = 0.0;
+  if (kind == XLMIMO_ULA) {
+    ey = ((double)t0 + (kMid - 0.5 * (double)(N - 1))) * pitch;
+  } else {  // the task lies in one row (n_y % TE == 0)
+    int64_t q, pp;
+    if (t0 < ((int64_t)1 << 31)) {
+      const uint32_t q32 = (uint32_t)t0 / (uint32_t)n_y;
+      q = q32;
+      pp = (int64_t)((uint32_t)t0 - q32 * (uint32_t)n_y);
+    } else {
+      q = t0 / n_y;
+      pp = t0 - q * n_y;
+    }
+    ey = ((double)pp + (kMid - 0.5 * (double)(n_y - 1))) * pitch;
+    ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
+  }
+  const double dy = ey - uc.y, dz = ez - uc.z;
+  const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
+  const double ir = xl::rsqrt_nr(r2);
+  const double rc = r2 * ir;
+  const double qc = rc * inv_lambda;
+  constexpr float k2pi = 6.28318530717958647692f;
+  const float fc = (float)(qc - rint(qc)) * k2pi;
+  const float irf = (float)ir, u = (float)(dy * ir);
+  const float w = fmaf(-u, u, 1.0f) * irf;
+  const float pl = k2pi * pitch_f * inv_lambda_f;
+  const float p1 = pitch_f * irf, pp = pitch_f * pl;
+  const float ca = u * pl;
+  const float cb = 0.5f * w * pp;
+  const float cg = -0.5f * u * w * p1 * pp;
+  const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;
+  const float ac = (float)uc.w * irf * rsqrtf((float)rc);
+  const float a0 = ac;
+  const float a1 = ac * (-1.5f * u * p1);
+  const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
+  if (N - t0 >= TE) {
+#pragma unroll
+    for (int m = 0; m < TE; ++m) {
+      const float fm = (float)m - (float)kMid;
+      const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
+      float sn, co;
+      __sincosf(ph, &sn, &co);
+      const float a = fmaf(fmaf(a2, fm, a1), fm, a0);
+      vr[m] = __float_as_uint(a * co) + 0x1000u;
+      vi[m] = __float_as_uint(-a * sn) + 0x1000u;
+    }
+  } else {
+    const int nv = (int)(N - t0);
+#pragma unroll
+    for (int m = 0; m < TE; ++m) {
+      const float fm = (float)m - (float)kMid;
+      const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
+      float sn, co;
+      __sincosf(ph, &sn, &co);
+      const float a = (m < nv) ? fmaf(fmaf(a2, fm, a1), fm, a0) : 0.0f;
+      vr[m] = __float_as_uint(a * co) + 0x1000u;
+      vi[m] = __float_as_uint(-a * sn) + 0x1000u;
+    }
+  }
+}
+
 constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
 #ifndef XL_GEN_GROUPS
 #define XL_GEN_GROUPS 10
@@ -469,6 +552,7 @@ constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM la
 constexpr int kMmaWarp = kEpiWarp0 + 4;            // 20
 constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 672
 
+template <int TE>
 __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -519,8 +603,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     const float pitch_f = (float)P.pitch;
     // element blocks stacked in the 128 rows (as in the stream kernel): block b of a
     // stage covers elements xs + 32 b .. + 31 in rows rb*b .. rb*b + 2K - 1
-    const int n_tasks = P.nblk * K * (kBoxK / kTaskE);
-    const int tpb = K * (kBoxK / kTaskE);  // tasks per block
+    constexpr int kTpr = kBoxK / TE;       // tasks per user row of a block (2 or 4)
+    const int n_tasks = P.nblk * K * kTpr;
+    const int tpb = K * kTpr;              // tasks per block
     const uint32_t stages_base = smem_u32(stages);
     int64_t kstart = 0;  // global index of the item's first stage
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -551,14 +636,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         int blk = gtid / tpb, tb = gtid - blk * tpb;
         for (int task = gtid; task < n_tasks; task += kGenThreads, tb += kGenThreads) {
           while (tb >= tpb) { tb -= tpb; ++blk; }
-          const int u = tb / (kBoxK / kTaskE), g8 = tb % (kBoxK / kTaskE);
+          const int u = tb / kTpr, g8 = tb % kTpr;
           const int row0 = blk * P.rb + 2 * u;
-          const int64_t t0 = xs + kBoxK * blk + kTaskE * g8;
-          uint32_t vr[kTaskE], vi[kTaskE];
-          gen_task_tf32(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
+          const int64_t t0 = xs + kBoxK * blk + TE * g8;
+          uint32_t vr[TE], vi[TE];
+          gen_task_c<TE>(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
 #pragma unroll
-          for (int h = 0; h < kTaskE / 4; ++h) {
-            const int chunk = (kTaskE / 4) * g8 + h;
+          for (int h = 0; h < TE / 4; ++h) {
+            const int chunk = (TE / 4) * g8 + h;
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0, chunk)),
                          "r"(vr[4 * h]), "r"(vr[4 * h + 1]), "r"(vr[4 * h + 2]), "r"(vr[4 * h + 3])
                          : "memory");
@@ -1126,13 +1211,19 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
   P.tmem_cols = cols;
   const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
-  cudaFuncSetAttribute(gram_fused_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = n_drops * P.n_chunks;
   const int grid = (int)(items < sms ? items : sms);
-  gram_fused_tc_kernel<<<grid, kFusedThreads, smem, s>>>(P);
+  // 16-element tasks wherever a task stays in one array row (every ULA; UPA rows of 16k)
+  if (a.kind == XLMIMO_ULA || a.n_y % 16 == 0) {
+    cudaFuncSetAttribute(gram_fused_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gram_fused_tc_kernel<16><<<grid, kFusedThreads, smem, s>>>(P);
+  } else {
+    cudaFuncSetAttribute(gram_fused_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gram_fused_tc_kernel<8><<<grid, kFusedThreads, smem, s>>>(P);
+  }
   return check_launch("gram_fused_tc_kernel");
 }
 
