@@ -15,10 +15,12 @@
 // quadrants 0..3), double-buffered TMEM accumulator so the epilogue of one chunk
 // overlaps the MMAs of the next.  Bounded mbarrier waits trap instead of hanging.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "xl_common.cuh"
 
@@ -36,6 +38,7 @@ constexpr int kChunk = 8192;           // elements per work item (one fp64 parti
 // <= ~3e-6); the epilogue folds the sub-chunk sums into a running fp32 sum kept in a third
 // TMEM region (drain_subchunk) and writes the item's fp64 partial after the last one.
 constexpr int kSubStages = 16;
+constexpr int kFSubStages = 8;  // fused kernel: fp16 stages hold 64 elements, so 8 stages = 32 MMAs x 16
 constexpr int kThreads = 256;
 
 // element blocks stacked per stage in the 128 MMA rows: 2K <= 32 -> 4 blocks, <= 64 -> 2, else 1
@@ -47,16 +50,19 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
 
+// Parity wait with a suspend-time hint: a waiting warp is parked (up to ~20 us per attempt,
+// woken when the phase completes) instead of re-issuing try_wait, so waiting warps do not
+// take issue slots from the working ones.  Bounded: a lost arrival traps instead of hanging.
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   const uint32_t a = smem_u32(b);
   uint32_t done = 0;
-  for (uint32_t it = 0; it < (1u << 26); ++it) {
+  for (uint32_t it = 0; it < (1u << 20); ++it) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(20000u)
         : "memory");
     if (done) return;
   }
@@ -97,6 +103,21 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major (same fields as tf32_idesc)
+__host__ __device__ constexpr uint32_t f16_idesc(int M, int N) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -105,6 +126,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// one lane of a converged warp (elect.sync): the warp runs the issue loop together, so its
+// descriptors and counters are warp-uniform and live in uniform registers, and one lane
+// issues each tcgen05 instruction (no per-instruction R2UR / ELECT retry loop)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -161,7 +193,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 // (even lane: j-pairs 0..3 of each 16-column slab, odd lane: 4..7) into the item's fp64
 // partial `out` (packed upper triangle).  16-column slabs keep the live set at 32 floats.
 __device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_col, uint32_t run_col, int R, int K,
-                                               int i, int plane, bool first, bool last, double *out) {
+                                               int i, int plane, bool first, bool last, double *out,
+                                               double post = 1.0) {
   for (int cb = 0; cb < (R + 15) / 16; ++cb) {
     float v[16];
     tmem_ld16(lane_base + acc_col + (uint32_t)(16 * cb), v);
@@ -187,8 +220,8 @@ __device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_
       else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
       if (i < K && j < K && j >= i) {
         const int p = i * K - i * (i - 1) / 2 + (j - i);
-        out[2 * p] = (double)rr + (double)rr2;
-        out[2 * p + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+        out[2 * p] = ((double)rr + (double)rr2) * post;
+        out[2 * p + 1] = (i == j) ? 0.0 : ((double)ri - (double)ir) * post;
       }
     }
   }
@@ -466,15 +499,16 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
 // one user, from an fp64 anchor at the task's CENTRE (element t0 + (TE - 1)/2, a half-
 // integer position), so the Taylor offsets are |m'| <= (TE - 1)/2 pitches: a 16-element task
 // has the truncation of gen_task_tf32's 8-element one (d^5/r^4 over 7.5 pitches) for half
-// the anchors.  Same expansion as gen_task_tf32 with m' = m - (TE - 1)/2.  The outputs are
-// rounded for the tensor core only: + half a TF32 ulp on the magnitude bits and NO mask --
-// kind::tf32 reads the top 19 bits of each 32-bit operand and ignores the other 13 (that
-// truncation is why raw fp32 would bias the diagonal), so the add alone is round-to-nearest
-// (ties away).  Full tasks (all TE elements < N) skip the per-element padding select.
+// the anchors.  Same expansion as gen_task_tf32 with m' = m - (TE - 1)/2.  Output: the
+// coefficients times 2^e (the drop's power-of-two scale, see gram_fused_tc_kernel) rounded
+// to fp16 (round to nearest even: 11 significant bits, the precision of TF32) and packed
+// in pairs, hr[q] = (re h_{2q}, re h_{2q+1}) low half first, hi likewise.  Full tasks
+// (all TE elements < N) skip the per-element padding select.
 template <int TE>
-__device__ __forceinline__ void gen_task_c(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
+__device__ __forceinline__ void gen_task_h(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
                                            int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
-                                           float pitch_f, uint32_t (&vr)[TE], uint32_t (&vi)[TE]) {
+                                           float pitch_f, float scale, uint32_t (&hr)[TE / 2],
+                                           uint32_t (&hi)[TE / 2]) {
   constexpr double kMid = 0.5 * (TE - 1);
   double ey, ez = 0.0;
   if (kind == XLMIMO_ULA) {
@@ -507,50 +541,82 @@ __device__ __forceinline__ void gen_task_c(const double4 &uc, int kind, int64_t 
   const float cb = 0.5f * w * pp;
   const float cg = -0.5f * u * w * p1 * pp;
   const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;
-  const float ac = (float)uc.w * irf * rsqrtf((float)rc);
+  const float ac = (float)uc.w * irf * rsqrtf((float)rc) * scale;
   const float a0 = ac;
   const float a1 = ac * (-1.5f * u * p1);
   const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
-  if (N - t0 >= TE) {
+  auto emit = [&](auto padded, int nv) {
+    float re[2], im[2];
 #pragma unroll
     for (int m = 0; m < TE; ++m) {
       const float fm = (float)m - (float)kMid;
       const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
       float sn, co;
       __sincosf(ph, &sn, &co);
-      const float a = fmaf(fmaf(a2, fm, a1), fm, a0);
-      vr[m] = __float_as_uint(a * co) + 0x1000u;
-      vi[m] = __float_as_uint(-a * sn) + 0x1000u;
+      float a = fmaf(fmaf(a2, fm, a1), fm, a0);
+      if (decltype(padded)::value) a = (m < nv) ? a : 0.0f;  // padding past N
+      re[m & 1] = a * co;
+      im[m & 1] = -a * sn;
+      if (m & 1) {
+        const __half2 hre = __floats2half2_rn(re[0], re[1]), him = __floats2half2_rn(im[0], im[1]);
+        hr[m >> 1] = *reinterpret_cast<const uint32_t *>(&hre);
+        hi[m >> 1] = *reinterpret_cast<const uint32_t *>(&him);
+      }
     }
-  } else {
-    const int nv = (int)(N - t0);
-#pragma unroll
-    for (int m = 0; m < TE; ++m) {
-      const float fm = (float)m - (float)kMid;
-      const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
-      float sn, co;
-      __sincosf(ph, &sn, &co);
-      const float a = (m < nv) ? fmaf(fmaf(a2, fm, a1), fm, a0) : 0.0f;
-      vr[m] = __float_as_uint(a * co) + 0x1000u;
-      vi[m] = __float_as_uint(-a * sn) + 0x1000u;
-    }
-  }
+  };
+  if (N - t0 >= TE) emit(std::false_type(), TE);  // every task but the array's last
+  else emit(std::true_type(), (int)(N - t0));
 }
 
-constexpr int kGenWarps = 2;       // warps per generator group (arrivals per full barrier)
-#ifndef XL_GEN_GROUPS
-#define XL_GEN_GROUPS 10
-#endif
-constexpr int kGenGroups = XL_GEN_GROUPS;  // group g makes stages k = g (mod groups), ring slot k % kFStages
-                                           // (10: cfg4 4.02 -> 3.76 ms, cfg3/cfg5 -1 %; 12 loses on cfg3/cfg5)
-#ifndef XL_FSTAGES
-#define XL_FSTAGES 12
-#endif
-constexpr int kFStages = XL_FSTAGES;  // ring slots: stage k -> slot k % kFStages, generated by group k % kGenGroups
+constexpr int kGenWarps = 2;       // pair kernels: warps per generator group (arrivals per full barrier)
 constexpr int kGenThreads = 32 * kGenWarps;
-constexpr int kEpiWarp0 = kGenWarps * kGenGroups;  // 16: warps 16..19 = TMEM lane quadrants 0..3
-constexpr int kMmaWarp = kEpiWarp0 + 4;            // 20
-constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 672
+// Fused K <= 64 kernel: kFGroups groups of kFGenWarps warps; group g makes stages
+// k = g (mod kFGroups) into ring slot k % kFStages.  The MMA consumes stages in order, so a
+// group's next stage (k + groups) waits for slot k + groups - slots to be consumed; with
+// slots >= 2 groups + 2 that stage belongs to an earlier round and the groups never wait
+// on each other (10 groups x 2 warps over 12 slots left the generators ~45 % of their time
+// in that wait: each round the later groups waited for the earlier ones' stages).
+#ifndef XL_FGEN_WARPS
+#define XL_FGEN_WARPS 4
+#endif
+#ifndef XL_FGEN_GROUPS
+#define XL_FGEN_GROUPS 5
+#endif
+#ifndef XL_FSTAGES
+#define XL_FSTAGES 13
+#endif
+constexpr int kFGenWarps = XL_FGEN_WARPS;
+constexpr int kFGroups = XL_FGEN_GROUPS;
+constexpr int kFStages = XL_FSTAGES;
+constexpr int kFGenThreads = 32 * kFGenWarps;
+constexpr int kEpiWarp0 = kFGenWarps * kFGroups;   // 20: warps 20..23 = TMEM lane quadrants 0..3
+constexpr int kMmaWarp = kEpiWarp0 + 4;            // 24
+constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 800
+
+constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one swizzle atom)
+
+// Per-drop power-of-two scale of the fp16 operands: the largest coefficient magnitude of a
+// user is sqrt(beta0) sqrt(x_eff) / x_eff^{3/2} = sqrt(beta0) / sqrt(xz2) (r >= x_eff), so
+// 2^e with e = -ilogb(sqrt(beta0) / sqrt(min_u xz2)) puts the drop's largest |h| in [1, 2)
+// and keeps the rest of it far inside fp16's normal range; the Gram is scaled by 4^e, undone
+// exactly in the epilogue.  Generators (from su) and epilogue (from pos via make_user)
+// evaluate the same doubles, so both sides use the same e.
+__device__ __forceinline__ float scale_of_min_xz2(double min_xz2, double sqrt_beta0) {
+  const int e = -ilogb(sqrt_beta0 / sqrt(min_xz2));
+  return __int_as_float((127 + e) << 23);
+}
+__device__ __forceinline__ float drop_scale(const double4 *su, int K, double sqrt_beta0) {
+  double m = su[0].x;
+  for (int u = 1; u < K; ++u) m = fmin(m, su[u].x);
+  return scale_of_min_xz2(m, sqrt_beta0);
+}
+__device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int kind, double sqrt_beta0, int lane) {
+  double m = INFINITY;
+  for (int u = lane; u < K; u += 32) m = fmin(m, xl::make_user(pos + u * 3, kind, sqrt_beta0).xz2);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return scale_of_min_xz2(m, sqrt_beta0);
+}
 
 template <int TE>
 __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
@@ -570,7 +636,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   for (int i = tid; i < kFStages * kStageBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < kFStages; ++s) {
-      mbar_init(&full[s], kGenWarps);
+      mbar_init(&full[s], kFGenWarps);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -590,20 +656,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
-  const int kb_per_chunk = kChunk / (kBoxK * P.nblk);
+  const int kb_per_chunk = kChunk / (kFBoxK * P.nblk);
 
   if (warp < kEpiWarp0) {  // ---------------- generators: group g makes stages k = g (mod 8)
     // The global stage sequence k (the MMA issuer's order) lives in slot k % 12 with
     // phase (k / 12) & 1; 12 slots for 8 groups let a group start its next stage
     // while the MMA still holds its previous one.
-    const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
+    const int grp = warp / kFGenWarps, gtid = tid - grp * kFGenThreads;
     double4 *su = su_all + grp * 64;
     const double inv_lambda = 1.0 / P.lambda;
     const float inv_lambda_f = (float)inv_lambda;
     const float pitch_f = (float)P.pitch;
     // element blocks stacked in the 128 rows (as in the stream kernel): block b of a
-    // stage covers elements xs + 32 b .. + 31 in rows rb*b .. rb*b + 2K - 1
-    constexpr int kTpr = kBoxK / TE;       // tasks per user row of a block (2 or 4)
+    // stage covers elements xs + 64 b .. + 63 (fp16: 64 per 128-B row) in rows rb*b .. rb*b + 2K - 1
+    constexpr int kTpr = kFBoxK / TE;      // tasks per user row of a block (4 or 8)
     const int n_tasks = P.nblk * K * kTpr;
     const int tpb = K * kTpr;              // tasks per block
     const uint32_t stages_base = smem_u32(stages);
@@ -613,19 +679,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int c = (int)(it - d * P.n_chunks);
       const int64_t x0 = (int64_t)c * kChunk;
       const int64_t rem = P.N - x0;
-      const int spb = kBoxK * P.nblk;  // elements per stage
+      const int spb = kFBoxK * P.nblk;  // elements per stage
       const int ns = (int)(((rem < kChunk ? rem : kChunk) + spb - 1) / spb);
-      int64_t k = kstart + (((int64_t)grp - kstart) % kGenGroups + kGenGroups) % kGenGroups;
+      int64_t k = kstart + (((int64_t)grp - kstart) % kFGroups + kFGroups) % kFGroups;
       kstart += ns;
       if (k >= kstart) continue;  // no stage of this item for this group
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
-      for (int u = gtid; u < K; u += kGenThreads) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
+      for (int u = gtid; u < K; u += kFGenThreads) {
         const double *p = P.pos + (d * K + u) * 3;
         const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
         su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
       }
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
-      for (; k < kstart; k += kGenGroups) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
+      const float scale = drop_scale(su, K, P.sqrt_beta0);
+      for (; k < kstart; k += kFGroups) {
         const int64_t xs = x0 + (k - (kstart - ns)) * spb;
         // more slots than groups: a group's next stage reuses a slot freed 4 stages ago,
         // so generation never waits on the MMA of its own previous stage
@@ -634,60 +701,71 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
         // (blk, tb) = divmod(task, tpb), stepped without a division (tpb = 4K >= 36 > 64/2)
         int blk = gtid / tpb, tb = gtid - blk * tpb;
-        for (int task = gtid; task < n_tasks; task += kGenThreads, tb += kGenThreads) {
+        for (int task = gtid; task < n_tasks; task += kFGenThreads, tb += kFGenThreads) {
           while (tb >= tpb) { tb -= tpb; ++blk; }
           const int u = tb / kTpr, g8 = tb % kTpr;
           const int row0 = blk * P.rb + 2 * u;
-          const int64_t t0 = xs + kBoxK * blk + TE * g8;
-          uint32_t vr[TE], vi[TE];
-          gen_task_c<TE>(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
+          const int64_t t0 = xs + kFBoxK * blk + TE * g8;
+          uint32_t hr[TE / 2], hi[TE / 2];
+#ifdef XL_EXP_NO_GEN  // tuning experiment: the MMA / epilogue-bound rate (results invalid)
 #pragma unroll
-          for (int h = 0; h < TE / 4; ++h) {
-            const int chunk = (TE / 4) * g8 + h;
+          for (int m = 0; m < TE / 2; ++m) hr[m] = hi[m] = (uint32_t)(t0 + m);
+#else
+          gen_task_h<TE>(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, scale, hr,
+                         hi);
+#endif
+#pragma unroll
+          for (int h = 0; h < TE / 8; ++h) {  // 8 fp16 = one 16-B chunk of the 128-B row
+            const int chunk = (TE / 8) * g8 + h;
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0, chunk)),
-                         "r"(vr[4 * h]), "r"(vr[4 * h + 1]), "r"(vr[4 * h + 2]), "r"(vr[4 * h + 3])
+                         "r"(hr[4 * h]), "r"(hr[4 * h + 1]), "r"(hr[4 * h + 2]), "r"(hr[4 * h + 3])
                          : "memory");
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0 + 1, chunk)),
-                         "r"(vi[4 * h]), "r"(vi[4 * h + 1]), "r"(vi[4 * h + 2]), "r"(vi[4 * h + 3])
+                         "r"(hi[4 * h]), "r"(hi[4 * h + 1]), "r"(hi[4 * h + 2]), "r"(hi[4 * h + 3])
                          : "memory");
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[slot]);  // kGenWarps arrivals complete the stage
+        if (lane == 0) mbar_arrive(&full[slot]);  // kFGenWarps arrivals complete the stage
       }
     }
-  } else if (warp == kMmaWarp) {  // ---------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = tf32_idesc(kRows, P.n_mma);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int64_t d = it / P.n_chunks;
-        const int c = (int)(it - d * P.n_chunks);
-        const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
-        for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {  // one TMEM sub-chunk
-          const int acc = local & 1;
-          const uint32_t acc_phase = (local >> 1) & 1;
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
+  } else if (warp == kMmaWarp) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+    const uint32_t idesc = f16_idesc(kRows, P.n_mma);
+    const uint64_t desc0 = sw128_desc(smem_u32(stages));  // slot s, k-step k: + s kStageBytes/16 + 2k
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t d = it / P.n_chunks;
+      const int c = (int)(it - d * P.n_chunks);
+      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk);
+      for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {  // one TMEM sub-chunk
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
+        const int s1 = s0 + kFSubStages < ns ? s0 + kFSubStages : ns;
+        for (int kb = s0; kb < s1; ++kb) {
+          mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
-          const int s1 = s0 + kSubStages < ns ? s0 + kSubStages : ns;
-          for (int kb = s0; kb < s1; ++kb) {
-            mbar_wait(&full[stage], phase);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t sa = smem_u32(stages + stage * kStageBytes);
+          const uint64_t ds = desc0 + (uint64_t)(stage * (kStageBytes >> 4));
+          if (elect_one()) {
+#ifdef XL_EXP_NO_MMA  // tuning experiment: the generator-bound rate (results invalid)
+            mbar_arrive(&empty[stage]);
+#else
 #pragma unroll
-            for (int k = 0; k < kBoxK / 8; ++k) {
-              const uint64_t desc = sw128_desc(sa + 32 * k);
-              mma_tf32(tmem_d, desc, desc, idesc, (kb > s0 || k > 0) ? 1u : 0u);
-            }
+            for (int k = 0; k < kFBoxK / 16; ++k)  // 16 fp16 (32 B) per MMA along K
+              mma_f16(tmem_d, ds + 2 * k, ds + 2 * k, idesc, (kb > s0 || k > 0) ? 1u : 0u);
             mma_commit(&empty[stage]);
-            if (++stage == kFStages) { stage = 0; phase ^= 1; }
+#endif
           }
-          mma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == kFStages) { stage = 0; phase ^= 1; }
         }
+        if (elect_one()) mma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else {  // ---------------- epilogue, warps kEpiWarp0..+3 = TMEM lane quadrants 0..3
@@ -704,15 +782,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
       double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
-      const int ns = item_stages(P.N, c, kb_per_chunk, kBoxK * P.nblk);
-      for (int s0 = 0; s0 < ns; s0 += kSubStages, ++local) {
+      const float sc = epi_drop_scale(P.pos + d * K * 3, K, P.kind, P.sqrt_beta0, lane);
+      const double post = 1.0 / ((double)sc * (double)sc);  // exact: sc is a power of two
+      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk);
+      for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tfull[acc], acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (has_users)
           drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * P.n_mma + col0),
-                         (uint32_t)(2 * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kSubStages >= ns, out);
+                         (uint32_t)(2 * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kFSubStages >= ns, out, post);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1210,7 +1290,7 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   uint32_t cols = 32;
   while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
   P.tmem_cols = cols;
-  const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kGenGroups * 64 * 32;
+  const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kFGroups * 64 * 32;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
