@@ -371,6 +371,114 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
   }
 }
 
+// ------------------------------------------------------------------ kernel W
+// Small arrays (N <= kWarpMaxN, one level, K <= 6, fp64): one WARP per drop, lane l takes
+// elements l, l + 32, ... (natural order), generates the drop's K coefficients per element
+// (coef_fast) and keeps the K(K+1)/2 complex sums in registers; the warp then reduces them
+// with a transpose-reduce (offsets 16..1, each lane keeping half of its values and
+// receiving the other half: 31 shuffled doubles for 32 slots instead of 5 x the slot
+// count), after which lane l holds slot l, and writes the Hermitian Gram directly -- no
+// partials, no block barriers, no second kernel.  cfg1's steady state (10^6 drops of
+// K = 4, N = 256) was 8.7 ms on the split kernel: one block per drop, per-warp partials
+// and a separate reduce for 8 elements per thread.
+constexpr int kWarpMaxN = 4096;
+constexpr int64_t kWarpMinDrops = 148 * 32;  // >= 4 warps per SM sub-partition, else the split path
+constexpr int kWarpBlock = 256;  // 8 drops per block
+
+template <int K, int KIND>
+__global__ void __launch_bounds__(kWarpBlock) gram_warp_kernel(GramParams P, int64_t n_drops, double *out) {
+  constexpr int NP = K * (K + 1) / 2;
+  static_assert(2 * NP <= 32, "gram_warp_kernel: K(K+1) <= 32");
+  const int lane = threadIdx.x & 31;
+  const int64_t drop = (int64_t)blockIdx.x * (kWarpBlock / 32) + (threadIdx.x >> 5);
+  if (drop >= n_drops) return;  // whole warp
+  double uy[K], uz[K], ux2[K], ua[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const xl::UserC u = xl::make_user(P.pos + (drop * K + k) * 3, KIND, P.sqrt_beta0);
+    ux2[k] = u.xz2;
+    uy[k] = u.y;
+    uz[k] = u.z;
+    ua[k] = u.amp;
+  }
+  double v[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = 0.0;
+  const double c4 = 4.0 * P.inv_lambda;
+  const int N = (int)P.N;
+  const double y0 = -0.5 * (double)(KIND == XLMIMO_ULA ? P.N - 1 : P.n_y - 1) * P.pitch;
+  const double z0 = -0.5 * (double)(P.n_z - 1) * P.pitch;
+  for (int m = lane; m < N; m += 32) {
+    double ey, ez = 0.0;
+    if (KIND == XLMIMO_ULA) {
+      ey = fma((double)m, P.pitch, y0);
+    } else {
+      const int q = m / (int)P.n_y, pp = m - q * (int)P.n_y;
+      ey = fma((double)pp, P.pitch, y0);
+      ez = fma((double)q, P.pitch, z0);
+    }
+    double hr[K], hi[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double dy = ey - uy[k];
+      double r2 = fma(dy, dy, ux2[k]);
+      if (KIND != XLMIMO_ULA) {
+        const double dz = ez - uz[k];
+        r2 = fma(dz, dz, r2);
+      }
+      xl::coef_fast(r2, ua[k], c4, hr[k], hi[k]);
+    }
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = i; j < K; ++j, ++q) {  // conj(h_i) h_j
+        if (i == j) {
+          v[2 * q] = fma(hr[i], hr[i], fma(hi[i], hi[i], v[2 * q]));
+        } else {
+          v[2 * q] = fma(hr[i], hr[j], fma(hi[i], hi[j], v[2 * q]));
+          v[2 * q + 1] = fma(hr[i], hi[j], fma(-hi[i], hr[j], v[2 * q + 1]));
+        }
+      }
+  }
+  // transpose-reduce: after offset o the lane keeps slots [0, o) (lane bit clear) or [o, 2o)
+  // (bit set), renumbered to [0, o); the final slot index is the lane index.
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      if (i >= 2 * NP && i + o >= 2 * NP) continue;  // both halves are padding: stays 0
+      const double send = up ? v[i] : v[i + o];
+      const double keep = up ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  if (lane < 2 * NP) {
+    const int p = lane >> 1, part = lane & 1;
+    int i = 0, rem = p;
+    while (rem >= K - i) { rem -= K - i; ++i; }
+    const int j = i + rem;
+    double *g = out + (size_t)drop * K * K * 2;
+    const double x = (part && i == j) ? 0.0 : v[0];
+    g[(i * K + j) * 2 + part] = x;
+    g[(j * K + i) * 2 + part] = part ? -x : x;
+  }
+}
+
+template <int KIND>
+void launch_warp_k(const GramParams &P, int K, int64_t n_drops, double *out, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((n_drops + kWarpBlock / 32 - 1) / (kWarpBlock / 32));
+  switch (K) {
+    case 1: gram_warp_kernel<1, KIND><<<blocks, kWarpBlock, 0, s>>>(P, n_drops, out); break;
+    case 2: gram_warp_kernel<2, KIND><<<blocks, kWarpBlock, 0, s>>>(P, n_drops, out); break;
+    case 3: gram_warp_kernel<3, KIND><<<blocks, kWarpBlock, 0, s>>>(P, n_drops, out); break;
+    case 4: gram_warp_kernel<4, KIND><<<blocks, kWarpBlock, 0, s>>>(P, n_drops, out); break;
+    case 5: gram_warp_kernel<5, KIND><<<blocks, kWarpBlock, 0, s>>>(P, n_drops, out); break;
+    default: break;
+  }
+}
+
 // ------------------------------------------------------------------ kernel M
 // FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) Gram, warp-independent, K <= 8G.
 // A warp covers 4 elements x 8 users per step: lane l computes the coefficient of
@@ -1653,8 +1761,20 @@ int64_t materialised_batch(int64_t N, int K, int64_t n_drops) {
   return b < n_drops ? b : n_drops;
 }
 
+// warp-per-drop kernel W: small single-level fp64 arrays in large batches (XLMIMO_OPT_GRAM_KERNEL
+// = 5 forces it where it applies, 1..4 keep the other kernels)
+bool use_warp_kernel(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
+  const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
+  const int64_t o = option(XLMIMO_OPT_GRAM_KERNEL);
+  const bool fits = precision == XLMIMO_FP64 && mode == XLMIMO_FUSED && n_lvl == 1 && K <= 5 && N <= kWarpMaxN;
+  if (!fits) return false;
+  if (o == 5) return true;
+  return o == 0 && n_drops >= kWarpMinDrops;
+}
+
 size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
+  if (use_warp_kernel(a, K, n_drops, n_lvl, precision, mode)) return 0;
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
   if (K > xl::kMaxK) {
@@ -1856,6 +1976,25 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   const size_t need = gram_ws_bytes(a, K, n_drops, n_lvl, precision, mode);
   if (ws_bytes < need || (need && !ws))
     return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
+  if (use_warp_kernel(a, K, n_drops, n_lvl, precision, mode)) {
+    GramParams P;
+    memset(&P, 0, sizeof(P));
+    P.pos = pos;
+    P.K = K;
+    P.kind = a.kind;
+    P.n_y = a.n_y;
+    P.n_z = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+    P.N = N;
+    P.inv_lambda = 1.0 / a.lambda;
+    P.pitch = a.pitch;
+    P.sqrt_beta0 = a.sqrt_beta0;
+    KTimer tm(s, "gram_fused_warp_fp64");
+    if (a.kind == XLMIMO_ULA) launch_warp_k<XLMIMO_ULA>(P, K, n_drops, out, s);
+    else launch_warp_k<XLMIMO_UPA>(P, K, n_drops, out, s);
+    tm.stop(s);
+    count_launch();
+    return check_launch("gram_warp_kernel");
+  }
   if (use_fused_tc(a, K, precision, n_lvl)) {
     int rc;
     {

@@ -482,3 +482,24 @@ def test_empty_batches_every_entry_point(xl, K):
     if K <= 64:
         rm, _ = xl.sum_rate_mismatched(G, Gt, [10.0])
         assert rm.shape == (0, 1)
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 256, 1, 4, 5000), ("ula", 1, 1, 3, 64), ("ula", 31, 1, 5, 64),
+                                              ("ula", 999, 1, 2, 64), ("ula", 4096, 1, 4, 40), ("ula", 256, 1, 1, 64),
+                                              ("upa", 37, 23, 4, 64), ("upa", 64, 64, 5, 16)])
+def test_gram_warp_kernel(xl, orc, kind, n_y, n_z, K, D):
+    """Kernel W (one warp per drop, small single-level arrays, K <= 5): the automatic choice at
+    >= 4736 drops (cfg1 geometry) and forced by XLMIMO_OPT_GRAM_KERNEL = 5 on smaller batches,
+    ragged N, N = 1, UPA; every entry vs the oracle at the fp64 tier, exactly Hermitian."""
+    fc = 28e9 if kind == "ula" else 100e9
+    ag, ao = _arr(xl, orc, kind, n_y, n_z, fc)
+    ug, _ = _users(xl, orc, (5.0, 50.0) if kind == "ula" else (2.0, 20.0), (-60.0, 60.0),
+                   (0.0, 0.0) if kind == "ula" else (-30.0, 30.0))
+    pos = xl.gen_drops(ug, K, D, seed=21)
+    with xl.option(xl.OPT_GRAM_KERNEL, 0 if D >= 4736 else 5):
+        G = xl.gram_exact(ag, pos).cpu().numpy()
+    idx = np.arange(D) if D <= 64 else np.r_[0:40, D - 40:D]
+    Go = orc.gram_exact(ao, pos.cpu().numpy()[idx])
+    assert normalized_err(G[idx], Go) <= 1e-9
+    assert np.array_equal(G, np.conj(np.swapaxes(G, 1, 2)))
+    assert np.all(np.imag(np.diagonal(G, axis1=1, axis2=2)) == 0)
