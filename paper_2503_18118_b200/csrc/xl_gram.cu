@@ -343,9 +343,9 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
         }
       }
     }
-    // reduce lanes of equal parity inside the warp; each warp writes its own
-    // partial (standard upper-triangle layout) -- no block barrier in the level
-    // loop, gram_reduce_kernel sums the NW partials in fixed order.
+    // reduce lanes of equal parity inside the warp, then the NW warps in fixed order through
+    // shared memory: one partial per (drop, split, level) -- the per-warp partials of round 1
+    // were 2.9x the algorithmic output bytes (ncu: 152 MB written per cfg2 launch).
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double x = acc[v];
@@ -353,21 +353,26 @@ __global__ void __launch_bounds__(NT, MINB) gram_split_kernel(GramParams P) {
       for (int o = 2; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       if (lane < 2) red[warp][lane][v] = x;
     }
-    __syncwarp();
+    __syncthreads();
     constexpr int NP = K * (K + 1) / 2;
-    double *out = P.ws + ((((size_t)drop * P.n_split + split) * P.n_lvl + l) * NW + warp) * (2 * NP);
-    for (int p = lane; p < NP; p += 32) {
+    double *out = P.ws + (((size_t)drop * P.n_split + split) * P.n_lvl + l) * (2 * NP);
+    for (int p = tid; p < NP; p += NT) {
       int i = 0, rem = p;
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
       int par, slot;
       bool cj;
       split_map<KH>(i, j, par, slot, cj);
-      const double re = red[warp][par][2 * slot], im = red[warp][par][2 * slot + 1];
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        re += red[w][par][2 * slot];
+        im += red[w][par][2 * slot + 1];
+      }
       out[2 * p] = re;
       out[2 * p + 1] = (i == j) ? 0.0 : (cj ? -im : im);
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -485,9 +490,10 @@ void launch_warp_k(const GramParams &P, int K, int64_t n_drops, double *out, cud
 // user l/4 (+ 8g for group g) at element l%4 -- exactly the m8n8k4 A-fragment
 // (row = user, k = element) and, for the same register, the B-fragment
 // (k = element, col = user).  Per step and group pair (g1 <= g2):
-//   RR += re_g1^T re_g2,  II += im_g1^T im_g2,  RI += re_g1^T im_g2  (+ IR for g1 < g2),
-// so that Re G = RR + II and Im G(i,j) = RI(i,j) - RI(j,i) (diagonal group) or
-// RI(i,j) - IR(i,j) (cross).  DMMA shares the FP64 pipe with DFMA on B200
+//   diagonal (g, g):  RR += re^T re,  II += im^T im,  RI += re^T im:
+//                     Re G = RR + II,  Im G(i,j) = RI(i,j) - RI(j,i);
+//   cross (g1 < g2):  P1 += re1^T re2,  P2 += im1^T im2,  P3 += (re1 + im1)^T (re2 - im2):
+//                     Re G = P1 + P2,  Im G = P1 - P2 - P3  (the 3M form of kernel MT2).  DMMA shares the FP64 pipe with DFMA on B200
 // (tools/pipes.cu) and computes the redundant lower halves, but leaves each
 // lane with one short coefficient chain and a handful of accumulator registers,
 // so occupancy (latency hiding) is high and no shuffles are needed.
@@ -500,8 +506,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 template <int G>
 struct MmaCfg {
   static constexpr int NDIAG = G;                 // RR, II, RI
-  static constexpr int NCROSS = G * (G - 1) / 2;  // RR, II, RI, IR
-  static constexpr int NMMA = 3 * NDIAG + 4 * NCROSS;
+  static constexpr int NCROSS = G * (G - 1) / 2;  // P1, P2, P3 (3M form, see kernel MT2)
+  static constexpr int NMMA = 3 * NDIAG + 3 * NCROSS;
 };
 
 template <int G, int NT, int MINB, int KIND>
@@ -561,12 +567,12 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
         dmma(acc[m++], hr[g1], hr[g1]);
         dmma(acc[m++], hi[g1], hi[g1]);
         dmma(acc[m++], hr[g1], hi[g1]);
+        const double sg = hr[g1] + hi[g1];
 #pragma unroll
         for (int g2 = g1 + 1; g2 < G; ++g2) {
           dmma(acc[m++], hr[g1], hr[g2]);
           dmma(acc[m++], hi[g1], hi[g2]);
-          dmma(acc[m++], hr[g1], hi[g2]);
-          dmma(acc[m++], hi[g1], hr[g2]);
+          dmma(acc[m++], sg, hr[g2] - hi[g2]);
         }
       }
     }
@@ -585,17 +591,17 @@ __global__ void __launch_bounds__(NT, MINB) gram_mma_kernel(GramParams P) {
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
       const int g1 = i >> 3, g2 = j >> 3, ii = i & 7, jj = j & 7;
-      // job index of the (g1, g2) block: diagonal blocks take 3 slots, cross blocks 4
-      int base = 0;
-      for (int g = 0; g < g1; ++g) base += 3 + 4 * (G - 1 - g);
+      // job index of the (g1, g2) block: 3 slots per block, row-major over g1 <= g2
+      const int base = 3 * (g1 * G - g1 * (g1 - 1) / 2);
       double re, im;
       if (g1 == g2) {
         re = cs[warp][base][ii][jj] + cs[warp][base + 1][ii][jj];
         im = cs[warp][base + 2][ii][jj] - cs[warp][base + 2][jj][ii];
       } else {
-        const int c = base + 3 + 4 * (g2 - g1 - 1);
-        re = cs[warp][c][ii][jj] + cs[warp][c + 1][ii][jj];
-        im = cs[warp][c + 2][ii][jj] - cs[warp][c + 3][ii][jj];
+        const int c = base + 3 * (g2 - g1);
+        const double p1 = cs[warp][c][ii][jj], p2 = cs[warp][c + 1][ii][jj];
+        re = p1 + p2;
+        im = p1 - p2 - cs[warp][c + 2][ii][jj];
       }
       out[2 * p] = re;
       out[2 * p + 1] = (i == j) ? 0.0 : im;
@@ -1703,7 +1709,7 @@ KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
   if (c.which == 1 && (env_nt == 64 || env_nt == 128 || env_nt == 192 || env_nt == 256)) c.nt = (int)env_nt;
   if (c.which == 2) c.nt = mma_nt(K <= 8 ? 1 : 2);
   const int threads = (c.which == 1 && (c.nt == 64)) ? 256 : (c.which == 1 && c.nt == 192) ? 128 : c.nt;
-  c.parts = (c.which == 1 || c.which == 2) ? threads / 32 : 1;
+  c.parts = c.which == 2 ? threads / 32 : 1;  // the split kernel reduces its warps in the block
   return c;
 }
 
