@@ -844,6 +844,15 @@ template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };  
 template <> struct Mt2Cfg<6> { static constexpr int JPW = 3, SG = 2, S = 8; };   // 7 stars, NW 14
 template <> struct Mt2Cfg<7> { static constexpr int JPW = 4, SG = 2, S = 8; };   // 7 stars, NW 14
 template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 9; };   // 12 stars, NW 12, 12 rows/warp
+// 64 < K <= 128 (the paper's K = 100 of E1/E2 and Fig. K_vs_E): one star per
+// warp, stars of a regular or near-regular tournament (warps not a multiple of 4 except G = 15)
+template <> struct Mt2Cfg<9> { static constexpr int JPW = 5, SG = 1, S = 4; };   // 9 stars
+template <> struct Mt2Cfg<10> { static constexpr int JPW = 5, SG = 1, S = 4; };  // 11 stars
+template <> struct Mt2Cfg<11> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 11 stars
+template <> struct Mt2Cfg<12> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 13 stars
+template <> struct Mt2Cfg<13> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 13 stars
+template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 15 stars
+template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
 
 template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::S; NBUF tile buffers
 struct Mt2 {
@@ -859,12 +868,13 @@ struct Mt2 {
 };
 
 // Star plan of the MT2 kernel: star s (warp's job group) = centre cen[s] and partners
-// par[s][k]; blk[g1 * 8 + g2] (g1 <= g2) = 2 * (job s * JPW + k) + (1 if the star holds
+// par[s][k]; blk[g1 * 16 + g2] (g1 <= g2) = 2 * (job s * JPW + k) + (1 if the star holds
 // the block as (g2, g1), i.e. transposed).
+constexpr int kMt2MaxG = 16;
 struct StarPlan {
-  int8_t cen[16];
-  int8_t par[16][4];
-  int16_t blk[64];
+  int8_t cen[32];
+  int8_t par[32][8];
+  int16_t blk[kMt2MaxG * kMt2MaxG];
 };
 
 struct FastDiv {  // q = (umulhi(m, t) + t) >> sh == t / d for 0 <= t < 2^31
@@ -1076,7 +1086,7 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
       int i = 0, rem = p;
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
-      const int bq = plan.blk[(i >> 3) * 8 + (j >> 3)];
+      const int bq = plan.blk[(i >> 3) * kMt2MaxG + (j >> 3)];
       const bool tr = bq & 1;  // block held as (g2, g1): read (j, i) and conjugate
       const int e = tr ? (j & 7) * 8 + (i & 7) : (i & 7) * 8 + (j & 7);
       const double *st = dsm + (size_t)(bq >> 1) * 3 * SG * 64 + e;
@@ -1100,10 +1110,10 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
 // centred-block count (+1 for its own diagonal block) is a multiple of JPW, by depth-first
 // search over the pairs; then cut each group's list (diagonal first) into stars.
 bool star_plan(int G, int JPW, StarPlan &pl) {
-  int pa[28], pb[28], n = 0;
+  int pa[kMt2MaxG * (kMt2MaxG - 1) / 2], pb[kMt2MaxG * (kMt2MaxG - 1) / 2], n = 0;
   for (int a = 0; a < G; ++a)
     for (int b = a + 1; b < G; ++b) { pa[n] = a; pb[n] = b; ++n; }
-  int out[8] = {0}, left[8], to[28];
+  int out[kMt2MaxG] = {0}, left[kMt2MaxG], to[kMt2MaxG * (kMt2MaxG - 1) / 2];
   for (int v = 0; v < G; ++v) left[v] = G - 1;
   auto can = [&](int v) {  // some multiple of JPW is still reachable for v
     for (int d = out[v]; d <= out[v] + left[v]; ++d)
@@ -1133,7 +1143,7 @@ bool star_plan(int G, int JPW, StarPlan &pl) {
     if ((out[v] + 1) % JPW) return false;
   int ns = 0;
   for (int v = 0; v < G; ++v) {
-    int list[8], m = 0;
+    int list[kMt2MaxG], m = 0;
     list[m++] = v;
     for (int e = 0; e < n; ++e)
       if ((to[e] ? pb[e] : pa[e]) == v) list[m++] = to[e] ? pa[e] : pb[e];
@@ -1143,8 +1153,8 @@ bool star_plan(int G, int JPW, StarPlan &pl) {
         const int p = list[q + t];
         pl.par[ns][t] = (int8_t)p;
         const int job = ns * JPW + t;
-        if (v <= p) pl.blk[v * 8 + p] = (int16_t)(2 * job);
-        else pl.blk[p * 8 + v] = (int16_t)(2 * job + 1);
+        if (v <= p) pl.blk[v * kMt2MaxG + p] = (int16_t)(2 * job);
+        else pl.blk[p * kMt2MaxG + v] = (int16_t)(2 * job + 1);
       }
     }
   }
@@ -1171,8 +1181,11 @@ int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int env = (int)xlh::option(XLMIMO_OPT_MT2_BUFFERS);
   const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
-  if (nbuf == 2)
-    return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
+  if constexpr (G <= 8) {
+    if (nbuf == 2)
+      return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
+  }
+  // K > 64: the ring only
   return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
 }
 
@@ -1778,12 +1791,22 @@ bool use_warp_kernel(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
   return o == 0 && n_drops >= kWarpMinDrops;
 }
 
+// fp64 fused Gram for 64 < K <= 128 on the MT2 kernel (3M DMMA stars) unless
+// XLMIMO_OPT_LARGE_K picks the block-pair (1) or SYRK (2) kernel
+constexpr int kMt2MaxK = 120;  // G <= 15 (G = 16 would need 8-block stars: register spills)
+bool use_mt2_large(const ArrayP &a, int K, int precision, int mode) {
+  const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
+  const int64_t o = option(XLMIMO_OPT_LARGE_K), gk = option(XLMIMO_OPT_GRAM_KERNEL);
+  return K > xl::kMaxK && K <= kMt2MaxK && precision == XLMIMO_FP64 && mode == XLMIMO_FUSED &&
+         N < ((int64_t)1 << 31) && o != 1 && o != 2 && gk != 3 && gk != 4;
+}
+
 size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int precision, int mode) {
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   if (use_warp_kernel(a, K, n_drops, n_lvl, precision, mode)) return 0;
   const int n_split = choose_split(n_drops, N);
   const size_t np = (size_t)K * (K + 1) / 2;
-  if (K > xl::kMaxK) {
+  if (K > xl::kMaxK && !use_mt2_large(a, K, precision, mode)) {
     if (precision == XLMIMO_FP32 && N >= kTcMinN) {  // tcgen05 block pairs (+ H chunks when streamed)
       const size_t part = ((size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double) + 255) / 256 * 256;
       const bool stream = use_stream_pair(K) || mode == XLMIMO_MATERIALIZED;
@@ -1931,7 +1954,7 @@ int launch_gram_blk(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
 int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops, const int64_t *lvl_end,
                       int n_lvl, int precision, int mode, double *out, void *ws, size_t ws_bytes,
                       cudaStream_t s) {
-  if (K > xl::kMaxK) {
+  if (K > xl::kMaxK && !use_mt2_large(a, K, precision, mode)) {
     // materialised for K > 64 = the TMA-fed pair stream over complex64 (TF32) chunks of H
     if (mode == XLMIMO_MATERIALIZED && precision != XLMIMO_FP32)
       return set_error(XLMIMO_EUNSUPPORTED, "gram_exact: XLMIMO_MATERIALIZED is complex64 (XLMIMO_FP32) only");
@@ -2061,7 +2084,14 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       case 5: rc = launch_mt2<5>(P, n_blocks, s); break;
       case 6: rc = launch_mt2<6>(P, n_blocks, s); break;
       case 7: rc = launch_mt2<7>(P, n_blocks, s); break;
-      default: rc = launch_mt2<8>(P, n_blocks, s); break;
+      case 8: rc = launch_mt2<8>(P, n_blocks, s); break;
+      case 9: rc = launch_mt2<9>(P, n_blocks, s); break;
+      case 10: rc = launch_mt2<10>(P, n_blocks, s); break;
+      case 11: rc = launch_mt2<11>(P, n_blocks, s); break;
+      case 12: rc = launch_mt2<12>(P, n_blocks, s); break;
+      case 13: rc = launch_mt2<13>(P, n_blocks, s); break;
+      case 14: rc = launch_mt2<14>(P, n_blocks, s); break;
+      default: rc = launch_mt2<15>(P, n_blocks, s); break;
     }
     if (rc) return rc;
   } else if (kc.which == 2) {

@@ -27,10 +27,11 @@ def xl():
 @pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 700, 1, 65, 3), ("ula", 1001, 1, 100, 2),
                                               ("ula", 640, 1, 128, 2), ("ula", 333, 1, 129, 2),
                                               ("ula", 500, 1, 200, 1), ("upa", 24, 20, 80, 2),
-                                              ("ula", 50, 1, 100, 2)])
+                                              ("ula", 50, 1, 100, 2), ("ula", 2000, 1, 113, 2),
+                                              ("ula", 999, 1, 120, 2), ("upa", 32, 16, 104, 2)])
 def test_gram_large_k_parity(xl, orc, kind, n_y, n_z, K, D):
-    """Block pairs of 64 users: full (K = 128), ragged (65, 100, 129, 200), UPA, and
-    N < K (rank-deficient G, N = 50)."""
+    """64 < K <= 120 on the MT2 3M-DMMA stars (65, 80 UPA, 100, 104 UPA, 113, 120), block
+    pairs of 64 users above (K = 128, ragged 129, 200), and N < K (rank-deficient G, N = 50)."""
     fc = 100e9
     if kind == "ula":
         a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
@@ -226,7 +227,7 @@ def test_exact_sweep_large_k_nested_levels(xl, orc):
     assert np.array_equal(res["n_valid"], nv)
 
 
-@pytest.mark.parametrize("path,K", [(1, 200), (2, 100), (2, 65)])
+@pytest.mark.parametrize("path,K", [(1, 200), (2, 100), (2, 65), (1, 100), (1, 72)])
 def test_large_k_paths_outside_their_default_range(xl, orc, path, K):
     """XLMIMO_OPT_LARGE_K forces the block-pair (1) or the SYRK (2) kernel; each must match
     the oracle outside the K range the default selection gives it."""
