@@ -210,8 +210,9 @@ XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drop
  *            PAPER.md:228) and M_sat = ceil((E[y_up]-E[y_down]) / pitch) (R15),
  *   per_drop (dev [n_drops][n_n][n_snr][n_recv] or NULL).
  * array->n_y is ignored (the grid is n_list).  Synchronises `stream` before return.
- * K <= 1024; for K > 64 the exact Gram is fp64 (EUNSUPPORTED otherwise) -- the
- * paper's K = 100 curves.
+ * K <= 1024 -- the paper's K = 100 curves.  For K > 64 an fp32 exact sweep
+ * runs the tcgen05 Gram once per N (those kernels have no nested levels): the same
+ * Grams, O(sum N) instead of O(max N) work.
  * EINVAL also for n_list not ascending / mixed parity, t not in (0,1). */
 XLMIMO_API size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
                                          int32_t K, int64_t n_drops, int32_t n_snr, uint32_t receivers,

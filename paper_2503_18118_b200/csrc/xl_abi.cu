@@ -73,8 +73,14 @@ struct Carve {
 };
 
 // Layout of the saturation-sweep workspace (shared by the size query and the call).
+// fp32 exact sweeps for K > 64 run the tcgen05 block-pair Gram once per N (its kernels have
+// no nested levels): Gram of the n-th centred array into `g1`, copied into level n of `grams`.
+bool sweep_per_level(int K, int gram_kind, int precision) {
+  return K > xl::kMaxK && gram_kind == XLMIMO_GRAM_EXACT && precision == XLMIMO_FP32;
+}
+
 struct SweepWs {
-  double *pos, *grams, *rates, *erg, *ergv, *sat, *satp;
+  double *pos, *grams, *g1, *rates, *erg, *ergv, *sat, *satp;
   int64_t *nval;
   uint32_t *flags;
   void *gws, *rws;
@@ -89,6 +95,8 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
   const int R = n_recv_of(receivers);
   w.pos = (double *)c.take((size_t)D * K * 3 * sizeof(double));
   w.grams = (double *)c.take((size_t)D * n_n * K * K * 2 * sizeof(double));
+  const bool per_level = sweep_per_level(K, gram_kind, precision) && n_n > 1;
+  w.g1 = (double *)c.take(per_level ? (size_t)D * K * K * 2 * sizeof(double) : 0);
   w.rates = (double *)c.take((size_t)D * n_n * n_snr * R * sizeof(double));
   w.flags = (uint32_t *)c.take((size_t)D * n_n * sizeof(uint32_t));
   w.erg = (double *)c.take((size_t)n_n * n_snr * R * sizeof(double));
@@ -100,7 +108,15 @@ SweepWs sweep_layout(void *ws, const xlh::ArrayP &ap, const int64_t *n_list, int
   if (gram_kind == XLMIMO_GRAM_EXACT) {
     xlh::ArrayP big = ap;
     big.n_y = n_list[n_n - 1];
-    w.gws_bytes = xlh::gram_ws_bytes(big, K, D, n_n, precision, XLMIMO_FUSED);
+    if (sweep_per_level(K, gram_kind, precision)) {  // the largest single-level workspace
+      for (int l = 0; l < n_n; ++l) {
+        big.n_y = n_list[l];
+        const size_t b = xlh::gram_ws_bytes(big, K, D, 1, precision, XLMIMO_FUSED);
+        if (b > w.gws_bytes) w.gws_bytes = b;
+      }
+    } else {
+      w.gws_bytes = xlh::gram_ws_bytes(big, K, D, n_n, precision, XLMIMO_FUSED);
+    }
   }
   w.gws = c.take(w.gws_bytes);
   // K > 64: receivers through the large-K path (CAP by Cholesky slots, MRC)
@@ -122,8 +138,6 @@ int validate_sweep(const xlmimo_array_t *array, const int64_t *n_list, int n_n, 
   }
   if (K < 1 || K > xl::kMaxKLarge)
     return xlh::set_error(K < 1 ? XLMIMO_EINVAL : XLMIMO_EUNSUPPORTED, "sweep: K=%d", K);
-  if (K > xl::kMaxK && gram_kind == XLMIMO_GRAM_EXACT && precision != XLMIMO_FP64)
-    return xlh::set_error(XLMIMO_EUNSUPPORTED, "sweep: K=%d > %d is fp64 only", K, xl::kMaxK);
   if (n_drops < 1) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_drops < 1");
   if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr) return xlh::set_error(XLMIMO_EINVAL, "sweep: n_snr out of [1,16]");
   if ((receivers & 15u) == 0 || (receivers & ~15u)) return xlh::set_error(XLMIMO_EINVAL, "sweep: receivers");
@@ -156,7 +170,21 @@ int run_sweep(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, c
     if ((rc = xlh::launch_gen_drops(*users, K, n_drops, seed, 0, w.pos, s))) return rc;
     P = w.pos;
   }
-  if (gram_kind == XLMIMO_GRAM_EXACT) {
+  if (gram_kind == XLMIMO_GRAM_EXACT && sweep_per_level(K, gram_kind, precision)) {
+    xlh::ArrayP al = ap;
+    const size_t gb = (size_t)K * K * 2 * sizeof(double);
+    rc = XLMIMO_OK;
+    for (int l = 0; l < n_n && !rc; ++l) {
+      al.n_y = n_list[l];
+      double *dst = n_n > 1 ? w.g1 : w.grams;
+      rc = xlh::launch_gram_exact(al, P, K, n_drops, &n_list[l], 1, precision, XLMIMO_FUSED, dst, w.gws, w.gws_bytes,
+                                  s);
+      if (!rc && n_n > 1 &&
+          cudaMemcpy2DAsync((char *)w.grams + l * gb, n_n * gb, w.g1, gb, gb, (size_t)n_drops,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        rc = xlh::check_launch("sweep: level copy");
+    }
+  } else if (gram_kind == XLMIMO_GRAM_EXACT) {
     xlh::ArrayP big = ap;
     big.n_y = n_list[n_n - 1];
     rc = xlh::launch_gram_exact(big, P, K, n_drops, n_list, n_n, precision, XLMIMO_FUSED, w.grams, w.gws,

@@ -38,7 +38,8 @@ constexpr int kChunk = 8192;           // elements per work item (one fp64 parti
 // <= ~3e-6); the epilogue folds the sub-chunk sums into a running fp32 sum kept in a third
 // TMEM region (drain_subchunk) and writes the item's fp64 partial after the last one.
 constexpr int kSubStages = 16;
-constexpr int kFSubStages = 8;  // fused kernel: fp16 stages hold 64 elements, so 8 stages = 32 MMAs x 16
+constexpr int kFSubStages = 8;
+constexpr int kPSubStages = 8;  // pair kernel: 8 stages x 4 MMAs per TMEM sub-chunk (K = 100 rates: -4e-4 bit at 16)  // fused kernel: fp16 stages hold 64 elements, so 8 stages = 32 MMAs x 16
 constexpr int kThreads = 256;
 
 // element blocks stacked per stage in the 128 MMA rows: 2K <= 32 -> 4 blocks, <= 64 -> 2, else 1
@@ -194,7 +195,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 // partial `out` (packed upper triangle).  16-column slabs keep the live set at 32 floats.
 __device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_col, uint32_t run_col, int R, int K,
                                                int i, int plane, bool first, bool last, double *out,
-                                               double post = 1.0) {
+                                               double post = 1.0, int j0 = 0) {
   for (int cb = 0; cb < (R + 15) / 16; ++cb) {
     float v[16];
     tmem_ld16(lane_base + acc_col + (uint32_t)(16 * cb), v);
@@ -214,12 +215,12 @@ __device__ __forceinline__ void drain_subchunk(uint32_t lane_base, uint32_t acc_
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const int jj = plane * 4 + h;
-      const int j = 8 * cb + jj;
+      const int j = j0 + 8 * cb + jj;
       float rr, rr2, ri, ir;  // R(2i,2j), R(2i+1,2j+1), R(2i,2j+1), R(2i+1,2j)
       if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
       else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
       if (i < K && j < K && j >= i) {
-        const int p = i * K - i * (i - 1) / 2 + (j - i);
+        const int64_t p = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
         out[2 * p] = ((double)rr + (double)rr2) * post;
         out[2 * p + 1] = (i == j) ? 0.0 : ((double)ri - (double)ir) * post;
       }
@@ -840,6 +841,13 @@ struct FusedPairParams {
   int64_t n_drops;
 };
 
+// stages (32 elements each) of pair-kernel chunk c (kPChunk elements, fewer in the last)
+__device__ __forceinline__ int pair_item_stages(int64_t N, int c) {
+  const int64_t rem = N - (int64_t)c * kPChunk;
+  const int64_t ns = (rem + kBoxK - 1) / kBoxK;
+  return ns < kPChunk / kBoxK ? (int)ns : kPChunk / kBoxK;
+}
+
 __device__ __forceinline__ void pair_of(int pair, int nb, int &bi, int &bj) {
   bi = 0;
   while (pair >= nb - bi) { pair -= nb - bi; ++bi; }
@@ -876,7 +884,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == kPMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
-                 "r"(256)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -948,39 +956,44 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
         if (lane == 0) mbar_arrive(&full[slot]);
       }
     }
-  } else if (warp == kPMmaWarp) {  // ---------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = tf32_idesc(kRows, kRows);
-      // (the original kernel's 12 slots over 8 groups satisfy the same groups <= slots rule)
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
-        const int64_t d = it / per_drop;
-        const int rem2 = (int)(it - d * per_drop);
-        const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
-        int bi, bj;
-        pair_of(pair, P.nb, bi, bj);
-        const bool diag = bi == bj;
-        const int64_t x0 = (int64_t)c * kPChunk;
+  } else if (warp == kPMmaWarp) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+    const uint32_t idesc = tf32_idesc(kRows, kRows);
+    // (the original kernel's 12 slots over 8 groups satisfy the same groups <= slots rule)
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t d = it / per_drop;
+      const int rem2 = (int)(it - d * per_drop);
+      const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
+      int bi, bj;
+      pair_of(pair, P.nb, bi, bj);
+      const bool diag = bi == bj;
+      const int ns = pair_item_stages(P.N, c);
+      for (int s0 = 0; s0 < ns; s0 += kPSubStages, ++local) {  // one TMEM sub-chunk (accumulation bias)
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tmem_d = tmem + (uint32_t)(acc * kRows);
-        for (int kb = 0; kb < kPChunk / kSpb; ++kb) {
-          if (x0 + (int64_t)kb * kSpb >= P.N) break;
+        const int s1 = s0 + kPSubStages < ns ? s0 + kPSubStages : ns;
+        for (int kb = s0; kb < s1; ++kb) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(stages + stage * kPSlotBytes);
           const uint32_t sb = diag ? sa : sa + kStageBytes;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kBoxK / 8; ++kk)
-            mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
+            for (int kk = 0; kk < kBoxK / 8; ++kk)
+              mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc,
+                       (kb > s0 || kk > 0) ? 1u : 0u);
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == kPSlots) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if (elect_one()) mma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else if (warp >= kPEpiWarp0) {  // ---------------- epilogue, warps kPEpiWarp0..+3 = TMEM lane quadrants
@@ -989,48 +1002,31 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
     const int il = row >> 1, plane = row & 1;
     const int64_t NP = (int64_t)K * (K + 1) / 2;
     int local = 0;
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / per_drop;
       const int rem2 = (int)(it - d * per_drop);
       const int pair = rem2 / P.n_chunks, c = rem2 - pair * P.n_chunks;
       int bi, bj;
       pair_of(pair, P.nb, bi, bj);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       double *out = P.ws + ((size_t)d * P.n_chunks + c) * (size_t)(2 * NP);
-      const int i = bi * kPUsers + il;
-      for (int cb = 0; cb < kRows / 32; ++cb) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kRows + 32 * cb), v);
-        float x[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, v[e], 1);
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const int jj = plane * 8 + h;
-          const int jl = 16 * cb + jj;
-          const int j = bj * kPUsers + jl;
-          float rr, rr2, ri, ir;
-          if (plane == 0) { rr = v[2 * jj]; ri = v[2 * jj + 1]; ir = x[2 * jj]; rr2 = x[2 * jj + 1]; }
-          else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
-          if (i < K && j < K && j >= i) {
-            const int64_t pp = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
-            out[2 * pp] = (double)rr + (double)rr2;
-            out[2 * pp + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
-          }
-        }
+      const int ns = pair_item_stages(P.N, c);
+      for (int s0 = 0; s0 < ns; s0 += kPSubStages, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tfull[acc], acc_phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * kRows), (uint32_t)(2 * kRows), kRows, K,
+                       bi * kPUsers + il, plane, s0 == 0, s0 + kPSubStages >= ns, out, 1.0, bj * kPUsers);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
   if (warp == kPMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 

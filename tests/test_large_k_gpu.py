@@ -227,6 +227,29 @@ def test_exact_sweep_large_k_nested_levels(xl, orc):
     assert np.array_equal(res["n_valid"], nv)
 
 
+def test_fp32_sweep_large_k_rates(xl, orc):
+    """fp32 exact sweep at E1's K = 100 (the tcgen05 block-pair Gram run once per
+    N, copied into the level slots) against the oracle's fp64 rates: the ergodic means (CAP,
+    ZF, MMSE, MRC) within the fp32 tier, 1e-3 bit; per drop within 5e-3 -- a sum over 100
+    users of per-user errors that the Gram's conditioning amplifies from the TF32 operand
+    rounding (normalised Gram error ~3e-5 at N = 1024, inside the 1e-4 Gram tier); counts
+    identical.  Before the pair kernel's TMEM sub-chunk folding (512 truncating MMA
+    accumulations per partial) the K = 100 rates carried a -4e-3 bit bias."""
+    K, D = 100, 6
+    nl = [1024, 2048, 6000, 12000]
+    a, ao = xl.Array.ula(max(nl), 100e9), orc.array("ula", n_y=max(nl), fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=9)
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    res = xl.saturation_sweep(a, nl, K, D, [0.0, 10.0], rec, pos=pos, precision=xl.FP32, per_drop=True)
+    erg, nv, _, pd = orc.saturation_sweep(ao, nl, pos.cpu().numpy(), [0.0, 10.0], rec, per_drop=True)
+    g = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(pd))
+    ok = ~np.isnan(pd)
+    assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= 5e-3
+    assert np.array_equal(res["n_valid"], nv)
+    assert np.nanmax(np.abs(res["ergodic"] - erg)) <= 1e-3
+
+
 @pytest.mark.parametrize("path,K", [(1, 200), (2, 100), (2, 65), (1, 100), (1, 72)])
 def test_large_k_paths_outside_their_default_range(xl, orc, path, K):
     """XLMIMO_OPT_LARGE_K forces the block-pair (1) or the SYRK (2) kernel; each must match
