@@ -58,6 +58,7 @@ FP64_OPS_PER_COEF = 31
 MUFU_PER_COEF_FP32 = 2   # the fused fp32 generator: MUFU sin + cos per coefficient
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6545.3   # B200_PROFILING.md / MEASURED_PEAKS.json copy bandwidth
+READ_PEAK_GBS = 7140.0      # read-only stream, tools/peaks.cu (profiles/r01/microbench_peaks.json)
 
 
 def parse():
@@ -142,10 +143,11 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kname: str, launch: str):
+def ncu_traffic(kname: str, launch: str, drops: float | None = None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of a kernel from the newest
     committed `ncu --set full` capture of the same launch (profiles/r*/ncu_traffic_*.json),
-    or None."""
+    or None.  With `drops`, the captured launch's bytes are scaled to that many drops (the
+    materialised stream's launches hold 16 drops but the last of a batch fewer)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_*.json")))
     for f in reversed(files):
@@ -155,7 +157,8 @@ def ncu_traffic(kname: str, launch: str):
             continue
         for e in (d if isinstance(d, list) else [d]):
             if e.get("kernel") == kname and e.get("launch_key") == launch:
-                return int(e["dram_bytes_read"]) + int(e["dram_bytes_write"])
+                b = int(e["dram_bytes_read"]) + int(e["dram_bytes_write"])
+                return int(b * drops / e["drops"]) if drops and e.get("drops") else b
     return None
 
 
@@ -463,7 +466,10 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
         bytes_launch = 8 * w.N * w.K * drops_per_launch
         ach = bytes_launch / (per_launch * 1e-3) / 1e9
         extra["roofline"] = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
-                             "traffic": ncu_traffic("gram_stream_tc_tf32", f"cfg5 mat32 B={int(drops_per_launch)}"),
+                             "traffic": ncu_traffic("gram_stream_tc_tf32", "cfg5 mat32", drops_per_launch),
+                             "frac_of_read_peak": ach / READ_PEAK_GBS,
+                             "read_peak_source": "profiles/r01/microbench_peaks.json (read-only stream, 7.14 TB/s; "
+                                                 "the copy figure above counts read + write)",
                              "kernel": "gram_stream_tc_tf32", "launch_ms": per_launch, "launches": st[0],
                              "algorithmic_bytes_per_launch": bytes_launch,
                              "work_model": "8 N K bytes per drop (complex64 H read once) x drops per launch",
@@ -473,7 +479,8 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
         bytes_launch = 8 * w.N * w.K * D * K_ / wr[0]
         extra["writer"] = {"kernel": "h_materialise (K4a)", "launch_ms": per_launch,
                            "gbs": bytes_launch / (per_launch * 1e-3) / 1e9,
-                           "frac_of_hbm_peak": bytes_launch / (per_launch * 1e-3) / 1e9 / hbm_gbs}
+                           "frac_of_hbm_peak": bytes_launch / (per_launch * 1e-3) / 1e9 / hbm_gbs,
+                           "traffic": ncu_traffic("h_materialise", "cfg5 mat32 writer", D * K_ / wr[0])}
     sub["cfg5_materialised"] = rec(w, D, ms, kt, nl_, extra)
     del ws
 
@@ -520,10 +527,12 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
         xl.sum_rate(g, list(w.snr_db), allr)
         return xl.sum_rate(gt, list(w.snr_db), allr, flags=fl)
     ms, kt, nl_, _ = timed(s_c1, K_, W_)
+    roof = fp64_roof(kt, ("gram_fused_split_fp64", "gram_fused_dmma_fp64", "gram_fused_small_fp64",
+                          "gram_fused_warp_fp64"), D, w.N, w.K, clk)
+    if roof:
+        roof["traffic"] = ncu_traffic(roof["kernel"], f"cfg1 steady D={D}")
     sub["cfg1_steady"] = rec(w, D, ms, kt, nl_, {
-        "step": "10^6 drops: drops + fused fp64 Gram + closed-form Gram + CAP/ZF/MMSE/MRC on both",
-        "roofline": fp64_roof(kt, ("gram_fused_split_fp64", "gram_fused_dmma_fp64", "gram_fused_small_fp64",
-                                   "gram_fused_warp_fp64"), D, w.N, w.K, clk)})
+        "step": "10^6 drops: drops + fused fp64 Gram + closed-form Gram + CAP/ZF/MMSE/MRC on both", "roofline": roof})
     del pos, G, ws
 
     # ---- cfg2: the saturation sweep (round 1's headline)
