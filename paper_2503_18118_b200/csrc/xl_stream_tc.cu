@@ -574,25 +574,27 @@ constexpr int kGenThreads = 32 * kGenWarps;
 // Fused K <= 64 kernel: kFGroups groups of kFGenWarps warps; group g makes stages
 // k = g (mod kFGroups) into ring slot k % kFStages.  The MMA consumes stages in order, so a
 // group's next stage (k + groups) waits for slot k + groups - slots to be consumed; with
-// slots >= 2 groups + 2 that stage belongs to an earlier round and the groups never wait
-// on each other (10 groups x 2 warps over 12 slots left the generators ~45 % of their time
-// in that wait: each round the later groups waited for the earlier ones' stages).
+// parity waits are exact while groups <= slots.  Measured (148 cfg5 drops / 10^4 cfg3 /
+// 10^3 cfg4, ms): 12 x 2 warps, 12 slots 9.82 / 2.78 / 2.35; 10 x 2, 12 slots 10.06 / 2.81 /
+// 2.44; 5 x 4, 13 slots 10.69 / 2.96; 8 x 3 10.55; 4 x 6 12.82.
 #ifndef XL_FGEN_WARPS
-#define XL_FGEN_WARPS 4
+#define XL_FGEN_WARPS 2
 #endif
 #ifndef XL_FGEN_GROUPS
-#define XL_FGEN_GROUPS 5
+#define XL_FGEN_GROUPS 12
 #endif
 #ifndef XL_FSTAGES
-#define XL_FSTAGES 13
+#define XL_FSTAGES 12
 #endif
 constexpr int kFGenWarps = XL_FGEN_WARPS;
 constexpr int kFGroups = XL_FGEN_GROUPS;
 constexpr int kFStages = XL_FSTAGES;
 constexpr int kFGenThreads = 32 * kFGenWarps;
-constexpr int kEpiWarp0 = kFGenWarps * kFGroups;   // 20: warps 20..23 = TMEM lane quadrants 0..3
-constexpr int kMmaWarp = kEpiWarp0 + 4;            // 24
-constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 800
+constexpr int kEpiWarp0 = kFGenWarps * kFGroups;   // 24: warps 24..27 = TMEM lane quadrants 0..3
+constexpr int kMmaWarp = kEpiWarp0 + 4;            // 28
+constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 928
+static_assert(kEpiWarp0 % 4 == 0, "epilogue warp q must sit in TMEM lane quadrant q (warp % 4)");
+static_assert(kFGroups <= kFStages, "a generator group may not lap a ring slot (parity waits)");
 
 constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one swizzle atom)
 
