@@ -493,17 +493,17 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
         g = xl.gram_exact(arr, pos, precision=xl.FP32, out=G, ws=ws)
         return xl.sum_rate(g, list(w.snr_db), w.receivers)
     ms, kt, nl_, _ = timed(s_f32, K_, W_)
-    extra = {"precision": "fp32 (TF32 tensor cores, fp64 distance/phase anchor, fp64 across chunks)"}
-    tc = kt.get("gram_fused_tc_tf32")
+    extra = {"precision": "fp32 tier (fp32 phasors from fp64 anchors, fp16 operands = 11 significant bits like TF32, tcgen05 kind::f16, fp32 accumulation, fp64 across chunks)"}
+    tc = kt.get("gram_fused_tc_f16")
     if tc:
         per_launch = tc[1] / tc[0]
         coefs = w.N * w.K * D * K_ / tc[0]
         ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
         peak = 148 * 16 * clk * 1e6 / 1e12
         extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s", "frac": ach / peak,
-                             "kernel": "gram_fused_tc_tf32", "launch_ms": per_launch, "launches": tc[0],
+                             "kernel": "gram_fused_tc_f16", "launch_ms": per_launch, "launches": tc[0],
                              "coefficients_per_clk_per_sm": coefs / (per_launch * 1e-3) / (clk * 1e6) / 148,
-                             "traffic": ncu_traffic("gram_fused_tc_tf32", f"cfg5 fp32 D={int(D * K_ / tc[0])}"),
+                             "traffic": ncu_traffic("gram_fused_tc_f16", f"cfg5 fp32 D={int(D * K_ / tc[0])}"),
                              "work_model": "2 MUFU (sin, cos) per element-user coefficient; peak = 148 SM x 16 MUFU "
                                            "lanes/clk x sm_max clock", "share_of_step": tc[1] / ms}
     sub["cfg5_fused_fp32"] = rec(w, D, ms, kt, nl_, extra)
@@ -584,14 +584,14 @@ def run_subrecords(xl, torch, np, dev, timed, fp64_roof, args, hbm_gbs, hbm_src,
                 extra["roofline"] = fp64_roof(kt, ("gram_fused_dmma_fp64", "gram_fused_dmma_tiled_fp64"), D, w.N,
                                               w.K, clk)
             else:
-                tc = kt.get("gram_fused_tc_tf32")
+                tc = kt.get("gram_fused_tc_f16")
                 if tc:
                     per_launch = tc[1] / tc[0]
                     coefs = w.N * w.K * D * K_ / tc[0]
                     ach = MUFU_PER_COEF_FP32 * coefs / (per_launch * 1e-3) / 1e12
                     peak = 148 * 16 * clk * 1e6 / 1e12
                     extra["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "MUFU Top/s",
-                                         "frac": ach / peak, "kernel": "gram_fused_tc_tf32", "launch_ms": per_launch,
+                                         "frac": ach / peak, "kernel": "gram_fused_tc_f16", "launch_ms": per_launch,
                                          "coefficients_per_clk_per_sm": coefs / (per_launch * 1e-3) / (clk * 1e6) / 148}
             sub[f"cfg{c}_{tag}"] = rec(w, D, ms, kt, nl_, extra)
             del ws

@@ -2027,7 +2027,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
   if (use_fused_tc(a, K, precision, n_lvl)) {
     int rc;
     {
-      KTimer tm(s, "gram_fused_tc_tf32");
+      KTimer tm(s, "gram_fused_tc_f16");
       rc = launch_fused_tc(a, pos, K, n_drops, N, (double *)ws, s);
       tm.stop(s);
       count_launch();
