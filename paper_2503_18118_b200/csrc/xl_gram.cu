@@ -1014,7 +1014,11 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
             r2 = fma(dz, dz, r2);
           }
           double hr, hi;
+#ifdef XL_EXP_MT2_NOGEN  // tuning experiment: the DMMA-side rate (results invalid)
+          hr = r2 * 1e-9; hi = uc.w;
+#else
           xl::coef_fast(r2, valid ? uc.w : 0.0, c4, hr, hi);
+#endif
           gre[row * 32 + lane] = hr;
           gim[row * 32 + lane] = hi;
         }
