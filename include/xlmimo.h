@@ -179,15 +179,18 @@ XLMIMO_API int xlmimo_sum_rate_ws(const double *gram, int32_t K, int64_t n_drops
  *   bounds (dev [n_drops][n_snr][3]) = { log2 U, log2 det(I + rho G), log2 L } with
  *            U = prod(1 + a_i) (Hadamard) and L = det(R) U
  *            (Schur-Horn), so log2 U >= C >= log2 L;
- *   eig    (dev [n_drops][K] or NULL, K <= 64) = eigenvalues of R ascending (cyclic
- *            Jacobi), whose mean log2 is -gap;
+ *   eig    (dev [n_drops][K] or NULL) = eigenvalues of R ascending, whose mean log2 is
+ *            -gap: parallel cyclic Jacobi for K <= 64; for K > 64 Householder reduction to
+ *            a real tridiagonal and bisection on Sturm counts (Fig. K_vs_E's spectrum at
+ *            K = 1000);
  *   flags  (dev [n_drops] or NULL, SET): G_NOT_PD (R not PD: log2 det R, gap, log2 L
  *            NaN), A_NOT_PD (I + rho G not PD for some SNR: that C NaN), MRC_UNDEF
  *            (some G_ii <= 0: R undefined, all NaN), NONFINITE (all NaN).
  * gram dev [n_drops][K][K][2]; snr_db host [n_snr] (<= 16).  K <= 1024; K > 64 needs
- * the workspace of the query (tiled Cholesky slots), K <= 64 none.
- * EUNSUPPORTED: K > 1024, or eig with K > 64.  EWORKSPACE: ws_bytes below the query. */
-XLMIMO_API size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr);
+ * the workspace of the query (tiled Cholesky slots, plus with_eig != 0 one K x K complex
+ * slot per resident CTA for the eigenvalues), K <= 64 none.
+ * EUNSUPPORTED: K > 1024.  EWORKSPACE: ws_bytes below the query. */
+XLMIMO_API size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr, int32_t with_eig);
 XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const double *snr_db,
                                    int32_t n_snr, double *rstat, double *bounds, double *eig, uint32_t *flags,
                                    void *ws, size_t ws_bytes, void *stream);

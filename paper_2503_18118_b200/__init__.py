@@ -94,7 +94,7 @@ def _load():
     L.xlmimo_sum_rate_workspace.argtypes = [i32, i64, i32, u32]
     L.xlmimo_sum_rate_workspace.restype = sz
     L.xlmimo_sum_rate_ws.argtypes = [vp, i32, i64, vp, i32, u32, vp, vp, vp, sz, vp]
-    L.xlmimo_app_a_bounds_workspace.argtypes = [i32, i64, i32]
+    L.xlmimo_app_a_bounds_workspace.argtypes = [i32, i64, i32, i32]
     L.xlmimo_app_a_bounds_workspace.restype = sz
     L.xlmimo_app_a_bounds.argtypes = [vp, i32, i64, vp, i32, vp, vp, vp, vp, vp, sz, vp]
     L.xlmimo_saturation_sweep_workspace.argtypes = [P(Array), vp, i32, i32, i64, i32, u32, i32, i32]
@@ -305,7 +305,8 @@ def sum_rate(gram: torch.Tensor, snr_db, receivers: int, flags: torch.Tensor | N
 def app_a_bounds(gram: torch.Tensor, snr_db, eig: bool = False, ws: torch.Tensor | None = None, stream=None):
     """NEXT-3, Appendix A per drop.  Returns rstat [D, 2] = (log2 det R,
     gap = -log2 det(R)/K), bounds [D, n_snr, 3] = (log2 U, log2 det(I + rho G), log2 L),
-    eigenvalues of R [D, K] ascending (K <= 64) or None, flags [D]."""
+    eigenvalues of R [D, K] ascending (Jacobi for K <= 64, Householder + bisection above) or
+    None, flags [D]."""
     _need_cuda()
     g = _gram_arg(gram)
     D, K = g.shape[0], g.shape[1]
@@ -314,7 +315,7 @@ def app_a_bounds(gram: torch.Tensor, snr_db, eig: bool = False, ws: torch.Tensor
     bounds = torch.empty((D, snr.size, 3), dtype=torch.float64, device=g.device)
     ev = torch.empty((D, K), dtype=torch.float64, device=g.device) if eig else None
     fl = torch.zeros(D, dtype=torch.int32, device=g.device)
-    need = int(_L.xlmimo_app_a_bounds_workspace(K, D, snr.size))
+    need = int(_L.xlmimo_app_a_bounds_workspace(K, D, snr.size, 1 if eig else 0))
     if need and (ws is None or ws.numel() < need):
         ws = _workspace(need, g.device)
     _check(_L.xlmimo_app_a_bounds(_dptr(g), K, D, _hptr(snr), snr.size, _dptr(rstat), _dptr(bounds),

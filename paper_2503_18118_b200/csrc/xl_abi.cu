@@ -387,9 +387,11 @@ int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, const double
   return xlmimo_sum_rate_ws(gram, K, n_drops, snr_db, n_snr, receivers, rates, flags, nullptr, 0, stream);
 }
 
-size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr) {
+size_t xlmimo_app_a_bounds_workspace(int32_t K, int64_t n_drops, int32_t n_snr, int32_t with_eig) {
   if (K < 1 || K > xl::kMaxKLarge || n_drops < 0 || n_snr < 1 || n_snr > xl::kMaxSnr) return 0;
-  return xlh::large_k_ws_bytes(K, n_drops, 1 + n_snr, false);
+  const size_t b = xlh::large_k_ws_bytes(K, n_drops, 1 + n_snr, false);
+  if (!with_eig || K <= xl::kMaxK) return b;
+  return (b + 255) / 256 * 256 + xlh::eig_ws_bytes(K, n_drops);
 }
 
 int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const double *snr_db, int32_t n_snr,
@@ -399,8 +401,6 @@ int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drops, const do
   g_err[0] = 0;
   if (K < 1 || n_drops < 0) return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: K=%d", K);
   if (K > xl::kMaxKLarge) return xlh::set_error(XLMIMO_EUNSUPPORTED, "app_a_bounds: K=%d > %d", K, xl::kMaxKLarge);
-  if (eig && K > xl::kMaxK)
-    return xlh::set_error(XLMIMO_EUNSUPPORTED, "app_a_bounds: eigenvalues need K <= %d", xl::kMaxK);
   if (!snr_db || n_snr < 1 || n_snr > xl::kMaxSnr)
     return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: n_snr out of [1,16]");
   if (n_drops > 0 && (!gram || !rstat || !bounds)) return xlh::set_error(XLMIMO_EINVAL, "app_a_bounds: null pointer");

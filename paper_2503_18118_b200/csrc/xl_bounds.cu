@@ -602,6 +602,143 @@ __device__ double block_sum(double v, double *red) {
   return s;
 }
 
+
+// ------------------------------------------------------------------ eigenvalues of R (64 < K <= 1024)
+// One CTA per matrix, R = D^{-1/2} G D^{-1/2} in a global slot (row-major, full Hermitian),
+// reduced to a real symmetric tridiagonal by K - 2 Householder reflections (unblocked:
+// for column k, v = x - alpha e1 with alpha = -e^{j arg x0} |x|, beta = 2 / v^H v, the
+// trailing block B <- H B H = B - v w^H - w v^H with p = beta B v, w = p - (beta/2)(v^H p) v;
+// the off-diagonal |alpha| -- a unitary diagonal similarity makes the complex tridiagonal
+// real), then every eigenvalue by bisection on Sturm counts (thread t finds the t-th
+// smallest, so the output is ascending).  Householder reduction is backward stable
+// (eigenvalue errors ~ K eps ||R||); the oracle's serial cyclic Jacobi is the reference.
+constexpr int kEigThreads = 1024;
+
+__global__ void __launch_bounds__(kEigThreads, 1) eig_householder_kernel(const double *gram, int K, int64_t n_drops,
+                                                                         double *eig, double2 *slots) {
+  extern __shared__ double2 esm[];
+  double2 *v = esm, *w = esm + K;                    // Householder vector, p / w
+  double *dg = reinterpret_cast<double *>(w + K);    // tridiagonal diagonal
+  double *oe = dg + K;                               // off-diagonal |alpha|
+  __shared__ double red[kEigThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kEigThreads / 32;
+  double2 *A = slots + (size_t)blockIdx.x * K * K;
+  for (int64_t d = blockIdx.x; d < n_drops; d += gridDim.x) {
+    const double2 *G = reinterpret_cast<const double2 *>(gram) + (size_t)d * K * K;
+    double *ev = eig + (size_t)d * K;
+    bool ok = true;
+    for (int i = tid; i < K; i += kEigThreads) ok &= G[(size_t)i * K + i].x > 0.0 && isfinite(G[(size_t)i * K + i].x);
+    for (size_t e = tid; e < (size_t)K * K; e += kEigThreads) ok &= isfinite(G[e].x) && isfinite(G[e].y);
+    if (!__syncthreads_and(ok ? 1 : 0)) {
+      for (int i = tid; i < K; i += kEigThreads) ev[i] = kNaN;
+      continue;
+    }
+    for (size_t e = tid; e < (size_t)K * K; e += kEigThreads) {
+      const int r = (int)(e / K), c = (int)(e - (size_t)r * K);
+      const double s = rsqrt(G[(size_t)r * K + r].x) * rsqrt(G[(size_t)c * K + c].x);
+      const double2 g = G[e];
+      A[e] = r == c ? make_double2(1.0, 0.0) : make_double2(g.x * s, g.y * s);
+    }
+    __syncthreads();
+    for (int k = 0; k + 1 < K; ++k) {
+      const int n = K - k - 1, o = k + 1;  // trailing block rows/cols o .. K-1
+      double part = 0.0;
+      for (int i = tid; i < n; i += kEigThreads) {
+        const double2 x = A[(size_t)(o + i) * K + k];
+        v[i] = x;
+        part += x.x * x.x + x.y * x.y;
+      }
+      const double sigma = block_sum(part, red);  // ends with a barrier: v is visible
+      const double2 x0 = v[0];
+      const double a0 = sqrt(x0.x * x0.x + x0.y * x0.y), nx = sqrt(sigma);
+      if (tid == 0) dg[k] = A[(size_t)k * K + k].x;
+      if (sigma - a0 * a0 <= 1e-300 || n == 1) {  // column already reduced: no reflection
+        if (tid == 0) oe[k] = a0;
+        __syncthreads();
+        continue;
+      }
+      const double2 ph = a0 > 0.0 ? make_double2(x0.x / a0, x0.y / a0) : make_double2(1.0, 0.0);
+      const double2 alpha = make_double2(-ph.x * nx, -ph.y * nx);
+      const double2 v0 = make_double2(x0.x - alpha.x, x0.y - alpha.y);
+      const double vv = sigma - a0 * a0 + v0.x * v0.x + v0.y * v0.y;
+      const double beta = 2.0 / vv;
+      __syncthreads();
+      if (tid == 0) {
+        v[0] = v0;
+        oe[k] = nx;
+      }
+      __syncthreads();
+      // p = beta B v: a warp per row, lanes along the row (coalesced)
+      double vpart = 0.0;
+      for (int i = warp; i < n; i += NW) {
+        const double2 *row = A + (size_t)(o + i) * K + o;
+        double sr = 0.0, si = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          const double2 b = row[j], vj = v[j];
+          sr = fma(b.x, vj.x, fma(-b.y, vj.y, sr));
+          si = fma(b.x, vj.y, fma(b.y, vj.x, si));
+        }
+        sr = xlk::warp_sum(sr) * beta;
+        si = xlk::warp_sum(si) * beta;
+        if (lane == 0) {
+          w[i] = make_double2(sr, si);
+          const double2 vi = v[i];
+          vpart += vi.x * sr + vi.y * si;  // Re(conj(v_i) p_i)
+        }
+      }
+      const double vhp = block_sum(vpart, red);
+      const double kk = 0.5 * beta * vhp;
+      for (int i = tid; i < n; i += kEigThreads) {
+        const double2 p = w[i], vi = v[i];
+        w[i] = make_double2(p.x - kk * vi.x, p.y - kk * vi.y);
+      }
+      __syncthreads();
+      // B <- B - v w^H - w v^H
+      for (int i = warp; i < n; i += NW) {
+        double2 *row = A + (size_t)(o + i) * K + o;
+        const double2 vi = v[i], wi = w[i];
+        for (int j = lane; j < n; j += 32) {
+          const double2 vj = v[j], wj = w[j];
+          double2 b = row[j];
+          // v_i conj(w_j) + w_i conj(v_j)
+          b.x -= vi.x * wj.x + vi.y * wj.y + wi.x * vj.x + wi.y * vj.y;
+          b.y -= vi.y * wj.x - vi.x * wj.y + wi.y * vj.x - wi.x * vj.y;
+          row[j] = b;
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) dg[K - 1] = A[(size_t)(K - 1) * K + (K - 1)].x;
+    __syncthreads();
+    // Gershgorin bounds, then bisection: thread t -> the t-th smallest eigenvalue
+    double lo = INFINITY, hi = -INFINITY;
+    for (int i = 0; i < K; ++i) {
+      const double r = (i > 0 ? oe[i - 1] : 0.0) + (i + 1 < K ? oe[i] : 0.0);
+      lo = fmin(lo, dg[i] - r);
+      hi = fmax(hi, dg[i] + r);
+    }
+    for (int t = tid; t < K; t += kEigThreads) {
+      double a = lo, b = hi;
+      for (int it = 0; it < 200 && b - a > 1e-15 * fmax(1.0, fabs(a) + fabs(b)); ++it) {
+        const double x = 0.5 * (a + b);
+        int cnt = 0;
+        double q = dg[0] - x;
+        cnt += q < 0.0;
+        for (int i = 1; i < K; ++i) {
+          if (q == 0.0) q = 1e-300;
+          q = dg[i] - x - oe[i - 1] * oe[i - 1] / q;
+          cnt += q < 0.0;
+        }
+        if (cnt > t) b = x;  // at least t + 1 eigenvalues below x
+        else a = x;
+      }
+      ev[t] = 0.5 * (a + b);
+    }
+    __syncthreads();
+  }
+}
+
 // App. A outputs from the tiled log-dets (matrix 0 = R, 1 + s = I + rho_s G)
 __global__ void __launch_bounds__(kCtaThreads) bounds_finish_kernel(BoundsParams P, const double *log2det) {
   __shared__ double red[kCtaThreads / 32];
@@ -907,6 +1044,18 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
 
 namespace xlh {
 
+// Eigenvalue slots for 64 < K: one K x K complex matrix per resident CTA (one per SM).
+int eig_ctas(int64_t n_drops) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int)(n_drops < sms ? n_drops : sms);
+}
+size_t eig_ws_bytes(int K, int64_t n_drops) {
+  if (K <= xl::kMaxK || n_drops == 0) return 0;
+  return align256((size_t)eig_ctas(n_drops) * K * K * sizeof(double2));
+}
+
 // Scratch for the large-K path: Cholesky slots + per-problem log-dets.
 size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat, bool with_dinv) {
   if (K <= xl::kMaxK || n_drops == 0 || n_mat == 0) return 0;
@@ -969,6 +1118,20 @@ int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_
     rc = check_launch("bounds_finish_kernel");
   }
   if (rc || !eig) return rc;
+  if (K > xl::kMaxK) {  // Householder tridiagonalisation + bisection, slots after the Cholesky scratch
+    const size_t off = align256(large_k_ws_bytes(K, n_drops, 1 + n_snr, false));
+    if (ws_bytes < off + eig_ws_bytes(K, n_drops) || !ws)
+      return set_error(XLMIMO_EWORKSPACE, "app_a_bounds: eigenvalues need %zu workspace bytes",
+                       off + eig_ws_bytes(K, n_drops));
+    const size_t smem = (size_t)K * 2 * sizeof(double2) + (size_t)K * 2 * sizeof(double);
+    KTimer tm(s, "eig_householder");
+    cudaFuncSetAttribute(eig_householder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_householder_kernel<<<(unsigned)eig_ctas(n_drops), kEigThreads, smem, s>>>(gram, K, n_drops, eig,
+                                                                               (double2 *)((char *)ws + off));
+    tm.stop(s);
+    count_launch();
+    return check_launch("eig_householder_kernel");
+  }
   const int Kp = K + (K & 1);
   const size_t per_warp = (size_t)Kp * (Kp + 1) * sizeof(double2);
   int nw = (int)((100 * 1024) / per_warp);

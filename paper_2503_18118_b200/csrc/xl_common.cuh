@@ -264,6 +264,7 @@ int launch_sum_rate(const double *gram, int K, int64_t n_prob, const double *snr
                     uint32_t receivers, double *rates, uint32_t *flags, cudaStream_t s);
 
 // xl_bounds.cu : Appendix A (NEXT-3) and the large-K (K > 64) receivers
+size_t eig_ws_bytes(int K, int64_t n_drops);
 size_t large_k_ws_bytes(int K, int64_t n_drops, int n_mat, bool with_dinv);
 size_t sum_rate_large_ws_bytes(int K, int64_t n_drops, int n_snr, uint32_t receivers);
 int launch_bounds(const double *gram, int K, int64_t n_drops, const double *snr_db, int n_snr, double *rstat,

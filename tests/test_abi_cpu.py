@@ -80,16 +80,18 @@ def test_invalid_arguments_are_rejected_without_a_device(lib):
     snr = np.zeros(1)
     assert L.xlmimo_sum_rate(ctypes.c_void_p(8), 4, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 0,
                              ctypes.c_void_p(8), None, None) == -1  # no receivers
-    # Appendix A / large K: eigenvalues only for K <= 64, K <= 1024, workspace for K > 64
+    # Appendix A / large K: K <= 1024, workspace for K > 64 (Cholesky slots, Householder slots)
     rs = ctypes.c_void_p(8)
     assert L.xlmimo_app_a_bounds(rs, 65, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, rs, None, None, 0,
-                                 None) == -2
+                                 None) == -3  # K > 64 eigenvalues: Householder slots in the workspace
     assert L.xlmimo_app_a_bounds(rs, 1025, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, None, None, None, 0,
                                  None) == -2
     assert L.xlmimo_app_a_bounds(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, rs, rs, None, None, None, 0,
                                  None) == -3
     assert L.xlmimo_app_a_bounds(rs, 8, 1, None, 1, rs, rs, None, None, None, 0, None) == -1
-    assert L.xlmimo_app_a_bounds_workspace(8, 100, 1) == 0 < L.xlmimo_app_a_bounds_workspace(100, 100, 1)
+    assert L.xlmimo_app_a_bounds_workspace(8, 100, 1, 0) == 0 < L.xlmimo_app_a_bounds_workspace(100, 100, 1, 0)
+    assert L.xlmimo_app_a_bounds_workspace(8, 100, 1, 1) == 0  # K <= 64: Jacobi in shared memory
+    assert L.xlmimo_app_a_bounds_workspace(100, 100, 1, 1) > L.xlmimo_app_a_bounds_workspace(100, 100, 1, 0)
     assert L.xlmimo_sum_rate(rs, 1025, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -2  # K>1024
     assert L.xlmimo_sum_rate(rs, 333, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -3  # ZF: ws
     assert L.xlmimo_sum_rate(rs, 100, 1, snr.ctypes.data_as(ctypes.c_void_p), 1, 2, rs, None, None) == -3  # ZF: ws

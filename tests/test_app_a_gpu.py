@@ -68,10 +68,11 @@ def test_app_a_parity_small_k(xl, orc, K, N, D):
                                    (200, 1000, 2), (333, 2000, 1)])
 def test_app_a_parity_large_k(xl, orc, K, N, D):
     """K > 64: the shared-memory Cholesky (K <= 160) and the tiled one (K > 160, ragged
-    last tile for 161, 200, 333)."""
+    last tile for 161, 200, 333); eigenvalues of R by Householder + bisection against the
+    oracle's cyclic Jacobi (1e-10) up to K = 200."""
     Gh = _rect_gram_oracle(orc, K, N, D, seed=K)
     G = torch.view_as_complex(torch.tensor(np.stack([Gh.real, Gh.imag], -1), device="cuda").contiguous())
-    _compare(xl, orc, Gh, G, eig=False)
+    _compare(xl, orc, Gh, G, eig=K <= 200)
 
 
 def test_app_a_flags_and_edges(xl, orc):
@@ -89,13 +90,11 @@ def test_app_a_flags_and_edges(xl, orc):
             Gl[d] = np.eye(KL)
             Gl[d, :4, :4] = G[d]
         Gld = torch.view_as_complex(torch.tensor(np.stack([Gl.real, Gl.imag], -1), device="cuda").contiguous())
-        _compare(xl, orc, Gl, Gld, eig=False)
+        _compare(xl, orc, Gl, Gld, eig=True)
     # empty batch
     e = torch.zeros((0, 8, 8), dtype=torch.complex128, device="cuda")
     rs, bo, _, _ = xl.app_a_bounds(e, SNR)
     assert rs.shape == (0, 2) and bo.shape == (0, 3, 3)
-    with pytest.raises(xl.XlmimoError):
-        xl.app_a_bounds(Gld, SNR, eig=True)  # eigenvalues need K <= 64
 
 
 @pytest.mark.parametrize("K,N,D", [(65, 3000, 3), (100, 20000, 2), (160, 500, 2), (161, 900, 2), (250, 4000, 2),
@@ -119,8 +118,20 @@ def test_sum_rate_large_k_parity(xl, orc, K, N, D):
 
 def test_app_a_paper_gap_k1000_gpu(xl, orc):
     """-E_K[log2 lambda^R] = 0.064 at K = 1000 (E1 user field, M = 35 000):
-    GPU log2 det R of the oracle's Gram equals the oracle's, and the paper's number."""
+    GPU log2 det R of the oracle's Gram equals the oracle's, and the paper's number.  The
+    eigenvalues of R behind it (Householder + bisection; the oracle's serial Jacobi is too
+    slow at K = 1000): ascending, positive, summing to trace R = K, their mean -log2 equal
+    to the gap from the independent Cholesky path, and equal to LAPACK's eigvalsh of the
+    oracle's R (the library routine the oracle's own Jacobi is pinned to)."""
     Gh = _rect_gram_oracle(orc, 1000, 35000, 1, seed=0)
     G = torch.view_as_complex(torch.tensor(np.stack([Gh.real, Gh.imag], -1), device="cuda").contiguous())
     rs, _ = _compare(xl, orc, Gh, G, eig=False)
     assert abs(rs[0, 1] - 0.064) < 1e-3
+    _, _, ev, _ = xl.app_a_bounds(G, SNR, eig=True)
+    ev = ev.cpu().numpy()[0]
+    assert np.all(np.diff(ev) >= 0) and ev[0] > 0
+    assert abs(ev.sum() - 1000.0) < 1e-9 * 1000
+    assert abs(-np.mean(np.log2(ev)) - rs[0, 1]) < 1e-9
+    d = np.sqrt(np.real(np.diagonal(Gh[0])))
+    ref = np.linalg.eigvalsh(Gh[0] / np.outer(d, d))
+    assert np.max(np.abs(ev - ref)) < 1e-10

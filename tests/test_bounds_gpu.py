@@ -96,8 +96,8 @@ def test_receivers_and_bounds_write_in_bounds(xl, K):
         b.check()
     rst = Guarded(D * 2)
     bo = Guarded(D * S * 3)
-    ev = Guarded(D * K) if K <= 64 else None
-    need = xl._L.xlmimo_app_a_bounds_workspace(K, D, S)
+    ev = Guarded(D * K)
+    need = xl._L.xlmimo_app_a_bounds_workspace(K, D, S, 1)
     ws2 = _ws(need)
     rc = xl._L.xlmimo_app_a_bounds(gp, K, D, sp, S, rst.ptr(), bo.ptr(), ev.ptr() if ev else None, None,
                                    ws2.ptr() if need else None, need, None)

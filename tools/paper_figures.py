@@ -104,12 +104,15 @@ def e3(D):
 
         def run():
             G = xl.gram_exact(a, pos)
-            return xl.app_a_bounds(G, [0.0, 30.0])
-        (rs, bo, _, fl), ms = dev_ms(run)
+            return xl.app_a_bounds(G, [0.0, 30.0], eig=True)
+        (rs, bo, ev, fl), ms = dev_ms(run)
         t_ms += ms
         gap = rs[:, 1].cpu().numpy()
         bo = bo.cpu().numpy()
+        lam = ev.cpu().numpy().ravel()
         out.append({"K": K, "gap_mean": float(np.nanmean(gap)), "gap_std": float(np.nanstd(gap)),
+                    "eig_R_quantiles_0_1_10_50_90_99_100": np.nanpercentile(lam, [0, 1, 10, 50, 90, 99, 100]).tolist(),
+                    "minus_mean_log2_eig": float(-np.nanmean(np.log2(lam))),
                     "flagged": int((fl != 0).sum()), "log2U_minus_C_0dB": float(np.mean(bo[:, 0, 0] - bo[:, 0, 1])),
                     "C_minus_log2L_0dB": float(np.mean(bo[:, 0, 1] - bo[:, 0, 2])), "device_ms": ms})
     return {"figure": "E3 K_vs_E", "M": 35000, "drops": D, "points": out,
