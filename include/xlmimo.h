@@ -106,7 +106,8 @@ XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint
  *   precision XLMIMO_FP64: fp64 everywhere.  XLMIMO_FP32: fp64 distance and
  *     phase reduction, fp32 phasor and in-tile accumulation, fp64 across tiles.
  *   mode XLMIMO_FUSED: H is never materialised.  XLMIMO_MATERIALIZED: H is
- *     written to the workspace as planar complex64 and streamed back (fp32 only).
+ *     written to the workspace as complex64 (TF32-rounded) and streamed back by TMA
+ *     (fp32 only; for K > 64 as L2-sized chunks of scaled fp16 pairs, below).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
  * Im G(i,i) = 0.  K <= 1024 -- 64 < K <= 1024 are the NEXT-3/E1-E3 user counts,
  * fp64 on DMMA, in blocks of 64 users up to K = 128 and above
@@ -114,8 +115,9 @@ XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint
  * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
  * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
  * operands generated in-kernel below K = 352 and, from K = 352 on or in MATERIALIZED
- * mode, read by TMA from complex64 (TF32) chunks of H written to the workspace
- * (<= 112 MB per unit of drops x 4096-element chunks).  Below 1024 elements an fp32
+ * mode, read by TMA from chunks of H written to the workspace as fp16 pairs with a
+ * per-drop power-of-two scale (11 significant bits, as TF32; <= 112 MB per unit of
+ * drops x 4096-element chunks, so the reads hit L2).  Below 1024 elements an fp32
  * request with K > 64 runs the fp64 kernels (TF32 rounding would not average out).
  * ws may be NULL iff the query returns 0.
  * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, fp32 with K > 64 on an

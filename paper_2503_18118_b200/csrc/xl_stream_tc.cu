@@ -1073,10 +1073,61 @@ __global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos
   }
 }
 
+// Per-drop power-of-two operand scale for the fp16 chunks (as the fused kernel's, R27):
+// one warp per drop, min over users of xz2 (make_user), e = -ilogb(sqrt(beta0)/sqrt(min)).
+__global__ void __launch_bounds__(256) drop_scale_kernel(const double *pos, int K, int kind, double sqrt_beta0,
+                                                         int64_t n_drops, float *scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t d = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (d >= n_drops) return;
+  scale[d] = epi_drop_scale(pos + d * K * 3, K, kind, sqrt_beta0, lane);
+}
+
+// K4a for the fp16 pair stream: H of a unit of drops x chunks in the tiled64 fp16 layout
+// [drop - drop0][N_pad / 64][2 Kr][64] (row 2k = Re h_k, 2k + 1 = Im h_k; one 128-B swizzle
+// row per user plane and tile), scaled per drop.  A warp covers one 64-element tile for
+// 32 / (64 / TE) users; lane = (user, TE-element task), one 32-B (TE = 16) or 16-B store
+// per plane.  Padded users (k >= K) and elements past N are 0.
+template <int TE>
+__global__ void __launch_bounds__(256) h_chunk_f16_kernel(const double *pos, int K, int Kr, int kind, int64_t N,
+                                                          int64_t t_first, int64_t n_pad, int64_t n_y, int64_t n_z,
+                                                          double pitch, double lambda, double sqrt_beta0,
+                                                          int64_t drop0, int n_ugrp, const float *scale,
+                                                          uint16_t *H) {
+  constexpr int LPR = 64 / TE, UPW = 32 / LPR;  // lanes per user row, users per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bd = blockIdx.y / n_ugrp, ug = blockIdx.y - bd * n_ugrp;
+  const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
+  if (tile * 64 >= n_pad) return;
+  const int u = UPW * ug + lane / LPR, g = lane % LPR;
+  if (u >= Kr) return;
+  uint16_t *row = H + (((size_t)bd * (n_pad / 64) + tile) * (2 * Kr) + 2 * u) * 64 + TE * g;
+  uint32_t hr[TE / 2], hi[TE / 2];
+  if (u < K) {
+    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
+    const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
+    const int64_t t0 = t_first + tile * 64 + TE * g;
+    const double inv_lambda = 1.0 / lambda;
+    gen_task_h<TE>(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch,
+                   scale[drop0 + bd], hr, hi);
+  } else {
+#pragma unroll
+    for (int m = 0; m < TE / 2; ++m) hr[m] = hi[m] = 0u;
+  }
+#pragma unroll
+  for (int h = 0; h < TE / 8; ++h) {  // L2-resident chunk: default-cached stores
+    *reinterpret_cast<uint4 *>(row + 8 * h) = make_uint4(hr[4 * h], hr[4 * h + 1], hr[4 * h + 2], hr[4 * h + 3]);
+    *reinterpret_cast<uint4 *>(row + 64 + 8 * h) =
+        make_uint4(hi[4 * h], hi[4 * h + 1], hi[4 * h + 2], hi[4 * h + 3]);
+  }
+}
+
 // K > 64 fp32 from a materialised chunk: the pair kernel's MMA and epilogue, fed by TMA
-// from the tiled32 H of a unit of B drops x C element chunks (kPChunk each, L2-sized)
-// instead of regenerating both 64-user blocks per pair.  tile index in the unit =
-// (b * C + c) * (kPChunk / 32) + kb; rows of block b: [128 b, 128 b + 128).
+// from the tiled64 fp16 H of a unit of B drops x C element chunks (kPChunk each, L2-sized;
+// fp16 operands with a per-drop scale as in the fused kernel, R27: half the L2 operand
+// bytes of the round-1 TF32 chunks, which bound this kernel) instead of regenerating both
+// 64-user blocks per pair.  tile index in the unit = (b * C + c) * (kPChunk / 64) + kb;
+// rows of block b: [128 b, 128 b + 128); tcgen05.mma kind::f16, M = 128, N = 256.
 constexpr int kSSlots = 4;                       // stream-pair ring: A 16 KB + B 32 KB per stage
 constexpr int kSSlotBytes = 3 * kStageBytes;
 struct StreamPairParams {
@@ -1087,6 +1138,7 @@ struct StreamPairParams {
   int n_ud, n_uc;    // drops and chunks in the unit
   int c0;            // first chunk of the unit
   int n_chunks;      // chunks per drop (partials layout)
+  const float *scale;  // per-drop fp16 operand scale (absolute drop index)
 };
 
 __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -1126,7 +1178,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
-  constexpr int kTilesPerChunk = kPChunk / kBoxK;
+  constexpr int kTilesPerChunk = kPChunk / kFBoxK;  // fp16 tiles of 64 elements
   // item = (drop, block row bi, column blocks bj, bj + 1 (bj = bi + 2q), chunk): the B
   // operand is 256 rows (two 64-user blocks; rows past 2 K_pad come in as TMA zero fill)
   auto decode = [&](int64_t it, int &bl, int &bi, int &bj, int &cl) {
@@ -1140,7 +1192,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
   };
   auto n_stages = [&](int cl) {
     const int64_t x0 = (int64_t)(P.c0 + cl) * kPChunk, rem = P.N - x0;
-    return (int)(((rem < kPChunk ? rem : kPChunk) + kBoxK - 1) / kBoxK);
+    return (int)(((rem < kPChunk ? rem : kPChunk) + kFBoxK - 1) / kFBoxK);
   };
 
   if (warp == 0) {
@@ -1165,7 +1217,7 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = tf32_idesc(kRows, 2 * kRows);
+      const uint32_t idesc = f16_idesc(kRows, 2 * kRows);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -1184,8 +1236,8 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
           const uint32_t sa = smem_u32(stages + stage * kSSlotBytes);
           const uint32_t sb = sa + kStageBytes;  // 256 rows: blocks bj, bj + 1
 #pragma unroll
-          for (int kk = 0; kk < kBoxK / 8; ++kk)
-            mma_tf32(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kFBoxK / 16; ++kk)  // 16 fp16 (32 B) per MMA along K
+            mma_f16(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&empty[stage]);
           if (++stage == kSSlots) { stage = 0; phase ^= 1; }
         }
@@ -1206,6 +1258,8 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
       mbar_wait(&tfull[acc], acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       double *out = P.ws + ((size_t)(P.drop0 + bl) * P.n_chunks + (P.c0 + cl)) * (size_t)(2 * NP);
+      const double sc = (double)P.scale[P.drop0 + bl];
+      const double post = 1.0 / (sc * sc);  // exact: a power of two
       const int i = bi * kPUsers + il;
       for (int cb = 0; cb < 2 * kRows / 32; ++cb) {
         float v[32];
@@ -1223,8 +1277,8 @@ __global__ void __launch_bounds__(256, 1) gram_stream_tc_pair_kernel(const __gri
           else { rr = x[2 * jj]; ri = x[2 * jj + 1]; ir = v[2 * jj]; rr2 = v[2 * jj + 1]; }
           if (i < K && j < K && j >= i) {
             const int64_t pp = (int64_t)i * K - (int64_t)i * (i - 1) / 2 + (j - i);
-            out[2 * pp] = (double)rr + (double)rr2;
-            out[2 * pp + 1] = (i == j) ? 0.0 : (double)ri - (double)ir;
+            out[2 * pp] = ((double)rr + (double)rr2) * post;
+            out[2 * pp + 1] = (i == j) ? 0.0 : ((double)ri - (double)ir) * post;
           }
         }
       }
@@ -1335,7 +1389,7 @@ PairUnit stream_pair_unit(int K, int64_t n_drops, int64_t N) {
   PairUnit u;
   const int nb = (K + kPUsers - 1) / kPUsers;
   u.Kp = nb * kPUsers;
-  const int64_t per = (int64_t)kPChunk * 2 * u.Kp * 4;  // one drop-chunk of H
+  const int64_t per = (int64_t)kPChunk * 2 * u.Kp * 2;  // one drop-chunk of H (fp16)
   const int64_t cap = 112ll << 20;  // most of the 126 MB L2 (measured best: 48 MB 84 ms, 112 MB 69 ms, 160+ MB 70 ms at E3)
   int64_t cells = cap / per;
   if (cells < 1) cells = 1;
@@ -1346,16 +1400,19 @@ PairUnit stream_pair_unit(int K, int64_t n_drops, int64_t N) {
   u.B = (int)(b < 1 ? 1 : b);
   return u;
 }
-size_t stream_pair_h_bytes(int K, int64_t n_drops, int64_t N) {
+size_t stream_pair_h_bytes(int K, int64_t n_drops, int64_t N) {  // H unit (fp16) + per-drop scales
   const PairUnit u = stream_pair_unit(K, n_drops, N);
-  return (size_t)u.B * u.C * kPChunk * 2 * u.Kp * 4;
+  return ((size_t)u.B * u.C * kPChunk * 2 * u.Kp * 2 + 255) / 256 * 256 + (size_t)n_drops * sizeof(float);
 }
 
 int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
-                          float *H, cudaStream_t s) {
+                          float *Hbuf, cudaStream_t s) {
   auto enc = encode_fn();
   if (!enc) return set_error(XLMIMO_ECUDA, "stream_tc_pair: cuTensorMapEncodeTiled unavailable");
   const PairUnit u = stream_pair_unit(K, n_drops, N);
+  uint16_t *H = reinterpret_cast<uint16_t *>(Hbuf);
+  float *scale = reinterpret_cast<float *>(
+      (char *)Hbuf + ((size_t)u.B * u.C * kPChunk * 2 * u.Kp * 2 + 255) / 256 * 256);
   const int nbk = u.Kp / kPUsers;
   const int chunks = fused_tc_pair_chunks(N);
   StreamPairParams P;
@@ -1366,6 +1423,14 @@ int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_d
   for (int bi = 0; bi < nbk; ++bi) P.n_pairs += (nbk - bi + 1) / 2;
   P.N = N;
   P.n_chunks = chunks;
+  P.scale = scale;
+  {
+    KTimer tm(s, "drop_scale");
+    drop_scale_kernel<<<(unsigned)((n_drops + 7) / 8), 256, 0, s>>>(pos, K, a.kind, a.sqrt_beta0, n_drops, scale);
+    tm.stop(s);
+    count_launch();
+  }
+  const int te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
   const size_t smem = 1024 + (size_t)kSSlots * kSSlotBytes + (2 * kSSlots + 4) * 8 + 16;
   cudaFuncSetAttribute(gram_stream_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148;
@@ -1376,20 +1441,29 @@ int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_d
     for (int c0 = 0; c0 < chunks; c0 += u.C) {
       const int ncu = (chunks - c0) < u.C ? chunks - c0 : u.C;
       const int64_t n_pad = (int64_t)ncu * kPChunk;
-      int rc;
       {
         KTimer tm(s, "h_materialise");
-        rc = launch_h_materialise_tc(a, pos, K, N, n_pad, d0, nd, H, s, u.Kp, (int64_t)c0 * kPChunk, 1);
+        const int upw = te16 ? 8 : 4;
+        const int n_ugrp = (u.Kp + upw - 1) / upw;
+        const dim3 grid((unsigned)((n_pad + 511) / 512), (unsigned)(nd * n_ugrp));
+        const int64_t nz = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+        if (te16)
+          h_chunk_f16_kernel<16><<<grid, 256, 0, s>>>(pos, K, u.Kp, a.kind, N, (int64_t)c0 * kPChunk, n_pad, a.n_y,
+                                                      nz, a.pitch, a.lambda, a.sqrt_beta0, d0, n_ugrp, scale, H);
+        else
+          h_chunk_f16_kernel<8><<<grid, 256, 0, s>>>(pos, K, u.Kp, a.kind, N, (int64_t)c0 * kPChunk, n_pad, a.n_y,
+                                                     nz, a.pitch, a.lambda, a.sqrt_beta0, d0, n_ugrp, scale, H);
         tm.stop(s);
         count_launch();
       }
+      int rc = check_launch("h_chunk_f16_kernel");
       if (rc) return rc;
       CUtensorMap map;
-      const cuuint64_t gdim[3] = {(cuuint64_t)kBoxK, (cuuint64_t)(2 * u.Kp), (cuuint64_t)nd * (n_pad / kBoxK)};
-      const cuuint64_t gstride[2] = {(cuuint64_t)kBoxK * 4, (cuuint64_t)kBoxK * 4 * 2 * u.Kp};
-      const cuuint32_t box[3] = {(cuuint32_t)kBoxK, (cuuint32_t)kRows, 1};
+      const cuuint64_t gdim[3] = {(cuuint64_t)kFBoxK, (cuuint64_t)(2 * u.Kp), (cuuint64_t)nd * (n_pad / kFBoxK)};
+      const cuuint64_t gstride[2] = {(cuuint64_t)kFBoxK * 2, (cuuint64_t)kFBoxK * 2 * 2 * u.Kp};
+      const cuuint32_t box[3] = {(cuuint32_t)kFBoxK, (cuuint32_t)kRows, 1};
       const cuuint32_t estride[3] = {1, 1, 1};
-      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)H, gdim, gstride, box, estride,
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void *)H, gdim, gstride, box, estride,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return set_error(XLMIMO_ECUDA, "stream_tc_pair: tensor map encode failed (%d)", (int)r);
@@ -1400,7 +1474,7 @@ int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_d
       const int64_t items = (int64_t)nd * P.n_pairs * ncu;
       const int grid = (int)(items < sms ? items : sms);
       {
-        KTimer tm(s, "gram_stream_tc_pair_tf32");
+        KTimer tm(s, "gram_stream_tc_pair_f16");
         gram_stream_tc_pair_kernel<<<grid, 256, smem, s>>>(map, P);
         tm.stop(s);
         count_launch();
