@@ -114,7 +114,7 @@ XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint
  * it as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
  * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
  * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
- * operands generated in-kernel below K = 352 and, from K = 352 on or in MATERIALIZED
+ * operands generated in-kernel up to K = 128 and, from K = 129 on or in MATERIALIZED
  * mode, read by TMA from chunks of H written to the workspace as fp16 pairs with a
  * per-drop power-of-two scale (11 significant bits, as TF32; <= 112 MB per unit of
  * drops x 4096-element chunks, so the reads hit L2).  Below 1024 elements an fp32

@@ -1631,7 +1631,9 @@ constexpr int kSyrkMinK = 129;  // measured (35 000 elements): K = 128 blk 61 vs
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
 // generated in-kernel below; XLMIMO_OPT_PAIR = 1 (gen) | 2 (stream) overrides.
-constexpr int kStreamPairMinK = 352;  // measured crossover (35 000 elements): K = 320 gen 12.2 vs stream 12.8 ms, K = 384 17.4 vs 13.6
+constexpr int kStreamPairMinK = 129;  // fp16 chunks win from K = 65 (35 000 elements: K = 100 11.7 vs 13.5 ms, 160 9.2 vs
+                                      // 14.8, 352 7.7 vs 16.8); up to 128 the in-kernel path stays, its TMEM folding
+                                      // keeping E1/E2's K = 100 rates unbiased (R28)
 bool use_stream_pair(int K) {
   const int64_t o = xlh::option(XLMIMO_OPT_PAIR);
   if (o == 1) return false;
