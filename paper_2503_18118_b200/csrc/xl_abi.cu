@@ -439,10 +439,12 @@ static const double kSnrProbe = 0.0;  // validate_sweep wants a non-null SNR lis
 size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n, int32_t K,
                                          int64_t n_drops, int32_t n_snr, uint32_t receivers, int32_t gram_kind,
                                          int32_t precision) {
-  if (validate_sweep(array, n_list, n_n, K, n_drops, &kSnrProbe, n_snr, receivers, gram_kind, precision, 0.5)) {
-    g_err[0] = 0;  // a size query reports a bad argument as 0 bytes, not as the thread's last error
-    return 0;
-  }
+  char saved[sizeof(g_err)];  // a size query reports a bad argument as 0 bytes; the thread's last error stays
+  memcpy(saved, g_err, sizeof(g_err));
+  const int bad = validate_sweep(array, n_list, n_n, K, n_drops, &kSnrProbe, n_snr, receivers, gram_kind, precision,
+                                 0.5);
+  memcpy(g_err, saved, sizeof(g_err));
+  if (bad) return 0;
   return sweep_layout(nullptr, to_params(array), n_list, n_n, K, n_drops, n_snr, receivers, gram_kind, precision)
       .total;
 }
