@@ -239,6 +239,7 @@ int launch_gram_syrk(const ArrayP &a, const double *pos, int K, int64_t n_drops,
 // xl_stream_tc.cu : tcgen05 TF32 streaming Gram over a materialised batch
 bool stream_tc_supported(int K, int64_t N);
 int stream_tc_chunks(int64_t N);
+int fused_tc_chunks(int64_t N, int64_t n_drops);
 int stream_tc_parts(int K);
 bool fused_tc_supported(const ArrayP &a, int K);
 bool fused_tc_supported_geometry(const ArrayP &a);

@@ -1826,7 +1826,8 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
     const size_t part = ((size_t)n_drops * parts * n_lvl * np * 2 * sizeof(double) + 255) / 256 * 256;
     return part + (size_t)materialised_batch(N, K, n_drops) * mat_npad(K, N) * K * 2 * sizeof(float);
   }
-  if (use_fused_tc(a, K, precision, n_lvl)) return (size_t)n_drops * stream_tc_chunks(N) * stream_tc_parts(K) * np * 2 * sizeof(double);
+  if (use_fused_tc(a, K, precision, n_lvl))
+    return (size_t)n_drops * fused_tc_chunks(N, n_drops) * stream_tc_parts(K) * np * 2 * sizeof(double);
   const KernelChoice kc = choose_kernel(a, K, precision);
   return (size_t)n_drops * n_split * n_lvl * kc.parts * np * 2 * sizeof(double);
 }
@@ -2042,7 +2043,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
     const int64_t n_items = n_drops * (int64_t)K * (K + 1) / 2;
     KTimer tr(s, "gram_reduce");
     gram_reduce_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>((const double *)ws, K, n_drops,
-                                                                        stream_tc_chunks(N), 1, stream_tc_parts(K), out);
+                                                                        fused_tc_chunks(N, n_drops), 1, stream_tc_parts(K), out);
     tr.stop(s);
     count_launch();
     return check_launch("gram_reduce_kernel");

@@ -241,9 +241,9 @@ struct StreamParams {
   uint32_t tmem_cols;
 };
 
-// stages of work item chunk c: kb_per_chunk, fewer in the ragged last chunk
-__device__ __forceinline__ int item_stages(int64_t N, int c, int kb_per_chunk, int spb) {
-  const int64_t rem = N - (int64_t)c * kChunk;
+// stages of work item chunk c (chunk elements each): kb_per_chunk, fewer in the ragged last chunk
+__device__ __forceinline__ int item_stages(int64_t N, int c, int kb_per_chunk, int spb, int chunk = kChunk) {
+  const int64_t rem = N - (int64_t)c * chunk;
   const int64_t ns = (rem + spb - 1) / spb;
   return ns < kb_per_chunk ? (int)ns : kb_per_chunk;
 }
@@ -400,6 +400,7 @@ struct FusedParams {
   int rb, nblk;      // rows per element block, blocks stacked per stage (as StreamParams)
   int n_mma;
   int n_chunks;
+  int chunk;         // elements per work item (a multiple of kChunk)
   int64_t n_drops;
   uint32_t tmem_cols;
 };
@@ -659,7 +660,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
-  const int kb_per_chunk = kChunk / (kFBoxK * P.nblk);
+  const int kb_per_chunk = P.chunk / (kFBoxK * P.nblk);
 
   if (warp < kEpiWarp0) {  // ---------------- generators: group g makes stages k = g (mod 8)
     // The global stage sequence k (the MMA issuer's order) lives in slot k % 12 with
@@ -680,10 +681,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
-      const int64_t x0 = (int64_t)c * kChunk;
+      const int64_t x0 = (int64_t)c * P.chunk;
       const int64_t rem = P.N - x0;
       const int spb = kFBoxK * P.nblk;  // elements per stage
-      const int ns = (int)(((rem < kChunk ? rem : kChunk) + spb - 1) / spb);
+      const int ns = (int)(((rem < P.chunk ? rem : P.chunk) + spb - 1) / spb);
       int64_t k = kstart + (((int64_t)grp - kstart) % kFGroups + kFGroups) % kFGroups;
       kstart += ns;
       if (k >= kstart) continue;  // no stage of this item for this group
@@ -742,7 +743,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
-      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk);
+      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk, P.chunk);
       for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {  // one TMEM sub-chunk
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
@@ -787,7 +788,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
       const float sc = epi_drop_scale(P.pos + d * K * 3, K, P.kind, P.sqrt_beta0, lane);
       const double post = 1.0 / ((double)sc * (double)sc);  // exact: sc is a power of two
-      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk);
+      const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk, P.chunk);
       for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
@@ -1314,6 +1315,19 @@ bool stream_tc_supported(int K, int64_t N) { return K >= 9 && K <= 64 && (N % 4)
 
 int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
 
+// Fused fp32 work items: the longest chunk (8192 .. 65536 elements, TMEM folding keeps the
+// accumulation unbiased at any length) that still leaves >= 4 waves of items, so the fp64
+// partials -- the kernel's only DRAM writes -- stay a small multiple of the output.
+int fused_tc_chunk(int64_t N, int64_t n_drops) {
+  int c = kChunk;
+  while (c < 65536 && n_drops * ((N + 2 * c - 1) / (2 * c)) >= 4 * 148) c *= 2;
+  return c;
+}
+int fused_tc_chunks(int64_t N, int64_t n_drops) {
+  const int c = fused_tc_chunk(N, n_drops);
+  return (int)((N + c - 1) / c);
+}
+
 // UPA: a generator task (kTaskE consecutive elements off one fp64 anchor, the delta
 // along y) must not cross a row of the n_y x n_z grid, so n_y must be a multiple of
 // kTaskE; other UPAs take the CUDA-core fp32 kernel.
@@ -1337,7 +1351,8 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   P.rb = rows_per_block(K);
   P.nblk = kRows / P.rb;
   P.n_mma = P.nblk > 1 ? kRows : (2 * K + 15) / 16 * 16;
-  P.n_chunks = stream_tc_chunks(N);
+  P.chunk = fused_tc_chunk(N, n_drops);
+  P.n_chunks = fused_tc_chunks(N, n_drops);
   P.n_drops = n_drops;
   uint32_t cols = 32;
   while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
