@@ -506,8 +506,15 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
 // to fp16 (round to nearest even: 11 significant bits, the precision of TF32) and packed
 // in pairs, hr[q] = (re h_{2q}, re h_{2q+1}) low half first, hi likewise.  Full tasks
 // (all TE elements < N) skip the per-element padding select.
+// A generator's user: the fp64 geometry of xl::UserC and its amplitude sqrt(beta0) sqrt(x_eff)
+// rounded to fp32 once per drop (the coefficient's amplitude is an fp32 product anyway).
+struct __align__(16) GenUser {
+  double xz2, y, z;
+  float amp, unused;
+};
+
 template <int TE>
-__device__ __forceinline__ void gen_task_h(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
+__device__ __forceinline__ void gen_task_h(const GenUser &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
                                            int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
                                            float pitch_f, float scale, uint32_t (&hr)[TE / 2],
                                            uint32_t (&hi)[TE / 2]) {
@@ -529,7 +536,7 @@ __device__ __forceinline__ void gen_task_h(const double4 &uc, int kind, int64_t 
     ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
   }
   const double dy = ey - uc.y, dz = ez - uc.z;
-  const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
+  const double r2 = fma(dy, dy, fma(dz, dz, uc.xz2));
   const double ir = xl::rsqrt_nr(r2);
   const double rc = r2 * ir;
   const double qc = rc * inv_lambda;
@@ -543,7 +550,9 @@ __device__ __forceinline__ void gen_task_h(const double4 &uc, int kind, int64_t 
   const float cb = 0.5f * w * pp;
   const float cg = -0.5f * u * w * p1 * pp;
   const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;
-  const float ac = (float)uc.w * irf * rsqrtf((float)rc) * scale;
+  float sq;  // r^{-1/2} from the fp32 1/r (one MUFU, no second double -> float conversion)
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(irf));
+  const float ac = uc.amp * irf * sq * scale;
   const float a0 = ac;
   const float a1 = ac * (-1.5f * u * p1);
   const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
@@ -609,9 +618,9 @@ __device__ __forceinline__ float scale_of_min_xz2(double min_xz2, double sqrt_be
   const int e = -ilogb(sqrt_beta0 / sqrt(min_xz2));
   return __int_as_float((127 + e) << 23);
 }
-__device__ __forceinline__ float drop_scale(const double4 *su, int K, double sqrt_beta0) {
-  double m = su[0].x;
-  for (int u = 1; u < K; ++u) m = fmin(m, su[u].x);
+__device__ __forceinline__ float drop_scale(const GenUser *su, int K, double sqrt_beta0) {
+  double m = su[0].xz2;
+  for (int u = 1; u < K; ++u) m = fmin(m, su[u].xz2);
   return scale_of_min_xz2(m, sqrt_beta0);
 }
 __device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int kind, double sqrt_beta0, int lane) {
@@ -632,7 +641,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   uint64_t *tfull = empty + kFStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
-  double4 *su_all = (double4 *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][64]
+  GenUser *su_all = (GenUser *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][64]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = P.K, R = 2 * K;
@@ -667,7 +676,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     // phase (k / 12) & 1; 12 slots for 8 groups let a group start its next stage
     // while the MMA still holds its previous one.
     const int grp = warp / kFGenWarps, gtid = tid - grp * kFGenThreads;
-    double4 *su = su_all + grp * 64;
+    GenUser *su = su_all + grp * 64;
     const double inv_lambda = 1.0 / P.lambda;
     const float inv_lambda_f = (float)inv_lambda;
     const float pitch_f = (float)P.pitch;
@@ -675,7 +684,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     // stage covers elements xs + 64 b .. + 63 (fp16: 64 per 128-B row) in rows rb*b .. rb*b + 2K - 1
     constexpr int kTpr = kFBoxK / TE;      // tasks per user row of a block (4 or 8)
     const int n_tasks = P.nblk * K * kTpr;
-    const int tpb = K * kTpr;              // tasks per block
+    constexpr int kUStep = kFGenThreads / kTpr;  // users a thread's task advances by
+    static_assert(kFGenThreads % kTpr == 0 && kUStep <= 16, "task stepping assumes kTpr | kFGenThreads");
+    const int g8 = gtid % kTpr;
+    int u_first = gtid / kTpr, blk_first = 0;
+    while (u_first >= K) { u_first -= K; ++blk_first; }
     const uint32_t stages_base = smem_u32(stages);
     int64_t kstart = 0;  // global index of the item's first stage
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -692,7 +705,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       for (int u = gtid; u < K; u += kFGenThreads) {
         const double *p = P.pos + (d * K + u) * 3;
         const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
-        su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+        su[u] = GenUser{uc.xz2, uc.y, uc.z, (float)uc.amp, 0.0f};
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
       const float scale = drop_scale(su, K, P.sqrt_beta0);
@@ -703,13 +716,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         const int slot = (int)(k % kFStages);
         const uint32_t slot_base = stages_base + slot * kStageBytes;
         mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
-        // (blk, tb) = divmod(task, tpb), stepped without a division (tpb = 4K >= 36 > 64/2)
-        int blk = gtid / tpb, tb = gtid - blk * tpb;
-        for (int task = gtid; task < n_tasks; task += kFGenThreads, tb += kFGenThreads) {
-          while (tb >= tpb) { tb -= tpb; ++blk; }
-          const int u = tb / kTpr, g8 = tb % kTpr;
+        // task = (blk, u, g8) with task = blk tpb + u kTpr + g8; the stride kFGenThreads is a
+        // multiple of kTpr, so g8 is the thread's constant and u steps by kUStep
+        int u = u_first, blk = blk_first;
+        for (int task = gtid; task < n_tasks; task += kFGenThreads) {
           const int row0 = blk * P.rb + 2 * u;
-          const int64_t t0 = xs + kFBoxK * blk + TE * g8;
+          const int64_t t0 = xs + (kFBoxK * blk + TE * g8);
           uint32_t hr[TE / 2], hi[TE / 2];
 #ifdef XL_EXP_NO_GEN  // tuning experiment: the MMA / epilogue-bound rate (results invalid)
 #pragma unroll
@@ -728,6 +740,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
                          "r"(hi[4 * h]), "r"(hi[4 * h + 1]), "r"(hi[4 * h + 2]), "r"(hi[4 * h + 3])
                          : "memory");
           }
+          u += kUStep;
+          while (u >= K) { u -= K; ++blk; }  // at most twice (kUStep <= 16 < 2K)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
@@ -1106,7 +1120,7 @@ __global__ void __launch_bounds__(256) h_chunk_f16_kernel(const double *pos, int
   uint32_t hr[TE / 2], hi[TE / 2];
   if (u < K) {
     const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
-    const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
+    const GenUser uc{c.xz2, c.y, c.z, (float)c.amp, 0.0f};
     const int64_t t0 = t_first + tile * 64 + TE * g;
     const double inv_lambda = 1.0 / lambda;
     gen_task_h<TE>(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch,
