@@ -391,6 +391,36 @@ __global__ void __launch_bounds__(kThreads, 1) gram_stream_tc_kernel(const __gri
 // amplitude a_c (1 + delta)^{-3/4} ~ a_c (1 - 3/4 delta + 21/32 delta^2); each
 // row chunk of 4 TF32 (RNA) values is one 16-byte store.  Elements are taken in
 // natural spatial order (the sum is order-free; no nested levels on this path).
+// Launch constants of the fp16 task generator (kernel parameters: the constant bank, no
+// registers).  A task's anchor is its centre: ey = (col + y_off) pitch, ez = (row + z_off)
+// pitch with col/row the array indices of its first element.
+struct GenConst {
+  double pitch, inv_lambda;
+  double y_off, z_off;  // (TE - 1)/2 - (n_cols - 1)/2, -(n_rows - 1)/2
+  int64_t N, n_y;       // elements (ULA: the level's N), UPA row length
+  double n_y_d, inv_ny;  // UPA: n_y and 1 / n_y as doubles
+  int kind;
+  float pitch_f, pl, cb0;  // pitch, 2 pi pitch / lambda, pitch pl / 2 (fp32)
+};
+
+inline GenConst make_gen_const(const xlh::ArrayP &a, int64_t N, int TE) {
+  GenConst g;
+  g.pitch = a.pitch;
+  g.inv_lambda = 1.0 / a.lambda;
+  g.kind = a.kind;
+  g.N = N;
+  g.n_y = a.n_y;
+  g.n_y_d = (double)a.n_y;
+  g.inv_ny = 1.0 / (double)a.n_y;
+  const double n_cols = a.kind == XLMIMO_ULA ? (double)N : (double)a.n_y;
+  g.y_off = 0.5 * (TE - 1) - 0.5 * (n_cols - 1.0);
+  g.z_off = a.kind == XLMIMO_ULA ? 0.0 : -0.5 * ((double)a.n_z - 1.0);
+  g.pitch_f = (float)a.pitch;
+  g.pl = 6.28318530717958647692f * g.pitch_f * (float)g.inv_lambda;
+  g.cb0 = 0.5f * g.pitch_f * g.pl;
+  return g;
+}
+
 struct FusedParams {
   const double *pos;
   double *ws;        // partials [drop][chunk][NP][2]
@@ -403,6 +433,7 @@ struct FusedParams {
   int chunk;         // elements per work item (a multiple of kChunk)
   int64_t n_drops;
   uint32_t tmem_cols;
+  GenConst g;        // the generator's launch constants (TE of the instantiation)
 };
 
 // TF32 round-to-nearest, ties away from zero, as integer ALU work (sign-magnitude:
@@ -506,6 +537,11 @@ __device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64
 // to fp16 (round to nearest even: 11 significant bits, the precision of TF32) and packed
 // in pairs, hr[q] = (re h_{2q}, re h_{2q+1}) low half first, hi likewise.  Full tasks
 // (all TE elements < N) skip the per-element padding select.
+// (double)t for 0 <= t < 2^52 without the XU-pipe I2F: t in the mantissa of 2^52, minus 2^52.
+__device__ __forceinline__ double i2d_exact(int64_t t) {
+  return __longlong_as_double(0x4330000000000000LL + t) - 4503599627370496.0;
+}
+
 // A generator's user: the fp64 geometry of xl::UserC and its amplitude sqrt(beta0) sqrt(x_eff)
 // rounded to fp32 once per drop (the coefficient's amplitude is an fp32 product anyway).
 struct __align__(16) GenUser {
@@ -513,70 +549,137 @@ struct __align__(16) GenUser {
   float amp, unused;
 };
 
-template <int TE>
-__device__ __forceinline__ void gen_task_h(const GenUser &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
-                                           int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
-                                           float pitch_f, float scale, uint32_t (&hr)[TE / 2],
-                                           uint32_t (&hi)[TE / 2]) {
-  constexpr double kMid = 0.5 * (TE - 1);
-  double ey, ez = 0.0;
-  if (kind == XLMIMO_ULA) {
-    ey = ((double)t0 + (kMid - 0.5 * (double)(N - 1))) * pitch;
-  } else {  // the task lies in one row (n_y % TE == 0)
-    int64_t q, pp;
-    if (t0 < ((int64_t)1 << 31)) {
-      const uint32_t q32 = (uint32_t)t0 / (uint32_t)n_y;
-      q = q32;
-      pp = (int64_t)((uint32_t)t0 - q32 * (uint32_t)n_y);
-    } else {
-      q = t0 / n_y;
-      pp = t0 - q * n_y;
-    }
-    ey = ((double)pp + (kMid - 0.5 * (double)(n_y - 1))) * pitch;
-    ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
+// A GenUser from shared memory by its shared-window address (LDS, not generic loads).
+__device__ __forceinline__ GenUser lds_user(uint32_t a) {
+  GenUser g;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(g.xz2), "=d"(g.y) : "r"(a));
+  asm volatile("ld.shared.f64 %0, [%1+16];" : "=d"(g.z) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1+24];" : "=f"(g.amp) : "r"(a));
+  g.unused = 0.0f;
+  return g;
+}
+
+// Anchor (task centre) of the task whose first element is t0, branch-free.  UPA tasks lie in
+// one row (n_y % TE == 0): row = floor((t0 + 1/2) / n_y) in fp64 (all values < 2^53, exact
+// after the +-1 fix-up), col = t0 - row n_y.
+template <int KIND>
+__device__ __forceinline__ void task_anchor(const GenConst &g, int64_t t0, double &ey, double &ez) {
+  const double td = i2d_exact(t0);
+  if constexpr (KIND == XLMIMO_ULA) {
+    ey = (td + g.y_off) * g.pitch;
+    ez = 0.0;
+  } else {
+    constexpr double kRnd = 6755399441055744.0;  // 1.5 2^52: x + kRnd - kRnd = rint(x)
+    double row = (fma(td + 0.5, g.inv_ny, -0.5) + kRnd) - kRnd;
+    double col = fma(-row, g.n_y_d, td);
+    if (col < 0.0) { col += g.n_y_d; row -= 1.0; }
+    if (col >= g.n_y_d) { col -= g.n_y_d; row += 1.0; }
+    ey = (col + g.y_off) * g.pitch;
+    ez = (row + g.z_off) * g.pitch;
   }
-  const double dy = ey - uc.y, dz = ez - uc.z;
-  const double r2 = fma(dy, dy, fma(dz, dz, uc.xz2));
-  const double ir = xl::rsqrt_nr(r2);
-  const double rc = r2 * ir;
-  const double qc = rc * inv_lambda;
+}
+
+// One task's expansion about its centre (fm = m - (TE-1)/2, |fm| <= 7.5 for TE = 16):
+//   phase fc + ca fm + cb fm^2 + cg fm^3 + cq fm^4, amplitude a0 + a1 fm + a2 fm^2.
+struct TaskCoef {
+  float fc, ca, cb, cg, cq, a0, a1, a2;
+};
+
+template <int KIND>
+__device__ __forceinline__ TaskCoef task_coef(const GenUser &uc, double ey, double ez, const GenConst &g,
+                                              float scale) {
+  const double dy = ey - uc.y;
+  double r2;
+  if constexpr (KIND == XLMIMO_ULA) {
+    r2 = fma(dy, dy, uc.xz2);
+  } else {
+    const double dz = ez - uc.z;
+    r2 = fma(dy, dy, fma(dz, dz, uc.xz2));
+  }
+  // 1/r: MUFU seed + one Newton step (relative error ~3e-13: ~5e-7 rad of phase at 10^5
+  // wavelengths, far below the fp16 operand's 2^-11)
+  const double ir = xl::rsqrt_newton(r2);
+  const double qc = (r2 * ir) * g.inv_lambda;
+  constexpr double kRnd = 6755399441055744.0;  // qc - rint(qc) on the FP64 pipe (|qc| < 2^51)
+  const double qf = qc - ((qc + kRnd) - kRnd);
   constexpr float k2pi = 6.28318530717958647692f;
-  const float fc = (float)(qc - rint(qc)) * k2pi;
+  TaskCoef c;
+  c.fc = (float)qf * k2pi;
   const float irf = (float)ir, u = (float)(dy * ir);
-  const float w = fmaf(-u, u, 1.0f) * irf;
-  const float pl = k2pi * pitch_f * inv_lambda_f;
-  const float p1 = pitch_f * irf, pp = pitch_f * pl;
-  const float ca = u * pl;
-  const float cb = 0.5f * w * pp;
-  const float cg = -0.5f * u * w * p1 * pp;
-  const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;
+  const float w = fmaf(-u, u, 1.0f) * irf;  // (1 - u^2) / r
+  const float p1 = g.pitch_f * irf;           // pitch / r
+  // pl = 2 pi pitch / lambda, pp = pitch pl:
+  //   ca = u pl, cb = w pp / 2, cg = -u w p1 pp / 2, cq = w (5u^2 - 1) p1^2 pp / 8
+  c.ca = u * g.pl;
+  c.cb = w * g.cb0;
+  c.cg = -u * p1 * c.cb;
+  c.cq = 0.25f * c.cb * fmaf(5.0f * u, u, -1.0f) * (p1 * p1);
   float sq;  // r^{-1/2} from the fp32 1/r (one MUFU, no second double -> float conversion)
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(irf));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(irf));  // irf >= 2^-126: no denormal path
+  // amplitude ac (1 + a1' fm + a2' fm^2): a1' = -3/2 u p1, a2' = 15/8 u^2 p1^2 - 3/4 w p1 pitch
   const float ac = uc.amp * irf * sq * scale;
-  const float a0 = ac;
-  const float a1 = ac * (-1.5f * u * p1);
-  const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
-  auto emit = [&](auto padded, int nv) {
-    float re[2], im[2];
+  c.a0 = ac;
+  const float acp = ac * p1;
+  c.a1 = acp * (-1.5f * u);
+  c.a2 = acp * fmaf(1.875f * u, u * p1, -0.75f * w * g.pitch_f);
+  return c;
+}
+
+// h_m = a(fm) e^{-j phase(fm)} for the TE elements, times the drop scale (in a0..a2), rounded
+// to fp16 (round to nearest even: 11 significant bits, the precision of TF32) and packed in
+// pairs, hr[q] = (re h_{2q}, re h_{2q+1}) low half first, hi likewise.  Elements m and
+// TE-1-m sit at fm = +-f: the even part of the phase E = fc + cb f^2 + cq f^4, the odd slope
+// O = ca + cg f^2 and the even amplitude A = a0 + a2 f^2 are shared, ph = E +- f O,
+// a = A +- f a1 (2.5 + 1.5 FFMA per element instead of the 4 + 2 of two Horner chains).
+template <int TE>
+__device__ __forceinline__ void task_emit(const TaskCoef &c, uint32_t (&hr)[TE / 2], uint32_t (&hi)[TE / 2]) {
+  float re[TE], im[TE];
 #pragma unroll
-    for (int m = 0; m < TE; ++m) {
-      const float fm = (float)m - (float)kMid;
-      const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
-      float sn, co;
-      __sincosf(ph, &sn, &co);
-      float a = fmaf(fmaf(a2, fm, a1), fm, a0);
-      if (decltype(padded)::value) a = (m < nv) ? a : 0.0f;  // padding past N
-      re[m & 1] = a * co;
-      im[m & 1] = -a * sn;
-      if (m & 1) {
-        const __half2 hre = __floats2half2_rn(re[0], re[1]), him = __floats2half2_rn(im[0], im[1]);
-        hr[m >> 1] = *reinterpret_cast<const uint32_t *>(&hre);
-        hi[m >> 1] = *reinterpret_cast<const uint32_t *>(&him);
-      }
+  for (int j = 0; j < TE / 2; ++j) {
+    const float f = (float)j + 0.5f;  // |m - kMid| of the pair (TE/2 - 1 - j, TE/2 + j)
+    const float f2 = f * f;
+    const float E = fmaf(fmaf(c.cq, f2, c.cb), f2, c.fc);
+    const float O = fmaf(c.cg, f2, c.ca);
+    const float A = fmaf(c.a2, f2, c.a0);
+    const int mp = TE / 2 + j, mn = TE / 2 - 1 - j;
+    float sp, cp, sn, cn;
+    __sincosf(fmaf(f, O, E), &sp, &cp);
+    __sincosf(fmaf(-f, O, E), &sn, &cn);
+    const float ap = fmaf(f, c.a1, A), an = fmaf(-f, c.a1, A);
+    re[mp] = ap * cp;
+    im[mp] = -ap * sp;
+    re[mn] = an * cn;
+    im[mn] = -an * sn;
+  }
+#pragma unroll
+  for (int m = 0; m < TE / 2; ++m) {
+    const __half2 hre = __floats2half2_rn(re[2 * m], re[2 * m + 1]);
+    const __half2 him = __floats2half2_rn(im[2 * m], im[2 * m + 1]);
+    hr[m] = *reinterpret_cast<const uint32_t *>(&hre);
+    hi[m] = *reinterpret_cast<const uint32_t *>(&him);
+  }
+}
+
+// Zero the elements m >= nv (past the array's end; only the array's last task has nv < TE).
+template <int TE>
+__device__ __forceinline__ void task_pad(int nv, uint32_t (&hr)[TE / 2], uint32_t (&hi)[TE / 2]) {
+#pragma unroll
+  for (int m = 0; m < TE; ++m)
+    if (m >= nv) {
+      const uint32_t keep = (m & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+      hr[m >> 1] &= keep;
+      hi[m >> 1] &= keep;
     }
-  };
-  if (N - t0 >= TE) emit(std::false_type(), TE);  // every task but the array's last
-  else emit(std::true_type(), (int)(N - t0));
+}
+
+// One whole task: anchor at t0 (first element), nv = elements inside the array.
+template <int TE, int KIND>
+__device__ __forceinline__ void gen_task_h(const GenUser &uc, int64_t t0, int nv, const GenConst &g, float scale,
+                                           uint32_t (&hr)[TE / 2], uint32_t (&hi)[TE / 2]) {
+  double ey, ez;
+  task_anchor<KIND>(g, t0, ey, ez);
+  task_emit<TE>(task_coef<KIND>(uc, ey, ez, g, scale), hr, hi);
+  if (nv < TE) task_pad<TE>(nv, hr, hi);
 }
 
 constexpr int kGenWarps = 2;       // pair kernels: warps per generator group (arrivals per full barrier)
@@ -607,6 +710,9 @@ static_assert(kEpiWarp0 % 4 == 0, "epilogue warp q must sit in TMEM lane quadran
 static_assert(kFGroups <= kFStages, "a generator group may not lap a ring slot (parity waits)");
 
 constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one swizzle atom)
+// byte offset of su_all from the 1024-aligned base: stages, full/empty[kFStages], tfull/tempty[2],
+// the TMEM base word (+16 B), rounded up to 64 B
+constexpr int kFSuOff = (kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 63) & ~63;
 
 // Per-drop power-of-two scale of the fp16 operands: the largest coefficient magnitude of a
 // user is sqrt(beta0) sqrt(x_eff) / x_eff^{3/2} = sqrt(beta0) / sqrt(xz2) (r >= x_eff), so
@@ -631,7 +737,7 @@ __device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int ki
   return scale_of_min_xz2(m, sqrt_beta0);
 }
 
-template <int TE>
+template <int TE, int KIND>
 __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -641,7 +747,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
   uint64_t *tfull = empty + kFStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
-  GenUser *su_all = (GenUser *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][64]
+  GenUser *su_all = (GenUser *)(base + kFSuOff);  // [groups][64], past the TMEM base word
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = P.K, R = 2 * K;
@@ -677,9 +783,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     // while the MMA still holds its previous one.
     const int grp = warp / kFGenWarps, gtid = tid - grp * kFGenThreads;
     GenUser *su = su_all + grp * 64;
-    const double inv_lambda = 1.0 / P.lambda;
-    const float inv_lambda_f = (float)inv_lambda;
-    const float pitch_f = (float)P.pitch;
+    // the same address in the shared window, from the (constant) window offset of smem_raw
+    uint32_t su_s = ((smem_u32(smem_raw) + 1023u) & ~1023u) + (uint32_t)kFSuOff + (uint32_t)grp * 64u * 32u;
+    asm volatile("" : "+r"(su_s));  // opaque: kept in a register, not re-derived per task
     // element blocks stacked in the 128 rows (as in the stream kernel): block b of a
     // stage covers elements xs + 64 b .. + 63 (fp16: 64 per 128-B row) in rows rb*b .. rb*b + 2K - 1
     constexpr int kTpr = kFBoxK / TE;      // tasks per user row of a block (4 or 8)
@@ -709,39 +815,69 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
       const float scale = drop_scale(su, K, P.sqrt_beta0);
+      // A task = (blk, u, g8) with task = blk tpb + u kTpr + g8; the stride kFGenThreads is a
+      // multiple of kTpr, so g8 is the thread's constant and u steps by kUStep.  Software
+      // pipeline: the next task's anchor and coefficients (the serial fp64 chain) are formed in
+      // the same basic block as the current task's phasors, so the chain's latency hides
+      // behind the MUFU work; the next task of a stage's last one is the first of the group's
+      // next stage.
+      auto prep = [&](int64_t xs_, int u_, int blk_, TaskCoef &c_, int &nv_, int &row0_) {
+        const int64_t t0 = xs_ + (kFBoxK * blk_ + TE * g8);
+        double ey, ez;
+        task_anchor<KIND>(P.g, t0, ey, ez);
+        c_ = task_coef<KIND>(lds_user(su_s + 32u * (uint32_t)u_), ey, ez, P.g, scale);
+        const int64_t left = P.N - t0;
+        nv_ = left < TE ? (int)left : TE;
+        row0_ = blk_ * P.rb + 2 * u_;
+      };
+      int64_t xs = x0 + (k - (kstart - ns)) * spb;
+      int u = u_first, blk = blk_first;
+      TaskCoef tc;
+      int nv, row0;
+      prep(xs, u, blk, tc, nv, row0);
       for (; k < kstart; k += kFGroups) {
-        const int64_t xs = x0 + (k - (kstart - ns)) * spb;
         // more slots than groups: a group's next stage reuses a slot freed 4 stages ago,
         // so generation never waits on the MMA of its own previous stage
         const int slot = (int)(k % kFStages);
         const uint32_t slot_base = stages_base + slot * kStageBytes;
         mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
-        // task = (blk, u, g8) with task = blk tpb + u kTpr + g8; the stride kFGenThreads is a
-        // multiple of kTpr, so g8 is the thread's constant and u steps by kUStep
-        int u = u_first, blk = blk_first;
         for (int task = gtid; task < n_tasks; task += kFGenThreads) {
-          const int row0 = blk * P.rb + 2 * u;
-          const int64_t t0 = xs + (kFBoxK * blk + TE * g8);
+          int un = u + kUStep, bn = blk;
+          if (un >= K) { un -= K; ++bn; }
+          if (un >= K) { un -= K; ++bn; }  // at most twice (kUStep <= 16 < 2K)
+          int64_t xsn = xs;
+          if (task + kFGenThreads >= n_tasks) { un = u_first; bn = blk_first; xsn = xs + (int64_t)kFGroups * spb; }
+          TaskCoef cn;
+          int nvn, rown;
+          prep(xsn, un, bn, cn, nvn, rown);
           uint32_t hr[TE / 2], hi[TE / 2];
 #ifdef XL_EXP_NO_GEN  // tuning experiment: the MMA / epilogue-bound rate (results invalid)
 #pragma unroll
-          for (int m = 0; m < TE / 2; ++m) hr[m] = hi[m] = (uint32_t)(t0 + m);
+          for (int m = 0; m < TE / 2; ++m) hr[m] = hi[m] = (uint32_t)(xs + m);
 #else
-          gen_task_h<TE>(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, scale, hr,
-                         hi);
+          task_emit<TE>(tc, hr, hi);
+          if (nv < TE) task_pad<TE>(nv, hr, hi);
 #endif
+          // SWIZZLE_128B: 16-B chunk c of row r at r 128 + ((c ^ (r & 7)) << 4); row0 is even, so
+          // the Im row's key is (row0 & 7) ^ 1, and the task's chunks are c0, c0 ^ 1 (c0 even)
+          const uint32_t rbase = slot_base + (uint32_t)row0 * 128u;
+          const uint32_t key = (uint32_t)((TE / 8) * g8) ^ (uint32_t)(row0 & 7);
 #pragma unroll
           for (int h = 0; h < TE / 8; ++h) {  // 8 fp16 = one 16-B chunk of the 128-B row
-            const int chunk = (TE / 8) * g8 + h;
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0, chunk)),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((key ^ (uint32_t)h) << 4)),
                          "r"(hr[4 * h]), "r"(hr[4 * h + 1]), "r"(hr[4 * h + 2]), "r"(hr[4 * h + 3])
                          : "memory");
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot_base + sw128_off(row0 + 1, chunk)),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                         ::"r"(rbase + 128u + ((key ^ 1u ^ (uint32_t)h) << 4)),
                          "r"(hi[4 * h]), "r"(hi[4 * h + 1]), "r"(hi[4 * h + 2]), "r"(hi[4 * h + 3])
                          : "memory");
           }
-          u += kUStep;
-          while (u >= K) { u -= K; ++blk; }  // at most twice (kUStep <= 16 < 2K)
+          tc = cn;
+          nv = nvn;
+          row0 = rown;
+          u = un;
+          blk = bn;
+          xs = xsn;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
@@ -1104,9 +1240,8 @@ __global__ void __launch_bounds__(256) drop_scale_kernel(const double *pos, int 
 // 32 / (64 / TE) users; lane = (user, TE-element task), one 32-B (TE = 16) or 16-B store
 // per plane.  Padded users (k >= K) and elements past N are 0.
 template <int TE>
-__global__ void __launch_bounds__(256) h_chunk_f16_kernel(const double *pos, int K, int Kr, int kind, int64_t N,
-                                                          int64_t t_first, int64_t n_pad, int64_t n_y, int64_t n_z,
-                                                          double pitch, double lambda, double sqrt_beta0,
+__global__ void __launch_bounds__(256) h_chunk_f16_kernel(const double *pos, int K, int Kr, const GenConst g,
+                                                          int64_t t_first, int64_t n_pad, double sqrt_beta0,
                                                           int64_t drop0, int n_ugrp, const float *scale,
                                                           uint16_t *H) {
   constexpr int LPR = 64 / TE, UPW = 32 / LPR;  // lanes per user row, users per warp
@@ -1114,17 +1249,18 @@ __global__ void __launch_bounds__(256) h_chunk_f16_kernel(const double *pos, int
   const int bd = blockIdx.y / n_ugrp, ug = blockIdx.y - bd * n_ugrp;
   const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
   if (tile * 64 >= n_pad) return;
-  const int u = UPW * ug + lane / LPR, g = lane % LPR;
+  const int u = UPW * ug + lane / LPR, lt = lane % LPR;
   if (u >= Kr) return;
-  uint16_t *row = H + (((size_t)bd * (n_pad / 64) + tile) * (2 * Kr) + 2 * u) * 64 + TE * g;
+  uint16_t *row = H + (((size_t)bd * (n_pad / 64) + tile) * (2 * Kr) + 2 * u) * 64 + TE * lt;
   uint32_t hr[TE / 2], hi[TE / 2];
   if (u < K) {
-    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
+    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, g.kind, sqrt_beta0);
     const GenUser uc{c.xz2, c.y, c.z, (float)c.amp, 0.0f};
-    const int64_t t0 = t_first + tile * 64 + TE * g;
-    const double inv_lambda = 1.0 / lambda;
-    gen_task_h<TE>(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch,
-                   scale[drop0 + bd], hr, hi);
+    const int64_t t0 = t_first + tile * 64 + TE * lt;
+    const int64_t left = g.N - t0;
+    const int nv = left < TE ? (int)left : TE;
+    if (g.kind == XLMIMO_ULA) gen_task_h<TE, XLMIMO_ULA>(uc, t0, nv, g, scale[drop0 + bd], hr, hi);
+    else gen_task_h<TE, XLMIMO_UPA>(uc, t0, nv, g, scale[drop0 + bd], hr, hi);
   } else {
 #pragma unroll
     for (int m = 0; m < TE / 2; ++m) hr[m] = hi[m] = 0u;
@@ -1378,13 +1514,15 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   const int64_t items = n_drops * P.n_chunks;
   const int grid = (int)(items < sms ? items : sms);
   // 16-element tasks wherever a task stays in one array row (every ULA; UPA rows of 16k)
-  if (a.kind == XLMIMO_ULA || a.n_y % 16 == 0) {
-    cudaFuncSetAttribute(gram_fused_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gram_fused_tc_kernel<16><<<grid, kFusedThreads, smem, s>>>(P);
-  } else {
-    cudaFuncSetAttribute(gram_fused_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gram_fused_tc_kernel<8><<<grid, kFusedThreads, smem, s>>>(P);
-  }
+  const bool te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
+  P.g = make_gen_const(a, N, te16 ? 16 : 8);
+  auto run = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kFusedThreads, smem, s>>>(P);
+  };
+  if (a.kind == XLMIMO_ULA) run(gram_fused_tc_kernel<16, XLMIMO_ULA>);
+  else if (te16) run(gram_fused_tc_kernel<16, XLMIMO_UPA>);
+  else run(gram_fused_tc_kernel<8, XLMIMO_UPA>);
   return check_launch("gram_fused_tc_kernel");
 }
 
@@ -1475,13 +1613,13 @@ int launch_stream_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_d
         const int upw = te16 ? 8 : 4;
         const int n_ugrp = (u.Kp + upw - 1) / upw;
         const dim3 grid((unsigned)((n_pad + 511) / 512), (unsigned)(nd * n_ugrp));
-        const int64_t nz = a.kind == XLMIMO_ULA ? 1 : a.n_z;
+        const GenConst g = make_gen_const(a, N, te16 ? 16 : 8);
         if (te16)
-          h_chunk_f16_kernel<16><<<grid, 256, 0, s>>>(pos, K, u.Kp, a.kind, N, (int64_t)c0 * kPChunk, n_pad, a.n_y,
-                                                      nz, a.pitch, a.lambda, a.sqrt_beta0, d0, n_ugrp, scale, H);
+          h_chunk_f16_kernel<16><<<grid, 256, 0, s>>>(pos, K, u.Kp, g, (int64_t)c0 * kPChunk, n_pad, a.sqrt_beta0,
+                                                      d0, n_ugrp, scale, H);
         else
-          h_chunk_f16_kernel<8><<<grid, 256, 0, s>>>(pos, K, u.Kp, a.kind, N, (int64_t)c0 * kPChunk, n_pad, a.n_y,
-                                                     nz, a.pitch, a.lambda, a.sqrt_beta0, d0, n_ugrp, scale, H);
+          h_chunk_f16_kernel<8><<<grid, 256, 0, s>>>(pos, K, u.Kp, g, (int64_t)c0 * kPChunk, n_pad, a.sqrt_beta0,
+                                                     d0, n_ugrp, scale, H);
         tm.stop(s);
         count_launch();
       }
