@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
+#include <type_traits>
 
 #include "xl_common.cuh"
 
@@ -549,6 +550,13 @@ struct __align__(16) GenUser {
   float amp, unused;
 };
 
+// fp32 of a positive normal double whose exponent fits fp32 (truncated mantissa): the
+// exponent field moves down by 1023 - 127 in modular 32-bit arithmetic (2 integer ops).
+__device__ __forceinline__ float f64_trunc_f32(double x) {
+  const uint32_t b = __funnelshift_l((uint32_t)__double2loint(x), (uint32_t)__double2hiint(x), 3);
+  return __uint_as_float(b - (896u << 23));
+}
+
 // A GenUser from shared memory by its shared-window address (LDS, not generic loads).
 __device__ __forceinline__ GenUser lds_user(uint32_t a) {
   GenUser g;
@@ -604,8 +612,11 @@ __device__ __forceinline__ TaskCoef task_coef(const GenUser &uc, double ey, doub
   const double qf = qc - ((qc + kRnd) - kRnd);
   constexpr float k2pi = 6.28318530717958647692f;
   TaskCoef c;
-  c.fc = (float)qf * k2pi;
-  const float irf = (float)ir, u = (float)(dy * ir);
+  // fp64 -> fp32 without the XU-pipe F2F: qf + 1.5 and u + 3 lie in [1, 2] and [2, 4] (fixed
+  // binade, + half a float ulp so the truncation rounds), 1/r is a normal float
+  c.fc = fmaf(f64_trunc_f32(qf + (1.5 + 0x1p-24)), k2pi, -1.5f * k2pi);
+  const float irf = f64_trunc_f32(ir);
+  const float u = f64_trunc_f32(fma(dy, ir, 3.0 + 0x1p-23)) - 3.0f;
   const float w = fmaf(-u, u, 1.0f) * irf;  // (1 - u^2) / r
   const float p1 = g.pitch_f * irf;           // pitch / r
   // pl = 2 pi pitch / lambda, pp = pitch pl:
@@ -793,8 +804,24 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     constexpr int kUStep = kFGenThreads / kTpr;  // users a thread's task advances by
     static_assert(kFGenThreads % kTpr == 0 && kUStep <= 16, "task stepping assumes kTpr | kFGenThreads");
     const int g8 = gtid % kTpr;
-    int u_first = gtid / kTpr, blk_first = 0;
-    while (u_first >= K) { u_first -= K; ++blk_first; }
+    // The thread's tasks of a stage (the same every stage): task = (blk, u, g8) with
+    // task = blk tpb + u kTpr + g8 for task = gtid, gtid + kFGenThreads, ...; the stride is a
+    // multiple of kTpr, so g8 is the thread's constant.  Byte j of tdesc = u | blk << 6 of its
+    // j-th task; n_my <= n_tasks / kFGenThreads <= 4 (TE = 16) or 8 (TE = 8) since nblk K <= 64.
+    using Desc = typename std::conditional<kTpr <= 4, uint32_t, uint64_t>::type;  // n_my <= kTpr bytes
+    Desc tdesc = 0;
+    int n_my = 0;
+    {
+      int u = gtid / kTpr, blk = 0;
+      while (u >= K) { u -= K; ++blk; }
+      for (int task = gtid; task < n_tasks; task += kFGenThreads, ++n_my) {
+        tdesc |= (Desc)(u | (blk << 6)) << (8 * n_my);
+        u += kUStep;
+        while (u >= K) { u -= K; ++blk; }
+      }
+    }
+    const uint32_t code0 = (uint32_t)tdesc & 0xFFu;
+    const Desc rest0 = tdesc >> 8;
     const uint32_t stages_base = smem_u32(stages);
     int64_t kstart = 0;  // global index of the item's first stage
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -821,7 +848,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       // the same basic block as the current task's phasors, so the chain's latency hides
       // behind the MUFU work; the next task of a stage's last one is the first of the group's
       // next stage.
-      auto prep = [&](int64_t xs_, int u_, int blk_, TaskCoef &c_, int &nv_, int &row0_) {
+      auto prep = [&](int64_t xs_, uint32_t code, TaskCoef &c_, int &nv_, int &row0_) {
+        const int u_ = (int)(code & 63u), blk_ = (int)(code >> 6);
         const int64_t t0 = xs_ + (kFBoxK * blk_ + TE * g8);
         double ey, ez;
         task_anchor<KIND>(P.g, t0, ey, ez);
@@ -831,25 +859,24 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         row0_ = blk_ * P.rb + 2 * u_;
       };
       int64_t xs = x0 + (k - (kstart - ns)) * spb;
-      int u = u_first, blk = blk_first;
       TaskCoef tc;
       int nv, row0;
-      prep(xs, u, blk, tc, nv, row0);
+      prep(xs, code0, tc, nv, row0);
       for (; k < kstart; k += kFGroups) {
         // more slots than groups: a group's next stage reuses a slot freed 4 stages ago,
         // so generation never waits on the MMA of its own previous stage
         const int slot = (int)(k % kFStages);
         const uint32_t slot_base = stages_base + slot * kStageBytes;
         mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
-        for (int task = gtid; task < n_tasks; task += kFGenThreads) {
-          int un = u + kUStep, bn = blk;
-          if (un >= K) { un -= K; ++bn; }
-          if (un >= K) { un -= K; ++bn; }  // at most twice (kUStep <= 16 < 2K)
-          int64_t xsn = xs;
-          if (task + kFGenThreads >= n_tasks) { un = u_first; bn = blk_first; xsn = xs + (int64_t)kFGroups * spb; }
+        Desc rest = rest0;  // codes of the tasks after the current one
+        for (int j = n_my; j > 0; --j) {
+          const bool last = j == 1;  // the next task is the first of the group's next stage
+          const uint32_t code_n = last ? code0 : (uint32_t)rest & 0xFFu;
+          rest >>= 8;
+          const int64_t xsn = last ? xs + (int64_t)kFGroups * spb : xs;
           TaskCoef cn;
           int nvn, rown;
-          prep(xsn, un, bn, cn, nvn, rown);
+          prep(xsn, code_n, cn, nvn, rown);
           uint32_t hr[TE / 2], hi[TE / 2];
 #ifdef XL_EXP_NO_GEN  // tuning experiment: the MMA / epilogue-bound rate (results invalid)
 #pragma unroll
@@ -875,8 +902,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
           tc = cn;
           nv = nvn;
           row0 = rown;
-          u = un;
-          blk = bn;
           xs = xsn;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
