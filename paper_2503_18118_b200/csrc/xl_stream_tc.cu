@@ -458,75 +458,6 @@ __device__ __forceinline__ void st_v8(float *p, const uint32_t (&v)[8]) {  // 32
                : "memory");
 }
 
-// One generator task: the TF32 (RNA) coefficients h = a e^{-j 2 pi r / lambda} (Eq. 3) of
-// one user at kTaskE consecutive elements (natural order) t0 .. t0 + 7 (offset d = m pitch
-// along y), from an fp64 anchor at t0: distance r_c, phase reduced as frac(r_c / lambda)
-// in fp64, and the Taylor coefficients of r(d) = sqrt(r_c^2 + 2 dy d + d^2) about d = 0,
-//   r = r_c + u d + (w/2) d^2 - (u w / (2 r_c)) d^3 + (w (5u^2 - 1) / (8 r_c^2)) d^4,
-//   u = dy / r_c,  w = (1 - u^2) / r_c,
-// turned into a quartic in m for the phase and a quadratic for the amplitude
-// a_c (r / r_c)^{-3/2}.  fp64 is kept where the phase needs it -- r_c (1/r to ~1 ulp) and
-// the reduction frac(r_c / lambda) -- and the Taylor coefficients follow in fp32 from u,
-// 1/r_c and r_c (relative 1e-7: < 4e-7 rad at m = 7).  The phase is carried in radians,
-// unreduced past the anchor: |phase| <= pi (1 + 2 pitch/lambda m) < 9 pi, which MUFU
-// sin/cos take directly (their own revolution reduction costs < 1e-6 rad here, far inside
-// the TF32 rounding).  Per element: 4 FFMA, the MUFU pre-scale, 2 MUFU, 2 FFMA + 2 FMUL
-// of amplitude and the integer RNA rounding.  Truncation over 7 pitches at 100 GHz:
-// phase d^5/r^4 ~ 7e-7 cycles even at r_c = 0.3 m (the cubic alone left 4e-5 cycles of
-// systematic error there), amplitude O((d/r)^3) ~ 4e-5 at 0.3 m (fp32 tier 1e-4).
-// Elements past N are 0.  uc = (x^2 + z^2 or x^2, y, z, sqrt(beta0) sqrt(x_eff)).
-__device__ __forceinline__ void gen_task_tf32(const double4 &uc, int kind, int64_t t0, int64_t N, int64_t n_y,
-                                              int64_t n_z, double pitch, double inv_lambda, float inv_lambda_f,
-                                              float pitch_f, uint32_t (&vr)[kTaskE], uint32_t (&vi)[kTaskE]) {
-  double ey, ez = 0.0;
-  if (kind == XLMIMO_ULA) {
-    ey = ((double)t0 - 0.5 * (double)(N - 1)) * pitch;
-  } else {
-    int64_t q, pp;
-    if (t0 < ((int64_t)1 << 31)) {  // 32-bit division (a 64-bit one is a long software sequence)
-      const uint32_t q32 = (uint32_t)t0 / (uint32_t)n_y;
-      q = q32;
-      pp = (int64_t)((uint32_t)t0 - q32 * (uint32_t)n_y);
-    } else {
-      q = t0 / n_y;
-      pp = t0 - q * n_y;
-    }
-    ey = ((double)pp - 0.5 * (double)(n_y - 1)) * pitch;
-    ez = ((double)q - 0.5 * (double)(n_z - 1)) * pitch;
-  }
-  const double dy = ey - uc.y, dz = ez - uc.z;
-  const double r2 = fma(dy, dy, fma(dz, dz, uc.x));
-  const double ir = xl::rsqrt_nr(r2);
-  const double rc = r2 * ir;
-  const double qc = rc * inv_lambda;
-  constexpr float k2pi = 6.28318530717958647692f;
-  const float fc = (float)(qc - rint(qc)) * k2pi;  // anchor phase, radians in [-pi, pi]
-  const float irf = (float)ir, u = (float)(dy * ir);
-  const float w = fmaf(-u, u, 1.0f) * irf;
-  const float pl = k2pi * pitch_f * inv_lambda_f;  // radians per pitch of path length
-  const float p1 = pitch_f * irf, pp = pitch_f * pl;
-  const float ca = u * pl;                                             // linear
-  const float cb = 0.5f * w * pp;                                      // quadratic
-  const float cg = -0.5f * u * w * p1 * pp;                            // cubic
-  const float cq = 0.125f * w * fmaf(5.0f * u, u, -1.0f) * p1 * p1 * pp;  // quartic
-  const float ac = (float)uc.w * irf * rsqrtf((float)rc);              // a_c = amp r_c^{-3/2}
-  // (r / r_c)^{-3/2} = 1 - 3/2 D + 15/8 D^2, D = (r - r_c) / r_c = u p1 m + (w/2) p1 pitch m^2
-  const float a0 = ac;
-  const float a1 = ac * (-1.5f * u * p1);
-  const float a2 = ac * fmaf(-0.75f * w * p1, pitch_f, 1.875f * u * u * p1 * p1);
-  const int64_t nv64 = N - t0;  // valid elements of this task (padding past N is 0)
-  const int nv = nv64 < kTaskE ? (int)nv64 : kTaskE;
-#pragma unroll
-  for (int m = 0; m < kTaskE; ++m) {
-    const float fm = (float)m;
-    const float ph = fmaf(fmaf(fmaf(fmaf(cq, fm, cg), fm, cb), fm, ca), fm, fc);
-    float sn, co;
-    __sincosf(ph, &sn, &co);
-    const float a = (m < nv) ? fmaf(fmaf(a2, fm, a1), fm, a0) : 0.0f;
-    vr[m] = tf32_rna(a * co);
-    vi[m] = tf32_rna(-a * sn);
-  }
-}
 
 
 // The fused kernel's generator task: TE (8 or 16) consecutive elements t0 .. t0 + TE - 1 of
@@ -691,6 +622,39 @@ __device__ __forceinline__ void gen_task_h(const GenUser &uc, int64_t t0, int nv
   task_anchor<KIND>(g, t0, ey, ez);
   task_emit<TE>(task_coef<KIND>(uc, ey, ez, g, scale), hr, hi);
   if (nv < TE) task_pad<TE>(nv, hr, hi);
+}
+
+// The same expansion with fp32 outputs rounded to TF32 (round to nearest, ties away:
+// tf32_rna) for the TF32 kernels, element m = 0..TE-1 in vr[m], vi[m]; elements m >= nv
+// (past the array's end) are 0.
+template <int TE>
+__device__ __forceinline__ void task_emit_tf32(const TaskCoef &c, int nv, uint32_t (&vr)[TE], uint32_t (&vi)[TE]) {
+#pragma unroll
+  for (int j = 0; j < TE / 2; ++j) {
+    const float f = (float)j + 0.5f;
+    const float f2 = f * f;
+    const float E = fmaf(fmaf(c.cq, f2, c.cb), f2, c.fc);
+    const float O = fmaf(c.cg, f2, c.ca);
+    const float A = fmaf(c.a2, f2, c.a0);
+    const int mp = TE / 2 + j, mn = TE / 2 - 1 - j;
+    float sp, cp, sn, cn;
+    __sincosf(fmaf(f, O, E), &sp, &cp);
+    __sincosf(fmaf(-f, O, E), &sn, &cn);
+    const float ap = mp < nv ? fmaf(f, c.a1, A) : 0.0f;
+    const float an = mn < nv ? fmaf(-f, c.a1, A) : 0.0f;
+    vr[mp] = tf32_rna(ap * cp);
+    vi[mp] = tf32_rna(-ap * sp);
+    vr[mn] = tf32_rna(an * cn);
+    vi[mn] = tf32_rna(-an * sn);
+  }
+}
+
+template <int TE, int KIND>
+__device__ __forceinline__ void gen_task_tf32(const GenUser &uc, int64_t t0, int nv, const GenConst &g,
+                                              uint32_t (&vr)[TE], uint32_t (&vi)[TE]) {
+  double ey, ez;
+  task_anchor<KIND>(g, t0, ey, ez);
+  task_emit_tf32<TE>(task_coef<KIND>(uc, ey, ez, g, 1.0f), nv, vr, vi);
 }
 
 constexpr int kGenWarps = 2;       // pair kernels: warps per generator group (arrivals per full barrier)
@@ -1017,6 +981,7 @@ struct FusedPairParams {
   double lambda, pitch, sqrt_beta0;
   int n_chunks;
   int64_t n_drops;
+  GenConst g;        // the generator's launch constants (TE = kTaskE)
 };
 
 // stages (32 elements each) of pair-kernel chunk c (kPChunk elements, fewer in the last)
@@ -1041,7 +1006,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
   uint64_t *tfull = empty + kPSlots;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
-  double4 *su_all = (double4 *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][128]
+  GenUser *su_all = (GenUser *)(((uintptr_t)(tmem_base_sh + 4) + 63) & ~(uintptr_t)63);  // [groups][128]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = P.K;
@@ -1076,10 +1041,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
     // (6 groups for 6 slots of 32 KB: more groups could lap a slot and pass a parity wait
     // one phase early)
     const int grp = warp / kGenWarps, gtid = tid - grp * kGenThreads;
-    double4 *su = su_all + grp * (2 * kPUsers);
-    const double inv_lambda = 1.0 / P.lambda;
-    const float inv_lambda_f = (float)inv_lambda;
-    const float pitch_f = (float)P.pitch;
+    GenUser *su = su_all + grp * (2 * kPUsers);
     const uint32_t stages_base = smem_u32(stages);
     int64_t kstart = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -1100,9 +1062,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
         const int gu = (u < kPUsers ? bi : bj) * kPUsers + (u & (kPUsers - 1));
         if (gu < K) {
           const xl::UserC uc = xl::make_user(P.pos + (d * K + gu) * 3, P.kind, P.sqrt_beta0);
-          su[u] = make_double4(uc.xz2, uc.y, uc.z, uc.amp);
+          su[u] = GenUser{uc.xz2, uc.y, uc.z, (float)uc.amp, 0.0f};
         } else {
-          su[u] = make_double4(1.0, 0.0, 0.0, 0.0);  // padded user: amplitude 0
+          su[u] = GenUser{1.0, 0.0, 0.0, 0.0f, 0.0f};  // padded user: amplitude 0
         }
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGenThreads) : "memory");
@@ -1117,7 +1079,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
           const int row0 = 2 * u;
           const int64_t t0 = xs + kTaskE * g8;
           uint32_t vr[kTaskE], vi[kTaskE];
-          gen_task_tf32(su[u], P.kind, t0, P.N, P.n_y, P.n_z, P.pitch, inv_lambda, inv_lambda_f, pitch_f, vr, vi);
+          const int64_t left = P.N - t0;
+          const int nv = left < kTaskE ? (int)left : kTaskE;
+          if (P.kind == XLMIMO_ULA) gen_task_tf32<kTaskE, XLMIMO_ULA>(su[u], t0, nv, P.g, vr, vi);
+          else gen_task_tf32<kTaskE, XLMIMO_UPA>(su[u], t0, nv, P.g, vr, vi);
 #pragma unroll
           for (int h = 0; h < kTaskE / 4; ++h) {
             const int chunk = (kTaskE / 4) * g8 + h;
@@ -1214,38 +1179,42 @@ __global__ void __launch_bounds__(kPairThreads, 1) gram_fused_tc_pair_kernel(Fus
 // (user u = lane / 4, elements 8 (lane % 4) .. +7), so each lane stores 2 x 32 B and a
 // warp writes sixteen full 128-B rows.  Block = 8 warps = 8 consecutive tiles; grid =
 // (ceil(N_pad / 256), batch drops x ceil(K / 8) user groups).  Elements past N are 0.
-__global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos, int K, int Kr, int kind, int64_t N,
-                                                               int64_t t_first, int64_t n_pad, int64_t n_y,
-                                                               int64_t n_z, double pitch, double lambda,
-                                                               double sqrt_beta0, int64_t drop0, int n_ugrp, float *H,
-                                                               int l2_keep) {
+template <int TE, int KIND>
+__global__ void __launch_bounds__(256) h_materialise_tc_kernel(const double *pos, int K, int Kr, const GenConst g,
+                                                               int64_t t_first, int64_t n_pad, double sqrt_beta0,
+                                                               int64_t drop0, int n_ugrp, float *H, int l2_keep) {
+  constexpr int LPR = 32 / TE, UPW = 32 / LPR;  // lanes per 32-element row, users per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bd = blockIdx.y / n_ugrp, ug = blockIdx.y - bd * n_ugrp;
   const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
   if (tile * 32 >= n_pad) return;
-  const int u = 8 * ug + (lane >> 2);
+  const int u = UPW * ug + lane / LPR, lt = lane % LPR;
   if (u >= Kr) return;
-  float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * Kr) + 2 * u) * 32 + 8 * (lane & 3);
-  uint32_t vr[kTaskE], vi[kTaskE];
+  float *row = H + (((size_t)bd * (n_pad / 32) + tile) * (2 * Kr) + 2 * u) * 32 + TE * lt;
+  uint32_t vr[TE], vi[TE];
   if (u < K) {
-    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, kind, sqrt_beta0);
-    const double4 uc = make_double4(c.xz2, c.y, c.z, c.amp);
-    const int64_t t0 = t_first + tile * 32 + 8 * (lane & 3);
-    const double inv_lambda = 1.0 / lambda;
-    gen_task_tf32(uc, kind, t0, N, n_y, n_z, pitch, inv_lambda, (float)inv_lambda, (float)pitch, vr, vi);
+    const xl::UserC c = xl::make_user(pos + ((drop0 + bd) * K + u) * 3, KIND, sqrt_beta0);
+    const int64_t t0 = t_first + tile * 32 + TE * lt;
+    const int64_t left = g.N - t0;
+    gen_task_tf32<TE, KIND>(GenUser{c.xz2, c.y, c.z, (float)c.amp, 0.0f}, t0, left < TE ? (int)left : TE, g, vr,
+                            vi);
   } else {  // padded user row (the pair stream reads whole 64-user blocks)
 #pragma unroll
-    for (int m = 0; m < kTaskE; ++m) vr[m] = vi[m] = 0u;
+    for (int m = 0; m < TE; ++m) vr[m] = vi[m] = 0u;
   }
-  // one 256-bit store per plane and lane: every warp store fills whole 32-byte sectors
-  // (two 128-bit stores left half-sector gaps per instruction); evict-first for the
-  // HBM stream, default for an L2-sized chunk that is read back at once (the pair stream)
-  if (l2_keep) {
-    st_v8(row, vr);
-    st_v8(row + 32, vi);
-  } else {
-    st_cs_v8(row, vr);
-    st_cs_v8(row + 32, vi);
+  // 256-bit stores (per plane TE / 8 of them, a lane's sectors whole): evict-first for the HBM
+  // stream, default for an L2-sized chunk that is read back at once (the pair stream)
+#pragma unroll
+  for (int h = 0; h < TE / 8; ++h) {
+    const uint32_t(&r8)[8] = *reinterpret_cast<const uint32_t(*)[8]>(vr + 8 * h);
+    const uint32_t(&i8)[8] = *reinterpret_cast<const uint32_t(*)[8]>(vi + 8 * h);
+    if (l2_keep) {
+      st_v8(row + 8 * h, r8);
+      st_v8(row + 32 + 8 * h, i8);
+    } else {
+      st_cs_v8(row + 8 * h, r8);
+      st_cs_v8(row + 32 + 8 * h, i8);
+    }
   }
 }
 
@@ -1561,11 +1530,21 @@ bool materialise_tc_supported(const ArrayP &a) { return a.kind == XLMIMO_ULA || 
 int launch_h_materialise_tc(const ArrayP &a, const double *pos, int K, int64_t N, int64_t n_pad, int64_t drop0,
                             int nb, float *H, cudaStream_t s, int Kr, int64_t t_first, int l2_keep) {
   if (Kr < K) Kr = K;
-  const int n_ugrp = (Kr + 7) / 8;
+  // 16-element tasks (16 users per warp) wherever a task stays in one array row
+  const bool te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
+  const int upw = te16 ? 16 : 8;
+  const int n_ugrp = (Kr + upw - 1) / upw;
   const dim3 grid((unsigned)((n_pad + 255) / 256), (unsigned)(nb * n_ugrp));
-  h_materialise_tc_kernel<<<grid, 256, 0, s>>>(pos, K, Kr, a.kind, N, t_first, n_pad, a.n_y,
-                                               a.kind == XLMIMO_ULA ? 1 : a.n_z, a.pitch, a.lambda, a.sqrt_beta0,
-                                               drop0, n_ugrp, H, l2_keep);
+  const GenConst g = make_gen_const(a, N, te16 ? 16 : kTaskE);
+  if (a.kind == XLMIMO_ULA)
+    h_materialise_tc_kernel<16, XLMIMO_ULA><<<grid, 256, 0, s>>>(pos, K, Kr, g, t_first, n_pad, a.sqrt_beta0, drop0,
+                                                                  n_ugrp, H, l2_keep);
+  else if (te16)
+    h_materialise_tc_kernel<16, XLMIMO_UPA><<<grid, 256, 0, s>>>(pos, K, Kr, g, t_first, n_pad, a.sqrt_beta0, drop0,
+                                                                  n_ugrp, H, l2_keep);
+  else
+    h_materialise_tc_kernel<kTaskE, XLMIMO_UPA><<<grid, 256, 0, s>>>(pos, K, Kr, g, t_first, n_pad, a.sqrt_beta0,
+                                                                      drop0, n_ugrp, H, l2_keep);
   return check_launch("h_materialise_tc_kernel");
 }
 
@@ -1696,6 +1675,7 @@ int launch_fused_tc_pair(const ArrayP &a, const double *pos, int K, int64_t n_dr
   P.sqrt_beta0 = a.sqrt_beta0;
   P.n_chunks = fused_tc_pair_chunks(N);
   P.n_drops = n_drops;
+  P.g = make_gen_const(a, N, kTaskE);
   const size_t smem = 1024 + (size_t)kPSlots * kPSlotBytes + (2 * kPSlots + 4) * 8 + 16 + 64 +
                       (size_t)kPGroups * 2 * kPUsers * 32;
   cudaFuncSetAttribute(gram_fused_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
