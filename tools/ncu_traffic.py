@@ -1,6 +1,8 @@
 """Extract per-launch DRAM traffic of captured kernels into the JSON bench.py reads.
 
-    python tools/ncu_traffic.py OUT.json REPORT.ncu-rep:KERNEL_KEY:LAUNCH_KEY[:DROPS] ...
+    python tools/ncu_traffic.py [--merge] OUT.json REPORT.ncu-rep:KERNEL_KEY:LAUNCH_KEY[:DROPS] ...
+
+--merge keeps OUT.json's entries for other (KERNEL_KEY, LAUNCH_KEY) pairs.
 
 KERNEL_KEY is the library's timer name for the kernel (the name bench.py's roofline
 carries), LAUNCH_KEY the bench launch it stands for (e.g. "cfg5 fp64 D=1000"), DROPS the
@@ -33,8 +35,12 @@ def metrics(path):
 
 
 def main():
+    args = sys.argv[1:]
+    merge = args[0] == "--merge"
+    if merge:
+        args = args[1:]
     out = []
-    for spec in sys.argv[2:]:
+    for spec in args[1:]:
         parts = spec.split(":")
         path, kname, key = parts[0], parts[1], parts[2]
         e = {"kernel": kname, "launch_key": key, "report": path.split("/")[-1]}
@@ -42,7 +48,14 @@ def main():
             e["drops"] = int(parts[3])
         e.update(metrics(path))
         out.append(e)
-    json.dump(out, open(sys.argv[1], "w"), indent=1)
+    if merge:
+        try:
+            old = json.load(open(args[0]))
+        except FileNotFoundError:
+            old = []
+        new_keys = {(e["kernel"], e["launch_key"]) for e in out}
+        out = [e for e in old if (e["kernel"], e["launch_key"]) not in new_keys] + out
+    json.dump(out, open(args[0], "w"), indent=1)
     print(json.dumps(out, indent=1))
 
 

@@ -1,0 +1,30 @@
+#!/bin/bash
+# Round-end evidence on the GPU box: GPU tests, smoke, bench (+ reference arm), the bench's
+# launch list and ncu --set full digests / DRAM traffic of the kernels that changed.
+#   bash tools/refresh_profiles.sh OUTDIR   (under gpurun_out/, merged back by gpurun)
+set -x
+O=${1:-gpurun_out/refresh}; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > $O/pytest_gpu.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+cap() { # tag cfg prec drops regex
+  python tools/prof_gram.py $2 $3 $4 > $O/plain_$1.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$5 -s 1 -c 1 -o $O/$1 -f \
+      python tools/prof_gram.py $2 $3 $4 > $O/ncu_$1.log 2>&1
+  python tools/ncu_summary.py $O/$1.ncu-rep > $O/ncu_full_$1.txt 2>&1
+  python tools/ncu_hot.py $O/$1.ncu-rep 40 > $O/ncu_hot_$1.txt 2>&1
+  python tools/ncu_lines.py $O/$1.ncu-rep 40 > $O/ncu_lines_$1.txt 2>&1
+}
+cap ftc_cfg5_d1000 5 fp32 1000 gram_fused_tc
+cap writer_cfg5 5 mat32 16 h_materialise
+cap ftc_cfg3 3 fp32 10000 gram_fused_tc
+cp profiles/r02/ncu_traffic_bench.json $O/ncu_traffic_bench.json
+python tools/ncu_traffic.py --merge $O/ncu_traffic_bench.json \
+  $O/ftc_cfg5_d1000.ncu-rep:gram_fused_tc_f16:"cfg5 fp32 D=1000":1000 \
+  $O/writer_cfg5.ncu-rep:h_materialise:"cfg5 mat32 writer":16 > $O/traffic.log 2>&1
+rm -f $O/*.ncu-rep
+cp $O/ncu_traffic_bench.json profiles/r02/ncu_traffic_bench.json  # the box's copy: bench reads it
+timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+timeout 900 python bench.py --steps 2 --warmup 1 --no-sub --no-cpu-baseline > $O/plain_launch.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv \
+      python bench.py --steps 2 --warmup 1 --no-sub --no-cpu-baseline > $O/ncu_launch.log 2>&1
