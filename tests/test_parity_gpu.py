@@ -503,3 +503,21 @@ def test_gram_warp_kernel(xl, orc, kind, n_y, n_z, K, D):
     assert normalized_err(G[idx], Go) <= 1e-9
     assert np.array_equal(G, np.conj(np.swapaxes(G, 1, 2)))
     assert np.all(np.imag(np.diagonal(G, axis1=1, axis2=2)) == 0)
+
+
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 100003, 1, 24, 600), ("upa", 40, 2500, 12, 600),
+                                              ("upa", 48, 2083, 40, 300)])
+def test_fused_fp32_long_chunks(xl, orc, kind, n_y, n_z, K, D):
+    """The fused fp32 kernel at launch sizes that give it long work items (its adaptive chunk:
+    the longest of 8K..64K elements leaving >= 4 waves, here 32K / 64K with a ragged last
+    item), on 16- and 8-element tasks (UPA rows of 40 elements: TE = 8) -- every entry of
+    sampled drops against the oracle at the fp32 tier (1e-4 normalised, R9)."""
+    a, ao = _arr(xl, orc, kind, n_y, n_z, 100e9)
+    u, _ = _users(xl, orc, (2.0, 20.0), (-60.0, 60.0), (-30.0, 30.0) if kind == "upa" else (0.0, 0.0))
+    pos = xl.gen_drops(u, K, D, seed=17)
+    G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+    pick = [0, D // 2, D - 1]
+    Go = orc.gram_exact_blas(ao, pos.cpu().numpy()[pick])
+    assert normalized_err(G[pick], Go) <= 1e-4
+    for d in pick:
+        assert np.array_equal(G[d], np.conj(G[d].T))
