@@ -854,6 +854,14 @@ template <> struct Mt2Cfg<13> { static constexpr int JPW = 7, SG = 1, S = 4; }; 
 template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 15 stars
 template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
 
+// Tile planes: re, im and re - im, the 3M partner operand (A_p - B_p), formed once per
+// coefficient by the generator instead of once per star and step by the consumers (the
+// DADDs waited on the busy FP64 pipe: cfg5 196.6 -> 189.2 ms per 296 drops, cfg4 -1.9 %,
+// K = 72 / 100 / 120 -3.8 / -2.3 / -0.4 %, bit-identical).  XL_MT2_DPLANE=0: two planes.
+#ifndef XL_MT2_DPLANE
+#define XL_MT2_DPLANE 1
+#endif
+constexpr int kMt2Planes = XL_MT2_DPLANE ? 3 : 2;
 template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::S; NBUF tile buffers
 struct Mt2 {
   static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
@@ -861,10 +869,11 @@ struct Mt2 {
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
   static_assert(J % JPW == 0 && S % SG == 0, "Mt2Cfg");
-  static constexpr size_t tiles_bytes = 2ull * NBUF * PLANE * sizeof(double);  // NBUF buffers x re/im
+  static constexpr int NPL = kMt2Planes;  // re, im (, re - im: the 3M partner operand)
+  static constexpr size_t tiles_bytes = (size_t)NPL * NBUF * PLANE * sizeof(double);  // NBUF buffers x planes
   static constexpr size_t stage_bytes = (size_t)J * 3 * SG * 64 * sizeof(double);
   static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
-  static_assert(smem <= 220 * 1024, "Mt2 shared memory");
+  static constexpr bool fits = smem <= 220 * 1024;
 };
 
 // Star plan of the MT2 kernel: star s (warp's job group) = centre cen[s] and partners
@@ -991,7 +1000,7 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     // (a UPA decode costs 4 FP64 ops, a ULA one 2: otherwise repeated for every group)
     constexpr int R = (ROWS + NW - 1) / NW;
     auto generate = [&](int t0, int buf) {
-      double *gre = dsm + buf * (2 * PLANE), *gim = gre + PLANE;
+      double *gre = dsm + buf * (C::NPL * PLANE), *gim = gre + PLANE;
       int s_cur = -1;
       bool valid = false;
       ElemPos ep;
@@ -1021,11 +1030,12 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
 #endif
           gre[row * 32 + lane] = hr;
           gim[row * 32 + lane] = hi;
+          if constexpr (C::NPL == 3) gim[PLANE + row * 32 + lane] = hr - hi;
         }
       }
     };
     auto consume = [&](int buf) {
-      const double *cre = dsm + buf * (2 * PLANE) + sg * (G * 32), *cim = cre + PLANE;
+      const double *cre = dsm + buf * (C::NPL * PLANE) + sg * (G * 32), *cim = cre + PLANE;
 #pragma unroll
       for (int si = 0; si < S / SG; ++si) {
         const int so = si * SG * G * 32;
@@ -1034,9 +1044,10 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
 #pragma unroll
         for (int k = 0; k < JPW; ++k) {
           const double br = cre[so + poff[k]], bi = cim[so + poff[k]];
-          dmma(acc[k][0], ar, br);       // P1
-          dmma(acc[k][1], ai, bi);       // P2
-          dmma(acc[k][2], as, br - bi);  // P3
+          const double bd = C::NPL == 3 ? cim[PLANE + so + poff[k]] : br - bi;
+          dmma(acc[k][0], ar, br);  // P1
+          dmma(acc[k][1], ai, bi);  // P2
+          dmma(acc[k][2], as, bd);  // P3
         }
       }
     };
@@ -1168,6 +1179,7 @@ bool star_plan(int G, int JPW, StarPlan &pl) {
 template <int G, int SM, int NBUF, int KIND>
 int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   using C = Mt2<G, SM, NBUF>;
+  static_assert(C::fits, "Mt2 shared memory");
   static StarPlan plan;
   static const bool ok = star_plan(G, C::JPW, plan);
   if (!ok) return xlh::set_error(XLMIMO_EUNSUPPORTED, "mt2: no star decomposition for G=%d, JPW=%d", G, C::JPW);
@@ -1178,19 +1190,24 @@ int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
 }
 
 // Tiles of 2*Mt2Cfg<G>::S steps.  Buffers: 2 (one barrier per tile) for G <= 4, the
-// 3-deep mbarrier ring above (measured on B200: cfg4 K=32 17.65 vs 18.50 ms with the
-// ring; cfg5 K=64 25.24 vs 25.79 ms).  XLMIMO_OPT_MT2_BUFFERS = 2|3 overrides.
+// 3-deep mbarrier ring above where its three planes fit (G = 5, 6; measured on B200 with
+// two planes: cfg4 K=32 17.65 vs 18.50 ms with the ring; cfg5 K=64 25.24 vs 25.79 ms);
+// G = 7, 8 take 2 buffers, K > 64 the ring with half-length tiles.  XLMIMO_OPT_MT2_BUFFERS
+// = 2|3 overrides where the ring fits.
 template <int G>
 int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int env = (int)xlh::option(XLMIMO_OPT_MT2_BUFFERS);
   const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
   if constexpr (G <= 8) {
-    if (nbuf == 2)
+    if (nbuf == 2 || !Mt2<G, 2, 3>::fits)
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
-  // K > 64: the ring only
-  return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
+  // K > 64: the ring only (half-length tiles when three planes do not fit)
+  if constexpr (Mt2<G, 2, 3>::fits)
+    return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
+  else
+    return ula ? launch_mt2_k<G, 1, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 1, 3, XLMIMO_UPA>(P, n_blocks, s);
 }
 
 // ------------------------------------------------------------------ kernel BLK
