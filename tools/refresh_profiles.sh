@@ -17,10 +17,13 @@ cap() { # tag cfg prec drops regex
 cap ftc_cfg5_d1000 5 fp32 1000 gram_fused_tc
 cap writer_cfg5 5 mat32 16 h_materialise
 cap ftc_cfg3 3 fp32 10000 gram_fused_tc
+cap mt2_cfg5_d1000 5 fp64 1000 gram_mt2
+cap mt2_cfg4 4 fp64 1000 gram_mt2
 cp profiles/r02/ncu_traffic_bench.json $O/ncu_traffic_bench.json
 python tools/ncu_traffic.py --merge $O/ncu_traffic_bench.json \
   $O/ftc_cfg5_d1000.ncu-rep:gram_fused_tc_f16:"cfg5 fp32 D=1000":1000 \
-  $O/writer_cfg5.ncu-rep:h_materialise:"cfg5 mat32 writer":16 > $O/traffic.log 2>&1
+  $O/writer_cfg5.ncu-rep:h_materialise:"cfg5 mat32 writer":16 \
+  $O/mt2_cfg5_d1000.ncu-rep:gram_fused_dmma_tiled_fp64:"cfg5 fp64 D=1000":1000 > $O/traffic.log 2>&1
 rm -f $O/*.ncu-rep
 cp $O/ncu_traffic_bench.json profiles/r02/ncu_traffic_bench.json  # the box's copy: bench reads it
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err
