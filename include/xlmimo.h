@@ -161,9 +161,9 @@ XLMIMO_API int xlmimo_sum_rate(const double *gram, int32_t K, int64_t n_drops, c
 
 /* The same receivers with a caller workspace, for K up to 1024.  For K > 64 the
  * Cholesky factors of I + rho G (CAP, MMSE) and of G (ZF) are formed one CTA per
- * matrix -- resident in shared memory for K <= 160, tiled (32 x 32 complex) in the
+ * matrix -- resident in shared memory for K <= 96, tiled (32 x 32 complex) in the
  * workspace above -- and the ZF/MMSE diagonals of the inverse follow from X = L^{-1}
- * (in place for K <= 160; blocked forward substitution, diagonal-tile inverses and
+ * (in place for K <= 96; blocked forward substitution, diagonal-tile inverses and
  * per-warp column panels in the workspace above); MRC comes straight from G.  The
  * workspace query returns 0 when none is needed (K <= 64); ws may then be NULL.
  * EWORKSPACE: ws_bytes below the query. */

@@ -14,9 +14,9 @@
 // Kernels
 //  * bounds_warp_kernel (K <= 64): one warp per drop, the packed lower triangle in
 //    shared memory, the same warp Cholesky as the receivers.
-//  * chol_smem_kernel (64 < K <= 160): one CTA per matrix, packed lower triangle in
+//  * chol_smem_kernel (64 < K <= 96): one CTA per matrix, packed lower triangle in
 //    shared memory, unblocked right-looking Cholesky.
-//  * chol_tiled_kernel (K > 160): one CTA per matrix in a global workspace slot, two
+//  * chol_tiled_kernel (K > 96): one CTA per matrix in a global workspace slot, two
 //    CTAs per SM, tiled Cholesky with 32 x 32 complex tiles on DMMA (panel groups of
 //    4, inverted diagonal tiles).  O(K^3/6) complex MACs per matrix; with dinv the
 //    blocked inverse L^{-1} (another K^3/6) on the same tile products.
@@ -171,7 +171,7 @@ __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, in
   return (i == j) ? make_double2(alpha + rho * g.x, 0.0) : make_double2(rho * g.x, rho * g.y);
 }
 
-// 64 < K <= kSmemK: one CTA per matrix, the packed lower triangle resident in shared
+// 64 < K <= kSmemMaxK: one CTA per matrix, the packed lower triangle resident in shared
 // memory (column-major packed: column j holds rows j..K-1 at off(j) = jK - j(j-1)/2),
 // unblocked right-looking Cholesky: per column j the pivot, the column scaled by
 // 1/L_jj, and the rank-1 update of the trailing triangle with warps over columns and
@@ -180,6 +180,13 @@ __device__ __forceinline__ double2 chol_entry(const double2 *G, int K, int i, in
 // substitution L x = e_i with x_m held by lane m % 32 (register slot m / 32), the
 // pivot element broadcast by shuffle, the column of L read from shared memory.
 constexpr int kSmemK = 160;
+// Largest K on the shared-memory kernel: the tiled DMMA kernel wins from K ~ 100 on
+// (1000 CAP + ZF + MMSE receivers, ms smem / tiled: K = 72 1.09 / 1.57, 100 2.56 / 2.42,
+// 128 6.43 / 2.43, 160 10.05 / 3.50; tools/ab_chol.py).
+#ifndef XL_CHOL_SMEM_MAXK
+#define XL_CHOL_SMEM_MAXK 96
+#endif
+constexpr int kSmemMaxK = XL_CHOL_SMEM_MAXK;
 constexpr int kSmemRpl = (kSmemK + 31) / 32;
 
 __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(kCtaThreads) chol_smem_kernel(CholParams P) {
   }
 }
 
-// K > kSmemK: one CTA per matrix in a global workspace slot (K_pad = 32 nt, row-major,
+// K > kSmemMaxK: one CTA per matrix in a global workspace slot (K_pad = 32 nt, row-major,
 // lower triangle used), tiled Cholesky with 32 x 32 complex tiles, panels in groups of
 // kGrp = 8 (left-looking inside a group, right-looking between groups):
 //  (0) the tiles of column k take the group's earlier panels: A_ik -= L_i,G' L_k,G'^H;
@@ -990,7 +997,7 @@ int n_tiled_slots(int64_t n_prob) {
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 size_t chol_slot_bytes(int K, int64_t n_prob, bool with_dinv) {
-  if (K <= kSmemK) return 0;
+  if (K <= kSmemMaxK) return 0;
   const int Kp = (K + kTile - 1) / kTile * kTile;
   const size_t slots = (size_t)n_tiled_slots(n_prob);
   size_t b = align256(slots * Kp * Kp * sizeof(double2));
@@ -1017,7 +1024,7 @@ int launch_chol(const double *gram, int K, int64_t n_drops, int n_mat, bool firs
   C.dinv = dinv;
   C.ws = (double2 *)ws;
   xlh::KTimer tm(s, "chol_logdet");
-  if (K <= kSmemK) {
+  if (K <= kSmemMaxK) {
     const size_t smem = (size_t)K * (K + 1) / 2 * sizeof(double2);
     const int per_sm = (int)((220 * 1024) / (smem + kSmemK * sizeof(double)));
     const int64_t grid = (int64_t)n_chol_slots(C.n_prob) * (per_sm > 1 ? per_sm : 1);
