@@ -105,6 +105,66 @@ __device__ __forceinline__ void ctile_mma(CTile &c, const double2 *__restrict__ 
     for (int q = 0; q < NB; ++q) b[q] = bn[q];
   }
 }
+// dst (MB 8 x NB 8 fragments from fragment (MB0, NB0), in memory) += A conj(Bt)^T, 3M form:
+// P1 = Ar Br^T, P2 = Ai Bi^T, P3 = (Ar + Ai)(Br - Bi)^T accumulated over the k-steps, then
+// Re C += P1 + P2, Im C += P3 - P1 + P2 (three DMMAs per fragment pair instead of four; the
+// operand sums are one DADD per fragment).  B is row-major Bt (B_NT), conjugated.
+template <int MB, int NB, int MB0, int NB0, int PFD>
+__device__ __forceinline__ void ctile_mma3m_nt(double2 *dst, size_t ld, const double2 *__restrict__ Am, size_t lda,
+                                               const double2 *__restrict__ Bm, size_t ldb, int nkb, int lane) {
+  const int qr = lane >> 2, qc = lane & 3;
+  double p1[MB][NB][2], p2[MB][NB][2], p3[MB][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) p1[mb][nb][e] = p2[mb][nb][e] = p3[mb][nb][e] = 0.0;
+  for (int q = 0; q < PFD && q < nkb; q += 2) frag_prefetch_l2<true>(Am, lda, Bm, ldb, q, lane);
+  auto load = [&](double2 (&a)[MB], double2 (&b)[NB], int kb) {
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) a[mb] = Am[(size_t)(8 * (MB0 + mb) + qr) * lda + 4 * kb + qc];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) b[nb] = Bm[(size_t)(8 * (NB0 + nb) + qr) * ldb + 4 * kb + qc];
+  };
+  double2 a[MB], b[NB];
+  load(a, b, 0);
+#pragma unroll 1
+  for (int kb = 0; kb < nkb; ++kb) {
+    if (!(kb & 1) && kb + PFD < nkb) frag_prefetch_l2<true>(Am, lda, Bm, ldb, kb + PFD, lane);
+    double2 an[MB], bn[NB];
+    load(an, bn, kb + 1 < nkb ? kb + 1 : kb);
+    double bd[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) bd[nb] = b[nb].x - b[nb].y;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const double as = a[mb].x + a[mb].y;
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        dmma_f64(p1[mb][nb], a[mb].x, b[nb].x);
+        dmma_f64(p2[mb][nb], a[mb].y, b[nb].y);
+        dmma_f64(p3[mb][nb], as, bd[nb]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MB; ++q) a[q] = an[q];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) b[q] = bn[q];
+  }
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      double2 *q = dst + (size_t)(8 * (MB0 + mb) + qr) * ld + 8 * (NB0 + nb) + 2 * qc;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double2 v = q[e];
+        q[e] = make_double2(v.x + (p1[mb][nb][e] + p2[mb][nb][e]), v.y + ((p3[mb][nb][e] - p1[mb][nb][e]) + p2[mb][nb][e]));
+      }
+    }
+}
+
 // pull a 32 x 32 complex tile (32 rows of 512 B) into L2 ahead of its use
 __device__ __forceinline__ void tile_prefetch_l2(const double2 *src, size_t ld, int lane) {
   const char *p = reinterpret_cast<const char *>(src + (size_t)lane * ld);

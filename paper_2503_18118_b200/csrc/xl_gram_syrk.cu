@@ -35,6 +35,12 @@ struct SyrkPlan {
 };
 
 constexpr int kSyrkWarps = 8;
+// Complex products in the 3M form on half tiles (column halves), as MT2: three DMMAs per
+// fragment pair instead of four.  E3 field, ms (4M -> 3M): K = 160 89.8 -> 83.6, 256 59.1
+// -> 54.7, 1000 82.6 -> 73.4 (tools/ab_syrk.py); row halves (2) 74.9 at K = 1000.  0: 4M.
+#ifndef XL_SYRK_3M
+#define XL_SYRK_3M 1
+#endif
 
 // Batch size B (drops), chunk CH = nsub x chs elements: the items of one SYRK launch
 // (B x tile pairs x nsub, one warp each, 8 per SM) should fill whole waves of the
@@ -141,10 +147,24 @@ __global__ void __launch_bounds__(32 * kSyrkWarps, 1)
   const bool lj = tj == nt - 1, li = ti == nt - 1;
   auto run = [&](auto mb, auto nb) {
     constexpr int MB = decltype(mb)::value, NB = decltype(nb)::value;
+#if XL_SYRK_3M
+    // 3M on half tiles (three accumulator sets of a 32 x 32 tile do not fit the registers),
+    // added into the partial in memory
+#if XL_SYRK_3M == 2  // halves along the rows
+    constexpr int MBA = MB < 2 ? MB : 2, MBB = MB - MBA;
+    ctile_mma3m_nt<MBA, NB, 0, 0, 8>(pt, kTile, A, CH, Bm, CH, chs / 4, lane);
+    if constexpr (MBB > 0) ctile_mma3m_nt<MBB, NB, MBA, 0, 8>(pt, kTile, A, CH, Bm, CH, chs / 4, lane);
+#else
+    constexpr int NBA = NB < 2 ? NB : 2, NBB = NB - NBA;
+    ctile_mma3m_nt<MB, NBA, 0, 0, 8>(pt, kTile, A, CH, Bm, CH, chs / 4, lane);
+    if constexpr (NBB > 0) ctile_mma3m_nt<MB, NBB, 0, NBA, 8>(pt, kTile, A, CH, Bm, CH, chs / 4, lane);
+#endif
+#else
     CTile c;
     ctile_load<false, MB, NB>(c, pt, kTile, lane);
     ctile_mma<true, true, true, MB, NB, 8>(c, A, CH, Bm, CH, chs / 4, lane);  // long slices: prefetch 8 ahead
     ctile_store<false, MB, NB>(c, pt, kTile, lane);
+#endif
   };
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
