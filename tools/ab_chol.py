@@ -15,12 +15,15 @@ import torch  # noqa: E402
 
 from variants import load  # noqa: E402
 
+KS = [(72, 1000), (100, 1000), (128, 1000), (160, 1000)]
+if os.environ.get("AB_CHOL_LARGE"):
+    KS = [(256, 296), (512, 148), (1000, 148)]
 for name in sys.argv[1:]:
     xl = load(name)
     par = importlib.import_module(xl.__name__ + ".parallel")
     a = xl.Array.ula(4096, 100e9)
-    for K in (72, 100, 128, 160):
-        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 1000, seed=13)
+    for K, D in KS:
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=13)
         G = xl.gram_exact(a, pos)
         r0, _ = xl.sum_rate(G, [10.0], xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_CAP)
         torch.cuda.synchronize()
