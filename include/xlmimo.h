@@ -269,7 +269,8 @@ XLMIMO_API int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, d
  * computed: every choice meets the same parity tier.  Not for concurrent use with
  * running entry points.  The library reads no environment variables.
  *   XLMIMO_OPT_LARGE_K      fp64 Gram for 64 < K: 1 block pairs, 2 chunked SYRK
- *   XLMIMO_OPT_PAIR         fp32 Gram for 64 < K: 1 operands generated in-kernel, 2 TMA-fed chunks
+ *   XLMIMO_OPT_PAIR         fp32 Gram for 64 < K: 1 TF32 block pairs generated in-kernel, 2 TMA-fed
+ *                           fp16 chunks (default: the fused fp16 kernel up to K = 128, chunks above)
  *   XLMIMO_OPT_GRAM_KERNEL  fused Gram, K <= 64: 1 split (K in {4,8}, ULA, fp64), 2 DMMA (K <= 16,
  *                           fp64), 3 CUDA-core register/tile kernels, 4 64-bit-index DMMA (K > 16)
  *   XLMIMO_OPT_SPLIT_NT     split kernel block variant: 64, 128, 192 (128 x 3/SM) or 256

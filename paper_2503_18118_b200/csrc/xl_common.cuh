@@ -242,6 +242,7 @@ int stream_tc_chunks(int64_t N);
 int fused_tc_chunks(int64_t N, int64_t n_drops);
 int stream_tc_parts(int K);
 bool fused_tc_supported(const ArrayP &a, int K);
+bool fused_tc_wide_supported(const ArrayP &a, int K);
 bool fused_tc_supported_geometry(const ArrayP &a);
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
                     cudaStream_t s);

@@ -1657,6 +1657,12 @@ bool use_stream_pair(int K) {
   if (o == 2) return true;
   return K >= kStreamPairMinK;
 }
+// 64 < K <= 128 fp32: the fused kernel's wide + narrow launches (xl_stream_tc.cu) unless
+// XLMIMO_OPT_PAIR = 1 (the block-pair kernel) or 2 (the pair stream) / MATERIALIZED
+bool use_fused_wide(const xlh::ArrayP &a, int K, int mode) {
+  return !use_stream_pair(K) && mode != XLMIMO_MATERIALIZED && xlh::option(XLMIMO_OPT_PAIR) != 1 &&
+         xlh::fused_tc_wide_supported(a, K);
+}
 bool use_gram_syrk(int K) {
   const int64_t o = xlh::option(XLMIMO_OPT_LARGE_K);
   if (o == 1) return false;
@@ -1831,6 +1837,7 @@ size_t gram_ws_bytes(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
   const size_t np = (size_t)K * (K + 1) / 2;
   if (K > xl::kMaxK && !use_mt2_large(a, K, precision, mode)) {
     if (precision == XLMIMO_FP32 && N >= kTcMinN) {  // tcgen05 block pairs (+ H chunks when streamed)
+      if (use_fused_wide(a, K, mode)) return (size_t)n_drops * fused_tc_chunks(N, n_drops) * np * 2 * sizeof(double);
       const size_t part = ((size_t)n_drops * fused_tc_pair_chunks(N) * np * 2 * sizeof(double) + 255) / 256 * 256;
       const bool stream = use_stream_pair(K) || mode == XLMIMO_MATERIALIZED;
       return part + (stream && n_drops > 0 ? stream_pair_h_bytes(K, n_drops, N) : 0);
@@ -1992,7 +1999,13 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       const size_t need = gram_ws_bytes(a, K, n_drops, 1, precision, mode);
       if (ws_bytes < need || !ws) return set_error(XLMIMO_EWORKSPACE, "gram: workspace %zu < %zu bytes", ws_bytes, need);
       int rc;
-      if (use_stream_pair(K) || mode == XLMIMO_MATERIALIZED) {  // times and counts its own launches
+      const bool wide = use_fused_wide(a, K, mode);
+      if (wide) {
+        KTimer tm(s, "gram_fused_tc_f16");
+        rc = launch_fused_tc(a, pos, K, n_drops, N, (double *)ws, s);
+        tm.stop(s);
+        count_launch(2);
+      } else if (use_stream_pair(K) || mode == XLMIMO_MATERIALIZED) {  // times and counts its own launches
         const size_t part =
             ((size_t)n_drops * fused_tc_pair_chunks(N) * ((size_t)K * (K + 1) / 2) * 2 * sizeof(double) + 255) /
             256 * 256;
@@ -2005,8 +2018,8 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       }
       if (rc) return rc;
       KTimer tr(s, "gram_reduce");
-      gram_reduce_rows_kernel<<<(unsigned)(n_drops * K), 256, 0, s>>>((const double *)ws, K,
-                                                                      fused_tc_pair_chunks(N), 1, out);
+      gram_reduce_rows_kernel<<<(unsigned)(n_drops * K), 256, 0, s>>>(
+          (const double *)ws, K, wide ? fused_tc_chunks(N, n_drops) : fused_tc_pair_chunks(N), 1, out);
       tr.stop(s);
       count_launch();
       return check_launch("gram_reduce_rows_kernel");

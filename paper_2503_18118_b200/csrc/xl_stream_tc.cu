@@ -435,6 +435,8 @@ struct FusedParams {
   int64_t n_drops;
   uint32_t tmem_cols;
   GenConst g;        // the generator's launch constants (TE of the instantiation)
+  int u0, k_gen;     // users generated: u0 .. u0 + k_gen - 1 of the K (rows 2u, 2u + 1)
+  int n_acc;         // TMEM accumulators (2: double-buffered, 1 when 3 n_mma > 512)
 };
 
 // TF32 round-to-nearest, ties away from zero, as integer ALU work (sign-magnitude:
@@ -689,6 +691,19 @@ constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one
 // the TMEM base word (+16 B), rounded up to 64 B
 constexpr int kFSuOff = (kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 63) & ~63;
 
+// Stage shapes of gram_fused_tc_kernel: narrow (K <= 64: 128 rows = 64 users, 12 slots, 12
+// groups of 2 warps) and wide (64 < K <= 128: 256 rows = the MMA's N, 6 slots of 32 KB, 6
+// groups of 4 warps; the A operand is the first 128 rows).  Same warps, threads and
+// shared-memory budget.
+template <bool WIDE>
+struct FCfg {
+  static constexpr int Groups = WIDE ? 6 : kFGroups, GenWarps = WIDE ? 4 : kFGenWarps;
+  static constexpr int Stages = WIDE ? 6 : kFStages, Rows = WIDE ? 256 : kRows, MaxUsers = Rows / 2;
+  static constexpr int GenThreads = 32 * GenWarps, StageBytes = Rows * 128, UBits = WIDE ? 7 : 6;
+  static constexpr int SuOff = (Stages * StageBytes + (2 * Stages + 4) * 8 + 16 + 63) & ~63;
+  static_assert(GenWarps * Groups == kEpiWarp0 && Groups <= Stages, "FCfg warps / slots");
+};
+
 // Per-drop power-of-two scale of the fp16 operands: the largest coefficient magnitude of a
 // user is sqrt(beta0) sqrt(x_eff) / x_eff^{3/2} = sqrt(beta0) / sqrt(xz2) (r >= x_eff), so
 // 2^e with e = -ilogb(sqrt(beta0) / sqrt(min_u xz2)) puts the drop's largest |h| in [1, 2)
@@ -712,25 +727,27 @@ __device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int ki
   return scale_of_min_xz2(m, sqrt_beta0);
 }
 
-template <int TE, int KIND>
+template <int TE, int KIND, bool WIDE>
 __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedParams P) {
+  using C = FCfg<WIDE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *stages = base;
-  uint64_t *full = (uint64_t *)(base + kFStages * kStageBytes);
-  uint64_t *empty = full + kFStages;
-  uint64_t *tfull = empty + kFStages;
+  uint64_t *full = (uint64_t *)(base + C::Stages * C::StageBytes);
+  uint64_t *empty = full + C::Stages;
+  uint64_t *tfull = empty + C::Stages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_base_sh = (uint32_t *)(tempty + 2);
-  GenUser *su_all = (GenUser *)(base + kFSuOff);  // [groups][64], past the TMEM base word
+  GenUser *su_all = (GenUser *)(base + C::SuOff);  // [groups][MaxUsers], past the TMEM base word
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = P.K, R = 2 * K;
+  const int K = P.K, KG = P.k_gen, R = 2 * KG;  // K: the drop's users (indexing), KG: generated here
   const int64_t n_items = P.n_drops * P.n_chunks;
-  for (int i = tid; i < kFStages * kStageBytes / 16; i += kFusedThreads) ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < C::Stages * C::StageBytes / 16; i += kFusedThreads)
+    ((uint4 *)stages)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
-    for (int s = 0; s < kFStages; ++s) {
-      mbar_init(&full[s], kFGenWarps);
+    for (int s = 0; s < C::Stages; ++s) {
+      mbar_init(&full[s], C::GenWarps);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -756,32 +773,33 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     // The global stage sequence k (the MMA issuer's order) lives in slot k % 12 with
     // phase (k / 12) & 1; 12 slots for 8 groups let a group start its next stage
     // while the MMA still holds its previous one.
-    const int grp = warp / kFGenWarps, gtid = tid - grp * kFGenThreads;
-    GenUser *su = su_all + grp * 64;
+    const int grp = warp / C::GenWarps, gtid = tid - grp * C::GenThreads;
+    GenUser *su = su_all + grp * C::MaxUsers;
     // the same address in the shared window, from the (constant) window offset of smem_raw
-    uint32_t su_s = ((smem_u32(smem_raw) + 1023u) & ~1023u) + (uint32_t)kFSuOff + (uint32_t)grp * 64u * 32u;
+    uint32_t su_s = ((smem_u32(smem_raw) + 1023u) & ~1023u) + (uint32_t)C::SuOff + (uint32_t)(grp * C::MaxUsers) * 32u;
     asm volatile("" : "+r"(su_s));  // opaque: kept in a register, not re-derived per task
     // element blocks stacked in the 128 rows (as in the stream kernel): block b of a
     // stage covers elements xs + 64 b .. + 63 (fp16: 64 per 128-B row) in rows rb*b .. rb*b + 2K - 1
     constexpr int kTpr = kFBoxK / TE;      // tasks per user row of a block (4 or 8)
-    const int n_tasks = P.nblk * K * kTpr;
-    constexpr int kUStep = kFGenThreads / kTpr;  // users a thread's task advances by
-    static_assert(kFGenThreads % kTpr == 0 && kUStep <= 16, "task stepping assumes kTpr | kFGenThreads");
+    const int n_tasks = P.nblk * KG * kTpr;
+    constexpr int kUStep = C::GenThreads / kTpr;  // users a thread's task advances by
+    static_assert(C::GenThreads % kTpr == 0, "task stepping assumes kTpr | GenThreads");
     const int g8 = gtid % kTpr;
     // The thread's tasks of a stage (the same every stage): task = (blk, u, g8) with
     // task = blk tpb + u kTpr + g8 for task = gtid, gtid + kFGenThreads, ...; the stride is a
-    // multiple of kTpr, so g8 is the thread's constant.  Byte j of tdesc = u | blk << 6 of its
-    // j-th task; n_my <= n_tasks / kFGenThreads <= 4 (TE = 16) or 8 (TE = 8) since nblk K <= 64.
+    // multiple of kTpr, so g8 is the thread's constant.  Byte j of tdesc = u | blk << UBits of
+    // its j-th task; n_my <= n_tasks / GenThreads <= 4 (TE = 16) or 8 (TE = 8) since nblk KG <=
+    // MaxUsers (wide: nblk = 1, u < 128).
     using Desc = typename std::conditional<kTpr <= 4, uint32_t, uint64_t>::type;  // n_my <= kTpr bytes
     Desc tdesc = 0;
     int n_my = 0;
     {
       int u = gtid / kTpr, blk = 0;
-      while (u >= K) { u -= K; ++blk; }
-      for (int task = gtid; task < n_tasks; task += kFGenThreads, ++n_my) {
-        tdesc |= (Desc)(u | (blk << 6)) << (8 * n_my);
+      while (u >= KG) { u -= KG; ++blk; }
+      for (int task = gtid; task < n_tasks; task += C::GenThreads, ++n_my) {
+        tdesc |= (Desc)(u | (blk << C::UBits)) << (8 * n_my);
         u += kUStep;
-        while (u >= K) { u -= K; ++blk; }
+        while (u >= KG) { u -= KG; ++blk; }
       }
     }
     const uint32_t code0 = (uint32_t)tdesc & 0xFFu;
@@ -795,17 +813,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int64_t rem = P.N - x0;
       const int spb = kFBoxK * P.nblk;  // elements per stage
       const int ns = (int)(((rem < P.chunk ? rem : P.chunk) + spb - 1) / spb);
-      int64_t k = kstart + (((int64_t)grp - kstart) % kFGroups + kFGroups) % kFGroups;
+      int64_t k = kstart + (((int64_t)grp - kstart) % C::Groups + C::Groups) % C::Groups;
       kstart += ns;
       if (k >= kstart) continue;  // no stage of this item for this group
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
-      for (int u = gtid; u < K; u += kFGenThreads) {
-        const double *p = P.pos + (d * K + u) * 3;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(C::GenThreads) : "memory");
+      for (int u = gtid; u < KG; u += C::GenThreads) {
+        const double *p = P.pos + (d * K + P.u0 + u) * 3;
         const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
         su[u] = GenUser{uc.xz2, uc.y, uc.z, (float)uc.amp, 0.0f};
       }
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kFGenThreads) : "memory");
-      const float scale = drop_scale(su, K, P.sqrt_beta0);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(C::GenThreads) : "memory");
+      const float scale = drop_scale(su, KG, P.sqrt_beta0);
       // A task = (blk, u, g8) with task = blk tpb + u kTpr + g8; the stride kFGenThreads is a
       // multiple of kTpr, so g8 is the thread's constant and u steps by kUStep.  Software
       // pipeline: the next task's anchor and coefficients (the serial fp64 chain) are formed in
@@ -813,7 +831,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       // behind the MUFU work; the next task of a stage's last one is the first of the group's
       // next stage.
       auto prep = [&](int64_t xs_, uint32_t code, TaskCoef &c_, int &nv_, int &row0_) {
-        const int u_ = (int)(code & 63u), blk_ = (int)(code >> 6);
+        const int u_ = (int)(code & ((1u << C::UBits) - 1u)), blk_ = (int)(code >> C::UBits);
         const int64_t t0 = xs_ + (kFBoxK * blk_ + TE * g8);
         double ey, ez;
         task_anchor<KIND>(P.g, t0, ey, ez);
@@ -826,18 +844,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       TaskCoef tc;
       int nv, row0;
       prep(xs, code0, tc, nv, row0);
-      for (; k < kstart; k += kFGroups) {
-        // more slots than groups: a group's next stage reuses a slot freed 4 stages ago,
-        // so generation never waits on the MMA of its own previous stage
-        const int slot = (int)(k % kFStages);
-        const uint32_t slot_base = stages_base + slot * kStageBytes;
-        mbar_wait(&empty[slot], ((uint32_t)(k / kFStages) & 1) ^ 1);
+      for (; k < kstart; k += C::Groups) {
+        const int slot = (int)(k % C::Stages);
+        const uint32_t slot_base = stages_base + slot * C::StageBytes;
+        mbar_wait(&empty[slot], ((uint32_t)(k / C::Stages) & 1) ^ 1);
         Desc rest = rest0;  // codes of the tasks after the current one
         for (int j = n_my; j > 0; --j) {
           const bool last = j == 1;  // the next task is the first of the group's next stage
           const uint32_t code_n = last ? code0 : (uint32_t)rest & 0xFFu;
           rest >>= 8;
-          const int64_t xsn = last ? xs + (int64_t)kFGroups * spb : xs;
+          const int64_t xsn = last ? xs + (int64_t)C::Groups * spb : xs;
           TaskCoef cn;
           int nvn, rown;
           prep(xsn, code_n, cn, nvn, rown);
@@ -870,12 +886,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[slot]);  // kFGenWarps arrivals complete the stage
+        if (lane == 0) mbar_arrive(&full[slot]);  // GenWarps arrivals complete the stage
       }
     }
   } else if (warp == kMmaWarp) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
     const uint32_t idesc = f16_idesc(kRows, P.n_mma);
-    const uint64_t desc0 = sw128_desc(smem_u32(stages));  // slot s, k-step k: + s kStageBytes/16 + 2k
+    const uint64_t desc0 = sw128_desc(smem_u32(stages));  // slot s, k-step k: + s StageBytes/16 + 2k
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -884,8 +900,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int c = (int)(it - d * P.n_chunks);
       const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk, P.chunk);
       for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {  // one TMEM sub-chunk
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = P.n_acc == 2 ? (local & 1) : 0;
+        const uint32_t acc_phase = (P.n_acc == 2 ? (local >> 1) : local) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tmem_d = tmem + (uint32_t)(acc * P.n_mma);
@@ -893,7 +909,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         for (int kb = s0; kb < s1; ++kb) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t ds = desc0 + (uint64_t)(stage * (kStageBytes >> 4));
+          const uint64_t ds = desc0 + (uint64_t)(stage * (C::StageBytes >> 4));
           if (elect_one()) {
 #ifdef XL_EXP_NO_MMA  // tuning experiment: the generator-bound rate (results invalid)
             mbar_arrive(&empty[stage]);
@@ -905,7 +921,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
 #endif
           }
           __syncwarp();
-          if (++stage == kFStages) { stage = 0; phase ^= 1; }
+          if (++stage == C::Stages) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) mma_commit(&tfull[acc]);
         __syncwarp();
@@ -916,7 +932,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     const int row = 32 * q + lane;
     const int blk = (32 * q) / P.rb;
     const int lr = row - blk * P.rb;
-    const int i = lr >> 1, plane = lr & 1;
+    const int i = P.u0 + (lr >> 1), plane = lr & 1;  // the drop's user index of this row
     const int col0 = blk * P.rb;
     const bool has_users = 32 * q - blk * P.rb < R;
     const int NP = K * (K + 1) / 2;
@@ -925,17 +941,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
       double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
-      const float sc = epi_drop_scale(P.pos + d * K * 3, K, P.kind, P.sqrt_beta0, lane);
+      const float sc = epi_drop_scale(P.pos + (d * K + P.u0) * 3, KG, P.kind, P.sqrt_beta0, lane);
       const double post = 1.0 / ((double)sc * (double)sc);  // exact: sc is a power of two
       const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk, P.chunk);
       for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = P.n_acc == 2 ? (local & 1) : 0;
+        const uint32_t acc_phase = (P.n_acc == 2 ? (local >> 1) : local) & 1;
         mbar_wait(&tfull[acc], acc_phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (has_users)
           drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * P.n_mma + col0),
-                         (uint32_t)(2 * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kFSubStages >= ns, out, post);
+                         (uint32_t)(P.n_acc * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kFSubStages >= ns,
+                         out, post, P.u0);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1477,8 +1494,19 @@ int fused_tc_chunks(int64_t N, int64_t n_drops) {
 // kTaskE; other UPAs take the CUDA-core fp32 kernel.
 bool fused_tc_supported_geometry(const ArrayP &a) { return a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0; }
 bool fused_tc_supported(const ArrayP &a, int K) { return K >= 9 && K <= 64 && fused_tc_supported_geometry(a); }
+// 64 < K <= 128 on the fused kernel (wide + narrow launches) unless XLMIMO_OPT_PAIR picks
+// the block-pair kernel (1) or the TMA-fed pair stream (2)
+bool fused_tc_wide_supported(const ArrayP &a, int K) {
+  return K > 64 && K <= 128 && fused_tc_supported_geometry(a);
+}
 
-// Fused fp32 Gram on tcgen05: partials [drop][chunk][NP][2] into ws (stream_tc_chunks(N) per drop).
+// Fused fp32 Gram on tcgen05: partials [drop][chunk][block][NP][2] (NP = K(K+1)/2) into ws,
+// fused_tc_chunks(N, n_drops) chunks per drop.  K <= 64: one narrow launch (element blocks
+// stacked in the 128 rows for small K).  64 < K <= 128: a wide launch (rows = all K users,
+// the MMA's A operand their first 64: the entries i < 64, j >= i) and a narrow one for users
+// 64..K-1 (i, j >= 64), one element block each, writing disjoint entries of the same
+// partials; every coefficient is generated once per launch that needs it (K + K - 64 user
+// rows per element, against 4 x 64 for the block-pair kernel at K = 100).
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
                     cudaStream_t s) {
   FusedParams P;
@@ -1492,16 +1520,9 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   P.lambda = a.lambda;
   P.pitch = a.pitch;
   P.sqrt_beta0 = a.sqrt_beta0;
-  P.rb = rows_per_block(K);
-  P.nblk = kRows / P.rb;
-  P.n_mma = P.nblk > 1 ? kRows : (2 * K + 15) / 16 * 16;
   P.chunk = fused_tc_chunk(N, n_drops);
   P.n_chunks = fused_tc_chunks(N, n_drops);
   P.n_drops = n_drops;
-  uint32_t cols = 32;
-  while (cols < (uint32_t)(3 * P.n_mma)) cols <<= 1;  // two accumulators + the running sum
-  P.tmem_cols = cols;
-  const size_t smem = 1024 + (size_t)kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 64 + kFGroups * 64 * 32;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1510,14 +1531,45 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   // 16-element tasks wherever a task stays in one array row (every ULA; UPA rows of 16k)
   const bool te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
   P.g = make_gen_const(a, N, te16 ? 16 : 8);
-  auto run = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kFusedThreads, smem, s>>>(P);
+  auto launch = [&](int u0, int k_gen, bool wide) {
+    P.u0 = u0;
+    P.k_gen = k_gen;
+    if (wide || K > 64) {  // one element block per stage
+      P.rb = wide ? 256 : kRows;
+      P.nblk = 1;
+      P.n_mma = (2 * k_gen + 15) / 16 * 16;
+    } else {
+      P.rb = rows_per_block(K);
+      P.nblk = kRows / P.rb;
+      P.n_mma = P.nblk > 1 ? kRows : (2 * K + 15) / 16 * 16;
+    }
+    P.n_acc = 3 * P.n_mma <= 512 ? 2 : 1;  // accumulators + the running sum within 512 columns
+    uint32_t cols = 32;
+    while (cols < (uint32_t)((P.n_acc + 1) * P.n_mma)) cols <<= 1;
+    P.tmem_cols = cols;
+    auto run = [&](auto kern, int stage_bytes, int stages, int groups, int max_users) {
+      const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + 64 +
+                          (size_t)groups * max_users * 32;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, kFusedThreads, smem, s>>>(P);
+    };
+    using CN = FCfg<false>;
+    using CW = FCfg<true>;
+    if (wide) {
+      if (a.kind == XLMIMO_ULA) run(gram_fused_tc_kernel<16, XLMIMO_ULA, true>, CW::StageBytes, CW::Stages, CW::Groups, CW::MaxUsers);
+      else if (te16) run(gram_fused_tc_kernel<16, XLMIMO_UPA, true>, CW::StageBytes, CW::Stages, CW::Groups, CW::MaxUsers);
+      else run(gram_fused_tc_kernel<8, XLMIMO_UPA, true>, CW::StageBytes, CW::Stages, CW::Groups, CW::MaxUsers);
+    } else {
+      if (a.kind == XLMIMO_ULA) run(gram_fused_tc_kernel<16, XLMIMO_ULA, false>, CN::StageBytes, CN::Stages, CN::Groups, CN::MaxUsers);
+      else if (te16) run(gram_fused_tc_kernel<16, XLMIMO_UPA, false>, CN::StageBytes, CN::Stages, CN::Groups, CN::MaxUsers);
+      else run(gram_fused_tc_kernel<8, XLMIMO_UPA, false>, CN::StageBytes, CN::Stages, CN::Groups, CN::MaxUsers);
+    }
+    return check_launch("gram_fused_tc_kernel");
   };
-  if (a.kind == XLMIMO_ULA) run(gram_fused_tc_kernel<16, XLMIMO_ULA>);
-  else if (te16) run(gram_fused_tc_kernel<16, XLMIMO_UPA>);
-  else run(gram_fused_tc_kernel<8, XLMIMO_UPA>);
-  return check_launch("gram_fused_tc_kernel");
+  if (K <= 64) return launch(0, K, false);
+  const int rc = launch(0, K, true);
+  if (rc) return rc;
+  return launch(64, K - 64, false);
 }
 
 int stream_tc_parts(int K) { return kRows / rows_per_block(K); }

@@ -110,6 +110,28 @@ def test_gram_large_k_fp32_parity(xl, orc, kind, n_y, n_z, K, D):
     assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
 
 
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 9001, 1, 128, 3), ("ula", 70001, 1, 86, 2),
+                                              ("upa", 48, 150, 97, 2), ("ula", 2048, 1, 65, 4)])
+def test_gram_fp32_wide_fused(xl, orc, kind, n_y, n_z, K, D):
+    """64 < K <= 128 at fp32 on the fused kernel: a wide launch (all K users as the MMA's N, the
+    first 64 as its M: entries i < 64) and a narrow one (users 64..K-1) into one set of
+    partials -- every entry against the oracle at the fp32 tier (1e-4 normalised), with a
+    single TMEM accumulator (3 N > 512: K = 86, 97, 128) and a double-buffered one (K = 65),
+    several chunks (N = 70001), UPA rows of 16k; Hermitian, real diagonal."""
+    fc = 100e9
+    if kind == "ula":
+        a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=K + 1)
+    else:
+        a, ao = xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, D, seed=K + 1)
+    G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+    Go = orc.gram_exact_blas(ao, pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-4
+    assert np.all(G.diagonal(axis1=1, axis2=2).imag == 0)
+    assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
+
+
 def test_gram_large_k_fp32_e3(xl, orc):
     """E3 size in fp32: K = 1000, M = 35 000 against the oracle (1e-4) and the paper's gap."""
     a = xl.Array.ula(35000, 100e9)
@@ -262,7 +284,7 @@ def test_large_k_paths_outside_their_default_range(xl, orc, path, K):
     assert normalized_err(G, Go) <= 1e-9
 
 
-@pytest.mark.parametrize("path,K", [(1, 400), (2, 100), (1, 200), (2, 65)])
+@pytest.mark.parametrize("path,K", [(1, 400), (2, 100), (1, 200), (2, 65), (1, 100)])
 def test_large_k_fp32_paths_outside_their_default_range(xl, orc, path, K):
     """XLMIMO_OPT_PAIR forces the in-kernel-generation (1) or the TMA-fed materialised-chunk
     (2) tcgen05 block-pair kernel at fp32; each must meet the fp32 tier (1e-4 normalised)
