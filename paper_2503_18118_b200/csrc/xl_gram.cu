@@ -1644,7 +1644,9 @@ int blk_pairs(int K) {
 }
 // K > 64, fp64: the chunked DMMA SYRK (xl_gram_syrk.cu) above 128 users, the
 // block-pair kernel below it; XLMIMO_OPT_LARGE_K = 1 (blocks) | 2 (SYRK) overrides.
-constexpr int kSyrkMinK = 129;  // measured (35 000 elements): K = 128 blk 61 vs SYRK 66 ms, K = 150 64 vs 57, K = 200 54 vs 49
+// measured (35 000 elements, 1000 drops, after the SYRK's 3M form): K = 121 blk 118.1 vs SYRK
+// 115.2 ms, K = 128 118.1 vs 115.9 (tools/time_k128.py); MT2 takes K <= 120 (65.6 ms at 120)
+constexpr int kSyrkMinK = 121;
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
 // generated in-kernel below; XLMIMO_OPT_PAIR = 1 (gen) | 2 (stream) overrides.
