@@ -853,6 +853,13 @@ template <> struct Mt2Cfg<12> { static constexpr int JPW = 6, SG = 1, S = 4; }; 
 template <> struct Mt2Cfg<13> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 13 stars
 template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 15 stars
 template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
+// 120 < K <= 128: 34 stars of 4 dealt to two launches of 17 warps (a single launch of 17
+// stars of 8 spills its accumulators); each launch generates all 16 groups
+template <> struct Mt2Cfg<16> { static constexpr int JPW = 4, SG = 1, S = 4, NL = 2; };
+template <int G, typename = void>
+struct Mt2Launches { static constexpr int value = 1; };
+template <int G>
+struct Mt2Launches<G, decltype((void)Mt2Cfg<G>::NL, void())> { static constexpr int value = Mt2Cfg<G>::NL; };
 
 // Tile planes: re, im and re - im, the 3M partner operand (A_p - B_p), formed once per
 // coefficient by the generator instead of once per star and step by the consumers (the
@@ -865,13 +872,14 @@ constexpr int kMt2Planes = XL_MT2_DPLANE ? 3 : 2;
 template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::S; NBUF tile buffers
 struct Mt2 {
   static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
-  static constexpr int JG = J / JPW, NW = JG * SG, NT = 32 * NW;
+  static constexpr int NL = Mt2Launches<G>::value;  // launches sharing the stars
+  static constexpr int JG = J / (JPW * NL), NW = JG * SG, NT = 32 * NW;  // stars per launch
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
-  static_assert(J % JPW == 0 && S % SG == 0, "Mt2Cfg");
+  static_assert(J % (JPW * NL) == 0 && S % SG == 0, "Mt2Cfg");
   static constexpr int NPL = kMt2Planes;  // re, im (, re - im: the 3M partner operand)
   static constexpr size_t tiles_bytes = (size_t)NPL * NBUF * PLANE * sizeof(double);  // NBUF buffers x planes
-  static constexpr size_t stage_bytes = (size_t)J * 3 * SG * 64 * sizeof(double);
+  static constexpr size_t stage_bytes = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
   static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
   static constexpr bool fits = smem <= 220 * 1024;
 };
@@ -881,8 +889,8 @@ struct Mt2 {
 // the block as (g2, g1), i.e. transposed).
 constexpr int kMt2MaxG = 16;
 struct StarPlan {
-  int8_t cen[32];
-  int8_t par[32][8];
+  int8_t cen[40];
+  int8_t par[40][8];
   int16_t blk[kMt2MaxG * kMt2MaxG];
 };
 
@@ -945,7 +953,8 @@ __device__ __forceinline__ void mt_arrive(uint64_t *bar) {
 // instead of draining the FP64 pipe at every tile boundary.
 template <int G, int SM, int NBUF, int KIND>
 __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramParams P, FastDiv fd,
-                                                                         const __grid_constant__ StarPlan plan) {
+                                                                         const __grid_constant__ StarPlan plan,
+                                                                         int star0) {
   using C = Mt2<G, SM, NBUF>;
   constexpr int JPW = C::JPW, SG = C::SG, S = C::S, NW = C::NW, NT = C::NT, JG = C::JG;
   constexpr int PLANE = C::PLANE, ROWS = C::ROWS;
@@ -974,10 +983,10 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int jg = warp % JG, sg = warp / JG;
-  const int coff = plan.cen[jg] * 32 + lane;  // the star's centre fragment
-  int poff[JPW];                              // its partners' fragments
+  const int coff = plan.cen[star0 + jg] * 32 + lane;  // the star's centre fragment
+  int poff[JPW];                                      // its partners' fragments
 #pragma unroll
-  for (int k = 0; k < JPW; ++k) poff[k] = plan.par[jg][k] * 32 + lane;
+  for (int k = 0; k < JPW; ++k) poff[k] = plan.par[star0 + jg][k] * 32 + lane;
   __syncthreads();
   const double c4 = 4.0 * P.inv_lambda;
   const bool n_odd = (P.N & 1) != 0;
@@ -1102,9 +1111,11 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
       const int bq = plan.blk[(i >> 3) * kMt2MaxG + (j >> 3)];
+      const int q = (bq >> 1) - star0 * JPW;  // this launch's job holding the block
+      if (C::NL > 1 && (q < 0 || q >= JG * JPW)) continue;  // another launch's block
       const bool tr = bq & 1;  // block held as (g2, g1): read (j, i) and conjugate
       const int e = tr ? (j & 7) * 8 + (i & 7) : (i & 7) * 8 + (j & 7);
-      const double *st = dsm + (size_t)(bq >> 1) * 3 * SG * 64 + e;
+      const double *st = dsm + (size_t)q * 3 * SG * 64 + e;
       double p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
       for (int g = 0; g < SG; ++g) {
@@ -1185,7 +1196,9 @@ int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   if (!ok) return xlh::set_error(XLMIMO_EUNSUPPORTED, "mt2: no star decomposition for G=%d, JPW=%d", G, C::JPW);
   const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
   cudaFuncSetAttribute(gram_mt2_kernel<G, SM, NBUF, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-  gram_mt2_kernel<G, SM, NBUF, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd, plan);
+  for (int l = 0; l < C::NL; ++l)  // each launch its share of the stars, disjoint entries of the partials
+    gram_mt2_kernel<G, SM, NBUF, KIND><<<(unsigned)n_blocks, C::NT, C::smem, s>>>(P, fd, plan, l * C::JG);
+  if (C::NL > 1) xlh::count_launch(C::NL - 1);  // the caller counts one
   return XLMIMO_OK;
 }
 
@@ -1824,7 +1837,7 @@ bool use_warp_kernel(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
 
 // fp64 fused Gram for 64 < K <= 128 on the MT2 kernel (3M DMMA stars) unless
 // XLMIMO_OPT_LARGE_K picks the block-pair (1) or SYRK (2) kernel
-constexpr int kMt2MaxK = 120;  // G <= 15 (G = 16 would need 8-block stars: register spills)
+constexpr int kMt2MaxK = 128;  // G <= 16 (G = 16 as two launches of 17 stars of 4)
 bool use_mt2_large(const ArrayP &a, int K, int precision, int mode) {
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   const int64_t o = option(XLMIMO_OPT_LARGE_K), gk = option(XLMIMO_OPT_GRAM_KERNEL);
@@ -2130,7 +2143,8 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
       case 12: rc = launch_mt2<12>(P, n_blocks, s); break;
       case 13: rc = launch_mt2<13>(P, n_blocks, s); break;
       case 14: rc = launch_mt2<14>(P, n_blocks, s); break;
-      default: rc = launch_mt2<15>(P, n_blocks, s); break;
+      case 15: rc = launch_mt2<15>(P, n_blocks, s); break;
+      default: rc = launch_mt2<16>(P, n_blocks, s); break;
     }
     if (rc) return rc;
   } else if (kc.which == 2) {

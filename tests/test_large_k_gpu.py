@@ -30,8 +30,9 @@ def xl():
                                               ("ula", 50, 1, 100, 2), ("ula", 2000, 1, 113, 2),
                                               ("ula", 999, 1, 120, 2), ("upa", 32, 16, 104, 2)])
 def test_gram_large_k_parity(xl, orc, kind, n_y, n_z, K, D):
-    """64 < K <= 120 on the MT2 3M-DMMA stars (65, 80 UPA, 100, 104 UPA, 113, 120), the 3M
-    SYRK above (K = 128, ragged 129, 200), and N < K (rank-deficient G, N = 50)."""
+    """64 < K <= 128 on the MT2 3M-DMMA stars (65, 80 UPA, 100, 104 UPA, 113, 120; 128 as two
+    launches of 17 stars), the 3M SYRK above (ragged 129, 200), and N < K (rank-deficient G,
+    N = 50)."""
     fc = 100e9
     if kind == "ula":
         a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
