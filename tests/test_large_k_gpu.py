@@ -296,3 +296,23 @@ def test_large_k_fp32_paths_outside_their_default_range(xl, orc, path, K):
         G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
     Go = orc.gram_exact(orc.array("ula", n_y=5000, fc_hz=100e9), pos.cpu().numpy())
     assert normalized_err(G, Go) <= 1e-4
+
+
+def test_every_kernel_boundary_in_k(xl, orc):
+    """Dispatch boundaries in K (W / split / M / MT2 G = 3..16 with its one- and two-launch
+    plans / SYRK; fused fp32 narrow, wide + narrow, pair stream) on one ULA and one UPA of a
+    few thousand elements: fp64 within 1e-9 and fp32 within 1e-4 (normalised) of the oracle,
+    every entry, for K on both sides of each boundary."""
+    ks = [1, 4, 5, 8, 9, 16, 17, 24, 25, 32, 33, 48, 49, 56, 57, 63, 64, 65, 72, 73, 96, 97, 104, 105,
+          112, 113, 120, 121, 127, 128, 129]
+    fc = 100e9
+    arrays = [(xl.Array.ula(3001, fc), orc.array("ula", n_y=3001, fc_hz=fc)),
+              (xl.Array.upa(48, 40, fc), orc.array("upa", n_y=48, n_z=40, fc_hz=fc))]
+    for (a, ao) in arrays:
+        for K in ks:
+            pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, 2, seed=100 + K)
+            Go = orc.gram_exact_blas(ao, pos.cpu().numpy())
+            G64 = xl.gram_exact(a, pos).cpu().numpy()
+            assert normalized_err(G64, Go) <= 1e-9, ("fp64", K)
+            G32 = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+            assert normalized_err(G32, Go) <= 1e-4, ("fp32", K)
