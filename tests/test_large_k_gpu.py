@@ -316,3 +316,22 @@ def test_every_kernel_boundary_in_k(xl, orc):
             assert normalized_err(G64, Go) <= 1e-9, ("fp64", K)
             G32 = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
             assert normalized_err(G32, Go) <= 1e-4, ("fp32", K)
+
+
+def test_receivers_every_boundary_in_k(xl, orc):
+    """Receiver dispatch boundaries (thread / warp / CTA shared-memory / tiled DMMA Cholesky):
+    CAP, ZF, MMSE, MRC per drop within 1e-6 bit of the oracle on the same fp64 Gram, flags
+    identical, for K on both sides of each boundary."""
+    fc = 100e9
+    a = xl.Array.ula(4001, fc)
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    for K in [8, 9, 64, 65, 96, 97, 128, 160, 161]:
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 3, seed=200 + K)
+        G = xl.gram_exact(a, pos)
+        r, fl = xl.sum_rate(G, [0.0, 10.0], rec)
+        ro, flo = orc.sum_rate(G.cpu().numpy(), [0.0, 10.0], rec)
+        assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo), K
+        rg = r.cpu().numpy()
+        ok = ~np.isnan(ro)
+        assert np.array_equal(np.isnan(rg), ~ok), K
+        assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 1e-6, K
