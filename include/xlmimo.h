@@ -110,15 +110,18 @@ XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint
  *     (fp32 only; for K > 64 as L2-sized chunks of scaled fp16 pairs, below).
  * pos (dev [n_drops][K][3]); gram (dev [n_drops][K][K][2]) full Hermitian with
  * Im G(i,i) = 0.  K <= 1024 -- 64 < K <= 1024 are the NEXT-3/E1-E3 user counts,
- * fp64 on DMMA, in blocks of 64 users up to K = 128 and above
+ * fp64 on DMMA in the 3M complex form, fused up to K = 128
+ * (blocks of 8 users dealt to warps as stars; 120 < K <= 128 in two launches) and above
  * it as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
- * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 in
- * blocks of 64 users (a UPA needing rows that are a multiple of 8, one level), the
- * operands generated in-kernel up to K = 128 and, from K = 129 on or in MATERIALIZED
- * mode, read by TMA from chunks of H written to the workspace as fp16 pairs with a
- * per-drop power-of-two scale (11 significant bits, as TF32; <= 112 MB per unit of
- * drops x 4096-element chunks, so the reads hit L2).  Below 1024 elements an fp32
- * request with K > 64 runs the fp64 kernels (TF32 rounding would not average out).
+ * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 (a UPA
+ * needing rows that are a multiple of 8, one level): fused up to K = 128 with the
+ * operands generated in-kernel as fp16 with a per-drop power-of-two scale (11
+ * significant bits, as TF32; 64 < K <= 128 as a launch over all users' columns for the
+ * first 64 rows plus one over the rest), and, from K = 129 on or in MATERIALIZED mode,
+ * read by TMA from chunks of H written to the workspace as scaled fp16 pairs (<= 112 MB
+ * per unit of drops x 4096-element chunks, so the reads hit L2).  Below 1024 elements
+ * an fp32 request with K > 64 runs the fp64 kernels (the operand rounding would not
+ * average out).
  * ws may be NULL iff the query returns 0.
  * EINVAL: bad array/arguments; EUNSUPPORTED: K > 1024, fp32 with K > 64 on an
  * unsupported UPA or with nested levels, or FP64 + MATERIALIZED; EWORKSPACE: ws_bytes
@@ -216,7 +219,7 @@ XLMIMO_API int xlmimo_app_a_bounds(const double *gram, int32_t K, int64_t n_drop
  *   per_drop (dev [n_drops][n_n][n_snr][n_recv] or NULL).
  * array->n_y is ignored (the grid is n_list).  Synchronises `stream` before return.
  * K <= 1024 -- the paper's K = 100 curves.  For K > 64 an fp32 exact sweep
- * runs the tcgen05 Gram once per N (those kernels have no nested levels): the same
+ * runs the tcgen05 Gram once per N (those launches have no nested levels): the same
  * Grams, O(sum N) instead of O(max N) work.
  * EINVAL also for n_list not ascending / mixed parity, t not in (0,1). */
 XLMIMO_API size_t xlmimo_saturation_sweep_workspace(const xlmimo_array_t *array, const int64_t *n_list, int32_t n_n,
