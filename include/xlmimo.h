@@ -114,10 +114,10 @@ XLMIMO_API int xlmimo_draw_words(int32_t K, int64_t n_drops, uint64_t seed, uint
  * (blocks of 8 users dealt to warps as stars; 120 < K <= 128 in two launches) and above
  * it as a chunked Hermitian rank-k update (H formed in the workspace a chunk of
  * elements at a time, <= 64 MB so it stays in L2, never whole); fp32 on tcgen05 (a UPA
- * needing rows that are a multiple of 8, one level): fused up to K = 128 with the
+ * needing rows that are a multiple of 8, one level): fused up to K = 256 with the
  * operands generated in-kernel as fp16 with a per-drop power-of-two scale (11
- * significant bits, as TF32; 64 < K <= 128 as a launch over all users' columns for the
- * first 64 rows plus one over the rest), and, from K = 129 on or in MATERIALIZED mode,
+ * significant bits, as TF32; K > 64 as launches per block of 64 row users over at most
+ * 128 column users each), and, from K = 257 on or in MATERIALIZED mode,
  * read by TMA from chunks of H written to the workspace as scaled fp16 pairs (<= 112 MB
  * per unit of drops x 4096-element chunks, so the reads hit L2).  Below 1024 elements
  * an fp32 request with K > 64 runs the fp64 kernels (the operand rounding would not
@@ -273,7 +273,7 @@ XLMIMO_API int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, d
  * running entry points.  The library reads no environment variables.
  *   XLMIMO_OPT_LARGE_K      fp64 Gram for 64 < K: 1 block pairs, 2 chunked SYRK
  *   XLMIMO_OPT_PAIR         fp32 Gram for 64 < K: 1 TF32 block pairs generated in-kernel, 2 TMA-fed
- *                           fp16 chunks (default: the fused fp16 kernel up to K = 128, chunks above)
+ *                           fp16 chunks (default: the fused fp16 kernel up to K = 256, chunks above)
  *   XLMIMO_OPT_GRAM_KERNEL  fused Gram, K <= 64: 1 split (K in {4,8}, ULA, fp64), 2 DMMA (K <= 16,
  *                           fp64), 3 CUDA-core register/tile kernels, 4 64-bit-index DMMA (K > 16)
  *   XLMIMO_OPT_SPLIT_NT     split kernel block variant: 64, 128, 192 (128 x 3/SM) or 256

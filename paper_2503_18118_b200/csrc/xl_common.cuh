@@ -243,6 +243,11 @@ int fused_tc_chunks(int64_t N, int64_t n_drops);
 int stream_tc_parts(int K);
 bool fused_tc_supported(const ArrayP &a, int K);
 bool fused_tc_wide_supported(const ArrayP &a, int K);
+int fused_tc_launches(int K);
+#ifndef XL_FUSED_TC_MAXK
+#define XL_FUSED_TC_MAXK 256  // tools/ab_cross.py: the fused launches win or tie up to 256
+#endif
+constexpr int kFusedTcMaxK = XL_FUSED_TC_MAXK;  // fp32 fused (generated fp16 operands) up to this K
 bool fused_tc_supported_geometry(const ArrayP &a);
 int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, int64_t N, double *ws,
                     cudaStream_t s);

@@ -1663,14 +1663,14 @@ constexpr int kSyrkMinK = 121;
 // K > 64, fp32: block pairs fed by TMA from materialised, L2-sized chunks of H from
 // kStreamPairMinK users on (generation once per coefficient instead of once per pair),
 // generated in-kernel below; XLMIMO_OPT_PAIR = 1 (gen) | 2 (stream) overrides.
-constexpr int kStreamPairMinK = 129;  // fp16 chunks win from K = 65 (35 000 elements: K = 100 11.7 vs 13.5 ms, 160 9.2 vs
+constexpr int kStreamPairMinK = 129;  // and above kFusedTcMaxK (256): the fused launches win below  // fp16 chunks win from K = 65 (35 000 elements: K = 100 11.7 vs 13.5 ms, 160 9.2 vs
                                       // 14.8, 352 7.7 vs 16.8); up to 128 the in-kernel path stays, its TMEM folding
                                       // keeping E1/E2's K = 100 rates unbiased (R28)
 bool use_stream_pair(int K) {
   const int64_t o = xlh::option(XLMIMO_OPT_PAIR);
   if (o == 1) return false;
   if (o == 2) return true;
-  return K >= kStreamPairMinK;
+  return K >= kStreamPairMinK && K > xlh::kFusedTcMaxK;
 }
 // 64 < K <= 128 fp32: the fused kernel's wide + narrow launches (xl_stream_tc.cu) unless
 // XLMIMO_OPT_PAIR = 1 (the block-pair kernel) or 2 (the pair stream) / MATERIALIZED
@@ -2019,7 +2019,7 @@ int launch_gram_exact(const ArrayP &a, const double *pos, int K, int64_t n_drops
         KTimer tm(s, "gram_fused_tc_f16");
         rc = launch_fused_tc(a, pos, K, n_drops, N, (double *)ws, s);
         tm.stop(s);
-        count_launch(2);
+        count_launch(fused_tc_launches(K));
       } else if (use_stream_pair(K) || mode == XLMIMO_MATERIALIZED) {  // times and counts its own launches
         const size_t part =
             ((size_t)n_drops * fused_tc_pair_chunks(N) * ((size_t)K * (K + 1) / 2) * 2 * sizeof(double) + 255) /

@@ -435,7 +435,9 @@ struct FusedParams {
   int64_t n_drops;
   uint32_t tmem_cols;
   GenConst g;        // the generator's launch constants (TE of the instantiation)
-  int u0, k_gen;     // users generated: u0 .. u0 + k_gen - 1 of the K (rows 2u, 2u + 1)
+  int u0, k_gen;     // users generated: u0 .. u0 + k_gen - 1 of the K (rows 2u, 2u + 1) ...
+  int ka, b0;        // ... or, with b_row > 0, u0 .. u0 + ka - 1 then b0 .. b0 + k_gen - ka - 1
+  int b_row;         // first stage row of the MMA's B operand: 0 (B = all rows) or 2 ka (cross)
   int n_acc;         // TMEM accumulators (2: double-buffered, 1 when 3 n_mma > 512)
 };
 
@@ -719,9 +721,11 @@ __device__ __forceinline__ float drop_scale(const GenUser *su, int K, double sqr
   for (int u = 1; u < K; ++u) m = fmin(m, su[u].xz2);
   return scale_of_min_xz2(m, sqrt_beta0);
 }
-__device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int kind, double sqrt_beta0, int lane) {
-  double m = INFINITY;
-  for (int u = lane; u < K; u += 32) m = fmin(m, xl::make_user(pos + u * 3, kind, sqrt_beta0).xz2);
+__device__ __forceinline__ float epi_drop_scale(const double *pos, int K, int kind, double sqrt_beta0, int lane,
+                                                int ka = 1 << 30, int boff = 0) {
+  double m = INFINITY;  // users 0 .. ka - 1, then ka + boff ..: the generators' users
+  for (int u = lane; u < K; u += 32)
+    m = fmin(m, xl::make_user(pos + (u < ka ? u : u + boff) * 3, kind, sqrt_beta0).xz2);
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
   return scale_of_min_xz2(m, sqrt_beta0);
@@ -818,7 +822,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
       if (k >= kstart) continue;  // no stage of this item for this group
       asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(C::GenThreads) : "memory");
       for (int u = gtid; u < KG; u += C::GenThreads) {
-        const double *p = P.pos + (d * K + P.u0 + u) * 3;
+        const double *p = P.pos + (d * K + (u < P.ka ? P.u0 + u : P.b0 + (u - P.ka))) * 3;
         const xl::UserC uc = xl::make_user(p, P.kind, P.sqrt_beta0);
         su[u] = GenUser{uc.xz2, uc.y, uc.z, (float)uc.amp, 0.0f};
       }
@@ -916,7 +920,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
 #else
 #pragma unroll
             for (int k = 0; k < kFBoxK / 16; ++k)  // 16 fp16 (32 B) per MMA along K
-              mma_f16(tmem_d, ds + 2 * k, ds + 2 * k, idesc, (kb > s0 || k > 0) ? 1u : 0u);
+              mma_f16(tmem_d, ds + 2 * k, ds + (uint64_t)(P.b_row * 8) + 2 * k, idesc, (kb > s0 || k > 0) ? 1u : 0u);
             mma_commit(&empty[stage]);
 #endif
           }
@@ -934,14 +938,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
     const int lr = row - blk * P.rb;
     const int i = P.u0 + (lr >> 1), plane = lr & 1;  // the drop's user index of this row
     const int col0 = blk * P.rb;
-    const bool has_users = 32 * q - blk * P.rb < R;
+    const bool cross = P.b_row > 0;  // rows = users u0.., columns = users b0..
+    const bool has_users = 32 * q - blk * P.rb < (cross ? 2 * P.ka : R);
+    const int n_cols = R - P.b_row, j0 = cross ? P.b0 : P.u0;
     const int NP = K * (K + 1) / 2;
     int local = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t d = it / P.n_chunks;
       const int c = (int)(it - d * P.n_chunks);
       double *out = P.ws + (((size_t)d * P.n_chunks + c) * P.nblk + blk) * (size_t)(2 * NP);
-      const float sc = epi_drop_scale(P.pos + (d * K + P.u0) * 3, KG, P.kind, P.sqrt_beta0, lane);
+      const float sc = epi_drop_scale(P.pos + (d * K + P.u0) * 3, KG, P.kind, P.sqrt_beta0, lane, P.ka,
+                                      P.b0 - P.u0 - P.ka);
       const double post = 1.0 / ((double)sc * (double)sc);  // exact: sc is a power of two
       const int ns = item_stages(P.N, c, kb_per_chunk, kFBoxK * P.nblk, P.chunk);
       for (int s0 = 0; s0 < ns; s0 += kFSubStages, ++local) {
@@ -951,8 +958,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) gram_fused_tc_kernel(FusedPa
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (has_users)
           drain_subchunk(tmem + ((uint32_t)(32 * q) << 16), (uint32_t)(acc * P.n_mma + col0),
-                         (uint32_t)(P.n_acc * P.n_mma + col0), R, K, i, plane, s0 == 0, s0 + kFSubStages >= ns,
-                         out, post, P.u0);
+                         (uint32_t)(P.n_acc * P.n_mma + col0), n_cols, K, i, plane, s0 == 0, s0 + kFSubStages >= ns,
+                         out, post, j0);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -1480,9 +1487,13 @@ int stream_tc_chunks(int64_t N) { return (int)((N + kChunk - 1) / kChunk); }
 // accumulation unbiased at any length) that still leaves >= 4 waves of items, so the fp64
 // partials -- the kernel's only DRAM writes -- stay a small multiple of the output.
 int fused_tc_chunk(int64_t N, int64_t n_drops) {
-  int c = kChunk;
+  int64_t c = kChunk;
   while (c < 65536 && n_drops * ((N + 2 * c - 1) / (2 * c)) >= 4 * 148) c *= 2;
-  return c;
+  // the same number of items, of equal length (a ragged last item would idle its CTA's
+  // generators): a multiple of 256 elements, whole stages for every block stacking
+  const int64_t n = (N + c - 1) / c;
+  const int64_t e = (N + n - 1) / n;
+  return (int)((e + 255) / 256 * 256);
 }
 int fused_tc_chunks(int64_t N, int64_t n_drops) {
   const int c = fused_tc_chunk(N, n_drops);
@@ -1494,10 +1505,10 @@ int fused_tc_chunks(int64_t N, int64_t n_drops) {
 // kTaskE; other UPAs take the CUDA-core fp32 kernel.
 bool fused_tc_supported_geometry(const ArrayP &a) { return a.kind == XLMIMO_ULA || (a.n_y % kTaskE) == 0; }
 bool fused_tc_supported(const ArrayP &a, int K) { return K >= 9 && K <= 64 && fused_tc_supported_geometry(a); }
-// 64 < K <= 128 on the fused kernel (wide + narrow launches) unless XLMIMO_OPT_PAIR picks
+// 64 < K <= kFusedTcMaxK on the fused kernel (wide, cross and narrow launches) unless XLMIMO_OPT_PAIR picks
 // the block-pair kernel (1) or the TMA-fed pair stream (2)
 bool fused_tc_wide_supported(const ArrayP &a, int K) {
-  return K > 64 && K <= 128 && fused_tc_supported_geometry(a);
+  return K > 64 && K <= kFusedTcMaxK && fused_tc_supported_geometry(a);
 }
 
 // Fused fp32 Gram on tcgen05: partials [drop][chunk][block][NP][2] (NP = K(K+1)/2) into ws,
@@ -1531,13 +1542,18 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   // 16-element tasks wherever a task stays in one array row (every ULA; UPA rows of 16k)
   const bool te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
   P.g = make_gen_const(a, N, te16 ? 16 : 8);
-  auto launch = [&](int u0, int k_gen, bool wide) {
+  int n_launch = 0;
+  auto launch = [&](int u0, int k_gen, bool wide, int b0 = 0, int kb = 0) {
+    ++n_launch;
     P.u0 = u0;
-    P.k_gen = k_gen;
+    P.k_gen = k_gen + kb;
+    P.ka = k_gen;
+    P.b0 = b0;
+    P.b_row = kb > 0 ? 2 * k_gen : 0;
     if (wide || K > 64) {  // one element block per stage
       P.rb = wide ? 256 : kRows;
       P.nblk = 1;
-      P.n_mma = (2 * k_gen + 15) / 16 * 16;
+      P.n_mma = (2 * (kb > 0 ? kb : k_gen) + 15) / 16 * 16;
     } else {
       P.rb = rows_per_block(K);
       P.nblk = kRows / P.rb;
@@ -1567,9 +1583,30 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
     return check_launch("gram_fused_tc_kernel");
   };
   if (K <= 64) return launch(0, K, false);
-  const int rc = launch(0, K, true);
-  if (rc) return rc;
-  return launch(64, K - 64, false);
+  // rows in blocks of 64 users a0..: a wide launch over users a0 .. a0 + 127 (the block's
+  // entries with j < a0 + 128) or a narrow one for the last block, then cross launches
+  // (the block's 64 rows x 64 further users per launch) for the columns beyond
+  for (int a0 = 0; a0 < K; a0 += 64) {
+    const int rest = K - a0;
+    int rc = rest <= 64 ? launch(a0, rest, false) : launch(a0, rest < 128 ? rest : 128, true);
+    if (rc) return rc;
+    for (int b0 = a0 + 128; b0 < K; b0 += 64) {
+      rc = launch(a0, 64, true, b0, K - b0 < 64 ? K - b0 : 64);
+      if (rc) return rc;
+    }
+  }
+  return XLMIMO_OK;
+}
+
+// launches of launch_fused_tc for K users (the caller's launch counter)
+int fused_tc_launches(int K) {
+  if (K <= 64) return 1;
+  int n = 0;
+  for (int a0 = 0; a0 < K; a0 += 64) {
+    ++n;
+    for (int b0 = a0 + 128; b0 < K; b0 += 64) ++n;
+  }
+  return n;
 }
 
 int stream_tc_parts(int K) { return kRows / rows_per_block(K); }

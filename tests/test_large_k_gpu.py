@@ -133,6 +133,46 @@ def test_gram_fp32_wide_fused(xl, orc, kind, n_y, n_z, K, D):
     assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
 
 
+@pytest.mark.parametrize("kind,n_y,n_z,K,D", [("ula", 5001, 1, 129, 2), ("ula", 3000, 1, 200, 2),
+                                              ("ula", 20000, 1, 256, 1), ("upa", 40, 60, 150, 2),
+                                              ("upa", 48, 50, 193, 1)])
+def test_gram_fp32_cross_fused(xl, orc, kind, n_y, n_z, K, D):
+    """128 < K <= 256 at fp32 on the fused kernel: per block of 64 row users a wide launch
+    (users a0 .. a0 + 127) or a narrow one, plus cross launches (the block's rows x 64 further
+    users, the MMA's B operand after the A rows in the stage) -- every entry against the
+    oracle (1e-4 normalised): a single extra user (K = 129), ragged cross blocks (200, 193),
+    K = 256, UPA rows of 8k (TE = 8) and 16k; Hermitian, real diagonal."""
+    fc = 100e9
+    if kind == "ula":
+        a, ao = xl.Array.ula(n_y, fc), orc.array("ula", n_y=n_y, fc_hz=fc)
+        pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=K + 7)
+    else:
+        a, ao = xl.Array.upa(n_y, n_z, fc), orc.array("upa", n_y=n_y, n_z=n_z, fc_hz=fc)
+        pos = xl.gen_drops(xl.Users.polar((2.0, 20.0), (-60, 60), (-30, 30)), K, D, seed=K + 7)
+    G = xl.gram_exact(a, pos, precision=xl.FP32).cpu().numpy()
+    Go = orc.gram_exact_blas(ao, pos.cpu().numpy())
+    assert normalized_err(G, Go) <= 1e-4
+    assert np.all(G.diagonal(axis1=1, axis2=2).imag == 0)
+    assert np.array_equal(G, np.conj(np.transpose(G, (0, 2, 1))))
+
+
+def test_fp32_rates_cross_fused(xl, orc):
+    """K = 192 at fp32 through the cross launches: per-drop CAP/ZF/MMSE/MRC rates against
+    the oracle's fp64 rates, ergodic within 1e-3 bit, every drop within 5e-3 (R29)."""
+    K, D = 192, 4
+    a, ao = xl.Array.ula(12000, 100e9), orc.array("ula", n_y=12000, fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=23)
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE | xl.RECV_MRC
+    r, fl = xl.sum_rate(xl.gram_exact(a, pos, precision=xl.FP32), [0.0, 10.0], rec)
+    ro, flo = orc.sum_rate(orc.gram_exact_blas(ao, pos.cpu().numpy()), [0.0, 10.0], rec)
+    assert np.array_equal(fl.cpu().numpy().astype(np.uint32), flo)
+    rg = r.cpu().numpy()
+    ok = ~np.isnan(ro)
+    assert np.array_equal(np.isnan(rg), ~ok)
+    assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 5e-3
+    assert np.max(np.abs(np.nanmean(rg, axis=0) - np.nanmean(ro, axis=0))) <= 1e-3
+
+
 def test_gram_large_k_fp32_e3(xl, orc):
     """E3 size in fp32: K = 1000, M = 35 000 against the oracle (1e-4) and the paper's gap."""
     a = xl.Array.ula(35000, 100e9)
