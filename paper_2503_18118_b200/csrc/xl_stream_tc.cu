@@ -38,9 +38,9 @@ constexpr int kChunk = 8192;           // elements per work item (one fp64 parti
 // the TMEM accumulator restarts every kSubStages stages (4 MMAs each: <= 64 MMAs, bias
 // <= ~3e-6); the epilogue folds the sub-chunk sums into a running fp32 sum kept in a third
 // TMEM region (drain_subchunk) and writes the item's fp64 partial after the last one.
-constexpr int kSubStages = 16;
-constexpr int kFSubStages = 8;
-constexpr int kPSubStages = 8;  // pair kernel: 8 stages x 4 MMAs per TMEM sub-chunk (K = 100 rates: -4e-4 bit at 16)  // fused kernel: fp16 stages hold 64 elements, so 8 stages = 32 MMAs x 16
+constexpr int kSubStages = 16;   // stream kernel (TF32): 16 stages x 4 MMAs (K = 8 each)
+constexpr int kFSubStages = 8;   // fused kernel (fp16): 8 stages of 64 elements = 32 MMAs (K = 16 each)
+constexpr int kPSubStages = 8;   // pair kernel: 8 stages x 4 MMAs (K = 100 rates: -4e-4 bit at 16)
 constexpr int kThreads = 256;
 
 // element blocks stacked per stage in the 128 MMA rows: 2K <= 32 -> 4 blocks, <= 64 -> 2, else 1
@@ -663,7 +663,7 @@ __device__ __forceinline__ void gen_task_tf32(const GenUser &uc, int64_t t0, int
 
 constexpr int kGenWarps = 2;       // pair kernels: warps per generator group (arrivals per full barrier)
 constexpr int kGenThreads = 32 * kGenWarps;
-// Fused K <= 64 kernel: kFGroups groups of kFGenWarps warps; group g makes stages
+// Fused kernel (narrow stages, FCfg<false>): kFGroups groups of kFGenWarps warps; group g makes stages
 // k = g (mod kFGroups) into ring slot k % kFStages.  The MMA consumes stages in order, so a
 // group's next stage (k + groups) waits for slot k + groups - slots to be consumed; with
 // parity waits are exact while groups <= slots.  Measured (148 cfg5 drops / 10^4 cfg3 /
