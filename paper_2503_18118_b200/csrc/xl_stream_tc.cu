@@ -693,10 +693,10 @@ constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one
 // the TMEM base word (+16 B), rounded up to 64 B
 constexpr int kFSuOff = (kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 63) & ~63;
 
-// Stage shapes of gram_fused_tc_kernel: narrow (K <= 64: 128 rows = 64 users, 12 slots, 12
-// groups of 2 warps) and wide (64 < K <= 128: 256 rows = the MMA's N, 6 slots of 32 KB, 6
-// groups of 4 warps; the A operand is the first 128 rows).  Same warps, threads and
-// shared-memory budget.
+// Stage shapes of gram_fused_tc_kernel: narrow (<= 64 users: 128 rows, 12 slots, 12 groups
+// of 2 warps) and wide (<= 128 users: 256 rows, 6 slots of 32 KB, 6 groups of 4 warps; the
+// MMA's A operand is the first 128 rows, its B operand all rows -- or, for a cross launch,
+// the rows after them).  Same warps, threads and shared-memory budget.
 template <bool WIDE>
 struct FCfg {
   static constexpr int Groups = WIDE ? 6 : kFGroups, GenWarps = WIDE ? 4 : kFGenWarps;
