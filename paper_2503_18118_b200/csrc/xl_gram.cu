@@ -883,6 +883,15 @@ struct Mt2 {
   static constexpr size_t smem = tiles_bytes > stage_bytes ? tiles_bytes : stage_bytes;
   static constexpr bool fits = smem <= 220 * 1024;
 };
+// Mt2<G, SM, NBUF>::fits without instantiating Mt2 (launch-time shape choices)
+template <int G, int SM, int NBUF>
+constexpr bool mt2_fits() {
+  constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
+  constexpr int JG = J / (JPW * Mt2Launches<G>::value);
+  constexpr size_t tiles = (size_t)kMt2Planes * NBUF * S * G * 32 * sizeof(double);
+  constexpr size_t stage = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
+  return (tiles > stage ? tiles : stage) <= 220 * 1024;
+}
 
 // Star plan of the MT2 kernel: star s (warp's job group) = centre cen[s] and partners
 // par[s][k]; blk[g1 * 16 + g2] (g1 <= g2) = 2 * (job s * JPW + k) + (1 if the star holds
@@ -1213,11 +1222,11 @@ int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
   if constexpr (G <= 8) {
-    if (nbuf == 2 || !Mt2<G, 2, 3>::fits)
+    if (nbuf == 2 || !mt2_fits<G, 2, 3>())
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
   // K > 64: the ring only (half-length tiles when three planes do not fit)
-  if constexpr (Mt2<G, 2, 3>::fits)
+  if constexpr (mt2_fits<G, 2, 3>())
     return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
   else
     return ula ? launch_mt2_k<G, 1, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 1, 3, XLMIMO_UPA>(P, n_blocks, s);
@@ -1773,7 +1782,7 @@ KernelChoice choose_kernel(const ArrayP &a, int K, int precision) {
 template <int G, int KIND>
 void launch_mma(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int v = mma_variant();
-  if (G == 1) {
+  if constexpr (G == 1) {
     switch (v) {
       case 1: gram_mma_kernel<G, 256, 6, KIND><<<(unsigned)n_blocks, 256, 0, s>>>(P); break;
       case 2: gram_mma_kernel<G, 128, 8, KIND><<<(unsigned)n_blocks, 128, 0, s>>>(P); break;

@@ -681,7 +681,6 @@ constexpr int kGenThreads = 32 * kGenWarps;
 constexpr int kFGenWarps = XL_FGEN_WARPS;
 constexpr int kFGroups = XL_FGEN_GROUPS;
 constexpr int kFStages = XL_FSTAGES;
-constexpr int kFGenThreads = 32 * kFGenWarps;
 constexpr int kEpiWarp0 = kFGenWarps * kFGroups;   // 24: warps 24..27 = TMEM lane quadrants 0..3
 constexpr int kMmaWarp = kEpiWarp0 + 4;            // 28
 constexpr int kFusedThreads = 32 * (kMmaWarp + 1);  // 928
@@ -689,9 +688,6 @@ static_assert(kEpiWarp0 % 4 == 0, "epilogue warp q must sit in TMEM lane quadran
 static_assert(kFGroups <= kFStages, "a generator group may not lap a ring slot (parity waits)");
 
 constexpr int kFBoxK = 64;  // fp16 elements per 128-B row of a fused stage (one swizzle atom)
-// byte offset of su_all from the 1024-aligned base: stages, full/empty[kFStages], tfull/tempty[2],
-// the TMEM base word (+16 B), rounded up to 64 B
-constexpr int kFSuOff = (kFStages * kStageBytes + (2 * kFStages + 4) * 8 + 16 + 63) & ~63;
 
 // Stage shapes of gram_fused_tc_kernel: narrow (<= 64 users: 128 rows, 12 slots, 12 groups
 // of 2 warps) and wide (<= 128 users: 256 rows, 6 slots of 32 KB, 6 groups of 4 warps; the
@@ -702,6 +698,8 @@ struct FCfg {
   static constexpr int Groups = WIDE ? 6 : kFGroups, GenWarps = WIDE ? 4 : kFGenWarps;
   static constexpr int Stages = WIDE ? 6 : kFStages, Rows = WIDE ? 256 : kRows, MaxUsers = Rows / 2;
   static constexpr int GenThreads = 32 * GenWarps, StageBytes = Rows * 128, UBits = WIDE ? 7 : 6;
+  // byte offset of su_all from the 1024-aligned base: stages, full/empty[Stages], tfull/tempty[2],
+  // the TMEM base word (+16 B), rounded up to 64 B
   static constexpr int SuOff = (Stages * StageBytes + (2 * Stages + 4) * 8 + 16 + 63) & ~63;
   static_assert(GenWarps * Groups == kEpiWarp0 && Groups <= Stages, "FCfg warps / slots");
 };
@@ -1542,9 +1540,7 @@ int launch_fused_tc(const ArrayP &a, const double *pos, int K, int64_t n_drops, 
   // 16-element tasks wherever a task stays in one array row (every ULA; UPA rows of 16k)
   const bool te16 = a.kind == XLMIMO_ULA || a.n_y % 16 == 0;
   P.g = make_gen_const(a, N, te16 ? 16 : 8);
-  int n_launch = 0;
   auto launch = [&](int u0, int k_gen, bool wide, int b0 = 0, int kb = 0) {
-    ++n_launch;
     P.u0 = u0;
     P.k_gen = k_gen + kb;
     P.ka = k_gen;
