@@ -1,4 +1,4 @@
-"""Per-config, per-path timings on one GPU (secondary to bench.py, which times cfg2).
+"""Per-config, per-path timings on one GPU (secondary to bench.py and its sub-records).
 
     python tools/bench_configs.py [cfgs...]      e.g. 1 3 4 5
 
