@@ -396,3 +396,26 @@ def test_fp32_rates_wide_single_accumulator(xl, orc):
     assert np.array_equal(np.isnan(rg), ~ok)
     assert np.max(np.abs(rg[ok] - ro[ok]), initial=0.0) <= 5e-3
     assert np.max(np.abs(np.nanmean(rg, axis=0) - np.nanmean(ro, axis=0))) <= 1e-3
+
+
+@pytest.mark.parametrize("K,prec,tol", [(128, "fp64", 1e-6), (160, "fp32", 1e-3)])
+def test_sweep_large_k_paths(xl, orc, K, prec, tol):
+    """The exact saturation sweep through the K > 120 paths: fp64 K = 128 on MT2's two
+    launches per tile (nested levels in one pass), fp32 K = 160 on the fused kernel's wide /
+    cross / narrow launches once per N (the workspace the largest level's) -- ergodic means
+    and per-drop rates against the oracle's fp64 sweep (fp64 1e-6 bit; fp32 1e-3 ergodic,
+    5e-3 per drop), counts identical."""
+    D = 3
+    nl = [1024, 2048, 4000]
+    a, ao = xl.Array.ula(max(nl), 100e9), orc.array("ula", n_y=max(nl), fc_hz=100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, D, seed=31)
+    rec = xl.RECV_CAP | xl.RECV_ZF | xl.RECV_MMSE
+    res = xl.saturation_sweep(a, nl, K, D, [10.0], rec, pos=pos,
+                              precision=xl.FP64 if prec == "fp64" else xl.FP32, per_drop=True)
+    erg, nv, _, pd = orc.saturation_sweep(ao, nl, pos.cpu().numpy(), [10.0], rec, per_drop=True)
+    g = res["per_drop"].cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(pd))
+    ok = ~np.isnan(pd)
+    assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= (tol if prec == "fp64" else 5e-3)
+    assert np.array_equal(res["n_valid"], nv)
+    assert np.nanmax(np.abs(res["ergodic"] - erg)) <= tol
