@@ -54,7 +54,10 @@ def _ws(nbytes):
                                                 (5, 513, 1, 0, "ula"), (16, 4099, 1, 0, "ula"), (40, 1030, 1, 0, "ula"),
                                                 (16, 4096, 1, 1, "ula"), (5, 1001, 1, 1, "ula"), (12, 300, 0, 0, "upa"),
                                                 (12, 300, 1, 0, "upa"), (70, 300, 0, 0, "upa"),
-                                                (130, 1100, 1, 0, "ula"), (150, 1030, 0, 0, "ula")])
+                                                (130, 1100, 1, 0, "ula"), (150, 1030, 0, 0, "ula"),
+                                                (100, 2048, 1, 0, "ula"), (200, 2048, 1, 0, "ula"),
+                                                (256, 1100, 1, 0, "ula"), (300, 1100, 1, 0, "ula"),
+                                                (100, 2048, 1, 1, "ula"), (128, 1000, 0, 0, "ula")])
 def test_gram_exact_writes_in_bounds(xl, K, N, prec, mode, kind):
     D = 3
     if kind == "ula":
