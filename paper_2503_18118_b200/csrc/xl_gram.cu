@@ -397,14 +397,17 @@ __global__ void __launch_bounds__(kWarpBlock) gram_warp_kernel(GramParams P, int
   const int lane = threadIdx.x & 31;
   const int64_t drop = (int64_t)blockIdx.x * (kWarpBlock / 32) + (threadIdx.x >> 5);
   if (drop >= n_drops) return;  // whole warp
+  // lane k forms user k (its amplitude takes two fp64 square roots: once per user, not once
+  // per user and lane), then every lane takes the K users by shuffle
   double uy[K], uz[K], ux2[K], ua[K];
+  xl::UserC mine{1.0, 0.0, 0.0, 0.0};
+  if (lane < K) mine = xl::make_user(P.pos + (drop * K + lane) * 3, KIND, P.sqrt_beta0);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const xl::UserC u = xl::make_user(P.pos + (drop * K + k) * 3, KIND, P.sqrt_beta0);
-    ux2[k] = u.xz2;
-    uy[k] = u.y;
-    uz[k] = u.z;
-    ua[k] = u.amp;
+    ux2[k] = __shfl_sync(0xffffffffu, mine.xz2, k);
+    uy[k] = __shfl_sync(0xffffffffu, mine.y, k);
+    uz[k] = __shfl_sync(0xffffffffu, mine.z, k);
+    ua[k] = __shfl_sync(0xffffffffu, mine.amp, k);
   }
   double v[32];
 #pragma unroll
