@@ -419,3 +419,16 @@ def test_sweep_large_k_paths(xl, orc, K, prec, tol):
     assert np.max(np.abs(g[ok] - pd[ok]), initial=0.0) <= (tol if prec == "fp64" else 5e-3)
     assert np.array_equal(res["n_valid"], nv)
     assert np.nanmax(np.abs(res["ergodic"] - erg)) <= tol
+
+
+@pytest.mark.parametrize("K,prec", [(100, "fp32"), (160, "fp32"), (256, "fp32"), (128, "fp64")])
+def test_large_k_paths_bitwise_deterministic(xl, K, prec):
+    """The multi-launch paths (fused fp32 wide / cross / narrow, MT2's two launches for
+    K = 128) write disjoint entries with fixed reduction orders: repeated calls are equal bit
+    for bit."""
+    a = xl.Array.ula(9000, 100e9)
+    pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 40, seed=41)
+    p = xl.FP32 if prec == "fp32" else xl.FP64
+    g1 = xl.gram_exact(a, pos, precision=p)
+    g2 = xl.gram_exact(a, pos, precision=p)
+    assert torch.equal(g1, g2)
