@@ -51,10 +51,10 @@ from workloads import CONFIGS, cmac_per_drop  # noqa: E402
 W = CONFIGS[5]
 # FP64-pipe work model per channel coefficient: the cheapest fp64
 # evaluation found (coef_fast): distance^2 2, 1/r 5, r 1, quarter-cycle reduction 3,
-# sin+cos minimax 12, r^{-3/2} 6, phasor 2 (MUFU seeds and the quadrant F2I are off the
-# FP64 pipe); then 4 FP64-pipe ops per off-diagonal complex MAC (DFMA, or a quarter of
+# sin+cos minimax 10 (degree 4 each, |err| <= 4.7e-11: xl_common.cuh), r^{-3/2} 6, phasor 2
+# (MUFU seeds and the quadrant F2I are off the FP64 pipe); then 4 FP64-pipe ops per off-diagonal complex MAC (DFMA, or a quarter of
 # the four real m8n8k4 DMMAs per 2x2 plane block), 2 per diagonal one.
-FP64_OPS_PER_COEF = 31
+FP64_OPS_PER_COEF = 29
 MUFU_PER_COEF_FP32 = 2   # the fused fp32 generator: MUFU sin + cos per coefficient
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6545.3   # B200_PROFILING.md / MEASURED_PEAKS.json copy bandwidth

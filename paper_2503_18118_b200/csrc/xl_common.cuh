@@ -81,16 +81,30 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return fma(y * e, p, y);
 }
 
-// Near-minimax polynomials (Chebyshev-node least squares, fitted in 50-digit
-// arithmetic) in u = g^2 for g in [-1/2, 1/2]:
-//   sin(pi/2 g) = g * S(u)  (degree 5, |err| <= 3.4e-15),
-//   cos(pi/2 g) = C5(u)     (degree 5, |err| <= 5.6e-14).
+// Near-minimax polynomials (Chebyshev-node Lawson fits in 50-digit arithmetic) in u = g^2
+// for g in [-1/2, 1/2]: sin(pi/2 g) = g * S(u), cos(pi/2 g) = C(u).
+//   XL_SINCOS_DEG 5: |err| <= 1.9e-15 (sin) / 5.6e-14 (cos), 11 FP64 instructions;
+//   XL_SINCOS_DEG 4: |err| <= 1.7e-12 (sin) / 4.7e-11 (cos), 9 FP64 instructions.
+// Either bound keeps a Gram entry within 2 max|err| sqrt(G_ii G_jj) of the exact one
+// (Cauchy-Schwarz over the coefficient errors), under the fp64 tier's 1e-9 (R9).
+#ifndef XL_SINCOS_DEG
+#define XL_SINCOS_DEG 4
+#endif
+#if XL_SINCOS_DEG == 5
 __constant__ double kSinPoly[6] = {1.5707963267948898981, -0.64596409750431005807, 0.079692626155777645619,
                                    -0.0046817525918122076931, 0.0001604292666631208935,
                                    -3.5563888496214387972e-6};
-__constant__ double kCosPoly5[6] = {0.99999999999994445739, -1.23370055012016865, 0.25366950715400581474,
-                                    -0.020863468005621057384, 0.00091916175238771112641,
-                                    -0.000024850988050231297507};
+__constant__ double kCosPoly[6] = {0.99999999999994445739, -1.23370055012016865, 0.25366950715400581474,
+                                   -0.020863468005621057384, 0.00091916175238771112641,
+                                   -0.000024850988050231297507};
+#elif XL_SINCOS_DEG == 4
+__constant__ double kSinPoly[5] = {1.570796326757624, -0.6459640945217848, 0.0796925593294654,
+                                   -0.004681141492935389, 0.00015798452268659335};
+__constant__ double kCosPoly[5] = {0.9999999999529987, -1.2337005406691752, 0.25366920425732364,
+                                   -0.020860073028414316, 0.000903634758823505};
+#else
+#error "XL_SINCOS_DEG must be 4 or 5"
+#endif
 
 // 1/sqrt(x) to ~3e-13 relative (MUFU seed + one Newton step, 4 FP64 instructions):
 // enough for the amplitude r^{-3/2}, not for the phase (see rsqrt_nr).
@@ -105,8 +119,8 @@ __device__ __forceinline__ double rsqrt_newton(double x) {
 // coefficient.  Phase: q4 = 4 r/lambda (quarter cycles), k = rint(q4) (FRND),
 // quadrant = k mod 4 (F2I, XU pipe), g = q4 - k in [-1/2, 1/2] exactly, angle =
 // (pi/2)(k + g): the fp64 range reduction of the north_star.  1/r to ~1 ulp
-// (Householder), r^{-3/2} to ~3e-13 (Newton), sin 3.4e-15 / cos 5.6e-14 abs:
-// 29 FP64-pipe instructions + 2 MUFU + 1 F2I per coefficient, no branches.
+// (Householder), r^{-3/2} to ~3e-13 (Newton), sin / cos as above: 29 (degree 5) or 27
+// (degree 4) FP64-pipe instructions + 2 MUFU + 1 F2I per coefficient, no branches.
 // c4 = 4 / lambda.
 __device__ __forceinline__ void coef_fast(double r2, double amp, double c4, double &re, double &im) {
   const double ir = rsqrt_nr(r2);
@@ -116,19 +130,14 @@ __device__ __forceinline__ void coef_fast(double r2, double amp, double c4, doub
   const int qd = (int)k;           // F2I on the XU pipe (q4 < 2^31)
   const double g = q4 - k;         // exact, |g| <= 1/2
   const double u = g * g;
-  double ps = kSinPoly[5];
-  ps = fma(ps, u, kSinPoly[4]);
-  ps = fma(ps, u, kSinPoly[3]);
-  ps = fma(ps, u, kSinPoly[2]);
-  ps = fma(ps, u, kSinPoly[1]);
-  ps = fma(ps, u, kSinPoly[0]);
+  double ps = kSinPoly[XL_SINCOS_DEG];
+#pragma unroll
+  for (int j = XL_SINCOS_DEG - 1; j >= 0; --j) ps = fma(ps, u, kSinPoly[j]);
   const double sn = ps * g;
-  double pc = kCosPoly5[5];
-  pc = fma(pc, u, kCosPoly5[4]);
-  pc = fma(pc, u, kCosPoly5[3]);
-  pc = fma(pc, u, kCosPoly5[2]);
-  pc = fma(pc, u, kCosPoly5[1]);
-  const double cs = fma(pc, u, kCosPoly5[0]);
+  double pc = kCosPoly[XL_SINCOS_DEG];
+#pragma unroll
+  for (int j = XL_SINCOS_DEG - 1; j >= 0; --j) pc = fma(pc, u, kCosPoly[j]);
+  const double cs = pc;
   const double a = amp * ir * rsqrt_newton(r);  // r^{-3/2}, ~3e-13 relative
   // quadrant q: (cos, sin) of (pi/2)(q + g) = q0 (cs, sn), q1 (-sn, cs), q2 (-cs, -sn), q3 (sn, -cs);
   // h = a (cos - j sin)  =>  re = a*c, im = a*(-s)

@@ -30,7 +30,7 @@ def build(name, src, flags):
         o = os.path.join(b.BUILD, os.path.basename(s) + ".o")
         if os.path.basename(s) == os.path.basename(src):
             o = os.path.join(out, os.path.basename(s) + ".o")
-            subprocess.check_call([b.NVCC, *b.ARCH, *b.FLAGS, *flags, "-c", s, "-o", o])
+            subprocess.check_call([b.NVCC, *b.ARCH, *b.FLAGS, *flags, "-c", src, "-o", o])
         objs.append(o)
     subprocess.check_call([b.NVCC, *b.ARCH, "-shared", "-cudart", "static", "-o", os.path.join(out, "libxlmimo.so"),
                            *objs])
