@@ -17,7 +17,7 @@ cap() { # tag cfg prec drops regex
 cap mt2_cfg5_d1000 5 fp64 1000 gram_mt2
 cap mt2_cfg4 4 fp64 1000 gram_mt2
 cap warp_cfg1 1 fp64 1000000 gram_warp
-cap mma_cfg3 3 fp64 10000 gram_mma_tiled
+cap mma_cfg3 3 fp64 10000 gram_mma_kernel
 cp profiles/r02/ncu_traffic_bench.json $O/ncu_traffic_bench.json
 python tools/ncu_traffic.py --merge $O/ncu_traffic_bench.json \
   $O/mt2_cfg5_d1000.ncu-rep:gram_fused_dmma_tiled_fp64:"cfg5 fp64 D=1000":1000 > $O/traffic.log 2>&1
