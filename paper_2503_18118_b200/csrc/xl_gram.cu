@@ -15,6 +15,7 @@
 //  tiles of 32 elements are generated into shared memory as interleaved complex,
 //  then each thread accumulates one 4x4 register block of the upper triangle
 //  over a subset of the tile's elements (kernel B).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -853,7 +854,22 @@ template <> struct Mt2Cfg<9> { static constexpr int JPW = 5, SG = 1, S = 4; };  
 template <> struct Mt2Cfg<10> { static constexpr int JPW = 5, SG = 1, S = 4; };  // 11 stars
 template <> struct Mt2Cfg<11> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 11 stars
 template <> struct Mt2Cfg<12> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 13 stars
+#ifndef XL_MT2_VAR13
+#define XL_MT2_VAR13 1
+#endif
+#if XL_MT2_VAR13
+// G = 13 (K = 97..104, E1's K = 100): 13 stars of 7 put 4 warps on one SM sub-partition and 3
+// on the others (the CTA runs at the busiest one's pace: 13/16); 16 stars of 6 or 5 blocks
+// (centred counts 5,5,5,6,...,6,11,11,12: a Landau score sequence) dealt so that each
+// sub-partition holds 22-23 blocks
+// (E1 field, K = 100, 1000 drops: 60.9 -> 58.3 ms; 20 stars of 5 or 4 at 96 registers: 64.2 ms)
+template <> struct Mt2Cfg<13> {
+  static constexpr int JPW = 6, SG = 1, S = 4, NSTAR = 16;
+  static constexpr int cent[13] = {5, 5, 5, 6, 6, 6, 6, 6, 6, 6, 11, 11, 12};
+};
+#else
 template <> struct Mt2Cfg<13> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 13 stars
+#endif
 template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 15 stars
 template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
 // 120 < K <= 128: 34 stars of 4 dealt to two launches of 17 warps (a single launch of 17
@@ -863,6 +879,11 @@ template <int G, typename = void>
 struct Mt2Launches { static constexpr int value = 1; };
 template <int G>
 struct Mt2Launches<G, decltype((void)Mt2Cfg<G>::NL, void())> { static constexpr int value = Mt2Cfg<G>::NL; };
+// variable-size stars (JPW or JPW - 1 blocks): Mt2Cfg<G>::NSTAR stars with centred counts cent[]
+template <int G, typename = void>
+struct Mt2Var { static constexpr int value = 0; };
+template <int G>
+struct Mt2Var<G, decltype((void)Mt2Cfg<G>::NSTAR, void())> { static constexpr int value = Mt2Cfg<G>::NSTAR; };
 
 // Tile planes: re, im and re - im, the 3M partner operand (A_p - B_p), formed once per
 // coefficient by the generator instead of once per star and step by the consumers (the
@@ -876,10 +897,11 @@ template <int G, int SM, int NBUF>  // SM: tile-length multiplier of Mt2Cfg<G>::
 struct Mt2 {
   static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
   static constexpr int NL = Mt2Launches<G>::value;  // launches sharing the stars
-  static constexpr int JG = J / (JPW * NL), NW = JG * SG, NT = 32 * NW;  // stars per launch
+  static constexpr int VAR = Mt2Var<G>::value;  // 0, or the star count of a variable-size plan
+  static constexpr int JG = VAR ? VAR : J / (JPW * NL), NW = JG * SG, NT = 32 * NW;  // stars per launch
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
-  static_assert(J % (JPW * NL) == 0 && S % SG == 0, "Mt2Cfg");
+  static_assert((VAR ? NL == 1 : J % (JPW * NL) == 0) && S % SG == 0, "Mt2Cfg");
   static constexpr int NPL = kMt2Planes;  // re, im (, re - im: the 3M partner operand)
   static constexpr size_t tiles_bytes = (size_t)NPL * NBUF * PLANE * sizeof(double);  // NBUF buffers x planes
   static constexpr size_t stage_bytes = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
@@ -890,7 +912,7 @@ struct Mt2 {
 template <int G, int SM, int NBUF>
 constexpr bool mt2_fits() {
   constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
-  constexpr int JG = J / (JPW * Mt2Launches<G>::value);
+  constexpr int JG = Mt2Var<G>::value ? Mt2Var<G>::value : J / (JPW * Mt2Launches<G>::value);
   constexpr size_t tiles = (size_t)kMt2Planes * NBUF * S * G * 32 * sizeof(double);
   constexpr size_t stage = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
   return (tiles > stage ? tiles : stage) <= 220 * 1024;
@@ -902,6 +924,7 @@ constexpr bool mt2_fits() {
 constexpr int kMt2MaxG = 16;
 struct StarPlan {
   int8_t cen[40];
+  int8_t nj[40];  // blocks of star s (JPW, or JPW - 1 in a variable-size plan)
   int8_t par[40][8];
   int16_t blk[kMt2MaxG * kMt2MaxG];
 };
@@ -996,6 +1019,7 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
   }
   const int jg = warp % JG, sg = warp / JG;
   const int coff = plan.cen[star0 + jg] * 32 + lane;  // the star's centre fragment
+  const int nj = C::VAR ? (int)plan.nj[star0 + jg] : JPW;  // blocks of this warp's star
   int poff[JPW];                                      // its partners' fragments
 #pragma unroll
   for (int k = 0; k < JPW; ++k) poff[k] = plan.par[star0 + jg][k] * 32 + lane;
@@ -1064,6 +1088,7 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
         const double as = ar + ai;
 #pragma unroll
         for (int k = 0; k < JPW; ++k) {
+          if (C::VAR && k >= nj) continue;  // a star of JPW - 1 blocks (warp-uniform)
           const double br = cre[so + poff[k]], bi = cim[so + poff[k]];
           const double bd = C::NPL == 3 ? cim[PLANE + so + poff[k]] : br - bi;
           dmma(acc[k][0], ar, br);  // P1
@@ -1187,6 +1212,7 @@ bool star_plan(int G, int JPW, StarPlan &pl) {
       if ((to[e] ? pb[e] : pa[e]) == v) list[m++] = to[e] ? pa[e] : pb[e];
     for (int q = 0; q < m; q += JPW, ++ns) {
       pl.cen[ns] = (int8_t)v;
+      pl.nj[ns] = (int8_t)JPW;
       for (int t = 0; t < JPW; ++t) {
         const int p = list[q + t];
         pl.par[ns][t] = (int8_t)p;
@@ -1199,12 +1225,85 @@ bool star_plan(int G, int JPW, StarPlan &pl) {
   return ns * JPW == G * (G + 1) / 2;
 }
 
+// Variable-size stars: orient the pairs so that group v centres exactly cent[v] blocks (its
+// diagonal included; cent - 1 must be a tournament score sequence, Landau), by the same
+// depth-first search with exact targets; cut each group's list into ceil(cent / JPW) stars
+// of JPW or JPW - 1 blocks; order the stars by size (largest first) so that warp w = star w
+// on sub-partition w % 4 gets an even share of blocks.  Jobs keep the slot stride JPW.
+bool star_plan_var(int G, int JPW, int NSTAR, const int *cent, StarPlan &pl) {
+  int pa[kMt2MaxG * (kMt2MaxG - 1) / 2], pb[kMt2MaxG * (kMt2MaxG - 1) / 2], n = 0;
+  for (int a = 0; a < G; ++a)
+    for (int b = a + 1; b < G; ++b) { pa[n] = a; pb[n] = b; ++n; }
+  int out[kMt2MaxG] = {0}, left[kMt2MaxG], to[kMt2MaxG * (kMt2MaxG - 1) / 2];
+  for (int v = 0; v < G; ++v) left[v] = G - 1;
+  auto can = [&](int v) { return out[v] <= cent[v] - 1 && out[v] + left[v] >= cent[v] - 1; };
+  std::vector<int> st;
+  int k = 0, choice = 0;
+  while (k < n) {
+    bool placed = false;
+    for (; choice < 2; ++choice) {
+      const int c = choice ? pb[k] : pa[k];
+      ++out[c]; --left[pa[k]]; --left[pb[k]];
+      if (can(pa[k]) && can(pb[k])) { to[k] = choice; st.push_back(choice); ++k; choice = 0; placed = true; break; }
+      --out[c]; ++left[pa[k]]; ++left[pb[k]];
+    }
+    if (placed) continue;
+    if (st.empty()) return false;
+    --k;
+    choice = st.back();
+    st.pop_back();
+    const int c = choice ? pb[k] : pa[k];
+    --out[c]; ++left[pa[k]]; ++left[pb[k]];
+    ++choice;
+  }
+  int scen[40], snj[40], spar[40][8], ns = 0;
+  for (int v = 0; v < G; ++v) {
+    if (out[v] + 1 != cent[v]) return false;
+    int list[kMt2MaxG], m = 0;
+    list[m++] = v;
+    for (int e = 0; e < n; ++e)
+      if ((to[e] ? pb[e] : pa[e]) == v) list[m++] = to[e] ? pa[e] : pb[e];
+    const int parts = (m + JPW - 1) / JPW, big = m - parts * (JPW - 1);  // parts of JPW, the rest JPW - 1
+    if (big < 0 || ns + parts > 40) return false;
+    for (int q = 0, i = 0; q < parts; ++q, ++ns) {
+      const int sz = q < big ? JPW : JPW - 1;
+      scen[ns] = v;
+      snj[ns] = sz;
+      for (int t = 0; t < JPW; ++t) spar[ns][t] = t < sz ? list[i + t] : v;
+      i += sz;
+    }
+  }
+  if (ns != NSTAR) return false;
+  int ord[40];
+  for (int i = 0; i < ns; ++i) ord[i] = i;
+  std::stable_sort(ord, ord + ns, [&](int x, int y) { return snj[x] > snj[y]; });
+  int total = 0;
+  for (int w = 0; w < ns; ++w) {
+    const int o = ord[w];
+    pl.cen[w] = (int8_t)scen[o];
+    pl.nj[w] = (int8_t)snj[o];
+    for (int t = 0; t < JPW; ++t) {
+      const int p = spar[o][t];
+      pl.par[w][t] = (int8_t)p;
+      if (t >= snj[o]) continue;
+      const int v = scen[o], job = w * JPW + t;
+      if (v <= p) pl.blk[v * kMt2MaxG + p] = (int16_t)(2 * job);
+      else pl.blk[p * kMt2MaxG + v] = (int16_t)(2 * job + 1);
+      ++total;
+    }
+  }
+  return total == G * (G + 1) / 2;
+}
+
 template <int G, int SM, int NBUF, int KIND>
 int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   using C = Mt2<G, SM, NBUF>;
   static_assert(C::fits, "Mt2 shared memory");
   static StarPlan plan;
-  static const bool ok = star_plan(G, C::JPW, plan);
+  static const bool ok = [] {
+    if constexpr (C::VAR) return star_plan_var(G, C::JPW, C::VAR, Mt2Cfg<G>::cent, plan);
+    else return star_plan(G, C::JPW, plan);
+  }();
   if (!ok) return xlh::set_error(XLMIMO_EUNSUPPORTED, "mt2: no star decomposition for G=%d, JPW=%d", G, C::JPW);
   const FastDiv fd = make_fastdiv((uint32_t)P.n_y);
   cudaFuncSetAttribute(gram_mt2_kernel<G, SM, NBUF, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
@@ -1226,6 +1325,12 @@ int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const bool ula = P.kind == XLMIMO_ULA;
   if constexpr (G <= 8) {
     if (nbuf == 2 || !mt2_fits<G, 2, 3>())
+      return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
+  }
+  // variable-size star plans (G = 13): full-length tiles and two buffers unless the ring is
+  // asked for (E1 field, K = 100, 1000 drops: 58.3 -> 57.2 ms)
+  if constexpr (Mt2Var<G>::value != 0 && mt2_fits<G, 2, 2>()) {
+    if (env != 3)
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
   // K > 64: the ring only (half-length tiles when three planes do not fit)
