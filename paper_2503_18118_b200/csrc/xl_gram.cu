@@ -846,14 +846,60 @@ template <> struct Mt2Cfg<3> { static constexpr int JPW = 2, SG = 4, S = 8; };  
 template <> struct Mt2Cfg<4> { static constexpr int JPW = 2, SG = 4, S = 10; };  // 5 stars, NW 20
 template <> struct Mt2Cfg<5> { static constexpr int JPW = 3, SG = 4, S = 8; };   // 5 stars, NW 20
 template <> struct Mt2Cfg<6> { static constexpr int JPW = 3, SG = 2, S = 8; };   // 7 stars, NW 14
+#ifndef XL_MT2_VARX
+#define XL_MT2_VARX 1
+#endif
+#if XL_MT2_VARX
+// 8 stars of 4 or 3 (centred counts 3,3,3,4,4,4,7) x 2 step groups = 16 warps instead of 7 x 2
+// (sub-partition loads 14 each instead of 16/16/12/12; K = 56: 19.8 -> 18.4 ms)
+template <> struct Mt2Cfg<7> {
+  static constexpr int JPW = 4, SG = 2, S = 8, NSTAR = 8;
+  static constexpr int cent[7] = {3, 3, 3, 4, 4, 4, 7};
+};
+#else
 template <> struct Mt2Cfg<7> { static constexpr int JPW = 4, SG = 2, S = 8; };   // 7 stars, NW 14
+#endif
 template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 9; };   // 12 stars, NW 12, 12 rows/warp
 // 64 < K <= 128 (the paper's K = 100 of E1/E2 and Fig. K_vs_E): one star per
 // warp, stars of a regular or near-regular tournament (warps not a multiple of 4 except G = 15)
+#ifndef XL_MT2_VAR9
+#define XL_MT2_VAR9 1
+#endif
+#if XL_MT2_VAR9
+// 12 stars of 4 or 3 (centred counts 4 x 6, 7 x 3) instead of 9 stars of 5 (SM sub-partition
+// loads 12/11/11/11 blocks instead of 15/10/10/10; K = 72: 34.8 -> 29.2 ms)
+template <> struct Mt2Cfg<9> {
+  static constexpr int JPW = 4, SG = 1, S = 4, NSTAR = 12;
+  static constexpr int cent[9] = {4, 4, 4, 4, 4, 4, 7, 7, 7};
+};
+#else
 template <> struct Mt2Cfg<9> { static constexpr int JPW = 5, SG = 1, S = 4; };   // 9 stars
+#endif
+#if XL_MT2_VARX
+// 16 stars of 4 or 3 (centred counts 4 x 4, 6 x 3, 7 x 3): loads 14/14/14/13 instead of 15/15/15/10
+// (E1 field, K = 80, 1000 drops: 37.0 -> 36.0 ms)
+template <> struct Mt2Cfg<10> {
+  static constexpr int JPW = 4, SG = 1, S = 4, NSTAR = 16;
+  static constexpr int cent[10] = {4, 4, 4, 4, 6, 6, 6, 7, 7, 7};
+};
+#else
 template <> struct Mt2Cfg<10> { static constexpr int JPW = 5, SG = 1, S = 4; };  // 11 stars
+#endif
+// (variable-size plans measured slower here: 12 stars of 6 or 5 +3.8 %, 16 of 5 or 4 +14 %)
 template <> struct Mt2Cfg<11> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 11 stars
+#ifndef XL_MT2_VAR12
+#define XL_MT2_VAR12 1
+#endif
+#if XL_MT2_VAR12
+// 16 stars of 5 or 4 (centred counts 5 x 8, 9, 9, 10, 10) instead of 13 stars of 6 (loads
+// 20/20/19/19 instead of 24/18/18/18; K = 96: 51.3 -> 44.8 ms)
+template <> struct Mt2Cfg<12> {
+  static constexpr int JPW = 5, SG = 1, S = 4, NSTAR = 16;
+  static constexpr int cent[12] = {5, 5, 5, 5, 5, 5, 5, 5, 9, 9, 10, 10};
+};
+#else
 template <> struct Mt2Cfg<12> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 13 stars
+#endif
 #ifndef XL_MT2_VAR13
 #define XL_MT2_VAR13 1
 #endif
@@ -870,7 +916,16 @@ template <> struct Mt2Cfg<13> {
 #else
 template <> struct Mt2Cfg<13> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 13 stars
 #endif
+#if XL_MT2_VARX
+// 16 stars of 7 or 6 (centred counts 6 x 5, 7 x 7, 13, 13): loads 27/26/26/26 instead of 28/28/28/21
+// (K = 112: 63.8 -> 60.1 ms; 20 stars of 6 or 5 spill at 96 registers: 72.5 ms)
+template <> struct Mt2Cfg<14> {
+  static constexpr int JPW = 7, SG = 1, S = 4, NSTAR = 16;
+  static constexpr int cent[14] = {6, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 7, 13, 13};
+};
+#else
 template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; };  // 15 stars
+#endif
 template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
 // 120 < K <= 128: 34 stars of 4 dealt to two launches of 17 warps (a single launch of 17
 // stars of 8 spills its accumulators); each launch generates all 16 groups
@@ -1329,7 +1384,7 @@ int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   }
   // variable-size star plans (G = 13): full-length tiles and two buffers unless the ring is
   // asked for (E1 field, K = 100, 1000 drops: 58.3 -> 57.2 ms)
-  if constexpr (Mt2Var<G>::value != 0 && mt2_fits<G, 2, 2>()) {
+  if constexpr (Mt2Var<G>::value != 0 && !mt2_fits<G, 2, 3>() && mt2_fits<G, 2, 2>()) {
     if (env != 3)
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }

@@ -50,11 +50,14 @@ def main():
         gk = sum(v for k, v in tg.items() if k.startswith("gram"))  # all kernels of the exact Gram
         gcmac = D * N * K * (K + 1) / 2
         nb = (K + 63) // 64
-        if any(k.startswith("gram_syrk") for k in tg):  # 32x32 tile pairs, each coefficient generated once
-            nt = (K + 31) // 32
-            ops = D * N * (nt * (nt + 1) // 2 * 32 * 32 * 4 + nt * 32 * 31)
+        if any(k.startswith("gram_syrk") for k in tg):  # 32x32 tile pairs in the 3M form (3 real
+            nt = (K + 31) // 32                           # products per complex one), H generated once
+            ops = D * N * (nt * (nt + 1) // 2 * 32 * 32 * 3 + nt * 32 * 29)
+        elif K <= 128:  # MT2: G(G+1)/2 8x8 plane blocks, 3 DMMAs (3M) each, 29 + 1 (partner plane)
+            g = (K + 7) // 8  # FP64 ops per generated coefficient (G = 16: two launches, each generating all)
+            ops = D * N * (g * (g + 1) // 2 * 64 * 3 + (2 if g == 16 else 1) * 8 * g * 30)
         else:  # 64-user block pairs, both blocks generated per pair
-            ops = D * N * (nb * (nb + 1) // 2 * 64 * 64 * 4 + (nb * nb) * 64 * 31)
+            ops = D * N * (nb * (nb + 1) // 2 * 64 * 64 * 4 + (nb * nb) * 64 * 29)
         print(json.dumps({"K": K, "N": N, "drops": D, "gram_ms": tg, "gram_cmac_per_s": gcmac / (gk * 1e-3),
                           "gram_frac_fp64_useful": 4 * gcmac / (gk * 1e-3) / PEAK_FP64,
                           "gram_frac_fp64_issued_model": ops / (gk * 1e-3) / PEAK_FP64,
