@@ -929,7 +929,16 @@ template <> struct Mt2Cfg<14> { static constexpr int JPW = 7, SG = 1, S = 4; }; 
 template <> struct Mt2Cfg<15> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 20 stars
 // 120 < K <= 128: 34 stars of 4 dealt to two launches of 17 warps (a single launch of 17
 // stars of 8 spills its accumulators); each launch generates all 16 groups
+#if XL_MT2_VARX
+// variable-size: 32 stars of 5 or 4 (every group centres 8 or 9 blocks), 16 per launch: loads
+// 18 / 16 blocks per sub-partition in the two launches instead of 20 and 20
+template <> struct Mt2Cfg<16> {
+  static constexpr int JPW = 5, SG = 1, S = 4, NL = 2, NSTAR = 32;
+  static constexpr int cent[16] = {8, 8, 8, 8, 8, 8, 8, 8, 9, 9, 9, 9, 9, 9, 9, 9};
+};
+#else
 template <> struct Mt2Cfg<16> { static constexpr int JPW = 4, SG = 1, S = 4, NL = 2; };
+#endif
 template <int G, typename = void>
 struct Mt2Launches { static constexpr int value = 1; };
 template <int G>
@@ -953,10 +962,10 @@ struct Mt2 {
   static constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
   static constexpr int NL = Mt2Launches<G>::value;  // launches sharing the stars
   static constexpr int VAR = Mt2Var<G>::value;  // 0, or the star count of a variable-size plan
-  static constexpr int JG = VAR ? VAR : J / (JPW * NL), NW = JG * SG, NT = 32 * NW;  // stars per launch
+  static constexpr int JG = VAR ? VAR / NL : J / (JPW * NL), NW = JG * SG, NT = 32 * NW;  // stars per launch
   static constexpr int PLANE = S * G * 32;  // doubles in one (re or im) tile plane set
   static constexpr int ROWS = S * G;        // 32-lane fragment rows per tile
-  static_assert((VAR ? NL == 1 : J % (JPW * NL) == 0) && S % SG == 0, "Mt2Cfg");
+  static_assert((VAR ? VAR % NL == 0 : J % (JPW * NL) == 0) && S % SG == 0, "Mt2Cfg");
   static constexpr int NPL = kMt2Planes;  // re, im (, re - im: the 3M partner operand)
   static constexpr size_t tiles_bytes = (size_t)NPL * NBUF * PLANE * sizeof(double);  // NBUF buffers x planes
   static constexpr size_t stage_bytes = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
@@ -967,7 +976,7 @@ struct Mt2 {
 template <int G, int SM, int NBUF>
 constexpr bool mt2_fits() {
   constexpr int J = G * (G + 1) / 2, JPW = Mt2Cfg<G>::JPW, SG = Mt2Cfg<G>::SG, S = SM * Mt2Cfg<G>::S;
-  constexpr int JG = Mt2Var<G>::value ? Mt2Var<G>::value : J / (JPW * Mt2Launches<G>::value);
+  constexpr int JG = Mt2Var<G>::value ? Mt2Var<G>::value / Mt2Launches<G>::value : J / (JPW * Mt2Launches<G>::value);
   constexpr size_t tiles = (size_t)kMt2Planes * NBUF * S * G * 32 * sizeof(double);
   constexpr size_t stage = (size_t)JG * JPW * 3 * SG * 64 * sizeof(double);
   return (tiles > stage ? tiles : stage) <= 220 * 1024;
@@ -2009,7 +2018,7 @@ bool use_warp_kernel(const ArrayP &a, int K, int64_t n_drops, int n_lvl, int pre
 
 // fp64 fused Gram for 64 < K <= 128 on the MT2 kernel (3M DMMA stars) unless
 // XLMIMO_OPT_LARGE_K picks the block-pair (1) or SYRK (2) kernel
-constexpr int kMt2MaxK = 128;  // G <= 16 (G = 16 as two launches of 17 stars of 4)
+constexpr int kMt2MaxK = 128;  // G <= 16 (G = 16 as two launches of 16 stars of 5 or 4)
 bool use_mt2_large(const ArrayP &a, int K, int precision, int mode) {
   const int64_t N = a.kind == XLMIMO_ULA ? a.n_y : a.n_y * a.n_z;
   const int64_t o = option(XLMIMO_OPT_LARGE_K), gk = option(XLMIMO_OPT_GRAM_KERNEL);
