@@ -861,7 +861,9 @@ template <> struct Mt2Cfg<7> { static constexpr int JPW = 4, SG = 2, S = 8; };  
 #endif
 template <> struct Mt2Cfg<8> { static constexpr int JPW = 3, SG = 1, S = 9; };   // 12 stars, NW 12, 12 rows/warp
 // 64 < K <= 128 (the paper's K = 100 of E1/E2 and Fig. K_vs_E): one star per
-// warp, stars of a regular or near-regular tournament (warps not a multiple of 4 except G = 15)
+// warp.  Uniform plans of a regular or near-regular tournament leave the warp count off a
+// multiple of 4 for most G (the SM sub-partitions then carry unequal shares), so G = 9, 10, 12,
+// 13, 14 (and 7, 16) use variable-size plans (star_plan_var); G = 11 and 15 stay uniform.
 #ifndef XL_MT2_VAR9
 #define XL_MT2_VAR9 1
 #endif
