@@ -57,7 +57,11 @@ def _ws(nbytes):
                                                 (130, 1100, 1, 0, "ula"), (150, 1030, 0, 0, "ula"),
                                                 (100, 2048, 1, 0, "ula"), (200, 2048, 1, 0, "ula"),
                                                 (256, 1100, 1, 0, "ula"), (300, 1100, 1, 0, "ula"),
-                                                (100, 2048, 1, 1, "ula"), (128, 1000, 0, 0, "ula")])
+                                                (100, 2048, 1, 1, "ula"), (128, 1000, 0, 0, "ula"),
+                                                # MT2's variable-size star plans (G = 7, 10, 12, 14, 13 UPA)
+                                                (56, 700, 0, 0, "ula"), (80, 333, 0, 0, "ula"),
+                                                (96, 333, 0, 0, "ula"), (112, 333, 0, 0, "ula"),
+                                                (104, 300, 0, 0, "upa")])
 def test_gram_exact_writes_in_bounds(xl, K, N, prec, mode, kind):
     D = 3
     if kind == "ula":
