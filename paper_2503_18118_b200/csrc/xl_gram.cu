@@ -887,8 +887,17 @@ template <> struct Mt2Cfg<10> {
 #else
 template <> struct Mt2Cfg<10> { static constexpr int JPW = 5, SG = 1, S = 4; };  // 11 stars
 #endif
-// (variable-size plans measured slower here: 12 stars of 6 or 5 +3.8 %, 16 of 5 or 4 +14 %)
+#if XL_MT2_VARX
+// 12 stars of 6 or 5 (centred counts 5 x 5, 6 x 5, 11; loads 17/17/16/16 instead of 18/18/18/12)
+// on 48-element tiles, so that the 132 generated rows split evenly (11 per warp): K = 88
+// 40.4 -> 37.7 ms (on 32-element tiles, 8 rows for 11 warps and none for the 12th: +3.8 %)
+template <> struct Mt2Cfg<11> {
+  static constexpr int JPW = 6, SG = 1, S = 6, NSTAR = 12;
+  static constexpr int cent[11] = {5, 5, 5, 5, 5, 6, 6, 6, 6, 6, 11};
+};
+#else
 template <> struct Mt2Cfg<11> { static constexpr int JPW = 6, SG = 1, S = 4; };  // 11 stars
+#endif
 #ifndef XL_MT2_VAR12
 #define XL_MT2_VAR12 1
 #endif
@@ -1109,7 +1118,15 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
     // warp w generates the consecutive rows [w R, (w+1) R) (row = s * G + g, g fastest),
     // so runs of up to G rows share one element step s and decode its coordinates once
     // (a UPA decode costs 4 FP64 ops, a ULA one 2: otherwise repeated for every group)
-    constexpr int R = (ROWS + NW - 1) / NW;
+    // ROWS % NW != 0 (G = 6, 13): the first ROWS % NW warps take one row more -- spread over the
+    // SM sub-partitions when that count is a multiple of 4 -- instead of R each and the tail warps
+    // none (XL_MT2_ROWS_CEIL: the old split)
+    constexpr int R = (ROWS + NW - 1) / NW, RLO = ROWS / NW, REX = ROWS % NW;
+#ifdef XL_MT2_ROWS_CEIL
+    const int rs = warp * R, rc = ROWS - rs < R ? ROWS - rs : R;
+#else
+    const int rs = warp * RLO + (warp < REX ? warp : REX), rc = RLO + (warp < REX ? 1 : 0);
+#endif
     auto generate = [&](int t0, int buf) {
       double *gre = dsm + buf * (C::NPL * PLANE), *gim = gre + PLANE;
       int s_cur = -1;
@@ -1117,8 +1134,8 @@ __global__ void __launch_bounds__(Mt2<G, SM, NBUF>::NT, 1) gram_mt2_kernel(GramP
       ElemPos ep;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const int row = warp * R + i;
-        if (ROWS % NW == 0 || row < ROWS) {
+        const int row = rs + i;
+        if (ROWS % NW == 0 || i < rc) {
           const int s = row / G, g = row - s * G;
           if (s != s_cur) {  // warp-uniform
             s_cur = s;
