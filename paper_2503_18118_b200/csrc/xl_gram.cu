@@ -1410,9 +1410,10 @@ int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
     if (nbuf == 2 || !mt2_fits<G, 2, 3>())
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
-  // variable-size star plans (G = 13): full-length tiles and two buffers unless the ring is
-  // asked for (E1 field, K = 100, 1000 drops: 58.3 -> 57.2 ms)
-  if constexpr (Mt2Var<G>::value != 0 && !mt2_fits<G, 2, 3>() && mt2_fits<G, 2, 2>()) {
+  // K > 64 where a 3-deep ring of full-length tiles does not fit: full-length tiles and two
+  // buffers rather than the ring on half-length tiles, unless the ring is asked for (E1 field,
+  // 1000 drops: K = 100 58.3 -> 57.2 ms, K = 120 64.5 -> 62.3 ms)
+  if constexpr (G > 8 && !mt2_fits<G, 2, 3>() && mt2_fits<G, 2, 2>()) {
     if (env != 3)
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
