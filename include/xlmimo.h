@@ -278,7 +278,8 @@ XLMIMO_API int xlmimo_gen_drops_rect(double x_min, double x_max, double y_min, d
  *                           fp64), 3 CUDA-core register/tile kernels, 4 64-bit-index DMMA (K > 16)
  *   XLMIMO_OPT_SPLIT_NT     split kernel block variant: 64, 128, 192 (128 x 3/SM) or 256
  *   XLMIMO_OPT_DMMA_VARIANT DMMA kernel block shape 0..3 (xl_gram.cu, mma_variant)
- *   XLMIMO_OPT_MT2_BUFFERS  DMMA K = 17..64 tile buffers: 2 or 3 (3 only where the ring fits: K <= 48)
+ *   XLMIMO_OPT_MT2_BUFFERS  DMMA K = 17..128 tile buffers: 2 (default) or 3 (the ring of full-length tiles where it
+ *                           fits, of half-length ones otherwise for K > 64)
  *   XLMIMO_OPT_STREAM       materialised fp32 stream: 1 CUDA cores instead of tcgen05
  * Returns XLMIMO_OK, or EINVAL for an unknown option (value not range-checked: an
  * out-of-range value means automatic). */

@@ -1396,28 +1396,19 @@ int launch_mt2_k(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   return XLMIMO_OK;
 }
 
-// Tiles of 2*Mt2Cfg<G>::S steps.  Buffers: 2 (one barrier per tile) for G <= 4, the
-// 3-deep mbarrier ring above where its three planes fit (G = 5, 6; measured on B200 with
-// two planes: cfg4 K=32 17.65 vs 18.50 ms with the ring; cfg5 K=64 25.24 vs 25.79 ms);
-// G = 7, 8 take 2 buffers, K > 64 the ring with half-length tiles.  XLMIMO_OPT_MT2_BUFFERS
-// = 2|3 overrides where the ring fits.
+// Tiles of 2*Mt2Cfg<G>::S steps in two buffers (one barrier per tile) for every G.  The 3-deep
+// mbarrier ring (full-length tiles where three planes fit, half-length ones for K > 64
+// otherwise) is kept as the XLMIMO_OPT_MT2_BUFFERS = 3 option: late round 2 it was slower or
+// equal at every K on the E1 field (tools/ab_mt2buf.py, 1000 drops: K = 40 11.05 -> 10.74 ms,
+// 48 15.85 -> 15.53, 72 29.23 -> 28.25, 80 35.92 -> 34.22, 100 58.8 -> 54.4, 120 64.5 -> 62.4).
 template <int G>
 int launch_mt2(const GramParams &P, int64_t n_blocks, cudaStream_t s) {
   const int env = (int)xlh::option(XLMIMO_OPT_MT2_BUFFERS);
-  const int nbuf = (env == 2 || env == 3) ? env : (G <= 4 ? 2 : 3);
   const bool ula = P.kind == XLMIMO_ULA;
-  if constexpr (G <= 8) {
-    if (nbuf == 2 || !mt2_fits<G, 2, 3>())
+  if constexpr (mt2_fits<G, 2, 2>()) {
+    if (env != 3 || (G <= 8 && !mt2_fits<G, 2, 3>()))
       return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
   }
-  // K > 64 where a 3-deep ring of full-length tiles does not fit: full-length tiles and two
-  // buffers rather than the ring on half-length tiles, unless the ring is asked for (E1 field,
-  // 1000 drops: K = 100 58.3 -> 57.2 ms, K = 120 64.5 -> 62.3 ms)
-  if constexpr (G > 8 && !mt2_fits<G, 2, 3>() && mt2_fits<G, 2, 2>()) {
-    if (env != 3)
-      return ula ? launch_mt2_k<G, 2, 2, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 2, XLMIMO_UPA>(P, n_blocks, s);
-  }
-  // K > 64: the ring only (half-length tiles when three planes do not fit)
   if constexpr (mt2_fits<G, 2, 3>())
     return ula ? launch_mt2_k<G, 2, 3, XLMIMO_ULA>(P, n_blocks, s) : launch_mt2_k<G, 2, 3, XLMIMO_UPA>(P, n_blocks, s);
   else

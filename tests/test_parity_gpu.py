@@ -521,3 +521,15 @@ def test_fused_fp32_long_chunks(xl, orc, kind, n_y, n_z, K, D):
     assert normalized_err(G[pick], Go) <= 1e-4
     for d in pick:
         assert np.array_equal(G[d], np.conj(G[d].T))
+
+
+@pytest.mark.parametrize("K,N", [(24, 1501), (40, 2049), (64, 3001), (100, 1003), (120, 999), (128, 777)])
+def test_mt2_ring_option_parity(xl, orc, K, N):
+    """MT2's 3-deep mbarrier ring (XLMIMO_OPT_MT2_BUFFERS = 3; two buffers are the default since
+    late round 2): full-length tiles where three planes fit, half-length ones above, against the
+    oracle at the fp64 tier, on ragged N."""
+    ag, ao = _arr(xl, orc, "ula", N, 1, 100e9)
+    pos = xl.gen_drops(xl.Users.polar((1.0, 12.0), (-60.0, 60.0)), K, 3, seed=K)
+    with xl.option(xl.OPT_MT2_BUFFERS, 3):
+        G = xl.gram_exact(ag, pos).cpu().numpy()
+    assert normalized_err(G, orc.gram_exact(ao, pos.cpu().numpy())) <= 1e-9
