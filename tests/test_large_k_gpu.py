@@ -421,11 +421,12 @@ def test_sweep_large_k_paths(xl, orc, K, prec, tol):
     assert np.nanmax(np.abs(res["ergodic"] - erg)) <= tol
 
 
-@pytest.mark.parametrize("K,prec", [(100, "fp32"), (160, "fp32"), (256, "fp32"), (128, "fp64")])
+@pytest.mark.parametrize("K,prec", [(100, "fp32"), (160, "fp32"), (256, "fp32"), (128, "fp64"),
+                                    (56, "fp64"), (72, "fp64"), (88, "fp64"), (100, "fp64"), (112, "fp64")])
 def test_large_k_paths_bitwise_deterministic(xl, K, prec):
     """The multi-launch paths (fused fp32 wide / cross / narrow, MT2's two launches for
-    K = 128) write disjoint entries with fixed reduction orders: repeated calls are equal bit
-    for bit."""
+    K = 128) and MT2's variable-size star plans (G = 7, 9, 11, 13, 14) write disjoint entries
+    with fixed reduction orders: repeated calls are equal bit for bit."""
     a = xl.Array.ula(9000, 100e9)
     pos = xl.gen_drops_rect((1.0, 10.0), (-7.5, 7.5), K, 40, seed=41)
     p = xl.FP32 if prec == "fp32" else xl.FP64
